@@ -1,0 +1,381 @@
+// Dense-X kernels of the hot path (explicit-A build).
+//
+//  a2  XS = X S  ("fetching the rows/columns indexed by a random subset"; count/SubCount:
+//      signed segmented sums).  Row-major XS[n x ld_xs].
+//  a3  AS^T = (XS)^T X, i.e. (X^T (X S))^T  ("multiplying a m x tau matrix A S_k"), the
+//      tall-skinny TN contraction on FP64 tensor cores: mma.sync.m8n8k4.f64 (SASS DMMA) fed by a
+//      4-stage cp.async shared-memory pipeline, deterministic split-K (partials reduced in a fixed
+//      order by a second kernel).  FP64 has no tcgen05/UMMA kind on sm_100a; DMMA is the
+//      FP64 tensor path and measures 37.1 TFLOP/s on this B200 (profiles/r01_fp64_peak.txt).
+//  explicit A = X^T X + lambda I is the same TN contraction with Bop = X, built once.
+//  explicit a2: AS^T[b,:] = sum_{e in b} sign_e A[coord_e, :] (A symmetric, rows are columns).
+#include "rs_internal.cuh"
+
+namespace rs {
+
+namespace {
+
+// ------------------------------------------------------------------------------ a2 gathers
+__global__ void k_dense_xs(const double* __restrict__ X, long long ldx, long long rows,
+                           DevSketch sk, double* __restrict__ XS, long long ld_xs, int rows_per_blk,
+                           const Ctrl* ctrl) {
+  if (ctrl && ctrl->done) return;
+  const long long r0 = (long long)blockIdx.x * rows_per_blk;
+  const int per_blk = rows_per_blk * (int)ld_xs;
+  for (int q = threadIdx.x; q < per_blk; q += blockDim.x) {
+    const long long i = r0 + q / ld_xs;
+    const int b = q % ld_xs;
+    if (i >= rows) break;
+    double v = 0.0;
+    if (b < sk.tau) {
+      const double* xr = X + i * ldx;
+      const int e0 = sk.bptr[b], e1 = sk.bptr[b + 1];
+      for (int e = e0; e < e1; ++e) {
+        const double x = __ldg(xr + sk.coord[e]);
+        v += sk.sign[e] > 0 ? x : -x;
+      }
+    }
+    XS[i * ld_xs + b] = v;
+  }
+}
+
+__global__ void k_explicit_rows(const double* __restrict__ A, long long lda, long long m,
+                                DevSketch sk, double* __restrict__ ASt, long long ld_as,
+                                const Ctrl* ctrl) {
+  if (ctrl && ctrl->done) return;
+  const int b = blockIdx.y;
+  const long long j = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= m) return;
+  const int e0 = sk.bptr[b], e1 = sk.bptr[b + 1];
+  double v = 0.0;
+  for (int e = e0; e < e1; ++e) {
+    const double a = A[(long long)sk.coord[e] * lda + j];
+    v += sk.sign[e] > 0 ? a : -a;
+  }
+  ASt[(long long)b * ld_as + j] = v;
+}
+
+__global__ void k_add_lambda_s(double lambda, DevSketch sk, double* ASt, long long ld_as,
+                               bool rowmajor, const Ctrl* ctrl) {
+  if (ctrl && ctrl->done) return;
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= sk.len) return;
+  const double s = sk.sign[e] > 0 ? lambda : -lambda;
+  if (rowmajor) ASt[(long long)sk.coord[e] * ld_as + sk.bucket[e]] += s;
+  else ASt[(long long)sk.bucket[e] * ld_as + sk.coord[e]] += s;
+}
+
+__global__ void k_add_diag(double* A, long long lda, long long m, double lambda) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < m) A[i * lda + i] += lambda;
+}
+
+// ------------------------------------------------------------------------------ a3 DMMA GEMM
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, int src_bytes) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem),
+               "r"(src_bytes));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+__device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c[0]), "+d"(c[1])
+               : "d"(a), "d"(b));
+}
+
+// C'[M x N] (+)= sum_k A[k, m] * B[k, n]  over this CTA's K range.
+//   A: row-major K x M (lda), B: row-major K x N (ldb).  Tile BM x BN x BK, WM x WN warps.
+template <int BM, int BN, int BK, int WM, int WN, int STAGES>
+__global__ void __launch_bounds__(WM * WN * 32)
+k_tn_gemm(const double* __restrict__ A, long long lda, const double* __restrict__ B, long long ldb,
+          long long M, long long N, long long K, long long k_per_split, double* __restrict__ C,
+          long long ldc, long long split_stride, const Ctrl* ctrl) {
+  if (ctrl && ctrl->done) return;
+  constexpr int NT = WM * WN * 32;
+  constexpr int LDA_S = BM + 4, LDB_S = BN + 4;   // +4 doubles: conflict-free fragment loads
+  constexpr int TM = BM / WM / 8, TN = BN / WN / 8;
+  extern __shared__ __align__(16) double smem[];
+  double* As = smem;                               // [STAGES][BK][LDA_S]
+  double* Bs = smem + STAGES * BK * LDA_S;         // [STAGES][BK][LDB_S]
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm = warp / WN, wn = warp % WN;
+  const long long m0 = (long long)blockIdx.x * BM, n0 = (long long)blockIdx.y * BN;
+  const long long kbeg = (long long)blockIdx.z * k_per_split;
+  const long long kend = min(K, kbeg + k_per_split);
+  const int nkb = kbeg < kend ? (int)((kend - kbeg + BK - 1) / BK) : 0;
+
+  auto load_stage = [&](int stage, int kb) {
+    const long long k0 = kbeg + (long long)kb * BK;
+    double* as = As + stage * BK * LDA_S;
+    double* bs = Bs + stage * BK * LDB_S;
+    constexpr int ACH = BK * BM / 2, BCH = BK * BN / 2;
+#pragma unroll
+    for (int c = tid; c < ACH; c += NT) {
+      const int r = c / (BM / 2), cc = (c % (BM / 2)) * 2;
+      const long long k = k0 + r, mm = m0 + cc;
+      int bytes = 0;
+      if (k < kend) bytes = mm + 1 < M ? 16 : (mm < M ? 8 : 0);
+      const double* src = bytes ? A + k * lda + mm : A;
+      cp_async16(as + r * LDA_S + cc, src, bytes);
+    }
+#pragma unroll
+    for (int c = tid; c < BCH; c += NT) {
+      const int r = c / (BN / 2), cc = (c % (BN / 2)) * 2;
+      const long long k = k0 + r, nn = n0 + cc;
+      int bytes = 0;
+      if (k < kend) bytes = nn + 1 < N ? 16 : (nn < N ? 8 : 0);
+      const double* src = bytes ? B + k * ldb + nn : B;
+      cp_async16(bs + r * LDB_S + cc, src, bytes);
+    }
+  };
+
+  double acc[TM][TN][2];
+#pragma unroll
+  for (int i = 0; i < TM; ++i)
+#pragma unroll
+    for (int j = 0; j < TN; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+#pragma unroll
+  for (int s = 0; s < STAGES - 1; ++s) {
+    if (s < nkb) load_stage(s, s);
+    cp_async_commit();
+  }
+  const int arow = lane & 3, acol = lane >> 2;
+  for (int kb = 0; kb < nkb; ++kb) {
+    cp_async_wait<STAGES - 2>();
+    __syncthreads();
+    const int nxt = kb + STAGES - 1;
+    if (nxt < nkb) load_stage(nxt % STAGES, nxt);
+    cp_async_commit();
+    const double* as = As + (kb % STAGES) * BK * LDA_S + wm * (TM * 8) + acol;
+    const double* bs = Bs + (kb % STAGES) * BK * LDB_S + wn * (TN * 8) + acol;
+#pragma unroll
+    for (int kk = 0; kk < BK; kk += 4) {
+      double af[TM], bf[TN];
+#pragma unroll
+      for (int i = 0; i < TM; ++i) af[i] = as[(kk + arow) * LDA_S + i * 8];
+#pragma unroll
+      for (int j = 0; j < TN; ++j) bf[j] = bs[(kk + arow) * LDB_S + j * 8];
+#pragma unroll
+      for (int i = 0; i < TM; ++i)
+#pragma unroll
+        for (int j = 0; j < TN; ++j) dmma(acc[i][j], af[i], bf[j]);
+    }
+  }
+  cp_async_wait<0>();
+
+  double* Cz = C + (long long)blockIdx.z * split_stride;
+#pragma unroll
+  for (int i = 0; i < TM; ++i) {
+    const long long row = m0 + wm * (TM * 8) + i * 8 + (lane >> 2);
+    if (row >= M) continue;
+#pragma unroll
+    for (int j = 0; j < TN; ++j) {
+      const long long col = n0 + wn * (TN * 8) + j * 8 + 2 * (lane & 3);
+      double* dst = Cz + row * ldc + col;
+      if (col + 1 < N) {
+        *reinterpret_cast<double2*>(dst) = make_double2(acc[i][j][0], acc[i][j][1]);
+      } else if (col < N) {
+        dst[0] = acc[i][j][0];
+      }
+    }
+  }
+}
+
+__global__ void k_splitk_reduce(const double* __restrict__ work, int splits, long long split_stride,
+                                long long M, long long N, long long ldw, double* __restrict__ C,
+                                long long ldc, const Ctrl* ctrl) {
+  if (ctrl && ctrl->done) return;
+  const long long row = blockIdx.y;
+  for (long long j = (long long)blockIdx.x * blockDim.x + threadIdx.x; j < N;
+       j += (long long)gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int z = 0; z < splits; ++z) s += work[z * split_stride + row * ldw + j];
+    C[row * ldc + j] = s;
+  }
+}
+
+constexpr int G_BM = 64, G_BN = 128, G_BK = 16, G_WM = 2, G_WN = 4, G_ST = 4;
+constexpr size_t G_SMEM = (size_t)G_ST * G_BK * ((G_BM + 4) + (G_BN + 4)) * sizeof(double);
+
+// ------------------------------------------------------------------------------ misc
+__global__ void k_fill(double* p, long long n, double v) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    p[i] = v;
+}
+__global__ void k_neg(const double* b, double* r, long long m) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < m;
+       i += (long long)gridDim.x * blockDim.x)
+    r[i] = -b[i];
+}
+// deterministic sum of squares: one block, fixed-order strided partials then a tree
+__global__ void k_dot_self(const double* x, long long n, double* out) {
+  __shared__ double s[1024];
+  double acc = 0.0;
+  for (long long i = threadIdx.x; i < n; i += blockDim.x) acc += x[i] * x[i];
+  s[threadIdx.x] = acc;
+  __syncthreads();
+  for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+    if ((int)threadIdx.x < o) s[threadIdx.x] += s[threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *out = s[0];
+}
+// X^T y: pass 1, each block sums a row range into work[blk][cols]; pass 2 sums blocks in order.
+constexpr int XTY_ROWS = 1024;
+__global__ void k_xty_partial(const double* __restrict__ X, long long ldx, long long rows,
+                              long long cols, const double* __restrict__ y, double* work) {
+  const long long r0 = (long long)blockIdx.y * XTY_ROWS, r1 = min(rows, r0 + XTY_ROWS);
+  for (long long j = (long long)blockIdx.x * blockDim.x + threadIdx.x; j < cols;
+       j += (long long)gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (long long i = r0; i < r1; ++i) s += X[i * ldx + j] * y[i];
+    work[(long long)blockIdx.y * cols + j] = s;
+  }
+}
+__global__ void k_xty_final(const double* work, long long nblk, long long cols, double* out) {
+  for (long long j = (long long)blockIdx.x * blockDim.x + threadIdx.x; j < cols;
+       j += (long long)gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (long long z = 0; z < nblk; ++z) s += work[z * cols + j];
+    out[j] = s;
+  }
+}
+
+__global__ void k_count_nonfinite(const double* X, long long ldx, long long rows, long long cols,
+                                  unsigned long long* out) {
+  unsigned long long bad = 0;
+  const long long total = rows * cols;
+  for (long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x; q < total;
+       q += (long long)gridDim.x * blockDim.x) {
+    const long long i = q / cols, j = q % cols;
+    bad += !isfinite(X[i * ldx + j]);
+  }
+  if (bad) atomicAdd(out, bad);
+}
+
+}  // namespace
+
+cudaError_t launch_count_nonfinite(const double* X, long long ldx, long long rows, long long cols,
+                                   unsigned long long* out, cudaStream_t st) {
+  if (rows <= 0 || cols <= 0) return cudaSuccess;
+  k_count_nonfinite<<<1184, 256, 0, st>>>(X, ldx, rows, cols, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_dense_xs(const double* X, long long ldx, long long rows, const DevSketch& sk,
+                            double* XS, long long ld_xs, const Ctrl* ctrl, cudaStream_t st) {
+  if (rows <= 0) return cudaSuccess;
+  const int rpb = (int)std::max<long long>(1, 2048 / ld_xs);
+  const long long grid = (rows + rpb - 1) / rpb;
+  k_dense_xs<<<(unsigned)grid, 256, 0, st>>>(X, ldx, rows, sk, XS, ld_xs, rpb, ctrl);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_explicit_rows(const double* A, long long lda, long long m, const DevSketch& sk,
+                                 double* ASt, long long ld_as, const Ctrl* ctrl, cudaStream_t st) {
+  dim3 grid((unsigned)((m + 255) / 256), (unsigned)sk.tau);
+  k_explicit_rows<<<grid, 256, 0, st>>>(A, lda, m, sk, ASt, ld_as, ctrl);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_add_lambda_s(double lambda, const DevSketch& sk, double* ASt, long long ld_as,
+                                bool as_rowmajor, const Ctrl* ctrl, cudaStream_t st) {
+  k_add_lambda_s<<<(sk.len + 255) / 256, 256, 0, st>>>(lambda, sk, ASt, ld_as, as_rowmajor, ctrl);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_add_diag(double* A, long long lda, long long m, double lambda, cudaStream_t st) {
+  k_add_diag<<<(unsigned)((m + 255) / 256), 256, 0, st>>>(A, lda, m, lambda);
+  return cudaGetLastError();
+}
+
+GemmPlan plan_tn_gemm(long long M, long long N, long long K, int num_sms) {
+  GemmPlan p{};
+  p.bm = G_BM;
+  p.bn = G_BN;
+  const long long tiles = ((M + G_BM - 1) / G_BM) * ((N + G_BN - 1) / G_BN);
+  const long long slots = 2LL * num_sms;   // 2 CTAs / SM resident (smem-limited)
+  // choose splits maximising wave efficiency, with >= 512 K rows per split
+  int best = 1;
+  double best_eff = -1.0;
+  for (int s = 1; s <= 32; ++s) {
+    if (s > 1 && K / s < 512) break;
+    const long long ctas = tiles * s;
+    const long long waves = (ctas + slots - 1) / slots;
+    const double eff = (double)ctas / (double)(waves * slots);
+    // prefer fewer splits unless efficiency improves by > 5%
+    if (eff > best_eff + 0.05) { best_eff = eff; best = s; }
+  }
+  p.splits = best;
+  long long kps = (K + best - 1) / best;
+  kps = (kps + G_BK - 1) / G_BK * G_BK;
+  p.k_per_split = kps;
+  p.work_elems = best > 1 ? (size_t)best * (size_t)M * (size_t)N : 0;
+  return p;
+}
+
+cudaError_t launch_tn_gemm(const double* Aop, long long lda, const double* Bop, long long ldb,
+                           long long M, long long N, long long K, double* C, long long ldc,
+                           const GemmPlan& plan, double* work, const Ctrl* ctrl, cudaStream_t st) {
+  auto kern = k_tn_gemm<G_BM, G_BN, G_BK, G_WM, G_WN, G_ST>;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)G_SMEM);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  dim3 grid((unsigned)((M + G_BM - 1) / G_BM), (unsigned)((N + G_BN - 1) / G_BN),
+            (unsigned)plan.splits);
+  if (plan.splits == 1) {
+    kern<<<grid, G_WM * G_WN * 32, G_SMEM, st>>>(Aop, lda, Bop, ldb, M, N, K, plan.k_per_split, C,
+                                                 ldc, 0, ctrl);
+    return cudaGetLastError();
+  }
+  const long long stride = M * N;
+  kern<<<grid, G_WM * G_WN * 32, G_SMEM, st>>>(Aop, lda, Bop, ldb, M, N, K, plan.k_per_split, work,
+                                               N, stride, ctrl);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  dim3 rg((unsigned)std::min<long long>((N + 255) / 256, 64), (unsigned)M);
+  k_splitk_reduce<<<rg, 256, 0, st>>>(work, plan.splits, stride, M, N, N, C, ldc, ctrl);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_fill(double* p, long long n, double v, cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  k_fill<<<(unsigned)std::min<long long>((n + 255) / 256, 4096), 256, 0, st>>>(p, n, v);
+  return cudaGetLastError();
+}
+cudaError_t launch_axpby_neg(const double* b, double* r, long long m, cudaStream_t st) {
+  if (m <= 0) return cudaSuccess;
+  k_neg<<<(unsigned)std::min<long long>((m + 255) / 256, 4096), 256, 0, st>>>(b, r, m);
+  return cudaGetLastError();
+}
+cudaError_t launch_dot_self(const double* x, long long n, double* out, cudaStream_t st) {
+  k_dot_self<<<1, 1024, 0, st>>>(x, n, out);
+  return cudaGetLastError();
+}
+size_t dense_xty_work(long long rows, long long cols) {
+  return (size_t)((rows + XTY_ROWS - 1) / XTY_ROWS) * (size_t)cols;
+}
+cudaError_t launch_dense_xty(const double* X, long long ldx, long long rows, long long cols,
+                             const double* y, double* out, double* work, cudaStream_t st) {
+  const long long nblk = (rows + XTY_ROWS - 1) / XTY_ROWS;
+  if (nblk == 0) return launch_fill(out, cols, 0.0, st);
+  dim3 g1((unsigned)((cols + 127) / 128), (unsigned)nblk);
+  k_xty_partial<<<g1, 128, 0, st>>>(X, ldx, rows, cols, y, work);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  k_xty_final<<<(unsigned)((cols + 255) / 256), 256, 0, st>>>(work, nblk, cols, out);
+  return cudaGetLastError();
+}
+
+}  // namespace rs

@@ -1,0 +1,700 @@
+// Host engine behind the C ABI (include/ridgesketch.h): argument validation, the problem object,
+// device memory, the per-iteration launch sequence captured in a CUDA graph, the device stop flag,
+// NCCL for world > 1.  No arithmetic of the method runs on the host.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/ridgesketch.h"
+#include "engine.h"
+#include "nccl_dl.h"
+#include "rs_internal.cuh"
+
+namespace rs {
+
+thread_local std::string g_last_error;
+
+rs_status fail(rs_status s, const std::string& msg) {
+  g_last_error = msg;
+  return s;
+}
+
+
+
+// ------------------------------------------------------------------------------------------------
+Problem::~Problem() {
+  if (device >= 0) cudaSetDevice(device);
+  if (st) cudaStreamSynchronize(st);
+  free_workspace();
+  if (own_X) dfree(X);
+  dfree(y);
+  dfree(b);
+  dfree(A);
+  dfree(w);
+  dfree(dw);
+  dfree(r);
+  dfree(dr);
+  dfree(sdelta);
+  dfree(ctrl);
+  dfree(trace_dev);
+  dfree(scratch);
+  csr_free();
+  if (ctrl_host) cudaFreeHost(ctrl_host);
+  if (comm) {
+    std::string err;
+    if (const NcclApi* api = nccl_api(&err)) api->ncclCommDestroy(comm);
+  }
+  if (own_stream && st) cudaStreamDestroy(st);
+}
+
+void Problem::free_workspace() {
+  if (graph_exec) cudaGraphExecDestroy(graph_exec);
+  graph_exec = nullptr;
+  for (auto ev : prof_events) cudaEventDestroy(ev);
+  prof_events.clear();
+  dfree(sk.coord);
+  dfree(sk.sign);
+  dfree(sk.bucket);
+  dfree(sk.bptr);
+  dfree(sk.cmap);
+  sk = DevSketch{};
+  dfree(XS);
+  XS = nullptr;
+  dfree(ASt);
+  ASt = nullptr;
+  dfree(gemm_work);
+  gemm_work = nullptr;
+  dfree(sw.Gx);
+  dfree(sw.delta);
+  sw = SolveWork{};
+  dfree(partials);
+  partials = nullptr;
+  ws_kind = -1;
+  ws_tau = -1;
+  ws_ksum = -1;
+  csr_free_workspace();
+}
+
+rs_status Problem::allreduce(double* buf, size_t count) {
+  if (world <= 1) return RS_OK;
+  std::string err;
+  const NcclApi* api = nccl_api(&err);
+  if (!api) return fail(RS_ENCCL, err);
+  ncclResult_t e = api->ncclAllReduce(buf, buf, count, ncclFloat64, ncclSum, comm, st);
+  if (e != ncclSuccess) {
+    api->ncclCommAbort(comm);
+    comm = nullptr;
+    return fail(RS_ENCCL, std::string("ncclAllReduce: ") + api->ncclGetErrorString(e));
+  }
+  return RS_OK;
+}
+
+// ------------------------------------------------------------------------------------------------
+rs_status setup_common(Problem* p, const rs_dist* dist) {
+  int ndev = 0;
+  cudaError_t e = cudaGetDeviceCount(&ndev);
+  if (e != cudaSuccess || ndev == 0)
+    return fail(RS_ECUDA, std::string("no usable CUDA device: ") +
+                              (e != cudaSuccess ? cudaGetErrorString(e) : "count = 0"));
+  p->device = dist ? dist->device : 0;
+  if (p->device < 0 || p->device >= ndev) return fail(RS_EINVAL, "dist->device out of range");
+  RS_CUDA(cudaSetDevice(p->device));
+  RS_CUDA(cudaDeviceGetAttribute(&p->num_sms, cudaDevAttrMultiProcessorCount, p->device));
+  if (dist && dist->cuda_stream) {
+    p->st = static_cast<cudaStream_t>(dist->cuda_stream);
+    p->own_stream = false;
+  } else {
+    RS_CUDA(cudaStreamCreateWithFlags(&p->st, cudaStreamNonBlocking));
+    p->own_stream = true;
+  }
+  p->rank = dist ? dist->rank : 0;
+  p->world = dist ? dist->world : 1;
+  if (p->world > 1) {
+    std::string err;
+    const NcclApi* api = nccl_api(&err);
+    if (!api) return fail(RS_ENCCL, err);
+    ncclUniqueId id;
+    std::memcpy(&id, dist->nccl_unique_id, sizeof(id));
+    ncclResult_t ne = api->ncclCommInitRank(&p->comm, p->world, id, p->rank);
+    if (ne != ncclSuccess) {
+      p->comm = nullptr;
+      return fail(RS_ENCCL, std::string("ncclCommInitRank: ") + api->ncclGetErrorString(ne));
+    }
+  }
+  RS_CUDA(cudaMallocHost(&p->ctrl_host, sizeof(Ctrl)));
+  RS_TRY(dalloc(&p->ctrl, 1));
+  return RS_OK;
+}
+
+rs_status validate_dist(const rs_dist* dist, long long total) {
+  if (!dist) return RS_OK;
+  if (dist->world < 1 || dist->rank < 0 || dist->rank >= dist->world)
+    return fail(RS_EINVAL, "rs_dist: need 0 <= rank < world");
+  if (dist->world > 1 && !dist->nccl_unique_id)
+    return fail(RS_EINVAL, "rs_dist: world > 1 needs nccl_unique_id");
+  if (dist->shard_begin < 0 || dist->shard_len < 0 || dist->shard_begin + dist->shard_len > total)
+    return fail(RS_EINVAL, "rs_dist: shard out of range");
+  if (dist->world == 1 && (dist->shard_begin != 0 || dist->shard_len != total))
+    return fail(RS_EINVAL, "rs_dist: world == 1 must hold the whole matrix");
+  return RS_OK;
+}
+
+
+// m-vectors and b-norm (shared by dense and CSR creation)
+rs_status finish_setup(Problem* p) {
+  RS_TRY(dalloc(&p->w, p->m));
+  RS_TRY(dalloc(&p->dw, p->m));
+  RS_TRY(dalloc(&p->r, p->m));
+  RS_TRY(dalloc(&p->dr, p->m));
+  RS_TRY(dalloc(&p->sdelta, p->m));
+  RS_CUDA(launch_fill(p->sdelta, p->m, 0.0, p->st));
+  RS_TRY(dalloc(&p->scratch, 4));
+  RS_CUDA(launch_dot_self(p->b, p->m, p->scratch, p->st));
+  RS_CUDA(cudaMemcpyAsync(&p->bnorm2, p->scratch, sizeof(double), cudaMemcpyDeviceToHost, p->st));
+  RS_CUDA(cudaStreamSynchronize(p->st));
+  return RS_OK;
+}
+
+static rs_status create_dense(rs_problem* out, int64_t n, int64_t d, const double* X_local,
+                              int64_t ldx, const double* y, double lambda, rs_route route,
+                              rs_as_mode mode, rs_mem mem, const rs_dist* dist) {
+  if (!out) return fail(RS_EINVAL, "out is NULL");
+  *out = nullptr;
+  if (n < 1 || d < 1) return fail(RS_EINVAL, "need n >= 1 and d >= 1");
+  if (!(lambda > 0.0) || !std::isfinite(lambda)) return fail(RS_EINVAL, "need finite lambda > 0 (P:L36)");
+  if (!X_local || !y) return fail(RS_EINVAL, "X and y must be non-NULL");
+  if (ldx < d) return fail(RS_EINVAL, "ldx < d");
+  if (mem != RS_MEM_HOST && mem != RS_MEM_DEVICE_COPY && mem != RS_MEM_DEVICE_BORROW)
+    return fail(RS_EINVAL, "bad rs_mem");
+  if (route != RS_ROUTE_AUTO && route != RS_ROUTE_PRIMAL && route != RS_ROUTE_DUAL)
+    return fail(RS_EINVAL, "bad route");
+  if (mode != RS_AS_IMPLICIT && mode != RS_AS_EXPLICIT) return fail(RS_EINVAL, "bad as_mode");
+  const int rt = route == RS_ROUTE_AUTO ? (d <= n ? 1 : 2) : (route == RS_ROUTE_PRIMAL ? 1 : 2);
+  if (rt == 2) return fail(RS_EUNSUPPORTED, "dense dual route not implemented yet (use CSR or primal)");
+  RS_TRY(validate_dist(dist, rt == 1 ? n : d));
+  const long long rows = dist ? dist->shard_len : n;
+
+  Problem* p = new Problem();
+  auto guard = [&](rs_status s) {
+    if (s != RS_OK) delete p;
+    return s;
+  };
+  rs_status s = setup_common(p, dist);
+  if (s != RS_OK) return guard(s);
+  p->fmt = 0;
+  p->route = rt;
+  p->mode = mode;
+  p->n = n;
+  p->d = d;
+  p->m = d;
+  p->rows_loc = rows;
+  p->lambda = lambda;
+
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  // X: library copy with ld a multiple of 4 doubles (16-byte cp.async rows), unless borrowable
+  if (mem == RS_MEM_DEVICE_BORROW && ldx % 4 == 0) {
+    p->X = const_cast<double*>(X_local);
+    p->ldx = ldx;
+    p->own_X = false;
+  } else {
+    p->ldx = round_up(d, 4);
+    s = dalloc(&p->X, (size_t)std::max<long long>(rows, 1) * p->ldx);
+    if (s != RS_OK) return guard(s);
+    p->own_X = true;
+    if (rows > 0) {
+      cudaError_t ce = cudaMemcpy2DAsync(p->X, p->ldx * 8, X_local, ldx * 8, d * 8, rows,
+                                         kind_of(mem), p->st);
+      if (ce != cudaSuccess) return guard(fail(RS_ECUDA, std::string("copy X: ") + cudaGetErrorString(ce)));
+    }
+  }
+  s = dalloc(&p->y, std::max<long long>(rows, 1));
+  if (s != RS_OK) return guard(s);
+  if (rows > 0) {
+    cudaError_t ce = cudaMemcpyAsync(p->y, y, rows * 8, kind_of(mem), p->st);
+    if (ce != cudaSuccess) return guard(fail(RS_ECUDA, std::string("copy y: ") + cudaGetErrorString(ce)));
+  }
+  // finiteness check of the local data
+  {
+    unsigned long long* cnt = nullptr;
+    s = dalloc(&cnt, 1);
+    if (s != RS_OK) return guard(s);
+    cudaMemsetAsync(cnt, 0, 8, p->st);
+    launch_count_nonfinite(p->X, p->ldx, rows, d, cnt, p->st);
+    launch_count_nonfinite(p->y, 1, rows, 1, cnt, p->st);
+    unsigned long long h = 0;
+    cudaMemcpyAsync(&h, cnt, 8, cudaMemcpyDeviceToHost, p->st);
+    cudaError_t ce = cudaStreamSynchronize(p->st);
+    dfree(cnt);
+    if (ce != cudaSuccess) return guard(fail(RS_ECUDA, cudaGetErrorString(ce)));
+    if (h) return guard(fail(RS_EINVAL, "X or y has non-finite entries"));
+  }
+  cudaEventRecord(e0, p->st);
+  // b = X^T y  (primal), summed over ranks
+  s = dalloc(&p->b, d);
+  if (s != RS_OK) return guard(s);
+  {
+    double* work = nullptr;
+    s = dalloc(&work, dense_xty_work(rows, d));
+    if (s != RS_OK) return guard(s);
+    cudaError_t ce = launch_dense_xty(p->X, p->ldx, rows, d, p->y, p->b, work, p->st);
+    cudaStreamSynchronize(p->st);
+    dfree(work);
+    if (ce != cudaSuccess) return guard(fail(RS_ECUDA, cudaGetErrorString(ce)));
+    s = p->allreduce(p->b, d);
+    if (s != RS_OK) return guard(s);
+  }
+  if (mode == RS_AS_EXPLICIT) {  // A = X^T X + lambda I, built once (DSYRK-shaped DMMA contraction)
+    p->lda = round_up(d, 4);
+    s = dalloc(&p->A, (size_t)d * p->lda);
+    if (s != RS_OK) return guard(s);
+    GemmPlan gp = plan_tn_gemm(d, d, rows, p->num_sms);
+    double* work = nullptr;
+    if (gp.work_elems) {
+      s = dalloc(&work, gp.work_elems);
+      if (s != RS_OK) return guard(s);
+    }
+    cudaError_t ce = cudaSuccess;
+    if (rows > 0)
+      ce = launch_tn_gemm(p->X, p->ldx, p->X, p->ldx, d, d, rows, p->A, p->lda, gp, work, nullptr, p->st);
+    else
+      ce = launch_fill(p->A, (long long)d * p->lda, 0.0, p->st);
+    cudaStreamSynchronize(p->st);
+    dfree(work);
+    if (ce != cudaSuccess) return guard(fail(RS_ECUDA, std::string("A build: ") + cudaGetErrorString(ce)));
+    s = p->allreduce(p->A, (size_t)d * p->lda);
+    if (s != RS_OK) return guard(s);
+    launch_add_diag(p->A, p->lda, d, lambda, p->st);
+  }
+  cudaEventRecord(e1, p->st);
+  s = finish_setup(p);
+  if (s != RS_OK) return guard(s);
+  float ms = 0;
+  cudaEventElapsedTime(&ms, e0, e1);
+  p->setup_seconds = ms * 1e-3;
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaError_t ce = cudaGetLastError();
+  if (ce != cudaSuccess) return guard(fail(RS_ECUDA, cudaGetErrorString(ce)));
+  *out = reinterpret_cast<rs_problem>(p);
+  return RS_OK;
+}
+
+// ------------------------------------------------------------------------------------------------
+static rs_status validate_opts(const Problem* p, const rs_solve_opts* o, int* ksum) {
+  if (!o) return fail(RS_EINVAL, "opts is NULL");
+  if (o->kind != RS_SKETCH_SUBSAMPLE && o->kind != RS_SKETCH_COUNT && o->kind != RS_SKETCH_SUBCOUNT)
+    return fail(RS_EINVAL, "bad sketch kind");
+  if (o->tau < 1 || o->tau > p->m) return fail(RS_EINVAL, "need 1 <= tau <= m");
+  if (!(o->gamma > 0.0 && o->gamma <= 1.0)) return fail(RS_EINVAL, "need gamma in (0, 1] (P:L566)");
+  if (!(o->beta >= 0.0 && o->beta <= 1.0)) return fail(RS_EINVAL, "need beta in [0, 1] (P:L566)");
+  if (!(o->tol >= 0.0) || !std::isfinite(o->tol)) return fail(RS_EINVAL, "need finite tol >= 0");
+  if (o->max_iter < 0) return fail(RS_EINVAL, "need max_iter >= 0");
+  if (o->trace_cap < 0 || (o->trace_cap > 0 && !o->trace)) return fail(RS_EINVAL, "bad trace buffer");
+  *ksum = 1;
+  if (o->kind == RS_SKETCH_SUBCOUNT) {
+    long long k = o->subcount_k;
+    if (k < 0) return fail(RS_EINVAL, "subcount_k < 0");
+    if (k == 0) k = (10 * o->tau <= p->m) ? 10 : p->m / o->tau;
+    if (k * o->tau > p->m) return fail(RS_EINVAL, "subcount: k * tau > m");
+    *ksum = (int)k;
+  }
+  if (o->kind == RS_SKETCH_COUNT && o->tau > 1536)
+    return fail(RS_EUNSUPPORTED, "count sketch with tau > 1536 not implemented");
+  if (o->kind != RS_SKETCH_COUNT && (long long)o->tau * *ksum > 8192)
+    return fail(RS_EUNSUPPORTED, "selection of more than 8192 coordinates not implemented");
+  if (p->m > 0x7fffffffLL) return fail(RS_EUNSUPPORTED, "m >= 2^31");
+  return RS_OK;
+}
+
+rs_status Problem::ensure_workspace(int kind, int tau, int ksum) {
+  if (ws_kind == kind && ws_tau == tau && ws_ksum == ksum) return RS_OK;
+  cudaStreamSynchronize(st);
+  free_workspace();
+  const size_t L = sketch_max_len(kind, (int)m, tau, ksum);
+  sk.kind = kind;
+  sk.m = (int)m;
+  sk.tau = tau;
+  sk.len = (int)L;
+  sk.ksum = ksum;
+  RS_TRY(dalloc(&sk.coord, L));
+  RS_TRY(dalloc(&sk.sign, L));
+  RS_TRY(dalloc(&sk.bucket, L));
+  RS_TRY(dalloc(&sk.bptr, tau + 1));
+  if (kind == SK_COUNT) RS_TRY(dalloc(&sk.cmap, m));
+  ld_as = round_up(m, 4);
+  RS_TRY(dalloc(&ASt, (size_t)tau * ld_as));
+  if (fmt == 0 && mode == RS_AS_IMPLICIT) {
+    ld_xs = round_up(tau, 4);
+    RS_TRY(dalloc(&XS, (size_t)std::max<long long>(rows_loc, 1) * ld_xs));
+    gp = plan_tn_gemm(tau, m, rows_loc, num_sms);
+    if (gp.work_elems) RS_TRY(dalloc(&gemm_work, gp.work_elems));
+  }
+  if (fmt == 1) RS_TRY(csr_ensure_workspace(kind, tau, ksum));
+  sw = plan_solve(tau, num_sms);
+  RS_TRY(dalloc(&sw.Gx, solve_gx_elems(tau)));
+  RS_TRY(dalloc(&sw.delta, tau));
+  RS_TRY(dalloc(&partials, update_partials(m)));
+  ws_kind = kind;
+  ws_tau = tau;
+  ws_ksum = ksum;
+  return RS_OK;
+}
+
+// One iteration of Alg. 2 as a launch sequence; `ev` (optional) = 2*RS_K_NCLASSES
+// events bracketing each kernel class.
+rs_status Problem::enqueue_iteration(const rs_solve_opts* o, cudaEvent_t* ev) {
+  auto mark = [&](int cls, int edge) {
+    if (ev) cudaEventRecord(ev[2 * cls + edge], st);
+  };
+  mark(RS_K_SKETCH, 0);
+  RS_CUDA(launch_sketch(sk, o->seed, ctrl, -1, st));                       // a1
+  mark(RS_K_SKETCH, 1);
+  if (fmt == 0 && mode == RS_AS_IMPLICIT) {
+    mark(RS_K_XS, 0);
+    RS_CUDA(launch_dense_xs(X, ldx, rows_loc, sk, XS, ld_xs, ctrl, st));    // a2  XS
+    mark(RS_K_XS, 1);
+    mark(RS_K_AS, 0);
+    RS_CUDA(launch_tn_gemm(XS, ld_xs, X, ldx, sk.tau, m, rows_loc, ASt, ld_as, gp, gemm_work,
+                           ctrl, st));                                       // a3  (X^T XS)^T
+    RS_TRY(allreduce(ASt, (size_t)sk.tau * ld_as));                         // sum over row shards
+    RS_CUDA(launch_add_lambda_s(lambda, sk, ASt, ld_as, false, ctrl, st));         // + lambda S
+    mark(RS_K_AS, 1);
+  } else if (fmt == 0) {
+    mark(RS_K_XS, 0);
+    RS_CUDA(launch_explicit_rows(A, lda, m, sk, ASt, ld_as, ctrl, st));      // a2  rows of A
+    mark(RS_K_XS, 1);
+  } else {
+    RS_TRY(csr_enqueue_as(o, ev));
+  }
+  mark(RS_K_SOLVE, 0);
+  RS_CUDA(launch_sketched_solve(ASt, ld_as, fmt == 1, r, sk, sw, sdelta, ctrl, st));  // a4 + a5
+  mark(RS_K_SOLVE, 1);
+  mark(RS_K_UPDATE, 0);
+  RS_CUDA(launch_update(ASt, ld_as, fmt == 1, sk.tau, sw.delta, sdelta, w, dw, r, dr, m, o->gamma, o->beta,
+                        partials, ctrl, st));                                // a6 + a7
+  mark(RS_K_UPDATE, 1);
+  return RS_OK;
+}
+
+static int status_of(int st) {
+  switch (st) {
+    case ST_DIVERGED: return RS_EDIVERGED;
+    case ST_NOTSPD: return RS_ENOTSPD;
+    case ST_OVERFLOW: return RS_EUNSUPPORTED;
+    default: return RS_OK;
+  }
+}
+
+rs_status Problem::solve(const rs_solve_opts* o, double* w_out, rs_mem w_mem, double* alpha_out,
+                         rs_report* rep) {
+  int ksum = 1;
+  RS_TRY(validate_opts(this, o, &ksum));
+  if (!w_out) return fail(RS_EINVAL, "w_out is NULL");
+  RS_CUDA(cudaSetDevice(device));
+  RS_TRY(ensure_workspace((int)o->kind, (int)o->tau, ksum));
+  // state: w^{-1} = w^0 = 0, r^{-1} = r^0 = -b
+  RS_CUDA(launch_fill(w, m, 0.0, st));
+  RS_CUDA(launch_fill(dw, m, 0.0, st));
+  RS_CUDA(launch_fill(dr, m, 0.0, st));
+  RS_CUDA(launch_fill(sdelta, m, 0.0, st));
+  RS_CUDA(launch_axpby_neg(b, r, m, st));
+  dfree(trace_dev);
+  trace_dev = nullptr;
+  if (o->trace_cap > 0) RS_TRY(dalloc(&trace_dev, o->trace_cap));
+  Ctrl c{};
+  c.k = 0;
+  c.bnorm2 = bnorm2;
+  c.rnorm2 = bnorm2;
+  c.tol = o->tol;
+  c.max_iter = o->max_iter;
+  c.trace = trace_dev;
+  c.trace_cap = o->trace_cap;
+  c.status = ST_RUNNING;
+  if (bnorm2 == 0.0 || o->tol >= 1.0) {   // ||r^0|| <= tol ||r^0||: w = 0 is returned
+    c.done = 1;
+    c.status = ST_CONVERGED;
+  } else if (o->max_iter == 0) {
+    c.done = 1;
+    c.status = ST_MAXITER;
+  }
+  *ctrl_host = c;
+  RS_CUDA(cudaMemcpyAsync(ctrl, ctrl_host, sizeof(Ctrl), cudaMemcpyHostToDevice, st));
+
+  // CUDA graph of `chunk` iterations
+  const int chunk = (int)(o->check_every > 0 ? std::min<long long>(o->check_every, 1024) : 16);
+  if (graph_exec) cudaGraphExecDestroy(graph_exec);
+  graph_exec = nullptr;
+  for (auto ev : prof_events) cudaEventDestroy(ev);
+  prof_events.clear();
+  if (o->profile) {
+    prof_events.resize((size_t)chunk * 2 * RS_K_NCLASSES);
+    for (auto& ev : prof_events) RS_CUDA(cudaEventCreate(&ev));
+  }
+  RS_CUDA(cudaStreamSynchronize(st));
+  {
+    cudaGraph_t g = nullptr;
+    RS_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+    rs_status s = RS_OK;
+    for (int i = 0; i < chunk && s == RS_OK; ++i)
+      s = enqueue_iteration(o, o->profile ? &prof_events[(size_t)i * 2 * RS_K_NCLASSES] : nullptr);
+    cudaError_t ce = cudaStreamEndCapture(st, &g);
+    if (s != RS_OK) {
+      if (g) cudaGraphDestroy(g);
+      return s;
+    }
+    if (ce != cudaSuccess) return fail(RS_ECUDA, std::string("graph capture: ") + cudaGetErrorString(ce));
+    ce = cudaGraphInstantiate(&graph_exec, g, 0);
+    cudaGraphDestroy(g);
+    if (ce != cudaSuccess) return fail(RS_ECUDA, std::string("graph instantiate: ") + cudaGetErrorString(ce));
+  }
+  double kms[RS_K_NCLASSES] = {0};
+  long long klaunch[RS_K_NCLASSES] = {0};
+  cudaEvent_t t0, t1;
+  RS_CUDA(cudaEventCreate(&t0));
+  RS_CUDA(cudaEventCreate(&t1));
+  RS_CUDA(cudaEventRecord(t0, st));
+  long long k_prev = 0;
+  while (!ctrl_host->done) {
+    RS_CUDA(cudaGraphLaunch(graph_exec, st));
+    RS_CUDA(cudaMemcpyAsync(ctrl_host, ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, st));
+    RS_CUDA(cudaStreamSynchronize(st));
+    if (o->profile) {
+      const long long ran = std::min<long long>(ctrl_host->k - k_prev, chunk);
+      for (long long i = 0; i < ran; ++i)
+        for (int cls = 0; cls < RS_K_NCLASSES; ++cls) {
+          float ms = 0;
+          cudaEvent_t* ev = &prof_events[(size_t)i * 2 * RS_K_NCLASSES];
+          if (cudaEventElapsedTime(&ms, ev[2 * cls], ev[2 * cls + 1]) == cudaSuccess && ms > 0) {
+            kms[cls] += ms;
+            klaunch[cls] += 1;
+          }
+        }
+      cudaGetLastError();
+    }
+    if (world > 1 && comm) {
+      std::string err;
+      const NcclApi* api = nccl_api(&err);
+      ncclResult_t ae = ncclSuccess;
+      if (api && api->ncclCommGetAsyncError(comm, &ae) == ncclSuccess && ae != ncclSuccess) {
+        api->ncclCommAbort(comm);
+        comm = nullptr;
+        return fail(RS_ENCCL, std::string("NCCL async error: ") + api->ncclGetErrorString(ae));
+      }
+    }
+    k_prev = ctrl_host->k;
+  }
+  RS_CUDA(cudaEventRecord(t1, st));
+  RS_CUDA(cudaEventSynchronize(t1));
+  float solve_ms = 0;
+  cudaEventElapsedTime(&solve_ms, t0, t1);
+  cudaEventDestroy(t0);
+  cudaEventDestroy(t1);
+  last_status = ctrl_host->status;
+
+  const Ctrl& h = *ctrl_host;
+  rs_report R{};
+  R.iterations = h.k;
+  R.converged = h.status == ST_CONVERGED;
+  R.rel_residual = bnorm2 > 0 ? std::sqrt(h.rnorm2) / std::sqrt(bnorm2) : 0.0;
+  R.setup_seconds = setup_seconds;
+  R.solve_seconds = solve_ms * 1e-3;
+  R.trace_len = std::min<long long>(h.k, o->trace_cap);
+  for (int cls = 0; cls < RS_K_NCLASSES; ++cls) {
+    R.kernel_ms[cls] = kms[cls];
+    R.kernel_launches[cls] = klaunch[cls];
+  }
+  if (rep) *rep = R;
+  if (o->trace && R.trace_len > 0)
+    RS_CUDA(cudaMemcpy(o->trace, trace_dev, R.trace_len * 8, cudaMemcpyDeviceToHost));
+  const int rc = status_of(h.status);
+  if (rc == RS_EUNSUPPORTED)
+    return fail(RS_EUNSUPPORTED, "CSR dual: sketched-row hash table overflow (bucket too dense)");
+  if (rc == RS_ENOTSPD)
+    return fail(RS_ENOTSPD, "Cholesky pivot <= 0 in S^T A S at iteration " + std::to_string(h.k));
+  // outputs (also on divergence: the last iterate)
+  RS_TRY(write_weights(w_out, w_mem, alpha_out));
+  if (rc == RS_EDIVERGED)
+    return fail(RS_EDIVERGED, "residual diverged (non-finite or > 1e8 relative) at iteration " +
+                                  std::to_string(h.k));
+  return RS_OK;
+}
+
+rs_status Problem::write_weights(double* w_out, rs_mem w_mem, double* alpha_out) {
+  const cudaMemcpyKind kd = w_mem == RS_MEM_HOST ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice;
+  if (route == 1) {
+    RS_CUDA(cudaMemcpyAsync(w_out, w, m * 8, kd, st));
+  } else {
+    RS_TRY(csr_dual_weights(w_out, kd));
+    if (alpha_out) RS_CUDA(cudaMemcpyAsync(alpha_out, w, m * 8, cudaMemcpyDeviceToHost, st));
+  }
+  RS_CUDA(cudaStreamSynchronize(st));
+  return RS_OK;
+}
+
+}  // namespace rs
+
+// ================================================================================================
+// C ABI
+using rs::Problem;
+using rs::fail;
+
+extern "C" {
+
+rs_status rs_create_dense(rs_problem* out, int64_t n, int64_t d, const double* X_local, int64_t ldx,
+                          const double* y, double lambda, rs_route route, rs_as_mode mode,
+                          rs_mem mem, const rs_dist* dist) {
+  return rs::create_dense(out, n, d, X_local, ldx, y, lambda, route, mode, mem, dist);
+}
+
+rs_status rs_create_csr(rs_problem* out, int64_t n, int64_t d, int64_t nnz_local,
+                        const int64_t* rowptr, const int32_t* colidx, const double* vals,
+                        const double* y, double lambda, rs_route route, rs_as_mode mode, rs_mem mem,
+                        const rs_dist* dist) {
+  return rs::create_csr(out, n, d, nnz_local, rowptr, colidx, vals, y, lambda, route, mode, mem,
+                        dist);
+}
+
+rs_status rs_solve(rs_problem p, const rs_solve_opts* opts, double* w_out, rs_mem w_mem,
+                   double* alpha_out, rs_report* report) {
+  if (!p) return fail(RS_EINVAL, "problem is NULL");
+  return reinterpret_cast<Problem*>(p)->solve(opts, w_out, w_mem, alpha_out, report);
+}
+
+rs_status rs_get_state(rs_problem p, double* w_sys, double* r, rs_mem mem) {
+  if (!p) return fail(RS_EINVAL, "problem is NULL");
+  Problem* q = reinterpret_cast<Problem*>(p);
+  if (!q->w) return fail(RS_EINVAL, "no state");
+  const cudaMemcpyKind kd = mem == RS_MEM_HOST ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice;
+  cudaSetDevice(q->device);
+  if (w_sys) RS_CUDA(cudaMemcpyAsync(w_sys, q->w, q->m * 8, kd, q->st));
+  if (r) RS_CUDA(cudaMemcpyAsync(r, q->r, q->m * 8, kd, q->st));
+  RS_CUDA(cudaStreamSynchronize(q->st));
+  return RS_OK;
+}
+
+rs_status rs_get_info(rs_problem p, int64_t* m, int* route) {
+  if (!p) return fail(RS_EINVAL, "problem is NULL");
+  Problem* q = reinterpret_cast<Problem*>(p);
+  if (m) *m = q->m;
+  if (route) *route = q->route;
+  return RS_OK;
+}
+
+rs_status rs_sketch_draw(rs_sketch_kind kind, int64_t m, int64_t tau, int64_t subcount_k,
+                         uint64_t seed, int64_t iter, int device, int32_t* coord, int32_t* bucket,
+                         int8_t* sign, int64_t* len_out) {
+  if (m < 1 || m > 0x7fffffffLL || tau < 1 || tau > m || iter < 0 || iter > 0xffffffffLL)
+    return fail(RS_EINVAL, "need 1 <= tau <= m < 2^31 and 0 <= iter < 2^32");
+  if (!coord || !bucket || !sign || !len_out) return fail(RS_EINVAL, "NULL output");
+  long long k = 1;
+  if (kind == RS_SKETCH_SUBCOUNT) {
+    k = subcount_k > 0 ? subcount_k : ((10 * tau <= m) ? 10 : m / tau);
+    if (k * tau > m) return fail(RS_EINVAL, "subcount: k * tau > m");
+  } else if (kind != RS_SKETCH_SUBSAMPLE && kind != RS_SKETCH_COUNT) {
+    return fail(RS_EINVAL, "bad sketch kind");
+  }
+  if (kind == RS_SKETCH_COUNT && tau > 1536) return fail(RS_EUNSUPPORTED, "count tau > 1536");
+  if (kind != RS_SKETCH_COUNT && tau * k > 8192) return fail(RS_EUNSUPPORTED, "selection > 8192");
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) return fail(RS_ECUDA, "no CUDA device");
+  RS_CUDA(cudaSetDevice(device));
+  rs::DevSketch sk{};
+  sk.kind = (int)kind;
+  sk.m = (int)m;
+  sk.tau = (int)tau;
+  sk.ksum = (int)k;
+  sk.len = (int)rs::sketch_max_len(sk.kind, sk.m, sk.tau, sk.ksum);
+  const size_t L = sk.len;
+  RS_CUDA(cudaMalloc(&sk.coord, L * 4));
+  RS_CUDA(cudaMalloc(&sk.bucket, L * 4));
+  RS_CUDA(cudaMalloc(&sk.sign, L));
+  RS_CUDA(cudaMalloc(&sk.bptr, (tau + 1) * 4));
+  if (kind == RS_SKETCH_COUNT) RS_CUDA(cudaMalloc(&sk.cmap, m * 4));
+  cudaError_t e = rs::launch_sketch(sk, seed, nullptr, iter, 0);
+  if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  if (e == cudaSuccess) e = cudaMemcpy(coord, sk.coord, L * 4, cudaMemcpyDeviceToHost);
+  if (e == cudaSuccess) e = cudaMemcpy(bucket, sk.bucket, L * 4, cudaMemcpyDeviceToHost);
+  if (e == cudaSuccess) e = cudaMemcpy(sign, sk.sign, L, cudaMemcpyDeviceToHost);
+  cudaFree(sk.coord);
+  cudaFree(sk.bucket);
+  cudaFree(sk.sign);
+  cudaFree(sk.bptr);
+  if (sk.cmap) cudaFree(sk.cmap);
+  if (e != cudaSuccess) return fail(RS_ECUDA, std::string("sketch draw: ") + cudaGetErrorString(e));
+  *len_out = (int64_t)L;
+  return RS_OK;
+}
+
+rs_status rs_shard_range(int64_t total, int rank, int world, int64_t* begin, int64_t* len) {
+  if (total < 0 || world < 1 || rank < 0 || rank >= world || !begin || !len)
+    return fail(RS_EINVAL, "bad shard arguments");
+  const int64_t q = total / world, rem = total % world;
+  *begin = rank * q + std::min<int64_t>(rank, rem);
+  *len = q + (rank < rem ? 1 : 0);
+  return RS_OK;
+}
+
+rs_status rs_shard_rows_nnz(int64_t n_rows, const int64_t* rowptr, int rank, int world,
+                            int64_t* begin, int64_t* len) {
+  if (n_rows < 0 || !rowptr || world < 1 || rank < 0 || rank >= world || !begin || !len)
+    return fail(RS_EINVAL, "bad shard arguments");
+  // boundary t (t = 1..world-1) = first row whose prefix nnz reaches t * nnz / world
+  const int64_t nnz = rowptr[n_rows];
+  auto boundary = [&](int t) -> int64_t {
+    if (t <= 0) return 0;
+    if (t >= world) return n_rows;
+    const long double target = (long double)nnz * t / world;
+    int64_t lo = 0, hi = n_rows;   // smallest row index i with rowptr[i] >= target
+    while (lo < hi) {
+      const int64_t mid = (lo + hi) / 2;
+      if ((long double)rowptr[mid] >= target) hi = mid;
+      else lo = mid + 1;
+    }
+    return lo;
+  };
+  const int64_t b0 = boundary(rank), b1 = boundary(rank + 1);
+  *begin = b0;
+  *len = std::max<int64_t>(0, b1 - b0);
+  return RS_OK;
+}
+
+rs_status rs_nccl_unique_id(void* out128) {
+  if (!out128) return fail(RS_EINVAL, "NULL output");
+  std::string err;
+  const rs::NcclApi* api = rs::nccl_api(&err);
+  if (!api) return fail(RS_ENCCL, err);
+  ncclUniqueId id;
+  ncclResult_t e = api->ncclGetUniqueId(&id);
+  if (e != ncclSuccess) return fail(RS_ENCCL, api->ncclGetErrorString(e));
+  std::memcpy(out128, &id, sizeof(id));
+  return RS_OK;
+}
+
+void rs_destroy(rs_problem p) { delete reinterpret_cast<Problem*>(p); }
+
+const char* rs_status_string(rs_status s) {
+  switch (s) {
+    case RS_OK: return "RS_OK";
+    case RS_EINVAL: return "RS_EINVAL: invalid argument";
+    case RS_EUNSUPPORTED: return "RS_EUNSUPPORTED: not implemented";
+    case RS_ENOMEM: return "RS_ENOMEM: device allocation failed";
+    case RS_ECUDA: return "RS_ECUDA: CUDA failure";
+    case RS_ENCCL: return "RS_ENCCL: NCCL failure";
+    case RS_ENOTSPD: return "RS_ENOTSPD: sketched system not positive definite";
+    case RS_EDIVERGED: return "RS_EDIVERGED: residual diverged";
+  }
+  return "unknown rs_status";
+}
+
+const char* rs_last_error(void) { return rs::g_last_error.c_str(); }
+
+int rs_abi_version(void) { return RS_ABI_VERSION; }
+
+}  // extern "C"

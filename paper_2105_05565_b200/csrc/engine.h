@@ -1,0 +1,121 @@
+// Problem object of the host engine (internal).
+#pragma once
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/ridgesketch.h"
+#include "rs_internal.cuh"
+
+namespace rs {
+
+rs_status fail(rs_status s, const std::string& msg);
+rs_status validate_dist(const rs_dist* dist, long long total);
+rs_status create_csr(rs_problem* out, int64_t n, int64_t d, int64_t nnz_local, const int64_t* rowptr,
+                     const int32_t* colidx, const double* vals, const double* y, double lambda,
+                     rs_route route, rs_as_mode mode, rs_mem mem, const rs_dist* dist);
+
+struct CsrData;   // csr.cu
+
+struct Problem {
+  // placement
+  int device = -1, num_sms = 148;
+  cudaStream_t st = nullptr;
+  bool own_stream = false;
+  int rank = 0, world = 1;
+  ncclComm_t comm = nullptr;
+  // problem
+  int fmt = 0;      // 0 dense, 1 CSR
+  int route = 1;    // 1 primal (m = d), 2 dual (m = n)
+  int mode = 0;     // rs_as_mode
+  long long n = 0, d = 0, m = 0;
+  long long rows_loc = 0;   // dense primal: local rows of X
+  double lambda = 0.0;
+  double* X = nullptr;
+  long long ldx = 0;
+  bool own_X = false;
+  double* y = nullptr;
+  double* b = nullptr;
+  double bnorm2 = 0.0;
+  double* A = nullptr;
+  long long lda = 0;
+  CsrData* csr = nullptr;
+  double setup_seconds = 0.0;
+  // iteration state (x, dx = x^k - x^{k-1}), R13
+  double *w = nullptr, *dw = nullptr, *r = nullptr, *dr = nullptr, *sdelta = nullptr;
+  Ctrl* ctrl = nullptr;
+  Ctrl* ctrl_host = nullptr;
+  double* trace_dev = nullptr;
+  double* scratch = nullptr;
+  int last_status = 0;
+  // per-(kind, tau) workspace
+  int ws_kind = -1, ws_tau = -1, ws_ksum = -1;
+  DevSketch sk{};
+  double* XS = nullptr;
+  long long ld_xs = 0;
+  double* ASt = nullptr;
+  long long ld_as = 0;
+  double* gemm_work = nullptr;
+  GemmPlan gp{};
+  SolveWork sw{};
+  double* partials = nullptr;
+  cudaGraphExec_t graph_exec = nullptr;
+  std::vector<cudaEvent_t> prof_events;
+
+  ~Problem();
+  void free_workspace();
+  rs_status allreduce(double* buf, size_t count);
+  rs_status ensure_workspace(int kind, int tau, int ksum);
+  rs_status enqueue_iteration(const rs_solve_opts* o, cudaEvent_t* ev);
+  rs_status solve(const rs_solve_opts* o, double* w_out, rs_mem w_mem, double* alpha_out,
+                  rs_report* rep);
+  rs_status write_weights(double* w_out, rs_mem w_mem, double* alpha_out);
+  // CSR parts (csr.cu)
+  void csr_free();
+  void csr_free_workspace();
+  rs_status csr_ensure_workspace(int kind, int tau, int ksum);
+  rs_status csr_enqueue_as(const rs_solve_opts* o, cudaEvent_t* ev);
+  rs_status csr_dual_weights(double* w_out, cudaMemcpyKind kd);
+};
+
+rs_status finish_setup(Problem* p);
+rs_status setup_common(Problem* p, const rs_dist* dist);
+
+#define RS_CUDA(expr)                                                                  \
+  do {                                                                                 \
+    cudaError_t _e = (expr);                                                           \
+    if (_e != cudaSuccess)                                                             \
+      return ::rs::fail(_e == cudaErrorMemoryAllocation ? RS_ENOMEM : RS_ECUDA,        \
+                        std::string(#expr) + ": " + cudaGetErrorString(_e));           \
+  } while (0)
+
+#define RS_TRY(expr)                  \
+  do {                                \
+    rs_status _s = (expr);            \
+    if (_s != RS_OK) return _s;       \
+  } while (0)
+
+template <class T>
+inline rs_status dalloc(T** p, size_t n) {
+  *p = nullptr;
+  if (n == 0) n = 1;
+  cudaError_t e = cudaMalloc(reinterpret_cast<void**>(p), n * sizeof(T));
+  if (e != cudaSuccess)
+    return fail(RS_ENOMEM, std::string("cudaMalloc(") + std::to_string(n * sizeof(T)) +
+                               " bytes): " + cudaGetErrorString(e));
+  return RS_OK;
+}
+
+inline void dfree(void* p) {
+  if (p) cudaFree(p);
+}
+
+inline long long round_up(long long x, long long q) { return (x + q - 1) / q * q; }
+
+inline cudaMemcpyKind kind_of(rs_mem mem) {
+  return mem == RS_MEM_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice;
+}
+
+}  // namespace rs

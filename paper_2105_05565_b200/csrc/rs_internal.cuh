@@ -1,0 +1,135 @@
+// Internal declarations shared by the CUDA translation units of libridgesketch.so.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace rs {
+
+// ---------------------------------------------------------------------------------------------
+// Device-resident control block: iteration counter, stop flag, residual norms.  Every per-iteration
+// kernel reads `done` first and returns immediately when it is set, so a CUDA graph of K captured
+// iterations stops exactly at the iteration where the stop rule fired (P:L729 while-condition).
+enum : int {
+  ST_RUNNING = 0, ST_CONVERGED = 1, ST_MAXITER = 2,
+  // errors (>= ST_DIVERGED): set by the kernel that detects them; the update kernel turns them
+  // into `done` (a cooperative kernel must never set `done` itself, see chol.cu)
+  ST_DIVERGED = 3, ST_NOTSPD = 4, ST_OVERFLOW = 5
+};
+
+struct Ctrl {
+  long long k;          // iterations performed so far (the sketch of the next step is S_k)
+  int done;             // 1: stop
+  int status;           // ST_*
+  double rnorm2;        // ||r^k||^2 of the maintained residual
+  double bnorm2;        // ||r^0||^2 = ||b||^2
+  double tol;
+  long long max_iter;
+  unsigned int arrive;  // last-block-done counter of the update kernel
+  int pad;
+  double* trace;        // device, may be null
+  long long trace_cap;
+};
+
+// ---------------------------------------------------------------------------------------------
+// Philox4x32-10 (Salmon et al., SC'11) -- the sketch-stream generator, DESIGN.md Section 3.
+__device__ __forceinline__ uint4 philox4x32_10(uint4 c, uint2 k) {
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    const unsigned lo0 = 0xD2511F53u * c.x, hi0 = __umulhi(0xD2511F53u, c.x);
+    const unsigned lo1 = 0xCD9E8D57u * c.z, hi1 = __umulhi(0xCD9E8D57u, c.z);
+    c = make_uint4(hi1 ^ c.y ^ k.x, lo1, hi0 ^ c.w ^ k.y, lo0);
+    if (r < 9) { k.x += 0x9E3779B9u; k.y += 0xBB67AE85u; }
+  }
+  return c;
+}
+
+// Sketch stream ids.
+enum : unsigned { STREAM_SELECT = 0, STREAM_COUNT = 1, STREAM_SUBCOUNT_SIGN = 2 };
+enum : int { SK_SUBSAMPLE = 0, SK_COUNT = 1, SK_SUBCOUNT = 2 };
+
+// Device sketch in bucket order: entries e in [bptr[b], bptr[b+1]) belong to bucket b;
+// S[coord[e], b] = sign[e].  For the count sketch cmap[i] = (bucket << 1) | (sign < 0) for every
+// coordinate i (the per-coordinate table used by the CSR primal kernel).
+struct DevSketch {
+  int kind;
+  int m, tau, len, ksum;  // len = number of entries; ksum = SubCount k
+  int* coord;             // [len_cap]
+  signed char* sign;      // [len_cap]
+  int* bucket;            // [len_cap]
+  int* bptr;              // [tau + 1]
+  int* cmap;              // [m] (count only)
+};
+
+// ---------------------------------------------------------------------------------------------
+// Kernel launchers (each returns cudaGetLastError()).  All take the control block so that they can
+// no-op once the solve has stopped.
+
+// a1 sketch draw.  uses seed key and iteration k read from ctrl (or `fixed_k` >= 0 if given).
+cudaError_t launch_sketch(const DevSketch& sk, uint64_t seed, const Ctrl* ctrl, long long fixed_k,
+                          cudaStream_t st);
+size_t sketch_max_len(int kind, int m, int tau, int ksum);
+
+// a2 dense: XS[i, b] = sum_{e in b} sign_e X[i, coord_e],  i < rows, row-major ld_xs (>= tau, pad
+// columns zeroed).
+cudaError_t launch_dense_xs(const double* X, long long ldx, long long rows, const DevSketch& sk,
+                            double* XS, long long ld_xs, const Ctrl* ctrl, cudaStream_t st);
+// a2 explicit: AS^T[b, :] = sum_{e in b} sign_e A[coord_e, :]  (A symmetric, m x m, ld lda).
+cudaError_t launch_explicit_rows(const double* A, long long lda, long long m, const DevSketch& sk,
+                                 double* ASt, long long ld_as, const Ctrl* ctrl, cudaStream_t st);
+
+// a3 dense TN contraction on FP64 tensor cores (DMMA):  C[M' x N'] (row-major, ldc) =
+//   sum_{k < K} Aop[k, 0:M'] (x) Bop[k, 0:N']  with Aop row-major (lda), Bop row-major (ldb),
+// split over `splits` K-ranges into `work` and reduced deterministically.  If work == nullptr,
+// splits must be 1.
+struct GemmPlan {
+  int bm, bn, splits;
+  long long k_per_split;
+  size_t work_elems;
+};
+GemmPlan plan_tn_gemm(long long M, long long N, long long K, int num_sms);
+cudaError_t launch_tn_gemm(const double* Aop, long long lda, const double* Bop, long long ldb,
+                           long long M, long long N, long long K, double* C, long long ldc,
+                           const GemmPlan& plan, double* work, const Ctrl* ctrl, cudaStream_t st);
+
+// lambda S:  AS^T[b_e, coord_e] += lambda * sign_e  (as_rowmajor: AS[coord_e, b_e]).
+cudaError_t launch_add_lambda_s(double lambda, const DevSketch& sk, double* ASt, long long ld_as,
+                                bool as_rowmajor, const Ctrl* ctrl, cudaStream_t st);
+// A += lambda I on a dense m x m.
+cudaError_t launch_add_diag(double* A, long long lda, long long m, double lambda, cudaStream_t st);
+
+// a4 + a5: G = S^T (A S) (lower), g = S^T r, empty-bucket rule, Cholesky, solves; writes
+// sdelta[coord_e] = sign_e * delta[b_e].  Gx / delta are workspace.
+struct SolveWork {
+  double* Gx;        // (tau + 1) x ldg, row-major, lower triangle + border row tau = g
+  long long ldg;
+  double* delta;     // tau
+  int grid;          // cooperative grid size for the Cholesky
+};
+SolveWork plan_solve(int tau, int num_sms);
+size_t solve_gx_elems(int tau);
+// AS layout: as_rowmajor = false -> AS^T stored tau x m (ld_as); true -> AS stored m x tau (ld_as).
+cudaError_t launch_sketched_solve(const double* ASt, long long ld_as, bool as_rowmajor,
+                                  const double* r, const DevSketch& sk, SolveWork& sw,
+                                  double* sdelta, Ctrl* ctrl, cudaStream_t st);
+
+// a6 fused update: u = AS delta (from AS^T rows), r/dr and w/dw heavy-ball, sdelta cleared,
+// ||r||^2, stop flag and iteration counter.
+size_t update_partials(long long m);
+cudaError_t launch_update(const double* ASt, long long ld_as, bool as_rowmajor, int tau,
+                          const double* delta, double* sdelta, double* w, double* dw, double* r,
+                          double* dr, long long m, double gamma, double beta, double* partials,
+                          Ctrl* ctrl, cudaStream_t st);
+
+// misc
+// *out += number of non-finite entries of the rows x cols block.
+cudaError_t launch_count_nonfinite(const double* X, long long ldx, long long rows, long long cols,
+                                   unsigned long long* out, cudaStream_t st);
+cudaError_t launch_fill(double* p, long long n, double v, cudaStream_t st);
+cudaError_t launch_axpby_neg(const double* b, double* r, long long m, cudaStream_t st);  // r = -b
+cudaError_t launch_dot_self(const double* x, long long n, double* out, cudaStream_t st);  // out = ||x||^2
+// y_out[j] = sum_i X[i, j] y[i]  (dense X^T y, rows x cols, deterministic two-pass).
+cudaError_t launch_dense_xty(const double* X, long long ldx, long long rows, long long cols,
+                             const double* y, double* out, double* work, cudaStream_t st);
+size_t dense_xty_work(long long rows, long long cols);
+
+}  // namespace rs

@@ -1,0 +1,194 @@
+// a6 + a7 -- fused momentum update and stop rule.
+//
+//   u = (A S_k) delta_k                                       ("multiplying a m x tau matrix")
+//   r^{k+1} = r^k - gamma u + beta (r^k - r^{k-1})            (Eq. res_update_mom)
+//   w^{k+1} = w^k - gamma S_k delta_k + beta (w^k - w^{k-1})
+// kept in the increment form (x, dx = x^k - x^{k-1}):  dx <- beta dx - gamma v;  x <- x + dx, which
+// is algebraically the printed recurrence (R13).  S_k delta_k arrives as the dense vector
+// `sdelta` (scattered by the solve kernel) and is cleared here for the next iteration.
+//   ||r^{k+1}||^2 is reduced deterministically (per-block partials, then the last block sums them
+// in a fixed order), and the last block applies the stop rule ||r^k|| <= tol ||r^0|| (P:L248-251,
+// DESIGN.md R1), the divergence guard and the iteration counter.
+#include "rs_internal.cuh"
+
+namespace rs {
+
+namespace {
+
+constexpr int UX = 32, UY = 8;   // block: 32 columns j x 8 slices of tau
+
+// k += 1, record ||r||, apply the stop rule (last block of the update kernel only).
+__device__ void finish_iteration(Ctrl* ctrl, double tot) {
+  ctrl->arrive = 0;
+  ctrl->rnorm2 = tot;
+  const long long k = ctrl->k + 1;
+  ctrl->k = k;
+  const double rel = sqrt(tot) / sqrt(ctrl->bnorm2);
+  if (ctrl->trace && k <= ctrl->trace_cap) ctrl->trace[k - 1] = rel;
+  if (!isfinite(tot) || rel > 1e8) {
+    ctrl->status = ST_DIVERGED;
+    ctrl->done = 1;
+  } else if (rel <= ctrl->tol) {
+    ctrl->status = ST_CONVERGED;
+    ctrl->done = 1;
+  } else if (k >= ctrl->max_iter) {
+    ctrl->status = ST_MAXITER;
+    ctrl->done = 1;
+  }
+}
+
+__global__ void __launch_bounds__(UX * UY)
+k_update(const double* __restrict__ ASt, long long ld_as, int tau, const double* __restrict__ delta,
+         double* __restrict__ sdelta, double* __restrict__ w, double* __restrict__ dw,
+         double* __restrict__ r, double* __restrict__ dr, long long m, double gamma, double beta,
+         double* __restrict__ partials, Ctrl* ctrl) {
+  if (ctrl->done) return;
+  if (ctrl->status >= ST_NOTSPD) {   // set by the solve / AS kernels of this iteration
+    if (blockIdx.x == 0 && threadIdx.x == 0 && threadIdx.y == 0) ctrl->done = 1;
+    return;
+  }
+  __shared__ double red[UY][UX + 1];
+  __shared__ double s_delta[1024];
+  __shared__ bool s_last;
+  const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * UX + tx;
+  const long long j = (long long)blockIdx.x * UX + tx;
+  const bool small = tau <= 1024;
+  if (small)
+    for (int b = tid; b < tau; b += UX * UY) s_delta[b] = delta[b];
+  __syncthreads();
+  double acc = 0.0;
+  if (j < m) {
+    for (int b = ty; b < tau; b += UY) {
+      const double db = small ? s_delta[b] : delta[b];
+      acc += ASt[(long long)b * ld_as + j] * db;
+    }
+  }
+  red[ty][tx] = acc;
+  __syncthreads();
+  double r2 = 0.0;
+  if (ty == 0) {
+    if (j < m) {
+      double u = 0.0;
+#pragma unroll
+      for (int q = 0; q < UY; ++q) u += red[q][tx];
+      const double drj = beta * dr[j] - gamma * u;
+      const double rj = r[j] + drj;
+      dr[j] = drj;
+      r[j] = rj;
+      const double sd = sdelta[j];
+      sdelta[j] = 0.0;
+      const double dwj = beta * dw[j] - gamma * sd;
+      dw[j] = dwj;
+      w[j] += dwj;
+      r2 = rj * rj;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) r2 += __shfl_down_sync(0xffffffffu, r2, o);
+    if (tx == 0) {
+      partials[blockIdx.x] = r2;
+      __threadfence();
+      const unsigned prev = atomicAdd(&ctrl->arrive, 1u);
+      s_last = (prev == gridDim.x - 1);
+    }
+  }
+  __syncthreads();
+  if (!s_last) return;
+  // last block: fixed-order reduction of the partials
+  __threadfence();
+  double s = 0.0;
+  for (unsigned q = tid; q < gridDim.x; q += UX * UY) s += __ldcg(&partials[q]);
+  red[ty][tx] = s;
+  __syncthreads();
+  if (tid == 0) {
+    double tot = 0.0;
+    for (int q = 0; q < UY; ++q)
+      for (int p = 0; p < UX; ++p) tot += red[q][p];
+    finish_iteration(ctrl, tot);
+  }
+}
+
+// Same for AS stored row-major (m x tau): one warp per coordinate j, lanes over the tau columns.
+constexpr int RM_WARPS = 8;
+__global__ void __launch_bounds__(RM_WARPS * 32)
+k_update_rm(const double* __restrict__ AS, long long ld_as, int tau,
+            const double* __restrict__ delta, double* __restrict__ sdelta, double* __restrict__ w,
+            double* __restrict__ dw, double* __restrict__ r, double* __restrict__ dr, long long m,
+            double gamma, double beta, double* __restrict__ partials, Ctrl* ctrl) {
+  if (ctrl->done) return;
+  if (ctrl->status >= ST_NOTSPD) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) ctrl->done = 1;
+    return;
+  }
+  __shared__ double s_delta[1024];
+  __shared__ double red[RM_WARPS];
+  __shared__ bool s_last;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const bool small = tau <= 1024;
+  if (small)
+    for (int b = tid; b < tau; b += RM_WARPS * 32) s_delta[b] = delta[b];
+  __syncthreads();
+  double r2 = 0.0;
+  // each block: RM_WARPS * 4 consecutive coordinates, one warp per coordinate at a time
+  const long long jb = (long long)blockIdx.x * RM_WARPS * 4;
+  for (int q = warp; q < RM_WARPS * 4; q += RM_WARPS) {
+    const long long j = jb + q;
+    if (j >= m) break;
+    const double* row = AS + j * ld_as;
+    double u = 0.0;
+    for (int b = lane; b < tau; b += 32) u += row[b] * (small ? s_delta[b] : delta[b]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) u += __shfl_xor_sync(0xffffffffu, u, o);
+    if (lane == 0) {
+      const double drj = beta * dr[j] - gamma * u;
+      const double rj = r[j] + drj;
+      dr[j] = drj;
+      r[j] = rj;
+      const double sd = sdelta[j];
+      sdelta[j] = 0.0;
+      const double dwj = beta * dw[j] - gamma * sd;
+      dw[j] = dwj;
+      w[j] += dwj;
+      r2 += rj * rj;
+    }
+  }
+  if (lane == 0) red[warp] = r2;
+  __syncthreads();
+  if (tid == 0) {
+    double s = 0.0;
+    for (int q = 0; q < RM_WARPS; ++q) s += red[q];
+    partials[blockIdx.x] = s;
+    __threadfence();
+    const unsigned prev = atomicAdd(&ctrl->arrive, 1u);
+    s_last = (prev == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  if (tid == 0) {
+    double tot = 0.0;
+    for (unsigned q = 0; q < gridDim.x; ++q) tot += __ldcg(&partials[q]);
+    finish_iteration(ctrl, tot);
+  }
+}
+
+}  // namespace
+
+size_t update_partials(long long m) { return (size_t)((m + UX - 1) / UX); }
+
+cudaError_t launch_update(const double* ASt, long long ld_as, bool as_rowmajor, int tau,
+                          const double* delta, double* sdelta, double* w, double* dw, double* r,
+                          double* dr, long long m, double gamma, double beta, double* partials,
+                          Ctrl* ctrl, cudaStream_t st) {
+  if (as_rowmajor) {
+    const unsigned g = (unsigned)((m + RM_WARPS * 4 - 1) / (RM_WARPS * 4));
+    k_update_rm<<<g, RM_WARPS * 32, 0, st>>>(ASt, ld_as, tau, delta, sdelta, w, dw, r, dr, m, gamma,
+                                             beta, partials, ctrl);
+    return cudaGetLastError();
+  }
+  const unsigned grid = (unsigned)((m + UX - 1) / UX);
+  k_update<<<grid, dim3(UX, UY), 0, st>>>(ASt, ld_as, tau, delta, sdelta, w, dw, r, dr, m, gamma,
+                                          beta, partials, ctrl);
+  return cudaGetLastError();
+}
+
+}  // namespace rs

@@ -1,0 +1,261 @@
+"""GPU parity: the CUDA path (through the C ABI) against the oracle, element by element, on the
+same seeded inputs.  Tolerances: sketches bit-exact; w and r after 50 steps within
+1e-10 relative (BASELINE.json); final w within 1e-6 of the direct solve (c1)."""
+
+import numpy as np
+import pytest
+import scipy.sparse as sp
+import torch
+
+import rsinputs
+from oracle import problem as OP
+from oracle import sketch as OS
+from oracle import solver as OV
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def rs():
+    from paper_2105_05565_b200 import build
+    build()
+    from paper_2105_05565_b200 import ridgesketch
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    return ridgesketch
+
+
+def rel(a, b):
+    nb = np.linalg.norm(b)
+    return np.linalg.norm(a - b) / (nb if nb > 0 else 1.0)
+
+
+# ---------------------------------------------------------------------------------- a1 sketches
+SKETCH_CASES = [
+    ("subsample", 50, 10, 0), ("subsample", 2000, 200, 0), ("subsample", 4096, 1024, 0),
+    ("subsample", 37, 37, 0), ("subsample", 1, 1, 0), ("subsample", 20000, 1, 0),
+    ("subsample", 50000, 777, 0), ("count", 6, 2, 0), ("count", 50, 10, 0),
+    ("count", 50000, 500, 0), ("count", 1000, 1, 0), ("count", 3000, 1536, 0),
+    ("subcount", 20000, 256, 4), ("subcount", 100, 5, 0), ("subcount", 30, 30, 0),
+    ("subcount", 2000, 64, 0)]
+
+
+@pytest.mark.parametrize("kind,m,tau,k", SKETCH_CASES)
+def test_sketch_bit_exact(rs, kind, m, tau, k):
+    for seed, it in ((0, 0), (0, 1), (12345, 7), (2**40 + 5, 123456)):
+        coord, bucket, sign = rs.rs_sketch_draw(kind, m, tau, seed, it, k)
+        ref = OS.draw(kind, m, tau, it, seed, k)
+        if kind == "count":
+            # GPU entries are in bucket order (ascending coordinate within a bucket)
+            order = np.lexsort((ref["coord"], ref["bucket"]))
+            assert np.array_equal(coord, ref["coord"][order])
+            assert np.array_equal(bucket, ref["bucket"][order])
+            assert np.array_equal(sign.astype(np.float64), ref["sign"][order])
+        else:
+            assert np.array_equal(coord, ref["coord"])
+            assert np.array_equal(bucket, ref["bucket"])
+            assert np.array_equal(sign.astype(np.float64), ref["sign"])
+
+
+# ---------------------------------------------------------------------------------- dense paths
+def _dense(n, d, seed=0, col_decay=False, noise=0.1):
+    X, y = rsinputs.dense_problem(n, d, seed=seed, col_decay=col_decay, noise=noise)
+    return X.numpy(), y.numpy()
+
+
+def _run_gpu_dense(rs, X, y, lam, mode, kind, tau, beta, iters, seed=0, k=0, device_input=False):
+    if device_input:
+        h = rs.rs_create_dense(torch.from_numpy(X).cuda(), torch.from_numpy(y).cuda(), lam, mode=mode)
+    else:
+        h = rs.rs_create_dense(X, y, lam, mode=mode)
+    try:
+        w, rep = rs.rs_solve(h, kind, tau, 1.0, beta, 0.0, iters, seed, k, check_every=7)
+        ws, r = rs.rs_get_state(h)
+    finally:
+        rs.rs_destroy(h)
+    return w, r, rep
+
+
+@pytest.mark.parametrize("beta", [0.0, 0.5])
+@pytest.mark.parametrize("mode", ["implicit", "explicit"])
+def test_config1_50_steps(rs, beta, mode):
+    cfg = rsinputs.CONFIGS["c1"]
+    X, y = _dense(cfg.n, cfg.d, noise=cfg.noise)
+    w, r, rep = _run_gpu_dense(rs, X, y, cfg.lam, mode, "subsample", cfg.tau, beta, 50)
+    ref = OV.solve(X, y, cfg.lam, "subsample", cfg.tau, 1.0, beta, 0.0, 50, seed=0)
+    assert rep["iterations"] == 50
+    assert rel(w, ref["w"]) <= 1e-10
+    assert rel(r, ref["r"]) <= 1e-10
+
+
+@pytest.mark.parametrize("mode", ["implicit", "explicit"])
+def test_config1_final_vs_direct(rs, mode):
+    cfg = rsinputs.CONFIGS["c1"]
+    X, y = _dense(cfg.n, cfg.d, noise=cfg.noise)
+    w, r, rep = _run_gpu_dense(rs, X, y, cfg.lam, mode, "subsample", cfg.tau, 0.0, 300)
+    pr = OP.build(X, y, cfg.lam)
+    w_star = OP.direct_solve(pr["A"], pr["b"])
+    assert rep["iterations"] == 300
+    assert rel(w, w_star) <= 1e-6
+    w5, _, _ = _run_gpu_dense(rs, X, y, cfg.lam, mode, "subsample", cfg.tau, 0.5, 1000)
+    assert rel(w5, w_star) <= 1e-6
+
+
+@pytest.mark.parametrize("kind,tau,k", [("subsample", 37, 0), ("count", 37, 0), ("subcount", 29, 3),
+                                        ("subsample", 130, 0), ("count", 300, 0)])
+@pytest.mark.parametrize("mode", ["implicit", "explicit"])
+def test_dense_ragged_parity(rs, kind, tau, k, mode):
+    """Several GEMM tiles (64 x 128) with ragged tails, split-K, all sketch kinds."""
+    X, y = _dense(3001, 301, seed=3, col_decay=True, noise=0.01)
+    lam = 0.3
+    w, r, rep = _run_gpu_dense(rs, X, y, lam, mode, kind, tau, 0.5, 12, seed=5, k=k,
+                               device_input=True)
+    ref = OV.solve(X, y, lam, kind, tau, 1.0, 0.5, 0.0, 12, seed=5, subcount_k=k)
+    assert rep["iterations"] == 12
+    assert rel(w, ref["w"]) <= 1e-10
+    assert rel(r, ref["r"]) <= 1e-10
+
+
+def test_dense_identity_sketch_one_step(rs):
+    X, y = _dense(400, 64, seed=4)
+    w, r, rep = _run_gpu_dense(rs, X, y, 0.5, "implicit", "subsample", 64, 0.0, 1)
+    pr = OP.build(X, y, 0.5)
+    w_star = np.linalg.solve(pr["A"], pr["b"])
+    assert rel(w, w_star) <= 1e-10 and np.linalg.norm(r) <= 1e-9 * np.linalg.norm(pr["b"])
+
+
+def test_dense_tau1_coordinate_descent(rs):
+    X, y = _dense(200, 20, seed=5)
+    w, r, rep = _run_gpu_dense(rs, X, y, 0.2, "implicit", "subsample", 1, 0.3, 40, seed=17)
+    ref = OV.solve(X, y, 0.2, "subsample", 1, 1.0, 0.3, 0.0, 40, seed=17)
+    assert rel(w, ref["w"]) <= 1e-10
+
+
+def test_tolerance_stop_iteration_count(rs):
+    X, y = _dense(2000, 100, seed=6, col_decay=True)
+    h = rs.rs_create_dense(X, y, 1.0)
+    try:
+        w, rep = rs.rs_solve(h, "subsample", 20, 1.0, 0.5, 1e-6, 100000, 3, trace_cap=5000)
+    finally:
+        rs.rs_destroy(h)
+    ref = OV.solve(X, y, 1.0, "subsample", 20, 1.0, 0.5, 1e-6, 100000, seed=3, trace=True)
+    assert rep["converged"] and ref["converged"]
+    assert abs(rep["iterations"] - ref["iterations"]) <= 1
+    n = min(len(rep["trace"]), len(ref["trace"]))
+    assert np.allclose(rep["trace"][:n], ref["trace"][:n], rtol=1e-8, atol=0)
+    assert rel(w, ref["w"]) <= 1e-8
+
+
+def test_zero_rhs_and_zero_iterations(rs):
+    X, _ = _dense(50, 5)
+    h = rs.rs_create_dense(X, np.zeros(50), 1.0)
+    try:
+        w, rep = rs.rs_solve(h, "subsample", 2, tol=1e-4, max_iter=100)
+        assert rep["iterations"] == 0 and rep["converged"] and np.all(w == 0)
+    finally:
+        rs.rs_destroy(h)
+    h = rs.rs_create_dense(X, np.ones(50), 1.0)
+    try:
+        w, rep = rs.rs_solve(h, "subsample", 2, tol=0.0, max_iter=0)
+        assert rep["iterations"] == 0 and np.all(w == 0)
+    finally:
+        rs.rs_destroy(h)
+
+
+def test_invalid_arguments_fail_loudly(rs):
+    X, y = _dense(50, 5)
+    with pytest.raises(rs.RSError) as e:
+        rs.rs_create_dense(np.where(X > 1, np.nan, X), y, 1.0)
+    assert e.value.status == rs.RS_EINVAL
+    h = rs.rs_create_dense(X, y, 1.0)
+    try:
+        for kw in (dict(tau=0), dict(tau=6), dict(gamma=0.0), dict(beta=1.5), dict(tol=-1.0)):
+            args = dict(kind="subsample", tau=2)
+            args.update(kw)
+            with pytest.raises(rs.RSError) as e:
+                rs.rs_solve(h, **args)
+            assert e.value.status == rs.RS_EINVAL
+        with pytest.raises(rs.RSError) as e:
+            rs.rs_solve(h, "subcount", tau=2, subcount_k=3)      # k tau = 6 > m = 5
+        assert e.value.status == rs.RS_EINVAL
+    finally:
+        rs.rs_destroy(h)
+
+
+# ---------------------------------------------------------------------------------- CSR paths
+def _csr_primal(n=4000, d=600, per_row=12, seed=1):
+    rp, ci, v, y = rsinputs.csr_uniform(n, d, per_row, seed=seed)
+    return rp, ci, v, y, rsinputs.csr_to_scipy(rp, ci, v, n, d)
+
+
+@pytest.mark.parametrize("kind,tau,k", [("count", 40, 0), ("subsample", 33, 0), ("subcount", 20, 3),
+                                        ("count", 599, 0)])
+def test_csr_primal_parity(rs, kind, tau, k):
+    n, d = 4000, 600
+    rp, ci, v, y, Xs = _csr_primal(n, d)
+    lam = 1e-2
+    h = rs.rs_create_csr(n, d, rp, ci, v, y, lam)
+    try:
+        w, rep = rs.rs_solve(h, kind, tau, 1.0, 0.5, 0.0, 15, seed=2, subcount_k=k)
+        ws, r = rs.rs_get_state(h)
+    finally:
+        rs.rs_destroy(h)
+    ref = OV.solve(Xs, y, lam, kind, tau, 1.0, 0.5, 0.0, 15, seed=2, subcount_k=k)
+    assert rel(w, ref["w"]) <= 1e-10
+    assert rel(r, ref["r"]) <= 1e-10
+
+
+@pytest.mark.parametrize("kind,tau,k", [("subcount", 16, 4), ("subsample", 25, 0), ("count", 12, 0)])
+def test_csr_dual_parity(rs, kind, tau, k):
+    n, d = 300, 5000
+    rp, ci, v, y = rsinputs.csr_zipf(n, d, 60, a=1.1, seed=3)
+    Xs = rsinputs.csr_to_scipy(rp, ci, v, n, d)
+    lam = 1e-1
+    h = rs.rs_create_csr(n, d, rp, ci, v, y, lam)
+    try:
+        w, rep = rs.rs_solve(h, kind, tau, 1.0, 0.5, 0.0, 15, seed=4, subcount_k=k, d=d, alpha=True)
+        alpha, r = rs.rs_get_state(h)
+    finally:
+        rs.rs_destroy(h)
+    ref = OV.solve(Xs, y, lam, kind, tau, 1.0, 0.5, 0.0, 15, seed=4, subcount_k=k)
+    assert ref["route"] == "dual"
+    assert rel(alpha, ref["w"]) <= 1e-10
+    assert rel(rep["alpha"], ref["w"]) <= 1e-10
+    assert rel(r, ref["r"]) <= 1e-10
+    assert rel(w, ref["weights"]) <= 1e-10
+
+
+def test_csr_dual_converges_to_direct(rs):
+    n, d = 120, 2000
+    rp, ci, v, y = rsinputs.csr_zipf(n, d, 40, a=1.1, seed=5)
+    Xs = rsinputs.csr_to_scipy(rp, ci, v, n, d)
+    lam = 1.0
+    h = rs.rs_create_csr(n, d, rp, ci, v, y, lam)
+    try:
+        w, rep = rs.rs_solve(h, "subcount", 12, 1.0, 0.5, 1e-12, 200000, seed=1, subcount_k=4, d=d)
+    finally:
+        rs.rs_destroy(h)
+    X = Xs.toarray()
+    pr = OP.build(X, y, lam, "primal")
+    w_star = np.linalg.solve(pr["A"], pr["b"])
+    assert rep["converged"]
+    assert rel(w, w_star) <= 1e-6
+
+
+# ---------------------------------------------------------------------------------- full size
+def test_config2_full_size_sampled(rs):
+    """BASELINE.json c2 at full size (1e5 x 2000, tau=200), the launch configuration bench.py
+    times: the first 3 iterations equal the oracle's (same X bytes, host copy)."""
+    cfg = rsinputs.CONFIGS["c2"]
+    Xd, yd = rsinputs.dense_problem(cfg.n, cfg.d, seed=0, col_decay=True, noise=cfg.noise,
+                                    device="cuda")
+    h = rs.rs_create_dense(Xd, yd, cfg.lam, borrow=True)
+    try:
+        w, rep = rs.rs_solve(h, "subsample", cfg.tau, 1.0, cfg.beta, 0.0, 3, seed=0)
+        _, r = rs.rs_get_state(h)
+    finally:
+        rs.rs_destroy(h)
+    X, y = Xd.cpu().numpy(), yd.cpu().numpy()
+    del Xd, yd
+    ref = OV.solve(X, y, cfg.lam, "subsample", cfg.tau, 1.0, cfg.beta, 0.0, 3, seed=0)
+    assert rel(w, ref["w"]) <= 1e-10
+    assert rel(r, ref["r"]) <= 1e-10
