@@ -1,0 +1,338 @@
+#!/usr/bin/env python
+"""Benchmark of the momentum sketch-and-project hot path (BASELINE.json metric) on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config c2]
+                    [--mode implicit|explicit]
+
+One "step" = one iteration of Alg. 2: sketch draw, X S, A S, S^T A S + Cholesky,
+fused momentum update -- every row of SURVEY §8(a).  Workload at N=1: BASELINE.json configs[1]
+(c2: dense primal 1e5 x 2000, subsample tau=200, gamma=1, beta=0.5, lambda=1e-4 n, tol 1e-4),
+synthetic data generated on the device from a fixed seed.
+
+Prints ONE JSON line (rank 0).  `value` = iterations per second of the solve (device time, CUDA
+events on the solver stream, max over ranks), `e2e` = the same metric through the public API from
+pinned host buffers (H2D of X and y, setup, solve to tol, D2H of w inside the timed region),
+`time_to_tol_s` = device seconds to ||r||/||b|| <= 1e-4, `roofline` = the dominant kernel (A S
+contraction, FP64 DMMA) against the measured FP64 peak, `cpu_baseline` = the oracle on the host.
+"""
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "sketch-and-project iters/s & s to ‖r‖/‖b‖≤1e-4; AS-pass HBM GB/s vs peak"
+FP64_DMMA_PEAK = 37.1   # TFLOP/s, measured on this pool's B200 (profiles/r01_fp64_peak.txt)
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f)
+    except Exception:
+        return {}
+
+
+class ClockSampler:
+    """nvidia-smi clocks and throttle reasons sampled every 200 ms during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device = device
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        self.lines = []
+        if self.proc is not None:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                out, _ = self.proc.communicate(timeout=5)
+                self.lines = [ln for ln in out.splitlines() if ln.strip()]
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for ln in getattr(self, "lines", []):
+            p = [t.strip() for t in ln.split(",")]
+            if len(p) < 8:
+                continue
+            try:
+                sm.append(float(p[0]))
+                mx = float(p[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, p[4:8]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def _dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+# ------------------------------------------------------------------------------ reference arm
+def run_reference(args):
+    """The oracle (oracle/, plain NumPy/SciPy fp64) on the same workload, on the host cores."""
+    world, rank, _ = _dist_env()
+    if rank != 0:
+        return 0
+    import numpy as np
+    import torch
+    import rsinputs
+    from oracle import solver as OV
+    cfg = rsinputs.CONFIGS[args.config]
+    dev = "cuda" if torch.cuda.is_available() else "cpu"
+    X, y = rsinputs.dense_problem(cfg.n, cfg.d, seed=0, col_decay=cfg.col_decay, noise=cfg.noise,
+                                  device=dev)
+    X, y = X.cpu().numpy(), y.cpu().numpy()
+    op = OV.Operator(X, y, cfg.lam, explicit=(args.mode == "explicit"))
+    OV.solve_momentum(op, cfg.sketch, cfg.tau, cfg.gamma, cfg.beta, 0.0, args.warmup, seed=0)
+    t0 = time.perf_counter()
+    OV.solve_momentum(op, cfg.sketch, cfg.tau, cfg.gamma, cfg.beta, 0.0, args.steps, seed=0)
+    el = time.perf_counter() - t0
+    v = args.steps / el
+    cores = os.cpu_count()
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": "iters/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * el / args.steps, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": _config_dict(cfg, args, world),
+        "cpu_baseline": {"value": v, "unit": "iters/s", "cores": cores, "kind": "oracle",
+                         "sample": f"{args.steps} oracle Alg. 2 iterations of {args.config} "
+                                   f"(full X) after {args.warmup} warm-up iterations"},
+        "e2e": {"value": v, "unit": "iters/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def _config_dict(cfg, args, world):
+    return {"workload": f"{cfg.name}: {'dense' if cfg.kind == 'dense' else 'CSR'} primal "
+                        f"{cfg.n}x{cfg.d}, {cfg.sketch} tau={cfg.tau}, gamma={cfg.gamma}, "
+                        f"beta={cfg.beta}, lambda={cfg.lam:g}, tol={cfg.tol:g}",
+            "as_mode": args.mode, "tau": cfg.tau, "n": cfg.n, "d": cfg.d,
+            "parallelism": f"X rows sharded over {world} GPU(s), NCCL allreduce of A S",
+            "l2": "inputs larger than L2 (X = %.2f GB > 126 MB)" % (cfg.n * cfg.d * 8 / 1e9)}
+
+
+# ------------------------------------------------------------------------------ our arm
+def run_ours(args):
+    import numpy as np
+    import torch
+    import rsinputs
+    from paper_2105_05565_b200 import build
+    build()
+    from paper_2105_05565_b200 import ridgesketch as rs
+
+    world, rank, local = _dist_env()
+    torch.cuda.set_device(local)
+    dist = None
+    pg = None
+    if world > 1:
+        import torch.distributed as tdist
+        tdist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        pg = tdist
+        obj = [rs.rs_nccl_unique_id() if rank == 0 else None]
+        tdist.broadcast_object_list(obj, src=0)
+        uid = obj[0]
+    cfg = rsinputs.CONFIGS[args.config]
+    assert cfg.kind == "dense", "bench drives the dense configs (c1, c2, c5)"
+    stream = torch.cuda.current_stream()
+    Xd, yd = rsinputs.dense_problem(cfg.n, cfg.d, seed=0, col_decay=cfg.col_decay, noise=cfg.noise,
+                                    device="cuda")
+    b0, ln = rs.rs_shard_range(cfg.n, rank, world)
+    if world > 1:
+        Xd = Xd[b0:b0 + ln].contiguous()
+        yd = yd[b0:b0 + ln].contiguous()
+        dist = dict(device=local, rank=rank, world=world, nccl_unique_id=uid,
+                    cuda_stream=stream.cuda_stream, shard_begin=b0, shard_len=ln)
+    else:
+        dist = dict(device=local, rank=0, world=1, cuda_stream=stream.cuda_stream,
+                    shard_begin=0, shard_len=cfg.n)
+    torch.cuda.synchronize()
+    h = rs.rs_create_dense(Xd, yd, cfg.lam, mode=args.mode, n=cfg.n, d=cfg.d, borrow=True,
+                           dist=dist)
+    common = dict(kind=cfg.sketch, tau=cfg.tau, gamma=cfg.gamma, beta=cfg.beta, seed=0,
+                  subcount_k=cfg.subcount_k)
+
+    def barrier():
+        if pg is not None:
+            pg.barrier()
+        torch.cuda.synchronize()
+
+    # warm-up (W iterations, untimed)
+    rs.rs_solve(h, tol=0.0, max_iter=max(args.warmup, 1), check_every=max(args.warmup, 1), **common)
+    # timed: exactly K iterations of the whole hot path, one CUDA graph launch of K iterations
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier()
+    with ClockSampler(local) as clk:
+        e0.record(stream)
+        _, rep = rs.rs_solve(h, tol=0.0, max_iter=args.steps, check_every=min(args.steps, 1024),
+                             profile=True, **common)
+        e1.record(stream)
+        barrier()
+    el_ms = e0.elapsed_time(e1)
+    if pg is not None:
+        t = torch.tensor([el_ms], device="cuda", dtype=torch.float64)
+        pg.all_reduce(t, op=pg.ReduceOp.MAX)
+        el_ms = float(t.item())
+    assert rep["iterations"] == args.steps
+    value = args.steps / (el_ms / 1e3)
+
+    # time to tolerance (second half of the metric), device time
+    barrier()
+    e2, e3 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e2.record(stream)
+    _, rep_tol = rs.rs_solve(h, tol=cfg.tol, max_iter=args.max_iter_tol, check_every=32, **common)
+    e3.record(stream)
+    barrier()
+    tol_ms = e2.elapsed_time(e3)
+    if pg is not None:
+        t = torch.tensor([tol_ms], device="cuda", dtype=torch.float64)
+        pg.all_reduce(t, op=pg.ReduceOp.MAX)
+        tol_ms = float(t.item())
+    rs.rs_destroy(h)
+
+    # roofline of the dominant kernel: the A S contraction (2 n d tau flop per launch)
+    kms, kl = rep["kernel_ms"], rep["kernel_launches"]
+    dom = max(kms, key=lambda k: kms[k])
+    as_ms = kms["as"] / max(kl["as"], 1)
+    flops = 2.0 * cfg.n * cfg.d * cfg.tau / world
+    if args.mode == "implicit":
+        achieved = flops / (as_ms * 1e-3) / 1e12
+        roof = {"kernel": "a3 A S = X^T (X S) contraction (DMMA, split-K reduce, + lambda S)",
+                "bound": "tensor", "achieved": achieved, "peak": FP64_DMMA_PEAK, "unit": "TFLOP/s",
+                "frac": achieved / FP64_DMMA_PEAK, "traffic": args.traffic,
+                "peak_source": "measured FP64 DMMA peak, profiles/r01_fp64_peak.txt "
+                               "(MEASURED_PEAKS.json has no FP64 figure)",
+                "algorithmic_per_launch": f"{flops:.3e} flop (2 n d tau)",
+                "avg_launch_ms": as_ms, "share_of_step": kms["as"] / max(el_ms, 1e-9)}
+    else:
+        xs_ms = kms["xs"] / max(kl["xs"], 1)
+        byt = cfg.tau * cfg.d * 8 * 2.0
+        achieved = byt / (xs_ms * 1e-3) / 1e9
+        peak = _peaks().get("hbm_gbs", 6556.5)
+        roof = {"kernel": "a2 explicit rows of A (gather + write A S^T)", "bound": "hbm",
+                "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                "traffic": args.traffic, "avg_launch_ms": xs_ms}
+    roof["step_share_by_class"] = {k: kms[k] / max(el_ms, 1e-9) for k in kms}
+    roof["dominant_class"] = dom
+
+    # end to end through the public API from pinned host buffers (rank-local shard)
+    e2e = None
+    if not args.no_e2e:
+        Xh = Xd.cpu().pin_memory()
+        yh = yd.cpu().pin_memory()
+        barrier()
+        e4, e5 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e4.record(stream)
+        h2 = rs.rs_create_dense(Xh, yh, cfg.lam, mode=args.mode, n=cfg.n, d=cfg.d, dist=dist)
+        w, rep_e2e = rs.rs_solve(h2, tol=cfg.tol, max_iter=args.max_iter_tol, check_every=32,
+                                 **common)
+        e5.record(stream)
+        barrier()
+        rs.rs_destroy(h2)
+        e2e_ms = e4.elapsed_time(e5)
+        if pg is not None:
+            t = torch.tensor([e2e_ms], device="cuda", dtype=torch.float64)
+            pg.all_reduce(t, op=pg.ReduceOp.MAX)
+            e2e_ms = float(t.item())
+        e2e = {"value": rep_e2e["iterations"] / (e2e_ms / 1e3), "unit": "iters/s",
+               "h2d_bytes_per_step": int(Xh.numel() * 8 + yh.numel() * 8),
+               "d2h_bytes_per_step": int(w.size * 8),
+               "step": "one public-API solve: rs_create_dense(pinned host X, y) + rs_solve to "
+                       "tol + w to host",
+               "seconds": e2e_ms / 1e3, "iterations": rep_e2e["iterations"]}
+        del Xh, yh
+
+    # CPU baseline: the oracle on a bounded sample, rank 0, N = 1 only
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        from oracle import solver as OV
+        X = Xd.cpu().numpy()
+        y = yd.cpu().numpy()
+        op = OV.Operator(X, y, cfg.lam, explicit=(args.mode == "explicit"))
+        OV.solve_momentum(op, cfg.sketch, cfg.tau, cfg.gamma, cfg.beta, 0.0, 1, seed=0)
+        t0 = time.perf_counter()
+        n_it = 0
+        while time.perf_counter() - t0 < args.cpu_seconds:
+            n_it += 3
+            OV.solve_momentum(op, cfg.sketch, cfg.tau, cfg.gamma, cfg.beta, 0.0, 3, seed=0)
+        el = time.perf_counter() - t0
+        cpu = {"value": n_it / el, "unit": "iters/s", "cores": os.cpu_count(), "kind": "oracle",
+               "sample": f"{n_it} oracle Alg. 2 iterations of {cfg.name} (full X, NumPy/SciPy "
+                         f"fp64, BLAS on all host cores), {el:.1f} s"}
+        del X, y
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "iters/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": el_ms / args.steps,
+            "higher_is_better": True, "scaling": "strong" if world > 1 else "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, generated on device)",
+            "config": _config_dict(cfg, args, world),
+            "time_to_tol_s": tol_ms / 1e3, "iterations_to_tol": rep_tol["iterations"],
+            "converged": rep_tol["converged"], "rel_residual": rep_tol["rel_residual"],
+            "e2e": e2e, "gpu_launches": rep["gpu_launches"], "roofline": roof,
+            "cpu_baseline": cpu, "clocks": clk.summary(),
+            "kernel_ms_per_step": {k: kms[k] / args.steps for k in kms},
+        }
+        print(json.dumps(line), flush=True)
+    if pg is not None:
+        pg.barrier()
+        pg.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c2")
+    ap.add_argument("--mode", default="implicit", choices=["implicit", "explicit"])
+    ap.add_argument("--max-iter-tol", type=int, default=20000)
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--traffic", type=float, default=None,
+                    help="ncu dram bytes per launch of the dominant kernel (from profiles/)")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

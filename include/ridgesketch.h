@@ -139,6 +139,8 @@ typedef struct {
   int64_t trace_len;
   double kernel_ms[RS_K_NCLASSES];       /* profile = 1 only                                    */
   int64_t kernel_launches[RS_K_NCLASSES];
+  int64_t gpu_launches;      /* CUDA kernels launched by the iteration loop (graph nodes run,
+                                including no-op launches after the stop flag in the last chunk) */
 } rs_report;
 
 /* Run Alg. 2 from w^0 = 0.  w_out: d doubles (the ridge weights; dual: X^T alpha), host memory

@@ -324,7 +324,7 @@ rs_status Problem::csr_ensure_workspace(int kind, int tau, int ksum) {
 rs_status Problem::csr_enqueue_as(const rs_solve_opts* o, cudaEvent_t* ev) {
   (void)o;
   auto mark = [&](int cls, int edge) {
-    if (ev) cudaEventRecord(ev[2 * cls + edge], st);
+    if (ev) cudaEventRecordWithFlags(ev[2 * cls + edge], st, cudaEventRecordExternal);
   };
   const int tau = sk.tau;
   if (route == 1) {

@@ -296,6 +296,11 @@ cudaError_t launch_add_diag(double* A, long long lda, long long m, double lambda
   return cudaGetLastError();
 }
 
+cudaError_t gemm_init() {
+  return cudaFuncSetAttribute(k_tn_gemm<G_BM, G_BN, G_BK, G_WM, G_WN, G_ST>,
+                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G_SMEM);
+}
+
 GemmPlan plan_tn_gemm(long long M, long long N, long long K, int num_sms) {
   GemmPlan p{};
   p.bm = G_BM;
@@ -317,7 +322,7 @@ GemmPlan plan_tn_gemm(long long M, long long N, long long K, int num_sms) {
   long long kps = (K + best - 1) / best;
   kps = (kps + G_BK - 1) / G_BK * G_BK;
   p.k_per_split = kps;
-  p.work_elems = best > 1 ? (size_t)best * (size_t)M * (size_t)N : 0;
+  p.work_elems = best > 1 ? (size_t)best * (size_t)M * (size_t)((N + 1) / 2 * 2) : 0;
   return p;
 }
 
@@ -325,13 +330,6 @@ cudaError_t launch_tn_gemm(const double* Aop, long long lda, const double* Bop, 
                            long long M, long long N, long long K, double* C, long long ldc,
                            const GemmPlan& plan, double* work, const Ctrl* ctrl, cudaStream_t st) {
   auto kern = k_tn_gemm<G_BM, G_BN, G_BK, G_WM, G_WN, G_ST>;
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)G_SMEM);
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
   dim3 grid((unsigned)((M + G_BM - 1) / G_BM), (unsigned)((N + G_BN - 1) / G_BN),
             (unsigned)plan.splits);
   if (plan.splits == 1) {
@@ -339,13 +337,14 @@ cudaError_t launch_tn_gemm(const double* Aop, long long lda, const double* Bop, 
                                                  ldc, 0, ctrl);
     return cudaGetLastError();
   }
-  const long long stride = M * N;
+  const long long ldw = (N + 1) / 2 * 2;   // even: 16-byte double2 stores in the epilogue
+  const long long stride = M * ldw;
   kern<<<grid, G_WM * G_WN * 32, G_SMEM, st>>>(Aop, lda, Bop, ldb, M, N, K, plan.k_per_split, work,
-                                               N, stride, ctrl);
+                                               ldw, stride, ctrl);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   dim3 rg((unsigned)std::min<long long>((N + 255) / 256, 64), (unsigned)M);
-  k_splitk_reduce<<<rg, 256, 0, st>>>(work, plan.splits, stride, M, N, N, C, ldc, ctrl);
+  k_splitk_reduce<<<rg, 256, 0, st>>>(work, plan.splits, stride, M, N, ldw, C, ldc, ctrl);
   return cudaGetLastError();
 }
 

@@ -105,6 +105,8 @@ rs_status setup_common(Problem* p, const rs_dist* dist) {
   if (p->device < 0 || p->device >= ndev) return fail(RS_EINVAL, "dist->device out of range");
   RS_CUDA(cudaSetDevice(p->device));
   RS_CUDA(cudaDeviceGetAttribute(&p->num_sms, cudaDevAttrMultiProcessorCount, p->device));
+  RS_CUDA(sketch_init());
+  RS_CUDA(gemm_init());
   if (dist && dist->cuda_stream) {
     p->st = static_cast<cudaStream_t>(dist->cuda_stream);
     p->own_stream = false;
@@ -328,8 +330,13 @@ rs_status Problem::ensure_workspace(int kind, int tau, int ksum) {
   RS_TRY(dalloc(&sk.bucket, L));
   RS_TRY(dalloc(&sk.bptr, tau + 1));
   if (kind == SK_COUNT) RS_TRY(dalloc(&sk.cmap, m));
-  ld_as = round_up(m, 4);
-  RS_TRY(dalloc(&ASt, (size_t)tau * ld_as));
+  if (fmt == 1) {   // CSR: AS row-major m x tau
+    ld_as = round_up(tau, 4);
+    RS_TRY(dalloc(&ASt, (size_t)m * ld_as));
+  } else {          // dense: AS^T row-major tau x m
+    ld_as = round_up(m, 4);
+    RS_TRY(dalloc(&ASt, (size_t)tau * ld_as));
+  }
   if (fmt == 0 && mode == RS_AS_IMPLICIT) {
     ld_xs = round_up(tau, 4);
     RS_TRY(dalloc(&XS, (size_t)std::max<long long>(rows_loc, 1) * ld_xs));
@@ -351,7 +358,7 @@ rs_status Problem::ensure_workspace(int kind, int tau, int ksum) {
 // events bracketing each kernel class.
 rs_status Problem::enqueue_iteration(const rs_solve_opts* o, cudaEvent_t* ev) {
   auto mark = [&](int cls, int edge) {
-    if (ev) cudaEventRecord(ev[2 * cls + edge], st);
+    if (ev) cudaEventRecordWithFlags(ev[2 * cls + edge], st, cudaEventRecordExternal);
   };
   mark(RS_K_SKETCH, 0);
   RS_CUDA(launch_sketch(sk, o->seed, ctrl, -1, st));                       // a1
@@ -440,6 +447,29 @@ rs_status Problem::solve(const rs_solve_opts* o, double* w_out, rs_mem w_mem, do
   RS_CUDA(cudaStreamSynchronize(st));
   {
     cudaGraph_t g = nullptr;
+    // count the kernel nodes of one iteration (for rs_report.gpu_launches)
+    {
+      cudaGraph_t g1 = nullptr;
+      RS_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+      rs_status s1 = enqueue_iteration(o, nullptr);
+      cudaError_t ce1 = cudaStreamEndCapture(st, &g1);
+      if (s1 != RS_OK) {
+        if (g1) cudaGraphDestroy(g1);
+        return s1;
+      }
+      if (ce1 != cudaSuccess) return fail(RS_ECUDA, std::string("graph capture: ") + cudaGetErrorString(ce1));
+      size_t nn = 0;
+      cudaGraphGetNodes(g1, nullptr, &nn);
+      std::vector<cudaGraphNode_t> nodes(nn);
+      cudaGraphGetNodes(g1, nodes.data(), &nn);
+      kernels_per_iter = 0;
+      for (auto nd : nodes) {
+        cudaGraphNodeType t;
+        cudaGraphNodeGetType(nd, &t);
+        if (t == cudaGraphNodeTypeKernel) ++kernels_per_iter;
+      }
+      cudaGraphDestroy(g1);
+    }
     RS_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
     rs_status s = RS_OK;
     for (int i = 0; i < chunk && s == RS_OK; ++i)
@@ -460,9 +490,10 @@ rs_status Problem::solve(const rs_solve_opts* o, double* w_out, rs_mem w_mem, do
   RS_CUDA(cudaEventCreate(&t0));
   RS_CUDA(cudaEventCreate(&t1));
   RS_CUDA(cudaEventRecord(t0, st));
-  long long k_prev = 0;
+  long long k_prev = 0, graph_launches = 0;
   while (!ctrl_host->done) {
     RS_CUDA(cudaGraphLaunch(graph_exec, st));
+    ++graph_launches;
     RS_CUDA(cudaMemcpyAsync(ctrl_host, ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, st));
     RS_CUDA(cudaStreamSynchronize(st));
     if (o->profile) {
@@ -510,6 +541,7 @@ rs_status Problem::solve(const rs_solve_opts* o, double* w_out, rs_mem w_mem, do
     R.kernel_ms[cls] = kms[cls];
     R.kernel_launches[cls] = klaunch[cls];
   }
+  R.gpu_launches = graph_launches * chunk * kernels_per_iter;
   if (rep) *rep = R;
   if (o->trace && R.trace_len > 0)
     RS_CUDA(cudaMemcpy(o->trace, trace_dev, R.trace_len * 8, cudaMemcpyDeviceToHost));
@@ -605,6 +637,7 @@ rs_status rs_sketch_draw(rs_sketch_kind kind, int64_t m, int64_t tau, int64_t su
   int ndev = 0;
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) return fail(RS_ECUDA, "no CUDA device");
   RS_CUDA(cudaSetDevice(device));
+  RS_CUDA(rs::sketch_init());
   rs::DevSketch sk{};
   sk.kind = (int)kind;
   sk.m = (int)m;

@@ -63,6 +63,7 @@ struct Problem {
   double* partials = nullptr;
   cudaGraphExec_t graph_exec = nullptr;
   std::vector<cudaEvent_t> prof_events;
+  long long kernels_per_iter = 0;   // counted while capturing one iteration
 
   ~Problem();
   void free_workspace();

@@ -64,6 +64,10 @@ struct DevSketch {
 // Kernel launchers (each returns cudaGetLastError()).  All take the control block so that they can
 // no-op once the solve has stopped.
 
+// One-time per-process kernel setup (attributes, flags); must run outside any stream capture.
+cudaError_t sketch_init();
+cudaError_t gemm_init();
+
 // a1 sketch draw.  uses seed key and iteration k read from ctrl (or `fixed_k` >= 0 if given).
 cudaError_t launch_sketch(const DevSketch& sk, uint64_t seed, const Ctrl* ctrl, long long fixed_k,
                           cudaStream_t st);

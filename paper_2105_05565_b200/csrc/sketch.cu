@@ -237,37 +237,37 @@ size_t sketch_max_len(int kind, int m, int tau, int ksum) {
 
 static int* g_err_flag = nullptr;   // device int set if the select hits an unsupported tie storm
 
+// One-time, per-device setup (never inside a stream capture): kernel attributes, error flag.
+cudaError_t sketch_init() {
+  cudaError_t e = cudaFuncSetAttribute(k_sketch_count, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       32 * kMaxCountTau * (int)sizeof(unsigned));
+  if (e != cudaSuccess) return e;
+  e = cudaFuncSetAttribute(k_sketch_select, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           kKeyCache * 8 + kMaxSelect * 12);
+  if (e != cudaSuccess) return e;
+  if (!g_err_flag) {
+    e = cudaMalloc(&g_err_flag, sizeof(int));
+    if (e != cudaSuccess) return e;
+    e = cudaMemset(g_err_flag, 0, sizeof(int));
+  }
+  return e;
+}
+
 cudaError_t launch_sketch(const DevSketch& sk, uint64_t seed, const Ctrl* ctrl, long long fixed_k,
                           cudaStream_t st) {
   const uint2 key = make_uint2((unsigned)(seed & 0xffffffffull), (unsigned)(seed >> 32));
   if (sk.kind == SK_COUNT) {
     if (sk.tau > kMaxCountTau) return cudaErrorInvalidValue;
     const size_t smem = (size_t)32 * sk.tau * sizeof(unsigned);
-    static bool attr = false;
-    if (!attr) {
-      cudaFuncSetAttribute(k_sketch_count, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           32 * kMaxCountTau * (int)sizeof(unsigned));
-      attr = true;
-    }
     k_sketch_count<<<1, kThreads, smem, st>>>(sk, key, ctrl, fixed_k);
     return cudaGetLastError();
   }
   if (sk.len > kMaxSelect) return cudaErrorInvalidValue;
-  if (!g_err_flag) {
-    cudaError_t e = cudaMalloc(&g_err_flag, sizeof(int));
-    if (e != cudaSuccess) return e;
-    cudaMemset(g_err_flag, 0, sizeof(int));
-  }
+  if (!g_err_flag) return cudaErrorInitializationError;   // sketch_init() not called
   int Lp = 1;
   while (Lp < sk.len) Lp <<= 1;
   const int kc = sk.m <= kKeyCache ? sk.m : 0;
   const size_t smem = (size_t)kc * 8 + (size_t)Lp * 12;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_sketch_select, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         kKeyCache * 8 + kMaxSelect * 12);
-    attr = true;
-  }
   k_sketch_select<<<1, kThreads, smem, st>>>(sk, key, ctrl, fixed_k, g_err_flag);
   return cudaGetLastError();
 }

@@ -52,7 +52,7 @@ class rs_report(C.Structure):
     _fields_ = [("iterations", C.c_int64), ("converged", C.c_int), ("rel_residual", C.c_double),
                 ("setup_seconds", C.c_double), ("solve_seconds", C.c_double),
                 ("trace_len", C.c_int64), ("kernel_ms", C.c_double * 5),
-                ("kernel_launches", C.c_int64 * 5)]
+                ("kernel_launches", C.c_int64 * 5), ("gpu_launches", C.c_int64)]
 
 
 _P = C.c_void_p
@@ -224,7 +224,8 @@ def rs_solve(h, kind="subsample", tau=1, gamma=1.0, beta=0.0, tol=0.0, max_iter=
                   rel_residual=rep.rel_residual, setup_seconds=rep.setup_seconds,
                   solve_seconds=rep.solve_seconds,
                   kernel_ms={k: rep.kernel_ms[i] for i, k in enumerate(KERNEL_CLASSES)},
-                  kernel_launches={k: rep.kernel_launches[i] for i, k in enumerate(KERNEL_CLASSES)})
+                  kernel_launches={k: rep.kernel_launches[i] for i, k in enumerate(KERNEL_CLASSES)},
+                  gpu_launches=rep.gpu_launches)
     if trace_cap:
         report["trace"] = trace[:rep.trace_len].copy()
     if al is not None:
