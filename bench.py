@@ -224,7 +224,7 @@ def run_ours(args):
     # roofline of the dominant kernel: the A S contraction (2 n d tau flop per launch)
     kms, kl = rep["kernel_ms"], rep["kernel_launches"]
     dom = max(kms, key=lambda k: kms[k])
-    as_ms = kms["as"] / max(kl["as"], 1)
+    as_ms = max(kms["as"] / max(kl["as"], 1), 1e-9)
     flops = 2.0 * cfg.n * cfg.d * cfg.tau / world
     if args.mode == "implicit":
         achieved = flops / (as_ms * 1e-3) / 1e12
@@ -236,7 +236,7 @@ def run_ours(args):
                 "algorithmic_per_launch": f"{flops:.3e} flop (2 n d tau)",
                 "avg_launch_ms": as_ms, "share_of_step": kms["as"] / max(el_ms, 1e-9)}
     else:
-        xs_ms = kms["xs"] / max(kl["xs"], 1)
+        xs_ms = max(kms["xs"] / max(kl["xs"], 1), 1e-9)
         byt = cfg.tau * cfg.d * 8 * 2.0
         achieved = byt / (xs_ms * 1e-3) / 1e9
         peak = _peaks().get("hbm_gbs", 6556.5)
