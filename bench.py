@@ -235,6 +235,23 @@ def run_ours(args):
                                "(MEASURED_PEAKS.json has no FP64 figure)",
                 "algorithmic_per_launch": f"{flops:.3e} flop (2 n d tau)",
                 "avg_launch_ms": as_ms, "share_of_step": kms["as"] / max(el_ms, 1e-9)}
+    elif args.mode == "gram":
+        byt = cfg.n / world * cfg.d * 8.0
+        achieved = byt / (as_ms * 1e-3) / 1e9
+        peak = _peaks().get("hbm_gbs", 6556.5)
+        gram_ms = max(kms["gram"] / max(kl["gram"], 1), 1e-9)
+        gflops = 2.0 * cfg.n / world * cfg.tau * cfg.tau
+        roof = {"kernel": "AS pass u = X^T (X S delta): one streaming read of X per iteration",
+                "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": achieved / peak, "traffic": args.traffic,
+                "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy, burst)",
+                "algorithmic_per_launch": f"{byt:.3e} bytes (n d 8)", "avg_launch_ms": as_ms,
+                "share_of_step": kms["as"] / max(el_ms, 1e-9),
+                "gram_contraction": {"achieved": gflops / (gram_ms * 1e-3) / 1e12,
+                                     "peak": FP64_DMMA_PEAK, "unit": "TFLOP/s",
+                                     "frac": gflops / (gram_ms * 1e-3) / 1e12 / FP64_DMMA_PEAK,
+                                     "avg_launch_ms": gram_ms,
+                                     "algorithmic_per_launch": f"{gflops:.3e} flop (2 n tau^2)"}}
     else:
         xs_ms = max(kms["xs"] / max(kl["xs"], 1), 1e-9)
         byt = cfg.tau * cfg.d * 8 * 2.0
@@ -319,7 +336,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c2")
-    ap.add_argument("--mode", default="implicit", choices=["implicit", "explicit"])
+    ap.add_argument("--mode", default="implicit", choices=["implicit", "explicit", "gram"])
     ap.add_argument("--max-iter-tol", type=int, default=20000)
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-e2e", action="store_true")

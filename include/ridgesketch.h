@@ -63,7 +63,10 @@ typedef enum { RS_ROUTE_AUTO = 0, RS_ROUTE_PRIMAL = 1, RS_ROUTE_DUAL = 2 } rs_ro
  *   EXPLICIT: A = B + lambda I is built once in rs_create (dense SYRK-style product), and every
  *             iteration gathers / sums the sketched rows of A (A symmetric, so rows = columns).
  *             Dense X only (RS_EUNSUPPORTED for CSR).                                            */
-typedef enum { RS_AS_IMPLICIT = 0, RS_AS_EXPLICIT = 1 } rs_as_mode;
+/*   GRAM    : (dense primal only) A S is never formed: G = (XS)^T(XS) + lambda S^T S
+ *             and A S delta = X^T (X S delta) + lambda S delta (one streaming pass over X per
+ *             iteration).  Same iterates as IMPLICIT in exact arithmetic.          */
+typedef enum { RS_AS_IMPLICIT = 0, RS_AS_EXPLICIT = 1, RS_AS_GRAM = 2 } rs_as_mode;
 
 typedef enum {
   RS_SKETCH_SUBSAMPLE = 0,   /* S = I_C, |C| = tau, uniform over tau-subsets (Eq. subsample)   */
@@ -124,10 +127,12 @@ typedef struct {
 enum {
   RS_K_SKETCH = 0,   /* a1 sketch draw                                                  */
   RS_K_XS = 1,       /* a2 column gather / signed segmented sum (X S, X^T S, rows of A)  */
-  RS_K_AS = 2,       /* a3 contraction A S (+ split-K reduce, allreduce, + lambda S)     */
+  RS_K_AS = 2,       /* a3 contraction A S (+ split-K reduce, allreduce, + lambda S);
+                        GRAM mode: the X^T (X S delta) streaming pass                     */
   RS_K_SOLVE = 3,    /* a4 + a5 S^T A S, S^T r, Cholesky, triangular solves, S delta     */
   RS_K_UPDATE = 4,   /* a6 fused momentum update + ||r||^2 + stop flag                   */
-  RS_K_NCLASSES = 5
+  RS_K_GRAM = 5,     /* GRAM mode: G = (XS)^T XS contraction (+ allreduce)               */
+  RS_K_NCLASSES = 6
 };
 
 typedef struct {

@@ -87,6 +87,32 @@ __global__ void k_form_g_rm(const double* __restrict__ AS, long long ld_as,
   }
 }
 
+// Gram mode: Gx[a][b] = Gram[a][b] + lambda |bucket a| delta_ab (b <= a); row tau = g = S^T r.
+__global__ void k_form_g_gram(const double* __restrict__ Gram, long long ld_gram, double lambda,
+                              const double* __restrict__ r, DevSketch sk, double* __restrict__ Gx,
+                              long long ldg, const Ctrl* ctrl) {
+  if (ctrl->done) return;
+  const int a = blockIdx.x, tau = sk.tau;
+  if (a == tau) {
+    for (int q = threadIdx.x; q < tau; q += blockDim.x) {
+      double s = 0.0;
+      for (int e = sk.bptr[q]; e < sk.bptr[q + 1]; ++e) {
+        const double v = r[sk.coord[e]];
+        s += sk.sign[e] > 0 ? v : -v;
+      }
+      Gx[(long long)tau * ldg + q] = s;
+    }
+    return;
+  }
+  const int e0 = sk.bptr[a], e1 = sk.bptr[a + 1];
+  for (int b = threadIdx.x; b <= a; b += blockDim.x) {
+    double s = Gram[(long long)a * ld_gram + b];
+    if (a == b) s += lambda * (double)(e1 - e0);
+    if (e0 == e1 || sk.bptr[b] == sk.bptr[b + 1]) s = (a == b) ? 1.0 : 0.0;   // R3
+    Gx[(long long)a * ldg + b] = s;
+  }
+}
+
 // Records a failed pivot.  `done` is NOT set here (a late-starting CTA of this cooperative grid
 // must not see it and skip the grid barriers); the update kernel turns the status into `done`.
 __device__ __forceinline__ void flag_notspd(Ctrl* ctrl) { ctrl->status = ST_NOTSPD; }
@@ -242,7 +268,220 @@ k_chol(double* __restrict__ Gx, long long ldg, int tau, DevSketch sk, double* __
   }
 }
 
+// Single-CTA path for tau <= kSmallTau.  The bordered matrix (lower triangle of G plus the row
+// g^T) lives in shared memory as 8 x 8 blocks, block-packed by block row (block (I, J), J <= I, at
+// index I(I+1)/2 + J), each block row-major with an XOR swizzle (column c of row r stored at
+// c ^ 4((r >> 1) & 1)) so that DMMA fragment loads are bank-conflict free.  Blocked right-looking
+// Cholesky, block width 8:
+//   panel p  : warp 0 factors the whole block column (diagonal block + every block below it,
+//              including the border row = forward substitution), left-looking inside the panel;
+//   trailing : all warps update blocks (I, J), p < J <= I, with two mma.sync.m8n8k4.f64 each
+//              (C -= L_Ip L_Jp^T, SASS DMMA).
+// Two block barriers per block column; then warp 0 runs the blocked backward substitution.
+constexpr int kSmallTau = 224;
+constexpr int kSmallThreads = 1024;
+constexpr int NB8 = 8;
+
+__device__ __forceinline__ int blk(int I, int J) { return I * (I + 1) / 2 + J; }
+// shared index of element (row, col) of the bordered matrix (col <= row, block-lower)
+__device__ __forceinline__ int sidx(int row, int col) {
+  const int I = row >> 3, J = col >> 3, r = row & 7, c = col & 7;
+  return blk(I, J) * 64 + r * 8 + (c ^ (((r >> 1) & 1) << 2));
+}
+__device__ __forceinline__ void dmma8(double (&c)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c[0]), "+d"(c[1])
+               : "d"(a), "d"(b));
+}
+
+__global__ void __launch_bounds__(kSmallThreads, 1)
+k_chol_small(const double* __restrict__ ASt, long long ld_as, bool rowmajor,
+             const double* __restrict__ Gram, long long ld_gram, double lambda,
+             const double* __restrict__ r, DevSketch sk, double* __restrict__ delta,
+             double* __restrict__ sdelta, Ctrl* ctrl) {
+  if (ctrl->done) return;
+  extern __shared__ double sL[];
+  const int tau = sk.tau, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int rows = tau + 1;
+  const int Tc = (tau + NB8 - 1) / NB8, Tr = (rows + NB8 - 1) / NB8;
+  const int nblk = blk(Tr - 1, 0) + min(Tr, Tc);   // blocks of the last block row: J < min(Tr, Tc)
+  __shared__ double s_inv[kSmallTau];
+  __shared__ int s_bad;
+  // trailing-tile list of step 0: (I, J) for 1 <= J < Tc, J <= I < Tr, ordered by J then I;
+  // s_toff[J] = index of the first tile of column J
+  constexpr int kMaxT = (kSmallTau + 1 + NB8 - 1) / NB8 + 1;
+  __shared__ unsigned char s_tI[kMaxT * kMaxT / 2 + kMaxT], s_tJ[kMaxT * kMaxT / 2 + kMaxT];
+  __shared__ int s_toff[kMaxT + 1];
+  if (tid == 0) {
+    s_bad = 0;
+    int t = 0;
+    s_toff[0] = 0;
+    for (int J = 0; J < Tc; ++J) {
+      s_toff[J] = t;
+      if (J == 0) continue;
+      for (int I = J; I < Tr; ++I, ++t) {
+        s_tI[t] = (unsigned char)I;
+        s_tJ[t] = (unsigned char)J;
+      }
+    }
+    s_toff[Tc] = t;
+  }
+  // ---- a4: gather G (lower) and g into the blocked layout; padding entries = 0
+  for (int q = tid; q < nblk * 64; q += kSmallThreads) sL[q] = 0.0;
+  __syncthreads();
+  for (int a = warp; a <= tau; a += kSmallThreads / 32) {   // one warp per row of G (row tau = g)
+    if (a == tau) {
+      for (int c = lane; c < tau; c += 32) {
+        double v = 0.0;
+        for (int t = sk.bptr[c]; t < sk.bptr[c + 1]; ++t) {
+          const double x = r[sk.coord[t]];
+          v += sk.sign[t] > 0 ? x : -x;
+        }
+        sL[sidx(tau, c)] = v;
+      }
+      continue;
+    }
+    const int e0 = sk.bptr[a], e1 = sk.bptr[a + 1];
+    for (int c = lane; c <= a; c += 32) {
+      double v = 0.0;
+      if (Gram) {   // Gram mode: G = (XS)^T XS + lambda S^T S, S^T S = diag(|bucket|)
+        v = Gram[(long long)a * ld_gram + c];
+        if (a == c) v += lambda * (double)(e1 - e0);
+      } else {
+        for (int t = e0; t < e1; ++t) {
+          const long long co = sk.coord[t];
+          const double x = rowmajor ? ASt[co * ld_as + c] : ASt[(long long)c * ld_as + co];
+          v += sk.sign[t] > 0 ? x : -x;
+        }
+      }
+      if (e0 == e1 || sk.bptr[c] == sk.bptr[c + 1]) v = (a == c) ? 1.0 : 0.0;   // R3
+      sL[sidx(a, c)] = v;
+    }
+  }
+  __syncthreads();
+  for (int p = 0; p < Tc; ++p) {
+    const int c0 = p * NB8;
+    const int ncol = min(NB8, tau - c0);
+    // ---- diagonal block (warp 0, registers): lane r holds row c0 + r; left-looking, rsqrt pivots
+    if (warp == 0) {
+      const int rr = lane & 7;
+      const int grow = c0 + rr;
+      double v[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) v[k] = (k <= rr && grow < rows) ? sL[sidx(grow, c0 + k)] : 0.0;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        if (j < ncol) {
+          double sj = v[j];
+#pragma unroll
+          for (int k = 0; k < j; ++k) sj -= v[k] * __shfl_sync(0xffffffffu, v[k], j);
+          double d = __shfl_sync(0xffffffffu, sj, j);
+          if (!(d > 0.0) || !isfinite(d)) { if (lane == 0) s_bad = 1; d = 1.0; }
+          const double inv = rsqrt(d);
+          if (rr == j) v[j] = d * inv;
+          else if (rr > j) v[j] = sj * inv;
+          if (lane == j) s_inv[c0 + j] = inv;
+        }
+      }
+      if (lane < 8 && grow < rows) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+          if (k <= rr && k < ncol) sL[sidx(grow, c0 + k)] = v[k];
+      }
+    }
+    __syncthreads();
+    // ---- panel below the diagonal block (all threads, one row each): x L_pp^T = g
+    for (int row = c0 + NB8 + tid; row < rows; row += kSmallThreads) {
+      double x[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) x[k] = k < ncol ? sL[sidx(row, c0 + k)] : 0.0;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        if (j < ncol) {
+#pragma unroll
+          for (int k = 0; k < j; ++k) x[j] -= x[k] * sL[sidx(c0 + j, c0 + k)];
+          x[j] *= s_inv[c0 + j];
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < 8; ++k)
+        if (k < ncol) sL[sidx(row, c0 + k)] = x[k];
+    }
+    __syncthreads();
+    // ---- trailing update of blocks (I, J), p < J <= I < Tr, J < Tc: C -= L_Ip L_Jp^T
+    {
+      const int ar = lane >> 2, ak = lane & 3;
+      // tiles with J >= p + 1 are a suffix of the step-0 list (ordered by J, then I)
+      const int t_end = s_toff[Tc];
+      for (int t = s_toff[p + 1] + warp; t < t_end; t += kSmallThreads / 32) {
+        const int I = s_tI[t], J = s_tJ[t];
+        const double* Lip = sL + blk(I, p) * 64;
+        const double* Ljp = sL + blk(J, p) * 64;
+        double* Cb = sL + blk(I, J) * 64;
+        const int sw = ((ar >> 1) & 1) << 2;
+        const double a0 = -Lip[ar * 8 + (ak ^ sw)], a1 = -Lip[ar * 8 + ((ak + 4) ^ sw)];
+        const double b0 = Ljp[ar * 8 + (ak ^ sw)], b1 = Ljp[ar * 8 + ((ak + 4) ^ sw)];
+        const int cr = ar, cc = 2 * ak;
+        const int csw = ((cr >> 1) & 1) << 2;
+        double acc[2] = {Cb[cr * 8 + (cc ^ csw)], Cb[cr * 8 + ((cc + 1) ^ csw)]};
+        dmma8(acc, a0, b0);
+        dmma8(acc, a1, b1);
+        Cb[cr * 8 + (cc ^ csw)] = acc[0];
+        Cb[cr * 8 + ((cc + 1) ^ csw)] = acc[1];
+      }
+    }
+    __syncthreads();
+  }
+  if (s_bad) {
+    if (tid == 0) ctrl->status = ST_NOTSPD;
+    return;
+  }
+  // ---- backward substitution L^T delta = y; y = border row, overwritten by delta.  Per block
+  // column (from the last): warp 0 solves the 8 x 8 diagonal block in registers, then all threads
+  // update y_k -= sum_{q in block} L[q][k] delta_q for k < c0.
+  for (int p = Tc - 1; p >= 0; --p) {
+    const int c0 = p * NB8, ncol = min(NB8, tau - c0);
+    if (warp == 0) {
+      const int q = lane & 7;
+      double yq = q < ncol ? sL[sidx(tau, c0 + q)] : 0.0;
+#pragma unroll
+      for (int j = 7; j >= 0; --j) {
+        if (j < ncol) {
+          const double dj = __shfl_sync(0xffffffffu, yq, j) * s_inv[c0 + j];
+          if (q == j) yq = dj;
+          else if (q < j) yq -= sL[sidx(c0 + j, c0 + q)] * dj;
+        }
+      }
+      if (lane < ncol) sL[sidx(tau, c0 + lane)] = yq;
+    }
+    __syncthreads();
+    for (int k = tid; k < c0; k += kSmallThreads) {
+      double s = 0.0;
+#pragma unroll
+      for (int q = 0; q < 8; ++q)
+        if (q < ncol) s += sL[sidx(c0 + q, k)] * sL[sidx(tau, c0 + q)];
+      sL[sidx(tau, k)] -= s;
+    }
+    __syncthreads();
+  }
+  for (int b = tid; b < tau; b += kSmallThreads) delta[b] = sL[sidx(tau, b)];
+  for (int e = tid; e < sk.len; e += kSmallThreads) {
+    const double dv = sL[sidx(tau, sk.bucket[e])];
+    sdelta[sk.coord[e]] = sk.sign[e] > 0 ? dv : -dv;
+  }
+}
+
+size_t small_smem(int tau) {
+  const int Tr = (tau + 1 + NB8 - 1) / NB8;
+  return (size_t)(Tr * (Tr + 1) / 2) * 64 * sizeof(double);
+}
+
 }  // namespace
+
+cudaError_t chol_init() {
+  return cudaFuncSetAttribute(k_chol_small, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)small_smem(kSmallTau));
+}
 
 size_t solve_gx_elems(int tau) {
   const long long ldg = ((long long)tau + NB - 1) / NB * NB;
@@ -261,9 +500,18 @@ SolveWork plan_solve(int tau, int num_sms) {
 }
 
 cudaError_t launch_sketched_solve(const double* ASt, long long ld_as, bool as_rowmajor,
+                                  const double* Gram, long long ld_gram, double lambda,
                                   const double* r, const DevSketch& sk, SolveWork& sw,
                                   double* sdelta, Ctrl* ctrl, cudaStream_t st) {
-  if (as_rowmajor)
+  if (sk.tau <= kSmallTau) {
+    k_chol_small<<<1, kSmallThreads, small_smem(sk.tau), st>>>(ASt, ld_as, as_rowmajor, Gram,
+                                                                ld_gram, lambda, r, sk, sw.delta,
+                                                                sdelta, ctrl);
+    return cudaGetLastError();
+  }
+  if (Gram)
+    k_form_g_gram<<<sk.tau + 1, 256, 0, st>>>(Gram, ld_gram, lambda, r, sk, sw.Gx, sw.ldg, ctrl);
+  else if (as_rowmajor)
     k_form_g_rm<<<sk.tau + 1, 256, 0, st>>>(ASt, ld_as, r, sk, sw.Gx, sw.ldg, ctrl);
   else
     k_form_g<<<sk.tau + 1, 256, 0, st>>>(ASt, ld_as, r, sk, sw.Gx, sw.ldg, ctrl);

@@ -88,16 +88,19 @@ __device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
 }
 
 // C'[M x N] (+)= sum_k A[k, m] * B[k, n]  over this CTA's K range.
-//   A: row-major K x M (lda), B: row-major K x N (ldb).  Tile BM x BN x BK, WM x WN warps.
-template <int BM, int BN, int BK, int WM, int WN, int STAGES>
-__global__ void __launch_bounds__(WM * WN * 32)
+//   A: row-major K x M (lda), B: row-major K x N (ldb).  CTA tile BM x BN x BK with WM x WN warps,
+//   each warp TM x TN DMMA 8x8 tiles (BM = 8 TM WM, BN = 8 TN WN).
+template <int TM, int TN, int WM, int WN, int STAGES, int MINB>
+__global__ void __launch_bounds__(WM * WN * 32, MINB)
 k_tn_gemm(const double* __restrict__ A, long long lda, const double* __restrict__ B, long long ldb,
           long long M, long long N, long long K, long long k_per_split, double* __restrict__ C,
           long long ldc, long long split_stride, const Ctrl* ctrl) {
   if (ctrl && ctrl->done) return;
+  constexpr int BM = 8 * TM * WM, BN = 8 * TN * WN, BK = 16;
   constexpr int NT = WM * WN * 32;
-  constexpr int LDA_S = BM + 4, LDB_S = BN + 4;   // +4 doubles: conflict-free fragment loads
-  constexpr int TM = BM / WM / 8, TN = BN / WN / 8;
+  // +4 doubles: BM + 4 = 4 or 12 mod 16, so the 16 lanes of a half-warp fragment load hit
+  // distinct 8-byte bank pairs; rows stay 16-byte aligned for cp.async
+  constexpr int LDA_S = BM + 4, LDB_S = BN + 4;
   extern __shared__ __align__(16) double smem[];
   double* As = smem;                               // [STAGES][BK][LDA_S]
   double* Bs = smem + STAGES * BK * LDA_S;         // [STAGES][BK][LDB_S]
@@ -200,8 +203,32 @@ __global__ void k_splitk_reduce(const double* __restrict__ work, int splits, lon
   }
 }
 
-constexpr int G_BM = 64, G_BN = 128, G_BK = 16, G_WM = 2, G_WN = 4, G_ST = 4;
-constexpr size_t G_SMEM = (size_t)G_ST * G_BK * ((G_BM + 4) + (G_BN + 4)) * sizeof(double);
+// Tile variants: the plan picks the one whose padded work / wave quantisation is smallest.
+struct Variant {
+  int tm, tn, wm, wn, stages;
+  int bm() const { return 8 * tm * wm; }
+  int bn() const { return 8 * tn * wn; }
+  int threads() const { return 32 * wm * wn; }
+  size_t smem() const { return (size_t)stages * 16 * ((bm() + 4) + (bn() + 4)) * sizeof(double); }
+};
+constexpr int kNumVariants = 3;
+const Variant kVariants[kNumVariants] = {
+    {4, 4, 2, 4, 4},   //  64 x 128, 8 warps
+    {5, 4, 5, 2, 4},   // 200 x  64, 10 warps (tau = 200: no M padding)
+    {4, 4, 4, 2, 4},   // 128 x  64, 8 warps
+};
+#define RS_GEMM_KERNELS(X)              \
+  X(0, k_tn_gemm<4, 4, 2, 4, 4, 2>)     \
+  X(1, k_tn_gemm<5, 4, 5, 2, 4, 1>)     \
+  X(2, k_tn_gemm<4, 4, 4, 2, 4, 1>)
+int g_ctas_per_sm[kNumVariants] = {1, 1, 1};
+
+const void* variant_fn(int v) {
+#define RS_CASE(i, ...) if (v == i) return (const void*)__VA_ARGS__;
+  RS_GEMM_KERNELS(RS_CASE)
+#undef RS_CASE
+  return nullptr;
+}
 
 // ------------------------------------------------------------------------------ misc
 __global__ void k_fill(double* p, long long n, double v) {
@@ -297,52 +324,74 @@ cudaError_t launch_add_diag(double* A, long long lda, long long m, double lambda
 }
 
 cudaError_t gemm_init() {
-  return cudaFuncSetAttribute(k_tn_gemm<G_BM, G_BN, G_BK, G_WM, G_WN, G_ST>,
-                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G_SMEM);
+  for (int v = 0; v < kNumVariants; ++v) {
+    const void* f = variant_fn(v);
+    cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)kVariants[v].smem());
+    if (e != cudaSuccess) return e;
+    int nb = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, f, kVariants[v].threads(),
+                                                      kVariants[v].smem());
+    if (e != cudaSuccess) return e;
+    g_ctas_per_sm[v] = nb > 0 ? nb : 1;
+  }
+  return cudaSuccess;
 }
 
+// Cost model: time ~ waves x (per-CTA tile work), waves = ceil(CTAs / resident slots); the
+// padded tile work counts the DMMA spent on ragged M / N edges; split-K adds a partial write.
 GemmPlan plan_tn_gemm(long long M, long long N, long long K, int num_sms) {
-  GemmPlan p{};
-  p.bm = G_BM;
-  p.bn = G_BN;
-  const long long tiles = ((M + G_BM - 1) / G_BM) * ((N + G_BN - 1) / G_BN);
-  const long long slots = 2LL * num_sms;   // 2 CTAs / SM resident (smem-limited)
-  // choose splits maximising wave efficiency, with >= 512 K rows per split
-  int best = 1;
-  double best_eff = -1.0;
-  for (int s = 1; s <= 32; ++s) {
-    if (s > 1 && K / s < 512) break;
-    const long long ctas = tiles * s;
-    const long long waves = (ctas + slots - 1) / slots;
-    const double eff = (double)ctas / (double)(waves * slots);
-    // prefer fewer splits unless efficiency improves by > 5%
-    if (eff > best_eff + 0.05) { best_eff = eff; best = s; }
+  GemmPlan best{};
+  double best_cost = 1e300;
+  for (int v = 0; v < kNumVariants; ++v) {
+    const Variant& V = kVariants[v];
+    const long long tm = (M + V.bm() - 1) / V.bm(), tn = (N + V.bn() - 1) / V.bn();
+    const long long tiles = tm * tn;
+    const long long slots = (long long)g_ctas_per_sm[v] * num_sms;
+    for (int s = 1; s <= 32; ++s) {
+      if (s > 1 && K / s < 256) break;
+      const long long ctas = tiles * s;
+      const long long waves = (ctas + slots - 1) / slots;
+      // per-SM work of one wave: g_ctas_per_sm CTAs of (bm x bn x K/s)
+      const double wave_work = (double)g_ctas_per_sm[v] * V.bm() * V.bn() * ((double)K / s);
+      double cost = waves * wave_work;
+      if (s > 1) cost += (double)s * M * N * 40.0 / num_sms;   // partial write + reduce
+      if (cost < best_cost * 0.98) {
+        best_cost = cost;
+        best.variant = v;
+        best.bm = V.bm();
+        best.bn = V.bn();
+        best.splits = s;
+      }
+    }
   }
-  p.splits = best;
-  long long kps = (K + best - 1) / best;
-  kps = (kps + G_BK - 1) / G_BK * G_BK;
-  p.k_per_split = kps;
-  p.work_elems = best > 1 ? (size_t)best * (size_t)M * (size_t)((N + 1) / 2 * 2) : 0;
-  return p;
+  long long kps = (K + best.splits - 1) / best.splits;
+  kps = (kps + 15) / 16 * 16;
+  best.k_per_split = kps;
+  best.work_elems = best.splits > 1 ? (size_t)best.splits * (size_t)M * (size_t)((N + 1) / 2 * 2) : 0;
+  return best;
 }
 
 cudaError_t launch_tn_gemm(const double* Aop, long long lda, const double* Bop, long long ldb,
                            long long M, long long N, long long K, double* C, long long ldc,
                            const GemmPlan& plan, double* work, const Ctrl* ctrl, cudaStream_t st) {
-  auto kern = k_tn_gemm<G_BM, G_BN, G_BK, G_WM, G_WN, G_ST>;
-  dim3 grid((unsigned)((M + G_BM - 1) / G_BM), (unsigned)((N + G_BN - 1) / G_BN),
+  const Variant& V = kVariants[plan.variant];
+  dim3 grid((unsigned)((M + V.bm() - 1) / V.bm()), (unsigned)((N + V.bn() - 1) / V.bn()),
             (unsigned)plan.splits);
-  if (plan.splits == 1) {
-    kern<<<grid, G_WM * G_WN * 32, G_SMEM, st>>>(Aop, lda, Bop, ldb, M, N, K, plan.k_per_split, C,
-                                                 ldc, 0, ctrl);
-    return cudaGetLastError();
-  }
+  const bool direct = plan.splits == 1;
   const long long ldw = (N + 1) / 2 * 2;   // even: 16-byte double2 stores in the epilogue
   const long long stride = M * ldw;
-  kern<<<grid, G_WM * G_WN * 32, G_SMEM, st>>>(Aop, lda, Bop, ldb, M, N, K, plan.k_per_split, work,
-                                               ldw, stride, ctrl);
+  double* out = direct ? C : work;
+  const long long ldo = direct ? ldc : ldw;
+  const long long so = direct ? 0 : stride;
+#define RS_LAUNCH(i, ...)                                                                   \
+  if (plan.variant == i)                                                                    \
+    __VA_ARGS__<<<grid, V.threads(), V.smem(), st>>>(Aop, lda, Bop, ldb, M, N, K,             \
+                                                     plan.k_per_split, out, ldo, so, ctrl);
+  RS_GEMM_KERNELS(RS_LAUNCH)
+#undef RS_LAUNCH
   cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess) return e;
+  if (e != cudaSuccess || direct) return e;
   dim3 rg((unsigned)std::min<long long>((N + 255) / 256, 64), (unsigned)M);
   k_splitk_reduce<<<rg, 256, 0, st>>>(work, plan.splits, stride, M, N, ldw, C, ldc, ctrl);
   return cudaGetLastError();

@@ -5,6 +5,8 @@
 
 #include <algorithm>
 #include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cmath>
 #include <cstring>
 #include <string>
@@ -65,6 +67,12 @@ void Problem::free_workspace() {
   sk = DevSketch{};
   dfree(XS);
   XS = nullptr;
+  dfree(Gram);
+  Gram = nullptr;
+  dfree(xp_part);
+  xp_part = nullptr;
+  dfree(uvec);
+  uvec = nullptr;
   dfree(ASt);
   ASt = nullptr;
   dfree(gemm_work);
@@ -107,6 +115,8 @@ rs_status setup_common(Problem* p, const rs_dist* dist) {
   RS_CUDA(cudaDeviceGetAttribute(&p->num_sms, cudaDevAttrMultiProcessorCount, p->device));
   RS_CUDA(sketch_init());
   RS_CUDA(gemm_init());
+  RS_CUDA(chol_init());
+  RS_CUDA(tma_gemm_init());
   if (dist && dist->cuda_stream) {
     p->st = static_cast<cudaStream_t>(dist->cuda_stream);
     p->own_stream = false;
@@ -175,9 +185,11 @@ static rs_status create_dense(rs_problem* out, int64_t n, int64_t d, const doubl
     return fail(RS_EINVAL, "bad rs_mem");
   if (route != RS_ROUTE_AUTO && route != RS_ROUTE_PRIMAL && route != RS_ROUTE_DUAL)
     return fail(RS_EINVAL, "bad route");
-  if (mode != RS_AS_IMPLICIT && mode != RS_AS_EXPLICIT) return fail(RS_EINVAL, "bad as_mode");
+  if (mode != RS_AS_IMPLICIT && mode != RS_AS_EXPLICIT && mode != RS_AS_GRAM)
+    return fail(RS_EINVAL, "bad as_mode");
   const int rt = route == RS_ROUTE_AUTO ? (d <= n ? 1 : 2) : (route == RS_ROUTE_PRIMAL ? 1 : 2);
   if (rt == 2) return fail(RS_EUNSUPPORTED, "dense dual route not implemented yet (use CSR or primal)");
+  if (mode == RS_AS_GRAM && d > 4096) return fail(RS_EUNSUPPORTED, "GRAM mode needs d <= 4096");
   RS_TRY(validate_dist(dist, rt == 1 ? n : d));
   const long long rows = dist ? dist->shard_len : n;
 
@@ -333,6 +345,21 @@ rs_status Problem::ensure_workspace(int kind, int tau, int ksum) {
   if (fmt == 1) {   // CSR: AS row-major m x tau
     ld_as = round_up(tau, 4);
     RS_TRY(dalloc(&ASt, (size_t)m * ld_as));
+  } else if (mode == RS_AS_GRAM) {   // no A S at all: XS, G, u
+    ld_as = round_up(m, 4);
+    ld_xs = round_up(tau, 4);
+    RS_TRY(dalloc(&XS, (size_t)std::max<long long>(rows_loc, 1) * ld_xs));
+    ld_gram = round_up(tau, 4);
+    RS_TRY(dalloc(&Gram, (size_t)tau * ld_gram));
+    RS_TRY(dalloc(&xp_part, xpass_partials(m, num_sms)));
+    RS_TRY(dalloc(&uvec, m));
+    if (rows_loc > 0) {
+      RS_CUDA(tma_gemm_plan(&tg_gram, XS, ld_xs, XS, ld_xs, tau, tau, rows_loc, num_sms));
+      if (tg_gram.work_elems) RS_TRY(dalloc(&gemm_work, tg_gram.work_elems));
+      if (std::getenv("RS_VERBOSE"))
+        fprintf(stderr, "[rs] gram gemm M=N=%d K=%lld: variant %d (%dx%d), splits %d\n", tau,
+                rows_loc, tg_gram.variant, tg_gram.bm, tg_gram.bn, tg_gram.splits);
+    }
   } else {          // dense: AS^T row-major tau x m
     ld_as = round_up(m, 4);
     RS_TRY(dalloc(&ASt, (size_t)tau * ld_as));
@@ -340,8 +367,18 @@ rs_status Problem::ensure_workspace(int kind, int tau, int ksum) {
   if (fmt == 0 && mode == RS_AS_IMPLICIT) {
     ld_xs = round_up(tau, 4);
     RS_TRY(dalloc(&XS, (size_t)std::max<long long>(rows_loc, 1) * ld_xs));
-    gp = plan_tn_gemm(tau, m, rows_loc, num_sms);
-    if (gp.work_elems) RS_TRY(dalloc(&gemm_work, gp.work_elems));
+    use_tma = !std::getenv("RS_NO_TMA") && rows_loc > 0;
+    if (use_tma) {
+      RS_CUDA(tma_gemm_plan(&tg, XS, ld_xs, X, ldx, tau, m, rows_loc, num_sms));
+      if (tg.work_elems) RS_TRY(dalloc(&gemm_work, tg.work_elems));
+    } else {
+      gp = plan_tn_gemm(tau, m, rows_loc, num_sms);
+      if (gp.work_elems) RS_TRY(dalloc(&gemm_work, gp.work_elems));
+    }
+    if (std::getenv("RS_VERBOSE"))
+      fprintf(stderr, "[rs] gemm M=%d N=%lld K=%lld: %s variant %d (%dx%d), splits %d\n", tau, m,
+              rows_loc, use_tma ? "TMA" : "cp.async", use_tma ? tg.variant : gp.variant,
+              use_tma ? tg.bm : gp.bm, use_tma ? tg.bn : gp.bn, use_tma ? tg.splits : gp.splits);
   }
   if (fmt == 1) RS_TRY(csr_ensure_workspace(kind, tau, ksum));
   sw = plan_solve(tau, num_sms);
@@ -363,13 +400,44 @@ rs_status Problem::enqueue_iteration(const rs_solve_opts* o, cudaEvent_t* ev) {
   mark(RS_K_SKETCH, 0);
   RS_CUDA(launch_sketch(sk, o->seed, ctrl, -1, st));                       // a1
   mark(RS_K_SKETCH, 1);
+  if (fmt == 0 && mode == RS_AS_GRAM) {
+    mark(RS_K_XS, 0);
+    RS_CUDA(launch_dense_xs(X, ldx, rows_loc, sk, XS, ld_xs, ctrl, st));    // a2  XS
+    mark(RS_K_XS, 1);
+    mark(RS_K_GRAM, 0);
+    if (rows_loc > 0)
+      RS_CUDA(tma_gemm_launch(tg_gram, Gram, ld_gram, gemm_work, ctrl, st));   // (XS)^T XS
+    else
+      RS_CUDA(launch_fill(Gram, (long long)sk.tau * ld_gram, 0.0, st));
+    RS_TRY(allreduce(Gram, (size_t)sk.tau * ld_gram));
+    mark(RS_K_GRAM, 1);
+    mark(RS_K_SOLVE, 0);
+    RS_CUDA(launch_sketched_solve(nullptr, 0, false, Gram, ld_gram, lambda, r, sk, sw, sdelta,
+                                  ctrl, st));                                // a4 + a5
+    mark(RS_K_SOLVE, 1);
+    mark(RS_K_AS, 0);
+    if (rows_loc > 0)
+      RS_CUDA(launch_xpass(X, ldx, rows_loc, m, sdelta, xp_part, uvec, num_sms, ctrl, st));
+    else
+      RS_CUDA(launch_fill(uvec, m, 0.0, st));
+    RS_TRY(allreduce(uvec, (size_t)m));                                     // X^T X S delta
+    mark(RS_K_AS, 1);
+    mark(RS_K_UPDATE, 0);
+    RS_CUDA(launch_update_vec(uvec, lambda, sdelta, w, dw, r, dr, m, o->gamma, o->beta, partials,
+                              ctrl, st));                                    // a6 + a7
+    mark(RS_K_UPDATE, 1);
+    return RS_OK;
+  }
   if (fmt == 0 && mode == RS_AS_IMPLICIT) {
     mark(RS_K_XS, 0);
     RS_CUDA(launch_dense_xs(X, ldx, rows_loc, sk, XS, ld_xs, ctrl, st));    // a2  XS
     mark(RS_K_XS, 1);
     mark(RS_K_AS, 0);
-    RS_CUDA(launch_tn_gemm(XS, ld_xs, X, ldx, sk.tau, m, rows_loc, ASt, ld_as, gp, gemm_work,
-                           ctrl, st));                                       // a3  (X^T XS)^T
+    if (use_tma)                                                             // a3  (X^T XS)^T
+      RS_CUDA(tma_gemm_launch(tg, ASt, ld_as, gemm_work, ctrl, st));
+    else
+      RS_CUDA(launch_tn_gemm(XS, ld_xs, X, ldx, sk.tau, m, rows_loc, ASt, ld_as, gp, gemm_work,
+                             ctrl, st));
     RS_TRY(allreduce(ASt, (size_t)sk.tau * ld_as));                         // sum over row shards
     RS_CUDA(launch_add_lambda_s(lambda, sk, ASt, ld_as, false, ctrl, st));         // + lambda S
     mark(RS_K_AS, 1);
@@ -381,7 +449,7 @@ rs_status Problem::enqueue_iteration(const rs_solve_opts* o, cudaEvent_t* ev) {
     RS_TRY(csr_enqueue_as(o, ev));
   }
   mark(RS_K_SOLVE, 0);
-  RS_CUDA(launch_sketched_solve(ASt, ld_as, fmt == 1, r, sk, sw, sdelta, ctrl, st));  // a4 + a5
+  RS_CUDA(launch_sketched_solve(ASt, ld_as, fmt == 1, nullptr, 0, 0.0, r, sk, sw, sdelta, ctrl, st));
   mark(RS_K_SOLVE, 1);
   mark(RS_K_UPDATE, 0);
   RS_CUDA(launch_update(ASt, ld_as, fmt == 1, sk.tau, sw.delta, sdelta, w, dw, r, dr, m, o->gamma, o->beta,

@@ -59,6 +59,14 @@ struct Problem {
   long long ld_as = 0;
   double* gemm_work = nullptr;
   GemmPlan gp{};
+  TmaGemm tg{};
+  // GRAM mode (NEXT-2)
+  TmaGemm tg_gram{};
+  double* Gram = nullptr;
+  long long ld_gram = 0;
+  double* xp_part = nullptr;
+  double* uvec = nullptr;
+  bool use_tma = true;
   SolveWork sw{};
   double* partials = nullptr;
   cudaGraphExec_t graph_exec = nullptr;

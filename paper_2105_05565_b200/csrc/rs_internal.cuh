@@ -67,6 +67,7 @@ struct DevSketch {
 // One-time per-process kernel setup (attributes, flags); must run outside any stream capture.
 cudaError_t sketch_init();
 cudaError_t gemm_init();
+cudaError_t chol_init();
 
 // a1 sketch draw.  uses seed key and iteration k read from ctrl (or `fixed_k` >= 0 if given).
 cudaError_t launch_sketch(const DevSketch& sk, uint64_t seed, const Ctrl* ctrl, long long fixed_k,
@@ -86,7 +87,7 @@ cudaError_t launch_explicit_rows(const double* A, long long lda, long long m, co
 // split over `splits` K-ranges into `work` and reduced deterministically.  If work == nullptr,
 // splits must be 1.
 struct GemmPlan {
-  int bm, bn, splits;
+  int variant, bm, bn, splits;
   long long k_per_split;
   size_t work_elems;
 };
@@ -94,6 +95,21 @@ GemmPlan plan_tn_gemm(long long M, long long N, long long K, int num_sms);
 cudaError_t launch_tn_gemm(const double* Aop, long long lda, const double* Bop, long long ldb,
                            long long M, long long N, long long K, double* C, long long ldc,
                            const GemmPlan& plan, double* work, const Ctrl* ctrl, cudaStream_t st);
+
+// Same contraction, TMA + mbarrier warp-specialised pipeline (gemm_tma.cu).  tmA / tmB hold two
+// CUtensorMap descriptors (64-byte aligned opaque blobs) encoded by tma_gemm_plan.
+struct TmaGemm {
+  alignas(64) unsigned char tmA[128];
+  alignas(64) unsigned char tmB[128];
+  int variant = 0, splits = 1, bm = 0, bn = 0;
+  long long M = 0, N = 0, K = 0, k_per_split = 0, ldw = 0;
+  size_t work_elems = 0;
+};
+cudaError_t tma_gemm_init();
+cudaError_t tma_gemm_plan(TmaGemm* g, const double* Aop, long long lda, const double* Bop,
+                          long long ldb, long long M, long long N, long long K, int num_sms);
+cudaError_t tma_gemm_launch(const TmaGemm& g, double* C, long long ldc, double* work,
+                            const Ctrl* ctrl, cudaStream_t st);
 
 // lambda S:  AS^T[b_e, coord_e] += lambda * sign_e  (as_rowmajor: AS[coord_e, b_e]).
 cudaError_t launch_add_lambda_s(double lambda, const DevSketch& sk, double* ASt, long long ld_as,
@@ -112,7 +128,9 @@ struct SolveWork {
 SolveWork plan_solve(int tau, int num_sms);
 size_t solve_gx_elems(int tau);
 // AS layout: as_rowmajor = false -> AS^T stored tau x m (ld_as); true -> AS stored m x tau (ld_as).
+// Gram mode (Gram != nullptr): G = Gram (tau x tau, ld_gram, lower read) + lambda diag(|bucket|).
 cudaError_t launch_sketched_solve(const double* ASt, long long ld_as, bool as_rowmajor,
+                                  const double* Gram, long long ld_gram, double lambda,
                                   const double* r, const DevSketch& sk, SolveWork& sw,
                                   double* sdelta, Ctrl* ctrl, cudaStream_t st);
 
@@ -123,6 +141,16 @@ cudaError_t launch_update(const double* ASt, long long ld_as, bool as_rowmajor, 
                           const double* delta, double* sdelta, double* w, double* dw, double* r,
                           double* dr, long long m, double gamma, double beta, double* partials,
                           Ctrl* ctrl, cudaStream_t st);
+
+// Gram mode (gram.cu): u = X^T (X v) in one pass over X (d <= 4096), partials reduced in order.
+size_t xpass_partials(long long d, int num_sms);
+cudaError_t launch_xpass(const double* X, long long ldx, long long rows, long long d,
+                         const double* v, double* partials, double* u, int num_sms,
+                         const Ctrl* ctrl, cudaStream_t st);
+// update with a dense u = X^T X S delta:  u_j + lambda sdelta_j  is A S delta
+cudaError_t launch_update_vec(const double* u, double lambda, double* sdelta, double* w, double* dw,
+                              double* r, double* dr, long long m, double gamma, double beta,
+                              double* partials, Ctrl* ctrl, cudaStream_t st);
 
 // misc
 // *out += number of non-finite entries of the rows x cols block.

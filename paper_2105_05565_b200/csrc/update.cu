@@ -171,7 +171,67 @@ k_update_rm(const double* __restrict__ AS, long long ld_as, int tau,
   }
 }
 
+// Gram mode: u given as a dense vector (X^T X S delta); A S delta = u + lambda S delta.
+constexpr int VT = 256;
+__global__ void __launch_bounds__(VT)
+k_update_vec(const double* __restrict__ u, double lambda, double* __restrict__ sdelta,
+             double* __restrict__ w, double* __restrict__ dw, double* __restrict__ r,
+             double* __restrict__ dr, long long m, double gamma, double beta,
+             double* __restrict__ partials, Ctrl* ctrl) {
+  if (ctrl->done) return;
+  if (ctrl->status >= ST_NOTSPD) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) ctrl->done = 1;
+    return;
+  }
+  __shared__ double red[VT / 32];
+  __shared__ bool s_last;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const long long j = (long long)blockIdx.x * VT + tid;
+  double r2 = 0.0;
+  if (j < m) {
+    const double sd = sdelta[j];
+    const double uj = u[j] + lambda * sd;
+    const double drj = beta * dr[j] - gamma * uj;
+    const double rj = r[j] + drj;
+    dr[j] = drj;
+    r[j] = rj;
+    sdelta[j] = 0.0;
+    const double dwj = beta * dw[j] - gamma * sd;
+    dw[j] = dwj;
+    w[j] += dwj;
+    r2 = rj * rj;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) r2 += __shfl_xor_sync(0xffffffffu, r2, o);
+  if (lane == 0) red[warp] = r2;
+  __syncthreads();
+  if (tid == 0) {
+    double s = 0.0;
+    for (int q = 0; q < VT / 32; ++q) s += red[q];
+    partials[blockIdx.x] = s;
+    __threadfence();
+    const unsigned prev = atomicAdd(&ctrl->arrive, 1u);
+    s_last = (prev == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  if (tid == 0) {
+    double tot = 0.0;
+    for (unsigned q = 0; q < gridDim.x; ++q) tot += __ldcg(&partials[q]);
+    finish_iteration(ctrl, tot);
+  }
+}
+
 }  // namespace
+
+cudaError_t launch_update_vec(const double* u, double lambda, double* sdelta, double* w, double* dw,
+                              double* r, double* dr, long long m, double gamma, double beta,
+                              double* partials, Ctrl* ctrl, cudaStream_t st) {
+  const unsigned g = (unsigned)((m + VT - 1) / VT);
+  k_update_vec<<<g, VT, 0, st>>>(u, lambda, sdelta, w, dw, r, dr, m, gamma, beta, partials, ctrl);
+  return cudaGetLastError();
+}
 
 size_t update_partials(long long m) { return (size_t)((m + UX - 1) / UX); }
 

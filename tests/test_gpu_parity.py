@@ -76,7 +76,7 @@ def _run_gpu_dense(rs, X, y, lam, mode, kind, tau, beta, iters, seed=0, k=0, dev
 
 
 @pytest.mark.parametrize("beta", [0.0, 0.5])
-@pytest.mark.parametrize("mode", ["implicit", "explicit"])
+@pytest.mark.parametrize("mode", ["implicit", "explicit", "gram"])
 def test_config1_50_steps(rs, beta, mode):
     cfg = rsinputs.CONFIGS["c1"]
     X, y = _dense(cfg.n, cfg.d, noise=cfg.noise)
@@ -87,7 +87,7 @@ def test_config1_50_steps(rs, beta, mode):
     assert rel(r, ref["r"]) <= 1e-10
 
 
-@pytest.mark.parametrize("mode", ["implicit", "explicit"])
+@pytest.mark.parametrize("mode", ["implicit", "explicit", "gram"])
 def test_config1_final_vs_direct(rs, mode):
     cfg = rsinputs.CONFIGS["c1"]
     X, y = _dense(cfg.n, cfg.d, noise=cfg.noise)
@@ -102,7 +102,7 @@ def test_config1_final_vs_direct(rs, mode):
 
 @pytest.mark.parametrize("kind,tau,k", [("subsample", 37, 0), ("count", 37, 0), ("subcount", 29, 3),
                                         ("subsample", 130, 0), ("count", 300, 0)])
-@pytest.mark.parametrize("mode", ["implicit", "explicit"])
+@pytest.mark.parametrize("mode", ["implicit", "explicit", "gram"])
 def test_dense_ragged_parity(rs, kind, tau, k, mode):
     """Several GEMM tiles (64 x 128) with ragged tails, split-K, all sketch kinds."""
     X, y = _dense(3001, 301, seed=3, col_decay=True, noise=0.01)
@@ -242,13 +242,14 @@ def test_csr_dual_converges_to_direct(rs):
 
 
 # ---------------------------------------------------------------------------------- full size
-def test_config2_full_size_sampled(rs):
+@pytest.mark.parametrize("mode", ["implicit", "gram"])
+def test_config2_full_size_sampled(rs, mode):
     """BASELINE.json c2 at full size (1e5 x 2000, tau=200), the launch configuration bench.py
     times: the first 3 iterations equal the oracle's (same X bytes, host copy)."""
     cfg = rsinputs.CONFIGS["c2"]
     Xd, yd = rsinputs.dense_problem(cfg.n, cfg.d, seed=0, col_decay=True, noise=cfg.noise,
                                     device="cuda")
-    h = rs.rs_create_dense(Xd, yd, cfg.lam, borrow=True)
+    h = rs.rs_create_dense(Xd, yd, cfg.lam, mode=mode, borrow=True)
     try:
         w, rep = rs.rs_solve(h, "subsample", cfg.tau, 1.0, cfg.beta, 0.0, 3, seed=0)
         _, r = rs.rs_get_state(h)
