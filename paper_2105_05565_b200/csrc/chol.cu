@@ -279,6 +279,9 @@ k_chol(double* __restrict__ Gx, long long ldg, int tau, DevSketch sk, double* __
 //              (C -= L_Ip L_Jp^T, SASS DMMA).
 // Two block barriers per block column; then warp 0 runs the blocked backward substitution.
 constexpr int kSmallTau = 224;
+// phase timers (debug; read by rs_internal_chol_times): 0 gather, 1 diag, 2 panel, 3 trailing,
+// 4 backward, 5 scatter, 6 calls
+__device__ unsigned long long g_chol_t[8];
 constexpr int kSmallThreads = 1024;
 constexpr int NB8 = 8;
 
@@ -326,6 +329,14 @@ k_chol_small(const double* __restrict__ ASt, long long ld_as, bool rowmajor,
     }
     s_toff[Tc] = t;
   }
+  long long tc0 = clock64(), tc1;
+  unsigned long long acc_t[6] = {0, 0, 0, 0, 0, 0};
+#define RS_STAMP(k)                       \
+  if (tid == 0) {                         \
+    tc1 = clock64();                      \
+    acc_t[k] += (unsigned long long)(tc1 - tc0); \
+    tc0 = tc1;                            \
+  }
   // ---- a4: gather G (lower) and g into the blocked layout; padding entries = 0
   for (int q = tid; q < nblk * 64; q += kSmallThreads) sL[q] = 0.0;
   __syncthreads();
@@ -359,6 +370,7 @@ k_chol_small(const double* __restrict__ ASt, long long ld_as, bool rowmajor,
     }
   }
   __syncthreads();
+  RS_STAMP(0)
   for (int p = 0; p < Tc; ++p) {
     const int c0 = p * NB8;
     const int ncol = min(NB8, tau - c0);
@@ -390,6 +402,7 @@ k_chol_small(const double* __restrict__ ASt, long long ld_as, bool rowmajor,
       }
     }
     __syncthreads();
+    RS_STAMP(1)
     // ---- panel below the diagonal block (all threads, one row each): x L_pp^T = g
     for (int row = c0 + NB8 + tid; row < rows; row += kSmallThreads) {
       double x[8];
@@ -408,6 +421,7 @@ k_chol_small(const double* __restrict__ ASt, long long ld_as, bool rowmajor,
         if (k < ncol) sL[sidx(row, c0 + k)] = x[k];
     }
     __syncthreads();
+    RS_STAMP(2)
     // ---- trailing update of blocks (I, J), p < J <= I < Tr, J < Tc: C -= L_Ip L_Jp^T
     {
       const int ar = lane >> 2, ak = lane & 3;
@@ -431,6 +445,7 @@ k_chol_small(const double* __restrict__ ASt, long long ld_as, bool rowmajor,
       }
     }
     __syncthreads();
+    RS_STAMP(3)
   }
   if (s_bad) {
     if (tid == 0) ctrl->status = ST_NOTSPD;
@@ -464,11 +479,18 @@ k_chol_small(const double* __restrict__ ASt, long long ld_as, bool rowmajor,
     }
     __syncthreads();
   }
+  RS_STAMP(4)
   for (int b = tid; b < tau; b += kSmallThreads) delta[b] = sL[sidx(tau, b)];
   for (int e = tid; e < sk.len; e += kSmallThreads) {
     const double dv = sL[sidx(tau, sk.bucket[e])];
     sdelta[sk.coord[e]] = sk.sign[e] > 0 ? dv : -dv;
   }
+  RS_STAMP(5)
+  if (tid == 0) {
+    for (int k = 0; k < 6; ++k) atomicAdd(&g_chol_t[k], acc_t[k]);
+    atomicAdd(&g_chol_t[6], 1ull);
+  }
+#undef RS_STAMP
 }
 
 size_t small_smem(int tau) {
@@ -477,6 +499,13 @@ size_t small_smem(int tau) {
 }
 
 }  // namespace
+
+extern "C" int rs_internal_chol_times(unsigned long long* out) {
+  cudaError_t e = cudaMemcpyFromSymbol(out, g_chol_t, sizeof(g_chol_t));
+  unsigned long long z[8] = {0};
+  cudaMemcpyToSymbol(g_chol_t, z, sizeof(z));
+  return (int)e;
+}
 
 cudaError_t chol_init() {
   return cudaFuncSetAttribute(k_chol_small, cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -117,6 +117,7 @@ rs_status setup_common(Problem* p, const rs_dist* dist) {
   RS_CUDA(gemm_init());
   RS_CUDA(chol_init());
   RS_CUDA(tma_gemm_init());
+  RS_CUDA(gram_init());
   if (dist && dist->cuda_stream) {
     p->st = static_cast<cudaStream_t>(dist->cuda_stream);
     p->own_stream = false;
@@ -351,9 +352,10 @@ rs_status Problem::ensure_workspace(int kind, int tau, int ksum) {
     RS_TRY(dalloc(&XS, (size_t)std::max<long long>(rows_loc, 1) * ld_xs));
     ld_gram = round_up(tau, 4);
     RS_TRY(dalloc(&Gram, (size_t)tau * ld_gram));
-    RS_TRY(dalloc(&xp_part, xpass_partials(m, num_sms)));
+    RS_TRY(dalloc(&xp_part, std::max(xpass_partials(m, num_sms), gram_fused_partials(num_sms))));
     RS_TRY(dalloc(&uvec, m));
-    if (rows_loc > 0) {
+    gram_fused = gram_fused_ok(kind, tau) && !std::getenv("RS_NO_GRAM_FUSED");
+    if (rows_loc > 0 && !gram_fused) {
       RS_CUDA(tma_gemm_plan(&tg_gram, XS, ld_xs, XS, ld_xs, tau, tau, rows_loc, num_sms));
       if (tg_gram.work_elems) RS_TRY(dalloc(&gemm_work, tg_gram.work_elems));
       if (std::getenv("RS_VERBOSE"))
@@ -401,11 +403,15 @@ rs_status Problem::enqueue_iteration(const rs_solve_opts* o, cudaEvent_t* ev) {
   RS_CUDA(launch_sketch(sk, o->seed, ctrl, -1, st));                       // a1
   mark(RS_K_SKETCH, 1);
   if (fmt == 0 && mode == RS_AS_GRAM) {
-    mark(RS_K_XS, 0);
-    RS_CUDA(launch_dense_xs(X, ldx, rows_loc, sk, XS, ld_xs, ctrl, st));    // a2  XS
-    mark(RS_K_XS, 1);
+    if (!gram_fused) {
+      mark(RS_K_XS, 0);
+      RS_CUDA(launch_dense_xs(X, ldx, rows_loc, sk, XS, ld_xs, ctrl, st));  // a2  XS
+      mark(RS_K_XS, 1);
+    }
     mark(RS_K_GRAM, 0);
-    if (rows_loc > 0)
+    if (rows_loc > 0 && gram_fused)                                          // gather + (XS)^T XS
+      RS_CUDA(launch_gram_fused(X, ldx, rows_loc, sk, xp_part, Gram, ld_gram, num_sms, ctrl, st));
+    else if (rows_loc > 0)
       RS_CUDA(tma_gemm_launch(tg_gram, Gram, ld_gram, gemm_work, ctrl, st));   // (XS)^T XS
     else
       RS_CUDA(launch_fill(Gram, (long long)sk.tau * ld_gram, 0.0, st));

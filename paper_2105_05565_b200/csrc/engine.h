@@ -66,6 +66,7 @@ struct Problem {
   long long ld_gram = 0;
   double* xp_part = nullptr;
   double* uvec = nullptr;
+  bool gram_fused = false;
   bool use_tma = true;
   SolveWork sw{};
   double* partials = nullptr;

@@ -147,6 +147,13 @@ size_t xpass_partials(long long d, int num_sms);
 cudaError_t launch_xpass(const double* X, long long ldx, long long rows, long long d,
                          const double* v, double* partials, double* u, int num_sms,
                          const Ctrl* ctrl, cudaStream_t st);
+// Fused gather + Gram (subsample, tau <= 200): G lower = sum_i X[i,C]^T X[i,C], no XS written.
+bool gram_fused_ok(int kind, int tau);
+size_t gram_fused_partials(int num_sms);
+cudaError_t gram_init();
+cudaError_t launch_gram_fused(const double* X, long long ldx, long long rows, const DevSketch& sk,
+                              double* partials, double* G, long long ldg, int num_sms,
+                              const Ctrl* ctrl, cudaStream_t st);
 // update with a dense u = X^T X S delta:  u_j + lambda sdelta_j  is A S delta
 cudaError_t launch_update_vec(const double* u, double lambda, double* sdelta, double* w, double* dw,
                               double* r, double* dr, long long m, double gamma, double beta,
