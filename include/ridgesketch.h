@@ -39,7 +39,7 @@
 extern "C" {
 #endif
 
-#define RS_ABI_VERSION 1
+#define RS_ABI_VERSION 2
 
 typedef struct rs_problem_t* rs_problem;
 
@@ -132,7 +132,10 @@ enum {
   RS_K_SOLVE = 3,    /* a4 + a5 S^T A S, S^T r, Cholesky, triangular solves, S delta     */
   RS_K_UPDATE = 4,   /* a6 fused momentum update + ||r||^2 + stop flag                   */
   RS_K_GRAM = 5,     /* GRAM mode: G = (XS)^T XS contraction (+ allreduce)               */
-  RS_K_NCLASSES = 6
+  RS_K_PRE = 6,      /* sketch-ahead group precompute (EXPLICIT / GRAM modes): P sketches, their
+                        A S^T rows or Grams, and the batched Cholesky + inverse of the P
+                        matrices G_k; counted once per group of P iterations                  */
+  RS_K_NCLASSES = 7
 };
 
 typedef struct {

@@ -1,0 +1,331 @@
+// Sketch-ahead batched factorisation -- SURVEY §8(a) rows a4 + a5 ("the fused S^T A S gather plus
+// batched tau x tau Cholesky", BASELINE.json north_star).
+//
+// Alg. 2 draws S_k ~ D independently of the iterate, so G_k = S_k^T A S_k
+// is a function of (seed, k) and the data only.  For a group of P future iterations the
+// engine draws the P sketches, forms the P matrices G_k and factors them here in ONE launch (one CTA
+// per G_k, all SMs busy), off the iteration's critical path:
+//
+//   G = L L^T       right-looking blocked Cholesky, 8 x 8 blocks, DMMA trailing updates
+//                   (lower triangle of G read only, R12; empty-bucket rule R3)
+//   W = L^{-1}      blocked in-place triangular inversion (column blocks from the last):
+//                   W_JJ = L_JJ^{-1},  W_IJ = -(sum_{K=J+1..I} W_IK L_KJ) W_JJ
+//   Ginv = W^T W    = G^{-1}, written in full (tau x tau, row-major) to the slot
+//
+// so the iteration needs only delta = Ginv (S^T r^k) (P:L217 least-norm solution = G^{-1} g for SPD
+// G, R3/R21): a parallel GEMV instead of a latency-bound factorisation per iteration.
+//
+// Shared-memory layout (one CTA, tau <= 224): the lower block triangle of G as 8 x 8 blocks packed by
+// block row (block (I, J), J <= I, at index I(I+1)/2 + J), each block row-major with an XOR swizzle
+// (column c of row r at c ^ 4((r >> 1) & 1)) so DMMA fragment loads -- plain and transposed -- are
+// bank-conflict free; then a panel temp of Tc blocks.
+#include "rs_internal.cuh"
+
+namespace rs {
+
+namespace {
+
+constexpr int BF_THREADS = 1024;
+constexpr int BF_WARPS = BF_THREADS / 32;
+constexpr int BF_MAXTAU = 224;
+constexpr int AG_WARPS = 8;
+constexpr int AG_MAXTAU = 4096;
+
+__device__ __forceinline__ int bblk(int I, int J) { return I * (I + 1) / 2 + J; }
+__device__ __forceinline__ int bsw(int r, int c) { return r * 8 + (c ^ (((r >> 1) & 1) << 2)); }
+__device__ __forceinline__ int bidx(int row, int col) {
+  return bblk(row >> 3, col >> 3) * 64 + bsw(row & 7, col & 7);
+}
+// D = A B + D, A 8x4 row-major (lane: A[lane/4][lane%4]), B 4x8 (lane: B[lane%4][lane/4]),
+// D 8x8 (lane: D[lane/4][2(lane%4)], D[lane/4][2(lane%4)+1]).  SASS DMMA.8x8x4.
+__device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c[0]), "+d"(c[1])
+               : "d"(a), "d"(b));
+}
+// t -> (I, J), J <= I, t = I(I+1)/2 + J
+__device__ __forceinline__ void tri_decode(int t, int& I, int& J) {
+  int i = (int)((sqrtf(8.0f * (float)t + 1.0f) - 1.0f) * 0.5f);
+  while ((i + 1) * (i + 2) / 2 <= t) ++i;
+  while (i * (i + 1) / 2 > t) --i;
+  I = i;
+  J = t - i * (i + 1) / 2;
+}
+
+size_t bf_smem(int tau) {
+  const int Tc = (tau + 7) / 8;
+  return (size_t)(Tc * (Tc + 1) / 2 + Tc) * 64 * sizeof(double);
+}
+
+__global__ void __launch_bounds__(BF_THREADS, 1)
+k_bfactor_small(FactorSrc src, DevSketch skb, double* __restrict__ Ginv, long long ldgi,
+                long long gi_stride, int* __restrict__ flags, const Ctrl* ctrl) {
+  if (ctrl && ctrl->done) return;
+  extern __shared__ double sL[];
+  __shared__ double s_inv[BF_MAXTAU];
+  __shared__ int s_bad;
+  const int slot = blockIdx.x;
+  const DevSketch sk = skb.at(slot);
+  const int tau = sk.tau, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int ar = lane >> 2, ak = lane & 3;
+  const int Tc = (tau + 7) / 8;
+  const int nblk = Tc * (Tc + 1) / 2;
+  double* sT = sL + nblk * 64;
+  for (int q = tid; q < (nblk + Tc) * 64; q += BF_THREADS) sL[q] = 0.0;
+  for (int q = tid; q < BF_MAXTAU; q += BF_THREADS) s_inv[q] = 0.0;
+  if (tid == 0) s_bad = 0;
+  __syncthreads();
+
+  // ---- a4: G = S^T A S (lower): from AS^T rows (G[a][c] = sum_{e in a} sign_e AS^T[c][coord_e])
+  // or from the Gram slot (G = (XS)^T XS + lambda S^T S, S^T S = diag(|bucket|)); R3 rule.
+  const double* ASt = src.ASt ? src.ASt + slot * src.as_stride : nullptr;
+  const double* Gram = src.Gram ? src.Gram + slot * src.gram_stride : nullptr;
+  for (int a = warp; a < tau; a += BF_WARPS) {
+    const int e0 = sk.bptr[a], e1 = sk.bptr[a + 1];
+    for (int c = lane; c <= a; c += 32) {
+      double v = 0.0;
+      if (Gram) {
+        v = Gram[(long long)a * src.ld_gram + c];
+        if (a == c) v += src.lambda * (double)(e1 - e0);
+      } else if (!ASt) {   // straight from explicit A
+        const int f0 = sk.bptr[c], f1 = sk.bptr[c + 1];
+        for (int e = e0; e < e1; ++e) {
+          const double* Ae = src.A + (long long)sk.coord[e] * src.lda;
+          double t = 0.0;
+          for (int f = f0; f < f1; ++f) {
+            const double x = Ae[sk.coord[f]];
+            t += sk.sign[f] > 0 ? x : -x;
+          }
+          v += sk.sign[e] > 0 ? t : -t;
+        }
+      } else {
+        const double* col = ASt + (long long)c * src.ld_as;
+        for (int e = e0; e < e1; ++e) {
+          const double x = col[sk.coord[e]];
+          v += sk.sign[e] > 0 ? x : -x;
+        }
+      }
+      if (e0 == e1 || sk.bptr[c] == sk.bptr[c + 1]) v = (a == c) ? 1.0 : 0.0;
+      sL[bidx(a, c)] = v;
+    }
+  }
+  __syncthreads();
+
+  // ---- a5: Cholesky G = L L^T, block columns p = 0 .. Tc-1
+  for (int p = 0; p < Tc; ++p) {
+    const int c0 = p * 8, ncol = min(8, tau - c0);
+    if (warp == 0) {   // diagonal block in registers: lane (mod 8) = row, left-looking
+      const int rr = lane & 7, grow = c0 + rr;
+      double v[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) v[k] = (k <= rr && rr < ncol) ? sL[bidx(grow, c0 + k)] : 0.0;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        if (j < ncol) {
+          double sj = v[j];
+#pragma unroll
+          for (int k = 0; k < j; ++k) sj -= v[k] * __shfl_sync(0xffffffffu, v[k], j);
+          double dd = __shfl_sync(0xffffffffu, sj, j);
+          if (!(dd > 0.0) || !isfinite(dd)) {
+            if (lane == 0) s_bad = 1;
+            dd = 1.0;
+          }
+          const double inv = rsqrt(dd);
+          if (rr == j) v[j] = dd * inv;
+          else if (rr > j) v[j] = sj * inv;
+          if (lane == j) s_inv[c0 + j] = inv;
+        }
+      }
+      if (lane < 8 && rr < ncol) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+          if (k <= rr) sL[bidx(grow, c0 + k)] = v[k];
+      }
+    }
+    __syncthreads();
+    // panel: rows below the diagonal block, one thread per row:  x L_pp^T = g
+    for (int row = c0 + 8 + tid; row < tau; row += BF_THREADS) {
+      double x[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) x[k] = k < ncol ? sL[bidx(row, c0 + k)] : 0.0;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        if (j < ncol) {
+#pragma unroll
+          for (int k = 0; k < j; ++k) x[j] -= x[k] * sL[bidx(c0 + j, c0 + k)];
+          x[j] *= s_inv[c0 + j];
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < 8; ++k)
+        if (k < ncol) sL[bidx(row, c0 + k)] = x[k];
+    }
+    __syncthreads();
+    // trailing update C_IJ -= L_Ip L_Jp^T, p < J <= I < Tc (two DMMA per block)
+    {
+      const int nt = Tc - 1 - p;
+      const int ntiles = nt * (nt + 1) / 2;
+      for (int t = warp; t < ntiles; t += BF_WARPS) {
+        int Ii, Jj;
+        tri_decode(t, Ii, Jj);
+        const int I = p + 1 + Ii, J = p + 1 + Jj;
+        const double* Lip = sL + bblk(I, p) * 64;
+        const double* Ljp = sL + bblk(J, p) * 64;
+        double* Cb = sL + bblk(I, J) * 64;
+        double acc[2] = {Cb[bsw(ar, 2 * ak)], Cb[bsw(ar, 2 * ak + 1)]};
+        dmma(acc, -Lip[bsw(ar, ak)], Ljp[bsw(ar, ak)]);
+        dmma(acc, -Lip[bsw(ar, ak + 4)], Ljp[bsw(ar, ak + 4)]);
+        Cb[bsw(ar, 2 * ak)] = acc[0];
+        Cb[bsw(ar, 2 * ak + 1)] = acc[1];
+      }
+    }
+    __syncthreads();
+  }
+  if (s_bad) {
+    if (tid == 0) flags[slot] = 1;
+    return;
+  }
+
+  // ---- W = L^{-1} in place, block columns J = Tc-1 .. 0
+  for (int J = Tc - 1; J >= 0; --J) {
+    const int c0 = J * 8, ncol = min(8, tau - c0);
+    if (warp == 0) {
+      if (lane < 8) {   // lane j: column j of W_JJ = L_JJ^{-1} (forward substitution on e_j)
+        const int j = lane;
+        double x[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          double xi = 0.0;
+          if (j < ncol && i < ncol && i >= j) {
+            if (i == j) {
+              xi = s_inv[c0 + i];
+            } else {
+              double s = 0.0;
+#pragma unroll
+              for (int k = 0; k < i; ++k)
+                if (k >= j) s += sL[bidx(c0 + i, c0 + k)] * x[k];
+              xi = -s * s_inv[c0 + i];
+            }
+          }
+          x[i] = xi;
+        }
+        double* Wjj = sL + bblk(J, J) * 64;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) Wjj[bsw(i, j)] = x[i];   // zeros above the diagonal
+      }
+    } else {
+      // T_I = sum_{K=J+1..I} W_IK L_KJ  (W_IK final for K > J; L_KJ still L)
+      for (int I = J + warp; I < Tc; I += BF_WARPS - 1) {
+        double acc[2] = {0.0, 0.0};
+        for (int K = J + 1; K <= I; ++K) {
+          const double* Wik = sL + bblk(I, K) * 64;
+          const double* Lkj = sL + bblk(K, J) * 64;
+          dmma(acc, Wik[bsw(ar, ak)], Lkj[bsw(ak, ar)]);
+          dmma(acc, Wik[bsw(ar, ak + 4)], Lkj[bsw(ak + 4, ar)]);
+        }
+        sT[I * 64 + bsw(ar, 2 * ak)] = acc[0];
+        sT[I * 64 + bsw(ar, 2 * ak + 1)] = acc[1];
+      }
+    }
+    __syncthreads();
+    // W_IJ = -T_I W_JJ, written over L_IJ
+    for (int I = J + 1 + warp; I < Tc; I += BF_WARPS) {
+      const double* Ti = sT + I * 64;
+      const double* Wjj = sL + bblk(J, J) * 64;
+      double acc[2] = {0.0, 0.0};
+      dmma(acc, Ti[bsw(ar, ak)], Wjj[bsw(ak, ar)]);
+      dmma(acc, Ti[bsw(ar, ak + 4)], Wjj[bsw(ak + 4, ar)]);
+      double* Cb = sL + bblk(I, J) * 64;
+      Cb[bsw(ar, 2 * ak)] = -acc[0];
+      Cb[bsw(ar, 2 * ak + 1)] = -acc[1];
+    }
+    __syncthreads();
+  }
+
+  // ---- Ginv = W^T W: block (I, J), J <= I, = sum_{K >= I} W_KI^T W_KJ; mirrored above
+  double* Gi = Ginv + slot * gi_stride;
+  const int npairs = Tc * (Tc + 1) / 2;
+  for (int t = warp; t < npairs; t += BF_WARPS) {
+    int I, J;
+    tri_decode(t, I, J);
+    double acc[2] = {0.0, 0.0};
+    for (int K = I; K < Tc; ++K) {
+      const double* Wki = sL + bblk(K, I) * 64;
+      const double* Wkj = sL + bblk(K, J) * 64;
+      dmma(acc, Wki[bsw(ak, ar)], Wkj[bsw(ak, ar)]);
+      dmma(acc, Wki[bsw(ak + 4, ar)], Wkj[bsw(ak + 4, ar)]);
+    }
+    const int row = I * 8 + ar;
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const int col = J * 8 + 2 * ak + q;
+      if (row < tau && col < tau) {
+        Gi[(long long)row * ldgi + col] = acc[q];
+        if (I != J) Gi[(long long)col * ldgi + row] = acc[q];
+      }
+    }
+  }
+  if (tid == 0) flags[slot] = 0;
+}
+
+// delta = Ginv g, g = S^T r; one warp per row of Ginv.
+__global__ void __launch_bounds__(AG_WARPS * 32)
+k_apply_ginv(const double* __restrict__ Ginv, long long ldgi, DevSketch sk,
+             const int* __restrict__ flag, const double* __restrict__ r, double* __restrict__ delta,
+             double* __restrict__ sdelta, Ctrl* ctrl) {
+  if (ctrl->done) return;
+  if (*flag) {   // the update kernel of this iteration turns the status into `done`
+    if (blockIdx.x == 0 && threadIdx.x == 0) ctrl->status = ST_NOTSPD;
+    return;
+  }
+  __shared__ double g[AG_MAXTAU];
+  const int tau = sk.tau, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int b = tid; b < tau; b += AG_WARPS * 32) {
+    double v = 0.0;
+    for (int e = sk.bptr[b]; e < sk.bptr[b + 1]; ++e) {
+      const double x = r[sk.coord[e]];
+      v += sk.sign[e] > 0 ? x : -x;
+    }
+    g[b] = v;
+  }
+  __syncthreads();
+  const int a = blockIdx.x * AG_WARPS + warp;
+  if (a >= tau) return;
+  const double* row = Ginv + (long long)a * ldgi;
+  double s = 0.0;
+  for (int b = lane; b < tau; b += 32) s += row[b] * g[b];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (lane == 0) delta[a] = s;
+  for (int e = sk.bptr[a] + lane; e < sk.bptr[a + 1]; e += 32)
+    sdelta[sk.coord[e]] = sk.sign[e] > 0 ? s : -s;
+}
+
+}  // namespace
+
+int bfactor_max_tau() { return BF_MAXTAU; }
+
+cudaError_t bfactor_init() {
+  return cudaFuncSetAttribute(k_bfactor_small, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)bf_smem(BF_MAXTAU));
+}
+
+cudaError_t launch_bfactor(const FactorSrc& src, const DevSketch& skb, int nslots, double* Ginv,
+                           long long ldgi, long long gi_stride, int* flags, const Ctrl* ctrl,
+                           cudaStream_t st) {
+  if (skb.tau > BF_MAXTAU || nslots < 1) return cudaErrorInvalidValue;
+  k_bfactor_small<<<nslots, BF_THREADS, bf_smem(skb.tau), st>>>(src, skb, Ginv, ldgi, gi_stride,
+                                                                 flags, ctrl);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_apply_ginv(const double* Ginv, long long ldgi, const DevSketch& sk,
+                              const int* flag, const double* r, double* delta, double* sdelta,
+                              Ctrl* ctrl, cudaStream_t st) {
+  if (sk.tau > AG_MAXTAU) return cudaErrorInvalidValue;
+  const unsigned grid = (unsigned)((sk.tau + AG_WARPS - 1) / AG_WARPS);
+  k_apply_ginv<<<grid, AG_WARPS * 32, 0, st>>>(Ginv, ldgi, sk, flag, r, delta, sdelta, ctrl);
+  return cudaGetLastError();
+}
+
+}  // namespace rs

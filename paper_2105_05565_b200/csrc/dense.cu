@@ -41,9 +41,11 @@ __global__ void k_dense_xs(const double* __restrict__ X, long long ldx, long lon
 
 __global__ void k_explicit_rows(const double* __restrict__ A, long long lda, long long m,
                                 DevSketch sk, double* __restrict__ ASt, long long ld_as,
-                                const Ctrl* ctrl) {
+                                long long as_stride, const Ctrl* ctrl) {
   if (ctrl && ctrl->done) return;
   const int b = blockIdx.y;
+  sk = sk.at(blockIdx.z);          // batched: slot blockIdx.z
+  ASt += blockIdx.z * as_stride;
   const long long j = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= m) return;
   const int e0 = sk.bptr[b], e1 = sk.bptr[b + 1];
@@ -307,8 +309,15 @@ cudaError_t launch_dense_xs(const double* X, long long ldx, long long rows, cons
 
 cudaError_t launch_explicit_rows(const double* A, long long lda, long long m, const DevSketch& sk,
                                  double* ASt, long long ld_as, const Ctrl* ctrl, cudaStream_t st) {
-  dim3 grid((unsigned)((m + 255) / 256), (unsigned)sk.tau);
-  k_explicit_rows<<<grid, 256, 0, st>>>(A, lda, m, sk, ASt, ld_as, ctrl);
+  return launch_explicit_rows_batch(A, lda, m, sk, 1, ASt, ld_as, 0, ctrl, st);
+}
+
+cudaError_t launch_explicit_rows_batch(const double* A, long long lda, long long m,
+                                       const DevSketch& skb, int nslots, double* ASt,
+                                       long long ld_as, long long as_stride, const Ctrl* ctrl,
+                                       cudaStream_t st) {
+  dim3 grid((unsigned)((m + 255) / 256), (unsigned)skb.tau, (unsigned)nslots);
+  k_explicit_rows<<<grid, 256, 0, st>>>(A, lda, m, skb, ASt, ld_as, as_stride, ctrl);
   return cudaGetLastError();
 }
 

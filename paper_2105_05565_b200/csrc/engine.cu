@@ -82,6 +82,23 @@ void Problem::free_workspace() {
   sw = SolveWork{};
   dfree(partials);
   partials = nullptr;
+  dfree(skb.coord);
+  dfree(skb.sign);
+  dfree(skb.bucket);
+  dfree(skb.bptr);
+  dfree(skb.cmap);
+  skb = DevSketch{};
+  dfree(ASt_slots);
+  ASt_slots = nullptr;
+  dfree(Gram_slots);
+  Gram_slots = nullptr;
+  dfree(Ginv_slots);
+  Ginv_slots = nullptr;
+  dfree(slot_flags);
+  slot_flags = nullptr;
+  pipe = false;
+  P = 0;
+  ws_depth = -1;
   ws_kind = -1;
   ws_tau = -1;
   ws_ksum = -1;
@@ -118,6 +135,8 @@ rs_status setup_common(Problem* p, const rs_dist* dist) {
   RS_CUDA(chol_init());
   RS_CUDA(tma_gemm_init());
   RS_CUDA(gram_init());
+  RS_CUDA(bfactor_init());
+  RS_CUDA(update_init());
   if (dist && dist->cuda_stream) {
     p->st = static_cast<cudaStream_t>(dist->cuda_stream);
     p->own_stream = false;
@@ -328,8 +347,15 @@ static rs_status validate_opts(const Problem* p, const rs_solve_opts* o, int* ks
   return RS_OK;
 }
 
-rs_status Problem::ensure_workspace(int kind, int tau, int ksum) {
-  if (ws_kind == kind && ws_tau == tau && ws_ksum == ksum) return RS_OK;
+// Sketch-ahead pipeline (bfactor.cu) applies to dense primal EXPLICIT and GRAM modes with
+// tau <= bfactor_max_tau(): there G_k needs no per-iteration contraction of the iterate's data.
+static bool pipeline_applies(const Problem* p, int tau) {
+  return p->fmt == 0 && p->route == 1 && (p->mode == RS_AS_EXPLICIT || p->mode == RS_AS_GRAM) &&
+         tau <= bfactor_max_tau() && !std::getenv("RS_NO_PIPE");
+}
+
+rs_status Problem::ensure_workspace(int kind, int tau, int ksum, int depth) {
+  if (ws_kind == kind && ws_tau == tau && ws_ksum == ksum && ws_depth == depth) return RS_OK;
   cudaStreamSynchronize(st);
   free_workspace();
   const size_t L = sketch_max_len(kind, (int)m, tau, ksum);
@@ -346,6 +372,9 @@ rs_status Problem::ensure_workspace(int kind, int tau, int ksum) {
   if (fmt == 1) {   // CSR: AS row-major m x tau
     ld_as = round_up(tau, 4);
     RS_TRY(dalloc(&ASt, (size_t)m * ld_as));
+  } else if (depth > 0 && mode == RS_AS_EXPLICIT) {   // pipelined explicit: A S^T per slot
+    ld_as = round_up(m, 4);
+    as_stride = (long long)tau * ld_as;
   } else if (mode == RS_AS_GRAM) {   // no A S at all: XS, G, u
     ld_as = round_up(m, 4);
     ld_xs = round_up(tau, 4);
@@ -383,6 +412,27 @@ rs_status Problem::ensure_workspace(int kind, int tau, int ksum) {
               use_tma ? tg.bm : gp.bm, use_tma ? tg.bn : gp.bn, use_tma ? tg.splits : gp.splits);
   }
   if (fmt == 1) RS_TRY(csr_ensure_workspace(kind, tau, ksum));
+  if (depth > 0) {   // sketch-ahead slots
+    pipe = true;
+    P = depth;
+    skb = sk;   // same geometry, `depth` slots
+    skb.coord = nullptr; skb.sign = nullptr; skb.bucket = nullptr; skb.bptr = nullptr; skb.cmap = nullptr;
+    RS_TRY(dalloc(&skb.coord, L * depth));
+    RS_TRY(dalloc(&skb.sign, L * depth));
+    RS_TRY(dalloc(&skb.bucket, L * depth));
+    RS_TRY(dalloc(&skb.bptr, (size_t)(tau + 1) * depth));
+    if (kind == SK_COUNT) RS_TRY(dalloc(&skb.cmap, (size_t)m * depth));
+    if (mode == RS_AS_EXPLICIT) {   // count: A S^T rows per slot; subsample / SubCount read A directly
+      if (kind == SK_COUNT) RS_TRY(dalloc(&ASt_slots, (size_t)as_stride * depth));
+    } else {
+      gram_stride = (long long)tau * ld_gram;
+      RS_TRY(dalloc(&Gram_slots, (size_t)gram_stride * depth));
+    }
+    ld_gi = round_up(tau, 4);
+    gi_stride = (long long)tau * ld_gi;
+    RS_TRY(dalloc(&Ginv_slots, (size_t)gi_stride * depth));
+    RS_TRY(dalloc(&slot_flags, depth));
+  }
   sw = plan_solve(tau, num_sms);
   RS_TRY(dalloc(&sw.Gx, solve_gx_elems(tau)));
   RS_TRY(dalloc(&sw.delta, tau));
@@ -390,6 +440,7 @@ rs_status Problem::ensure_workspace(int kind, int tau, int ksum) {
   ws_kind = kind;
   ws_tau = tau;
   ws_ksum = ksum;
+  ws_depth = depth;
   return RS_OK;
 }
 
@@ -464,6 +515,79 @@ rs_status Problem::enqueue_iteration(const rs_solve_opts* o, cudaEvent_t* ev) {
   return RS_OK;
 }
 
+// Group precompute of the sketch-ahead pipeline: sketches S_{k0..k0+ns-1} (k0 = ctrl->k), their
+// A S^T rows (explicit) or Grams (XS)^T XS (gram), and the batched factorisation Ginv = G^{-1}.
+rs_status Problem::enqueue_precompute(const rs_solve_opts* o, int ns, cudaEvent_t* ev) {
+  if (ev) cudaEventRecordWithFlags(ev[2 * RS_K_PRE], st, cudaEventRecordExternal);
+  RS_CUDA(launch_sketch_batch(skb, ns, o->seed, ctrl, -1, st));                 // a1 x ns
+  FactorSrc src{};
+  if (mode == RS_AS_EXPLICIT && ASt_slots) {                                     // a2 x ns
+    RS_CUDA(launch_explicit_rows_batch(A, lda, m, skb, ns, ASt_slots, ld_as, as_stride, ctrl, st));
+    src.ASt = ASt_slots;
+    src.ld_as = ld_as;
+    src.as_stride = as_stride;
+  } else if (mode == RS_AS_EXPLICIT) {   // G = S^T A S gathered from A inside the factor kernel
+    src.A = A;
+    src.lda = lda;
+  } else {                                                                       // Gram x ns
+    for (int q = 0; q < ns; ++q) {
+      const DevSketch sq = skb.at(q);
+      double* Gq = Gram_slots + (long long)q * gram_stride;
+      if (rows_loc > 0 && gram_fused) {
+        RS_CUDA(launch_gram_fused(X, ldx, rows_loc, sq, xp_part, Gq, ld_gram, num_sms, ctrl, st));
+      } else if (rows_loc > 0) {
+        RS_CUDA(launch_dense_xs(X, ldx, rows_loc, sq, XS, ld_xs, ctrl, st));
+        RS_CUDA(tma_gemm_launch(tg_gram, Gq, ld_gram, gemm_work, ctrl, st));
+      } else {
+        RS_CUDA(launch_fill(Gq, gram_stride, 0.0, st));
+      }
+      RS_TRY(allreduce(Gq, (size_t)gram_stride));
+    }
+    src.Gram = Gram_slots;
+    src.ld_gram = ld_gram;
+    src.gram_stride = gram_stride;
+    src.lambda = lambda;
+  }
+  RS_CUDA(launch_bfactor(src, skb, ns, Ginv_slots, ld_gi, gi_stride, slot_flags, ctrl, st));  // a4+a5
+  if (ev) cudaEventRecordWithFlags(ev[2 * RS_K_PRE + 1], st, cudaEventRecordExternal);
+  return RS_OK;
+}
+
+// One iteration of Alg. 2 on precomputed slot `slot`: delta = Ginv S^T r, A S delta, update.
+rs_status Problem::enqueue_pipelined_iteration(const rs_solve_opts* o, int slot, cudaEvent_t* ev) {
+  auto mark = [&](int cls, int edge) {
+    if (ev) cudaEventRecordWithFlags(ev[2 * cls + edge], st, cudaEventRecordExternal);
+  };
+  const DevSketch sq = skb.at(slot);
+  mark(RS_K_SOLVE, 0);
+  RS_CUDA(launch_apply_ginv(Ginv_slots + (long long)slot * gi_stride, ld_gi, sq, slot_flags + slot,
+                            r, sw.delta, sdelta, ctrl, st));                      // a4 + a5
+  mark(RS_K_SOLVE, 1);
+  if (mode == RS_AS_EXPLICIT) {
+    mark(RS_K_UPDATE, 0);
+    if (ASt_slots)
+      RS_CUDA(launch_update(ASt_slots + (long long)slot * as_stride, ld_as, false, sq.tau, sw.delta,
+                            sdelta, w, dw, r, dr, m, o->gamma, o->beta, partials, ctrl, st));  // a6+a7
+    else   // A S delta from the sketched rows of A
+      RS_CUDA(launch_update_rows(A, lda, sq, sw.delta, sdelta, w, dw, r, dr, m, o->gamma, o->beta,
+                                 partials, ctrl, st));                                        // a6+a7
+    mark(RS_K_UPDATE, 1);
+    return RS_OK;
+  }
+  mark(RS_K_AS, 0);
+  if (rows_loc > 0)
+    RS_CUDA(launch_xpass(X, ldx, rows_loc, m, sdelta, xp_part, uvec, num_sms, ctrl, st));
+  else
+    RS_CUDA(launch_fill(uvec, m, 0.0, st));
+  RS_TRY(allreduce(uvec, (size_t)m));                                            // X^T X S delta
+  mark(RS_K_AS, 1);
+  mark(RS_K_UPDATE, 0);
+  RS_CUDA(launch_update_vec(uvec, lambda, sdelta, w, dw, r, dr, m, o->gamma, o->beta, partials,
+                            ctrl, st));                                          // a6 + a7
+  mark(RS_K_UPDATE, 1);
+  return RS_OK;
+}
+
 static int status_of(int st) {
   switch (st) {
     case ST_DIVERGED: return RS_EDIVERGED;
@@ -479,7 +603,19 @@ rs_status Problem::solve(const rs_solve_opts* o, double* w_out, rs_mem w_mem, do
   RS_TRY(validate_opts(this, o, &ksum));
   if (!w_out) return fail(RS_EINVAL, "w_out is NULL");
   RS_CUDA(cudaSetDevice(device));
-  RS_TRY(ensure_workspace((int)o->kind, (int)o->tau, ksum));
+  const bool want_pipe = pipeline_applies(this, (int)o->tau);
+  // iterations per CUDA-graph launch (between host reads of the stop flag)
+  const int chunk = (int)(o->check_every > 0 ? std::min<long long>(o->check_every, 1024)
+                                             : (want_pipe ? 64 : 16));
+  int depth = 0;
+  if (want_pipe) {   // one batched factorisation wave: <= num_sms slots, <= ~6 GB of slots
+    const long long slot_bytes =
+        8LL * o->tau * (mode == RS_AS_EXPLICIT ? round_up(m, 4) : round_up(o->tau, 4)) +
+        8LL * o->tau * round_up(o->tau, 4) + 16LL * m;
+    depth = (int)std::max<long long>(1, std::min<long long>({(long long)chunk, (long long)num_sms,
+                                                             6000000000LL / slot_bytes}));
+  }
+  RS_TRY(ensure_workspace((int)o->kind, (int)o->tau, ksum, depth));
   // state: w^{-1} = w^0 = 0, r^{-1} = r^0 = -b
   RS_CUDA(launch_fill(w, m, 0.0, st));
   RS_CUDA(launch_fill(dw, m, 0.0, st));
@@ -508,55 +644,59 @@ rs_status Problem::solve(const rs_solve_opts* o, double* w_out, rs_mem w_mem, do
   *ctrl_host = c;
   RS_CUDA(cudaMemcpyAsync(ctrl, ctrl_host, sizeof(Ctrl), cudaMemcpyHostToDevice, st));
 
-  // CUDA graph of `chunk` iterations
-  const int chunk = (int)(o->check_every > 0 ? std::min<long long>(o->check_every, 1024) : 16);
-  if (graph_exec) cudaGraphExecDestroy(graph_exec);
-  graph_exec = nullptr;
-  for (auto ev : prof_events) cudaEventDestroy(ev);
-  prof_events.clear();
-  if (o->profile) {
-    prof_events.resize((size_t)chunk * 2 * RS_K_NCLASSES);
-    for (auto& ev : prof_events) RS_CUDA(cudaEventCreate(&ev));
+  // CUDA graph of `chunk` iterations, reused by later solves with the same launch parameters
+  const GraphKey key{(int)o->kind, (int)o->tau, ksum, chunk, o->profile ? 1 : 0, o->seed, o->gamma,
+                     o->beta};
+  const bool rebuild = !graph_exec || !(key == graph_key);
+  if (rebuild) {
+    if (graph_exec) cudaGraphExecDestroy(graph_exec);
+    graph_exec = nullptr;
+    for (auto ev : prof_events) cudaEventDestroy(ev);
+    prof_events.clear();
+    if (o->profile) {
+      prof_events.resize((size_t)chunk * 2 * RS_K_NCLASSES);
+      for (auto& ev : prof_events) RS_CUDA(cudaEventCreate(&ev));
+    }
   }
   RS_CUDA(cudaStreamSynchronize(st));
-  {
+  if (rebuild) {
     cudaGraph_t g = nullptr;
-    // count the kernel nodes of one iteration (for rs_report.gpu_launches)
-    {
-      cudaGraph_t g1 = nullptr;
-      RS_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
-      rs_status s1 = enqueue_iteration(o, nullptr);
-      cudaError_t ce1 = cudaStreamEndCapture(st, &g1);
-      if (s1 != RS_OK) {
-        if (g1) cudaGraphDestroy(g1);
-        return s1;
-      }
-      if (ce1 != cudaSuccess) return fail(RS_ECUDA, std::string("graph capture: ") + cudaGetErrorString(ce1));
-      size_t nn = 0;
-      cudaGraphGetNodes(g1, nullptr, &nn);
-      std::vector<cudaGraphNode_t> nodes(nn);
-      cudaGraphGetNodes(g1, nodes.data(), &nn);
-      kernels_per_iter = 0;
-      for (auto nd : nodes) {
-        cudaGraphNodeType t;
-        cudaGraphNodeGetType(nd, &t);
-        if (t == cudaGraphNodeTypeKernel) ++kernels_per_iter;
-      }
-      cudaGraphDestroy(g1);
-    }
     RS_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
     rs_status s = RS_OK;
-    for (int i = 0; i < chunk && s == RS_OK; ++i)
-      s = enqueue_iteration(o, o->profile ? &prof_events[(size_t)i * 2 * RS_K_NCLASSES] : nullptr);
+    auto evs = [&](int i) { return o->profile ? &prof_events[(size_t)i * 2 * RS_K_NCLASSES] : nullptr; };
+    for (int i = 0; i < chunk && s == RS_OK;) {
+      if (pipe) {   // group: precompute ns slots, then ns iterations on them
+        const int ns = std::min(P, chunk - i);
+        s = enqueue_precompute(o, ns, evs(i));
+        for (int q = 0; q < ns && s == RS_OK; ++q) s = enqueue_pipelined_iteration(o, q, evs(i + q));
+        i += ns;
+      } else {
+        s = enqueue_iteration(o, evs(i));
+        ++i;
+      }
+    }
     cudaError_t ce = cudaStreamEndCapture(st, &g);
     if (s != RS_OK) {
       if (g) cudaGraphDestroy(g);
       return s;
     }
     if (ce != cudaSuccess) return fail(RS_ECUDA, std::string("graph capture: ") + cudaGetErrorString(ce));
+    {   // kernel nodes per graph launch (rs_report.gpu_launches)
+      size_t nn = 0;
+      cudaGraphGetNodes(g, nullptr, &nn);
+      std::vector<cudaGraphNode_t> nodes(nn);
+      cudaGraphGetNodes(g, nodes.data(), &nn);
+      kernels_per_iter = 0;
+      for (auto nd : nodes) {
+        cudaGraphNodeType t;
+        cudaGraphNodeGetType(nd, &t);
+        if (t == cudaGraphNodeTypeKernel) ++kernels_per_iter;
+      }
+    }
     ce = cudaGraphInstantiate(&graph_exec, g, 0);
     cudaGraphDestroy(g);
     if (ce != cudaSuccess) return fail(RS_ECUDA, std::string("graph instantiate: ") + cudaGetErrorString(ce));
+    graph_key = key;
   }
   double kms[RS_K_NCLASSES] = {0};
   long long klaunch[RS_K_NCLASSES] = {0};
@@ -615,7 +755,7 @@ rs_status Problem::solve(const rs_solve_opts* o, double* w_out, rs_mem w_mem, do
     R.kernel_ms[cls] = kms[cls];
     R.kernel_launches[cls] = klaunch[cls];
   }
-  R.gpu_launches = graph_launches * chunk * kernels_per_iter;
+  R.gpu_launches = graph_launches * kernels_per_iter;   // kernel nodes per graph launch
   if (rep) *rep = R;
   if (o->trace && R.trace_len > 0)
     RS_CUDA(cudaMemcpy(o->trace, trace_dev, R.trace_len * 8, cudaMemcpyDeviceToHost));

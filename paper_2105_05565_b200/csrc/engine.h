@@ -19,6 +19,17 @@ rs_status create_csr(rs_problem* out, int64_t n, int64_t d, int64_t nnz_local, c
 
 struct CsrData;   // csr.cu
 
+// Launch parameters baked into the captured iteration graph (tol / max_iter live in Ctrl).
+struct GraphKey {
+  int kind = -1, tau = 0, ksum = 0, chunk = 0, profile = 0;
+  uint64_t seed = 0;
+  double gamma = 0.0, beta = 0.0;
+  bool operator==(const GraphKey& o) const {
+    return kind == o.kind && tau == o.tau && ksum == o.ksum && chunk == o.chunk &&
+           profile == o.profile && seed == o.seed && gamma == o.gamma && beta == o.beta;
+  }
+};
+
 struct Problem {
   // placement
   int device = -1, num_sms = 148;
@@ -51,7 +62,7 @@ struct Problem {
   double* scratch = nullptr;
   int last_status = 0;
   // per-(kind, tau) workspace
-  int ws_kind = -1, ws_tau = -1, ws_ksum = -1;
+  int ws_kind = -1, ws_tau = -1, ws_ksum = -1, ws_depth = -1;
   DevSketch sk{};
   double* XS = nullptr;
   long long ld_xs = 0;
@@ -68,17 +79,31 @@ struct Problem {
   double* uvec = nullptr;
   bool gram_fused = false;
   bool use_tma = true;
+  // sketch-ahead pipeline (bfactor.cu): P slots of (sketch, A S^T or Gram, Ginv, flag)
+  bool pipe = false;
+  int P = 0;
+  DevSketch skb{};
+  double* ASt_slots = nullptr;
+  long long as_stride = 0;
+  double* Gram_slots = nullptr;
+  long long gram_stride = 0;
+  double* Ginv_slots = nullptr;
+  long long ld_gi = 0, gi_stride = 0;
+  int* slot_flags = nullptr;
   SolveWork sw{};
   double* partials = nullptr;
   cudaGraphExec_t graph_exec = nullptr;
+  GraphKey graph_key{};
   std::vector<cudaEvent_t> prof_events;
-  long long kernels_per_iter = 0;   // counted while capturing one iteration
+  long long kernels_per_iter = 0;   // kernel nodes of one graph launch (chunk iterations)
 
   ~Problem();
   void free_workspace();
   rs_status allreduce(double* buf, size_t count);
-  rs_status ensure_workspace(int kind, int tau, int ksum);
+  rs_status ensure_workspace(int kind, int tau, int ksum, int depth);
   rs_status enqueue_iteration(const rs_solve_opts* o, cudaEvent_t* ev);
+  rs_status enqueue_precompute(const rs_solve_opts* o, int nslots, cudaEvent_t* ev);
+  rs_status enqueue_pipelined_iteration(const rs_solve_opts* o, int slot, cudaEvent_t* ev);
   rs_status solve(const rs_solve_opts* o, double* w_out, rs_mem w_mem, double* alpha_out,
                   rs_report* rep);
   rs_status write_weights(double* w_out, rs_mem w_mem, double* alpha_out);

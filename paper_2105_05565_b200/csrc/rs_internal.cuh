@@ -58,6 +58,17 @@ struct DevSketch {
   int* bucket;            // [len_cap]
   int* bptr;              // [tau + 1]
   int* cmap;              // [m] (count only)
+  // Batched sketches (pipelined modes): slot s of an array of sketches laid out with strides
+  // len (coord/sign/bucket), tau + 1 (bptr) and m (cmap).
+  __host__ __device__ DevSketch at(int s) const {
+    DevSketch o = *this;
+    o.coord += (long long)s * len;
+    o.sign += (long long)s * len;
+    o.bucket += (long long)s * len;
+    o.bptr += (long long)s * (tau + 1);
+    if (cmap) o.cmap += (long long)s * m;
+    return o;
+  }
 };
 
 // ---------------------------------------------------------------------------------------------
@@ -68,10 +79,15 @@ struct DevSketch {
 cudaError_t sketch_init();
 cudaError_t gemm_init();
 cudaError_t chol_init();
+cudaError_t update_init();
 
 // a1 sketch draw.  uses seed key and iteration k read from ctrl (or `fixed_k` >= 0 if given).
 cudaError_t launch_sketch(const DevSketch& sk, uint64_t seed, const Ctrl* ctrl, long long fixed_k,
                           cudaStream_t st);
+// Batched: slot s of `skb` (DevSketch::at) receives S_{k0 + s}, s < nslots, k0 = ctrl->k at launch
+// (or fixed_k >= 0).  One CTA per slot.
+cudaError_t launch_sketch_batch(const DevSketch& skb, int nslots, uint64_t seed, const Ctrl* ctrl,
+                                long long fixed_k, cudaStream_t st);
 size_t sketch_max_len(int kind, int m, int tau, int ksum);
 
 // a2 dense: XS[i, b] = sum_{e in b} sign_e X[i, coord_e],  i < rows, row-major ld_xs (>= tau, pad
@@ -81,6 +97,11 @@ cudaError_t launch_dense_xs(const double* X, long long ldx, long long rows, cons
 // a2 explicit: AS^T[b, :] = sum_{e in b} sign_e A[coord_e, :]  (A symmetric, m x m, ld lda).
 cudaError_t launch_explicit_rows(const double* A, long long lda, long long m, const DevSketch& sk,
                                  double* ASt, long long ld_as, const Ctrl* ctrl, cudaStream_t st);
+// Batched over `nslots` sketch slots: AS^T of slot s at ASt + s * as_stride.
+cudaError_t launch_explicit_rows_batch(const double* A, long long lda, long long m,
+                                       const DevSketch& skb, int nslots, double* ASt,
+                                       long long ld_as, long long as_stride, const Ctrl* ctrl,
+                                       cudaStream_t st);
 
 // a3 dense TN contraction on FP64 tensor cores (DMMA):  C[M' x N'] (row-major, ldc) =
 //   sum_{k < K} Aop[k, 0:M'] (x) Bop[k, 0:N']  with Aop row-major (lda), Bop row-major (ldb),
@@ -154,10 +175,42 @@ cudaError_t gram_init();
 cudaError_t launch_gram_fused(const double* X, long long ldx, long long rows, const DevSketch& sk,
                               double* partials, double* G, long long ldg, int num_sms,
                               const Ctrl* ctrl, cudaStream_t st);
+// explicit A, sketch with few entries (subsample / SubCount):
+//   u_j = sum_e sign_e delta[bucket_e] A[coord_e][j]  (= (A S delta)_j, A symmetric), then the update
+cudaError_t launch_update_rows(const double* A, long long lda, const DevSketch& sk,
+                               const double* delta, double* sdelta, double* w, double* dw,
+                               double* r, double* dr, long long m, double gamma, double beta,
+                               double* partials, Ctrl* ctrl, cudaStream_t st);
 // update with a dense u = X^T X S delta:  u_j + lambda sdelta_j  is A S delta
 cudaError_t launch_update_vec(const double* u, double lambda, double* sdelta, double* w, double* dw,
                               double* r, double* dr, long long m, double gamma, double beta,
                               double* partials, Ctrl* ctrl, cudaStream_t st);
+
+// ---------------------------------------------------------------------------------------------
+// Sketch-ahead pipeline (bfactor.cu).  G_k = S_k^T A S_k depends only on S_k (drawn from (seed, k),
+// P:L214) and on the data, never on the iterate, so for a group of P future iterations the
+// sketches, G_k and its factorisation are computed ahead in one batched pass (one CTA per G_k):
+//   G = L L^T (Cholesky, lower triangle read, R12), W = L^{-1}, Ginv = W^T W  (full tau x tau).
+// The iteration itself then needs only  delta = Ginv (S^T r).
+struct FactorSrc {
+  const double* ASt;      // AS^T slots (tau x ld_as each, slot stride as_stride), or null
+  long long ld_as, as_stride;
+  const double* Gram;     // Gram slots (XS)^T XS (tau x ld_gram, stride gram_stride), or null
+  long long ld_gram, gram_stride;
+  double lambda;          // Gram source: G = Gram + lambda S^T S
+  const double* A;        // explicit A (m x m, lda): G[a][c] = sum_{e in a, f in c} s_e s_f A[e][f]
+  long long lda;
+};
+int bfactor_max_tau();
+cudaError_t bfactor_init();
+// flags[s] = 1 if G of slot s was not SPD (a pivot <= 0 or non-finite after the empty-bucket rule)
+cudaError_t launch_bfactor(const FactorSrc& src, const DevSketch& skb, int nslots, double* Ginv,
+                           long long ldgi, long long gi_stride, int* flags, const Ctrl* ctrl,
+                           cudaStream_t st);
+// delta = Ginv (S^T r), sdelta[coord_e] = sign_e delta[bucket_e]; flag != 0 -> status NOTSPD.
+cudaError_t launch_apply_ginv(const double* Ginv, long long ldgi, const DevSketch& sk,
+                              const int* flag, const double* r, double* delta, double* sdelta,
+                              Ctrl* ctrl, cudaStream_t st);
 
 // misc
 // *out += number of non-finite entries of the rows x cols block.

@@ -223,7 +223,100 @@ k_update_vec(const double* __restrict__ u, double lambda, double* __restrict__ s
   }
 }
 
+// Explicit A, few sketch entries: block = 32 coordinates j x 32 entry slices; u_j =
+// sum_e sd_e A[coord_e][j] with sd_e = sign_e delta[bucket_e] staged in shared memory (rows of A are
+// contiguous: coalesced over j, L2-resident when A fits).
+constexpr int RW_Y = 32;
+__global__ void __launch_bounds__(32 * RW_Y)
+k_update_rows(const double* __restrict__ A, long long lda, DevSketch sk,
+              const double* __restrict__ delta, double* __restrict__ sdelta,
+              double* __restrict__ w, double* __restrict__ dw, double* __restrict__ r,
+              double* __restrict__ dr, long long m, double gamma, double beta,
+              double* __restrict__ partials, Ctrl* ctrl) {
+  if (ctrl->done) return;
+  if (ctrl->status >= ST_NOTSPD) {
+    if (blockIdx.x == 0 && threadIdx.x == 0 && threadIdx.y == 0) ctrl->done = 1;
+    return;
+  }
+  extern __shared__ double rw_sm[];   // [len] sd_e, then [len] coord_e (as int)
+  __shared__ double red[RW_Y][33];
+  __shared__ bool s_last;
+  const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * 32 + tx;
+  const int len = sk.bptr[sk.tau];
+  int* s_coord = reinterpret_cast<int*>(rw_sm + len);
+  for (int e = tid; e < len; e += 32 * RW_Y) {
+    const double dv = delta[sk.bucket[e]];
+    rw_sm[e] = sk.sign[e] > 0 ? dv : -dv;
+    s_coord[e] = sk.coord[e];
+  }
+  __syncthreads();
+  const long long j = (long long)blockIdx.x * 32 + tx;
+  double acc = 0.0;
+  if (j < m) {
+    const double* Aj = A + j;
+#pragma unroll 4
+    for (int e = ty; e < len; e += RW_Y) acc += rw_sm[e] * Aj[(long long)s_coord[e] * lda];
+  }
+  red[ty][tx] = acc;
+  __syncthreads();
+  if (ty == 0) {
+    double r2 = 0.0;
+    if (j < m) {
+      double u = 0.0;
+#pragma unroll
+      for (int q = 0; q < RW_Y; ++q) u += red[q][tx];
+      const double drj = beta * dr[j] - gamma * u;
+      const double rj = r[j] + drj;
+      dr[j] = drj;
+      r[j] = rj;
+      const double sd = sdelta[j];
+      sdelta[j] = 0.0;
+      const double dwj = beta * dw[j] - gamma * sd;
+      dw[j] = dwj;
+      w[j] += dwj;
+      r2 = rj * rj;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) r2 += __shfl_down_sync(0xffffffffu, r2, o);
+    if (tx == 0) {
+      partials[blockIdx.x] = r2;
+      __threadfence();
+      const unsigned prev = atomicAdd(&ctrl->arrive, 1u);
+      s_last = (prev == gridDim.x - 1);
+    }
+  }
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  double s = 0.0;
+  for (unsigned q = tid; q < gridDim.x; q += 32 * RW_Y) s += __ldcg(&partials[q]);
+  red[ty][tx] = s;
+  __syncthreads();
+  if (tid == 0) {
+    double tot = 0.0;
+    for (int q = 0; q < RW_Y; ++q)
+      for (int p = 0; p < 32; ++p) tot += red[q][p];
+    finish_iteration(ctrl, tot);
+  }
+}
+
 }  // namespace
+
+cudaError_t update_init() {
+  return cudaFuncSetAttribute(k_update_rows, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+}
+
+cudaError_t launch_update_rows(const double* A, long long lda, const DevSketch& sk,
+                               const double* delta, double* sdelta, double* w, double* dw,
+                               double* r, double* dr, long long m, double gamma, double beta,
+                               double* partials, Ctrl* ctrl, cudaStream_t st) {
+  const size_t smem = (size_t)sk.len * 12;
+  if (smem > 200 * 1024) return cudaErrorInvalidValue;
+  const unsigned g = (unsigned)((m + 31) / 32);
+  k_update_rows<<<g, dim3(32, RW_Y), smem, st>>>(A, lda, sk, delta, sdelta, w, dw, r, dr, m, gamma,
+                                                 beta, partials, ctrl);
+  return cudaGetLastError();
+}
 
 cudaError_t launch_update_vec(const double* u, double lambda, double* sdelta, double* w, double* dw,
                               double* r, double* dr, long long m, double gamma, double beta,

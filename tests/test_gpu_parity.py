@@ -115,6 +115,46 @@ def test_dense_ragged_parity(rs, kind, tau, k, mode):
     assert rel(r, ref["r"]) <= 1e-10
 
 
+@pytest.mark.parametrize("mode", ["implicit", "explicit", "gram"])
+def test_dense_count_empty_buckets(rs, mode):
+    """c1 shape with the count sketch (m = 50, tau = 10): ~5% of iterations have an empty bucket,
+    exercising the empty-bucket rule (R3) in every factorisation path."""
+    cfg = rsinputs.CONFIGS["c1"]
+    X, y = _dense(cfg.n, cfg.d, noise=cfg.noise)
+    w, r, rep = _run_gpu_dense(rs, X, y, cfg.lam, mode, "count", cfg.tau, 0.5, 60, seed=2)
+    ref = OV.solve(X, y, cfg.lam, "count", cfg.tau, 1.0, 0.5, 0.0, 60, seed=2)
+    assert rep["iterations"] == 60
+    assert rel(w, ref["w"]) <= 1e-10
+    assert rel(r, ref["r"]) <= 1e-10
+
+
+@pytest.mark.parametrize("mode", ["explicit", "gram"])
+@pytest.mark.parametrize("check_every", [1, 64, 300])
+def test_sketch_ahead_group_sizes(rs, mode, check_every):
+    """Sketch-ahead pipeline (bfactor.cu): groups of 1, 64 and > num_SMs slots (clamped) give the
+    oracle's iterates; 150 iterations cross several group and graph-launch boundaries."""
+    X, y = _dense(2000, 160, seed=7, col_decay=True, noise=0.01)
+    h = rs.rs_create_dense(X, y, 0.7, mode=mode)
+    try:
+        w, rep = rs.rs_solve(h, "subsample", 48, 1.0, 0.5, 0.0, 150, 11, check_every=check_every)
+        _, r = rs.rs_get_state(h)
+    finally:
+        rs.rs_destroy(h)
+    ref = OV.solve(X, y, 0.7, "subsample", 48, 1.0, 0.5, 0.0, 150, seed=11)
+    assert rep["iterations"] == 150
+    assert rel(w, ref["w"]) <= 1e-10
+    assert rel(r, ref["r"]) <= 1e-10
+
+
+def test_dense_identity_sketch_one_step_explicit(rs):
+    """S = I (tau = m): one step solves A w = b exactly through the batched factor."""
+    X, y = _dense(400, 64, seed=4)
+    w, r, rep = _run_gpu_dense(rs, X, y, 0.5, "explicit", "subsample", 64, 0.0, 1)
+    pr = OP.build(X, y, 0.5)
+    assert rel(w, OP.direct_solve(pr["A"], pr["b"])) <= 1e-11
+    assert np.linalg.norm(r) <= 1e-11 * np.linalg.norm(pr["b"])
+
+
 def test_dense_identity_sketch_one_step(rs):
     X, y = _dense(400, 64, seed=4)
     w, r, rep = _run_gpu_dense(rs, X, y, 0.5, "implicit", "subsample", 64, 0.0, 1)
