@@ -135,12 +135,30 @@ def run_reference(args):
 
 
 def _config_dict(cfg, args, world):
-    return {"workload": f"{cfg.name}: {'dense' if cfg.kind == 'dense' else 'CSR'} primal "
-                        f"{cfg.n}x{cfg.d}, {cfg.sketch} tau={cfg.tau}, gamma={cfg.gamma}, "
-                        f"beta={cfg.beta}, lambda={cfg.lam:g}, tol={cfg.tol:g}",
+    dual = cfg.d > cfg.n
+    if cfg.kind == "dense":
+        xb = cfg.n * cfg.d * 8
+        shape = "dense"
+    else:
+        xb = cfg.n * cfg.nnz_per_row * 12
+        shape = f"CSR ~{cfg.nnz_per_row} nnz/row" + (f", Zipf({cfg.zipf_a}) columns" if cfg.zipf_a
+                                                      else ", uniform columns, unit rows")
+    extra = f", k={cfg.subcount_k}" if cfg.sketch == "subcount" else ""
+    return {"workload": f"{cfg.name}: {shape} {'dual' if dual else 'primal'} {cfg.n}x{cfg.d}, "
+                        f"{cfg.sketch} tau={cfg.tau}{extra}, gamma={cfg.gamma}, beta={cfg.beta}, "
+                        f"lambda={cfg.lam:g}, tol={cfg.tol:g}",
             "as_mode": args.mode, "tau": cfg.tau, "n": cfg.n, "d": cfg.d,
-            "parallelism": f"X rows sharded over {world} GPU(s), NCCL allreduce of A S",
-            "l2": "inputs larger than L2 (X = %.2f GB > 126 MB)" % (cfg.n * cfg.d * 8 / 1e9)}
+            "parallelism": (f"X {'columns (features)' if dual else 'rows'} sharded over {world} "
+                            f"GPU(s), NCCL allreduce of the partial A S"),
+            "l2": "inputs larger than L2 (X = %.2f GB > 126 MB)" % (xb / 1e9)}
+
+
+def _csr_column_block(np, rowptr, colidx, vals, c0, clen):
+    """Columns [c0, c0 + clen) of a CSR matrix, with local column indices (dual feature shard)."""
+    keep = (colidx >= c0) & (colidx < c0 + clen)
+    ck = np.concatenate([[0], np.cumsum(keep, dtype=np.int64)])
+    rp = ck[rowptr].astype(np.int64)
+    return rp, (colidx[keep] - c0).astype(np.int32), vals[keep]
 
 
 # ------------------------------------------------------------------------------ our arm
@@ -164,24 +182,53 @@ def run_ours(args):
         tdist.broadcast_object_list(obj, src=0)
         uid = obj[0]
     cfg = rsinputs.CONFIGS[args.config]
-    assert cfg.kind == "dense", "bench drives the dense configs (c1, c2, c5)"
     stream = torch.cuda.current_stream()
-    Xd, yd = rsinputs.dense_problem(cfg.n, cfg.d, seed=0, col_decay=cfg.col_decay, noise=cfg.noise,
-                                    device="cuda")
-    b0, ln = rs.rs_shard_range(cfg.n, rank, world)
+    if args.mode is None:
+        args.mode = "gram" if cfg.kind == "dense" else "implicit"
+    if cfg.kind == "dense":
+        Xd, yd = rsinputs.dense_problem(cfg.n, cfg.d, seed=0, col_decay=cfg.col_decay,
+                                        noise=cfg.noise, device="cuda")
+        b0, ln = rs.rs_shard_range(cfg.n, rank, world)
+        if world > 1:
+            Xd = Xd[b0:b0 + ln].contiguous()
+            yd = yd[b0:b0 + ln].contiguous()
+        host = None
+    else:   # CSR (c3 primal: row shards balanced by nnz; c4 dual: feature (column) shards)
+        if cfg.zipf_a > 0:
+            rp, ci, va, yv = rsinputs.csr_zipf(cfg.n, cfg.d, cfg.nnz_per_row, a=cfg.zipf_a, seed=0)
+        else:
+            rp, ci, va, yv = rsinputs.csr_uniform(cfg.n, cfg.d, cfg.nnz_per_row, seed=0)
+        host = (rp, ci, va, yv)
+        dual = cfg.d > cfg.n
+        if dual:
+            b0, ln = rs.rs_shard_range(cfg.d, rank, world)
+            rp, ci, va = _csr_column_block(np, rp, ci, va, b0, ln)
+        else:
+            b0, ln = rs.rs_shard_rows_nnz(rp, rank, world)
+            e0, e1 = rp[b0], rp[b0 + ln]
+            rp, ci, va, yv = rp[b0:b0 + ln + 1] - e0, ci[e0:e1], va[e0:e1], yv[b0:b0 + ln]
+        Xd = (torch.from_numpy(np.ascontiguousarray(rp)).cuda(),
+              torch.from_numpy(np.ascontiguousarray(ci)).cuda(),
+              torch.from_numpy(np.ascontiguousarray(va)).cuda())
+        yd = torch.from_numpy(np.ascontiguousarray(yv)).cuda()
     if world > 1:
-        Xd = Xd[b0:b0 + ln].contiguous()
-        yd = yd[b0:b0 + ln].contiguous()
         dist = dict(device=local, rank=rank, world=world, nccl_unique_id=uid,
                     cuda_stream=stream.cuda_stream, shard_begin=b0, shard_len=ln)
     else:
         dist = dict(device=local, rank=0, world=1, cuda_stream=stream.cuda_stream,
-                    shard_begin=0, shard_len=cfg.n)
+                    shard_begin=0, shard_len=ln)
+
+    def create(X, y, borrow):
+        if cfg.kind == "dense":
+            return rs.rs_create_dense(X, y, cfg.lam, mode=args.mode, n=cfg.n, d=cfg.d,
+                                      borrow=borrow, dist=dist)
+        return rs.rs_create_csr(cfg.n, cfg.d, X[0], X[1], X[2], y, cfg.lam, mode=args.mode,
+                                dist=dist)
+
     torch.cuda.synchronize()
-    h = rs.rs_create_dense(Xd, yd, cfg.lam, mode=args.mode, n=cfg.n, d=cfg.d, borrow=True,
-                           dist=dist)
+    h = create(Xd, yd, True)
     common = dict(kind=cfg.sketch, tau=cfg.tau, gamma=cfg.gamma, beta=cfg.beta, seed=0,
-                  subcount_k=cfg.subcount_k)
+                  subcount_k=cfg.subcount_k, d=cfg.d)
 
     def barrier():
         if pg is not None:
@@ -234,7 +281,7 @@ def run_ours(args):
     dom = max(kms, key=lambda k: kms[k])
     as_ms = max(kms["as"] / max(kl["as"], 1), 1e-9)
     flops = 2.0 * cfg.n * cfg.d * cfg.tau / world
-    if args.mode == "implicit":
+    if args.mode == "implicit" and cfg.kind == "dense":
         achieved = flops / (as_ms * 1e-3) / 1e12
         roof = {"kernel": "a3 A S = X^T (X S) contraction (DMMA, split-K reduce, + lambda S)",
                 "bound": "tensor", "achieved": achieved, "peak": FP64_DMMA_PEAK, "unit": "TFLOP/s",
@@ -242,6 +289,19 @@ def run_ours(args):
                 "peak_source": "measured FP64 DMMA peak, profiles/r01_fp64_peak.txt "
                                "(MEASURED_PEAKS.json has no FP64 figure)",
                 "algorithmic_per_launch": f"{flops:.3e} flop (2 n d tau)",
+                "avg_launch_ms": as_ms, "share_of_step": kms["as"] / max(prof_ms, 1e-9)}
+    elif cfg.kind != "dense":
+        nnz = int(host[0][-1])
+        m = cfg.d if cfg.d <= cfg.n else cfg.n
+        byt = 2.0 * nnz * 12 / world + m * cfg.tau * 8.0
+        achieved = byt / (as_ms * 1e-3) / 1e9
+        peak = _peaks().get("hbm_gbs", 6556.5)
+        roof = {"kernel": ("a2+a3 CSR primal A S = X^T (X S) (warp per coordinate, CSC x CSR)"
+                           if m == cfg.d else "a2+a3 CSR dual A S = X (X^T S) (hashed z_b, warp per row)"),
+                "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": achieved / peak, "traffic": args.traffic,
+                "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy, burst)",
+                "algorithmic_per_launch": f"{byt:.3e} bytes (X as CSR + CSC read once, A S written)",
                 "avg_launch_ms": as_ms, "share_of_step": kms["as"] / max(prof_ms, 1e-9)}
     elif args.mode == "gram":
         byt = cfg.n / world * cfg.d * 8.0
@@ -277,12 +337,17 @@ def run_ours(args):
     # end to end through the public API from pinned host buffers (rank-local shard)
     e2e = None
     if not args.no_e2e:
-        Xh = Xd.cpu().pin_memory()
+        if cfg.kind == "dense":
+            Xh = Xd.cpu().pin_memory()
+        else:
+            Xh = tuple(t.cpu().pin_memory() for t in Xd)
         yh = yd.cpu().pin_memory()
+        h2d = sum(t.numel() * t.element_size() for t in (Xh if isinstance(Xh, tuple) else (Xh,)))
+        h2d += yh.numel() * 8
         barrier()
         e4, e5 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e4.record(stream)
-        h2 = rs.rs_create_dense(Xh, yh, cfg.lam, mode=args.mode, n=cfg.n, d=cfg.d, dist=dist)
+        h2 = create(Xh, yh, False)
         w, rep_e2e = rs.rs_solve(h2, tol=cfg.tol, max_iter=args.max_iter_tol, check_every=0,
                                  **common)
         e5.record(stream)
@@ -294,10 +359,10 @@ def run_ours(args):
             pg.all_reduce(t, op=pg.ReduceOp.MAX)
             e2e_ms = float(t.item())
         e2e = {"value": rep_e2e["iterations"] / (e2e_ms / 1e3), "unit": "iters/s",
-               "h2d_bytes_per_step": int(Xh.numel() * 8 + yh.numel() * 8),
+               "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(w.size * 8),
-               "step": "one public-API solve: rs_create_dense(pinned host X, y) + rs_solve to "
-                       "tol + w to host",
+               "step": "one public-API solve: rs_create_(dense|csr)(pinned host X, y) + rs_solve "
+                       "to tol + w to host",
                "seconds": e2e_ms / 1e3, "iterations": rep_e2e["iterations"]}
         del Xh, yh
 
@@ -305,19 +370,25 @@ def run_ours(args):
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         from oracle import solver as OV
-        X = Xd.cpu().numpy()
-        y = yd.cpu().numpy()
+        if host is None:
+            X = Xd.cpu().numpy()
+            y = yd.cpu().numpy()
+        else:
+            X = rsinputs.csr_to_scipy(host[0], host[1], host[2], cfg.n, cfg.d)
+            y = host[3]
         op = OV.Operator(X, y, cfg.lam, explicit=(args.mode == "explicit"))
-        OV.solve_momentum(op, cfg.sketch, cfg.tau, cfg.gamma, cfg.beta, 0.0, 1, seed=0)
+        kw = dict(seed=0, subcount_k=cfg.subcount_k)
+        OV.solve_momentum(op, cfg.sketch, cfg.tau, cfg.gamma, cfg.beta, 0.0, 1, **kw)
         t0 = time.perf_counter()
         n_it = 0
         while time.perf_counter() - t0 < args.cpu_seconds:
-            n_it += 3
-            OV.solve_momentum(op, cfg.sketch, cfg.tau, cfg.gamma, cfg.beta, 0.0, 3, seed=0)
+            n_it += 1
+            OV.solve_momentum(op, cfg.sketch, cfg.tau, cfg.gamma, cfg.beta, 0.0, 1, **kw)
         el = time.perf_counter() - t0
         cpu = {"value": n_it / el, "unit": "iters/s", "cores": os.cpu_count(), "kind": "oracle",
                "sample": f"{n_it} oracle Alg. 2 iterations of {cfg.name} (full X, NumPy/SciPy "
-                         f"fp64, BLAS on all host cores), {el:.1f} s"}
+                         f"fp64, BLAS on all host cores, 1 warm-up iteration excluded), "
+                         f"{el:.1f} s"}
         del X, y
 
     if rank == 0:
@@ -325,7 +396,8 @@ def run_ours(args):
             "metric": METRIC, "value": value, "unit": "iters/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": el_ms / args.steps,
             "higher_is_better": True, "scaling": "strong" if world > 1 else "weak",
-            "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, generated on device)",
+            "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded; DESIGN.md §5 recipe for BASELINE.json " + cfg.name + ")",
             "config": _config_dict(cfg, args, world),
             "time_to_tol_s": tol_ms / 1e3, "iterations_to_tol": rep_tol["iterations"],
             "converged": rep_tol["converged"], "rel_residual": rep_tol["rel_residual"],
@@ -347,7 +419,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c2")
-    ap.add_argument("--mode", default="implicit", choices=["implicit", "explicit", "gram"])
+    ap.add_argument("--mode", default=None, choices=["implicit", "explicit", "gram"],
+                    help="how A S is formed (default: gram for dense, implicit for CSR)")
     ap.add_argument("--max-iter-tol", type=int, default=20000)
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-e2e", action="store_true")

@@ -184,15 +184,28 @@ k_xpass_tma(const double* __restrict__ X, long long ldx, long long rows, long lo
   }
 }
 
-// u[j] = sum_c partials[c][j]  (fixed order)
-__global__ void k_xpass_reduce(const double* __restrict__ partials, int nparts, long long d,
-                               double* __restrict__ u, const Ctrl* ctrl) {
+// u[j] = sum_c partials[c][j]  (fixed order: 8 interleaved slices c = ty (mod 8) summed in
+// ascending c, then the slices in ascending ty).  Block: 32 coordinates x 8 slices.
+constexpr int XR_Y = 8;
+__global__ void __launch_bounds__(32 * XR_Y)
+k_xpass_reduce(const double* __restrict__ partials, int nparts, long long d,
+               double* __restrict__ u, const Ctrl* ctrl) {
   if (ctrl->done) return;
-  for (long long j = (long long)blockIdx.x * blockDim.x + threadIdx.x; j < d;
-       j += (long long)gridDim.x * blockDim.x) {
-    double s = 0.0;
-    for (int c = 0; c < nparts; ++c) s += partials[(long long)c * d + j];
-    u[j] = s;
+  __shared__ double red[XR_Y][33];
+  const int tx = threadIdx.x, ty = threadIdx.y;
+  const long long j = (long long)blockIdx.x * 32 + tx;
+  double s = 0.0;
+  if (j < d) {
+#pragma unroll 4
+    for (int c = ty; c < nparts; c += XR_Y) s += __ldcs(partials + (long long)c * d + j);
+  }
+  red[ty][tx] = s;
+  __syncthreads();
+  if (ty == 0 && j < d) {
+    double t = 0.0;
+#pragma unroll
+    for (int q = 0; q < XR_Y; ++q) t += red[q][tx];
+    u[j] = t;
   }
 }
 
@@ -273,16 +286,16 @@ k_gram_fused(const double* __restrict__ X, long long ldx, long long rows, DevSke
       const double* st = gsm + (kb % GF_STAGES) * GF_BK * GF_LD + acol;
 #pragma unroll
       for (int kk = 0; kk < GF_BK; kk += 4) {
-        double af[5], bf[5];
+        double bf[5];
         const double* rowp = st + (kk + arow) * GF_LD;
-#pragma unroll
-        for (int x = 0; x < 5; ++x) af[x] = rowp[I * 40 + x * 8];
 #pragma unroll
         for (int y = 0; y < 5; ++y) bf[y] = rowp[J * 40 + y * 8];
 #pragma unroll
-        for (int x = 0; x < 5; ++x)
+        for (int x = 0; x < 5; ++x) {   // one A fragment live at a time (register budget 128)
+          const double af = rowp[I * 40 + x * 8];
 #pragma unroll
-          for (int y = 0; y < 5; ++y) dmma_g(acc[x][y], af[x], bf[y]);
+          for (int y = 0; y < 5; ++y) dmma_g(acc[x][y], af, bf[y]);
+        }
       }
     }
   }
@@ -303,14 +316,16 @@ k_gram_fused(const double* __restrict__ X, long long ldx, long long rows, DevSke
   }
 }
 
-// G[a][b] = sum_c partials[c][a][b] for b <= a (fixed order)
+// G[a][b] = sum_c partials[c][a][b] for b <= a (fixed order: c ascending)
 __global__ void k_gram_reduce(const double* __restrict__ partials, int nparts, int tau,
                               double* __restrict__ G, long long ldg, const Ctrl* ctrl) {
   if (ctrl->done) return;
   const int a = blockIdx.x;
   for (int b = threadIdx.x; b <= a; b += blockDim.x) {
+    const double* p = partials + a * GF_MAXTAU + b;
     double s = 0.0;
-    for (int c = 0; c < nparts; ++c) s += partials[(long long)c * GF_MAXTAU * GF_MAXTAU + a * GF_MAXTAU + b];
+#pragma unroll 8
+    for (int c = 0; c < nparts; ++c) s += __ldcs(p + (long long)c * GF_MAXTAU * GF_MAXTAU);
     G[(long long)a * ldg + b] = s;
   }
 }
@@ -363,7 +378,7 @@ cudaError_t launch_xpass(const double* X, long long ldx, long long rows, long lo
   }
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
-  k_xpass_reduce<<<(unsigned)((d + 255) / 256), 256, 0, st>>>(partials, nc, d, u, ctrl);
+  k_xpass_reduce<<<(unsigned)((d + 31) / 32), dim3(32, XR_Y), 0, st>>>(partials, nc, d, u, ctrl);
   return cudaGetLastError();
 }
 
