@@ -19,27 +19,14 @@
 #include <algorithm>
 #include <string>
 
+#include "csr.h"
 #include "engine.h"
 #include "nccl_dl.h"
 #include "rs_internal.cuh"
 
 namespace rs {
 
-struct CsrData {
-  long long rows = 0, cols = 0, nnz = 0;   // local block: rows x cols
-  long long* rowptr = nullptr;
-  int* colidx = nullptr;
-  double* vals = nullptr;
-  long long* colptr = nullptr;   // CSC
-  int* rowidx = nullptr;
-  double* cvals = nullptr;
-  long long max_row_nnz = 0;
-  long long col_offset = 0;      // dual: first global feature of this rank's column block
-  // workspace
-  int* cmap_all = nullptr;       // primal: coordinate -> (bucket << 1 | neg) or -1
-  int hash_slots = 0, hash_log2 = 0, group = 0, chunks = 0;
-  size_t dual_smem = 0;
-};
+
 
 namespace {
 
@@ -265,6 +252,13 @@ k_csr_dual_as(const long long* __restrict__ rowptr, const int* __restrict__ coli
 
 }  // namespace
 
+cudaError_t launch_cmap_build(const DevSketch& sk, int* cmap_all, long long m, const Ctrl* ctrl,
+                              cudaStream_t st) {
+  k_cmap_clear<<<(unsigned)std::min<long long>((m + 255) / 256, 1024), 256, 0, st>>>(cmap_all, m, ctrl);
+  k_cmap_scatter<<<(sk.len + 255) / 256, 256, 0, st>>>(sk, cmap_all, ctrl);
+  return cudaGetLastError();
+}
+
 // ================================================================================================
 void Problem::csr_free() {
   if (!csr) return;
@@ -283,10 +277,12 @@ void Problem::csr_free_workspace() {
   if (!csr) return;
   dfree(csr->cmap_all);
   csr->cmap_all = nullptr;
+  csr_gram_free();
 }
 
 rs_status Problem::csr_ensure_workspace(int kind, int tau, int ksum) {
   (void)ksum;
+  if (mode == RS_AS_GRAM) return csr_gram_workspace(kind, tau);
   if (route == 1) {
     if (kind != SK_COUNT) RS_TRY(dalloc(&csr->cmap_all, m));
     const size_t smem = (size_t)P_WARPS * tau * sizeof(double);
@@ -394,7 +390,7 @@ rs_status create_csr(rs_problem* out, int64_t n, int64_t d, int64_t nnz_local, c
   if (route != RS_ROUTE_AUTO && route != RS_ROUTE_PRIMAL && route != RS_ROUTE_DUAL)
     return fail(RS_EINVAL, "bad route");
   if (mode == RS_AS_EXPLICIT) return fail(RS_EUNSUPPORTED, "explicit A with CSR X (SURVEY NEXT-3)");
-  if (mode != RS_AS_IMPLICIT) return fail(RS_EINVAL, "bad as_mode");
+  if (mode != RS_AS_IMPLICIT && mode != RS_AS_GRAM) return fail(RS_EINVAL, "bad as_mode");
   const int rt = route == RS_ROUTE_AUTO ? (d <= n ? 1 : 2) : (route == RS_ROUTE_PRIMAL ? 1 : 2);
   RS_TRY(validate_dist(dist, rt == 1 ? n : d));
   const long long rows = rt == 1 ? (dist ? dist->shard_len : n) : n;

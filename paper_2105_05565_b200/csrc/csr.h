@@ -1,0 +1,41 @@
+// CSR-X data of a problem (internal; csr.cu, csr_gram.cu).
+#pragma once
+#include <cuda_runtime.h>
+
+#include "rs_internal.cuh"
+
+namespace rs {
+
+struct CsrData {
+  long long rows = 0, cols = 0, nnz = 0;   // local block: rows x cols
+  long long* rowptr = nullptr;
+  int* colidx = nullptr;
+  double* vals = nullptr;
+  long long* colptr = nullptr;   // CSC
+  int* rowidx = nullptr;
+  double* cvals = nullptr;
+  long long max_row_nnz = 0;
+  long long col_offset = 0;      // dual: first global feature of this rank's column block
+  // workspace
+  int* cmap_all = nullptr;       // coordinate -> (bucket << 1 | neg) or -1 (subsample / SubCount)
+  int hash_slots = 0, hash_log2 = 0, group = 0, chunks = 0;
+  size_t dual_smem = 0;
+  // GRAM mode (csr_gram.cu): the hashed rows of R = X (primal) or X^T (dual), the band plan of
+  // the lower triangle of (RS)^T (RS), and the two SpMV vectors
+  int* hb = nullptr;             // [nnz] bucket of the k-th merged entry of a row (ascending)
+  double* hv = nullptr;          // [nnz] its value sum_{j in row, h(j) = b} sign_j R_ij
+  int* hcnt = nullptr;           // [R rows] merged entries per row
+  int* band_a0 = nullptr;        // [nbands + 1] first G row of every band
+  long long* chunk_r0 = nullptr; // [nchunks + 1] first R row of every chunk (nnz-balanced)
+  int nbands = 0, nchunks = 0;
+  double* gpart = nullptr;       // [nchunks][tau (tau + 1) / 2] packed lower-triangle partials
+  long long gpart_stride = 0;
+  double* tvec = nullptr;        // [R rows]  t = R (S delta)
+  size_t hr_smem = 0, gb_smem = 0;
+};
+
+// per-iteration map coordinate -> (bucket << 1 | neg), -1 outside the sketch (subsample / SubCount)
+cudaError_t launch_cmap_build(const DevSketch& sk, int* cmap_all, long long m, const Ctrl* ctrl,
+                              cudaStream_t st);
+
+}  // namespace rs

@@ -369,7 +369,8 @@ rs_status Problem::ensure_workspace(int kind, int tau, int ksum, int depth) {
   RS_TRY(dalloc(&sk.bucket, L));
   RS_TRY(dalloc(&sk.bptr, tau + 1));
   if (kind == SK_COUNT) RS_TRY(dalloc(&sk.cmap, m));
-  if (fmt == 1) {   // CSR: AS row-major m x tau
+  if (fmt == 1 && mode == RS_AS_GRAM) {   // CSR GRAM: buffers in csr_gram_workspace
+  } else if (fmt == 1) {   // CSR: AS row-major m x tau
     ld_as = round_up(tau, 4);
     RS_TRY(dalloc(&ASt, (size_t)m * ld_as));
   } else if (depth > 0 && mode == RS_AS_EXPLICIT) {   // pipelined explicit: A S^T per slot
@@ -453,6 +454,7 @@ rs_status Problem::enqueue_iteration(const rs_solve_opts* o, cudaEvent_t* ev) {
   mark(RS_K_SKETCH, 0);
   RS_CUDA(launch_sketch(sk, o->seed, ctrl, -1, st));                       // a1
   mark(RS_K_SKETCH, 1);
+  if (fmt == 1 && mode == RS_AS_GRAM) return csr_enqueue_gram(o, ev);
   if (fmt == 0 && mode == RS_AS_GRAM) {
     if (!gram_fused) {
       mark(RS_K_XS, 0);

@@ -113,6 +113,10 @@ struct Problem {
   rs_status csr_ensure_workspace(int kind, int tau, int ksum);
   rs_status csr_enqueue_as(const rs_solve_opts* o, cudaEvent_t* ev);
   rs_status csr_dual_weights(double* w_out, cudaMemcpyKind kd);
+  // CSR GRAM mode (csr_gram.cu)
+  void csr_gram_free();
+  rs_status csr_gram_workspace(int kind, int tau);
+  rs_status csr_enqueue_gram(const rs_solve_opts* o, cudaEvent_t* ev);
 };
 
 rs_status finish_setup(Problem* p);

@@ -229,11 +229,12 @@ def _csr_primal(n=4000, d=600, per_row=12, seed=1):
 
 @pytest.mark.parametrize("kind,tau,k", [("count", 40, 0), ("subsample", 33, 0), ("subcount", 20, 3),
                                         ("count", 599, 0)])
-def test_csr_primal_parity(rs, kind, tau, k):
+@pytest.mark.parametrize("mode", ["implicit", "gram"])
+def test_csr_primal_parity(rs, kind, tau, k, mode):
     n, d = 4000, 600
     rp, ci, v, y, Xs = _csr_primal(n, d)
     lam = 1e-2
-    h = rs.rs_create_csr(n, d, rp, ci, v, y, lam)
+    h = rs.rs_create_csr(n, d, rp, ci, v, y, lam, mode=mode)
     try:
         w, rep = rs.rs_solve(h, kind, tau, 1.0, 0.5, 0.0, 15, seed=2, subcount_k=k)
         ws, r = rs.rs_get_state(h)
@@ -244,13 +245,15 @@ def test_csr_primal_parity(rs, kind, tau, k):
     assert rel(r, ref["r"]) <= 1e-10
 
 
-@pytest.mark.parametrize("kind,tau,k", [("subcount", 16, 4), ("subsample", 25, 0), ("count", 12, 0)])
-def test_csr_dual_parity(rs, kind, tau, k):
+@pytest.mark.parametrize("kind,tau,k", [("subcount", 16, 4), ("subsample", 25, 0), ("count", 12, 0),
+                                        ("subcount", 240, 1)])
+@pytest.mark.parametrize("mode", ["implicit", "gram"])
+def test_csr_dual_parity(rs, kind, tau, k, mode):
     n, d = 300, 5000
     rp, ci, v, y = rsinputs.csr_zipf(n, d, 60, a=1.1, seed=3)
     Xs = rsinputs.csr_to_scipy(rp, ci, v, n, d)
     lam = 1e-1
-    h = rs.rs_create_csr(n, d, rp, ci, v, y, lam)
+    h = rs.rs_create_csr(n, d, rp, ci, v, y, lam, mode=mode)
     try:
         w, rep = rs.rs_solve(h, kind, tau, 1.0, 0.5, 0.0, 15, seed=4, subcount_k=k, d=d, alpha=True)
         alpha, r = rs.rs_get_state(h)
@@ -264,12 +267,13 @@ def test_csr_dual_parity(rs, kind, tau, k):
     assert rel(w, ref["weights"]) <= 1e-10
 
 
-def test_csr_dual_converges_to_direct(rs):
+@pytest.mark.parametrize("mode", ["implicit", "gram"])
+def test_csr_dual_converges_to_direct(rs, mode):
     n, d = 120, 2000
     rp, ci, v, y = rsinputs.csr_zipf(n, d, 40, a=1.1, seed=5)
     Xs = rsinputs.csr_to_scipy(rp, ci, v, n, d)
     lam = 1.0
-    h = rs.rs_create_csr(n, d, rp, ci, v, y, lam)
+    h = rs.rs_create_csr(n, d, rp, ci, v, y, lam, mode=mode)
     try:
         w, rep = rs.rs_solve(h, "subcount", 12, 1.0, 0.5, 1e-12, 200000, seed=1, subcount_k=4, d=d)
     finally:
@@ -298,5 +302,23 @@ def test_config2_full_size_sampled(rs, mode):
     X, y = Xd.cpu().numpy(), yd.cpu().numpy()
     del Xd, yd
     ref = OV.solve(X, y, cfg.lam, "subsample", cfg.tau, 1.0, cfg.beta, 0.0, 3, seed=0)
+    assert rel(w, ref["w"]) <= 1e-10
+    assert rel(r, ref["r"]) <= 1e-10
+
+
+@pytest.mark.parametrize("kind,tau,k", [("count", 64, 0), ("subsample", 150, 0), ("subcount", 50, 4)])
+@pytest.mark.parametrize("mode", ["implicit", "gram"])
+def test_csr_primal_long_rows(rs, kind, tau, k, mode):
+    """Rows longer than a warp (c3 has ~50 non-zeros per row): multi-chunk merge of equal buckets."""
+    n, d = 3000, 400
+    rp, ci, v, y, Xs = _csr_primal(n, d, per_row=70, seed=7)
+    lam = 1e-2
+    h = rs.rs_create_csr(n, d, rp, ci, v, y, lam, mode=mode)
+    try:
+        w, rep = rs.rs_solve(h, kind, tau, 1.0, 0.5, 0.0, 12, seed=3, subcount_k=k)
+        ws, r = rs.rs_get_state(h)
+    finally:
+        rs.rs_destroy(h)
+    ref = OV.solve(Xs, y, lam, kind, tau, 1.0, 0.5, 0.0, 12, seed=3, subcount_k=k)
     assert rel(w, ref["w"]) <= 1e-10
     assert rel(r, ref["r"]) <= 1e-10
