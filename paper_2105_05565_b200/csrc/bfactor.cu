@@ -268,10 +268,28 @@ k_bfactor_small(FactorSrc src, DevSketch skb, double* __restrict__ Ginv, long lo
   if (tid == 0) flags[slot] = 0;
 }
 
-// delta = Ginv g, g = S^T r; one warp per row of Ginv.
+// g = S^T r: one warp per bucket (lanes over the bucket's entries, fixed-order reduction).
+__global__ void __launch_bounds__(AG_WARPS * 32)
+k_sketch_g(DevSketch sk, const int* __restrict__ flag, const double* __restrict__ r,
+           double* __restrict__ g, const Ctrl* ctrl) {
+  if (ctrl->done || *flag) return;
+  const int lane = threadIdx.x & 31;
+  const int b = blockIdx.x * AG_WARPS + (threadIdx.x >> 5);
+  if (b >= sk.tau) return;
+  double v = 0.0;
+  for (int e = sk.bptr[b] + lane; e < sk.bptr[b + 1]; e += 32) {
+    const double x = r[sk.coord[e]];
+    v += sk.sign[e] > 0 ? x : -x;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  if (lane == 0) g[b] = v;
+}
+
+// delta = Ginv g; one warp per row of Ginv.
 __global__ void __launch_bounds__(AG_WARPS * 32)
 k_apply_ginv(const double* __restrict__ Ginv, long long ldgi, DevSketch sk,
-             const int* __restrict__ flag, const double* __restrict__ r, double* __restrict__ delta,
+             const int* __restrict__ flag, const double* __restrict__ gv, double* __restrict__ delta,
              double* __restrict__ sdelta, Ctrl* ctrl) {
   if (ctrl->done) return;
   if (*flag) {   // the update kernel of this iteration turns the status into `done`
@@ -280,14 +298,7 @@ k_apply_ginv(const double* __restrict__ Ginv, long long ldgi, DevSketch sk,
   }
   __shared__ double g[AG_MAXTAU];
   const int tau = sk.tau, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  for (int b = tid; b < tau; b += AG_WARPS * 32) {
-    double v = 0.0;
-    for (int e = sk.bptr[b]; e < sk.bptr[b + 1]; ++e) {
-      const double x = r[sk.coord[e]];
-      v += sk.sign[e] > 0 ? x : -x;
-    }
-    g[b] = v;
-  }
+  for (int b = tid; b < tau; b += AG_WARPS * 32) g[b] = gv[b];
   __syncthreads();
   const int a = blockIdx.x * AG_WARPS + warp;
   if (a >= tau) return;
@@ -301,9 +312,260 @@ k_apply_ginv(const double* __restrict__ Ginv, long long ldgi, DevSketch sk,
     sdelta[sk.coord[e]] = sk.sign[e] > 0 ? s : -s;
 }
 
+// =================================================================================================
+// Large tau (BF_MAXTAU < tau <= BB_MAXTAU): the same three steps with G held in global memory (a
+// per-slot work matrix, zero-padded to whole 32 x 32 tiles with an identity tail so that every tile
+// is full), one CTA of 16 warps per slot, every tile product on DMMA (one warp per 32 x 32 tile):
+//   Cholesky   right-looking over block columns p: warp 0 factors L_pp in registers and forms
+//              L_pp^{-1}; panel L_ip = G_ip L_pp^{-T}; trailing G_ij -= L_ip L_jp^T (j <= i)
+//   W = L^{-1} block columns J from the last: T_I = sum_{K=J+1..I} W_IK L_KJ, W_IJ = -T_I W_JJ
+//   Ginv       = W^T W, block (I, J) = sum_{K >= I} W_KI^T W_KJ, mirrored into the full slot
+constexpr int BB_THREADS = 512;
+constexpr int BB_WARPS = BB_THREADS / 32;
+constexpr int BB_MAXTAU = 4096;
+
+__host__ __device__ __forceinline__ int bb_tp(int tau) { return (tau + 31) / 32 * 32; }
+
+// acc[R][C] (8 x 8 blocks of a 32 x 32 tile) += op(A) op(B) (op(A) scaled by `sign`), with
+// op(A)[r][k] = TA ? A[k][r] : A[r][k] and op(B)[k][c] = TB ? B[c][k] : B[k][c]; A has leading
+// dimension lda, B ldb (row-major).
+template <bool TA, bool TB>
+__device__ __forceinline__ void mma_tile(double (&acc)[4][4][2], const double* A, int lda,
+                                         const double* B, int ldb, int lane, double sign) {
+  const int q = lane >> 2, k4 = lane & 3;
+#pragma unroll 2
+  for (int K = 0; K < 8; ++K) {
+    double a[4], b[4];
+#pragma unroll
+    for (int R = 0; R < 4; ++R) {
+      const int r = 8 * R + q, k = 4 * K + k4;
+      a[R] = sign * (TA ? A[(long long)k * lda + r] : A[(long long)r * lda + k]);
+    }
+#pragma unroll
+    for (int C = 0; C < 4; ++C) {
+      const int c = 8 * C + q, k = 4 * K + k4;
+      b[C] = TB ? B[(long long)c * ldb + k] : B[(long long)k * ldb + c];
+    }
+#pragma unroll
+    for (int R = 0; R < 4; ++R)
+#pragma unroll
+      for (int C = 0; C < 4; ++C) dmma(acc[R][C], a[R], b[C]);
+  }
+}
+__device__ __forceinline__ void acc_load(double (&acc)[4][4][2], const double* Ct, int ld, int lane) {
+  const int q = lane >> 2, k4 = lane & 3;
+#pragma unroll
+  for (int R = 0; R < 4; ++R)
+#pragma unroll
+    for (int C = 0; C < 4; ++C) {
+      const double* p = Ct + (long long)(8 * R + q) * ld + 8 * C + 2 * k4;
+      acc[R][C][0] = p[0];
+      acc[R][C][1] = p[1];
+    }
+}
+__device__ __forceinline__ void acc_zero(double (&acc)[4][4][2]) {
+#pragma unroll
+  for (int R = 0; R < 4; ++R)
+#pragma unroll
+    for (int C = 0; C < 4; ++C) acc[R][C][0] = acc[R][C][1] = 0.0;
+}
+__device__ __forceinline__ void acc_store(const double (&acc)[4][4][2], double* Ct, int ld, int lane) {
+  const int q = lane >> 2, k4 = lane & 3;
+#pragma unroll
+  for (int R = 0; R < 4; ++R)
+#pragma unroll
+    for (int C = 0; C < 4; ++C) {
+      double* p = Ct + (long long)(8 * R + q) * ld + 8 * C + 2 * k4;
+      p[0] = acc[R][C][0];
+      p[1] = acc[R][C][1];
+    }
+}
+
+// Diagonal tile p (warp 0): L_pp in registers (lane i = row i, right-looking), written back over
+// the tile; L_pp^{-1} (lane j = column j, forward substitution) written to Di (32 x 32 row-major,
+// zeros above the diagonal).  Returns false if a pivot was <= 0 or non-finite.
+__device__ __noinline__ bool diag_factor(double* D, int ld, double* Di, double (*sL)[33], int lane) {
+  bool bad = false;
+  double v[32];
+#pragma unroll
+  for (int k = 0; k < 32; ++k) v[k] = k <= lane ? D[(long long)lane * ld + k] : 0.0;
+#pragma unroll
+  for (int j = 0; j < 32; ++j) {
+    double d = __shfl_sync(0xffffffffu, v[j], j);
+    if (!(d > 0.0) || !isfinite(d)) {
+      bad = true;
+      d = 1.0;
+    }
+    const double ljj = sqrt(d), inv = 1.0 / ljj;
+    if (lane == j) v[j] = ljj;
+    else if (lane > j) v[j] *= inv;
+    const double lij = lane > j ? v[j] : 0.0;
+#pragma unroll
+    for (int k = j + 1; k < 32; ++k) v[k] -= lij * __shfl_sync(0xffffffffu, lij, k);
+  }
+#pragma unroll
+  for (int k = 0; k < 32; ++k) {
+    const double x = k <= lane ? v[k] : 0.0;
+    D[(long long)lane * ld + k] = x;
+    sL[lane][k] = x;
+  }
+  __syncwarp();
+#pragma unroll 1
+  for (int i = 0; i < 32; ++i) {   // column `lane` of L^{-1}: x_i, reusing v as x
+    double s = (i == lane) ? 1.0 : 0.0;
+#pragma unroll
+    for (int k = 0; k < 32; ++k)
+      if (k < i) s -= sL[i][k] * Di[k * 32 + lane];
+    Di[i * 32 + lane] = i < lane ? 0.0 : s / sL[i][i];
+    __syncwarp();
+  }
+  return bad;
+}
+
+__global__ void __launch_bounds__(BB_THREADS, 1)
+k_bfactor_big(FactorSrc src, DevSketch skb, double* __restrict__ Ginv, long long ldgi,
+              long long gi_stride, double* work, long long work_stride, int* __restrict__ flags,
+              const Ctrl* ctrl) {
+  if (ctrl && ctrl->done) return;
+  __shared__ double sL[32][33];
+  __shared__ int s_bad;
+  const int slot = blockIdx.x;
+  const DevSketch sk = skb.at(slot);
+  const int tau = sk.tau, tp = bb_tp(tau), Tc = tp / 32;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  double* Wm = work + slot * work_stride;           // tp x tp, row-major
+  double* dinv = Wm + (long long)tp * tp;           // Tc tiles 32 x 32 (L_pp^{-1})
+  double* tmp = dinv + (long long)Tc * 1024;        // Tc tiles (T_I)
+  auto T = [&](int I, int J) { return Wm + (long long)(32 * I) * tp + 32 * J; };
+  if (tid == 0) s_bad = 0;
+
+  // ---- a4: lower triangle of G (R3 empty-bucket rule), identity on the padding
+  const double* ASt = src.ASt ? src.ASt + slot * src.as_stride : nullptr;
+  const double* Gram = src.Gram ? src.Gram + slot * src.gram_stride : nullptr;
+  for (int a = warp; a < tp; a += BB_WARPS) {
+    const int a32 = a & ~31;
+    const int e0 = a < tau ? sk.bptr[a] : 0, e1 = a < tau ? sk.bptr[a + 1] : 0;
+    for (int c = lane; c < a32 + 32; c += 32) {   // every lower tile of row a
+      double v = 0.0;
+      if (a >= tau || c >= tau || c > a) {
+        v = (a == c) ? 1.0 : 0.0;
+      } else if (Gram) {
+        v = Gram[(long long)a * src.ld_gram + c];
+        if (a == c) v += src.lambda * (double)(e1 - e0);
+      } else if (!ASt) {
+        const int f0 = sk.bptr[c], f1 = sk.bptr[c + 1];
+        for (int e = e0; e < e1; ++e) {
+          const double* Ae = src.A + (long long)sk.coord[e] * src.lda;
+          double t = 0.0;
+          for (int f = f0; f < f1; ++f) {
+            const double x = Ae[sk.coord[f]];
+            t += sk.sign[f] > 0 ? x : -x;
+          }
+          v += sk.sign[e] > 0 ? t : -t;
+        }
+      } else {
+        const double* col = ASt + (long long)c * src.ld_as;
+        for (int e = e0; e < e1; ++e) {
+          const double x = col[sk.coord[e]];
+          v += sk.sign[e] > 0 ? x : -x;
+        }
+      }
+      if (a < tau && c < tau && c <= a && (e0 == e1 || sk.bptr[c] == sk.bptr[c + 1]))
+        v = (a == c) ? 1.0 : 0.0;
+      Wm[(long long)a * tp + c] = v;
+    }
+  }
+  __syncthreads();
+
+  double acc[4][4][2];
+  // ---- a5: Cholesky G = L L^T
+  for (int p = 0; p < Tc; ++p) {
+    if (warp == 0) {
+      const bool bad = diag_factor(T(p, p), tp, dinv + (long long)p * 1024, sL, lane);
+      if (bad && lane == 0) s_bad = 1;
+    }
+    __syncthreads();
+    // panel: L_ip = G_ip (L_pp^{-1})^T, in place (the warp reads its whole tile before storing)
+    for (int i = p + 1 + warp; i < Tc; i += BB_WARPS) {
+      acc_zero(acc);
+      mma_tile<false, true>(acc, T(i, p), tp, dinv + (long long)p * 1024, 32, lane, 1.0);
+      acc_store(acc, T(i, p), tp, lane);
+    }
+    __syncthreads();
+    // trailing: G_ij -= L_ip L_jp^T, p < j <= i
+    {
+      const int nt = Tc - 1 - p, ntiles = nt * (nt + 1) / 2;
+      for (int t = warp; t < ntiles; t += BB_WARPS) {
+        int Ii, Jj;
+        tri_decode(t, Ii, Jj);
+        const int i = p + 1 + Ii, j = p + 1 + Jj;
+        acc_load(acc, T(i, j), tp, lane);
+        mma_tile<false, true>(acc, T(i, p), tp, T(j, p), tp, lane, -1.0);
+        acc_store(acc, T(i, j), tp, lane);
+      }
+    }
+    __syncthreads();
+  }
+  if (s_bad) {
+    if (tid == 0) flags[slot] = 1;
+    return;
+  }
+  // ---- W = L^{-1}, block columns J = Tc-1 .. 0 (W_IK final for K > J; L_KJ still L)
+  for (int J = Tc - 1; J >= 0; --J) {
+    for (int I = J + 1 + warp; I < Tc; I += BB_WARPS) {
+      acc_zero(acc);
+      for (int K = J + 1; K <= I; ++K) mma_tile<false, false>(acc, T(I, K), tp, T(K, J), tp, lane, 1.0);
+      acc_store(acc, tmp + (long long)I * 1024, 32, lane);
+    }
+    __syncthreads();
+    // W_IJ = -T_I W_JJ over L_IJ;  W_JJ = L_JJ^{-1} over L_JJ
+    for (int I = J + 1 + warp; I < Tc; I += BB_WARPS) {
+      acc_zero(acc);
+      mma_tile<false, false>(acc, tmp + (long long)I * 1024, 32, dinv + (long long)J * 1024, 32, lane,
+                             -1.0);
+      acc_store(acc, T(I, J), tp, lane);
+    }
+    if (warp == BB_WARPS - 1) {
+      const double* Wjj = dinv + (long long)J * 1024;
+      double* D = T(J, J);
+      for (int q = lane; q < 1024; q += 32) D[(long long)(q >> 5) * tp + (q & 31)] = Wjj[q];
+    }
+    __syncthreads();
+  }
+  // ---- Ginv = W^T W (block (I, J), J <= I), mirrored
+  double* Gi = Ginv + slot * gi_stride;
+  const int npairs = Tc * (Tc + 1) / 2;
+  for (int t = warp; t < npairs; t += BB_WARPS) {
+    int I, J;
+    tri_decode(t, I, J);
+    acc_zero(acc);
+    for (int K = I; K < Tc; ++K) mma_tile<true, false>(acc, T(K, I), tp, T(K, J), tp, lane, 1.0);
+    const int q = lane >> 2, k4 = lane & 3;
+#pragma unroll
+    for (int R = 0; R < 4; ++R)
+#pragma unroll
+      for (int C = 0; C < 4; ++C)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int row = 32 * I + 8 * R + q, col = 32 * J + 8 * C + 2 * k4 + h;
+          if (row < tau && col < tau) {
+            Gi[(long long)row * ldgi + col] = acc[R][C][h];
+            if (I != J) Gi[(long long)col * ldgi + row] = acc[R][C][h];
+          }
+        }
+  }
+  if (tid == 0) flags[slot] = 0;
+}
+
 }  // namespace
 
-int bfactor_max_tau() { return BF_MAXTAU; }
+int bfactor_max_tau() { return BB_MAXTAU; }
+
+size_t bfactor_work_elems(int tau) {
+  if (tau <= BF_MAXTAU) return 0;
+  const long long tp = bb_tp(tau);
+  return (size_t)(tp * tp + 2 * (tp / 32) * 1024);
+}
 
 cudaError_t bfactor_init() {
   return cudaFuncSetAttribute(k_bfactor_small, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -311,20 +573,27 @@ cudaError_t bfactor_init() {
 }
 
 cudaError_t launch_bfactor(const FactorSrc& src, const DevSketch& skb, int nslots, double* Ginv,
-                           long long ldgi, long long gi_stride, int* flags, const Ctrl* ctrl,
-                           cudaStream_t st) {
-  if (skb.tau > BF_MAXTAU || nslots < 1) return cudaErrorInvalidValue;
+                           long long ldgi, long long gi_stride, int* flags, double* work,
+                           const Ctrl* ctrl, cudaStream_t st) {
+  if (skb.tau > BB_MAXTAU || nslots < 1) return cudaErrorInvalidValue;
+  if (skb.tau > BF_MAXTAU) {
+    if (!work) return cudaErrorInvalidValue;
+    k_bfactor_big<<<nslots, BB_THREADS, 0, st>>>(src, skb, Ginv, ldgi, gi_stride, work,
+                                                 (long long)bfactor_work_elems(skb.tau), flags, ctrl);
+    return cudaGetLastError();
+  }
   k_bfactor_small<<<nslots, BF_THREADS, bf_smem(skb.tau), st>>>(src, skb, Ginv, ldgi, gi_stride,
                                                                  flags, ctrl);
   return cudaGetLastError();
 }
 
 cudaError_t launch_apply_ginv(const double* Ginv, long long ldgi, const DevSketch& sk,
-                              const int* flag, const double* r, double* delta, double* sdelta,
-                              Ctrl* ctrl, cudaStream_t st) {
+                              const int* flag, const double* r, double* gbuf, double* delta,
+                              double* sdelta, Ctrl* ctrl, cudaStream_t st) {
   if (sk.tau > AG_MAXTAU) return cudaErrorInvalidValue;
   const unsigned grid = (unsigned)((sk.tau + AG_WARPS - 1) / AG_WARPS);
-  k_apply_ginv<<<grid, AG_WARPS * 32, 0, st>>>(Ginv, ldgi, sk, flag, r, delta, sdelta, ctrl);
+  k_sketch_g<<<grid, AG_WARPS * 32, 0, st>>>(sk, flag, r, gbuf, ctrl);
+  k_apply_ginv<<<grid, AG_WARPS * 32, 0, st>>>(Ginv, ldgi, sk, flag, gbuf, delta, sdelta, ctrl);
   return cudaGetLastError();
 }
 

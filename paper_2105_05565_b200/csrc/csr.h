@@ -31,6 +31,11 @@ struct CsrData {
   double* gpart = nullptr;       // [nchunks][tau (tau + 1) / 2] packed lower-triangle partials
   long long gpart_stride = 0;
   double* tvec = nullptr;        // [R rows]  t = R (S delta)
+  // rows longer than `heavy` are handled one CTA per row (Zipf-popular features of c4)
+  long long heavyR = 0, heavyRt = 0;
+  int* heavy_rowsR = nullptr;
+  int* heavy_rowsRt = nullptr;
+  int nheavyR = 0, nheavyRt = 0;
   size_t hr_smem = 0, gb_smem = 0;
 };
 

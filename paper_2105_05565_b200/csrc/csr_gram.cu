@@ -44,86 +44,148 @@ constexpr int GB_BUDGET = 26624;   // doubles of one band (208 KB of shared memo
 __host__ __device__ __forceinline__ long long tri(long long a) { return a * (a + 1) / 2; }
 
 // ------------------------------------------------------------------------------------ stage 1
+// Per-warp merge state in shared memory: acc[tau] (values), stage[32], bits[ceil(tau/32)] (touched).
+struct WarpMerge {
+  double* acc;
+  double* stage;
+  unsigned* bits;
+  int nw;
+  __device__ WarpMerge(double* hsm, int tau, int w) {
+    nw = (tau + 31) >> 5;
+    acc = hsm + (size_t)w * tau;
+    stage = hsm + (size_t)HR_WARPS * tau + w * 32;
+    bits = reinterpret_cast<unsigned*>(hsm + (size_t)HR_WARPS * (tau + 32)) + w * nw;
+  }
+  // one entry per lane (cm < 0: none); equal buckets summed by the group leader in lane order
+  __device__ __forceinline__ void add(int cm, double x, int lane) {
+    if (!__ballot_sync(FULL, cm >= 0)) return;
+    const int b = cm >> 1;
+    const unsigned grp = __match_any_sync(FULL, cm >= 0 ? b : -1);
+    stage[lane] = x;
+    __syncwarp();
+    if (cm >= 0 && lane == __ffs(grp) - 1) {
+      double s = 0.0;
+      for (unsigned g = grp; g; g &= g - 1) s += stage[__ffs(g) - 1];
+      const unsigned bit = 1u << (b & 31);
+      const unsigned old = atomicOr(&bits[b >> 5], bit);
+      if (old & bit) acc[b] += s;
+      else acc[b] = s;
+    }
+    __syncwarp();
+  }
+  // write the touched buckets in ascending order to hb/hv at `a`, clear; returns the count
+  __device__ __forceinline__ int flush(long long a, int* hb, double* hv, int lane) {
+    int total = 0;
+    for (int w0 = 0; w0 < nw; w0 += 32) {
+      const int wi = w0 + lane;
+      unsigned word = wi < nw ? bits[wi] : 0u;
+      const int c = __popc(word);
+      int incl = c;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(FULL, incl, o);
+        if (lane >= o) incl += y;
+      }
+      long long pos = a + total + incl - c;
+      for (; word; word &= word - 1) {
+        const int bucket = wi * 32 + __ffs(word) - 1;
+        hb[pos] = bucket;
+        hv[pos] = acc[bucket];
+        ++pos;
+      }
+      if (wi < nw) bits[wi] = 0u;
+      total += __shfl_sync(FULL, incl, 31);
+    }
+    __syncwarp();
+    return total;
+  }
+};
+
+__device__ __forceinline__ int cm_of(const int* __restrict__ cmap, const int* __restrict__ idx,
+                                     long long t, long long e) {
+  return t < e ? __ldg(cmap + __ldg(idx + t)) : -1;
+}
+
+// light rows (<= heavy threshold): one warp per row, 32-row blocks of row pointers per warp,
+// 64 entries loaded per step
 __global__ void __launch_bounds__(HR_WARPS * 32)
 k_hash_rows(const long long* __restrict__ ptr, const int* __restrict__ idx,
-            const double* __restrict__ val, long long rows, const int* __restrict__ cmap, int tau,
-            int* __restrict__ hb, double* __restrict__ hv, int* __restrict__ hcnt,
+            const double* __restrict__ val, long long rows, long long heavy, const int* __restrict__ cmap,
+            int tau, int* __restrict__ hb, double* __restrict__ hv, int* __restrict__ hcnt,
             const Ctrl* ctrl) {
   if (ctrl->done) return;
   extern __shared__ double hsm[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int nw = (tau + 31) >> 5;
-  double* acc = hsm + (size_t)warp * tau;
-  double* stage = hsm + (size_t)HR_WARPS * tau + warp * 32;
-  unsigned* bits = reinterpret_cast<unsigned*>(hsm + (size_t)HR_WARPS * (tau + 32)) + warp * nw;
-  for (int q = lane; q < nw; q += 32) bits[q] = 0u;
+  WarpMerge M(hsm, tau, warp);
+  for (int q = lane; q < M.nw; q += 32) M.bits[q] = 0u;
   __syncwarp();
   const long long nwarps = (long long)gridDim.x * HR_WARPS;
-  for (long long i = (long long)blockIdx.x * HR_WARPS + warp; i < rows; i += nwarps) {
-    const long long a = ptr[i], e = ptr[i + 1];
+  for (long long i0 = ((long long)blockIdx.x * HR_WARPS + warp) * 32; i0 < rows; i0 += nwarps * 32) {
+    const long long il = i0 + lane;
+    const long long pa = il < rows ? ptr[il] : 0, pe = il < rows ? ptr[il + 1] : 0;
+    const int nr = (int)min(32LL, rows - i0);
+    for (int j = 0; j < nr; ++j) {
+      const long long a = __shfl_sync(FULL, pa, j), e = __shfl_sync(FULL, pe, j);
+      if (e - a > heavy) continue;   // k_hash_rows_heavy
+      for (long long base = a; base < e; base += 64) {
+        const long long t0 = base + lane, t1 = base + 32 + lane;
+        const int cm0 = cm_of(cmap, idx, t0, e), cm1 = cm_of(cmap, idx, t1, e);
+        const double v0 = cm0 >= 0 ? val[t0] : 0.0, v1 = cm1 >= 0 ? val[t1] : 0.0;
+        M.add(cm0, (cm0 & 1) ? -v0 : v0, lane);
+        M.add(cm1, (cm1 & 1) ? -v1 : v1, lane);
+      }
+      const int total = M.flush(a, hb, hv, lane);
+      if (lane == 0) hcnt[i0 + j] = total;
+    }
+  }
+}
+
+// heavy rows: one CTA per row; warp w merges chunks w, w + 8, ... into its own accumulator, then the
+// eight accumulators are summed in warp order (deterministic) and warp 0 writes the merged row
+__global__ void __launch_bounds__(HR_WARPS * 32)
+k_hash_rows_heavy(const long long* __restrict__ ptr, const int* __restrict__ idx,
+                  const double* __restrict__ val, const int* __restrict__ heavy_rows,
+                  const int* __restrict__ cmap, int tau, int* __restrict__ hb,
+                  double* __restrict__ hv, int* __restrict__ hcnt, const Ctrl* ctrl) {
+  if (ctrl->done) return;
+  extern __shared__ double hsm[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  WarpMerge M(hsm, tau, warp);
+  for (int q = lane; q < M.nw; q += 32) M.bits[q] = 0u;
+  __syncwarp();
+  const long long i = heavy_rows[blockIdx.x];
+  const long long a = ptr[i], e = ptr[i + 1];
+  for (long long base = a + 32LL * warp; base < e; base += 32LL * HR_WARPS) {
+    const long long t = base + lane;
+    const int cm = cm_of(cmap, idx, t, e);
+    const double v = cm >= 0 ? val[t] : 0.0;
+    M.add(cm, (cm & 1) ? -v : v, lane);
+  }
+  __syncthreads();
+  // sum the warps' accumulators into warp 0's (thread owns bucket b; other threads only set
+  // other bits of warp 0's words, so the read of bit b is race free)
+  WarpMerge M0(hsm, tau, 0);
+  for (int b = threadIdx.x; b < tau; b += HR_WARPS * 32) {
+    double s = 0.0;
     bool any = false;
-    for (long long base = a; base < e; base += 32) {
-      const long long t = base + lane;
-      int cm = -1;
-      double x = 0.0;
-      if (t < e) {
-        cm = __ldg(cmap + idx[t]);
-        if (cm >= 0) x = (cm & 1) ? -val[t] : val[t];
-      }
-      if (!__ballot_sync(FULL, cm >= 0)) continue;
-      any = true;
-      const int b = cm >> 1;
-      const unsigned grp = __match_any_sync(FULL, cm >= 0 ? b : -1);
-      stage[lane] = x;
-      __syncwarp();
-      if (cm >= 0 && lane == __ffs(grp) - 1) {   // leader: sum of the group in lane order
-        double s = 0.0;
-        for (unsigned g = grp; g; g &= g - 1) s += stage[__ffs(g) - 1];
-        const unsigned bit = 1u << (b & 31);
-        const unsigned old = atomicOr(&bits[b >> 5], bit);
-        if (old & bit) acc[b] += s;
-        else acc[b] = s;
-      }
-      __syncwarp();
-    }
-    int total = 0;
-    if (any) {   // compaction in ascending bucket order
-      for (int w0 = 0; w0 < nw; w0 += 32) {
-        const int wi = w0 + lane;
-        unsigned word = wi < nw ? bits[wi] : 0u;
-        const int c = __popc(word);
-        int incl = c;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          const int y = __shfl_up_sync(FULL, incl, o);
-          if (lane >= o) incl += y;
-        }
-        long long pos = a + total + incl - c;
-        for (; word; word &= word - 1) {
-          const int bucket = wi * 32 + __ffs(word) - 1;
-          hb[pos] = bucket;
-          hv[pos] = acc[bucket];
-          ++pos;
-        }
-        if (wi < nw) bits[wi] = 0u;
-        total += __shfl_sync(FULL, incl, 31);
+    for (int w = 0; w < HR_WARPS; ++w) {
+      WarpMerge Mw(hsm, tau, w);
+      if (Mw.bits[b >> 5] & (1u << (b & 31))) {
+        s += Mw.acc[b];
+        any = true;
       }
     }
+    M0.acc[b] = s;
+    if (any) atomicOr(&M0.bits[b >> 5], 1u << (b & 31));
+  }
+  __syncthreads();
+  if (warp == 0) {
+    const int total = M.flush(a, hb, hv, lane);
     if (lane == 0) hcnt[i] = total;
-    __syncwarp();
   }
 }
 
 // ------------------------------------------------------------------------------------ stage 2
-__device__ __forceinline__ void pair_decode(long long q, int& s, int& t) {
-  // q = tri(s) + t, 0 <= t <= s
-  int i = (int)((sqrt(8.0 * (double)q + 1.0) - 1.0) * 0.5);
-  while (tri(i + 1) <= q) ++i;
-  while (tri(i) > q) --i;
-  s = i;
-  t = (int)(q - tri(i));
-}
-
 __global__ void __launch_bounds__(GB_THREADS, 1)
 k_gram_bands(const long long* __restrict__ ptr, const int* __restrict__ hcnt,
              const int* __restrict__ hb, const double* __restrict__ hv,
@@ -138,25 +200,33 @@ k_gram_bands(const long long* __restrict__ ptr, const int* __restrict__ hcnt,
   __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const long long r0 = chunk_r0[blockIdx.y], r1 = chunk_r0[blockIdx.y + 1];
-  for (long long r = r0 + warp; r < r1; r += GB_THREADS / 32) {
-    const int L = hcnt[r];
-    if (L == 0) continue;
-    const long long off = ptr[r];
-    const int* B = hb + off;
-    const double* V = hv + off;
-    int s0 = 0, s1 = 0;   // entries with bucket < a0, < a1 (B ascending)
-    for (int q = 0; q < L; q += 32) {
-      const int bq = q + lane < L ? B[q + lane] : INT_MAX;
-      s0 += __popc(__ballot_sync(FULL, bq < a0));
-      s1 += __popc(__ballot_sync(FULL, bq < a1));
-    }
-    if (s1 == s0) continue;
-    const long long p0 = tri(s0), np = tri(s1) - p0;   // pairs (s, t), s0 <= s < s1, t <= s
-    for (long long p = lane; p < np; p += 32) {
-      int s, t;
-      pair_decode(p0 + p, s, t);
-      const int bs = B[s];
-      atomicAdd(&band[tri(bs) - base + B[t]], V[s] * V[t]);
+  for (long long rb = r0 + 32LL * warp; rb < r1; rb += 32LL * (GB_THREADS / 32)) {
+    const long long rl = rb + lane;
+    const int Ll = rl < r1 ? hcnt[rl] : 0;
+    const long long offl = Ll ? ptr[rl] : 0;
+    for (unsigned nz = __ballot_sync(FULL, Ll > 0); nz; nz &= nz - 1) {
+      const int j = __ffs(nz) - 1;
+      const int L = __shfl_sync(FULL, Ll, j);
+      const long long off = __shfl_sync(FULL, offl, j);
+      const int* B = hb + off;
+      const double* V = hv + off;
+      int s0 = 0, s1 = 0;   // entries with bucket < a0, < a1 (B ascending)
+      for (int q = 0; q < L; q += 32) {
+        const int bq = q + lane < L ? B[q + lane] : INT_MAX;
+        s0 += __popc(__ballot_sync(FULL, bq < a0));
+        s1 += __popc(__ballot_sync(FULL, bq < a1));
+        if (__shfl_sync(FULL, bq, 31) >= a1) break;
+      }
+      if (s1 == s0) continue;
+      // pairs (s, t), s0 <= s < s1, t <= s, enumerated q = tri(s) + t; lane cursor advances by 32
+      const long long np = tri(s1) - tri(s0);
+      int s = s0, t = lane;
+      while (t > s) { t -= s + 1; ++s; }
+      for (long long p = lane; p < np; p += 32) {
+        atomicAdd(&band[tri(B[s]) - base + B[t]], V[s] * V[t]);
+        t += 32;
+        while (t > s) { t -= s + 1; ++s; }
+      }
     }
   }
   __syncthreads();
@@ -194,11 +264,12 @@ __global__ void k_chunk_bounds(const long long* __restrict__ ptr, long long rows
 }
 
 // ------------------------------------------------------------------------------------ SpMV
+// out[i] = sum_q val[q] v[idx[q]] over row i; rows longer than `heavy` are left to k_spmv_heavy
 template <int VW>
 __global__ void __launch_bounds__(256)
 k_spmv(const long long* __restrict__ ptr, const int* __restrict__ idx,
-       const double* __restrict__ val, long long rows, const double* __restrict__ v,
-       double* __restrict__ out, const Ctrl* ctrl) {
+       const double* __restrict__ val, long long rows, long long heavy,
+       const double* __restrict__ v, double* __restrict__ out, const Ctrl* ctrl) {
   if (ctrl->done) return;
   const int sub = threadIdx.x & (VW - 1);
   const long long g = ((long long)blockIdx.x * blockDim.x + threadIdx.x) / VW;
@@ -206,26 +277,67 @@ k_spmv(const long long* __restrict__ ptr, const int* __restrict__ idx,
   const long long rows_pad = (rows + ng - 1) / ng * ng;   // whole sub-warps iterate together
   for (long long i = g; i < rows_pad; i += ng) {
     double s = 0.0;
-    if (i < rows)
-      for (long long q = ptr[i] + sub; q < ptr[i + 1]; q += VW) s += val[q] * __ldg(v + idx[q]);
+    long long a = 0, e = 0;
+    if (i < rows) {
+      a = ptr[i];
+      e = ptr[i + 1];
+      if (e - a <= heavy)
+        for (long long q = a + sub; q < e; q += VW) s += val[q] * __ldg(v + idx[q]);
+    }
 #pragma unroll
     for (int o = VW / 2; o > 0; o >>= 1) s += __shfl_xor_sync(FULL, s, o, VW);
-    if (sub == 0 && i < rows) out[i] = s;
+    if (sub == 0 && i < rows && e - a <= heavy) out[i] = s;
   }
 }
 
+constexpr int SH_THREADS = 256;
+__global__ void __launch_bounds__(SH_THREADS)
+k_spmv_heavy(const long long* __restrict__ ptr, const int* __restrict__ idx,
+             const double* __restrict__ val, const int* __restrict__ heavy_rows,
+             const double* __restrict__ v, double* __restrict__ out, const Ctrl* ctrl) {
+  if (ctrl->done) return;
+  __shared__ double red[SH_THREADS / 32];
+  const long long i = heavy_rows[blockIdx.x];
+  double s = 0.0;
+  for (long long q = ptr[i] + threadIdx.x; q < ptr[i + 1]; q += SH_THREADS) s += val[q] * __ldg(v + idx[q]);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(FULL, s, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < SH_THREADS / 32; ++w) t += red[w];
+    out[i] = t;
+  }
+}
+
+__global__ void k_heavy_list(const long long* __restrict__ ptr, long long rows, long long heavy,
+                             int* __restrict__ list, int* __restrict__ count) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < rows;
+       i += (long long)gridDim.x * blockDim.x)
+    if (ptr[i + 1] - ptr[i] > heavy) list[atomicAdd(count, 1)] = (int)i;
+}
+
 cudaError_t launch_spmv(const long long* ptr, const int* idx, const double* val, long long rows,
-                        long long nnz, const double* v, double* out, int num_sms, const Ctrl* ctrl,
+                        long long nnz, long long heavy, const int* heavy_rows, int nheavy,
+                        const double* v, double* out, int num_sms, const Ctrl* ctrl,
                         cudaStream_t st) {
   if (rows <= 0) return cudaSuccess;
   const double avg = (double)nnz / (double)rows;
   const unsigned grid = (unsigned)std::max<long long>(1, std::min<long long>((rows * 32 + 255) / 256,
                                                                              (long long)num_sms * 16));
-  if (avg >= 24) k_spmv<32><<<grid, 256, 0, st>>>(ptr, idx, val, rows, v, out, ctrl);
-  else if (avg >= 12) k_spmv<16><<<grid, 256, 0, st>>>(ptr, idx, val, rows, v, out, ctrl);
-  else if (avg >= 6) k_spmv<8><<<grid, 256, 0, st>>>(ptr, idx, val, rows, v, out, ctrl);
-  else k_spmv<4><<<grid, 256, 0, st>>>(ptr, idx, val, rows, v, out, ctrl);
+  if (avg >= 24) k_spmv<32><<<grid, 256, 0, st>>>(ptr, idx, val, rows, heavy, v, out, ctrl);
+  else if (avg >= 12) k_spmv<16><<<grid, 256, 0, st>>>(ptr, idx, val, rows, heavy, v, out, ctrl);
+  else if (avg >= 6) k_spmv<8><<<grid, 256, 0, st>>>(ptr, idx, val, rows, heavy, v, out, ctrl);
+  else k_spmv<4><<<grid, 256, 0, st>>>(ptr, idx, val, rows, heavy, v, out, ctrl);
+  if (nheavy > 0) k_spmv_heavy<<<nheavy, SH_THREADS, 0, st>>>(ptr, idx, val, heavy_rows, v, out, ctrl);
   return cudaGetLastError();
+}
+
+// heavy threshold: max(256, 8 x mean row length)
+long long heavy_threshold(long long nnz, long long rows) {
+  const long long avg = rows > 0 ? (nnz + rows - 1) / rows : 0;
+  return std::max<long long>(256, 8 * avg);
 }
 
 }  // namespace
@@ -247,6 +359,10 @@ void Problem::csr_gram_free() {
   dfree(csr->chunk_r0);
   dfree(csr->gpart);
   dfree(csr->tvec);
+  dfree(csr->heavy_rowsR);
+  dfree(csr->heavy_rowsRt);
+  csr->heavy_rowsR = csr->heavy_rowsRt = nullptr;
+  csr->nheavyR = csr->nheavyRt = 0;
   csr->hb = nullptr;
   csr->hv = nullptr;
   csr->hcnt = nullptr;
@@ -301,16 +417,87 @@ rs_status Problem::csr_gram_workspace(int kind, int tau) {
   RS_CUDA(cudaGetLastError());
   c->gpart_stride = round_up(total, 4);
   RS_TRY(dalloc(&c->gpart, (size_t)c->gpart_stride * c->nchunks));
+  // heavy-row lists of R and R^T
+  {
+    const RView Rt = route == 1 ? RView{c->colptr, c->rowidx, c->cvals, c->cols}
+                                : RView{c->rowptr, c->colidx, c->vals, c->rows};
+    int* cnt = nullptr;
+    RS_TRY(dalloc(&cnt, 2));
+    RS_CUDA(cudaMemsetAsync(cnt, 0, 2 * sizeof(int), st));
+    c->heavyR = heavy_threshold(c->nnz, R.rows);
+    c->heavyRt = heavy_threshold(c->nnz, Rt.rows);
+    RS_TRY(dalloc(&c->heavy_rowsR, std::max<long long>(1, c->nnz / (c->heavyR + 1) + 1)));
+    RS_TRY(dalloc(&c->heavy_rowsRt, std::max<long long>(1, c->nnz / (c->heavyRt + 1) + 1)));
+    if (R.rows > 0)
+      k_heavy_list<<<(unsigned)std::min<long long>((R.rows + 255) / 256, 4096), 256, 0, st>>>(
+          R.ptr, R.rows, c->heavyR, c->heavy_rowsR, cnt);
+    if (Rt.rows > 0)
+      k_heavy_list<<<(unsigned)std::min<long long>((Rt.rows + 255) / 256, 4096), 256, 0, st>>>(
+          Rt.ptr, Rt.rows, c->heavyRt, c->heavy_rowsRt, cnt + 1);
+    int h[2] = {0, 0};
+    RS_CUDA(cudaMemcpyAsync(h, cnt, sizeof(h), cudaMemcpyDeviceToHost, st));
+    RS_CUDA(cudaStreamSynchronize(st));
+    dfree(cnt);
+    c->nheavyR = h[0];
+    c->nheavyRt = h[1];
+  }
   c->gb_smem = (size_t)maxband * sizeof(double);
   c->hr_smem = (size_t)HR_WARPS * (tau + 32) * sizeof(double) + (size_t)HR_WARPS * ((tau + 31) / 32) * 4;
   RS_CUDA(cudaFuncSetAttribute(k_gram_bands, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                (int)std::max<size_t>(c->gb_smem, 48 * 1024)));
   RS_CUDA(cudaFuncSetAttribute(k_hash_rows, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                (int)std::max<size_t>(c->hr_smem, 48 * 1024)));
+  RS_CUDA(cudaFuncSetAttribute(k_hash_rows_heavy, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)std::max<size_t>(c->hr_smem, 48 * 1024)));
   RS_CUDA(cudaStreamSynchronize(st));
   if (std::getenv("RS_VERBOSE"))
-    fprintf(stderr, "[rs] csr gram: tau %d, %d bands (max %lld doubles), %d chunks\n", tau,
-            c->nbands, maxband, c->nchunks);
+    fprintf(stderr, "[rs] csr gram: tau %d, %d bands (max %lld doubles), %d chunks, heavy rows "
+            "%d (> %lld) / %d (> %lld)\n", tau, c->nbands, maxband, c->nchunks, c->nheavyR,
+            c->heavyR, c->nheavyRt, c->heavyRt);
+  return RS_OK;
+}
+
+rs_status Problem::csr_gram_into(const DevSketch& s, double* G) {
+  CsrData* c = csr;
+  const RView R = route == 1 ? RView{c->rowptr, c->colidx, c->vals, c->rows}
+                             : RView{c->colptr, c->rowidx, c->cvals, c->cols};
+  const int tau = s.tau;
+  const int* cmap = s.cmap;
+  if (s.kind != SK_COUNT) {
+    RS_CUDA(launch_cmap_build(s, c->cmap_all, m, ctrl, st));
+    cmap = c->cmap_all;
+  }
+  if (R.rows > 0) {   // a2: rows of R S, merged and bucket-sorted
+    const unsigned grid = (unsigned)std::max<long long>(
+        1, std::min<long long>((R.rows + HR_WARPS - 1) / HR_WARPS, (long long)num_sms * 8));
+    k_hash_rows<<<grid, HR_WARPS * 32, c->hr_smem, st>>>(R.ptr, R.idx, R.val, R.rows, c->heavyR,
+                                                          cmap, tau, c->hb, c->hv, c->hcnt, ctrl);
+    if (c->nheavyR > 0)
+      k_hash_rows_heavy<<<c->nheavyR, HR_WARPS * 32, c->hr_smem, st>>>(
+          R.ptr, R.idx, R.val, c->heavy_rowsR, cmap, tau, c->hb, c->hv, c->hcnt, ctrl);
+    RS_CUDA(cudaGetLastError());
+    // a3/a4: (R S)^T (R S), lower triangle
+    k_gram_bands<<<dim3((unsigned)c->nbands, (unsigned)c->nchunks), GB_THREADS, c->gb_smem, st>>>(
+        R.ptr, c->hcnt, c->hb, c->hv, c->band_a0, c->chunk_r0, c->gpart, c->gpart_stride, ctrl);
+    RS_CUDA(cudaGetLastError());
+    k_gram_band_reduce<<<tau, 256, 0, st>>>(c->gpart, c->nchunks, c->gpart_stride, G, ld_gram, ctrl);
+    RS_CUDA(cudaGetLastError());
+  } else {
+    RS_CUDA(launch_fill(G, (long long)tau * ld_gram, 0.0, st));
+  }
+  return allreduce(G, (size_t)tau * ld_gram);
+}
+
+rs_status Problem::csr_gram_apply(const double* v, double* u) {
+  CsrData* c = csr;
+  const RView R = route == 1 ? RView{c->rowptr, c->colidx, c->vals, c->rows}
+                             : RView{c->colptr, c->rowidx, c->cvals, c->cols};
+  const RView Rt = route == 1 ? RView{c->colptr, c->rowidx, c->cvals, c->cols}
+                              : RView{c->rowptr, c->colidx, c->vals, c->rows};
+  RS_CUDA(launch_spmv(R.ptr, R.idx, R.val, R.rows, c->nnz, c->heavyR, c->heavy_rowsR, c->nheavyR,
+                      v, c->tvec, num_sms, ctrl, st));
+  RS_CUDA(launch_spmv(Rt.ptr, Rt.idx, Rt.val, Rt.rows, c->nnz, c->heavyRt, c->heavy_rowsRt,
+                      c->nheavyRt, c->tvec, u, num_sms, ctrl, st));
   return RS_OK;
 }
 
@@ -319,45 +506,15 @@ rs_status Problem::csr_enqueue_gram(const rs_solve_opts* o, cudaEvent_t* ev) {
   auto mark = [&](int cls, int edge) {
     if (ev) cudaEventRecordWithFlags(ev[2 * cls + edge], st, cudaEventRecordExternal);
   };
-  CsrData* c = csr;
-  const RView R = route == 1 ? RView{c->rowptr, c->colidx, c->vals, c->rows}
-                             : RView{c->colptr, c->rowidx, c->cvals, c->cols};
-  const RView Rt = route == 1 ? RView{c->colptr, c->rowidx, c->cvals, c->cols}
-                              : RView{c->rowptr, c->colidx, c->vals, c->rows};
-  const int tau = sk.tau;
-  mark(RS_K_XS, 0);
-  const int* cmap = sk.cmap;
-  if (sk.kind != SK_COUNT) {
-    RS_CUDA(launch_cmap_build(sk, c->cmap_all, m, ctrl, st));
-    cmap = c->cmap_all;
-  }
-  if (R.rows > 0) {   // a2: rows of R S, merged and bucket-sorted
-    const unsigned grid = (unsigned)std::max<long long>(
-        1, std::min<long long>((R.rows + HR_WARPS - 1) / HR_WARPS, (long long)num_sms * 8));
-    k_hash_rows<<<grid, HR_WARPS * 32, c->hr_smem, st>>>(R.ptr, R.idx, R.val, R.rows, cmap, tau,
-                                                          c->hb, c->hv, c->hcnt, ctrl);
-    RS_CUDA(cudaGetLastError());
-  }
-  mark(RS_K_XS, 1);
   mark(RS_K_GRAM, 0);
-  if (R.rows > 0) {   // a3/a4: (R S)^T (R S), lower triangle
-    k_gram_bands<<<dim3((unsigned)c->nbands, (unsigned)c->nchunks), GB_THREADS, c->gb_smem, st>>>(
-        R.ptr, c->hcnt, c->hb, c->hv, c->band_a0, c->chunk_r0, c->gpart, c->gpart_stride, ctrl);
-    RS_CUDA(cudaGetLastError());
-    k_gram_band_reduce<<<tau, 256, 0, st>>>(c->gpart, c->nchunks, c->gpart_stride, Gram, ld_gram, ctrl);
-    RS_CUDA(cudaGetLastError());
-  } else {
-    RS_CUDA(launch_fill(Gram, (long long)tau * ld_gram, 0.0, st));
-  }
-  RS_TRY(allreduce(Gram, (size_t)tau * ld_gram));
+  RS_TRY(csr_gram_into(sk, Gram));                                                // a2 - a4
   mark(RS_K_GRAM, 1);
   mark(RS_K_SOLVE, 0);
   RS_CUDA(launch_sketched_solve(nullptr, 0, false, Gram, ld_gram, lambda, r, sk, sw, sdelta, ctrl,
                                 st));                                              // a4 + a5
   mark(RS_K_SOLVE, 1);
   mark(RS_K_AS, 0);   // u = R^T (R (S delta)), summed over ranks
-  RS_CUDA(launch_spmv(R.ptr, R.idx, R.val, R.rows, c->nnz, sdelta, c->tvec, num_sms, ctrl, st));
-  RS_CUDA(launch_spmv(Rt.ptr, Rt.idx, Rt.val, Rt.rows, c->nnz, c->tvec, uvec, num_sms, ctrl, st));
+  RS_TRY(csr_gram_apply(sdelta, uvec));
   RS_TRY(allreduce(uvec, (size_t)m));
   mark(RS_K_AS, 1);
   mark(RS_K_UPDATE, 0);

@@ -96,6 +96,8 @@ void Problem::free_workspace() {
   Ginv_slots = nullptr;
   dfree(slot_flags);
   slot_flags = nullptr;
+  dfree(bf_work);
+  bf_work = nullptr;
   pipe = false;
   P = 0;
   ws_depth = -1;
@@ -350,8 +352,10 @@ static rs_status validate_opts(const Problem* p, const rs_solve_opts* o, int* ks
 // Sketch-ahead pipeline (bfactor.cu) applies to dense primal EXPLICIT and GRAM modes with
 // tau <= bfactor_max_tau(): there G_k needs no per-iteration contraction of the iterate's data.
 static bool pipeline_applies(const Problem* p, int tau) {
-  return p->fmt == 0 && p->route == 1 && (p->mode == RS_AS_EXPLICIT || p->mode == RS_AS_GRAM) &&
-         tau <= bfactor_max_tau() && !std::getenv("RS_NO_PIPE");
+  const bool dense = p->fmt == 0 && p->route == 1 &&
+                     (p->mode == RS_AS_EXPLICIT || p->mode == RS_AS_GRAM);
+  const bool csr = p->fmt == 1 && p->mode == RS_AS_GRAM;
+  return (dense || csr) && tau <= bfactor_max_tau() && !std::getenv("RS_NO_PIPE");
 }
 
 rs_status Problem::ensure_workspace(int kind, int tau, int ksum, int depth) {
@@ -433,6 +437,7 @@ rs_status Problem::ensure_workspace(int kind, int tau, int ksum, int depth) {
     gi_stride = (long long)tau * ld_gi;
     RS_TRY(dalloc(&Ginv_slots, (size_t)gi_stride * depth));
     RS_TRY(dalloc(&slot_flags, depth));
+    if (bfactor_work_elems(tau)) RS_TRY(dalloc(&bf_work, bfactor_work_elems(tau) * depth));
   }
   sw = plan_solve(tau, num_sms);
   RS_TRY(dalloc(&sw.Gx, solve_gx_elems(tau)));
@@ -535,7 +540,9 @@ rs_status Problem::enqueue_precompute(const rs_solve_opts* o, int ns, cudaEvent_
     for (int q = 0; q < ns; ++q) {
       const DevSketch sq = skb.at(q);
       double* Gq = Gram_slots + (long long)q * gram_stride;
-      if (rows_loc > 0 && gram_fused) {
+      if (fmt == 1) {
+        RS_TRY(csr_gram_into(sq, Gq));
+      } else if (rows_loc > 0 && gram_fused) {
         RS_CUDA(launch_gram_fused(X, ldx, rows_loc, sq, xp_part, Gq, ld_gram, num_sms, ctrl, st));
       } else if (rows_loc > 0) {
         RS_CUDA(launch_dense_xs(X, ldx, rows_loc, sq, XS, ld_xs, ctrl, st));
@@ -550,7 +557,8 @@ rs_status Problem::enqueue_precompute(const rs_solve_opts* o, int ns, cudaEvent_
     src.gram_stride = gram_stride;
     src.lambda = lambda;
   }
-  RS_CUDA(launch_bfactor(src, skb, ns, Ginv_slots, ld_gi, gi_stride, slot_flags, ctrl, st));  // a4+a5
+  RS_CUDA(launch_bfactor(src, skb, ns, Ginv_slots, ld_gi, gi_stride, slot_flags, bf_work, ctrl,
+                         st));                                                              // a4+a5
   if (ev) cudaEventRecordWithFlags(ev[2 * RS_K_PRE + 1], st, cudaEventRecordExternal);
   return RS_OK;
 }
@@ -563,7 +571,7 @@ rs_status Problem::enqueue_pipelined_iteration(const rs_solve_opts* o, int slot,
   const DevSketch sq = skb.at(slot);
   mark(RS_K_SOLVE, 0);
   RS_CUDA(launch_apply_ginv(Ginv_slots + (long long)slot * gi_stride, ld_gi, sq, slot_flags + slot,
-                            r, sw.delta, sdelta, ctrl, st));                      // a4 + a5
+                            r, sw.Gx, sw.delta, sdelta, ctrl, st));               // a4 + a5
   mark(RS_K_SOLVE, 1);
   if (mode == RS_AS_EXPLICIT) {
     mark(RS_K_UPDATE, 0);
@@ -577,7 +585,9 @@ rs_status Problem::enqueue_pipelined_iteration(const rs_solve_opts* o, int slot,
     return RS_OK;
   }
   mark(RS_K_AS, 0);
-  if (rows_loc > 0)
+  if (fmt == 1)
+    RS_TRY(csr_gram_apply(sdelta, uvec));                                        // R^T R S delta
+  else if (rows_loc > 0)
     RS_CUDA(launch_xpass(X, ldx, rows_loc, m, sdelta, xp_part, uvec, num_sms, ctrl, st));
   else
     RS_CUDA(launch_fill(uvec, m, 0.0, st));
@@ -613,7 +623,7 @@ rs_status Problem::solve(const rs_solve_opts* o, double* w_out, rs_mem w_mem, do
   if (want_pipe) {   // one batched factorisation wave: <= num_sms slots, <= ~6 GB of slots
     const long long slot_bytes =
         8LL * o->tau * (mode == RS_AS_EXPLICIT ? round_up(m, 4) : round_up(o->tau, 4)) +
-        8LL * o->tau * round_up(o->tau, 4) + 16LL * m;
+        8LL * o->tau * round_up(o->tau, 4) + 16LL * m + 8LL * (long long)bfactor_work_elems((int)o->tau);
     depth = (int)std::max<long long>(1, std::min<long long>({(long long)chunk, (long long)num_sms,
                                                              6000000000LL / slot_bytes}));
   }

@@ -90,6 +90,7 @@ struct Problem {
   double* Ginv_slots = nullptr;
   long long ld_gi = 0, gi_stride = 0;
   int* slot_flags = nullptr;
+  double* bf_work = nullptr;     // tau > 224: per-slot work matrices of the batched factorisation
   SolveWork sw{};
   double* partials = nullptr;
   cudaGraphExec_t graph_exec = nullptr;
@@ -117,6 +118,8 @@ struct Problem {
   void csr_gram_free();
   rs_status csr_gram_workspace(int kind, int tau);
   rs_status csr_enqueue_gram(const rs_solve_opts* o, cudaEvent_t* ev);
+  rs_status csr_gram_into(const DevSketch& s, double* G);      // G = (R S)^T (R S), lower
+  rs_status csr_gram_apply(const double* v, double* u);        // u = R^T (R v), local part
 };
 
 rs_status finish_setup(Problem* p);

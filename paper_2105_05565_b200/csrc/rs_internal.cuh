@@ -204,13 +204,16 @@ struct FactorSrc {
 int bfactor_max_tau();
 cudaError_t bfactor_init();
 // flags[s] = 1 if G of slot s was not SPD (a pivot <= 0 or non-finite after the empty-bucket rule)
+// tau > 224: `work` = nslots x bfactor_work_elems(tau) doubles of scratch (null otherwise).
+size_t bfactor_work_elems(int tau);
 cudaError_t launch_bfactor(const FactorSrc& src, const DevSketch& skb, int nslots, double* Ginv,
-                           long long ldgi, long long gi_stride, int* flags, const Ctrl* ctrl,
-                           cudaStream_t st);
+                           long long ldgi, long long gi_stride, int* flags, double* work,
+                           const Ctrl* ctrl, cudaStream_t st);
 // delta = Ginv (S^T r), sdelta[coord_e] = sign_e delta[bucket_e]; flag != 0 -> status NOTSPD.
+// gbuf: tau doubles of scratch (g).
 cudaError_t launch_apply_ginv(const double* Ginv, long long ldgi, const DevSketch& sk,
-                              const int* flag, const double* r, double* delta, double* sdelta,
-                              Ctrl* ctrl, cudaStream_t st);
+                              const int* flag, const double* r, double* gbuf, double* delta,
+                              double* sdelta, Ctrl* ctrl, cudaStream_t st);
 
 // misc
 // *out += number of non-finite entries of the rows x cols block.

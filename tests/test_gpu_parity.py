@@ -322,3 +322,17 @@ def test_csr_primal_long_rows(rs, kind, tau, k, mode):
     ref = OV.solve(Xs, y, lam, kind, tau, 1.0, 0.5, 0.0, 12, seed=3, subcount_k=k)
     assert rel(w, ref["w"]) <= 1e-10
     assert rel(r, ref["r"]) <= 1e-10
+
+
+@pytest.mark.parametrize("kind,tau,k", [("subsample", 260, 0), ("count", 300, 0), ("subcount", 230, 2)])
+@pytest.mark.parametrize("mode", ["explicit", "gram"])
+def test_dense_large_tau_sketch_ahead(rs, kind, tau, k, mode):
+    """tau > 224: the sketch-ahead pipeline factors G_k in global memory (k_bfactor_big, 32 x 32
+    DMMA tiles, ragged tau padded with an identity tail)."""
+    n, d = 3000, 700
+    X, y = rsinputs.dense_problem(n, d, seed=11)
+    X, y = X.numpy(), y.numpy()
+    w, r, rep = _run_gpu_dense(rs, X, y, 0.5, mode, kind, tau, 0.5, 10, seed=6, k=k)
+    ref = OV.solve(X, y, 0.5, kind, tau, 1.0, 0.5, 0.0, 10, seed=6, subcount_k=k)
+    assert rel(w, ref["w"]) <= 1e-10
+    assert rel(r, ref["r"]) <= 1e-10
