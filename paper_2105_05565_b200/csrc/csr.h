@@ -36,6 +36,7 @@ struct CsrData {
   int* heavy_rowsR = nullptr;
   int* heavy_rowsRt = nullptr;
   int nheavyR = 0, nheavyRt = 0;
+  int* chunk_h0 = nullptr;       // [nchunks + 1] first heavy row (sorted list) of every chunk
   size_t hr_smem = 0, gb_smem = 0;
 };
 

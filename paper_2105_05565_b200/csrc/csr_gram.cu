@@ -190,6 +190,7 @@ __global__ void __launch_bounds__(GB_THREADS, 1)
 k_gram_bands(const long long* __restrict__ ptr, const int* __restrict__ hcnt,
              const int* __restrict__ hb, const double* __restrict__ hv,
              const int* __restrict__ band_a0, const long long* __restrict__ chunk_r0,
+             long long heavy, const int* __restrict__ heavy_rows, const int* __restrict__ chunk_h0,
              double* __restrict__ part, long long part_stride, const Ctrl* ctrl) {
   if (ctrl->done) return;
   extern __shared__ double band[];
@@ -202,8 +203,9 @@ k_gram_bands(const long long* __restrict__ ptr, const int* __restrict__ hcnt,
   const long long r0 = chunk_r0[blockIdx.y], r1 = chunk_r0[blockIdx.y + 1];
   for (long long rb = r0 + 32LL * warp; rb < r1; rb += 32LL * (GB_THREADS / 32)) {
     const long long rl = rb + lane;
-    const int Ll = rl < r1 ? hcnt[rl] : 0;
+    int Ll = rl < r1 ? hcnt[rl] : 0;
     const long long offl = Ll ? ptr[rl] : 0;
+    if (Ll && ptr[rl + 1] - offl > heavy) Ll = 0;   // heavy phase below
     for (unsigned nz = __ballot_sync(FULL, Ll > 0); nz; nz &= nz - 1) {
       const int j = __ffs(nz) - 1;
       const int L = __shfl_sync(FULL, Ll, j);
@@ -218,14 +220,37 @@ k_gram_bands(const long long* __restrict__ ptr, const int* __restrict__ hcnt,
         if (__shfl_sync(FULL, bq, 31) >= a1) break;
       }
       if (s1 == s0) continue;
-      // pairs (s, t), s0 <= s < s1, t <= s, enumerated q = tri(s) + t; lane cursor advances by 32
-      const long long np = tri(s1) - tri(s0);
+      // pairs (s, t), s0 <= s < s1, t <= s, enumerated q = tri(s) + t: every lane busy, its
+      // cursor advancing by 32 pairs per step
+      const int np = (int)(tri(s1) - tri(s0));
       int s = s0, t = lane;
       while (t > s) { t -= s + 1; ++s; }
-      for (long long p = lane; p < np; p += 32) {
+      for (int p = lane; p < np; p += 32) {
         atomicAdd(&band[tri(B[s]) - base + B[t]], V[s] * V[t]);
         t += 32;
         while (t > s) { t -= s + 1; ++s; }
+      }
+    }
+  }
+  // heavy rows of the chunk (Zipf-popular features): all warps on one row at a time, warp w owns
+  // the G rows b = w (mod 32) of the band, so the updates need no atomics and no barrier
+  __syncthreads();
+  for (int h = chunk_h0[blockIdx.y]; h < chunk_h0[blockIdx.y + 1]; ++h) {
+    const long long r = heavy_rows[h];
+    const int L = hcnt[r];
+    const long long off = ptr[r];
+    const int* B = hb + off;
+    const double* V = hv + off;
+    for (int q = 0; q < L; q += 32) {
+      const int bq = q + lane < L ? B[q + lane] : INT_MAX;
+      if (__shfl_sync(FULL, bq, 0) >= a1) break;
+      for (unsigned mine = __ballot_sync(FULL, bq >= a0 && bq < a1 && (bq & 31) == warp); mine;
+           mine &= mine - 1) {
+        const int s = q + __ffs(mine) - 1;
+        const int bs = B[s];
+        const double vs = V[s];
+        double* rowp = band + (tri(bs) - base);
+        for (int t = lane; t <= s; t += 32) rowp[B[t]] += vs * V[t];
       }
     }
   }
@@ -361,6 +386,8 @@ void Problem::csr_gram_free() {
   dfree(csr->tvec);
   dfree(csr->heavy_rowsR);
   dfree(csr->heavy_rowsRt);
+  dfree(csr->chunk_h0);
+  csr->chunk_h0 = nullptr;
   csr->heavy_rowsR = csr->heavy_rowsRt = nullptr;
   csr->nheavyR = csr->nheavyRt = 0;
   csr->hb = nullptr;
@@ -440,6 +467,20 @@ rs_status Problem::csr_gram_workspace(int kind, int tau) {
     dfree(cnt);
     c->nheavyR = h[0];
     c->nheavyRt = h[1];
+    // sorted heavy rows of R and their range per stage-2 chunk
+    std::vector<int> hl(c->nheavyR);
+    std::vector<long long> cr(c->nchunks + 1);
+    if (c->nheavyR)
+      RS_CUDA(cudaMemcpy(hl.data(), c->heavy_rowsR, hl.size() * sizeof(int), cudaMemcpyDeviceToHost));
+    RS_CUDA(cudaMemcpy(cr.data(), c->chunk_r0, cr.size() * sizeof(long long), cudaMemcpyDeviceToHost));
+    std::sort(hl.begin(), hl.end());
+    std::vector<int> h0(c->nchunks + 1);
+    for (int k = 0; k <= c->nchunks; ++k)
+      h0[k] = (int)(std::lower_bound(hl.begin(), hl.end(), cr[k]) - hl.begin());
+    if (c->nheavyR)
+      RS_CUDA(cudaMemcpy(c->heavy_rowsR, hl.data(), hl.size() * sizeof(int), cudaMemcpyHostToDevice));
+    RS_TRY(dalloc(&c->chunk_h0, h0.size()));
+    RS_CUDA(cudaMemcpy(c->chunk_h0, h0.data(), h0.size() * sizeof(int), cudaMemcpyHostToDevice));
   }
   c->gb_smem = (size_t)maxband * sizeof(double);
   c->hr_smem = (size_t)HR_WARPS * (tau + 32) * sizeof(double) + (size_t)HR_WARPS * ((tau + 31) / 32) * 4;
@@ -478,7 +519,8 @@ rs_status Problem::csr_gram_into(const DevSketch& s, double* G) {
     RS_CUDA(cudaGetLastError());
     // a3/a4: (R S)^T (R S), lower triangle
     k_gram_bands<<<dim3((unsigned)c->nbands, (unsigned)c->nchunks), GB_THREADS, c->gb_smem, st>>>(
-        R.ptr, c->hcnt, c->hb, c->hv, c->band_a0, c->chunk_r0, c->gpart, c->gpart_stride, ctrl);
+        R.ptr, c->hcnt, c->hb, c->hv, c->band_a0, c->chunk_r0, c->heavyR, c->heavy_rowsR,
+        c->chunk_h0, c->gpart, c->gpart_stride, ctrl);
     RS_CUDA(cudaGetLastError());
     k_gram_band_reduce<<<tau, 256, 0, st>>>(c->gpart, c->nchunks, c->gpart_stride, G, ld_gram, ctrl);
     RS_CUDA(cudaGetLastError());

@@ -618,7 +618,7 @@ rs_status Problem::solve(const rs_solve_opts* o, double* w_out, rs_mem w_mem, do
   const bool want_pipe = pipeline_applies(this, (int)o->tau);
   // iterations per CUDA-graph launch (between host reads of the stop flag)
   const int chunk = (int)(o->check_every > 0 ? std::min<long long>(o->check_every, 1024)
-                                             : (want_pipe ? 64 : 16));
+                                             : (want_pipe ? (o->tau > 224 ? num_sms : 64) : 16));
   int depth = 0;
   if (want_pipe) {   // one batched factorisation wave: <= num_sms slots, <= ~6 GB of slots
     const long long slot_bytes =
