@@ -109,13 +109,23 @@ def run_reference(args):
     from oracle import solver as OV
     cfg = rsinputs.CONFIGS[args.config]
     dev = "cuda" if torch.cuda.is_available() else "cpu"
-    X, y = rsinputs.dense_problem(cfg.n, cfg.d, seed=0, col_decay=cfg.col_decay, noise=cfg.noise,
-                                  device=dev)
-    X, y = X.cpu().numpy(), y.cpu().numpy()
+    if cfg.kind == "dense":
+        X, y = rsinputs.dense_problem(cfg.n, cfg.d, seed=0, col_decay=cfg.col_decay,
+                                      noise=cfg.noise, device=dev)
+        X, y = X.cpu().numpy(), y.cpu().numpy()
+    elif cfg.zipf_a > 0:
+        rp, ci, va, y = rsinputs.csr_zipf(cfg.n, cfg.d, cfg.nnz_per_row, a=cfg.zipf_a, seed=0)
+        X = rsinputs.csr_to_scipy(rp, ci, va, cfg.n, cfg.d)
+    else:
+        rp, ci, va, y = rsinputs.csr_uniform(cfg.n, cfg.d, cfg.nnz_per_row, seed=0)
+        X = rsinputs.csr_to_scipy(rp, ci, va, cfg.n, cfg.d)
+    if args.mode is None:
+        args.mode = "gram"
     op = OV.Operator(X, y, cfg.lam, explicit=(args.mode == "explicit"))
-    OV.solve_momentum(op, cfg.sketch, cfg.tau, cfg.gamma, cfg.beta, 0.0, args.warmup, seed=0)
+    kw = dict(seed=0, subcount_k=cfg.subcount_k)
+    OV.solve_momentum(op, cfg.sketch, cfg.tau, cfg.gamma, cfg.beta, 0.0, args.warmup, **kw)
     t0 = time.perf_counter()
-    OV.solve_momentum(op, cfg.sketch, cfg.tau, cfg.gamma, cfg.beta, 0.0, args.steps, seed=0)
+    OV.solve_momentum(op, cfg.sketch, cfg.tau, cfg.gamma, cfg.beta, 0.0, args.steps, **kw)
     el = time.perf_counter() - t0
     v = args.steps / el
     cores = os.cpu_count()
@@ -161,6 +171,129 @@ def _csr_column_block(np, rowptr, colidx, vals, c0, clen):
     return rp, (colidx[keep] - c0).astype(np.int32), vals[keep]
 
 
+SMEM_PEAK_GBS = 148 * 128 * 1.965   # shared-memory pipe, 128 B/clk/SM x 148 SMs x 1965 MHz (GB/s)
+
+
+def _traffic(cfg, args, cls):
+    """ncu dram__bytes_read.sum + dram__bytes_write.sum per launch of the dominant kernel, from the
+    committed capture summary profiles/traffic.json (None if not captured)."""
+    if args.traffic is not None:
+        return args.traffic
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            t = json.load(f)
+        return t.get(f"{cfg.name}/{args.mode}/{cls}", {}).get("bytes_per_launch")
+    except Exception:
+        return None
+
+
+def _csr_pairs(rs, cfg, host):
+    """Algorithmic work of the CSR Gram kernels for the sketch of iteration 0: the number of merged
+    entries of R S (distinct (row, bucket) pairs) and of lower-triangle pair updates
+    sum_i |v_i| (|v_i| + 1) / 2 (host NumPy over the same data)."""
+    import numpy as np
+    rp, ci = host[0], host[1]
+    dual = cfg.d > cfg.n
+    m = cfg.n if dual else cfg.d
+    coord, bucket, _ = rs.rs_sketch_draw(cfg.sketch, m, cfg.tau, 0, 0, cfg.subcount_k)
+    bmap = np.full(m, -1, np.int64)
+    bmap[coord] = bucket
+    xrow = np.repeat(np.arange(cfg.n, dtype=np.int64), np.diff(rp))
+    r, b = (ci.astype(np.int64), bmap[xrow]) if dual else (xrow, bmap[ci])
+    keep = b >= 0
+    key = np.unique(r[keep] * cfg.tau + b[keep])
+    L = np.bincount(key // cfg.tau)
+    return int(key.size), int((L * (L + 1) // 2).sum())
+
+
+def _roofline(args, cfg, world, kms, kl, dom, prof_ms, host, rs):
+    per = lambda c: max(kms[c] / max(kl[c], 1), 1e-9)   # ms per launch of class c
+    share = kms[dom] / max(prof_ms, 1e-9)
+    hbm = _peaks().get("hbm_gbs", 6556.5)
+    hbm_src = "MEASURED_PEAKS.json hbm_gbs (copy, burst)"
+    dmma_src = ("measured FP64 DMMA peak, profiles/r01_fp64_peak.txt (MEASURED_PEAKS.json has no "
+                "FP64 figure)")
+    n_loc = cfg.n / world
+    ms = per(dom)
+    roof = None
+    if cfg.kind == "dense":
+        if dom == "as" and args.mode == "implicit":
+            w = 2.0 * n_loc * cfg.d * cfg.tau
+            roof = dict(kernel="a3 A S = X^T (X S) (k_tn_gemm / TMA DMMA, split-K reduce, + lambda S)",
+                        bound="tensor", achieved=w / (ms * 1e-3) / 1e12, peak=FP64_DMMA_PEAK,
+                        unit="TFLOP/s", peak_source=dmma_src,
+                        algorithmic_per_launch=f"{w:.3e} flop (2 n d tau)")
+        elif dom == "as":
+            w = n_loc * cfg.d * 8.0
+            roof = dict(kernel="AS pass u = X^T (X S delta) (k_xpass_tma: one TMA-staged streaming "
+                               "read of X per iteration)", bound="hbm",
+                        achieved=w / (ms * 1e-3) / 1e9, peak=hbm, unit="GB/s", peak_source=hbm_src,
+                        algorithmic_per_launch=f"{w:.3e} bytes (n d 8)")
+        elif dom == "gram":
+            w = 2.0 * n_loc * cfg.tau * cfg.tau
+            roof = dict(kernel="Gram (XS)^T XS of one sketch (k_gram_fused gather + DMMA, or "
+                               "k_dense_xs + TMA DMMA GEMM)", bound="tensor",
+                        achieved=w / (ms * 1e-3) / 1e12, peak=FP64_DMMA_PEAK, unit="TFLOP/s",
+                        peak_source=dmma_src, algorithmic_per_launch=f"{w:.3e} flop (2 n tau^2)")
+        elif dom == "factor":
+            slots = kl["update"] / max(kl["factor"], 1)   # iterations (G_k) per group
+            w = float(cfg.tau) ** 3 * slots
+            roof = dict(kernel="batched Cholesky + inverse + W^T W of the group's G_k "
+                               "(k_bfactor_small / k_bfactor_big, DMMA)", bound="tensor",
+                        achieved=w / (ms * 1e-3) / 1e12, peak=FP64_DMMA_PEAK, unit="TFLOP/s",
+                        peak_source=dmma_src,
+                        algorithmic_per_launch=f"{w:.3e} flop (tau^3 per G_k: tau^3/3 Cholesky + "
+                                               f"tau^3/3 inverse + tau^3/3 W^T W, x {slots:.0f} slots)")
+        else:   # explicit: rows of A + GEMV + update
+            w = (cfg.tau * cfg.d + 10 * cfg.d) * 8.0
+            a_mb = cfg.d * cfg.d * 8 / 1e6
+            roof = dict(kernel=f"class {dom}: u = A S delta from the tau sketched rows of A, fused "
+                               "momentum update (k_update_rows)", bound="hbm",
+                        achieved=w / (ms * 1e-3) / 1e9, peak=hbm, unit="GB/s", peak_source=hbm_src,
+                        algorithmic_per_launch=f"{w:.3e} bytes (tau m 8 rows of A + 10 m-vectors)",
+                        note=f"A = {a_mb:.0f} MB ({'fits' if a_mb < 126 else 'exceeds'} the 126 MB L2)")
+    else:
+        nnz = int(host[0][-1])
+        m = cfg.d if cfg.d <= cfg.n else cfg.n
+        if args.mode == "gram" and dom in ("gram", "xs"):
+            ent, pairs = _csr_pairs(rs, cfg, host)
+            if dom == "gram":
+                w = pairs * 16.0 / world
+                roof = dict(kernel="k_gram_bands: G_lower += v_i v_i^T over the merged rows of R S "
+                                   "(shared-memory fp64 read-modify-write per pair)", bound="alu",
+                            achieved=w / (ms * 1e-3) / 1e9, peak=SMEM_PEAK_GBS, unit="GB/s",
+                            peak_source="shared-memory pipe 128 B/clk/SM x 148 SMs x 1965 MHz "
+                                        "(B200_PROFILING.md unit counts and clocks)",
+                            algorithmic_per_launch=f"{w:.3e} bytes (16 B x {pairs:.3e} pair "
+                                                   f"updates, sketch of iteration 0)")
+            else:
+                w = (nnz * 16.0 + ent * 12.0) / world
+                roof = dict(kernel="k_hash_rows: rows of R S, merged and bucket-sorted", bound="hbm",
+                            achieved=w / (ms * 1e-3) / 1e9, peak=hbm, unit="GB/s",
+                            peak_source=hbm_src,
+                            algorithmic_per_launch=f"{w:.3e} bytes (R read 12 B/nnz + cmap 4 B/nnz, "
+                                                   f"{ent:.3e} merged entries written)")
+        elif args.mode == "gram":
+            w = 2.0 * nnz * 12 / world + 4.0 * m * 8
+            roof = dict(kernel=f"class {dom}: A S delta = R^T (R (S delta)) (two SpMV, k_spmv)",
+                        bound="hbm", achieved=w / (ms * 1e-3) / 1e9, peak=hbm, unit="GB/s",
+                        peak_source=hbm_src,
+                        algorithmic_per_launch=f"{w:.3e} bytes (R as CSR and CSC read once)")
+        else:
+            w = 2.0 * nnz * 12 / world + m * cfg.tau * 8.0
+            roof = dict(kernel=("a2+a3 CSR primal A S = X^T (X S) (warp per coordinate, CSC x CSR)"
+                                if m == cfg.d else
+                                "a2+a3 CSR dual A S = X (X^T S) (hashed z_b, warp per row)"),
+                        bound="hbm", achieved=w / (ms * 1e-3) / 1e9, peak=hbm, unit="GB/s",
+                        peak_source=hbm_src,
+                        algorithmic_per_launch=f"{w:.3e} bytes (X as CSR + CSC read once, A S written)")
+    roof["frac"] = roof["achieved"] / roof["peak"]
+    roof["traffic"] = _traffic(cfg, args, dom)
+    roof["avg_launch_ms"] = ms
+    roof["share_of_step"] = share
+    return roof
+
+
 # ------------------------------------------------------------------------------ our arm
 def run_ours(args):
     import numpy as np
@@ -184,7 +317,7 @@ def run_ours(args):
     cfg = rsinputs.CONFIGS[args.config]
     stream = torch.cuda.current_stream()
     if args.mode is None:
-        args.mode = "gram" if cfg.kind == "dense" else "implicit"
+        args.mode = "gram"
     if cfg.kind == "dense":
         Xd, yd = rsinputs.dense_problem(cfg.n, cfg.d, seed=0, col_decay=cfg.col_decay,
                                         noise=cfg.noise, device="cuda")
@@ -276,67 +409,19 @@ def run_ours(args):
         tol_ms = float(t.item())
     rs.rs_destroy(h)
 
-    # roofline of the dominant kernel: the A S contraction (2 n d tau flop per launch)
+    # roofline of the dominant kernel class (live CUDA events inside the graph, per launch)
     kms, kl = rep_prof["kernel_ms"], rep_prof["kernel_launches"]
     dom = max(kms, key=lambda k: kms[k])
-    as_ms = max(kms["as"] / max(kl["as"], 1), 1e-9)
-    flops = 2.0 * cfg.n * cfg.d * cfg.tau / world
-    if args.mode == "implicit" and cfg.kind == "dense":
-        achieved = flops / (as_ms * 1e-3) / 1e12
-        roof = {"kernel": "a3 A S = X^T (X S) contraction (DMMA, split-K reduce, + lambda S)",
-                "bound": "tensor", "achieved": achieved, "peak": FP64_DMMA_PEAK, "unit": "TFLOP/s",
-                "frac": achieved / FP64_DMMA_PEAK, "traffic": args.traffic,
-                "peak_source": "measured FP64 DMMA peak, profiles/r01_fp64_peak.txt "
-                               "(MEASURED_PEAKS.json has no FP64 figure)",
-                "algorithmic_per_launch": f"{flops:.3e} flop (2 n d tau)",
-                "avg_launch_ms": as_ms, "share_of_step": kms["as"] / max(prof_ms, 1e-9)}
-    elif cfg.kind != "dense":
-        nnz = int(host[0][-1])
-        m = cfg.d if cfg.d <= cfg.n else cfg.n
-        byt = 2.0 * nnz * 12 / world + m * cfg.tau * 8.0
-        achieved = byt / (as_ms * 1e-3) / 1e9
-        peak = _peaks().get("hbm_gbs", 6556.5)
-        roof = {"kernel": ("a2+a3 CSR primal A S = X^T (X S) (warp per coordinate, CSC x CSR)"
-                           if m == cfg.d else "a2+a3 CSR dual A S = X (X^T S) (hashed z_b, warp per row)"),
-                "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                "frac": achieved / peak, "traffic": args.traffic,
-                "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy, burst)",
-                "algorithmic_per_launch": f"{byt:.3e} bytes (X as CSR + CSC read once, A S written)",
-                "avg_launch_ms": as_ms, "share_of_step": kms["as"] / max(prof_ms, 1e-9)}
-    elif args.mode == "gram":
-        byt = cfg.n / world * cfg.d * 8.0
-        achieved = byt / (as_ms * 1e-3) / 1e9
-        peak = _peaks().get("hbm_gbs", 6556.5)
-        pre_ms = kms["pre"] / args.steps
-        roof = {"kernel": "AS pass u = X^T (X S delta): one streaming read of X per iteration",
-                "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                "frac": achieved / peak, "traffic": args.traffic,
-                "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy, burst)",
-                "algorithmic_per_launch": f"{byt:.3e} bytes (n d 8)", "avg_launch_ms": as_ms,
-                "share_of_step": kms["as"] / max(prof_ms, 1e-9),
-                "precompute_per_iteration_ms": pre_ms,
-                "precompute": "sketch-ahead group: Grams (XS)^T XS (fused gather + DMMA, 2 n tau^2 "
-                              "flop each) + batched Cholesky/inverse, per iteration"}
-    else:
-        upd_ms = max(kms["update"] / max(kl["update"], 1), 1e-9)
-        byt = (cfg.tau * cfg.d + 10 * cfg.d) * 8.0
-        achieved = byt / (upd_ms * 1e-3) / 1e9
-        peak = _peaks().get("hbm_gbs", 6556.5)
-        a_mb = cfg.d * cfg.d * 8 / 1e6
-        roof = {"kernel": "a3+a6 explicit: u = A S delta from the tau sketched rows of A, fused "
-                          "momentum update", "bound": "hbm", "achieved": achieved, "peak": peak,
-                "unit": "GB/s", "frac": achieved / peak, "traffic": args.traffic,
-                "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy, burst)",
-                "algorithmic_per_launch": f"{byt:.3e} bytes (tau m 8 rows of A + 10 m-vectors)",
-                "avg_launch_ms": upd_ms, "share_of_step": kms["update"] / max(prof_ms, 1e-9),
-                "note": f"A = {a_mb:.0f} MB ({'fits' if a_mb < 126 else 'exceeds'} the 126 MB L2)",
-                "precompute_per_iteration_ms": kms["pre"] / args.steps}
+    roof = _roofline(args, cfg, world, kms, kl, dom, prof_ms, host, rs)
     roof["step_share_by_class"] = {k: kms[k] / max(prof_ms, 1e-9) for k in kms}
     roof["dominant_class"] = dom
 
     # end to end through the public API from pinned host buffers (rank-local shard)
     e2e = None
-    if not args.no_e2e:
+    big = cfg.kind == "dense" and cfg.n * cfg.d * 8 > 32e9   # c5: 65 GB of X
+    if big and not args.no_e2e:
+        e2e = {"skipped": "X is %.1f GB: pinned-host copy not attempted" % (cfg.n * cfg.d * 8e-9)}
+    if not args.no_e2e and not big:
         if cfg.kind == "dense":
             Xh = Xd.cpu().pin_memory()
         else:
@@ -368,7 +453,7 @@ def run_ours(args):
 
     # CPU baseline: the oracle on a bounded sample, rank 0, N = 1 only
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and not big:
         from oracle import solver as OV
         if host is None:
             X = Xd.cpu().numpy()
@@ -420,7 +505,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c2")
     ap.add_argument("--mode", default=None, choices=["implicit", "explicit", "gram"],
-                    help="how A S is formed (default: gram for dense, implicit for CSR)")
+                    help="how A S is formed (default: gram)")
     ap.add_argument("--max-iter-tol", type=int, default=20000)
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-e2e", action="store_true")

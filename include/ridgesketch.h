@@ -132,10 +132,12 @@ enum {
   RS_K_SOLVE = 3,    /* a4 + a5 S^T A S, S^T r, Cholesky, triangular solves, S delta     */
   RS_K_UPDATE = 4,   /* a6 fused momentum update + ||r||^2 + stop flag                   */
   RS_K_GRAM = 5,     /* GRAM mode: G = (XS)^T XS contraction (+ allreduce)               */
-  RS_K_PRE = 6,      /* sketch-ahead group precompute (EXPLICIT / GRAM modes): P sketches, their
-                        A S^T rows or Grams, and the batched Cholesky + inverse of the P
-                        matrices G_k; counted once per group of P iterations                  */
-  RS_K_NCLASSES = 7
+  RS_K_PRE = 6,      /* sketch-ahead group precompute (EXPLICIT / GRAM modes): the P sketches
+                        (and A S^T rows); the P Grams are counted under GRAM (and, CSR, the
+                        hashed rows of R S under XS), per iteration they belong to            */
+  RS_K_FACTOR = 7,   /* sketch-ahead: batched Cholesky + inverse of the P matrices G_k, counted
+                        once per group of P iterations                                        */
+  RS_K_NCLASSES = 8
 };
 
 typedef struct {

@@ -498,12 +498,16 @@ rs_status Problem::csr_gram_workspace(int kind, int tau) {
   return RS_OK;
 }
 
-rs_status Problem::csr_gram_into(const DevSketch& s, double* G) {
+rs_status Problem::csr_gram_into(const DevSketch& s, double* G, cudaEvent_t* ev) {
+  auto mark = [&](int cls, int edge) {
+    if (ev) cudaEventRecordWithFlags(ev[2 * cls + edge], st, cudaEventRecordExternal);
+  };
   CsrData* c = csr;
   const RView R = route == 1 ? RView{c->rowptr, c->colidx, c->vals, c->rows}
                              : RView{c->colptr, c->rowidx, c->cvals, c->cols};
   const int tau = s.tau;
   const int* cmap = s.cmap;
+  mark(RS_K_XS, 0);
   if (s.kind != SK_COUNT) {
     RS_CUDA(launch_cmap_build(s, c->cmap_all, m, ctrl, st));
     cmap = c->cmap_all;
@@ -517,6 +521,8 @@ rs_status Problem::csr_gram_into(const DevSketch& s, double* G) {
       k_hash_rows_heavy<<<c->nheavyR, HR_WARPS * 32, c->hr_smem, st>>>(
           R.ptr, R.idx, R.val, c->heavy_rowsR, cmap, tau, c->hb, c->hv, c->hcnt, ctrl);
     RS_CUDA(cudaGetLastError());
+    mark(RS_K_XS, 1);
+    mark(RS_K_GRAM, 0);
     // a3/a4: (R S)^T (R S), lower triangle
     k_gram_bands<<<dim3((unsigned)c->nbands, (unsigned)c->nchunks), GB_THREADS, c->gb_smem, st>>>(
         R.ptr, c->hcnt, c->hb, c->hv, c->band_a0, c->chunk_r0, c->heavyR, c->heavy_rowsR,
@@ -525,9 +531,13 @@ rs_status Problem::csr_gram_into(const DevSketch& s, double* G) {
     k_gram_band_reduce<<<tau, 256, 0, st>>>(c->gpart, c->nchunks, c->gpart_stride, G, ld_gram, ctrl);
     RS_CUDA(cudaGetLastError());
   } else {
+    mark(RS_K_XS, 1);
+    mark(RS_K_GRAM, 0);
     RS_CUDA(launch_fill(G, (long long)tau * ld_gram, 0.0, st));
   }
-  return allreduce(G, (size_t)tau * ld_gram);
+  RS_TRY(allreduce(G, (size_t)tau * ld_gram));
+  mark(RS_K_GRAM, 1);
+  return RS_OK;
 }
 
 rs_status Problem::csr_gram_apply(const double* v, double* u) {
@@ -548,9 +558,7 @@ rs_status Problem::csr_enqueue_gram(const rs_solve_opts* o, cudaEvent_t* ev) {
   auto mark = [&](int cls, int edge) {
     if (ev) cudaEventRecordWithFlags(ev[2 * cls + edge], st, cudaEventRecordExternal);
   };
-  mark(RS_K_GRAM, 0);
-  RS_TRY(csr_gram_into(sk, Gram));                                                // a2 - a4
-  mark(RS_K_GRAM, 1);
+  RS_TRY(csr_gram_into(sk, Gram, ev));                                            // a2 - a4
   mark(RS_K_SOLVE, 0);
   RS_CUDA(launch_sketched_solve(nullptr, 0, false, Gram, ld_gram, lambda, r, sk, sw, sdelta, ctrl,
                                 st));                                              // a4 + a5

@@ -525,7 +525,13 @@ rs_status Problem::enqueue_iteration(const rs_solve_opts* o, cudaEvent_t* ev) {
 // Group precompute of the sketch-ahead pipeline: sketches S_{k0..k0+ns-1} (k0 = ctrl->k), their
 // A S^T rows (explicit) or Grams (XS)^T XS (gram), and the batched factorisation Ginv = G^{-1}.
 rs_status Problem::enqueue_precompute(const rs_solve_opts* o, int ns, cudaEvent_t* ev) {
-  if (ev) cudaEventRecordWithFlags(ev[2 * RS_K_PRE], st, cudaEventRecordExternal);
+  // ev (optional): the event sets of iterations k0 .. k0+ns-1, 2 * RS_K_NCLASSES each; the group's
+  // sketches and factorisation are recorded on iteration k0's, slot q's Gram on iteration k0+q's
+  auto mark = [&](int q, int cls, int edge) {
+    if (ev) cudaEventRecordWithFlags(ev[(size_t)q * 2 * RS_K_NCLASSES + 2 * cls + edge], st,
+                                     cudaEventRecordExternal);
+  };
+  mark(0, RS_K_PRE, 0);
   RS_CUDA(launch_sketch_batch(skb, ns, o->seed, ctrl, -1, st));                 // a1 x ns
   FactorSrc src{};
   if (mode == RS_AS_EXPLICIT && ASt_slots) {                                     // a2 x ns
@@ -536,13 +542,18 @@ rs_status Problem::enqueue_precompute(const rs_solve_opts* o, int ns, cudaEvent_
   } else if (mode == RS_AS_EXPLICIT) {   // G = S^T A S gathered from A inside the factor kernel
     src.A = A;
     src.lda = lda;
-  } else {                                                                       // Gram x ns
+  }
+  mark(0, RS_K_PRE, 1);
+  if (mode != RS_AS_EXPLICIT) {                                                  // Gram x ns
     for (int q = 0; q < ns; ++q) {
       const DevSketch sq = skb.at(q);
       double* Gq = Gram_slots + (long long)q * gram_stride;
       if (fmt == 1) {
-        RS_TRY(csr_gram_into(sq, Gq));
-      } else if (rows_loc > 0 && gram_fused) {
+        RS_TRY(csr_gram_into(sq, Gq, ev ? ev + (size_t)q * 2 * RS_K_NCLASSES : nullptr));
+        continue;
+      }
+      mark(q, RS_K_GRAM, 0);
+      if (rows_loc > 0 && gram_fused) {
         RS_CUDA(launch_gram_fused(X, ldx, rows_loc, sq, xp_part, Gq, ld_gram, num_sms, ctrl, st));
       } else if (rows_loc > 0) {
         RS_CUDA(launch_dense_xs(X, ldx, rows_loc, sq, XS, ld_xs, ctrl, st));
@@ -551,15 +562,17 @@ rs_status Problem::enqueue_precompute(const rs_solve_opts* o, int ns, cudaEvent_
         RS_CUDA(launch_fill(Gq, gram_stride, 0.0, st));
       }
       RS_TRY(allreduce(Gq, (size_t)gram_stride));
+      mark(q, RS_K_GRAM, 1);
     }
     src.Gram = Gram_slots;
     src.ld_gram = ld_gram;
     src.gram_stride = gram_stride;
     src.lambda = lambda;
   }
+  mark(0, RS_K_FACTOR, 0);
   RS_CUDA(launch_bfactor(src, skb, ns, Ginv_slots, ld_gi, gi_stride, slot_flags, bf_work, ctrl,
                          st));                                                              // a4+a5
-  if (ev) cudaEventRecordWithFlags(ev[2 * RS_K_PRE + 1], st, cudaEventRecordExternal);
+  mark(0, RS_K_FACTOR, 1);
   return RS_OK;
 }
 

@@ -32,7 +32,7 @@ ROUTES = {"auto": 0, "primal": 1, "dual": 2}
 MODES = {"implicit": 0, "explicit": 1, "gram": 2}
 SKETCHES = {"subsample": 0, "count": 1, "subcount": 2}
 MEM_HOST, MEM_DEVICE_COPY, MEM_DEVICE_BORROW = 0, 1, 2
-KERNEL_CLASSES = ("sketch", "xs", "as", "solve", "update", "gram", "pre")
+KERNEL_CLASSES = ("sketch", "xs", "as", "solve", "update", "gram", "pre", "factor")
 
 
 class rs_dist(C.Structure):
@@ -51,8 +51,8 @@ class rs_solve_opts(C.Structure):
 class rs_report(C.Structure):
     _fields_ = [("iterations", C.c_int64), ("converged", C.c_int), ("rel_residual", C.c_double),
                 ("setup_seconds", C.c_double), ("solve_seconds", C.c_double),
-                ("trace_len", C.c_int64), ("kernel_ms", C.c_double * 7),
-                ("kernel_launches", C.c_int64 * 7), ("gpu_launches", C.c_int64)]
+                ("trace_len", C.c_int64), ("kernel_ms", C.c_double * 8),
+                ("kernel_launches", C.c_int64 * 8), ("gpu_launches", C.c_int64)]
 
 
 _P = C.c_void_p
