@@ -98,6 +98,10 @@ void Problem::free_workspace() {
   slot_flags = nullptr;
   dfree(bf_work);
   bf_work = nullptr;
+  dfree(gf_part);
+  gf_part = nullptr;
+  pipe_xg = false;
+  ws_xg = -1;
   pipe = false;
   P = 0;
   ws_depth = -1;
@@ -358,8 +362,9 @@ static bool pipeline_applies(const Problem* p, int tau) {
   return (dense || csr) && tau <= bfactor_max_tau() && !std::getenv("RS_NO_PIPE");
 }
 
-rs_status Problem::ensure_workspace(int kind, int tau, int ksum, int depth) {
-  if (ws_kind == kind && ws_tau == tau && ws_ksum == ksum && ws_depth == depth) return RS_OK;
+rs_status Problem::ensure_workspace(int kind, int tau, int ksum, int depth, bool xg) {
+  if (ws_kind == kind && ws_tau == tau && ws_ksum == ksum && ws_depth == depth && ws_xg == (int)xg)
+    return RS_OK;
   cudaStreamSynchronize(st);
   free_workspace();
   const size_t L = sketch_max_len(kind, (int)m, tau, ksum);
@@ -417,9 +422,14 @@ rs_status Problem::ensure_workspace(int kind, int tau, int ksum, int depth) {
               use_tma ? tg.bm : gp.bm, use_tma ? tg.bn : gp.bn, use_tma ? tg.splits : gp.splits);
   }
   if (fmt == 1) RS_TRY(csr_ensure_workspace(kind, tau, ksum));
-  if (depth > 0) {   // sketch-ahead slots
+  if (depth > 0) {   // sketch-ahead slots (two sets of `depth` for the fused pipeline)
     pipe = true;
+    pipe_xg = xg;
     P = depth;
+    if (xg) {
+      depth *= 2;
+      RS_TRY(dalloc(&gf_part, gram_fused_partials(num_sms)));
+    }
     skb = sk;   // same geometry, `depth` slots
     skb.coord = nullptr; skb.sign = nullptr; skb.bucket = nullptr; skb.bptr = nullptr; skb.cmap = nullptr;
     RS_TRY(dalloc(&skb.coord, L * depth));
@@ -446,7 +456,8 @@ rs_status Problem::ensure_workspace(int kind, int tau, int ksum, int depth) {
   ws_kind = kind;
   ws_tau = tau;
   ws_ksum = ksum;
-  ws_depth = depth;
+  ws_depth = xg ? depth / 2 : depth;
+  ws_xg = (int)xg;
   return RS_OK;
 }
 
@@ -613,6 +624,49 @@ rs_status Problem::enqueue_pipelined_iteration(const rs_solve_opts* o, int slot,
   return RS_OK;
 }
 
+// One group of P iterations of the fused pipeline on slot set g (g = 0, 1): draw the sketches of
+// the other set (iterations k0 + P .. k0 + 2P - 1), run the P iterations -- each X pass also forms
+// the Gram of the other set's slot q -- then factor the other set.
+rs_status Problem::enqueue_group_xg(const rs_solve_opts* o, int g, cudaEvent_t* ev) {
+  auto mark = [&](int q, int cls, int edge) {
+    if (ev) cudaEventRecordWithFlags(ev[(size_t)q * 2 * RS_K_NCLASSES + 2 * cls + edge], st,
+                                     cudaEventRecordExternal);
+  };
+  const int cur = g, nxt = 1 - g;
+  const DevSketch sc = skb.at(cur * P), sn = skb.at(nxt * P);
+  mark(0, RS_K_PRE, 0);
+  RS_CUDA(launch_sketch_batch(sn, P, o->seed, ctrl, -1, st, P));                  // a1 x P (ahead)
+  mark(0, RS_K_PRE, 1);
+  for (int q = 0; q < P; ++q) {
+    const long long cs = (long long)cur * P + q, ns = (long long)nxt * P + q;
+    mark(q, RS_K_SOLVE, 0);
+    RS_CUDA(launch_apply_ginv(Ginv_slots + cs * gi_stride, ld_gi, sc.at(q), slot_flags + cs, r, sw.Gx,
+                              sw.delta, sdelta, ctrl, st));                       // a4 + a5
+    mark(q, RS_K_SOLVE, 1);
+    mark(q, RS_K_AS, 0);
+    double* Gq = Gram_slots + ns * gram_stride;
+    RS_CUDA(launch_xpass_gram(X, ldx, rows_loc, m, sdelta, xp_part, uvec, sn.at(q), gf_part, Gq,
+                              ld_gram, num_sms, ctrl, st));       // X^T X S delta + Gram ahead
+    RS_TRY(allreduce(uvec, (size_t)m));
+    RS_TRY(allreduce(Gq, (size_t)gram_stride));
+    mark(q, RS_K_AS, 1);
+    mark(q, RS_K_UPDATE, 0);
+    RS_CUDA(launch_update_vec(uvec, lambda, sdelta, w, dw, r, dr, m, o->gamma, o->beta, partials,
+                              ctrl, st));                                          // a6 + a7
+    mark(q, RS_K_UPDATE, 1);
+  }
+  FactorSrc src{};
+  src.Gram = Gram_slots + (long long)nxt * P * gram_stride;
+  src.ld_gram = ld_gram;
+  src.gram_stride = gram_stride;
+  src.lambda = lambda;
+  mark(0, RS_K_FACTOR, 0);
+  RS_CUDA(launch_bfactor(src, sn, P, Ginv_slots + (long long)nxt * P * gi_stride, ld_gi, gi_stride,
+                         slot_flags + (long long)nxt * P, bf_work, ctrl, st));   // a4 + a5 ahead
+  mark(0, RS_K_FACTOR, 1);
+  return RS_OK;
+}
+
 static int status_of(int st) {
   switch (st) {
     case ST_DIVERGED: return RS_EDIVERGED;
@@ -630,8 +684,13 @@ rs_status Problem::solve(const rs_solve_opts* o, double* w_out, rs_mem w_mem, do
   RS_CUDA(cudaSetDevice(device));
   const bool want_pipe = pipeline_applies(this, (int)o->tau);
   // iterations per CUDA-graph launch (between host reads of the stop flag)
-  const int chunk = (int)(o->check_every > 0 ? std::min<long long>(o->check_every, 1024)
-                                             : (want_pipe ? (o->tau > 224 ? num_sms : 64) : 16));
+  int chunk = (int)(o->check_every > 0 ? std::min<long long>(o->check_every, 1024)
+                                       : (want_pipe ? (o->tau > 224 ? num_sms : 64) : 16));
+  // fused X pass + Gram ahead (k_xpass_gram1, opt-in RS_XG=1: on c2 it measures 0.69 ms per
+  // iteration vs 0.65 ms for the separate k_xpass_tma + k_gram_fused, profiles/README.md)
+  const bool want_xg = want_pipe && fmt == 0 && mode == RS_AS_GRAM && rows_loc > 0 &&
+                       xpass_gram_ok((int)o->kind, (int)o->tau, d, ldx) && std::getenv("RS_XG");
+  if (want_xg) chunk = std::max(2, chunk & ~1);   // two groups of P = chunk / 2
   int depth = 0;
   if (want_pipe) {   // one batched factorisation wave: <= num_sms slots, <= ~6 GB of slots
     const long long slot_bytes =
@@ -639,8 +698,12 @@ rs_status Problem::solve(const rs_solve_opts* o, double* w_out, rs_mem w_mem, do
         8LL * o->tau * round_up(o->tau, 4) + 16LL * m + 8LL * (long long)bfactor_work_elems((int)o->tau);
     depth = (int)std::max<long long>(1, std::min<long long>({(long long)chunk, (long long)num_sms,
                                                              6000000000LL / slot_bytes}));
+    if (want_xg) {
+      depth = std::min(depth, chunk / 2);
+      chunk = 2 * depth;
+    }
   }
-  RS_TRY(ensure_workspace((int)o->kind, (int)o->tau, ksum, depth));
+  RS_TRY(ensure_workspace((int)o->kind, (int)o->tau, ksum, depth, want_xg));
   // state: w^{-1} = w^0 = 0, r^{-1} = r^0 = -b
   RS_CUDA(launch_fill(w, m, 0.0, st));
   RS_CUDA(launch_fill(dw, m, 0.0, st));
@@ -690,7 +753,10 @@ rs_status Problem::solve(const rs_solve_opts* o, double* w_out, rs_mem w_mem, do
     rs_status s = RS_OK;
     auto evs = [&](int i) { return o->profile ? &prof_events[(size_t)i * 2 * RS_K_NCLASSES] : nullptr; };
     for (int i = 0; i < chunk && s == RS_OK;) {
-      if (pipe) {   // group: precompute ns slots, then ns iterations on them
+      if (pipe_xg) {   // two groups, alternating slot sets
+        s = enqueue_group_xg(o, (i / P) & 1, evs(i));
+        i += P;
+      } else if (pipe) {   // group: precompute ns slots, then ns iterations on them
         const int ns = std::min(P, chunk - i);
         s = enqueue_precompute(o, ns, evs(i));
         for (int q = 0; q < ns && s == RS_OK; ++q) s = enqueue_pipelined_iteration(o, q, evs(i + q));
@@ -729,6 +795,8 @@ rs_status Problem::solve(const rs_solve_opts* o, double* w_out, rs_mem w_mem, do
   RS_CUDA(cudaEventCreate(&t0));
   RS_CUDA(cudaEventCreate(&t1));
   RS_CUDA(cudaEventRecord(t0, st));
+  // fused pipeline: slot set 0 (iterations 0 .. P-1) is formed and factored up front
+  if (pipe_xg && !ctrl_host->done) RS_TRY(enqueue_precompute(o, P, nullptr));
   long long k_prev = 0, graph_launches = 0;
   while (!ctrl_host->done) {
     RS_CUDA(cudaGraphLaunch(graph_exec, st));

@@ -91,6 +91,11 @@ struct Problem {
   long long ld_gi = 0, gi_stride = 0;
   int* slot_flags = nullptr;
   double* bf_work = nullptr;     // tau > 224: per-slot work matrices of the batched factorisation
+  // fused pipeline (dense GRAM, subsample tau <= 200): two slot sets of P; while group g runs on
+  // set g % 2, its X passes also form the Grams of the other set (k_xpass_gram)
+  bool pipe_xg = false;
+  int ws_xg = -1;
+  double* gf_part = nullptr;
   SolveWork sw{};
   double* partials = nullptr;
   cudaGraphExec_t graph_exec = nullptr;
@@ -101,7 +106,8 @@ struct Problem {
   ~Problem();
   void free_workspace();
   rs_status allreduce(double* buf, size_t count);
-  rs_status ensure_workspace(int kind, int tau, int ksum, int depth);
+  rs_status ensure_workspace(int kind, int tau, int ksum, int depth, bool xg = false);
+  rs_status enqueue_group_xg(const rs_solve_opts* o, int g, cudaEvent_t* ev);
   rs_status enqueue_iteration(const rs_solve_opts* o, cudaEvent_t* ev);
   rs_status enqueue_precompute(const rs_solve_opts* o, int nslots, cudaEvent_t* ev);
   rs_status enqueue_pipelined_iteration(const rs_solve_opts* o, int slot, cudaEvent_t* ev);

@@ -330,6 +330,358 @@ __global__ void k_gram_reduce(const double* __restrict__ partials, int nparts, i
   }
 }
 
+
+// ---------------------------------------------------------------------------------------------
+// Fused X pass (dense GRAM, subsample tau <= 200, d <= 3360): one TMA-staged stream of X serves
+//   (1) this iteration's u = X^T (X v), v = S_k delta_k                 (k_xpass_tma's work)
+//   (2) the Gram (X S')^T (X S') of a FUTURE sketch S' = S_{k+P}       (k_gram_fused's work)
+// G_{k+P} does not depend on the iterate (S_k is drawn independently of w^k), so the
+// sketch-ahead pipeline computes it while X streams through shared memory for iteration k: X is
+// read from HBM once per iteration instead of twice (the column gather of k_gram_fused alone
+// touches ~0.8 of X's sectors).  4 rows of X per ring stage = one DMMA k-step of the Gram.
+constexpr int XG_CONS = 15;                 // 16 warps = 4 per SMSP -> 128 registers per thread
+constexpr int XG_THREADS = (XG_CONS + 1) * 32;
+constexpr int XG_R = 4;
+
+
+// Single-CTA variant: 15 consumer warps + 1 producer (4 warps per SMSP -> 128 registers).
+// Per ring stage (4 rows of X): every consumer thread forms its Q partial row dots and gathers <= 2
+// of the stage's 4 x tau sketched values into a compact slab (GF_LD stride, conflict-free DMMA
+// fragments, double-buffered); one named barrier; then the row-dot reduction + axpy, and the warp's
+// <= 22 Gram tiles (row-major order of the lower 8 x 8 tiles, tile list in shared memory, 44
+// accumulator doubles per thread) as one DMMA k-step.  v is read from shared memory; the row
+// loops run over whole 480-column strides (columns >= d are selected to zero, never stored).
+constexpr int XG1_TPW = 22;   // tiles per warp
+
+template <int Q>
+__global__ void __launch_bounds__(XG_THREADS, 1)
+k_xpass_gram1(const double* __restrict__ X, long long ldx, long long rows, long long d,
+              const double* __restrict__ v, double* __restrict__ upart, long long rows_per_cta,
+              int stages, DevSketch skg, double* __restrict__ gpart, const Ctrl* ctrl) {
+  if (ctrl->done) return;
+  constexpr int NC = XG_CONS * 32;                      // consumer threads
+  extern __shared__ __align__(128) double xs_ring[];   // [stages][XG_R * ldx] + pad, v[NC * Q]
+  __shared__ __align__(8) uint64_t full[8], empty[8];
+  __shared__ double red[2][XG_R][XG_CONS];
+  __shared__ __align__(16) double slab[2][XG_R][GF_LD];
+  __shared__ short2 s_tile[XG_CONS][XG1_TPW];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int tau = skg.tau;
+  const int ldxi = (int)ldx;
+  const int stage_elems = XG_R * ldxi;
+  double* sv = xs_ring + (size_t)stages * stage_elems + NC * Q;   // after the ring + a pad
+  for (int j = tid; j < NC * Q; j += XG_THREADS) sv[j] = j < d ? v[j] : 0.0;
+  const int T8 = (tau + 7) / 8, ntiles = T8 * (T8 + 1) / 2;
+  for (int t = tid; t < XG_CONS * XG1_TPW; t += XG_THREADS) {
+    int i = (int)((sqrtf(8.0f * (float)t + 1.0f) - 1.0f) * 0.5f);
+    while ((i + 1) * (i + 2) / 2 <= t) ++i;
+    while (i * (i + 1) / 2 > t) --i;
+    s_tile[t / XG1_TPW][t % XG1_TPW] = make_short2((short)(i * 8), (short)((t - i * (i + 1) / 2) * 8));
+  }
+  // this thread's gather slots e = tid, tid + NC of the 4 x (8 T8) slab: row e / (8 T8), col e % ..
+  const int tw = 8 * T8;
+  int gcol[2], grow[2], gdst[2];
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const int e = tid + h * NC;
+    const int rr = tw ? e / tw : XG_R, b = tw ? e % tw : 0;
+    const int c = (rr < XG_R && b < tau) ? skg.coord[skg.bptr[b]] : -1;
+    grow[h] = rr < XG_R ? rr : -1;
+    gcol[h] = c;
+    gdst[h] = rr < XG_R ? rr * GF_LD + b : -1;
+  }
+  const long long r0 = (long long)blockIdx.x * rows_per_cta;
+  const long long r1 = min(rows, r0 + rows_per_cta);
+  const int nblk = r0 < r1 ? (int)((r1 - r0 + XG_R - 1) / XG_R) : 0;
+  if (tid == 0) {
+    for (int s = 0; s < stages; ++s) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(su32(&full[s])));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(su32(&empty[s])), "r"(XG_CONS));
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+  if (warp == XG_CONS) {   // producer
+    if (lane == 0) {
+      for (int b = 0; b < nblk; ++b) {
+        const int s = b % stages;
+        if (b >= stages) xt_wait(&empty[s], ((b / stages) - 1) & 1);
+        const long long i0 = r0 + (long long)b * XG_R;
+        const int nr = (int)min((long long)XG_R, r1 - i0);
+        const unsigned bytes = (unsigned)(nr * ldx * 8);
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(su32(&full[s])),
+                     "r"(bytes) : "memory");
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n"
+            ::"r"(su32(xs_ring + s * stage_elems)), "l"(X + i0 * ldx), "r"(bytes), "r"(su32(&full[s]))
+            : "memory");
+      }
+    }
+    return;
+  }
+  double acc[Q];
+#pragma unroll
+  for (int q = 0; q < Q; ++q) acc[q] = 0.0;
+  const int t0 = warp * XG1_TPW;
+  const int nt = max(0, min(XG1_TPW, ntiles - t0));
+  double gacc[XG1_TPW][2];
+#pragma unroll
+  for (int q = 0; q < XG1_TPW; ++q) gacc[q][0] = gacc[q][1] = 0.0;
+  const int arow = lane & 3, acol = lane >> 2;
+  int buf = 0;
+  for (int b = 0; b < nblk; ++b) {
+    const int s = b % stages;
+    xt_wait(&full[s], (b / stages) & 1);
+    const double* xs = xs_ring + s * stage_elems;
+    const int nr = (int)min((long long)XG_R, r1 - (r0 + (long long)b * XG_R));
+    // row dots (rows >= nr: stale ring data, their results are never used; columns >= d are
+    // selected away -- the padding of X and the bytes after a row are not guaranteed finite)
+#pragma unroll
+    for (int r = 0; r < XG_R; ++r) {
+      const double* row = xs + r * ldxi + tid;
+      double sdot = 0.0;
+#pragma unroll
+      for (int q = 0; q < Q; ++q) {
+        const double x = row[q * NC];
+        sdot += (tid + q * NC < d ? x : 0.0) * sv[tid + q * NC];
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) sdot += __shfl_xor_sync(0xffffffffu, sdot, o);
+      if (lane == 0) red[buf][r][warp] = sdot;
+    }
+    // gather the sketched columns of the stage into the slab (rows >= nr as zeros)
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+      if (gdst[h] >= 0)
+        slab[buf][0][gdst[h]] = (gcol[h] >= 0 && grow[h] < nr) ? xs[grow[h] * ldxi + gcol[h]] : 0.0;
+    asm volatile("bar.sync 1, %0;\n" ::"n"(NC) : "memory");
+#pragma unroll
+    for (int r = 0; r < XG_R; ++r) {
+      if (r < nr) {
+        double t = 0.0;
+#pragma unroll
+        for (int w = 0; w < XG_CONS; ++w) t += red[buf][r][w];
+        const double* row = xs + r * ldxi + tid;
+#pragma unroll
+        for (int q = 0; q < Q; ++q) acc[q] += t * row[q * NC];
+      }
+    }
+    const double* sl = &slab[buf][arow][acol];
+#pragma unroll
+    for (int q = 0; q < XG1_TPW; ++q) {
+      if (q < nt) {
+        const short2 ij = s_tile[warp][q];
+        dmma_g(gacc[q], sl[ij.x], sl[ij.y]);
+      }
+    }
+    buf ^= 1;
+    __syncwarp();
+    if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(su32(&empty[s])) : "memory");
+  }
+#pragma unroll
+  for (int q = 0; q < Q; ++q) {
+    const long long j = tid + (long long)NC * q;
+    if (j < d) upart[(long long)blockIdx.x * d + j] = acc[q];
+  }
+  double* out = gpart + (long long)blockIdx.x * GF_MAXTAU * GF_MAXTAU;
+#pragma unroll
+  for (int q = 0; q < XG1_TPW; ++q) {
+    if (q < nt) {
+      const short2 ij = s_tile[warp][q];
+      const int a = ij.x + (lane >> 2), c = ij.y + 2 * (lane & 3);
+      if (a < tau) {
+        if (c <= a && c < tau) out[a * GF_MAXTAU + c] = gacc[q][0];
+        if (c + 1 <= a && c + 1 < tau) out[a * GF_MAXTAU + c + 1] = gacc[q][1];
+      }
+    }
+  }
+}
+
+// Cluster-pair variant: the Gram accumulators of a whole tau <= 200 lower triangle (20100 doubles)
+// do not fit one SM's register file next to the X-pass state, so two CTAs of a cluster on two SMs
+// share ONE stream of X: CTA rank 0 multicasts every ring stage (cp.async.bulk ...
+// .multicast::cluster) into both CTAs' shared memory; each CTA owns half of the Gram's 40 x 40
+// regions (every warp 5 x 3 or 5 x 2 DMMA tiles) and the X-pass rows of every other stage.
+// Stage reuse: each CTA's `empty` barrier counts the consumer warps of BOTH CTAs (local arrive +
+// remote arrive through mapa), each CTA's producer re-arms its own `full` barrier with the stage's
+// byte count, so both copies of a stage are free before rank 0 overwrites them.
+__device__ __forceinline__ unsigned cluster_rank() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;\n" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_remote(uint64_t* bar, unsigned rank) {
+  asm volatile(
+      "{\n.reg .b32 ra;\nmapa.shared::cluster.u32 ra, %0, %1;\n"
+      "mbarrier.arrive.release.cluster.shared::cluster.b64 _, [ra];\n}\n" ::"r"(su32(bar)), "r"(rank)
+      : "memory");
+}
+
+template <int Q>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(XG_THREADS, 1)
+k_xpass_gram2(const double* __restrict__ X, long long ldx, long long rows, long long d,
+              const double* __restrict__ v, double* __restrict__ upart, long long rows_per_pair,
+              int stages, DevSketch skg, double* __restrict__ gpart, const Ctrl* ctrl) {
+  if (ctrl->done) return;   // uniform over the grid (ctrl is not written during this kernel)
+  extern __shared__ __align__(128) double xs_ring[];   // [stages][XG_R * ldx]
+  __shared__ __align__(8) uint64_t full[8], empty[8];
+  __shared__ double red[2][XG_R][XG_CONS];
+  __shared__ int s_col[GF_MAXTAU + 8];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const unsigned rank = cluster_rank(), peer = rank ^ 1u;
+  const int tau = skg.tau;
+  for (int b = tid; b < GF_MAXTAU + 8; b += XG_THREADS)
+    s_col[b] = b < tau ? skg.coord[skg.bptr[b]] : -1;
+  const long long pair = blockIdx.x >> 1;
+  const long long r0 = pair * rows_per_pair;
+  const long long r1 = min(rows, r0 + rows_per_pair);
+  const int nblk = r0 < r1 ? (int)((r1 - r0 + XG_R - 1) / XG_R) : 0;
+  const long long stage_elems = (long long)XG_R * ldx;
+  if (tid == 0) {
+    for (int s = 0; s < stages; ++s) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(su32(&full[s])));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(su32(&empty[s])), "r"(2 * XG_CONS));
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+  cluster_sync_all();   // both CTAs' barriers initialised before any remote arrive / multicast
+  if (warp == XG_CONS) {   // producer: re-arm the local full barrier; rank 0 issues the multicast
+    if (lane == 0) {
+      for (int b = 0; b < nblk; ++b) {
+        const int s = b % stages;
+        if (b >= stages) xt_wait(&empty[s], ((b / stages) - 1) & 1);
+        const long long i0 = r0 + (long long)b * XG_R;
+        const int nr = (int)min((long long)XG_R, r1 - i0);
+        const unsigned bytes = (unsigned)(nr * ldx * 8);
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(su32(&full[s])),
+                     "r"(bytes) : "memory");
+        if (rank == 0) {
+          const unsigned short mask = 3;
+          asm volatile(
+              "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
+              " [%0], [%1], %2, [%3], %4;\n"
+              ::"r"(su32(xs_ring + s * stage_elems)), "l"(X + i0 * ldx), "r"(bytes),
+                "r"(su32(&full[s])), "h"(mask) : "memory");
+        }
+      }
+    }
+  } else {
+    // consumers: X pass on the stages b with b % 2 == rank
+    double vr[Q], acc[Q];
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+      const long long j = tid + (long long)(XG_CONS * 32) * q;
+      vr[q] = j < d ? v[j] : 0.0;
+      acc[q] = 0.0;
+    }
+    // Gram: half-region h = 15 rank + warp of the 15 (I >= J) 40 x 40 regions x 2 halves:
+    // region h / 2, tile columns y in [0, 3) (h even) or [3, 5) (h odd)
+    const int ng = (tau + 39) / 40;
+    const int h = XG_CONS * (int)rank + warp;
+    const int t = h >> 1;
+    int I = -1, J = -1;
+    {
+      int u = 0;
+      for (int a = 0; a < ng; ++a)
+        for (int b = 0; b <= a; ++b, ++u)
+          if (u == t) { I = a; J = b; }
+    }
+    const bool gactive = I >= 0;
+    const int y0 = (h & 1) ? 3 : 0, ny = (h & 1) ? 2 : 3;
+    double gacc[5][3][2];
+#pragma unroll
+    for (int x = 0; x < 5; ++x)
+#pragma unroll
+      for (int y = 0; y < 3; ++y) gacc[x][y][0] = gacc[x][y][1] = 0.0;
+    const int arow = lane & 3, acol = lane >> 2;
+    int buf = 0;
+    for (int b = 0; b < nblk; ++b) {
+      const int s = b % stages;
+      xt_wait(&full[s], (b / stages) & 1);
+      const double* xs = xs_ring + s * stage_elems;
+      const long long i0 = r0 + (long long)b * XG_R;
+      const int nr = (int)min((long long)XG_R, r1 - i0);
+      const bool mine = (b & 1) == (int)rank;
+      if (mine) {
+        for (int r = 0; r < nr; ++r) {
+          const double* row = xs + r * ldx;
+          double sdot = 0.0;
+#pragma unroll
+          for (int q = 0; q < Q; ++q) {
+            const long long j = tid + (long long)(XG_CONS * 32) * q;
+            if (j < d) sdot += row[j] * vr[q];
+          }
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) sdot += __shfl_xor_sync(0xffffffffu, sdot, o);
+          if (lane == 0) red[buf][r][warp] = sdot;
+        }
+      }
+      if (gactive) {   // k-step over the stage's 4 rows (rows >= nr read as zero)
+        const bool rok = arow < nr;
+        const double* rp = xs + arow * ldx;
+        double bf[3];
+#pragma unroll
+        for (int y = 0; y < 3; ++y) {
+          const int c = y < ny ? s_col[J * 40 + (y0 + y) * 8 + acol] : -1;
+          bf[y] = (rok && c >= 0) ? rp[c] : 0.0;
+        }
+#pragma unroll
+        for (int x = 0; x < 5; ++x) {
+          const int c = s_col[I * 40 + x * 8 + acol];
+          const double af = (rok && c >= 0) ? rp[c] : 0.0;
+#pragma unroll
+          for (int y = 0; y < 3; ++y)
+            if (y < ny) dmma_g(gacc[x][y], af, bf[y]);
+        }
+      }
+      if (mine) {
+        asm volatile("bar.sync 1, %0;\n" ::"n"(XG_CONS * 32) : "memory");
+        for (int r = 0; r < nr; ++r) {
+          double tt = 0.0;
+#pragma unroll
+          for (int w = 0; w < XG_CONS; ++w) tt += red[buf][r][w];
+          const double* row = xs + r * ldx;
+#pragma unroll
+          for (int q = 0; q < Q; ++q) {
+            const long long j = tid + (long long)(XG_CONS * 32) * q;
+            if (j < d) acc[q] += tt * row[j];
+          }
+        }
+        buf ^= 1;
+      }
+      __syncwarp();
+      if (lane == 0) {
+        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(su32(&empty[s])) : "memory");
+        mbar_arrive_remote(&empty[s], peer);
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+      const long long j = tid + (long long)(XG_CONS * 32) * q;
+      if (j < d) upart[(long long)blockIdx.x * d + j] = acc[q];
+    }
+    if (gactive) {
+      double* out = gpart + pair * GF_MAXTAU * GF_MAXTAU;
+#pragma unroll
+      for (int x = 0; x < 5; ++x) {
+        const int a = I * 40 + x * 8 + (lane >> 2);
+#pragma unroll
+        for (int y = 0; y < 3; ++y) {
+          const int c = J * 40 + (y0 + y) * 8 + 2 * (lane & 3);
+          if (y < ny && a < tau) {
+            if (c < tau) out[a * GF_MAXTAU + c] = gacc[x][y][0];
+            if (c + 1 < tau) out[a * GF_MAXTAU + c + 1] = gacc[x][y][1];
+          }
+        }
+      }
+    }
+  }
+  cluster_sync_all();   // the peer may still arrive on our barriers / receive our multicast
+}
 }  // namespace
 
 bool gram_fused_ok(int kind, int tau) { return kind == SK_SUBSAMPLE && tau <= GF_MAXTAU; }
@@ -382,4 +734,53 @@ cudaError_t launch_xpass(const double* X, long long ldx, long long rows, long lo
   return cudaGetLastError();
 }
 
+bool xpass_gram_ok(int kind, int tau, long long d, long long ldx) {
+  return kind == SK_SUBSAMPLE && tau <= GF_MAXTAU && d <= 7 * XG_CONS * 32 &&
+         2 * XG_R * ldx * 8 <= 200 * 1024;
+}
+
+cudaError_t launch_xpass_gram(const double* X, long long ldx, long long rows, long long d,
+                              const double* v, double* upart, double* u, const DevSketch& skg,
+                              double* gpart, double* G, long long ldg, int num_sms,
+                              const Ctrl* ctrl, cudaStream_t st) {
+  const int nc = xpass_ctas(num_sms) & ~1;   // cluster pairs
+  const int npairs = nc / 2;
+  const long long rpp = std::max<long long>(1, (rows + npairs - 1) / npairs);
+  const long long stage_bytes = (long long)XG_R * ldx * 8;
+  const int stages = (int)std::min<long long>(8, (200 * 1024) / stage_bytes);
+  if (stages < 2 || skg.tau > GF_MAXTAU) return cudaErrorInvalidValue;
+  const size_t smem = (size_t)stages * stage_bytes;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_xpass_gram2<5>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k_xpass_gram2<7>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k_xpass_gram1<5>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k_xpass_gram1<7>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    attr = true;
+  }
+  static const bool pair = std::getenv("RS_XG_PAIR") != nullptr;
+  if (pair) {
+    if (d <= 5 * XG_CONS * 32)
+      k_xpass_gram2<5><<<nc, XG_THREADS, smem, st>>>(X, ldx, rows, d, v, upart, rpp, stages, skg, gpart, ctrl);
+    else
+      k_xpass_gram2<7><<<nc, XG_THREADS, smem, st>>>(X, ldx, rows, d, v, upart, rpp, stages, skg, gpart, ctrl);
+  } else {   // single CTA per SM: stages from 200 KB minus v
+    const int Q = d <= 5 * XG_CONS * 32 ? 5 : 7;
+    const long long extra = 2LL * Q * XG_CONS * 32 * 8;   // read pad after the ring + v
+    const int st1 = (int)std::min<long long>(8, (200 * 1024 - extra) / stage_bytes);
+    if (st1 < 2) return cudaErrorInvalidValue;
+    const size_t smem1 = (size_t)st1 * stage_bytes + (size_t)extra;
+    const long long rpc = std::max<long long>(1, (rows + nc - 1) / nc);
+    if (d <= 5 * XG_CONS * 32)
+      k_xpass_gram1<5><<<nc, XG_THREADS, smem1, st>>>(X, ldx, rows, d, v, upart, rpc, st1, skg, gpart, ctrl);
+    else
+      k_xpass_gram1<7><<<nc, XG_THREADS, smem1, st>>>(X, ldx, rows, d, v, upart, rpc, st1, skg, gpart, ctrl);
+  }
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  k_xpass_reduce<<<(unsigned)((d + 31) / 32), dim3(32, XR_Y), 0, st>>>(upart, nc, d, u, ctrl);
+  if (skg.tau > 0)
+    k_gram_reduce<<<skg.tau, 256, 0, st>>>(gpart, pair ? npairs : nc, skg.tau, G, ldg, ctrl);
+  return cudaGetLastError();
+}
 }  // namespace rs

@@ -86,8 +86,9 @@ cudaError_t launch_sketch(const DevSketch& sk, uint64_t seed, const Ctrl* ctrl, 
                           cudaStream_t st);
 // Batched: slot s of `skb` (DevSketch::at) receives S_{k0 + s}, s < nslots, k0 = ctrl->k at launch
 // (or fixed_k >= 0).  One CTA per slot.
+// kofs: slot s receives S_{ctrl->k + kofs + s} (fixed_k < 0).
 cudaError_t launch_sketch_batch(const DevSketch& skb, int nslots, uint64_t seed, const Ctrl* ctrl,
-                                long long fixed_k, cudaStream_t st);
+                                long long fixed_k, cudaStream_t st, long long kofs = 0);
 size_t sketch_max_len(int kind, int m, int tau, int ksum);
 
 // a2 dense: XS[i, b] = sum_{e in b} sign_e X[i, coord_e],  i < rows, row-major ld_xs (>= tau, pad
@@ -170,6 +171,13 @@ cudaError_t launch_xpass(const double* X, long long ldx, long long rows, long lo
                          const Ctrl* ctrl, cudaStream_t st);
 // Fused gather + Gram (subsample, tau <= 200): G lower = sum_i X[i,C]^T X[i,C], no XS written.
 bool gram_fused_ok(int kind, int tau);
+// Fused X pass: u = X^T (X v) for this iteration AND the Gram (X S')^T (X S') of a future
+// subsample sketch S' (skg.tau == 0: none) from the same TMA-staged rows of X; d <= 3200.
+bool xpass_gram_ok(int kind, int tau, long long d, long long ldx);
+cudaError_t launch_xpass_gram(const double* X, long long ldx, long long rows, long long d,
+                              const double* v, double* upart, double* u, const DevSketch& skg,
+                              double* gpart, double* G, long long ldg, int num_sms,
+                              const Ctrl* ctrl, cudaStream_t st);
 size_t gram_fused_partials(int num_sms);
 cudaError_t gram_init();
 cudaError_t launch_gram_fused(const double* X, long long ldx, long long rows, const DevSketch& sk,

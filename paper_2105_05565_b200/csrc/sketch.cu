@@ -31,11 +31,12 @@ __device__ __forceinline__ bool lt_pair(unsigned long long ka, unsigned ia, unsi
 }
 
 __global__ void __launch_bounds__(kThreads, 1)
-k_sketch_select(DevSketch skb, uint2 key, const Ctrl* ctrl, long long fixed_k, int* err) {
+k_sketch_select(DevSketch skb, uint2 key, const Ctrl* ctrl, long long fixed_k, long long kofs,
+                int* err) {
   if (fixed_k < 0 && ctrl->done) return;
   // slot blockIdx.x of a batch receives the sketch of iteration k0 + blockIdx.x
   const DevSketch sk = skb.at(blockIdx.x);
-  const unsigned it = (unsigned)((fixed_k >= 0 ? fixed_k : ctrl->k) + blockIdx.x);
+  const unsigned it = (unsigned)((fixed_k >= 0 ? fixed_k : ctrl->k + kofs) + blockIdx.x);
   const int m = sk.m, L = sk.len, tid = threadIdx.x;
   extern __shared__ unsigned long long dsm[];
   // layout: [cache: kc u64][sort keys: Lp u64][sort idx: Lp u32]
@@ -155,10 +156,10 @@ k_sketch_select(DevSketch skb, uint2 key, const Ctrl* ctrl, long long fixed_k, i
 }
 
 __global__ void __launch_bounds__(kThreads, 1)
-k_sketch_count(DevSketch skb, uint2 key, const Ctrl* ctrl, long long fixed_k) {
+k_sketch_count(DevSketch skb, uint2 key, const Ctrl* ctrl, long long fixed_k, long long kofs) {
   if (fixed_k < 0 && ctrl->done) return;
   const DevSketch sk = skb.at(blockIdx.x);
-  const unsigned it = (unsigned)((fixed_k >= 0 ? fixed_k : ctrl->k) + blockIdx.x);
+  const unsigned it = (unsigned)((fixed_k >= 0 ? fixed_k : ctrl->k + kofs) + blockIdx.x);
   const int m = sk.m, tau = sk.tau, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   extern __shared__ unsigned long long dsm[];
   unsigned* hist = reinterpret_cast<unsigned*>(dsm);   // [32][tau]
@@ -258,17 +259,17 @@ cudaError_t sketch_init() {
 
 cudaError_t launch_sketch(const DevSketch& sk, uint64_t seed, const Ctrl* ctrl, long long fixed_k,
                           cudaStream_t st) {
-  return launch_sketch_batch(sk, 1, seed, ctrl, fixed_k, st);
+  return launch_sketch_batch(sk, 1, seed, ctrl, fixed_k, st, 0);
 }
 
 cudaError_t launch_sketch_batch(const DevSketch& sk, int nslots, uint64_t seed, const Ctrl* ctrl,
-                                long long fixed_k, cudaStream_t st) {
+                                long long fixed_k, cudaStream_t st, long long kofs) {
   if (nslots < 1) return cudaErrorInvalidValue;
   const uint2 key = make_uint2((unsigned)(seed & 0xffffffffull), (unsigned)(seed >> 32));
   if (sk.kind == SK_COUNT) {
     if (sk.tau > kMaxCountTau) return cudaErrorInvalidValue;
     const size_t smem = (size_t)32 * sk.tau * sizeof(unsigned);
-    k_sketch_count<<<nslots, kThreads, smem, st>>>(sk, key, ctrl, fixed_k);
+    k_sketch_count<<<nslots, kThreads, smem, st>>>(sk, key, ctrl, fixed_k, kofs);
     return cudaGetLastError();
   }
   if (sk.len > kMaxSelect) return cudaErrorInvalidValue;
@@ -277,7 +278,7 @@ cudaError_t launch_sketch_batch(const DevSketch& sk, int nslots, uint64_t seed, 
   while (Lp < sk.len) Lp <<= 1;
   const int kc = sk.m <= kKeyCache ? sk.m : 0;
   const size_t smem = (size_t)kc * 8 + (size_t)Lp * 12;
-  k_sketch_select<<<nslots, kThreads, smem, st>>>(sk, key, ctrl, fixed_k, g_err_flag);
+  k_sketch_select<<<nslots, kThreads, smem, st>>>(sk, key, ctrl, fixed_k, kofs, g_err_flag);
   return cudaGetLastError();
 }
 

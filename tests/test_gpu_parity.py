@@ -336,3 +336,99 @@ def test_dense_large_tau_sketch_ahead(rs, kind, tau, k, mode):
     ref = OV.solve(X, y, 0.5, kind, tau, 1.0, 0.5, 0.0, 10, seed=6, subcount_k=k)
     assert rel(w, ref["w"]) <= 1e-10
     assert rel(r, ref["r"]) <= 1e-10
+
+
+@pytest.mark.parametrize("n,d,tau,check_every", [(1000, 50, 10, 7), (3001, 470, 200, 64), (2999, 1990, 123, 2)])
+def test_dense_fused_xpass_gram(rs, monkeypatch, n, d, tau, check_every):
+    """Opt-in fused pipeline (RS_XG=1, k_xpass_gram1): each X pass also forms the Gram of the
+    sketch P iterations ahead; two alternating slot sets."""
+    monkeypatch.setenv("RS_XG", "1")
+    X, y = rsinputs.dense_problem(n, d, seed=4)
+    X, y = X.numpy(), y.numpy()
+    h = rs.rs_create_dense(X, y, 0.3, mode="gram")
+    try:
+        w, rep = rs.rs_solve(h, "subsample", tau, 1.0, 0.5, 0.0, 11, 8, check_every=check_every)
+        _, r = rs.rs_get_state(h)
+    finally:
+        rs.rs_destroy(h)
+    ref = OV.solve(X, y, 0.3, "subsample", tau, 1.0, 0.5, 0.0, 11, seed=8)
+    assert rep["iterations"] == 11
+    assert rel(w, ref["w"]) <= 1e-10
+    assert rel(r, ref["r"]) <= 1e-10
+
+
+# ------------------------------------------------------------- full size, bench launch config
+def _csr_cfg(name):
+    cfg = rsinputs.CONFIGS[name]
+    if cfg.zipf_a > 0:
+        rp, ci, va, y = rsinputs.csr_zipf(cfg.n, cfg.d, cfg.nnz_per_row, a=cfg.zipf_a, seed=0)
+    else:
+        rp, ci, va, y = rsinputs.csr_uniform(cfg.n, cfg.d, cfg.nnz_per_row, seed=0)
+    return cfg, rp, ci, va, y
+
+
+@pytest.mark.parametrize("name,iters", [("c3", 1), ("c4", 3)])
+def test_csr_configs_full_size(rs, name, iters):
+    """BASELINE.json c3 / c4 at full size in bench.py's default mode (GRAM, sketch-ahead pipeline,
+    check_every = 50): the first iterations equal the oracle's (c3: 5e5 x 5e4 count tau = 500;
+    c4: 2e4 x 1e6 Zipf dual, SubCount tau = 256, k = 4)."""
+    cfg, rp, ci, va, y = _csr_cfg(name)
+    h = rs.rs_create_csr(cfg.n, cfg.d, rp, ci, va, y, cfg.lam, mode="gram")
+    try:
+        w, rep = rs.rs_solve(h, cfg.sketch, cfg.tau, cfg.gamma, cfg.beta, 0.0, iters, seed=0,
+                             subcount_k=cfg.subcount_k, check_every=50, d=cfg.d)
+        it, r = rs.rs_get_state(h)
+    finally:
+        rs.rs_destroy(h)
+    Xs = rsinputs.csr_to_scipy(rp, ci, va, cfg.n, cfg.d)
+    ref = OV.solve(Xs, y, cfg.lam, cfg.sketch, cfg.tau, cfg.gamma, cfg.beta, 0.0, iters, seed=0,
+                   subcount_k=cfg.subcount_k)
+    assert rep["iterations"] == iters
+    assert rel(it, ref["w"]) <= 1e-10
+    assert rel(r, ref["r"]) <= 1e-10
+
+
+def test_config5_full_size_invariants(rs):
+    """BASELINE.json c5 (2e6 x 4096 fp64, 65.5 GB on the device) in EXPLICIT mode (bench's c5
+    line): the sketches are the oracle's bit for bit, beta = 0 steps satisfy the projection
+    constraint S_k^T r^{k+1} = 0, and the maintained residual equals A w - b at sampled
+    coordinates, with A w - b recomputed on the host in fp64 from X streamed back in row chunks."""
+    from oracle import sketch as OS
+    cfg = rsinputs.CONFIGS["c5"]
+    free, _ = torch.cuda.mem_get_info()
+    if free < 80e9:
+        pytest.skip("needs ~80 GB of free device memory")
+    Xd, yd = rsinputs.dense_problem(cfg.n, cfg.d, seed=0, col_decay=True, noise=cfg.noise,
+                                    device="cuda")
+    h = rs.rs_create_dense(Xd, yd, cfg.lam, mode="explicit", borrow=True)
+    try:
+        w, rep = rs.rs_solve(h, "subsample", cfg.tau, 1.0, 0.0, 0.0, 3, seed=0, check_every=3)
+        _, r = rs.rs_get_state(h)
+    finally:
+        rs.rs_destroy(h)
+    assert rep["iterations"] == 3
+    for k in range(3):
+        c, b, s = rs.rs_sketch_draw("subsample", cfg.d, cfg.tau, 0, k)
+        ref = OS.draw("subsample", cfg.d, cfg.tau, k, 0)
+        assert np.array_equal(c, ref["coord"]) and np.array_equal(b, ref["bucket"])
+    c2 = rs.rs_sketch_draw("subsample", cfg.d, cfg.tau, 0, 2)[0]
+    bn = None
+    rng = np.random.default_rng(5)
+    J = np.unique(np.concatenate([rng.choice(cfg.d, 64, replace=False), c2[:16]]))
+    # host fp64: t = X w, u_J = X[:, J]^T t, b_J = X[:, J]^T y, chunk by chunk
+    u = np.zeros(J.size)
+    bJ = np.zeros(J.size)
+    bfull = np.zeros(cfg.d)
+    for i0 in range(0, cfg.n, 100_000):
+        Xc = Xd[i0:i0 + 100_000].cpu().numpy()
+        yc = yd[i0:i0 + 100_000].cpu().numpy()
+        t = Xc @ w
+        u += Xc[:, J].T @ t
+        bJ += Xc[:, J].T @ yc
+        bfull += Xc.T @ yc
+    del Xd, yd
+    torch.cuda.empty_cache()
+    bn = np.linalg.norm(bfull)
+    resid = u + cfg.lam * w[J] - bJ
+    assert np.max(np.abs(r[J] - resid)) <= 1e-9 * bn
+    assert np.max(np.abs(r[c2])) <= 1e-9 * bn   # beta = 0: S_2^T r^3 = 0
