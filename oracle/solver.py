@@ -79,9 +79,10 @@ def sketched_solve(G, g, empty):
 
 
 def solve_momentum(op, kind, tau, gamma=1.0, beta=0.0, tol=0.0, max_iter=100, seed=0,
-                   subcount_k=0, record=False, trace=False):
-    """Alg. 2 with constant (gamma, beta).  Returns dict(w, r, iterations, converged, trace,
-    [records]).  `w` is the system iterate (alpha in the dual route)."""
+                   subcount_k=0, record=False, trace=False, schedule=None):
+    """Alg. 2 with constant (gamma, beta), or with gamma_k, beta_k = schedule(k) (P:L730, an
+    oracle.momentum schedule).  Returns dict(w, r, iterations, converged, trace, [records]).
+    `w` is the system iterate (alpha in the dual route)."""
     m = op.m
     b = op.b
     w_prev = np.zeros(m)
@@ -94,6 +95,8 @@ def solve_momentum(op, kind, tau, gamma=1.0, beta=0.0, tol=0.0, max_iter=100, se
     if nb == 0.0:   # b = 0: w^0 = 0 is the solution, 0 iterations
         return dict(w=w, r=r, iterations=0, converged=True, **out)
     while k < max_iter and np.linalg.norm(r) > tol * nb:
+        if schedule is not None:
+            gamma, beta = schedule(k)  # gamma_k, beta_k
         sk = SK.draw(kind, m, tau, k, seed, subcount_k)
         S = SK.materialize(sk)
         AS = op.AS(S)
@@ -136,10 +139,16 @@ def solve_sketch_project(op, kind, tau, tol=0.0, max_iter=100, seed=0, subcount_
 
 
 def solve(X, y, lam, kind, tau, gamma=1.0, beta=0.0, tol=0.0, max_iter=100, seed=0,
-          subcount_k=0, explicit=False, which=None, record=False, trace=False):
-    """Whole ridge solve: build the system, run Alg. 2, recover w (dual: X^T alpha)."""
+          subcount_k=0, explicit=False, which=None, record=False, trace=False,
+          momentum="constant", eta=0.995):
+    """Whole ridge solve: build the system, run Alg. 2, recover w (dual: X^T alpha).
+    momentum: "constant" (gamma, beta) or an oracle.momentum schedule ("heuristic", "theory",
+    "cor1") with parameter eta."""
+    from . import momentum as MOM
     op = Operator(X, y, lam, which, explicit)
-    res = solve_momentum(op, kind, tau, gamma, beta, tol, max_iter, seed, subcount_k, record, trace)
+    sched = None if momentum == "constant" else MOM.make(momentum, gamma, beta, eta)
+    res = solve_momentum(op, kind, tau, gamma, beta, tol, max_iter, seed, subcount_k, record, trace,
+                         schedule=sched)
     res["route"] = op.route
     res["weights"] = res["w"] if op.route == P.PRIMAL else P.recover_weights(X, res["w"])
     return res
