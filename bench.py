@@ -158,6 +158,7 @@ def _config_dict(cfg, args, world):
                         f"{cfg.sketch} tau={cfg.tau}{extra}, gamma={cfg.gamma}, beta={cfg.beta}, "
                         f"lambda={cfg.lam:g}, tol={cfg.tol:g}",
             "as_mode": args.mode, "tau": cfg.tau, "n": cfg.n, "d": cfg.d,
+            "momentum": args.momentum if args.momentum == "constant" else f"{args.momentum}(eta={args.eta})",
             "parallelism": (f"X {'columns (features)' if dual else 'rows'} sharded over {world} "
                             f"GPU(s), NCCL allreduce of the partial A S"),
             "l2": "inputs larger than L2 (X = %.2f GB > 126 MB)" % (xb / 1e9)}
@@ -361,7 +362,7 @@ def run_ours(args):
     torch.cuda.synchronize()
     h = create(Xd, yd, True)
     common = dict(kind=cfg.sketch, tau=cfg.tau, gamma=cfg.gamma, beta=cfg.beta, seed=0,
-                  subcount_k=cfg.subcount_k, d=cfg.d)
+                  subcount_k=cfg.subcount_k, d=cfg.d, momentum=args.momentum, eta=args.eta)
 
     def barrier():
         if pg is not None:
@@ -507,6 +508,9 @@ def main():
     ap.add_argument("--mode", default=None, choices=["implicit", "explicit", "gram"],
                     help="how A S is formed (default: gram)")
     ap.add_argument("--max-iter-tol", type=int, default=20000)
+    ap.add_argument("--momentum", default="constant", choices=["constant", "heuristic", "theory", "cor1"],
+                    help="momentum schedule (BASELINE.json configs: constant gamma, beta)")
+    ap.add_argument("--eta", type=float, default=0.995)
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")

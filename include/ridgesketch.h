@@ -121,7 +121,22 @@ typedef struct {
   double* trace;        /* host, may be NULL: ||r^k||/||r^0|| for k = 1..trace_cap             */
   int64_t trace_cap;
   int profile;          /* 1: time every kernel class with CUDA events inside the graph       */
+  int momentum;         /* rs_momentum: how (gamma_k, beta_k) evolve           */
+  double eta;           /* schedule parameter eta in (0, 1) (HEURISTIC, THEORY, COR1)          */
 } rs_solve_opts;
+
+/* Momentum parameter schedules (Section "Momentum"):
+ *   CONSTANT : gamma_k = gamma, beta_k = beta ("constant beta setting")
+ *   HEURISTIC: gamma_k = 1, beta_k = 1 - (2 - eta) / ((k+1)(1-eta) + 1)  (Eq. parametersheurististic,
+ *              P:L937-942); eta = 0.995 in the equations, 0.5 in the figure captions (DESIGN R17)
+ *   THEORY   : eta_k = eta while beta < 0.5, then 1 (Eq. parameterswitchtheory; DESIGN
+ *              R24), zeta_k from Thm. 1 (Eq. zeta_kaptheo), mapped to (gamma_k, beta_k) by
+ *              Eq. etalambdatogammbetagen
+ *   COR1     : constant eta < 1, gamma_k = eta / ((k+1)(1-eta) + 1), beta_k as HEURISTIC (Cor. 1,
+ *              Eq. cst_eta_lambda_to_gamma_beta_formula)
+ * gamma and beta of the options are ignored by the non-constant schedules.  Errors: RS_EINVAL for
+ * an unknown schedule or eta outside (0, 1). */
+typedef enum { RS_MOM_CONSTANT = 0, RS_MOM_HEURISTIC = 1, RS_MOM_THEORY = 2, RS_MOM_COR1 = 3 } rs_momentum;
 
 /* Kernel classes reported in rs_report.kernel_ms (summed over the solve) when profile = 1. */
 enum {

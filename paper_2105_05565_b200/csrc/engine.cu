@@ -44,6 +44,7 @@ Problem::~Problem() {
   dfree(sdelta);
   dfree(ctrl);
   dfree(trace_dev);
+  dfree(mom_tab_dev);
   dfree(scratch);
   csr_free();
   if (ctrl_host) cudaFreeHost(ctrl_host);
@@ -337,6 +338,10 @@ static rs_status validate_opts(const Problem* p, const rs_solve_opts* o, int* ks
   if (!(o->tol >= 0.0) || !std::isfinite(o->tol)) return fail(RS_EINVAL, "need finite tol >= 0");
   if (o->max_iter < 0) return fail(RS_EINVAL, "need max_iter >= 0");
   if (o->trace_cap < 0 || (o->trace_cap > 0 && !o->trace)) return fail(RS_EINVAL, "bad trace buffer");
+  if (o->momentum < RS_MOM_CONSTANT || o->momentum > RS_MOM_COR1)
+    return fail(RS_EINVAL, "bad momentum schedule");
+  if (o->momentum != RS_MOM_CONSTANT && !(o->eta > 0.0 && o->eta < 1.0))
+    return fail(RS_EINVAL, "need eta in (0, 1) for a momentum schedule (P:L620)");
   *ksum = 1;
   if (o->kind == RS_SKETCH_SUBCOUNT) {
     long long k = o->subcount_k;
@@ -676,6 +681,34 @@ static int status_of(int st) {
   }
 }
 
+// THEORY schedule (Eq. parameterswitchtheory through Thm. 1, R24): (gamma_k, beta_k)
+// until eta has switched to 1, after which zeta is frozen and the last pair repeats.
+static std::vector<double> theory_table(double eta) {
+  std::vector<double> t;
+  double S = 0.0, e = eta, zeta = 0.0;   // sum_{t<k} eta_t (1 - eta_t), eta_k, zeta_k
+  bool switched = false;
+  for (int k = 0; k < 10000000; ++k) {
+    const double S1 = S + e * (1.0 - e);
+    double e1 = switched ? 1.0 : eta;
+    double z1 = S1 / e1;
+    double g = e / (z1 + 1.0), b = zeta / (z1 + 1.0);
+    if (!switched && b >= 0.5) {
+      switched = true;
+      e1 = 1.0;
+      z1 = S1 / e1;
+      g = e / (z1 + 1.0);
+      b = zeta / (z1 + 1.0);
+    }
+    t.push_back(g);
+    t.push_back(b);
+    if (e == 1.0) break;
+    S = S1;
+    e = e1;
+    zeta = z1;
+  }
+  return t;
+}
+
 rs_status Problem::solve(const rs_solve_opts* o, double* w_out, rs_mem w_mem, double* alpha_out,
                          rs_report* rep) {
   int ksum = 1;
@@ -721,6 +754,18 @@ rs_status Problem::solve(const rs_solve_opts* o, double* w_out, rs_mem w_mem, do
   c.max_iter = o->max_iter;
   c.trace = trace_dev;
   c.trace_cap = o->trace_cap;
+  c.mom_kind = o->momentum == RS_MOM_HEURISTIC ? 1 : o->momentum == RS_MOM_THEORY ? 2
+             : o->momentum == RS_MOM_COR1 ? 3 : 0;
+  c.mom_eta = o->eta;
+  dfree(mom_tab_dev);
+  mom_tab_dev = nullptr;
+  if (o->momentum == RS_MOM_THEORY) {
+    const std::vector<double> tab = theory_table(o->eta);
+    RS_TRY(dalloc(&mom_tab_dev, tab.size()));
+    RS_CUDA(cudaMemcpyAsync(mom_tab_dev, tab.data(), tab.size() * 8, cudaMemcpyHostToDevice, st));
+    c.mom_tab = mom_tab_dev;
+    c.mom_ntab = (long long)tab.size() / 2;
+  }
   c.status = ST_RUNNING;
   if (bnorm2 == 0.0 || o->tol >= 1.0) {   // ||r^0|| <= tol ||r^0||: w = 0 is returned
     c.done = 1;

@@ -59,6 +59,7 @@ struct Problem {
   Ctrl* ctrl = nullptr;
   Ctrl* ctrl_host = nullptr;
   double* trace_dev = nullptr;
+  double* mom_tab_dev = nullptr;   // THEORY momentum schedule table
   double* scratch = nullptr;
   int last_status = 0;
   // per-(kind, tau) workspace

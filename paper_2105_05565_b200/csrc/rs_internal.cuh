@@ -28,7 +28,30 @@ struct Ctrl {
   int pad;
   double* trace;        // device, may be null
   long long trace_cap;
+  // momentum schedule (rs_momentum): 0 constant (kernel arguments), 1 heuristic, 2 table, 3 Cor. 1
+  int mom_kind;
+  int mom_pad;
+  double mom_eta;
+  const double* mom_tab;   // kind 2: (gamma_k, beta_k) pairs, k < mom_ntab; the last pair repeats
+  long long mom_ntab;
 };
+
+// (gamma_k, beta_k) of iteration k = ctrl->k (read by the update kernels before ctrl->k moves on)
+__device__ __forceinline__ void mom_at(const Ctrl* c, double& gamma, double& beta) {
+  const int kind = c->mom_kind;
+  if (kind == 0) return;
+  const long long k = c->k;
+  if (kind == 2) {
+    const long long i = k < c->mom_ntab ? k : c->mom_ntab - 1;
+    gamma = c->mom_tab[2 * i];
+    beta = c->mom_tab[2 * i + 1];
+    return;
+  }
+  const double eta = c->mom_eta;
+  const double den = (double)(k + 1) * (1.0 - eta) + 1.0;
+  beta = 1.0 - (2.0 - eta) / den;
+  gamma = kind == 3 ? eta / den : 1.0;
+}
 
 // ---------------------------------------------------------------------------------------------
 // Philox4x32-10 (Salmon et al., SC'11) -- the sketch-stream generator, DESIGN.md Section 3.

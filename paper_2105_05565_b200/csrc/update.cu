@@ -47,6 +47,7 @@ k_update(const double* __restrict__ ASt, long long ld_as, int tau, const double*
     if (blockIdx.x == 0 && threadIdx.x == 0 && threadIdx.y == 0) ctrl->done = 1;
     return;
   }
+  mom_at(ctrl, gamma, beta);   // schedule (gamma_k, beta_k), rs_momentum
   __shared__ double red[UY][UX + 1];
   __shared__ double s_delta[1024];
   __shared__ bool s_last;
@@ -119,6 +120,7 @@ k_update_rm(const double* __restrict__ AS, long long ld_as, int tau,
     if (blockIdx.x == 0 && threadIdx.x == 0) ctrl->done = 1;
     return;
   }
+  mom_at(ctrl, gamma, beta);   // schedule (gamma_k, beta_k), rs_momentum
   __shared__ double s_delta[1024];
   __shared__ double red[RM_WARPS];
   __shared__ bool s_last;
@@ -183,6 +185,7 @@ k_update_vec(const double* __restrict__ u, double lambda, double* __restrict__ s
     if (blockIdx.x == 0 && threadIdx.x == 0) ctrl->done = 1;
     return;
   }
+  mom_at(ctrl, gamma, beta);   // schedule (gamma_k, beta_k), rs_momentum
   __shared__ double red[VT / 32];
   __shared__ bool s_last;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -238,6 +241,7 @@ k_update_rows(const double* __restrict__ A, long long lda, DevSketch sk,
     if (blockIdx.x == 0 && threadIdx.x == 0 && threadIdx.y == 0) ctrl->done = 1;
     return;
   }
+  mom_at(ctrl, gamma, beta);   // schedule (gamma_k, beta_k), rs_momentum
   extern __shared__ double rw_sm[];   // [len] sd_e, then [len] coord_e (as int)
   __shared__ double red[RW_Y][33];
   __shared__ bool s_last;

@@ -45,7 +45,11 @@ class rs_solve_opts(C.Structure):
     _fields_ = [("kind", C.c_int), ("tau", C.c_int64), ("subcount_k", C.c_int64),
                 ("gamma", C.c_double), ("beta", C.c_double), ("tol", C.c_double),
                 ("max_iter", C.c_int64), ("seed", C.c_uint64), ("check_every", C.c_int64),
-                ("trace", C.c_void_p), ("trace_cap", C.c_int64), ("profile", C.c_int)]
+                ("trace", C.c_void_p), ("trace_cap", C.c_int64), ("profile", C.c_int),
+                ("momentum", C.c_int), ("eta", C.c_double)]
+
+
+MOMENTUM = {"constant": 0, "heuristic": 1, "theory": 2, "cor1": 3}
 
 
 class rs_report(C.Structure):
@@ -187,9 +191,10 @@ def rs_get_info(h):
 
 def rs_solve(h, kind="subsample", tau=1, gamma=1.0, beta=0.0, tol=0.0, max_iter=100, seed=0,
              subcount_k=0, check_every=0, trace_cap=0, profile=False, w_out=None, alpha=False,
-             d=None):
+             d=None, momentum="constant", eta=0.995):
     """Run Alg. 2.  Returns (w, report_dict[, trace]) where w is a NumPy array (host), or the
-    given `w_out` (a CUDA tensor: written on the device)."""
+    given `w_out` (a CUDA tensor: written on the device).  momentum: "constant" (gamma, beta) or
+    a schedule "heuristic" | "theory" | "cor1" with parameter eta (rs_momentum)."""
     m, route = rs_get_info(h)
     o = rs_solve_opts()
     o.kind = SKETCHES[kind]
@@ -205,6 +210,8 @@ def rs_solve(h, kind="subsample", tau=1, gamma=1.0, beta=0.0, tol=0.0, max_iter=
     o.trace = trace.ctypes.data if trace_cap else None
     o.trace_cap = int(trace_cap)
     o.profile = 1 if profile else 0
+    o.momentum = MOMENTUM[momentum]
+    o.eta = float(eta)
     rep = rs_report()
     if w_out is None:
         if d is None:
@@ -285,17 +292,20 @@ def rs_destroy(h):
 class RidgeSketch:
     """RidgeSketch(alpha, algo_mode="mom", solver="subsample", sketch_size=tau) (P:L1256-1261).
 
-    algo_mode: "mom" (constant gamma, beta) or "plain" (gamma=1, beta=0, Alg. 1).
+    algo_mode: "mom" (constant gamma, beta), "plain" (gamma=1, beta=0, Alg. 1), or a
+    momentum schedule "heuristic" | "theory" | "cor1" (parameter eta; rs_momentum).
     solver: "subsample" | "count" | "subcount".  fit(X, y) accepts dense NumPy / torch arrays or a
     scipy.sparse CSR matrix, and stores the weights in `coef_`."""
 
     def __init__(self, alpha=1.0, algo_mode="mom", solver="subsample", sketch_size=10, gamma=1.0,
                  beta=0.5, tol=1e-4, max_iter=10_000, seed=0, subcount_k=0, as_mode="implicit",
-                 route="auto"):
+                 route="auto", eta=0.995):
         self.alpha, self.algo_mode, self.solver, self.sketch_size = alpha, algo_mode, solver, sketch_size
         self.gamma, self.beta = (1.0, 0.0) if algo_mode == "plain" else (gamma, beta)
         self.tol, self.max_iter, self.seed, self.subcount_k = tol, max_iter, seed, subcount_k
         self.as_mode, self.route = as_mode, route
+        self.momentum = algo_mode if algo_mode in ("heuristic", "theory", "cor1") else "constant"
+        self.eta = eta
         self.coef_ = None
         self.report_ = None
 
@@ -317,7 +327,8 @@ class RidgeSketch:
             h = rs_create_dense(X, y, self.alpha, self.route, self.as_mode)
         try:
             w, rep = rs_solve(h, self.solver, self.sketch_size, self.gamma, self.beta, self.tol,
-                              self.max_iter, self.seed, self.subcount_k, d=d)
+                              self.max_iter, self.seed, self.subcount_k, d=d,
+                              momentum=self.momentum, eta=self.eta)
         finally:
             rs_destroy(h)
         self.coef_, self.report_ = w, rep

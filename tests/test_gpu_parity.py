@@ -439,3 +439,53 @@ def test_config5_full_size_invariants(rs):
     assert np.all(err <= 1e-12 * (mag + cfg.lam * np.abs(w[J]))), \
         (err.max(), (err / (mag + 1e-300)).max(), bn)
     assert np.max(np.abs(r[c2])) <= 1e-10 * bn, (np.max(np.abs(r[c2])), bn)   # S_2^T r^3 = 0
+
+
+# ------------------------------------------------------------------ momentum schedules (NEXT-1)
+@pytest.mark.parametrize("momentum,eta", [("heuristic", 0.995), ("theory", 0.995), ("cor1", 0.5),
+                                          ("cor1", 0.9)])
+@pytest.mark.parametrize("mode", ["implicit", "explicit", "gram"])
+def test_momentum_schedules_dense(rs, momentum, eta, mode):
+    """Iteration-dependent (gamma_k, beta_k) of the paper's schedules (rs_momentum) equal the
+    oracle's (oracle/momentum.py) over 260 iterations -- past THEORY's switch (~k = 200)."""
+    X, y = rsinputs.dense_problem(600, 40, seed=12)
+    X, y = X.numpy(), y.numpy()
+    h = rs.rs_create_dense(X, y, 0.2, mode=mode)
+    try:
+        w, rep = rs.rs_solve(h, "subsample", 6, 1.0, 0.0, 0.0, 260, seed=3, check_every=37,
+                             momentum=momentum, eta=eta)
+        _, r = rs.rs_get_state(h)
+    finally:
+        rs.rs_destroy(h)
+    ref = OV.solve(X, y, 0.2, "subsample", 6, tol=0.0, max_iter=260, seed=3, momentum=momentum,
+                   eta=eta)
+    assert rep["iterations"] == 260
+    assert rel(w, ref["w"]) <= 1e-9
+    assert rel(r, ref["r"]) <= 1e-9
+
+
+@pytest.mark.parametrize("momentum", ["heuristic", "theory"])
+def test_momentum_schedules_csr(rs, momentum):
+    n, d = 3000, 300
+    rp, ci, v, y, Xs = _csr_primal(n, d, per_row=20, seed=4)
+    h = rs.rs_create_csr(n, d, rp, ci, v, y, 1e-2, mode="gram")
+    try:
+        w, rep = rs.rs_solve(h, "count", 30, 1.0, 0.0, 0.0, 220, seed=5, momentum=momentum)
+        _, r = rs.rs_get_state(h)
+    finally:
+        rs.rs_destroy(h)
+    ref = OV.solve(Xs, y, 1e-2, "count", 30, tol=0.0, max_iter=220, seed=5, momentum=momentum)
+    assert rel(w, ref["w"]) <= 1e-9
+    assert rel(r, ref["r"]) <= 1e-9
+
+
+def test_momentum_invalid(rs):
+    X, y = _dense(50, 5)
+    h = rs.rs_create_dense(X, y, 1.0)
+    try:
+        with pytest.raises(rs.RSError):
+            rs.rs_solve(h, "subsample", 2, max_iter=3, momentum="cor1", eta=1.0)
+        with pytest.raises(rs.RSError):
+            rs.rs_solve(h, "subsample", 2, max_iter=3, momentum="theory", eta=0.0)
+    finally:
+        rs.rs_destroy(h)
