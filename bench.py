@@ -486,6 +486,8 @@ def run_ours(args):
             "data": "synthetic (seeded; DESIGN.md §5 recipe for BASELINE.json " + cfg.name + ")",
             "config": _config_dict(cfg, args, world),
             "time_to_tol_s": tol_ms / 1e3, "iterations_to_tol": rep_tol["iterations"],
+            "setup_s": rep_tol["setup_seconds"],
+            "setup": "device work of rs_create: b = X^T y (+ explicit A = X^T X + lambda I, CSC copy)",
             "converged": rep_tol["converged"], "rel_residual": rep_tol["rel_residual"],
             "e2e": e2e, "gpu_launches": rep["gpu_launches"], "roofline": roof,
             "cpu_baseline": cpu, "clocks": clk.summary(),

@@ -295,17 +295,23 @@ static rs_status create_dense(rs_problem* out, int64_t n, int64_t d, const doubl
     p->lda = round_up(d, 4);
     s = dalloc(&p->A, (size_t)d * p->lda);
     if (s != RS_OK) return guard(s);
-    GemmPlan gp = plan_tn_gemm(d, d, rows, p->num_sms);
+    // lower-triangle tiles only on the TMA/DMMA contraction (d^2 n flop instead of 2 d^2 n), then
+    // the upper triangle mirrored: A is symmetric
     double* work = nullptr;
-    if (gp.work_elems) {
-      s = dalloc(&work, gp.work_elems);
-      if (s != RS_OK) return guard(s);
-    }
     cudaError_t ce = cudaSuccess;
-    if (rows > 0)
-      ce = launch_tn_gemm(p->X, p->ldx, p->X, p->ldx, d, d, rows, p->A, p->lda, gp, work, nullptr, p->st);
-    else
+    if (rows > 0) {
+      TmaGemm tg{};
+      ce = tma_gemm_plan(&tg, p->X, p->ldx, p->X, p->ldx, d, d, rows, p->num_sms);
+      tg.lower = 1;
+      if (ce == cudaSuccess && tg.work_elems) {
+        s = dalloc(&work, tg.work_elems);
+        if (s != RS_OK) return guard(s);
+      }
+      if (ce == cudaSuccess) ce = tma_gemm_launch(tg, p->A, p->lda, work, nullptr, p->st);
+      if (ce == cudaSuccess) ce = launch_mirror_lower(p->A, p->lda, d, p->st);
+    } else {
       ce = launch_fill(p->A, (long long)d * p->lda, 0.0, p->st);
+    }
     cudaStreamSynchronize(p->st);
     dfree(work);
     if (ce != cudaSuccess) return guard(fail(RS_ECUDA, std::string("A build: ") + cudaGetErrorString(ce)));

@@ -65,7 +65,7 @@ template <int TM, int TN, int WM, int WN, int STAGES>
 __global__ void __launch_bounds__((WM * WN + 1) * 32, 1)
 k_tn_gemm_tma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
               long long M, long long N, long long K, long long k_per_split, double* __restrict__ C,
-              long long ldc, long long split_stride, const Ctrl* ctrl) {
+              long long ldc, long long split_stride, int lower, const Ctrl* ctrl) {
   if (ctrl && ctrl->done) return;
   constexpr int BM = 8 * TM * WM, BN = 8 * TN * WN;
   constexpr int LDA_S = BM + 4, LDB_S = BN + 4;
@@ -79,6 +79,7 @@ k_tn_gemm_tma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const long long m0 = (long long)blockIdx.x * BM, n0 = (long long)blockIdx.y * BN;
+  if (lower && m0 + BM <= n0) return;   // tile strictly above the diagonal (SYRK-shaped use)
   const long long kbeg = (long long)blockIdx.z * k_per_split;
   const long long kend = min(K, kbeg + k_per_split);
   const int nkb = kbeg < kend ? (int)((kend - kbeg + BK - 1) / BK) : 0;
@@ -289,13 +290,36 @@ cudaError_t tma_gemm_launch(const TmaGemm& g, double* C, long long ldc, double* 
 #define RS_LAUNCH(i, ...)                                                                     \
   if (g.variant == i)                                                                         \
     __VA_ARGS__<<<grid, V.threads(), V.smem(), st>>>(ta, tb, g.M, g.N, g.K, g.k_per_split, out, \
-                                                     ldo, so, ctrl);
+                                                     ldo, so, g.lower, ctrl);
   RS_TGEMM(RS_LAUNCH)
 #undef RS_LAUNCH
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess || direct) return e;
   dim3 rg((unsigned)std::min<long long>((g.N + 255) / 256, 64), (unsigned)g.M);
   k_splitk_reduce2<<<rg, 256, 0, st>>>(work, g.splits, so, g.M, g.N, g.ldw, C, ldc, ctrl);
+  return cudaGetLastError();
+}
+
+__global__ void k_mirror_lower(double* A, long long lda, long long m) {
+  // 32 x 32 tiles (I, J), I > J: A[J-tile]^T <- A[I-tile]; diagonal tiles: upper from lower
+  __shared__ double t[32][33];
+  const int I = blockIdx.y, J = blockIdx.x;
+  if (J > I) return;
+  const long long r0 = (long long)I * 32, c0 = (long long)J * 32;
+  for (int y = threadIdx.y; y < 32; y += blockDim.y) {
+    const long long r = r0 + y, c = c0 + threadIdx.x;
+    t[y][threadIdx.x] = (r < m && c < m) ? A[r * lda + c] : 0.0;
+  }
+  __syncthreads();
+  for (int y = threadIdx.y; y < 32; y += blockDim.y) {
+    const long long r = c0 + y, c = r0 + threadIdx.x;   // element (c, r) of the source tile
+    if (r < m && c < m && c > r) A[r * lda + c] = t[threadIdx.x][y];
+  }
+}
+
+cudaError_t launch_mirror_lower(double* A, long long lda, long long m, cudaStream_t st) {
+  const unsigned T = (unsigned)((m + 31) / 32);
+  k_mirror_lower<<<dim3(T, T), dim3(32, 8), 0, st>>>(A, lda, m);
   return cudaGetLastError();
 }
 

@@ -721,7 +721,11 @@ cudaError_t launch_xpass(const double* X, long long ldx, long long rows, long lo
   // ring: R rows per stage (~64 KB), as many stages as fit in ~200 KB (>= 2)
   const long long row_bytes = ldx * 8;
   int R = (int)std::max<long long>(1, std::min<long long>(XT_MAXR, 65536 / row_bytes));
+  static const char* er = std::getenv("RS_XP_R");   // tuning overrides (bench sweeps only)
+  if (er) R = std::max(1, std::min(XT_MAXR, atoi(er)));
   int stages = (int)std::min<long long>(8, (200 * 1024) / (R * row_bytes));
+  static const char* es = std::getenv("RS_XP_STAGES");
+  if (es) stages = std::max(2, std::min(stages, atoi(es)));
   if (!no_tma && stages >= 2 && d <= (long long)XT_CONS * 32 * XT_Q) {
     const size_t smem = (size_t)stages * R * row_bytes;
     k_xpass_tma<<<nc, XT_THREADS, smem, st>>>(X, ldx, rows, d, v, partials, rpc, R, stages, ctrl);

@@ -147,9 +147,12 @@ struct TmaGemm {
   alignas(64) unsigned char tmA[128];
   alignas(64) unsigned char tmB[128];
   int variant = 0, splits = 1, bm = 0, bn = 0;
+  int lower = 0;   // 1: only tiles touching the lower triangle (C symmetric, e.g. A = X^T X)
   long long M = 0, N = 0, K = 0, k_per_split = 0, ldw = 0;
   size_t work_elems = 0;
 };
+// A[j][i] = A[i][j] for i > j (upper triangle from the lower one), m x m, ld lda.
+cudaError_t launch_mirror_lower(double* A, long long lda, long long m, cudaStream_t st);
 cudaError_t tma_gemm_init();
 cudaError_t tma_gemm_plan(TmaGemm* g, const double* Aop, long long lda, const double* Bop,
                           long long ldb, long long M, long long N, long long K, int num_sms);
