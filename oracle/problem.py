@@ -55,3 +55,28 @@ def direct_solve(A, b):
     """Direct SPD solve via Cholesky: A = L L^T, then two triangular solves."""
     c = sla.cho_factor(A, lower=True)
     return sla.cho_solve(c, b)
+
+
+def rbf_kernel(X, sigma):
+    """Gaussian (RBF) kernel matrix K_ij = exp(-||x_i - x_j||^2 / (2 sigma^2)) (P:L175-180,
+    Eq. Gausskernel), from the explicit differences x_i - x_j (one row of K at a time)."""
+    X = np.asarray(X, dtype=np.float64)
+    n = X.shape[0]
+    K = np.empty((n, n))
+    for i in range(n):
+        diff = X - X[i]
+        K[i] = np.exp(-np.einsum("jk,jk->j", diff, diff) / (2.0 * sigma * sigma))
+    return K
+
+
+def build_kernel(X, y, lam, sigma):
+    """Kernel ridge system: K (K + lambda I) alpha = K y (Eq. kernelridge), i.e.
+    A = K^T (K + lambda I), b = K^T y, m = n; the predictor is K alpha."""
+    if not lam > 0:
+        raise ValueError("lambda must be > 0 (P:L36)")
+    K = rbf_kernel(X, sigma)
+    y = np.asarray(y, dtype=np.float64)
+    n = K.shape[0]
+    A = K.T @ (K + lam * np.eye(n))
+    b = K.T @ y
+    return dict(route="kernel", m=n, A=A, b=b, K=K, lam=lam)

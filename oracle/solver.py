@@ -42,6 +42,16 @@ class Operator:
                   else np.asarray(y, dtype=np.float64).copy())
         self.A = P.build(X, y, lam, self.route)["A"] if explicit else None
 
+    @classmethod
+    def from_system(cls, A, b):
+        """An explicit system A w = b (e.g. kernel ridge)."""
+        op = cls.__new__(cls)
+        op.X, op.lam, op.route = None, 0.0, "explicit"
+        op.m = A.shape[0]
+        op.A = np.asarray(A, dtype=np.float64)
+        op.b = np.asarray(b, dtype=np.float64).ravel()
+        return op
+
     def AS(self, S):
         """A S as a dense m x tau array (S: scipy sparse m x tau)."""
         if self.A is not None:
@@ -151,4 +161,19 @@ def solve(X, y, lam, kind, tau, gamma=1.0, beta=0.0, tol=0.0, max_iter=100, seed
                          schedule=sched)
     res["route"] = op.route
     res["weights"] = res["w"] if op.route == P.PRIMAL else P.recover_weights(X, res["w"])
+    return res
+
+
+def solve_kernel(X, y, lam, sigma, kind, tau, gamma=1.0, beta=0.0, tol=0.0, max_iter=100, seed=0,
+                 subcount_k=0, momentum="constant", eta=0.995):
+    """Kernel ridge regression: Alg. 2 on K (K + lambda I) alpha = K y."""
+    from . import momentum as MOM
+    sysk = P.build_kernel(X, y, lam, sigma)
+    op = Operator.from_system(sysk["A"], sysk["b"])
+    sched = None if momentum == "constant" else MOM.make(momentum, gamma, beta, eta)
+    res = solve_momentum(op, kind, tau, gamma, beta, tol, max_iter, seed, subcount_k,
+                         schedule=sched)
+    res["route"] = "kernel"
+    res["weights"] = res["w"]
+    res["K"] = sysk["K"]
     return res
