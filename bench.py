@@ -109,7 +109,13 @@ def run_reference(args):
     from oracle import solver as OV
     cfg = rsinputs.CONFIGS[args.config]
     dev = "cuda" if torch.cuda.is_available() else "cpu"
-    if cfg.kind == "dense":
+    if cfg.kind == "kernel":
+        from oracle import problem as OP
+        Xk, yk = rsinputs.kernel_problem(cfg.n, cfg.d, seed=0, noise=cfg.noise)
+        sysk = OP.build_kernel(Xk, yk, cfg.lam, cfg.extra["sigma"])
+        X, y = None, None
+        args.mode = "explicit"
+    elif cfg.kind == "dense":
         X, y = rsinputs.dense_problem(cfg.n, cfg.d, seed=0, col_decay=cfg.col_decay,
                                       noise=cfg.noise, device=dev)
         X, y = X.cpu().numpy(), y.cpu().numpy()
@@ -121,7 +127,10 @@ def run_reference(args):
         X = rsinputs.csr_to_scipy(rp, ci, va, cfg.n, cfg.d)
     if args.mode is None:
         args.mode = "gram"
-    op = OV.Operator(X, y, cfg.lam, explicit=(args.mode == "explicit"))
+    if cfg.kind == "kernel":
+        op = OV.Operator.from_system(sysk["A"], sysk["b"])
+    else:
+        op = OV.Operator(X, y, cfg.lam, explicit=(args.mode == "explicit"))
     kw = dict(seed=0, subcount_k=cfg.subcount_k)
     OV.solve_momentum(op, cfg.sketch, cfg.tau, cfg.gamma, cfg.beta, 0.0, args.warmup, **kw)
     t0 = time.perf_counter()
@@ -145,8 +154,11 @@ def run_reference(args):
 
 
 def _config_dict(cfg, args, world):
-    dual = cfg.d > cfg.n
-    if cfg.kind == "dense":
+    dual = cfg.d > cfg.n and cfg.kind != "kernel"
+    if cfg.kind == "kernel":
+        xb = cfg.n * cfg.n * 8
+        shape = f"kernel ridge (Gaussian sigma={cfg.extra['sigma']:.3g}, A = K(K + lambda I) n x n)"
+    elif cfg.kind == "dense":
         xb = cfg.n * cfg.d * 8
         shape = "dense"
     else:
@@ -161,7 +173,7 @@ def _config_dict(cfg, args, world):
             "momentum": args.momentum if args.momentum == "constant" else f"{args.momentum}(eta={args.eta})",
             "parallelism": (f"X {'columns (features)' if dual else 'rows'} sharded over {world} "
                             f"GPU(s), NCCL allreduce of the partial A S"),
-            "l2": "inputs larger than L2 (X = %.2f GB > 126 MB)" % (xb / 1e9)}
+            "l2": "inputs larger than L2 (%s = %.2f GB > 126 MB)" % ("A" if cfg.kind == "kernel" else "X", xb / 1e9)}
 
 
 def _csr_column_block(np, rowptr, colidx, vals, c0, clen):
@@ -217,6 +229,9 @@ def _roofline(args, cfg, world, kms, kl, dom, prof_ms, host, rs):
     n_loc = cfg.n / world
     ms = per(dom)
     roof = None
+    if cfg.kind == "kernel":   # EXPLICIT path on the n x n system
+        import rsinputs
+        cfg = rsinputs.Config(cfg.name, "dense", cfg.n, cfg.n, cfg.lam, cfg.sketch, cfg.tau)
     if cfg.kind == "dense":
         if dom == "as" and args.mode == "implicit":
             w = 2.0 * n_loc * cfg.d * cfg.tau
@@ -319,7 +334,15 @@ def run_ours(args):
     stream = torch.cuda.current_stream()
     if args.mode is None:
         args.mode = "gram"
-    if cfg.kind == "dense":
+    if cfg.kind == "kernel":
+        if world > 1:
+            raise SystemExit("kernel ridge route: one GPU (rs_create_kernel v1)")
+        Xk, yk = rsinputs.kernel_problem(cfg.n, cfg.d, seed=0, noise=cfg.noise)
+        Xd, yd = torch.from_numpy(Xk).cuda(), torch.from_numpy(yk).cuda()
+        b0, ln = 0, cfg.n
+        host = None
+        args.mode = "explicit"
+    elif cfg.kind == "dense":
         Xd, yd = rsinputs.dense_problem(cfg.n, cfg.d, seed=0, col_decay=cfg.col_decay,
                                         noise=cfg.noise, device="cuda")
         b0, ln = rs.rs_shard_range(cfg.n, rank, world)
@@ -353,6 +376,8 @@ def run_ours(args):
                     shard_begin=0, shard_len=ln)
 
     def create(X, y, borrow):
+        if cfg.kind == "kernel":
+            return rs.rs_create_kernel(X, y, cfg.lam, cfg.extra["sigma"])
         if cfg.kind == "dense":
             return rs.rs_create_dense(X, y, cfg.lam, mode=args.mode, n=cfg.n, d=cfg.d,
                                       borrow=borrow, dist=dist)
@@ -362,7 +387,8 @@ def run_ours(args):
     torch.cuda.synchronize()
     h = create(Xd, yd, True)
     common = dict(kind=cfg.sketch, tau=cfg.tau, gamma=cfg.gamma, beta=cfg.beta, seed=0,
-                  subcount_k=cfg.subcount_k, d=cfg.d, momentum=args.momentum, eta=args.eta)
+                  subcount_k=cfg.subcount_k, d=cfg.n if cfg.kind == "kernel" else cfg.d,
+                  momentum=args.momentum, eta=args.eta)
 
     def barrier():
         if pg is not None:
@@ -423,7 +449,7 @@ def run_ours(args):
     if big and not args.no_e2e:
         e2e = {"skipped": "X is %.1f GB: pinned-host copy not attempted" % (cfg.n * cfg.d * 8e-9)}
     if not args.no_e2e and not big:
-        if cfg.kind == "dense":
+        if cfg.kind in ("dense", "kernel"):
             Xh = Xd.cpu().pin_memory()
         else:
             Xh = tuple(t.cpu().pin_memory() for t in Xd)
@@ -462,7 +488,13 @@ def run_ours(args):
         else:
             X = rsinputs.csr_to_scipy(host[0], host[1], host[2], cfg.n, cfg.d)
             y = host[3]
-        op = OV.Operator(X, y, cfg.lam, explicit=(args.mode == "explicit"))
+        if cfg.kind == "kernel":
+            from oracle import problem as OP
+            sysk = OP.build_kernel(X, y, cfg.lam, cfg.extra["sigma"])
+            op = OV.Operator.from_system(sysk["A"], sysk["b"])
+            del sysk
+        else:
+            op = OV.Operator(X, y, cfg.lam, explicit=(args.mode == "explicit"))
         kw = dict(seed=0, subcount_k=cfg.subcount_k)
         OV.solve_momentum(op, cfg.sketch, cfg.tau, cfg.gamma, cfg.beta, 0.0, 1, **kw)
         t0 = time.perf_counter()

@@ -109,6 +109,19 @@ rs_status rs_create_csr(rs_problem* out, int64_t n, int64_t d, int64_t nnz_local
                         const double* y, double lambda, rs_route route, rs_as_mode mode,
                         rs_mem mem, const rs_dist* dist);
 
+/* Kernel ridge regression (Section "Using a kernel"): the n x n system
+ * K (K + lambda I) alpha = K y (Eq. kernelridge) with the Gaussian kernel
+ * K_ij = exp(-||x_i - x_j||^2 / (2 sigma^2)) (Eq. Gausskernel), i.e. A = K^T (K + lambda I) and
+ * b = K^T y, built on the device (K from X, A = K K + lambda K on FP64 tensor cores)
+ * and solved by the EXPLICIT-mode path.  X: n x d row-major (ldx >= d), y: n; both copied (mem:
+ * HOST or DEVICE_COPY/BORROW, read only during the call).  rs_solve returns alpha (n doubles) as
+ * the weight vector; predictions on the inputs are K alpha.  Memory: 2 n^2 doubles
+ * during setup, n^2 after.  Errors: RS_EINVAL (n, d < 1, lambda <= 0, sigma <= 0, ldx < d,
+ * non-finite data), RS_EUNSUPPORTED (dist with world > 1: one GPU in this version). */
+rs_status rs_create_kernel(rs_problem* out, int64_t n, int64_t d, const double* X, int64_t ldx,
+                           const double* y, double lambda, double sigma, rs_mem mem,
+                           const rs_dist* dist);
+
 typedef struct {
   rs_sketch_kind kind;
   int64_t tau;          /* sketch size, 1 <= tau <= m                                         */

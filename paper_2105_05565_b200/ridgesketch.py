@@ -64,6 +64,8 @@ _lib.rs_create_dense.argtypes = [C.POINTER(_P), C.c_int64, C.c_int64, _P, C.c_in
                                  C.c_int, C.c_int, C.c_int, C.POINTER(rs_dist)]
 _lib.rs_create_csr.argtypes = [C.POINTER(_P), C.c_int64, C.c_int64, C.c_int64, _P, _P, _P, _P,
                                C.c_double, C.c_int, C.c_int, C.c_int, C.POINTER(rs_dist)]
+_lib.rs_create_kernel.argtypes = [C.POINTER(_P), C.c_int64, C.c_int64, _P, C.c_int64, _P, C.c_double,
+                                  C.c_double, C.c_int, C.POINTER(rs_dist)]
 _lib.rs_solve.argtypes = [_P, C.POINTER(rs_solve_opts), _P, C.c_int, _P, C.POINTER(rs_report)]
 _lib.rs_get_state.argtypes = [_P, _P, _P, C.c_int]
 _lib.rs_get_info.argtypes = [_P, C.POINTER(C.c_int64), C.POINTER(C.c_int)]
@@ -179,6 +181,21 @@ def rs_create_csr(n, d, rowptr, colidx, vals, y, lam, route="auto", mode="implic
     st = _lib.rs_create_csr(C.byref(h), n, d, nnz, rp, cp, vp, yp, float(lam), ROUTES[route],
                             MODES[mode], mem, C.byref(ds) if ds is not None else None)
     _check(st, "rs_create_csr")
+    return h
+
+
+def rs_create_kernel(X, y, lam, sigma, dist=None):
+    """Kernel ridge regression problem (rs_create_kernel): A = K (K + lam I), b = K y with the
+    Gaussian kernel of bandwidth sigma; rs_solve then returns alpha (n)."""
+    n, d = X.shape
+    xp, mem, xk, dev = _arr(X, np.float64)
+    yp, ymem, yk, ydev = _arr(y, np.float64)
+    if dev != ydev:
+        raise ValueError("X and y must both be host or both be device arrays")
+    h = _P()
+    ds = _dist(dist)
+    _check(_lib.rs_create_kernel(C.byref(h), n, d, xp, d, yp, float(lam), float(sigma), mem,
+                                 C.byref(ds) if ds is not None else None), "rs_create_kernel")
     return h
 
 

@@ -45,6 +45,11 @@ CONFIGS = {
                  nnz_per_row=500, zipf_a=1.1),
     "c5": Config("c5", "dense", 2_000_000, 4096, 1e-4 * 2_000_000, "subsample", 1024,
                  col_decay=True),
+    # Kernel ridge stand-in (not a BASELINE.json config): California-Housing-shaped
+    # (n = 20640, d = 8), Gaussian kernel with the median-distance bandwidth
+    # sigma^2 = E||x - x'||^2 / 2 = d, subsample tau = m / 20.
+    "k1": Config("k1", "kernel", 20_640, 8, 1e-3, "subsample", 1032, noise=0.1,
+                 extra={"sigma": 8 ** 0.5}),
 }
 
 
@@ -117,3 +122,13 @@ def csr_zipf(n, d, nnz_per_row, a=1.1, seed=0):
 def csr_to_scipy(rowptr, colidx, vals, n, d):
     import scipy.sparse as sp
     return sp.csr_matrix((vals, colidx, rowptr), shape=(n, d))
+
+
+def kernel_problem(n, d, seed=0, noise=0.1):
+    """Inputs for the kernel ridge route: X ~ N(0,1) (n x d), y = sin(X w*) + noise N(0,1),
+    w* ~ N(0, 1/d) (a smooth nonlinear target the Gaussian kernel can fit)."""
+    rng = np.random.default_rng(seed)
+    X = rng.standard_normal((n, d))
+    w = rng.standard_normal(d) / np.sqrt(d)
+    y = np.sin(X @ w) + noise * rng.standard_normal(n)
+    return X, y

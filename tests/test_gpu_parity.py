@@ -489,3 +489,52 @@ def test_momentum_invalid(rs):
             rs.rs_solve(h, "subsample", 2, max_iter=3, momentum="theory", eta=0.0)
     finally:
         rs.rs_destroy(h)
+
+
+# ------------------------------------------------------------------ kernel ridge route (NEXT-4)
+@pytest.mark.parametrize("kind,tau,k,beta", [("subsample", 20, 0, 0.5), ("count", 17, 0, 0.5),
+                                             ("subcount", 12, 3, 0.0), ("subsample", 240, 0, 0.5)])
+def test_kernel_ridge_parity(rs, kind, tau, k, beta):
+    """rs_create_kernel builds K (Eq. Gausskernel), A = K (K + lambda I), b = K y on the device;
+    the EXPLICIT iterations then equal the oracle's (oracle/problem.build_kernel)."""
+    rng = np.random.default_rng(7)
+    n, d = 301, 5
+    X = rng.standard_normal((n, d))
+    y = np.sin(X @ rng.standard_normal(d)) + 0.05 * rng.standard_normal(n)
+    lam, sigma = 0.2, 1.7
+    h = rs.rs_create_kernel(X, y, lam, sigma)
+    try:
+        a, rep = rs.rs_solve(h, kind, tau, 1.0, beta, 0.0, 30, seed=4, subcount_k=k)
+        _, r = rs.rs_get_state(h)
+    finally:
+        rs.rs_destroy(h)
+    ref = OV.solve_kernel(X, y, lam, sigma, kind, tau, 1.0, beta, 0.0, 30, seed=4, subcount_k=k)
+    assert rep["iterations"] == 30
+    assert rel(a, ref["w"]) <= 1e-10
+    assert rel(r, ref["r"]) <= 1e-10
+
+
+def test_kernel_ridge_converges_and_predicts(rs):
+    rng = np.random.default_rng(8)
+    n, d = 200, 3
+    X = rng.standard_normal((n, d))
+    y = np.cos(X[:, 0]) + 0.5 * X[:, 1]
+    lam, sigma = 1.0, 1.0
+    h = rs.rs_create_kernel(torch.from_numpy(X).cuda(), torch.from_numpy(y).cuda(), lam, sigma)
+    try:
+        a, rep = rs.rs_solve(h, "subsample", 40, 1.0, 0.0, 1e-11, 100000, seed=1)
+    finally:
+        rs.rs_destroy(h)
+    s = OP.build_kernel(X, y, lam, sigma)
+    a_star = OP.direct_solve(s["A"], s["b"])
+    assert rep["converged"]
+    assert rel(a, a_star) <= 1e-6
+    assert rel(s["K"] @ a, s["K"] @ a_star) <= 1e-7   # predictions on the inputs (P:L171-173)
+
+
+def test_kernel_invalid(rs):
+    X = np.zeros((4, 2))
+    with pytest.raises(rs.RSError):
+        rs.rs_create_kernel(X, np.zeros(4), 1.0, 0.0)
+    with pytest.raises(rs.RSError):
+        rs.rs_create_kernel(X, np.zeros(4), -1.0, 1.0)
