@@ -733,7 +733,8 @@ rs_status Problem::solve(const rs_solve_opts* o, double* w_out, rs_mem w_mem, do
   int depth = 0;
   if (want_pipe) {   // one batched factorisation wave: <= num_sms slots, <= ~6 GB of slots
     const long long slot_bytes =
-        8LL * o->tau * (mode == RS_AS_EXPLICIT ? round_up(m, 4) : round_up(o->tau, 4)) +
+        8LL * o->tau * (mode == RS_AS_EXPLICIT ? (o->kind == RS_SKETCH_COUNT ? round_up(m, 4) : 0)
+                                               : round_up(o->tau, 4)) +
         8LL * o->tau * round_up(o->tau, 4) + 16LL * m + 8LL * (long long)bfactor_work_elems((int)o->tau);
     depth = (int)std::max<long long>(1, std::min<long long>({(long long)chunk, (long long)num_sms,
                                                              6000000000LL / slot_bytes}));
