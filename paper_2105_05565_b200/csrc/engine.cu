@@ -83,6 +83,10 @@ void Problem::free_workspace() {
   sw = SolveWork{};
   dfree(partials);
   partials = nullptr;
+  dfree(rows_part);
+  rows_part = nullptr;
+  dfree(rows_cnt);
+  rows_cnt = nullptr;
   dfree(skb.coord);
   dfree(skb.sign);
   dfree(skb.bucket);
@@ -299,9 +303,18 @@ static rs_status create_dense(rs_problem* out, int64_t n, int64_t d, const doubl
     // the upper triangle mirrored: A is symmetric
     double* work = nullptr;
     cudaError_t ce = cudaSuccess;
-    if (rows > 0) {
+    if (rows > 0 && std::getenv("RS_A_BUILD_CPASYNC")) {   // comparison path (k_tn_gemm, full)
+      GemmPlan gp = plan_tn_gemm(d, d, rows, p->num_sms);
+      if (gp.work_elems) {
+        s = dalloc(&work, gp.work_elems);
+        if (s != RS_OK) return guard(s);
+      }
+      ce = launch_tn_gemm(p->X, p->ldx, p->X, p->ldx, d, d, rows, p->A, p->lda, gp, work, nullptr, p->st);
+    } else if (rows > 0) {
       TmaGemm tg{};
       ce = tma_gemm_plan(&tg, p->X, p->ldx, p->X, p->ldx, d, d, rows, p->num_sms);
+      if (std::getenv("RS_VERBOSE"))
+        fprintf(stderr, "[rs] A build: TMA variant %d (%dx%d), splits %d\n", tg.variant, tg.bm, tg.bn, tg.splits);
       tg.lower = 1;
       if (ce == cudaSuccess && tg.work_elems) {
         s = dalloc(&work, tg.work_elems);
@@ -464,6 +477,11 @@ rs_status Problem::ensure_workspace(int kind, int tau, int ksum, int depth, bool
   RS_TRY(dalloc(&sw.Gx, solve_gx_elems(tau)));
   RS_TRY(dalloc(&sw.delta, tau));
   RS_TRY(dalloc(&partials, update_partials(m)));
+  if (mode == RS_AS_EXPLICIT && fmt == 0) {   // split-row update scratch (k_update_rows)
+    RS_TRY(dalloc(&rows_part, update_rows_scratch(m)));
+    RS_TRY(dalloc(&rows_cnt, update_rows_counters(m)));
+    RS_CUDA(cudaMemsetAsync(rows_cnt, 0, update_rows_counters(m) * sizeof(int), st));
+  }
   ws_kind = kind;
   ws_tau = tau;
   ws_ksum = ksum;
@@ -615,7 +633,7 @@ rs_status Problem::enqueue_pipelined_iteration(const rs_solve_opts* o, int slot,
                             sdelta, w, dw, r, dr, m, o->gamma, o->beta, partials, ctrl, st));  // a6+a7
     else   // A S delta from the sketched rows of A
       RS_CUDA(launch_update_rows(A, lda, sq, sw.delta, sdelta, w, dw, r, dr, m, o->gamma, o->beta,
-                                 partials, ctrl, st));                                        // a6+a7
+                                 partials, rows_part, rows_cnt, num_sms, ctrl, st));          // a6+a7
     mark(RS_K_UPDATE, 1);
     return RS_OK;
   }

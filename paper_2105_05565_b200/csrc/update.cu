@@ -9,6 +9,8 @@
 //   ||r^{k+1}||^2 is reduced deterministically (per-block partials, then the last block sums them
 // in a fixed order), and the last block applies the stop rule ||r^k|| <= tol ||r^0|| (P:L248-251,
 // DESIGN.md R1), the divergence guard and the iteration counter.
+#include <algorithm>
+
 #include "rs_internal.cuh"
 
 namespace rs {
@@ -229,29 +231,39 @@ k_update_vec(const double* __restrict__ u, double lambda, double* __restrict__ s
 // Explicit A, few sketch entries: block = 32 coordinates j x 32 entry slices; u_j =
 // sum_e sd_e A[coord_e][j] with sd_e = sign_e delta[bucket_e] staged in shared memory (rows of A are
 // contiguous: coalesced over j, L2-resident when A fits).
-constexpr int RW_Y = 32;
+constexpr int RW_Y = 8;
+constexpr int RW_MAXS = 16;
+// u = A S delta over the rows e of slot `sk` (A symmetric: row coord_e = column), split over
+// gridDim.y row ranges: block (cb, sp) sums rows e in its range for columns 32 cb .. 32 cb + 31
+// into upart[sp][j]; the last split of a column block (counter cnt[cb]) adds the splits in order
+// (deterministic), applies the momentum update to its 32 coordinates and contributes ||r||^2;
+// the last column block finishes the iteration.
 __global__ void __launch_bounds__(32 * RW_Y)
 k_update_rows(const double* __restrict__ A, long long lda, DevSketch sk,
               const double* __restrict__ delta, double* __restrict__ sdelta,
               double* __restrict__ w, double* __restrict__ dw, double* __restrict__ r,
               double* __restrict__ dr, long long m, double gamma, double beta,
-              double* __restrict__ partials, Ctrl* ctrl) {
+              double* __restrict__ partials, double* __restrict__ upart, int* __restrict__ cnt,
+              Ctrl* ctrl) {
   if (ctrl->done) return;
   if (ctrl->status >= ST_NOTSPD) {
-    if (blockIdx.x == 0 && threadIdx.x == 0 && threadIdx.y == 0) ctrl->done = 1;
+    if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0 && threadIdx.y == 0) ctrl->done = 1;
     return;
   }
   mom_at(ctrl, gamma, beta);   // schedule (gamma_k, beta_k), rs_momentum
-  extern __shared__ double rw_sm[];   // [len] sd_e, then [len] coord_e (as int)
+  extern __shared__ double rw_sm[];   // [span] sd_e, then [span] coord_e (as int)
   __shared__ double red[RW_Y][33];
   __shared__ bool s_last;
   const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * 32 + tx;
   const int len = sk.bptr[sk.tau];
-  int* s_coord = reinterpret_cast<int*>(rw_sm + len);
-  for (int e = tid; e < len; e += 32 * RW_Y) {
-    const double dv = delta[sk.bucket[e]];
-    rw_sm[e] = sk.sign[e] > 0 ? dv : -dv;
-    s_coord[e] = sk.coord[e];
+  const int ns = gridDim.y, sp = blockIdx.y;
+  const int per = (len + ns - 1) / ns;
+  const int e0 = min(len, sp * per), e1 = min(len, e0 + per), span = e1 - e0;
+  int* s_coord = reinterpret_cast<int*>(rw_sm + per);
+  for (int e = tid; e < span; e += 32 * RW_Y) {
+    const double dv = delta[sk.bucket[e0 + e]];
+    rw_sm[e] = sk.sign[e0 + e] > 0 ? dv : -dv;
+    s_coord[e] = sk.coord[e0 + e];
   }
   __syncthreads();
   const long long j = (long long)blockIdx.x * 32 + tx;
@@ -259,16 +271,29 @@ k_update_rows(const double* __restrict__ A, long long lda, DevSketch sk,
   if (j < m) {
     const double* Aj = A + j;
 #pragma unroll 4
-    for (int e = ty; e < len; e += RW_Y) acc += rw_sm[e] * Aj[(long long)s_coord[e] * lda];
+    for (int e = ty; e < span; e += RW_Y) acc += rw_sm[e] * Aj[(long long)s_coord[e] * lda];
   }
   red[ty][tx] = acc;
   __syncthreads();
   if (ty == 0) {
+    double u = 0.0;
+#pragma unroll
+    for (int q = 0; q < RW_Y; ++q) u += red[q][tx];
+    if (j < m) upart[(long long)sp * m + j] = u;
+    __threadfence();
+    __syncwarp();
+    if (tx == 0) s_last = atomicAdd(&cnt[blockIdx.x], 1) == ns - 1;
+    __syncwarp();
+  }
+  __syncthreads();
+  if (!s_last) return;
+  // last split of this column block: u_j = sum of the splits in order, then the update
+  if (ty == 0) {
+    __threadfence();
     double r2 = 0.0;
     if (j < m) {
       double u = 0.0;
-#pragma unroll
-      for (int q = 0; q < RW_Y; ++q) u += red[q][tx];
+      for (int q = 0; q < ns; ++q) u += __ldcg(&upart[(long long)q * m + j]);
       const double drj = beta * dr[j] - gamma * u;
       const double rj = r[j] + drj;
       dr[j] = drj;
@@ -283,6 +308,7 @@ k_update_rows(const double* __restrict__ A, long long lda, DevSketch sk,
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) r2 += __shfl_down_sync(0xffffffffu, r2, o);
     if (tx == 0) {
+      cnt[blockIdx.x] = 0;
       partials[blockIdx.x] = r2;
       __threadfence();
       const unsigned prev = atomicAdd(&ctrl->arrive, 1u);
@@ -292,9 +318,9 @@ k_update_rows(const double* __restrict__ A, long long lda, DevSketch sk,
   __syncthreads();
   if (!s_last) return;
   __threadfence();
-  double s = 0.0;
-  for (unsigned q = tid; q < gridDim.x; q += 32 * RW_Y) s += __ldcg(&partials[q]);
-  red[ty][tx] = s;
+  double s2 = 0.0;
+  for (unsigned q = tid; q < gridDim.x; q += 32 * RW_Y) s2 += __ldcg(&partials[q]);
+  red[ty][tx] = s2;
   __syncthreads();
   if (tid == 0) {
     double tot = 0.0;
@@ -310,15 +336,22 @@ cudaError_t update_init() {
   return cudaFuncSetAttribute(k_update_rows, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
 }
 
+size_t update_rows_scratch(long long m) { return (size_t)RW_MAXS * (size_t)m; }
+size_t update_rows_counters(long long m) { return (size_t)((m + 31) / 32); }
+
 cudaError_t launch_update_rows(const double* A, long long lda, const DevSketch& sk,
                                const double* delta, double* sdelta, double* w, double* dw,
                                double* r, double* dr, long long m, double gamma, double beta,
-                               double* partials, Ctrl* ctrl, cudaStream_t st) {
-  const size_t smem = (size_t)sk.len * 12;
+                               double* partials, double* upart, int* cnt, int num_sms, Ctrl* ctrl,
+                               cudaStream_t st) {
+  const long long cb = (m + 31) / 32;
+  int ns = (int)std::max<long long>(1, std::min<long long>(RW_MAXS, (2LL * num_sms + cb - 1) / cb));
+  ns = std::max(1, std::min(ns, sk.len / 8));
+  const int per = (sk.len + ns - 1) / ns;
+  const size_t smem = (size_t)per * 12;
   if (smem > 200 * 1024) return cudaErrorInvalidValue;
-  const unsigned g = (unsigned)((m + 31) / 32);
-  k_update_rows<<<g, dim3(32, RW_Y), smem, st>>>(A, lda, sk, delta, sdelta, w, dw, r, dr, m, gamma,
-                                                 beta, partials, ctrl);
+  k_update_rows<<<dim3((unsigned)cb, (unsigned)ns), dim3(32, RW_Y), smem, st>>>(
+      A, lda, sk, delta, sdelta, w, dw, r, dr, m, gamma, beta, partials, upart, cnt, ctrl);
   return cudaGetLastError();
 }
 
