@@ -78,7 +78,10 @@ typedef enum {
  *   HOST          : host memory; copied (H2D) into library-owned device memory.
  *   DEVICE_COPY   : device memory; copied (D2D) into library-owned device memory.
  *   DEVICE_BORROW : device memory used in place; the caller keeps it alive and unchanged until
- *                   rs_destroy.  (Dense X is copied anyway if ldx is not a multiple of 4.)   */
+ *                   rs_destroy.  (Dense X is copied anyway if ldx is not a multiple of 4.)
+ * Device inputs must be complete when the call is made: the library works on its own stream
+ * (or rs_dist.cuda_stream), which is not ordered with the producer's stream -- synchronise the
+ * producer (or pass its stream in rs_dist) first. */
 typedef enum { RS_MEM_HOST = 0, RS_MEM_DEVICE_COPY = 1, RS_MEM_DEVICE_BORROW = 2 } rs_mem;
 
 /* Process layout (one process per GPU).  NULL means world = 1 on the current device with the

@@ -117,7 +117,9 @@ def _is_torch(x):
 
 
 def _arr(x, dtype):
-    """(pointer, mem, keepalive, is_device) for a NumPy array or torch tensor."""
+    """(pointer, mem, keepalive, is_device) for a NumPy array or torch tensor.  A CUDA tensor's
+    producer stream is synchronised first: the library works on its own stream, which is not
+    ordered with torch's (include/ridgesketch.h: device inputs must be complete at the call)."""
     if _is_torch(x):
         import torch
         tdt = {np.float64: torch.float64, np.int64: torch.int64, np.int32: torch.int32}[dtype]
@@ -126,6 +128,8 @@ def _arr(x, dtype):
         if not x.is_contiguous():
             x = x.contiguous()
         dev = x.is_cuda
+        if dev:
+            torch.cuda.current_stream(x.device).synchronize()
         return x.data_ptr(), (MEM_DEVICE_COPY if dev else MEM_HOST), x, dev
     a = np.ascontiguousarray(x, dtype=dtype)
     return a.ctypes.data, MEM_HOST, a, False

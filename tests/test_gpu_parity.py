@@ -545,3 +545,23 @@ def test_kernel_invalid(rs):
         rs.rs_create_kernel(X, np.zeros(4), 1.0, 0.0)
     with pytest.raises(rs.RSError):
         rs.rs_create_kernel(X, np.zeros(4), -1.0, 1.0)
+
+
+@pytest.mark.parametrize("mode,kind,tau", [("explicit", "subsample", 300), ("explicit", "subsample", 120),
+                                           ("explicit", "count", 260), ("gram", "subsample", 300),
+                                           ("implicit", "subsample", 300)])
+def test_dirty_device_memory(rs, mode, kind, tau):
+    """Every device buffer is written before it is read: the same solve after the allocator's pages
+    were filled with NaN (freed by torch and handed back to the driver) equals the oracle."""
+    free, _ = torch.cuda.mem_get_info()
+    junk = torch.full((int(min(free * 0.8, 60e9)) // 8,), float("nan"), dtype=torch.float64,
+                      device="cuda")
+    del junk
+    torch.cuda.empty_cache()
+    n, d = 2500, 900
+    X, y = rsinputs.dense_problem(n, d, seed=21)
+    X, y = X.numpy(), y.numpy()
+    w, r, rep = _run_gpu_dense(rs, X, y, 0.7, mode, kind, tau, 0.5, 9, seed=2)
+    ref = OV.solve(X, y, 0.7, kind, tau, 1.0, 0.5, 0.0, 9, seed=2)
+    assert rel(w, ref["w"]) <= 1e-10
+    assert rel(r, ref["r"]) <= 1e-10
