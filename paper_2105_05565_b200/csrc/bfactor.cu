@@ -60,7 +60,7 @@ size_t bf_smem(int tau) {
 __global__ void __launch_bounds__(BF_THREADS, 1)
 k_bfactor_small(FactorSrc src, DevSketch skb, double* __restrict__ Ginv, long long ldgi,
                 long long gi_stride, int* __restrict__ flags, const Ctrl* ctrl) {
-  if (ctrl && ctrl->done) return;
+  if (slot_unused(ctrl, blockIdx.x)) return;
   extern __shared__ double sL[];
   __shared__ double s_inv[BF_MAXTAU];
   __shared__ int s_bad;
@@ -426,7 +426,7 @@ __global__ void __launch_bounds__(BB_THREADS, 1)
 k_bfactor_big(FactorSrc src, DevSketch skb, double* __restrict__ Ginv, long long ldgi,
               long long gi_stride, double* work, long long work_stride, int* __restrict__ flags,
               const Ctrl* ctrl) {
-  if (ctrl && ctrl->done) return;
+  if (slot_unused(ctrl, blockIdx.x)) return;
   __shared__ double sL[32][33];
   __shared__ int s_bad;
   const int slot = blockIdx.x;

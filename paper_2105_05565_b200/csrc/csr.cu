@@ -107,14 +107,14 @@ __global__ void k_csc_spmv_t(const long long* colptr, const int* rowidx, const d
 
 // ------------------------------------------------------------------------------ per-iteration
 // primal: per-coordinate sketch map for subsample / SubCount (count uses its own cmap)
-__global__ void k_cmap_clear(int* cmap, long long m, const Ctrl* ctrl) {
-  if (ctrl->done) return;
+__global__ void k_cmap_clear(int* cmap, long long m, const Ctrl* ctrl, int slot = 0) {
+  if (slot_unused(ctrl, slot)) return;
   for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < m;
        i += (long long)gridDim.x * blockDim.x)
     cmap[i] = -1;
 }
-__global__ void k_cmap_scatter(DevSketch sk, int* cmap, const Ctrl* ctrl) {
-  if (ctrl->done) return;
+__global__ void k_cmap_scatter(DevSketch sk, int* cmap, const Ctrl* ctrl, int slot = 0) {
+  if (slot_unused(ctrl, slot)) return;
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
   if (e < sk.len) cmap[sk.coord[e]] = (sk.bucket[e] << 1) | (sk.sign[e] < 0 ? 1 : 0);
 }
@@ -253,9 +253,10 @@ k_csr_dual_as(const long long* __restrict__ rowptr, const int* __restrict__ coli
 }  // namespace
 
 cudaError_t launch_cmap_build(const DevSketch& sk, int* cmap_all, long long m, const Ctrl* ctrl,
-                              cudaStream_t st) {
-  k_cmap_clear<<<(unsigned)std::min<long long>((m + 255) / 256, 1024), 256, 0, st>>>(cmap_all, m, ctrl);
-  k_cmap_scatter<<<(sk.len + 255) / 256, 256, 0, st>>>(sk, cmap_all, ctrl);
+                              cudaStream_t st, int slot) {
+  k_cmap_clear<<<(unsigned)std::min<long long>((m + 255) / 256, 1024), 256, 0, st>>>(cmap_all, m, ctrl,
+                                                                                     slot);
+  k_cmap_scatter<<<(sk.len + 255) / 256, 256, 0, st>>>(sk, cmap_all, ctrl, slot);
   return cudaGetLastError();
 }
 

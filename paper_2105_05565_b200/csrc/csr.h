@@ -42,6 +42,6 @@ struct CsrData {
 
 // per-iteration map coordinate -> (bucket << 1 | neg), -1 outside the sketch (subsample / SubCount)
 cudaError_t launch_cmap_build(const DevSketch& sk, int* cmap_all, long long m, const Ctrl* ctrl,
-                              cudaStream_t st);
+                              cudaStream_t st, int slot = 0);
 
 }  // namespace rs

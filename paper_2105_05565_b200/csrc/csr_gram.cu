@@ -112,8 +112,8 @@ __global__ void __launch_bounds__(HR_WARPS * 32)
 k_hash_rows(const long long* __restrict__ ptr, const int* __restrict__ idx,
             const double* __restrict__ val, long long rows, long long heavy, const int* __restrict__ cmap,
             int tau, int* __restrict__ hb, double* __restrict__ hv, int* __restrict__ hcnt,
-            const Ctrl* ctrl) {
-  if (ctrl->done) return;
+            int slot, const Ctrl* ctrl) {
+  if (slot_unused(ctrl, slot)) return;
   extern __shared__ double hsm[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   WarpMerge M(hsm, tau, warp);
@@ -146,8 +146,8 @@ __global__ void __launch_bounds__(HR_WARPS * 32)
 k_hash_rows_heavy(const long long* __restrict__ ptr, const int* __restrict__ idx,
                   const double* __restrict__ val, const int* __restrict__ heavy_rows,
                   const int* __restrict__ cmap, int tau, int* __restrict__ hb,
-                  double* __restrict__ hv, int* __restrict__ hcnt, const Ctrl* ctrl) {
-  if (ctrl->done) return;
+                  double* __restrict__ hv, int* __restrict__ hcnt, int slot, const Ctrl* ctrl) {
+  if (slot_unused(ctrl, slot)) return;
   extern __shared__ double hsm[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   WarpMerge M(hsm, tau, warp);
@@ -191,8 +191,8 @@ k_gram_bands(const long long* __restrict__ ptr, const int* __restrict__ hcnt,
              const int* __restrict__ hb, const double* __restrict__ hv,
              const int* __restrict__ band_a0, const long long* __restrict__ chunk_r0,
              long long heavy, const int* __restrict__ heavy_rows, const int* __restrict__ chunk_h0,
-             double* __restrict__ part, long long part_stride, const Ctrl* ctrl) {
-  if (ctrl->done) return;
+             double* __restrict__ part, long long part_stride, int slot, const Ctrl* ctrl) {
+  if (slot_unused(ctrl, slot)) return;
   extern __shared__ double band[];
   const int a0 = band_a0[blockIdx.x], a1 = band_a0[blockIdx.x + 1];
   const long long base = tri(a0);
@@ -261,8 +261,8 @@ k_gram_bands(const long long* __restrict__ ptr, const int* __restrict__ hcnt,
 
 __global__ void k_gram_band_reduce(const double* __restrict__ part, int nchunks,
                                    long long part_stride, double* __restrict__ G, long long ldg,
-                                   const Ctrl* ctrl) {
-  if (ctrl->done) return;
+                                   int slot, const Ctrl* ctrl) {
+  if (slot_unused(ctrl, slot)) return;
   const int a = blockIdx.x;
   const long long base = tri(a);
   for (int c = threadIdx.x; c <= a; c += blockDim.x) {
@@ -498,7 +498,7 @@ rs_status Problem::csr_gram_workspace(int kind, int tau) {
   return RS_OK;
 }
 
-rs_status Problem::csr_gram_into(const DevSketch& s, double* G, cudaEvent_t* ev) {
+rs_status Problem::csr_gram_into(const DevSketch& s, double* G, cudaEvent_t* ev, int slot) {
   auto mark = [&](int cls, int edge) {
     if (ev) cudaEventRecordWithFlags(ev[2 * cls + edge], st, cudaEventRecordExternal);
   };
@@ -509,26 +509,27 @@ rs_status Problem::csr_gram_into(const DevSketch& s, double* G, cudaEvent_t* ev)
   const int* cmap = s.cmap;
   mark(RS_K_XS, 0);
   if (s.kind != SK_COUNT) {
-    RS_CUDA(launch_cmap_build(s, c->cmap_all, m, ctrl, st));
+    RS_CUDA(launch_cmap_build(s, c->cmap_all, m, ctrl, st, slot));
     cmap = c->cmap_all;
   }
   if (R.rows > 0) {   // a2: rows of R S, merged and bucket-sorted
     const unsigned grid = (unsigned)std::max<long long>(
         1, std::min<long long>((R.rows + HR_WARPS - 1) / HR_WARPS, (long long)num_sms * 8));
     k_hash_rows<<<grid, HR_WARPS * 32, c->hr_smem, st>>>(R.ptr, R.idx, R.val, R.rows, c->heavyR,
-                                                          cmap, tau, c->hb, c->hv, c->hcnt, ctrl);
+                                                          cmap, tau, c->hb, c->hv, c->hcnt, slot, ctrl);
     if (c->nheavyR > 0)
       k_hash_rows_heavy<<<c->nheavyR, HR_WARPS * 32, c->hr_smem, st>>>(
-          R.ptr, R.idx, R.val, c->heavy_rowsR, cmap, tau, c->hb, c->hv, c->hcnt, ctrl);
+          R.ptr, R.idx, R.val, c->heavy_rowsR, cmap, tau, c->hb, c->hv, c->hcnt, slot, ctrl);
     RS_CUDA(cudaGetLastError());
     mark(RS_K_XS, 1);
     mark(RS_K_GRAM, 0);
     // a3/a4: (R S)^T (R S), lower triangle
     k_gram_bands<<<dim3((unsigned)c->nbands, (unsigned)c->nchunks), GB_THREADS, c->gb_smem, st>>>(
         R.ptr, c->hcnt, c->hb, c->hv, c->band_a0, c->chunk_r0, c->heavyR, c->heavy_rowsR,
-        c->chunk_h0, c->gpart, c->gpart_stride, ctrl);
+        c->chunk_h0, c->gpart, c->gpart_stride, slot, ctrl);
     RS_CUDA(cudaGetLastError());
-    k_gram_band_reduce<<<tau, 256, 0, st>>>(c->gpart, c->nchunks, c->gpart_stride, G, ld_gram, ctrl);
+    k_gram_band_reduce<<<tau, 256, 0, st>>>(c->gpart, c->nchunks, c->gpart_stride, G, ld_gram, slot,
+                                            ctrl);
     RS_CUDA(cudaGetLastError());
   } else {
     mark(RS_K_XS, 1);

@@ -18,8 +18,8 @@ namespace {
 // ------------------------------------------------------------------------------ a2 gathers
 __global__ void k_dense_xs(const double* __restrict__ X, long long ldx, long long rows,
                            DevSketch sk, double* __restrict__ XS, long long ld_xs, int rows_per_blk,
-                           const Ctrl* ctrl) {
-  if (ctrl && ctrl->done) return;
+                           const Ctrl* ctrl, int slot) {
+  if (slot_unused(ctrl, slot)) return;
   const long long r0 = (long long)blockIdx.x * rows_per_blk;
   const int per_blk = rows_per_blk * (int)ld_xs;
   for (int q = threadIdx.x; q < per_blk; q += blockDim.x) {
@@ -42,7 +42,7 @@ __global__ void k_dense_xs(const double* __restrict__ X, long long ldx, long lon
 __global__ void k_explicit_rows(const double* __restrict__ A, long long lda, long long m,
                                 DevSketch sk, double* __restrict__ ASt, long long ld_as,
                                 long long as_stride, const Ctrl* ctrl) {
-  if (ctrl && ctrl->done) return;
+  if (slot_unused(ctrl, blockIdx.z)) return;
   const int b = blockIdx.y;
   sk = sk.at(blockIdx.z);          // batched: slot blockIdx.z
   ASt += blockIdx.z * as_stride;
@@ -299,11 +299,12 @@ cudaError_t launch_count_nonfinite(const double* X, long long ldx, long long row
 }
 
 cudaError_t launch_dense_xs(const double* X, long long ldx, long long rows, const DevSketch& sk,
-                            double* XS, long long ld_xs, const Ctrl* ctrl, cudaStream_t st) {
+                            double* XS, long long ld_xs, const Ctrl* ctrl, cudaStream_t st,
+                            int slot) {
   if (rows <= 0) return cudaSuccess;
   const int rpb = (int)std::max<long long>(1, 2048 / ld_xs);
   const long long grid = (rows + rpb - 1) / rpb;
-  k_dense_xs<<<(unsigned)grid, 256, 0, st>>>(X, ldx, rows, sk, XS, ld_xs, rpb, ctrl);
+  k_dense_xs<<<(unsigned)grid, 256, 0, st>>>(X, ldx, rows, sk, XS, ld_xs, rpb, ctrl, slot);
   return cudaGetLastError();
 }
 

@@ -589,14 +589,14 @@ rs_status Problem::enqueue_precompute(const rs_solve_opts* o, int ns, cudaEvent_
       const DevSketch sq = skb.at(q);
       double* Gq = Gram_slots + (long long)q * gram_stride;
       if (fmt == 1) {
-        RS_TRY(csr_gram_into(sq, Gq, ev ? ev + (size_t)q * 2 * RS_K_NCLASSES : nullptr));
+        RS_TRY(csr_gram_into(sq, Gq, ev ? ev + (size_t)q * 2 * RS_K_NCLASSES : nullptr, q));
         continue;
       }
       mark(q, RS_K_GRAM, 0);
       if (rows_loc > 0 && gram_fused) {
-        RS_CUDA(launch_gram_fused(X, ldx, rows_loc, sq, xp_part, Gq, ld_gram, num_sms, ctrl, st));
+        RS_CUDA(launch_gram_fused(X, ldx, rows_loc, sq, xp_part, Gq, ld_gram, num_sms, ctrl, st, q));
       } else if (rows_loc > 0) {
-        RS_CUDA(launch_dense_xs(X, ldx, rows_loc, sq, XS, ld_xs, ctrl, st));
+        RS_CUDA(launch_dense_xs(X, ldx, rows_loc, sq, XS, ld_xs, ctrl, st, q));
         RS_CUDA(tma_gemm_launch(tg_gram, Gq, ld_gram, gemm_work, ctrl, st));
       } else {
         RS_CUDA(launch_fill(Gq, gram_stride, 0.0, st));
@@ -675,7 +675,7 @@ rs_status Problem::enqueue_group_xg(const rs_solve_opts* o, int g, cudaEvent_t* 
     mark(q, RS_K_AS, 0);
     double* Gq = Gram_slots + ns * gram_stride;
     RS_CUDA(launch_xpass_gram(X, ldx, rows_loc, m, sdelta, xp_part, uvec, sn.at(q), gf_part, Gq,
-                              ld_gram, num_sms, ctrl, st));       // X^T X S delta + Gram ahead
+                              ld_gram, num_sms, ctrl, st, P));    // X^T X S delta + Gram ahead
     RS_TRY(allreduce(uvec, (size_t)m));
     RS_TRY(allreduce(Gq, (size_t)gram_stride));
     mark(q, RS_K_AS, 1);

@@ -234,8 +234,8 @@ __device__ __forceinline__ void dmma_g(double (&c)[2], double a, double b) {
 
 __global__ void __launch_bounds__(GF_THREADS, 1)
 k_gram_fused(const double* __restrict__ X, long long ldx, long long rows, DevSketch sk,
-             long long rows_per_cta, double* __restrict__ partials, const Ctrl* ctrl) {
-  if (ctrl->done) return;
+             long long rows_per_cta, double* __restrict__ partials, int slot, const Ctrl* ctrl) {
+  if (slot_unused(ctrl, slot)) return;
   extern __shared__ __align__(16) double gsm[];   // [GF_STAGES][GF_BK][GF_LD]
   __shared__ int s_col[GF_MAXTAU];
   const int tau = sk.tau, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -318,8 +318,8 @@ k_gram_fused(const double* __restrict__ X, long long ldx, long long rows, DevSke
 
 // G[a][b] = sum_c partials[c][a][b] for b <= a (fixed order: c ascending)
 __global__ void k_gram_reduce(const double* __restrict__ partials, int nparts, int tau,
-                              double* __restrict__ G, long long ldg, const Ctrl* ctrl) {
-  if (ctrl->done) return;
+                              double* __restrict__ G, long long ldg, const Ctrl* ctrl, int slot = 0) {
+  if (slot_unused(ctrl, slot)) return;
   const int a = blockIdx.x;
   for (int b = threadIdx.x; b <= a; b += blockDim.x) {
     const double* p = partials + a * GF_MAXTAU + b;
@@ -357,7 +357,7 @@ template <int Q>
 __global__ void __launch_bounds__(XG_THREADS, 1)
 k_xpass_gram1(const double* __restrict__ X, long long ldx, long long rows, long long d,
               const double* __restrict__ v, double* __restrict__ upart, long long rows_per_cta,
-              int stages, DevSketch skg, double* __restrict__ gpart, const Ctrl* ctrl) {
+              int stages, DevSketch skg, double* __restrict__ gpart, int gofs, const Ctrl* ctrl) {
   if (ctrl->done) return;
   constexpr int NC = XG_CONS * 32;                      // consumer threads
   extern __shared__ __align__(128) double xs_ring[];   // [stages][XG_R * ldx] + pad, v[NC * Q]
@@ -366,7 +366,7 @@ k_xpass_gram1(const double* __restrict__ X, long long ldx, long long rows, long 
   __shared__ __align__(16) double slab[2][XG_R][GF_LD];
   __shared__ short2 s_tile[XG_CONS][XG1_TPW];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int tau = skg.tau;
+  const int tau = slot_unused(ctrl, gofs) ? 0 : skg.tau;   // future slot needed?
   const int ldxi = (int)ldx;
   const int stage_elems = XG_R * ldxi;
   double* sv = xs_ring + (size_t)stages * stage_elems + NC * Q;   // after the ring + a pad
@@ -524,7 +524,7 @@ template <int Q>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(XG_THREADS, 1)
 k_xpass_gram2(const double* __restrict__ X, long long ldx, long long rows, long long d,
               const double* __restrict__ v, double* __restrict__ upart, long long rows_per_pair,
-              int stages, DevSketch skg, double* __restrict__ gpart, const Ctrl* ctrl) {
+              int stages, DevSketch skg, double* __restrict__ gpart, int gofs, const Ctrl* ctrl) {
   if (ctrl->done) return;   // uniform over the grid (ctrl is not written during this kernel)
   extern __shared__ __align__(128) double xs_ring[];   // [stages][XG_R * ldx]
   __shared__ __align__(8) uint64_t full[8], empty[8];
@@ -532,7 +532,7 @@ k_xpass_gram2(const double* __restrict__ X, long long ldx, long long rows, long 
   __shared__ int s_col[GF_MAXTAU + 8];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const unsigned rank = cluster_rank(), peer = rank ^ 1u;
-  const int tau = skg.tau;
+  const int tau = slot_unused(ctrl, gofs) ? 0 : skg.tau;   // future slot needed?
   for (int b = tid; b < GF_MAXTAU + 8; b += XG_THREADS)
     s_col[b] = b < tau ? skg.coord[skg.bptr[b]] : -1;
   const long long pair = blockIdx.x >> 1;
@@ -697,14 +697,14 @@ cudaError_t gram_init() {
 
 cudaError_t launch_gram_fused(const double* X, long long ldx, long long rows, const DevSketch& sk,
                               double* partials, double* G, long long ldg, int num_sms,
-                              const Ctrl* ctrl, cudaStream_t st) {
+                              const Ctrl* ctrl, cudaStream_t st, int slot) {
   const int nc = num_sms;
   const long long rpc = std::max<long long>(GF_BK, ((rows + nc - 1) / nc + GF_BK - 1) / GF_BK * GF_BK);
   const size_t smem = (size_t)GF_STAGES * GF_BK * GF_LD * sizeof(double);
-  k_gram_fused<<<nc, GF_THREADS, smem, st>>>(X, ldx, rows, sk, rpc, partials, ctrl);
+  k_gram_fused<<<nc, GF_THREADS, smem, st>>>(X, ldx, rows, sk, rpc, partials, slot, ctrl);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
-  k_gram_reduce<<<sk.tau, 256, 0, st>>>(partials, nc, sk.tau, G, ldg, ctrl);
+  k_gram_reduce<<<sk.tau, 256, 0, st>>>(partials, nc, sk.tau, G, ldg, ctrl, slot);
   return cudaGetLastError();
 }
 
@@ -746,7 +746,7 @@ bool xpass_gram_ok(int kind, int tau, long long d, long long ldx) {
 cudaError_t launch_xpass_gram(const double* X, long long ldx, long long rows, long long d,
                               const double* v, double* upart, double* u, const DevSketch& skg,
                               double* gpart, double* G, long long ldg, int num_sms,
-                              const Ctrl* ctrl, cudaStream_t st) {
+                              const Ctrl* ctrl, cudaStream_t st, int gofs) {
   const int nc = xpass_ctas(num_sms) & ~1;   // cluster pairs
   const int npairs = nc / 2;
   const long long rpp = std::max<long long>(1, (rows + npairs - 1) / npairs);
@@ -765,9 +765,9 @@ cudaError_t launch_xpass_gram(const double* X, long long ldx, long long rows, lo
   static const bool pair = std::getenv("RS_XG_PAIR") != nullptr;
   if (pair) {
     if (d <= 5 * XG_CONS * 32)
-      k_xpass_gram2<5><<<nc, XG_THREADS, smem, st>>>(X, ldx, rows, d, v, upart, rpp, stages, skg, gpart, ctrl);
+      k_xpass_gram2<5><<<nc, XG_THREADS, smem, st>>>(X, ldx, rows, d, v, upart, rpp, stages, skg, gpart, gofs, ctrl);
     else
-      k_xpass_gram2<7><<<nc, XG_THREADS, smem, st>>>(X, ldx, rows, d, v, upart, rpp, stages, skg, gpart, ctrl);
+      k_xpass_gram2<7><<<nc, XG_THREADS, smem, st>>>(X, ldx, rows, d, v, upart, rpp, stages, skg, gpart, gofs, ctrl);
   } else {   // single CTA per SM: stages from 200 KB minus v
     const int Q = d <= 5 * XG_CONS * 32 ? 5 : 7;
     const long long extra = 2LL * Q * XG_CONS * 32 * 8;   // read pad after the ring + v
@@ -776,15 +776,15 @@ cudaError_t launch_xpass_gram(const double* X, long long ldx, long long rows, lo
     const size_t smem1 = (size_t)st1 * stage_bytes + (size_t)extra;
     const long long rpc = std::max<long long>(1, (rows + nc - 1) / nc);
     if (d <= 5 * XG_CONS * 32)
-      k_xpass_gram1<5><<<nc, XG_THREADS, smem1, st>>>(X, ldx, rows, d, v, upart, rpc, st1, skg, gpart, ctrl);
+      k_xpass_gram1<5><<<nc, XG_THREADS, smem1, st>>>(X, ldx, rows, d, v, upart, rpc, st1, skg, gpart, gofs, ctrl);
     else
-      k_xpass_gram1<7><<<nc, XG_THREADS, smem1, st>>>(X, ldx, rows, d, v, upart, rpc, st1, skg, gpart, ctrl);
+      k_xpass_gram1<7><<<nc, XG_THREADS, smem1, st>>>(X, ldx, rows, d, v, upart, rpc, st1, skg, gpart, gofs, ctrl);
   }
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   k_xpass_reduce<<<(unsigned)((d + 31) / 32), dim3(32, XR_Y), 0, st>>>(upart, nc, d, u, ctrl);
   if (skg.tau > 0)
-    k_gram_reduce<<<skg.tau, 256, 0, st>>>(gpart, pair ? npairs : nc, skg.tau, G, ldg, ctrl);
+    k_gram_reduce<<<skg.tau, 256, 0, st>>>(gpart, pair ? npairs : nc, skg.tau, G, ldg, ctrl, gofs);
   return cudaGetLastError();
 }
 }  // namespace rs

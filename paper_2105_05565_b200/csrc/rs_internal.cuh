@@ -53,6 +53,12 @@ __device__ __forceinline__ void mom_at(const Ctrl* c, double& gamma, double& bet
   gamma = kind == 3 ? eta / den : 1.0;
 }
 
+// Sketch-ahead slot q of the group that starts at iteration ctrl->k is needed only if
+// k + q < max_iter (and the solve is still running).
+__device__ __forceinline__ bool slot_unused(const Ctrl* c, long long q) {
+  return c && (c->done || c->k + q >= c->max_iter);
+}
+
 // ---------------------------------------------------------------------------------------------
 // Philox4x32-10 (Salmon et al., SC'11) -- the sketch-stream generator, DESIGN.md Section 3.
 __device__ __forceinline__ uint4 philox4x32_10(uint4 c, uint2 k) {
@@ -117,7 +123,8 @@ size_t sketch_max_len(int kind, int m, int tau, int ksum);
 // a2 dense: XS[i, b] = sum_{e in b} sign_e X[i, coord_e],  i < rows, row-major ld_xs (>= tau, pad
 // columns zeroed).
 cudaError_t launch_dense_xs(const double* X, long long ldx, long long rows, const DevSketch& sk,
-                            double* XS, long long ld_xs, const Ctrl* ctrl, cudaStream_t st);
+                            double* XS, long long ld_xs, const Ctrl* ctrl, cudaStream_t st,
+                            int slot = 0);
 // a2 explicit: AS^T[b, :] = sum_{e in b} sign_e A[coord_e, :]  (A symmetric, m x m, ld lda).
 cudaError_t launch_explicit_rows(const double* A, long long lda, long long m, const DevSketch& sk,
                                  double* ASt, long long ld_as, const Ctrl* ctrl, cudaStream_t st);
@@ -203,12 +210,13 @@ bool xpass_gram_ok(int kind, int tau, long long d, long long ldx);
 cudaError_t launch_xpass_gram(const double* X, long long ldx, long long rows, long long d,
                               const double* v, double* upart, double* u, const DevSketch& skg,
                               double* gpart, double* G, long long ldg, int num_sms,
-                              const Ctrl* ctrl, cudaStream_t st);
+                              const Ctrl* ctrl, cudaStream_t st, int gofs);
 size_t gram_fused_partials(int num_sms);
 cudaError_t gram_init();
 cudaError_t launch_gram_fused(const double* X, long long ldx, long long rows, const DevSketch& sk,
                               double* partials, double* G, long long ldg, int num_sms,
-                              const Ctrl* ctrl, cudaStream_t st);
+                              const Ctrl* ctrl, cudaStream_t st,
+                              int slot = 0);
 // explicit A, sketch with few entries (subsample / SubCount):
 //   u_j = sum_e sign_e delta[bucket_e] A[coord_e][j]  (= (A S delta)_j, A symmetric), then the update
 size_t update_rows_scratch(long long m);    // doubles of `upart`

@@ -33,7 +33,7 @@ __device__ __forceinline__ bool lt_pair(unsigned long long ka, unsigned ia, unsi
 __global__ void __launch_bounds__(kThreads, 1)
 k_sketch_select(DevSketch skb, uint2 key, const Ctrl* ctrl, long long fixed_k, long long kofs,
                 int* err) {
-  if (fixed_k < 0 && ctrl->done) return;
+  if (fixed_k < 0 && slot_unused(ctrl, kofs + blockIdx.x)) return;
   // slot blockIdx.x of a batch receives the sketch of iteration k0 + blockIdx.x
   const DevSketch sk = skb.at(blockIdx.x);
   const unsigned it = (unsigned)((fixed_k >= 0 ? fixed_k : ctrl->k + kofs) + blockIdx.x);
@@ -157,7 +157,7 @@ k_sketch_select(DevSketch skb, uint2 key, const Ctrl* ctrl, long long fixed_k, l
 
 __global__ void __launch_bounds__(kThreads, 1)
 k_sketch_count(DevSketch skb, uint2 key, const Ctrl* ctrl, long long fixed_k, long long kofs) {
-  if (fixed_k < 0 && ctrl->done) return;
+  if (fixed_k < 0 && slot_unused(ctrl, kofs + blockIdx.x)) return;
   const DevSketch sk = skb.at(blockIdx.x);
   const unsigned it = (unsigned)((fixed_k >= 0 ? fixed_k : ctrl->k + kofs) + blockIdx.x);
   const int m = sk.m, tau = sk.tau, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
