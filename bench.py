@@ -229,9 +229,13 @@ def _roofline(args, cfg, world, kms, kl, dom, prof_ms, host, rs):
     n_loc = cfg.n / world
     ms = per(dom)
     roof = None
-    if cfg.kind == "kernel":   # EXPLICIT path on the n x n system
+    if cfg.kind == "kernel" or (cfg.kind == "csr" and args.mode == "explicit"):
+        # EXPLICIT path on the m x m system (kernel ridge: m = n; CSR: m = d primal, n dual)
         import rsinputs
-        cfg = rsinputs.Config(cfg.name, "dense", cfg.n, cfg.n, cfg.lam, cfg.sketch, cfg.tau)
+        m_sys = cfg.n if (cfg.kind == "kernel" or cfg.d > cfg.n) else cfg.d
+        rows_s = cfg.tau * (max(cfg.subcount_k, 1) if cfg.sketch == "subcount" else 1)
+        cfg = rsinputs.Config(cfg.name, "dense", m_sys, m_sys, cfg.lam, cfg.sketch, cfg.tau,
+                              extra={"rows": rows_s})
     if cfg.kind == "dense":
         if dom == "as" and args.mode == "implicit":
             w = 2.0 * n_loc * cfg.d * cfg.tau
@@ -261,12 +265,13 @@ def _roofline(args, cfg, world, kms, kl, dom, prof_ms, host, rs):
                         algorithmic_per_launch=f"{w:.3e} flop (tau^3 per G_k: tau^3/3 Cholesky + "
                                                f"tau^3/3 inverse + tau^3/3 W^T W, x {slots:.0f} slots)")
         else:   # explicit: rows of A + GEMV + update
-            w = (cfg.tau * cfg.d + 10 * cfg.d) * 8.0
+            rows_s = cfg.extra.get("rows", cfg.tau)
+            w = (rows_s * cfg.d + 10 * cfg.d) * 8.0
             a_mb = cfg.d * cfg.d * 8 / 1e6
             roof = dict(kernel=f"class {dom}: u = A S delta from the tau sketched rows of A, fused "
                                "momentum update (k_update_rows)", bound="hbm",
                         achieved=w / (ms * 1e-3) / 1e9, peak=hbm, unit="GB/s", peak_source=hbm_src,
-                        algorithmic_per_launch=f"{w:.3e} bytes (tau m 8 rows of A + 10 m-vectors)",
+                        algorithmic_per_launch=f"{w:.3e} bytes ({rows_s} sketched rows of A x m x 8 + 10 m-vectors)",
                         note=f"A = {a_mb:.0f} MB ({'fits' if a_mb < 126 else 'exceeds'} the 126 MB L2)")
     else:
         nnz = int(host[0][-1])

@@ -390,8 +390,8 @@ rs_status create_csr(rs_problem* out, int64_t n, int64_t d, int64_t nnz_local, c
     return fail(RS_EINVAL, "bad rs_mem");
   if (route != RS_ROUTE_AUTO && route != RS_ROUTE_PRIMAL && route != RS_ROUTE_DUAL)
     return fail(RS_EINVAL, "bad route");
-  if (mode == RS_AS_EXPLICIT) return fail(RS_EUNSUPPORTED, "explicit A with CSR X (SURVEY NEXT-3)");
-  if (mode != RS_AS_IMPLICIT && mode != RS_AS_GRAM) return fail(RS_EINVAL, "bad as_mode");
+  if (mode != RS_AS_IMPLICIT && mode != RS_AS_GRAM && mode != RS_AS_EXPLICIT)
+    return fail(RS_EINVAL, "bad as_mode");
   const int rt = route == RS_ROUTE_AUTO ? (d <= n ? 1 : 2) : (route == RS_ROUTE_PRIMAL ? 1 : 2);
   RS_TRY(validate_dist(dist, rt == 1 ? n : d));
   const long long rows = rt == 1 ? (dist ? dist->shard_len : n) : n;
@@ -502,6 +502,10 @@ rs_status create_csr(rs_problem* out, int64_t n, int64_t d, int64_t nnz_local, c
     if (s != RS_OK) return guard(s);
   } else {
     cudaMemcpyAsync(p->b, p->y, n * 8, cudaMemcpyDeviceToDevice, st);
+  }
+  if (mode == RS_AS_EXPLICIT) {   // dense A = R^T R + lambda I from the sparse X
+    s = p->csr_build_explicit();
+    if (s != RS_OK) return guard(s);
   }
   cudaEventRecord(e1, st);
   s = finish_setup(p);

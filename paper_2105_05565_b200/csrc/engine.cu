@@ -380,8 +380,9 @@ static rs_status validate_opts(const Problem* p, const rs_solve_opts* o, int* ks
 // Sketch-ahead pipeline (bfactor.cu) applies to dense primal EXPLICIT and GRAM modes with
 // tau <= bfactor_max_tau(): there G_k needs no per-iteration contraction of the iterate's data.
 static bool pipeline_applies(const Problem* p, int tau) {
-  const bool dense = p->fmt == 0 && p->route == 1 &&
-                     (p->mode == RS_AS_EXPLICIT || p->mode == RS_AS_GRAM);
+  const bool dense = (p->fmt == 0 && p->route == 1 &&
+                      (p->mode == RS_AS_EXPLICIT || p->mode == RS_AS_GRAM)) ||
+                     p->mode == RS_AS_EXPLICIT;   // CSR explicit: dense A built in rs_create_csr
   const bool csr = p->fmt == 1 && p->mode == RS_AS_GRAM;
   return (dense || csr) && tau <= bfactor_max_tau() && !std::getenv("RS_NO_PIPE");
 }
@@ -403,7 +404,7 @@ rs_status Problem::ensure_workspace(int kind, int tau, int ksum, int depth, bool
   RS_TRY(dalloc(&sk.bptr, tau + 1));
   if (kind == SK_COUNT) RS_TRY(dalloc(&sk.cmap, m));
   if (fmt == 1 && mode == RS_AS_GRAM) {   // CSR GRAM: buffers in csr_gram_workspace
-  } else if (fmt == 1) {   // CSR: AS row-major m x tau
+  } else if (fmt == 1 && mode != RS_AS_EXPLICIT) {   // CSR IMPLICIT: AS row-major m x tau
     ld_as = round_up(tau, 4);
     RS_TRY(dalloc(&ASt, (size_t)m * ld_as));
   } else if (depth > 0 && mode == RS_AS_EXPLICIT) {   // pipelined explicit: A S^T per slot
@@ -445,7 +446,7 @@ rs_status Problem::ensure_workspace(int kind, int tau, int ksum, int depth, bool
               rows_loc, use_tma ? "TMA" : "cp.async", use_tma ? tg.variant : gp.variant,
               use_tma ? tg.bm : gp.bm, use_tma ? tg.bn : gp.bn, use_tma ? tg.splits : gp.splits);
   }
-  if (fmt == 1) RS_TRY(csr_ensure_workspace(kind, tau, ksum));
+  if (fmt == 1 && mode != RS_AS_EXPLICIT) RS_TRY(csr_ensure_workspace(kind, tau, ksum));
   if (depth > 0) {   // sketch-ahead slots (two sets of `depth` for the fused pipeline)
     pipe = true;
     pipe_xg = xg;
@@ -477,7 +478,7 @@ rs_status Problem::ensure_workspace(int kind, int tau, int ksum, int depth, bool
   RS_TRY(dalloc(&sw.Gx, solve_gx_elems(tau)));
   RS_TRY(dalloc(&sw.delta, tau));
   RS_TRY(dalloc(&partials, update_partials(m)));
-  if (mode == RS_AS_EXPLICIT && fmt == 0) {   // split-row update scratch (k_update_rows)
+  if (mode == RS_AS_EXPLICIT) {   // split-row update scratch (k_update_rows)
     RS_TRY(dalloc(&rows_part, update_rows_scratch(m)));
     RS_TRY(dalloc(&rows_cnt, update_rows_counters(m)));
     RS_CUDA(cudaMemsetAsync(rows_cnt, 0, update_rows_counters(m) * sizeof(int), st));
@@ -545,7 +546,7 @@ rs_status Problem::enqueue_iteration(const rs_solve_opts* o, cudaEvent_t* ev) {
     RS_TRY(allreduce(ASt, (size_t)sk.tau * ld_as));                         // sum over row shards
     RS_CUDA(launch_add_lambda_s(lambda, sk, ASt, ld_as, false, ctrl, st));         // + lambda S
     mark(RS_K_AS, 1);
-  } else if (fmt == 0) {
+  } else if (mode == RS_AS_EXPLICIT) {
     mark(RS_K_XS, 0);
     RS_CUDA(launch_explicit_rows(A, lda, m, sk, ASt, ld_as, ctrl, st));      // a2  rows of A
     mark(RS_K_XS, 1);
@@ -553,10 +554,11 @@ rs_status Problem::enqueue_iteration(const rs_solve_opts* o, cudaEvent_t* ev) {
     RS_TRY(csr_enqueue_as(o, ev));
   }
   mark(RS_K_SOLVE, 0);
-  RS_CUDA(launch_sketched_solve(ASt, ld_as, fmt == 1, nullptr, 0, 0.0, r, sk, sw, sdelta, ctrl, st));
+  const bool as_rm = fmt == 1 && mode != RS_AS_EXPLICIT;   // CSR IMPLICIT stores AS row-major
+  RS_CUDA(launch_sketched_solve(ASt, ld_as, as_rm, nullptr, 0, 0.0, r, sk, sw, sdelta, ctrl, st));
   mark(RS_K_SOLVE, 1);
   mark(RS_K_UPDATE, 0);
-  RS_CUDA(launch_update(ASt, ld_as, fmt == 1, sk.tau, sw.delta, sdelta, w, dw, r, dr, m, o->gamma, o->beta,
+  RS_CUDA(launch_update(ASt, ld_as, as_rm, sk.tau, sw.delta, sdelta, w, dw, r, dr, m, o->gamma, o->beta,
                         partials, ctrl, st));                                // a6 + a7
   mark(RS_K_UPDATE, 1);
   return RS_OK;

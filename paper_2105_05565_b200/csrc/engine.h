@@ -125,6 +125,7 @@ struct Problem {
   rs_status csr_dual_weights(double* w_out, cudaMemcpyKind kd);
   // CSR GRAM mode (csr_gram.cu)
   void csr_gram_free();
+  rs_status csr_build_explicit();                              // csr_explicit.cu
   rs_status csr_gram_workspace(int kind, int tau);
   rs_status csr_enqueue_gram(const rs_solve_opts* o, cudaEvent_t* ev);
   rs_status csr_gram_into(const DevSketch& s, double* G, cudaEvent_t* ev, int slot = 0);   // (R S)^T (R S)

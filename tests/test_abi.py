@@ -82,8 +82,11 @@ def test_validation_before_gpu(rs):
     assert e.value.status == rs.RS_EINVAL
     with pytest.raises(rs.RSError) as e:
         rs.rs_create_csr(3, 2, np.array([0, 1, 1, 1]), np.array([0], np.int32), np.ones(1),
-                         y, 1.0, mode="explicit")
-    assert e.value.status == rs.RS_EUNSUPPORTED
+                         y, -1.0, mode="explicit")
+    assert e.value.status == rs.RS_EINVAL
+    with pytest.raises(rs.RSError) as e:
+        rs.rs_create_kernel(X, y, 1.0, 0.0)    # sigma must be > 0
+    assert e.value.status == rs.RS_EINVAL
     with pytest.raises(rs.RSError) as e:
         rs.rs_sketch_draw("count", 10, 11, 0, 0)   # tau > m
     assert e.value.status == rs.RS_EINVAL

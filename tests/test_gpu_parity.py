@@ -565,3 +565,57 @@ def test_dirty_device_memory(rs, mode, kind, tau):
     ref = OV.solve(X, y, 0.7, kind, tau, 1.0, 0.5, 0.0, 9, seed=2)
     assert rel(w, ref["w"]) <= 1e-10
     assert rel(r, ref["r"]) <= 1e-10
+
+
+# -------------------------------------------------------------- sparse explicit A (NEXT-3)
+@pytest.mark.parametrize("kind,tau,k", [("count", 40, 0), ("subsample", 33, 0), ("subcount", 20, 3),
+                                        ("count", 300, 0)])
+def test_csr_explicit_primal(rs, kind, tau, k):
+    n, d = 4000, 600
+    rp, ci, v, y, Xs = _csr_primal(n, d, per_row=90, seed=9)   # rows > 64 nnz: heavy-row DMMA block
+    h = rs.rs_create_csr(n, d, rp, ci, v, y, 1e-2, mode="explicit")
+    try:
+        w, rep = rs.rs_solve(h, kind, tau, 1.0, 0.5, 0.0, 15, seed=2, subcount_k=k)
+        ws, r = rs.rs_get_state(h)
+    finally:
+        rs.rs_destroy(h)
+    ref = OV.solve(Xs, y, 1e-2, kind, tau, 1.0, 0.5, 0.0, 15, seed=2, subcount_k=k, explicit=True)
+    assert rel(w, ref["w"]) <= 1e-10
+    assert rel(r, ref["r"]) <= 1e-10
+
+
+@pytest.mark.parametrize("kind,tau,k", [("subcount", 16, 4), ("subsample", 25, 0), ("count", 12, 0),
+                                        ("subcount", 240, 1)])
+def test_csr_explicit_dual(rs, kind, tau, k):
+    n, d = 300, 5000
+    rp, ci, v, y = rsinputs.csr_zipf(n, d, 60, a=1.1, seed=3)   # Zipf head: columns > 64 nnz
+    Xs = rsinputs.csr_to_scipy(rp, ci, v, n, d)
+    h = rs.rs_create_csr(n, d, rp, ci, v, y, 1e-1, mode="explicit")
+    try:
+        w, rep = rs.rs_solve(h, kind, tau, 1.0, 0.5, 0.0, 15, seed=4, subcount_k=k, d=d, alpha=True)
+        alpha, r = rs.rs_get_state(h)
+    finally:
+        rs.rs_destroy(h)
+    ref = OV.solve(Xs, y, 1e-1, kind, tau, 1.0, 0.5, 0.0, 15, seed=4, subcount_k=k, explicit=True)
+    assert rel(alpha, ref["w"]) <= 1e-10
+    assert rel(r, ref["r"]) <= 1e-10
+    assert rel(w, ref["weights"]) <= 1e-10
+
+
+def test_csr_explicit_config4_full_size(rs):
+    """BASELINE.json c4 (2e4 x 1e6, Zipf) with the sparse explicit A (NEXT-3): 3 iterations equal
+    the oracle's (implicit oracle: A S = X (X^T S) + lambda S, the same iterates in exact
+    arithmetic)."""
+    cfg, rp, ci, va, y = _csr_cfg("c4")
+    h = rs.rs_create_csr(cfg.n, cfg.d, rp, ci, va, y, cfg.lam, mode="explicit")
+    try:
+        w, rep = rs.rs_solve(h, cfg.sketch, cfg.tau, cfg.gamma, cfg.beta, 0.0, 3, seed=0,
+                             subcount_k=cfg.subcount_k, check_every=50, d=cfg.d)
+        it, r = rs.rs_get_state(h)
+    finally:
+        rs.rs_destroy(h)
+    Xs = rsinputs.csr_to_scipy(rp, ci, va, cfg.n, cfg.d)
+    ref = OV.solve(Xs, y, cfg.lam, cfg.sketch, cfg.tau, cfg.gamma, cfg.beta, 0.0, 3, seed=0,
+                   subcount_k=cfg.subcount_k)
+    assert rel(it, ref["w"]) <= 1e-10
+    assert rel(r, ref["r"]) <= 1e-10
