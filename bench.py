@@ -257,13 +257,16 @@ def _roofline(args, cfg, world, kms, kl, dom, prof_ms, host, rs):
                         peak_source=dmma_src, algorithmic_per_launch=f"{w:.3e} flop (2 n tau^2)")
         elif dom == "factor":
             slots = kl["update"] / max(kl["factor"], 1)   # iterations (G_k) per group
-            w = float(cfg.tau) ** 3 * slots
-            roof = dict(kernel="batched Cholesky + inverse + W^T W of the group's G_k "
-                               "(k_bfactor_small / k_bfactor_big, DMMA)", bound="tensor",
+            big = cfg.tau > 224   # k_bfactor_big stores W = L^{-1}; W^T W is applied as two GEMVs
+            w = float(cfg.tau) ** 3 * (2.0 / 3.0 if big else 1.0) * slots
+            what = ("tau^3/3 Cholesky + tau^3/3 inverse" if big else
+                    "tau^3/3 Cholesky + tau^3/3 inverse + tau^3/3 W^T W")
+            roof = dict(kernel="batched Cholesky + triangular inverse of the group's G_k "
+                               f"({'k_bfactor_big' if big else 'k_bfactor_small'}, DMMA)",
+                        bound="tensor",
                         achieved=w / (ms * 1e-3) / 1e12, peak=FP64_DMMA_PEAK, unit="TFLOP/s",
                         peak_source=dmma_src,
-                        algorithmic_per_launch=f"{w:.3e} flop (tau^3 per G_k: tau^3/3 Cholesky + "
-                                               f"tau^3/3 inverse + tau^3/3 W^T W, x {slots:.0f} slots)")
+                        algorithmic_per_launch=f"{w:.3e} flop ({what} per G_k, x {slots:.0f} slots)")
         else:   # explicit: rows of A + GEMV + update
             rows_s = cfg.extra.get("rows", cfg.tau)
             w = (rows_s * cfg.d + 10 * cfg.d) * 8.0

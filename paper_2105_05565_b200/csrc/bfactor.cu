@@ -10,15 +10,19 @@
 //                   (lower triangle of G read only, R12; empty-bucket rule R3)
 //   W = L^{-1}      blocked in-place triangular inversion (column blocks from the last):
 //                   W_JJ = L_JJ^{-1},  W_IJ = -(sum_{K=J+1..I} W_IK L_KJ) W_JJ
-//   Ginv = W^T W    = G^{-1}, written in full (tau x tau, row-major) to the slot
+//   Ginv = W^T W    = G^{-1}, written in full (tau x tau, row-major) to the slot (tau <= 224); for
+//                   tau > 224 the slot holds W (lower) and W^T (upper) instead
 //
-// so the iteration needs only delta = Ginv (S^T r^k) (P:L217 least-norm solution = G^{-1} g for SPD
-// G, R3/R21): a parallel GEMV instead of a latency-bound factorisation per iteration.
+// so the iteration needs only delta = Ginv (S^T r^k) = W^T (W g) (P:L217 least-norm solution =
+// G^{-1} g for SPD G, R3/R21): parallel GEMVs instead of a latency-bound factorisation per
+// iteration.
 //
 // Shared-memory layout (one CTA, tau <= 224): the lower block triangle of G as 8 x 8 blocks packed by
 // block row (block (I, J), J <= I, at index I(I+1)/2 + J), each block row-major with an XOR swizzle
 // (column c of row r at c ^ 4((r >> 1) & 1)) so DMMA fragment loads -- plain and transposed -- are
 // bank-conflict free; then a panel temp of Tc blocks.
+#include <cstdlib>
+
 #include "rs_internal.cuh"
 
 namespace rs {
@@ -272,6 +276,7 @@ k_bfactor_small(FactorSrc src, DevSketch skb, double* __restrict__ Ginv, long lo
 __global__ void __launch_bounds__(AG_WARPS * 32)
 k_sketch_g(DevSketch sk, const int* __restrict__ flag, const double* __restrict__ r,
            double* __restrict__ g, const Ctrl* ctrl) {
+  pdl_trigger();   // the iteration's GEMV / update kernels may start their static loads
   if (ctrl->done || *flag) return;
   const int lane = threadIdx.x & 31;
   const int b = blockIdx.x * AG_WARPS + (threadIdx.x >> 5);
@@ -286,40 +291,80 @@ k_sketch_g(DevSketch sk, const int* __restrict__ flag, const double* __restrict_
   if (lane == 0) g[b] = v;
 }
 
-// delta = Ginv g; one warp per row of Ginv.
+// Row GEMVs of the iteration, out_a = sum_c M[a][c] x_c over the column range of row a:
+//   AP_FULL   (tau <= 224)  the slot holds G^{-1} in full:        delta = G^{-1} g, c in [0, tau)
+//   AP_LOWER  (tau > 224)   lower triangle of the slot = W = L^{-1}: t = W g,      c in [0, a]
+//   AP_UPPER  (tau > 224)   upper triangle of the slot = W^T:       delta = W^T t, c in [a, tau)
+// AP_FULL / AP_UPPER also scatter S delta.  A block of 8 warps owns 2 rows, 4 warps per row
+// (32-column chunks interleaved over the 4 warps).  The kernels are launched as a PDL chain after
+// k_sketch_g: the first AP_PRE chunks of each lane's part of the row (the slot is static) are
+// loaded into registers BEFORE pdl_wait(), so the slot reads of all three kernels of the iteration
+// overlap each other and the predecessor; only the x vector is read after the wait.
+enum { AP_FULL = 0, AP_LOWER = 1, AP_UPPER = 2 };
+constexpr int AP_WPR = 4;                      // warps per row
+constexpr int AP_ROWS = AG_WARPS / AP_WPR;     // rows per block
+constexpr int AP_PRE = 8;                      // register-preloaded values per lane (1024 columns)
+
+template <int MODE>
 __global__ void __launch_bounds__(AG_WARPS * 32)
-k_apply_ginv(const double* __restrict__ Ginv, long long ldgi, DevSketch sk,
-             const int* __restrict__ flag, const double* __restrict__ gv, double* __restrict__ delta,
-             double* __restrict__ sdelta, Ctrl* ctrl) {
-  if (ctrl->done) return;
-  if (*flag) {   // the update kernel of this iteration turns the status into `done`
-    if (blockIdx.x == 0 && threadIdx.x == 0) ctrl->status = ST_NOTSPD;
+k_apply_rows(const double* __restrict__ Mx, long long ldm, DevSketch sk, const int* __restrict__ flag,
+             const double* __restrict__ x, double* __restrict__ out, double* __restrict__ sdelta,
+             Ctrl* ctrl) {
+  pdl_trigger();
+  if (ctrl->done) return;   // previous iteration's stop rule (static for this chain)
+  const int bad = *flag;    // factor slot not SPD (static)
+  __shared__ double xs[AG_MAXTAU];
+  __shared__ double red[AG_WARPS];
+  const int tau = sk.tau, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int q = warp % AP_WPR, a = blockIdx.x * AP_ROWS + warp / AP_WPR;
+  const int c0 = MODE == AP_UPPER ? a : 0, c1 = MODE == AP_LOWER ? a + 1 : tau;
+  const double* row = Mx + (long long)min(a, tau - 1) * ldm;
+  const int cb = c0 + 32 * q + lane;                 // chunk u: column cb + 128 u
+  const int p1 = min(c1, c0 + 32 * AP_WPR * AP_PRE);   // end of the preloaded pass
+  double v[AP_PRE];
+#pragma unroll
+  for (int u = 0; u < AP_PRE; ++u) {
+    const int c = cb + 32 * AP_WPR * u;
+    v[u] = (!bad && a < tau && c < p1) ? __ldg(row + c) : 0.0;
+  }
+  pdl_wait();
+  if (bad) {   // the update kernel of this iteration turns the status into `done`
+    if (MODE != AP_UPPER && blockIdx.x == 0 && tid == 0) ctrl->status = ST_NOTSPD;
     return;
   }
-  __shared__ double g[AG_MAXTAU];
-  const int tau = sk.tau, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  for (int b = tid; b < tau; b += AG_WARPS * 32) g[b] = gv[b];
+  const int xlo = MODE == AP_UPPER ? min(tau, blockIdx.x * AP_ROWS) : 0;
+  const int xhi = MODE == AP_LOWER ? min(tau, (blockIdx.x + 1) * AP_ROWS) : tau;
+  for (int c = xlo + tid; c < xhi; c += AG_WARPS * 32) xs[c] = x[c];
   __syncthreads();
-  const int a = blockIdx.x * AG_WARPS + warp;
-  if (a >= tau) return;
-  const double* row = Ginv + (long long)a * ldgi;
-  double s = 0.0;
-  for (int b = lane; b < tau; b += 32) s += row[b] * g[b];
+  double s0 = 0.0, s1 = 0.0;
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-  if (lane == 0) delta[a] = s;
-  for (int e = sk.bptr[a] + lane; e < sk.bptr[a + 1]; e += 32)
-    sdelta[sk.coord[e]] = sk.sign[e] > 0 ? s : -s;
+  for (int u = 0; u < AP_PRE; ++u) {
+    const int c = cb + 32 * AP_WPR * u;
+    if (c < p1) (u & 1 ? s1 : s0) += v[u] * xs[c];
+  }
+  for (int c = p1 + 32 * q + lane; c < c1; c += 32 * AP_WPR) s0 += __ldg(row + c) * xs[c];
+  double t = s0 + s1;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+  if (lane == 0) red[warp] = t;
+  __syncthreads();
+  if (q != 0 || a >= tau) return;
+  const int w0 = warp;   // first warp of the row
+  const double sa = (red[w0] + red[w0 + 1]) + (red[w0 + 2] + red[w0 + 3]);
+  if (lane == 0) out[a] = sa;
+  if (MODE != AP_LOWER)
+    for (int e = sk.bptr[a] + lane; e < sk.bptr[a + 1]; e += 32)
+      sdelta[sk.coord[e]] = sk.sign[e] > 0 ? sa : -sa;
 }
 
 // =================================================================================================
-// Large tau (BF_MAXTAU < tau <= BB_MAXTAU): the same three steps with G held in global memory (a
+// Large tau (BF_MAXTAU < tau <= BB_MAXTAU): the first two steps with G held in global memory (a
 // per-slot work matrix, zero-padded to whole 32 x 32 tiles with an identity tail so that every tile
 // is full), one CTA of 16 warps per slot, every tile product on DMMA (one warp per 32 x 32 tile):
 //   Cholesky   right-looking over block columns p: warp 0 factors L_pp in registers and forms
 //              L_pp^{-1}; panel L_ip = G_ip L_pp^{-T}; trailing G_ij -= L_ip L_jp^T (j <= i)
 //   W = L^{-1} block columns J from the last: T_I = sum_{K=J+1..I} W_IK L_KJ, W_IJ = -T_I W_JJ
-//   Ginv       = W^T W, block (I, J) = sum_{K >= I} W_KI^T W_KJ, mirrored into the full slot
+//   the slot receives W (lower) and W^T (upper); delta = W^T (W g) per iteration (k_apply_w, _wt)
 constexpr int BB_THREADS = 512;
 constexpr int BB_WARPS = BB_THREADS / 32;
 constexpr int BB_MAXTAU = 4096;
@@ -532,28 +577,16 @@ k_bfactor_big(FactorSrc src, DevSketch skb, double* __restrict__ Ginv, long long
     }
     __syncthreads();
   }
-  // ---- Ginv = W^T W (block (I, J), J <= I), mirrored
+  // ---- the slot receives W = L^{-1} in its lower triangle and W^T in its upper triangle (both
+  // row-contiguous): G^{-1} = W^T W is applied as two triangular GEMVs per iteration (k_apply_w,
+  // k_apply_wt), which saves the W^T W product (a third of the factorisation's flops)
   double* Gi = Ginv + slot * gi_stride;
-  const int npairs = Tc * (Tc + 1) / 2;
-  for (int t = warp; t < npairs; t += BB_WARPS) {
-    int I, J;
-    tri_decode(t, I, J);
-    acc_zero(acc);
-    for (int K = I; K < Tc; ++K) mma_tile<true, false>(acc, T(K, I), tp, T(K, J), tp, lane, 1.0);
-    const int q = lane >> 2, k4 = lane & 3;
-#pragma unroll
-    for (int R = 0; R < 4; ++R)
-#pragma unroll
-      for (int C = 0; C < 4; ++C)
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const int row = 32 * I + 8 * R + q, col = 32 * J + 8 * C + 2 * k4 + h;
-          if (row < tau && col < tau) {
-            Gi[(long long)row * ldgi + col] = acc[R][C][h];
-            if (I != J) Gi[(long long)col * ldgi + row] = acc[R][C][h];
-          }
-        }
-  }
+  for (int row = warp; row < tau; row += BB_WARPS)
+    for (int col = lane; col <= row; col += 32) {
+      const double x = Wm[(long long)row * tp + col];
+      Gi[(long long)row * ldgi + col] = x;
+      if (col < row) Gi[(long long)col * ldgi + row] = x;
+    }
   if (tid == 0) flags[slot] = 0;
 }
 
@@ -591,10 +624,31 @@ cudaError_t launch_apply_ginv(const double* Ginv, long long ldgi, const DevSketc
                               const int* flag, const double* r, double* gbuf, double* delta,
                               double* sdelta, Ctrl* ctrl, cudaStream_t st) {
   if (sk.tau > AG_MAXTAU) return cudaErrorInvalidValue;
-  const unsigned grid = (unsigned)((sk.tau + AG_WARPS - 1) / AG_WARPS);
-  k_sketch_g<<<grid, AG_WARPS * 32, 0, st>>>(sk, flag, r, gbuf, ctrl);
-  k_apply_ginv<<<grid, AG_WARPS * 32, 0, st>>>(Ginv, ldgi, sk, flag, gbuf, delta, sdelta, ctrl);
-  return cudaGetLastError();
+  k_sketch_g<<<(unsigned)((sk.tau + AG_WARPS - 1) / AG_WARPS), AG_WARPS * 32, 0, st>>>(sk, flag, r,
+                                                                                      gbuf, ctrl);
+  {
+    const cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+  }
+  const dim3 grid((unsigned)((sk.tau + AP_ROWS - 1) / AP_ROWS)), blk(AG_WARPS * 32);
+  if (sk.tau > BF_MAXTAU) {   // slot holds W = L^{-1} (lower) and W^T (upper): delta = W^T (W g)
+    double* tv = gbuf + sk.tau;
+    const cudaError_t e = launch_pdl(k_apply_rows<AP_LOWER>, grid, blk, 0, st, Ginv, ldgi, sk, flag,
+                                     (const double*)gbuf, tv, sdelta, ctrl);
+    if (e != cudaSuccess) return e;
+    return launch_pdl(k_apply_rows<AP_UPPER>, grid, blk, 0, st, Ginv, ldgi, sk, flag,
+                      (const double*)tv, delta, sdelta, ctrl);
+  }
+  return launch_pdl(k_apply_rows<AP_FULL>, grid, blk, 0, st, Ginv, ldgi, sk, flag,
+                    (const double*)gbuf, delta, sdelta, ctrl);
+}
+
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("RS_PDL");
+    return !(e && e[0] == '0');
+  }();
+  return on;
 }
 
 }  // namespace rs

@@ -36,6 +36,33 @@ struct Ctrl {
   long long mom_ntab;
 };
 
+// Programmatic dependent launch (PDL).  A kernel launched by launch_pdl may start while its
+// predecessor in the stream is still running.  Everything it reads before pdl_wait() must have been
+// written before the last ordinarily launched kernel of the chain (static data: A, the sketches, the
+// factor slots, and ctrl->done of the previous iteration); pdl_wait() blocks until the predecessor
+// grid has completed and its writes are visible (a no-op without the launch attribute);
+// pdl_trigger() lets the successor launch.  RS_PDL=0 in the environment turns PDL off.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() {
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+}
+bool pdl_enabled();
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                       Args... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, ((KArgs)args)...);
+}
+
 // (gamma_k, beta_k) of iteration k = ctrl->k (read by the update kernels before ctrl->k moves on)
 __device__ __forceinline__ void mom_at(const Ctrl* c, double& gamma, double& beta) {
   const int kind = c->mom_kind;
@@ -255,7 +282,8 @@ cudaError_t launch_bfactor(const FactorSrc& src, const DevSketch& skb, int nslot
                            long long ldgi, long long gi_stride, int* flags, double* work,
                            const Ctrl* ctrl, cudaStream_t st);
 // delta = Ginv (S^T r), sdelta[coord_e] = sign_e delta[bucket_e]; flag != 0 -> status NOTSPD.
-// gbuf: tau doubles of scratch (g).
+// tau <= 224: the slot holds G^{-1} (full); tau > 224: it holds W = L^{-1} (lower) and
+// delta = W^T (W g).  gbuf: 2 tau doubles of scratch (g, W g).
 cudaError_t launch_apply_ginv(const double* Ginv, long long ldgi, const DevSketch& sk,
                               const int* flag, const double* r, double* gbuf, double* delta,
                               double* sdelta, Ctrl* ctrl, cudaStream_t st);

@@ -228,16 +228,19 @@ k_update_vec(const double* __restrict__ u, double lambda, double* __restrict__ s
   }
 }
 
-// Explicit A, few sketch entries: block = 32 coordinates j x 32 entry slices; u_j =
-// sum_e sd_e A[coord_e][j] with sd_e = sign_e delta[bucket_e] staged in shared memory (rows of A are
-// contiguous: coalesced over j, L2-resident when A fits).
+// Explicit A, few sketch entries: block = 64 coordinates j (a warp reads 512 contiguous bytes of a
+// row of A as double2) x RW_Y warps over the entries; u_j = sum_e sd_e A[coord_e][j] with
+// sd_e = sign_e delta[bucket_e] (A symmetric: row coord_e = column coord_e).  Launched as the last
+// kernel of the iteration's PDL chain (bfactor.cu): the first RW_PRE rows of each warp (A and the
+// sketch are static) are loaded into registers BEFORE pdl_wait(), overlapping the solve kernels.
 constexpr int RW_Y = 8;
+constexpr int RW_PRE = 8;
+constexpr int RW_COLS = 64;
 constexpr int RW_MAXS = 16;
-// u = A S delta over the rows e of slot `sk` (A symmetric: row coord_e = column), split over
-// gridDim.y row ranges: block (cb, sp) sums rows e in its range for columns 32 cb .. 32 cb + 31
-// into upart[sp][j]; the last split of a column block (counter cnt[cb]) adds the splits in order
-// (deterministic), applies the momentum update to its 32 coordinates and contributes ||r||^2;
-// the last column block finishes the iteration.
+// u = A S delta over the rows e of slot `sk`, split over gridDim.y row ranges: block (cb, sp) sums
+// rows e in its range for columns 64 cb .. 64 cb + 63 into upart[sp][j]; the last split of a column
+// block (counter cnt[cb]) adds the splits in order (deterministic), applies the momentum update to
+// its 64 coordinates and contributes ||r||^2; the last column block finishes the iteration.
 __global__ void __launch_bounds__(32 * RW_Y)
 k_update_rows(const double* __restrict__ A, long long lda, DevSketch sk,
               const double* __restrict__ delta, double* __restrict__ sdelta,
@@ -245,41 +248,70 @@ k_update_rows(const double* __restrict__ A, long long lda, DevSketch sk,
               double* __restrict__ dr, long long m, double gamma, double beta,
               double* __restrict__ partials, double* __restrict__ upart, int* __restrict__ cnt,
               Ctrl* ctrl) {
-  if (ctrl->done) return;
-  if (ctrl->status >= ST_NOTSPD) {
-    if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0 && threadIdx.y == 0) ctrl->done = 1;
-    return;
-  }
-  mom_at(ctrl, gamma, beta);   // schedule (gamma_k, beta_k), rs_momentum
-  extern __shared__ double rw_sm[];   // [span] sd_e, then [span] coord_e (as int)
-  __shared__ double red[RW_Y][33];
+  pdl_trigger();
+  if (ctrl->done) return;   // previous iteration's stop rule (static for this chain)
+  __shared__ double red[RW_Y][2][33];
   __shared__ bool s_last;
   const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * 32 + tx;
-  const int len = sk.bptr[sk.tau];
+  const int len = sk.len;   // = bptr[tau] for subsample / SubCount / count
   const int ns = gridDim.y, sp = blockIdx.y;
   const int per = (len + ns - 1) / ns;
   const int e0 = min(len, sp * per), e1 = min(len, e0 + per), span = e1 - e0;
-  int* s_coord = reinterpret_cast<int*>(rw_sm + per);
-  for (int e = tid; e < span; e += 32 * RW_Y) {
+  // lane tx owns columns j0, j0 + 1 (lda is a multiple of 4 doubles, so the pair is 16-B aligned and
+  // inside the row's padding when j0 + 1 == m)
+  const long long j0 = (long long)blockIdx.x * RW_COLS + 2 * tx;
+  const bool jin = j0 < m;
+  double2 v[RW_PRE];
+  int sb[RW_PRE];   // bucket, bit-complemented for a negative sign
+#pragma unroll
+  for (int u = 0; u < RW_PRE; ++u) {
+    const int e = ty + RW_Y * u;
+    v[u] = make_double2(0.0, 0.0);
+    sb[u] = 0;
+    if (e < span) {
+      const int c = sk.coord[e0 + e];
+      sb[u] = sk.sign[e0 + e] > 0 ? sk.bucket[e0 + e] : ~sk.bucket[e0 + e];
+      if (jin) v[u] = __ldg(reinterpret_cast<const double2*>(A + (long long)c * lda + j0));
+    }
+  }
+  pdl_wait();
+  if (ctrl->status >= ST_NOTSPD) {   // set by the solve kernels of this iteration
+    if (blockIdx.x == 0 && blockIdx.y == 0 && tid == 0) ctrl->done = 1;
+    return;
+  }
+  mom_at(ctrl, gamma, beta);   // schedule (gamma_k, beta_k), rs_momentum
+  double a0 = 0.0, a1 = 0.0;
+#pragma unroll
+  for (int u = 0; u < RW_PRE; ++u) {
+    if (ty + RW_Y * u < span) {
+      const double dv = delta[sb[u] >= 0 ? sb[u] : ~sb[u]];
+      const double sd = sb[u] >= 0 ? dv : -dv;
+      a0 += sd * v[u].x;
+      a1 += sd * v[u].y;
+    }
+  }
+  for (int e = ty + RW_Y * RW_PRE; e < span; e += RW_Y) {
+    const int c = sk.coord[e0 + e];
     const double dv = delta[sk.bucket[e0 + e]];
-    rw_sm[e] = sk.sign[e0 + e] > 0 ? dv : -dv;
-    s_coord[e] = sk.coord[e0 + e];
+    const double sd = sk.sign[e0 + e] > 0 ? dv : -dv;
+    if (jin) {
+      const double2 x = __ldg(reinterpret_cast<const double2*>(A + (long long)c * lda + j0));
+      a0 += sd * x.x;
+      a1 += sd * x.y;
+    }
   }
-  __syncthreads();
-  const long long j = (long long)blockIdx.x * 32 + tx;
-  double acc = 0.0;
-  if (j < m) {
-    const double* Aj = A + j;
-#pragma unroll 4
-    for (int e = ty; e < span; e += RW_Y) acc += rw_sm[e] * Aj[(long long)s_coord[e] * lda];
-  }
-  red[ty][tx] = acc;
+  red[ty][0][tx] = a0;
+  red[ty][1][tx] = a1;
   __syncthreads();
   if (ty == 0) {
-    double u = 0.0;
+    double u0 = 0.0, u1 = 0.0;
 #pragma unroll
-    for (int q = 0; q < RW_Y; ++q) u += red[q][tx];
-    if (j < m) upart[(long long)sp * m + j] = u;
+    for (int q = 0; q < RW_Y; ++q) {
+      u0 += red[q][0][tx];
+      u1 += red[q][1][tx];
+    }
+    if (j0 < m) upart[(long long)sp * m + j0] = u0;
+    if (j0 + 1 < m) upart[(long long)sp * m + j0 + 1] = u1;
     __threadfence();
     __syncwarp();
     if (tx == 0) s_last = atomicAdd(&cnt[blockIdx.x], 1) == ns - 1;
@@ -291,19 +323,23 @@ k_update_rows(const double* __restrict__ A, long long lda, DevSketch sk,
   if (ty == 0) {
     __threadfence();
     double r2 = 0.0;
-    if (j < m) {
-      double u = 0.0;
-      for (int q = 0; q < ns; ++q) u += __ldcg(&upart[(long long)q * m + j]);
-      const double drj = beta * dr[j] - gamma * u;
-      const double rj = r[j] + drj;
-      dr[j] = drj;
-      r[j] = rj;
-      const double sd = sdelta[j];
-      sdelta[j] = 0.0;
-      const double dwj = beta * dw[j] - gamma * sd;
-      dw[j] = dwj;
-      w[j] += dwj;
-      r2 = rj * rj;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const long long j = j0 + h;
+      if (j < m) {
+        double u = 0.0;
+        for (int q = 0; q < ns; ++q) u += __ldcg(&upart[(long long)q * m + j]);
+        const double drj = beta * dr[j] - gamma * u;
+        const double rj = r[j] + drj;
+        dr[j] = drj;
+        r[j] = rj;
+        const double sd = sdelta[j];
+        sdelta[j] = 0.0;
+        const double dwj = beta * dw[j] - gamma * sd;
+        dw[j] = dwj;
+        w[j] += dwj;
+        r2 += rj * rj;
+      }
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) r2 += __shfl_down_sync(0xffffffffu, r2, o);
@@ -320,12 +356,12 @@ k_update_rows(const double* __restrict__ A, long long lda, DevSketch sk,
   __threadfence();
   double s2 = 0.0;
   for (unsigned q = tid; q < gridDim.x; q += 32 * RW_Y) s2 += __ldcg(&partials[q]);
-  red[ty][tx] = s2;
+  red[ty][0][tx] = s2;
   __syncthreads();
   if (tid == 0) {
     double tot = 0.0;
     for (int q = 0; q < RW_Y; ++q)
-      for (int p = 0; p < 32; ++p) tot += red[q][p];
+      for (int p = 0; p < 32; ++p) tot += red[q][0][p];
     finish_iteration(ctrl, tot);
   }
 }
@@ -333,7 +369,7 @@ k_update_rows(const double* __restrict__ A, long long lda, DevSketch sk,
 }  // namespace
 
 cudaError_t update_init() {
-  return cudaFuncSetAttribute(k_update_rows, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  return cudaSuccess;
 }
 
 size_t update_rows_scratch(long long m) { return (size_t)RW_MAXS * (size_t)m; }
@@ -344,15 +380,13 @@ cudaError_t launch_update_rows(const double* A, long long lda, const DevSketch& 
                                double* r, double* dr, long long m, double gamma, double beta,
                                double* partials, double* upart, int* cnt, int num_sms, Ctrl* ctrl,
                                cudaStream_t st) {
-  const long long cb = (m + 31) / 32;
-  int ns = (int)std::max<long long>(1, std::min<long long>(RW_MAXS, (2LL * num_sms + cb - 1) / cb));
-  ns = std::max(1, std::min(ns, sk.len / 8));
-  const int per = (sk.len + ns - 1) / ns;
-  const size_t smem = (size_t)per * 12;
-  if (smem > 200 * 1024) return cudaErrorInvalidValue;
-  k_update_rows<<<dim3((unsigned)cb, (unsigned)ns), dim3(32, RW_Y), smem, st>>>(
-      A, lda, sk, delta, sdelta, w, dw, r, dr, m, gamma, beta, partials, upart, cnt, ctrl);
-  return cudaGetLastError();
+  const long long cb = (m + RW_COLS - 1) / RW_COLS;
+  // splits: every warp's rows fit its register preload when possible, and >= 2 blocks per SM
+  long long ns = (sk.len + RW_Y * RW_PRE - 1) / (RW_Y * RW_PRE);
+  ns = std::max(ns, (2LL * num_sms + cb - 1) / cb);
+  ns = std::max(1LL, std::min<long long>({ns, (long long)RW_MAXS, (long long)sk.len / RW_Y}));
+  return launch_pdl(k_update_rows, dim3((unsigned)cb, (unsigned)ns), dim3(32, RW_Y), 0, st, A, lda,
+                    sk, delta, sdelta, w, dw, r, dr, m, gamma, beta, partials, upart, cnt, ctrl);
 }
 
 cudaError_t launch_update_vec(const double* u, double lambda, double* sdelta, double* w, double* dw,
