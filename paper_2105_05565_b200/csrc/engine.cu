@@ -522,7 +522,8 @@ rs_status Problem::enqueue_iteration(const rs_solve_opts* o, cudaEvent_t* ev) {
     mark(RS_K_SOLVE, 1);
     mark(RS_K_AS, 0);
     if (rows_loc > 0)
-      RS_CUDA(launch_xpass(X, ldx, rows_loc, m, sdelta, xp_part, uvec, num_sms, ctrl, st));
+      RS_CUDA(launch_xpass(X, ldx, rows_loc, m, sdelta, xp_part, uvec, num_sms, ctrl, st, &sk,
+                           sw.delta));
     else
       RS_CUDA(launch_fill(uvec, m, 0.0, st));
     RS_TRY(allreduce(uvec, (size_t)m));                                     // X^T X S delta
@@ -643,7 +644,8 @@ rs_status Problem::enqueue_pipelined_iteration(const rs_solve_opts* o, int slot,
   if (fmt == 1)
     RS_TRY(csr_gram_apply(sdelta, uvec));                                        // R^T R S delta
   else if (rows_loc > 0)
-    RS_CUDA(launch_xpass(X, ldx, rows_loc, m, sdelta, xp_part, uvec, num_sms, ctrl, st));
+    RS_CUDA(launch_xpass(X, ldx, rows_loc, m, sdelta, xp_part, uvec, num_sms, ctrl, st, &sq,
+                         sw.delta));
   else
     RS_CUDA(launch_fill(uvec, m, 0.0, st));
   RS_TRY(allreduce(uvec, (size_t)m));                                            // X^T X S delta

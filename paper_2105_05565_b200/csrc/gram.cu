@@ -184,6 +184,113 @@ k_xpass_tma(const double* __restrict__ X, long long ldx, long long rows, long lo
   }
 }
 
+// Row-owner variant (d <= 2048, v = S delta sparse): the same TMA ring, but each consumer warp owns
+// whole rows (local row i -> warp i mod 8), so no CTA barrier or cross-warp reduction per row:
+//   t_i = <X_i, v> over the len sketch entries only (v = S delta has len nonzeros: coord_e, and
+//         sd_e = sign_e delta_{bucket_e}, staged once in shared memory behind the ring),
+//   acc += t_i X_i (the warp's own d-vector accumulator in registers, XR_NQ values per lane).
+// Every warp waits on every block's "full" barrier in order (also blocks without a row of its own),
+// so no warp can run two phases ahead of a stage; "empty" counts the R row releases of a stage.  At
+// the end the 8 warp accumulators are summed in warp order through shared memory (deterministic).
+constexpr int XR_CONS = 8;
+constexpr int XR_THREADS = (XR_CONS + 1) * 32;
+constexpr int XR_NQ = 64;                     // d <= 2048
+constexpr int XR_MAXLEN = 4096;               // sketch entries
+
+__global__ void __launch_bounds__(XR_THREADS, 1)
+k_xpass_rows(const double* __restrict__ X, long long ldx, long long rows, long long d, DevSketch sk,
+             const double* __restrict__ delta, double* __restrict__ partials,
+             long long rows_per_cta, int R, int stages, const Ctrl* ctrl) {
+  if (ctrl->done) return;
+  extern __shared__ __align__(128) double xs_ring[];   // [stages][R * ldx], then sd[len], coord[len]
+  __shared__ __align__(8) uint64_t full[8], empty[8];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const long long r0 = (long long)blockIdx.x * rows_per_cta;
+  const long long r1 = min(rows, r0 + rows_per_cta);
+  const long long nrows = r0 < r1 ? r1 - r0 : 0;
+  const int nblk = (int)((nrows + R - 1) / R);
+  const long long stage_elems = (long long)R * ldx;
+  const int len = sk.len;
+  double* s_sd = xs_ring + stages * stage_elems;
+  int* s_co = reinterpret_cast<int*>(s_sd + len);
+  if (tid == 0) {
+    for (int s = 0; s < stages; ++s) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(su32(&full[s])));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(su32(&empty[s])), "r"(R));
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  for (int e = tid; e < len; e += XR_THREADS) {
+    const double dv = delta[sk.bucket[e]];
+    s_sd[e] = sk.sign[e] > 0 ? dv : -dv;
+    s_co[e] = sk.coord[e];
+  }
+  __syncthreads();
+  if (warp == XR_CONS) {   // producer
+    if (lane == 0) {
+      for (int b = 0; b < nblk; ++b) {
+        const int s = b % stages;
+        if (b >= stages) xt_wait(&empty[s], ((b / stages) - 1) & 1);
+        const long long i0 = r0 + (long long)b * R;
+        const int nr = (int)min((long long)R, r1 - i0);
+        const unsigned bytes = (unsigned)(nr * ldx * 8);
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(su32(&full[s])),
+                     "r"(bytes) : "memory");
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n"
+            ::"r"(su32(xs_ring + s * stage_elems)), "l"(X + i0 * ldx), "r"(bytes), "r"(su32(&full[s]))
+            : "memory");
+      }
+    }
+    return;
+  }
+  double acc[XR_NQ];
+#pragma unroll
+  for (int q = 0; q < XR_NQ; ++q) acc[q] = 0.0;
+  for (int b = 0; b < nblk; ++b) {
+    const int s = b % stages;
+    xt_wait(&full[s], (b / stages) & 1);
+    const long long i0 = (long long)b * R;
+    const int nr = (int)min((long long)R, nrows - i0);
+    // rows i0 + r of this block owned by this warp: (i0 + r) mod 8 == warp
+    for (int r = (int)((warp - i0 % XR_CONS + XR_CONS) % XR_CONS); r < nr; r += XR_CONS) {
+      const double* row = xs_ring + s * stage_elems + (long long)r * ldx;
+      double t0 = 0.0, t1 = 0.0;
+      int e = lane;
+      for (; e + 32 < len; e += 64) {
+        t0 += s_sd[e] * row[s_co[e]];
+        t1 += s_sd[e + 32] * row[s_co[e + 32]];
+      }
+      if (e < len) t0 += s_sd[e] * row[s_co[e]];
+      double t = t0 + t1;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+#pragma unroll
+      for (int q = 0; q < XR_NQ; ++q) {
+        const int j = lane + 32 * q;
+        if (j < d) acc[q] += t * row[j];
+      }
+      __syncwarp();
+      if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(su32(&empty[s])) : "memory");
+    }
+  }
+  // every block's data has been consumed: the ring is free for the 8 warp accumulators
+  asm volatile("bar.sync 1, %0;\n" ::"n"(XR_CONS * 32) : "memory");
+  double* wacc = xs_ring + (long long)warp * d;
+#pragma unroll
+  for (int q = 0; q < XR_NQ; ++q) {
+    const int j = lane + 32 * q;
+    if (j < d) wacc[j] = acc[q];
+  }
+  asm volatile("bar.sync 1, %0;\n" ::"n"(XR_CONS * 32) : "memory");
+  for (long long j = tid; j < d; j += XR_CONS * 32) {
+    double u = 0.0;
+#pragma unroll
+    for (int w = 0; w < XR_CONS; ++w) u += xs_ring[(long long)w * d + j];
+    partials[(long long)blockIdx.x * d + j] = u;
+  }
+}
+
 // u[j] = sum_c partials[c][j]  (fixed order: 8 interleaved slices c = ty (mod 8) summed in
 // ascending c, then the slices in ascending ty).  Block: 32 coordinates x 8 slices.
 constexpr int XR_Y = 8;
@@ -691,6 +798,8 @@ cudaError_t gram_init() {
   cudaError_t e = cudaFuncSetAttribute(k_xpass_tma, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        210 * 1024);
   if (e != cudaSuccess) return e;
+  e = cudaFuncSetAttribute(k_xpass_rows, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+  if (e != cudaSuccess) return e;
   return cudaFuncSetAttribute(k_gram_fused, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               GF_STAGES * GF_BK * GF_LD * (int)sizeof(double));
 }
@@ -713,11 +822,13 @@ size_t xpass_partials(long long d, int num_sms) { return (size_t)num_sms * (size
 
 cudaError_t launch_xpass(const double* X, long long ldx, long long rows, long long d,
                          const double* v, double* partials, double* u, int num_sms,
-                         const Ctrl* ctrl, cudaStream_t st) {
+                         const Ctrl* ctrl, cudaStream_t st, const DevSketch* sk,
+                         const double* delta) {
   if (d > (long long)XP_THREADS * XP_Q) return cudaErrorInvalidValue;
   const int nc = xpass_ctas(num_sms);
   const long long rpc = std::max<long long>(1, (rows + nc - 1) / nc);
   static const bool no_tma = std::getenv("RS_NO_TMA_XPASS") != nullptr;
+  static const bool no_rows = std::getenv("RS_NO_XPASS_ROWS") != nullptr;
   // ring: R rows per stage (~64 KB), as many stages as fit in ~200 KB (>= 2)
   const long long row_bytes = ldx * 8;
   int R = (int)std::max<long long>(1, std::min<long long>(XT_MAXR, 65536 / row_bytes));
@@ -726,9 +837,13 @@ cudaError_t launch_xpass(const double* X, long long ldx, long long rows, long lo
   int stages = (int)std::min<long long>(8, (200 * 1024) / (R * row_bytes));
   static const char* es = std::getenv("RS_XP_STAGES");
   if (es) stages = std::max(2, std::min(stages, atoi(es)));
-  if (!no_tma && stages >= 2 && d <= (long long)XT_CONS * 32 * XT_Q) {
-    const size_t smem = (size_t)stages * R * row_bytes;
-    k_xpass_tma<<<nc, XT_THREADS, smem, st>>>(X, ldx, rows, d, v, partials, rpc, R, stages, ctrl);
+  const size_t ring = (size_t)stages * R * row_bytes;
+  if (!no_tma && !no_rows && sk && delta && d <= 32LL * XR_NQ && sk->len <= XR_MAXLEN &&
+      stages >= 2 && ring >= (size_t)XR_CONS * d * 8 && ring + (size_t)sk->len * 12 <= 220 * 1024) {
+    k_xpass_rows<<<nc, XR_THREADS, ring + (size_t)sk->len * 12, st>>>(X, ldx, rows, d, *sk, delta,
+                                                                      partials, rpc, R, stages, ctrl);
+  } else if (!no_tma && stages >= 2 && d <= (long long)XT_CONS * 32 * XT_Q) {
+    k_xpass_tma<<<nc, XT_THREADS, ring, st>>>(X, ldx, rows, d, v, partials, rpc, R, stages, ctrl);
   } else {
     k_xpass<<<nc, XP_THREADS, 0, st>>>(X, ldx, rows, d, v, partials, rpc, ctrl);
   }

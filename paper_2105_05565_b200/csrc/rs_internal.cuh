@@ -226,9 +226,12 @@ cudaError_t launch_update(const double* ASt, long long ld_as, bool as_rowmajor, 
 
 // Gram mode (gram.cu): u = X^T (X v) in one pass over X (d <= 4096), partials reduced in order.
 size_t xpass_partials(long long d, int num_sms);
+// v = S delta (dense, m); when the sketch and delta are given and d <= 2048, the row-owner kernel
+// forms <X_i, v> from the sketch entries only.
 cudaError_t launch_xpass(const double* X, long long ldx, long long rows, long long d,
                          const double* v, double* partials, double* u, int num_sms,
-                         const Ctrl* ctrl, cudaStream_t st);
+                         const Ctrl* ctrl, cudaStream_t st, const DevSketch* sk = nullptr,
+                         const double* delta = nullptr);
 // Fused gather + Gram (subsample, tau <= 200): G lower = sum_i X[i,C]^T X[i,C], no XS written.
 bool gram_fused_ok(int kind, int tau);
 // Fused X pass: u = X^T (X v) for this iteration AND the Gram (X S')^T (X S') of a future
