@@ -245,16 +245,18 @@ def _roofline(args, cfg, world, kms, kl, dom, prof_ms, host, rs):
                         algorithmic_per_launch=f"{w:.3e} flop (2 n d tau)")
         elif dom == "as":
             w = n_loc * cfg.d * 8.0
-            roof = dict(kernel="AS pass u = X^T (X S delta) (k_xpass_tma: one TMA-staged streaming "
-                               "read of X per iteration)", bound="hbm",
+            roof = dict(kernel="AS pass u = X^T (X S delta) (k_xpass_rows / k_xpass_tma: one "
+                               "TMA-staged streaming read of X per iteration)", bound="hbm",
                         achieved=w / (ms * 1e-3) / 1e9, peak=hbm, unit="GB/s", peak_source=hbm_src,
                         algorithmic_per_launch=f"{w:.3e} bytes (n d 8)")
         elif dom == "gram":
-            w = 2.0 * n_loc * cfg.tau * cfg.tau
-            roof = dict(kernel="Gram (XS)^T XS of one sketch (k_gram_fused gather + DMMA, or "
-                               "k_dense_xs + TMA DMMA GEMM)", bound="tensor",
+            w = 1.0 * n_loc * cfg.tau * (cfg.tau + 1)   # symmetric: the lower triangle only
+            roof = dict(kernel="Gram (XS)^T XS of one sketch (k_gram_xt: the tau sketched rows "
+                               "of X^T, DMMA; else k_gram_fused gather or XS + TMA DMMA GEMM)",
+                        bound="tensor",
                         achieved=w / (ms * 1e-3) / 1e12, peak=FP64_DMMA_PEAK, unit="TFLOP/s",
-                        peak_source=dmma_src, algorithmic_per_launch=f"{w:.3e} flop (2 n tau^2)")
+                        peak_source=dmma_src,
+                        algorithmic_per_launch=f"{w:.3e} flop (n tau (tau + 1): lower triangle)")
         elif dom == "factor":
             slots = kl["update"] / max(kl["factor"], 1)   # iterations (G_k) per group
             big = cfg.tau > 224   # k_bfactor_big stores W = L^{-1}; W^T W is applied as two GEMVs

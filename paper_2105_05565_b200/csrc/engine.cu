@@ -33,6 +33,7 @@ Problem::~Problem() {
   if (device >= 0) cudaSetDevice(device);
   if (st) cudaStreamSynchronize(st);
   free_workspace();
+  dfree(XT);
   if (own_X) dfree(X);
   dfree(y);
   dfree(b);
@@ -419,6 +420,18 @@ rs_status Problem::ensure_workspace(int kind, int tau, int ksum, int depth, bool
     RS_TRY(dalloc(&xp_part, std::max(xpass_partials(m, num_sms), gram_fused_partials(num_sms))));
     RS_TRY(dalloc(&uvec, m));
     gram_fused = gram_fused_ok(kind, tau) && !std::getenv("RS_NO_GRAM_FUSED");
+    if (gram_fused && rows_loc > 0 && !XT && !std::getenv("RS_NO_XT")) {
+      // the Gram reads the tau sketched columns as contiguous rows of X^T: built once per
+      // problem when it fits next to X (2 GiB margin)
+      const long long ldt = round_up(rows_loc, 4);
+      size_t fr = 0, tot = 0;
+      cudaMemGetInfo(&fr, &tot);
+      if ((double)m * ldt * 8.0 + 2.0 * (1 << 30) < (double)fr) {
+        RS_TRY(dalloc(&XT, (size_t)m * ldt));
+        ldxt = ldt;
+        RS_CUDA(launch_transpose(X, ldx, rows_loc, m, XT, ldxt, st));
+      }
+    }
     if (rows_loc > 0 && !gram_fused) {
       RS_CUDA(tma_gemm_plan(&tg_gram, XS, ld_xs, XS, ld_xs, tau, tau, rows_loc, num_sms));
       if (tg_gram.work_elems) RS_TRY(dalloc(&gemm_work, tg_gram.work_elems));
@@ -508,7 +521,9 @@ rs_status Problem::enqueue_iteration(const rs_solve_opts* o, cudaEvent_t* ev) {
       mark(RS_K_XS, 1);
     }
     mark(RS_K_GRAM, 0);
-    if (rows_loc > 0 && gram_fused)                                          // gather + (XS)^T XS
+    if (rows_loc > 0 && XT)                                                  // (XS)^T XS from X^T
+      RS_CUDA(launch_gram_xt(XT, ldxt, rows_loc, sk, xp_part, Gram, ld_gram, num_sms, ctrl, st));
+    else if (rows_loc > 0 && gram_fused)                                     // gather + (XS)^T XS
       RS_CUDA(launch_gram_fused(X, ldx, rows_loc, sk, xp_part, Gram, ld_gram, num_sms, ctrl, st));
     else if (rows_loc > 0)
       RS_CUDA(tma_gemm_launch(tg_gram, Gram, ld_gram, gemm_work, ctrl, st));   // (XS)^T XS
@@ -596,7 +611,9 @@ rs_status Problem::enqueue_precompute(const rs_solve_opts* o, int ns, cudaEvent_
         continue;
       }
       mark(q, RS_K_GRAM, 0);
-      if (rows_loc > 0 && gram_fused) {
+      if (rows_loc > 0 && XT) {
+        RS_CUDA(launch_gram_xt(XT, ldxt, rows_loc, sq, xp_part, Gq, ld_gram, num_sms, ctrl, st, q));
+      } else if (rows_loc > 0 && gram_fused) {
         RS_CUDA(launch_gram_fused(X, ldx, rows_loc, sq, xp_part, Gq, ld_gram, num_sms, ctrl, st, q));
       } else if (rows_loc > 0) {
         RS_CUDA(launch_dense_xs(X, ldx, rows_loc, sq, XS, ld_xs, ctrl, st, q));

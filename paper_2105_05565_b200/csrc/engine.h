@@ -79,6 +79,8 @@ struct Problem {
   double* xp_part = nullptr;
   double* uvec = nullptr;
   bool gram_fused = false;
+  double* XT = nullptr;          // dense GRAM, subsample tau <= 200: transposed local rows (d x ldxt)
+  long long ldxt = 0;
   bool use_tma = true;
   // sketch-ahead pipeline (bfactor.cu): P slots of (sketch, A S^T or Gram, Ginv, flag)
   bool pipe = false;

@@ -376,7 +376,7 @@ k_gram_fused(const double* __restrict__ X, long long ldx, long long rows, DevSke
       for (int b = 0; b <= a; ++b, ++t)
         if (t == warp) { I = a; J = b; }
   }
-  const bool active = I >= 0;
+  const bool active = I >= 0, diag = I == J;
   double acc[5][5][2];
 #pragma unroll
   for (int x = 0; x < 5; ++x)
@@ -401,7 +401,8 @@ k_gram_fused(const double* __restrict__ X, long long ldx, long long rows, DevSke
         for (int x = 0; x < 5; ++x) {   // one A fragment live at a time (register budget 128)
           const double af = rowp[I * 40 + x * 8];
 #pragma unroll
-          for (int y = 0; y < 5; ++y) dmma_g(acc[x][y], af, bf[y]);
+          for (int y = 0; y < 5; ++y)
+            if (!diag || y <= x) dmma_g(acc[x][y], af, bf[y]);   // diagonal region: lower tiles
         }
       }
     }
@@ -423,19 +424,164 @@ k_gram_fused(const double* __restrict__ X, long long ldx, long long rows, DevSke
   }
 }
 
-// G[a][b] = sum_c partials[c][a][b] for b <= a (fixed order: c ascending)
-__global__ void k_gram_reduce(const double* __restrict__ partials, int nparts, int tau,
-                              double* __restrict__ G, long long ldg, const Ctrl* ctrl, int slot = 0) {
+// Gram from the transposed copy XT (d x n, row-major, built once per problem): the tau sketched
+// columns of X are tau contiguous rows of XT, so a K-slice of the Gram reads tau coalesced
+// 128-byte segments per 16 rows of X (the algorithmic tau n 8 bytes) instead of gathering 8-byte
+// elements that touch ~0.8 of X's lines.  Stage layout [region rows][GX_LDK] (k contiguous,
+// stride 20 doubles: conflict-free DMMA fragments); the same 15-warp 40 x 40 region split and
+// per-CTA partials as k_gram_fused, reduced in order by k_gram_reduce.
+// BK k-values per stage (row stride BK + 4 doubles: conflict-free fragments), STAGES deep
+template <int BK> struct GxCfg {
+  static constexpr int LDK = BK + 4;
+  static constexpr int STAGES = BK == 16 ? 6 : 3;
+};
+
+__device__ __forceinline__ void cp_async16z(void* smem, const void* gmem, int src_bytes) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(src_bytes));
+}
+
+template <int GX_BK>
+__global__ void __launch_bounds__(GF_THREADS, 1)
+k_gram_xt(const double* __restrict__ XT, long long ldxt, long long rows, DevSketch sk,
+          long long rows_per_cta, double* __restrict__ partials, int slot, const Ctrl* ctrl) {
+  constexpr int GX_LDK = GxCfg<GX_BK>::LDK, GX_STAGES = GxCfg<GX_BK>::STAGES;
   if (slot_unused(ctrl, slot)) return;
-  const int a = blockIdx.x;
-  for (int b = threadIdx.x; b <= a; b += blockDim.x) {
-    const double* p = partials + a * GF_MAXTAU + b;
-    double s = 0.0;
-#pragma unroll 8
-    for (int c = 0; c < nparts; ++c) s += __ldcs(p + (long long)c * GF_MAXTAU * GF_MAXTAU);
-    G[(long long)a * ldg + b] = s;
+  extern __shared__ __align__(16) double gsm[];   // [GX_STAGES][ng * 40][GX_LDK]
+  __shared__ int s_col[GF_MAXTAU];
+  const int tau = sk.tau, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int b = tid; b < tau; b += GF_THREADS) s_col[b] = sk.coord[sk.bptr[b]];
+  __syncthreads();
+  const long long r0 = (long long)blockIdx.x * rows_per_cta;
+  const long long r1 = min(rows, r0 + rows_per_cta);
+  const int nkb = r0 < r1 ? (int)((r1 - r0 + GX_BK - 1) / GX_BK) : 0;
+  const int ng = (tau + 39) / 40, srows = ng * 40;
+  const int stage_elems = srows * GX_LDK;
+  auto load = [&](int stage, int kb) {
+    double* dst = gsm + stage * stage_elems;
+    const long long k0 = r0 + (long long)kb * GX_BK;
+    for (int q = tid; q < srows * (GX_BK / 2); q += GF_THREADS) {
+      const int b = q / (GX_BK / 2), h = q % (GX_BK / 2);
+      const long long k = k0 + 2 * h;
+      const int nb = (b < tau) ? (int)max(0LL, min(2LL, r1 - k)) * 8 : 0;
+      cp_async16z(dst + b * GX_LDK + 2 * h, nb ? XT + (long long)s_col[b] * ldxt + k : XT, nb);
+    }
+  };
+#pragma unroll
+  for (int s = 0; s < GX_STAGES - 1; ++s) {
+    if (s < nkb) load(s, s);
+    asm volatile("cp.async.commit_group;\n");
+  }
+  int I = -1, J = -1;
+  {
+    int t = 0;
+    for (int a = 0; a < ng; ++a)
+      for (int b = 0; b <= a; ++b, ++t)
+        if (t == warp) { I = a; J = b; }
+  }
+  const bool active = I >= 0, diag = I == J;
+  double acc[5][5][2];
+#pragma unroll
+  for (int x = 0; x < 5; ++x)
+#pragma unroll
+    for (int y = 0; y < 5; ++y) acc[x][y][0] = acc[x][y][1] = 0.0;
+  const int kq = lane & 3, mq = lane >> 2;
+  for (int kb = 0; kb < nkb; ++kb) {
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(GX_STAGES - 2));
+    __syncthreads();
+    const int nxt = kb + GX_STAGES - 1;
+    if (nxt < nkb) load(nxt % GX_STAGES, nxt);
+    asm volatile("cp.async.commit_group;\n");
+    if (active) {
+      const double* st = gsm + (kb % GX_STAGES) * stage_elems + mq * GX_LDK + kq;
+      const double* sa = st + (I * 40) * GX_LDK;
+      const double* sb = st + (J * 40) * GX_LDK;
+#pragma unroll
+      for (int kk = 0; kk < GX_BK; kk += 4) {
+        double bf[5];
+#pragma unroll
+        for (int y = 0; y < 5; ++y) bf[y] = sb[y * 8 * GX_LDK + kk];
+#pragma unroll
+        for (int x = 0; x < 5; ++x) {
+          const double af = sa[x * 8 * GX_LDK + kk];
+#pragma unroll
+          for (int y = 0; y < 5; ++y)
+            if (!diag || y <= x) dmma_g(acc[x][y], af, bf[y]);   // diagonal region: lower tiles
+        }
+      }
+    }
+  }
+  asm volatile("cp.async.wait_group 0;\n");
+  if (!active) return;
+  double* out = partials + (long long)blockIdx.x * GF_MAXTAU * GF_MAXTAU;
+#pragma unroll
+  for (int x = 0; x < 5; ++x) {
+    const int a = I * 40 + x * 8 + (lane >> 2);
+#pragma unroll
+    for (int y = 0; y < 5; ++y) {
+      const int b = J * 40 + y * 8 + 2 * (lane & 3);
+      if (a < tau) {
+        if (b < tau) out[a * GF_MAXTAU + b] = acc[x][y][0];
+        if (b + 1 < tau) out[a * GF_MAXTAU + b + 1] = acc[x][y][1];
+      }
+    }
   }
 }
+
+template <int BK>
+size_t gram_xt_smem(int tau) {
+  return (size_t)GxCfg<BK>::STAGES * ((tau + 39) / 40 * 40) * GxCfg<BK>::LDK * 8;
+}
+int gx_bk() {
+  static const int bk = [] {
+    const char* e = std::getenv("RS_GX_BK");
+    return e && atoi(e) == 16 ? 16 : 32;
+  }();
+  return bk;
+}
+
+// XT[j][i] = X[i][j] (32 x 32 tiles through shared memory)
+__global__ void k_transpose(const double* __restrict__ X, long long ldx, long long rows, long long d,
+                            double* __restrict__ XT, long long ldxt) {
+  __shared__ double t[32][33];
+  const long long i0 = (long long)blockIdx.y * 32, j0 = (long long)blockIdx.x * 32;
+  for (int y = threadIdx.y; y < 32; y += blockDim.y) {
+    const long long i = i0 + y, j = j0 + threadIdx.x;
+    t[y][threadIdx.x] = (i < rows && j < d) ? X[i * ldx + j] : 0.0;
+  }
+  __syncthreads();
+  for (int y = threadIdx.y; y < 32; y += blockDim.y) {
+    const long long j = j0 + y, i = i0 + threadIdx.x;
+    if (j < d && i < ldxt) XT[j * ldxt + i] = t[threadIdx.x][y];
+  }
+}
+
+// G[a][b] = sum_c partials[c][a][b] for b <= a (fixed order: 8 interleaved slices c = ty (mod 8)
+// summed in ascending c, then the slices in ascending ty).  Block: 32 consecutive entries of the
+// square GF_MAXTAU x GF_MAXTAU partial layout x 8 slices; entries above the diagonal are skipped.
+__global__ void __launch_bounds__(256)
+k_gram_reduce(const double* __restrict__ partials, int nparts, int tau, double* __restrict__ G,
+              long long ldg, const Ctrl* ctrl, int slot = 0) {
+  if (slot_unused(ctrl, slot)) return;
+  __shared__ double red[8][33];
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  const int q = blockIdx.x * 32 + tx, a = q / GF_MAXTAU, b = q % GF_MAXTAU;
+  const bool in = a < tau && b <= a;
+  double s = 0.0;
+  if (in) {
+#pragma unroll 4
+    for (int c = ty; c < nparts; c += 8) s += __ldcs(partials + (long long)c * GF_MAXTAU * GF_MAXTAU + q);
+  }
+  red[ty][tx] = s;
+  __syncthreads();
+  if (ty == 0 && in) {
+    double t = 0.0;
+#pragma unroll
+    for (int y = 0; y < 8; ++y) t += red[y][tx];
+    G[(long long)a * ldg + b] = t;
+  }
+}
+inline unsigned gram_reduce_grid(int tau) { return (unsigned)((tau * GF_MAXTAU + 31) / 32); }
 
 
 // ---------------------------------------------------------------------------------------------
@@ -800,6 +946,12 @@ cudaError_t gram_init() {
   if (e != cudaSuccess) return e;
   e = cudaFuncSetAttribute(k_xpass_rows, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
   if (e != cudaSuccess) return e;
+  e = cudaFuncSetAttribute(k_gram_xt<16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)gram_xt_smem<16>(GF_MAXTAU));
+  if (e != cudaSuccess) return e;
+  e = cudaFuncSetAttribute(k_gram_xt<32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)gram_xt_smem<32>(GF_MAXTAU));
+  if (e != cudaSuccess) return e;
   return cudaFuncSetAttribute(k_gram_fused, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               GF_STAGES * GF_BK * GF_LD * (int)sizeof(double));
 }
@@ -813,7 +965,32 @@ cudaError_t launch_gram_fused(const double* X, long long ldx, long long rows, co
   k_gram_fused<<<nc, GF_THREADS, smem, st>>>(X, ldx, rows, sk, rpc, partials, slot, ctrl);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
-  k_gram_reduce<<<sk.tau, 256, 0, st>>>(partials, nc, sk.tau, G, ldg, ctrl, slot);
+  k_gram_reduce<<<gram_reduce_grid(sk.tau), 256, 0, st>>>(partials, nc, sk.tau, G, ldg, ctrl, slot);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_transpose(const double* X, long long ldx, long long rows, long long d, double* XT,
+                             long long ldxt, cudaStream_t st) {
+  const dim3 grid((unsigned)((d + 31) / 32), (unsigned)((ldxt + 31) / 32));
+  k_transpose<<<grid, dim3(32, 8), 0, st>>>(X, ldx, rows, d, XT, ldxt);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_gram_xt(const double* XT, long long ldxt, long long rows, const DevSketch& sk,
+                           double* partials, double* G, long long ldg, int num_sms,
+                           const Ctrl* ctrl, cudaStream_t st, int slot) {
+  const int nc = num_sms;
+  const int bk = gx_bk();
+  const long long rpc = std::max<long long>(bk, ((rows + nc - 1) / nc + bk - 1) / bk * bk);
+  if (bk == 16)
+    k_gram_xt<16><<<nc, GF_THREADS, gram_xt_smem<16>(sk.tau), st>>>(XT, ldxt, rows, sk, rpc, partials,
+                                                                   slot, ctrl);
+  else
+    k_gram_xt<32><<<nc, GF_THREADS, gram_xt_smem<32>(sk.tau), st>>>(XT, ldxt, rows, sk, rpc, partials,
+                                                                   slot, ctrl);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  k_gram_reduce<<<gram_reduce_grid(sk.tau), 256, 0, st>>>(partials, nc, sk.tau, G, ldg, ctrl, slot);
   return cudaGetLastError();
 }
 
@@ -899,7 +1076,7 @@ cudaError_t launch_xpass_gram(const double* X, long long ldx, long long rows, lo
   if (e != cudaSuccess) return e;
   k_xpass_reduce<<<(unsigned)((d + 31) / 32), dim3(32, XR_Y), 0, st>>>(upart, nc, d, u, ctrl);
   if (skg.tau > 0)
-    k_gram_reduce<<<skg.tau, 256, 0, st>>>(gpart, pair ? npairs : nc, skg.tau, G, ldg, ctrl, gofs);
+    k_gram_reduce<<<gram_reduce_grid(skg.tau), 256, 0, st>>>(gpart, pair ? npairs : nc, skg.tau, G, ldg, ctrl, gofs);
   return cudaGetLastError();
 }
 }  // namespace rs

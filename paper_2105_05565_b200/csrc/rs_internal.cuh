@@ -226,6 +226,13 @@ cudaError_t launch_update(const double* ASt, long long ld_as, bool as_rowmajor, 
 
 // Gram mode (gram.cu): u = X^T (X v) in one pass over X (d <= 4096), partials reduced in order.
 size_t xpass_partials(long long d, int num_sms);
+// Transposed copy XT (d x ldxt) of the local rows of X, and the Gram (XS)^T XS of a subsample
+// sketch (tau <= 200) read from it as tau contiguous rows (partials: gram_fused_partials).
+cudaError_t launch_transpose(const double* X, long long ldx, long long rows, long long d, double* XT,
+                             long long ldxt, cudaStream_t st);
+cudaError_t launch_gram_xt(const double* XT, long long ldxt, long long rows, const DevSketch& sk,
+                           double* partials, double* G, long long ldg, int num_sms,
+                           const Ctrl* ctrl, cudaStream_t st, int slot = 0);
 // v = S delta (dense, m); when the sketch and delta are given and d <= 2048, the row-owner kernel
 // forms <X_i, v> from the sketch entries only.
 cudaError_t launch_xpass(const double* X, long long ldx, long long rows, long long d,
