@@ -51,6 +51,10 @@ class ClockSampler:
         self.proc = None
 
     def __enter__(self):
+        # the sampler's own start-up (NVML init) must not overlap the timed region: wait for its
+        # first sample before returning; lines are collected by a reader thread
+        import threading
+        self.lines = []
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
@@ -58,18 +62,31 @@ class ClockSampler:
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
         except Exception:
             self.proc = None
+            return self
+        first = threading.Event()
+
+        def reader():
+            for ln in self.proc.stdout:
+                if ln.strip():
+                    self.lines.append(ln)
+                    first.set()
+            first.set()
+
+        self.thread = threading.Thread(target=reader, daemon=True)
+        self.thread.start()
+        first.wait(timeout=5.0)
+        self.n_before = len(self.lines)
         return self
 
     def __exit__(self, *a):
-        self.lines = []
         if self.proc is not None:
             time.sleep(0.25)
             self.proc.terminate()
             try:
-                out, _ = self.proc.communicate(timeout=5)
-                self.lines = [ln for ln in out.splitlines() if ln.strip()]
+                self.proc.wait(timeout=5)
             except Exception:
                 self.proc.kill()
+            self.thread.join(timeout=5)
 
     def summary(self):
         sm, mx, reasons = [], None, set()

@@ -305,17 +305,23 @@ constexpr int AP_WPR = 4;                      // warps per row
 constexpr int AP_ROWS = AG_WARPS / AP_WPR;     // rows per block
 constexpr int AP_PRE = 8;                      // register-preloaded values per lane (1024 columns)
 
+constexpr int AP_MAXFUSE = 4096;               // sketch entries of a fused g = S^T r
+
+// x = g (MODE AP_FULL / AP_LOWER) or t (AP_UPPER).  gv == null: g = S^T r is formed here for the
+// buckets the block needs (few entries per bucket): the entries (static) are staged before
+// pdl_wait(), the residual is gathered after it.
 template <int MODE>
 __global__ void __launch_bounds__(AG_WARPS * 32)
 k_apply_rows(const double* __restrict__ Mx, long long ldm, DevSketch sk, const int* __restrict__ flag,
-             const double* __restrict__ x, double* __restrict__ out, double* __restrict__ sdelta,
-             Ctrl* ctrl) {
+             const double* __restrict__ x, const double* __restrict__ r, double* __restrict__ out,
+             double* __restrict__ sdelta, Ctrl* ctrl) {
   pdl_trigger();
-  if (ctrl->done) return;   // previous iteration's stop rule (static for this chain)
-  const int bad = *flag;    // factor slot not SPD (static)
-  __shared__ double xs[AG_MAXTAU];
+  extern __shared__ double xs[];     // [tau] x, then (fused g) s_bp[tau + 1], s_ce[len]
   __shared__ double red[AG_WARPS];
+  const int bad = *flag;    // factor slot not SPD (static)
   const int tau = sk.tau, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  int* s_bp = reinterpret_cast<int*>(xs + tau);
+  int* s_ce = s_bp + tau + 1;         // coord_e, bit-complemented for a negative sign
   const int q = warp % AP_WPR, a = blockIdx.x * AP_ROWS + warp / AP_WPR;
   const int c0 = MODE == AP_UPPER ? a : 0, c1 = MODE == AP_LOWER ? a + 1 : tau;
   const double* row = Mx + (long long)min(a, tau - 1) * ldm;
@@ -327,14 +333,36 @@ k_apply_rows(const double* __restrict__ Mx, long long ldm, DevSketch sk, const i
     const int c = cb + 32 * AP_WPR * u;
     v[u] = (!bad && a < tau && c < p1) ? __ldg(row + c) : 0.0;
   }
+  const int xlo = MODE == AP_UPPER ? min(tau, blockIdx.x * AP_ROWS) : 0;
+  const int xhi = MODE == AP_LOWER ? min(tau, (blockIdx.x + 1) * AP_ROWS) : tau;
+  const bool fuse = MODE != AP_UPPER && x == nullptr;
+  int e_lo = 0;
+  if (fuse) {   // static sketch entries of buckets [xlo, xhi)
+    e_lo = sk.bptr[xlo];
+    const int e_hi = sk.bptr[xhi];
+    for (int b = xlo + tid; b <= xhi; b += AG_WARPS * 32) s_bp[b - xlo] = sk.bptr[b] - e_lo;
+    for (int e = e_lo + tid; e < e_hi; e += AG_WARPS * 32)
+      s_ce[e - e_lo] = sk.sign[e] > 0 ? sk.coord[e] : ~sk.coord[e];
+  }
   pdl_wait();
+  if (ctrl->done) return;   // the previous iteration's stop rule (written by the predecessor)
   if (bad) {   // the update kernel of this iteration turns the status into `done`
     if (MODE != AP_UPPER && blockIdx.x == 0 && tid == 0) ctrl->status = ST_NOTSPD;
     return;
   }
-  const int xlo = MODE == AP_UPPER ? min(tau, blockIdx.x * AP_ROWS) : 0;
-  const int xhi = MODE == AP_LOWER ? min(tau, (blockIdx.x + 1) * AP_ROWS) : tau;
-  for (int c = xlo + tid; c < xhi; c += AG_WARPS * 32) xs[c] = x[c];
+  if (fuse) {
+    __syncthreads();
+    for (int b = xlo + tid; b < xhi; b += AG_WARPS * 32) {
+      double g = 0.0;
+      for (int e = s_bp[b - xlo]; e < s_bp[b - xlo + 1]; ++e) {
+        const int ce = s_ce[e];
+        g += ce >= 0 ? __ldcg(r + ce) : -__ldcg(r + ~ce);
+      }
+      xs[b] = g;
+    }
+  } else {
+    for (int c = xlo + tid; c < xhi; c += AG_WARPS * 32) xs[c] = x[c];
+  }
   __syncthreads();
   double s0 = 0.0, s1 = 0.0;
 #pragma unroll
@@ -601,6 +629,16 @@ size_t bfactor_work_elems(int tau) {
 }
 
 cudaError_t bfactor_init() {
+  const int ap_smem = AG_MAXTAU * 8 + (AG_MAXTAU + 1 + AP_MAXFUSE) * 4;
+  cudaError_t e = cudaFuncSetAttribute(k_apply_rows<AP_FULL>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, ap_smem);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(k_apply_rows<AP_LOWER>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             ap_smem);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(k_apply_rows<AP_UPPER>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             ap_smem);
+  if (e != cudaSuccess) return e;
   return cudaFuncSetAttribute(k_bfactor_small, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               (int)bf_smem(BF_MAXTAU));
 }
@@ -622,25 +660,37 @@ cudaError_t launch_bfactor(const FactorSrc& src, const DevSketch& skb, int nslot
 
 cudaError_t launch_apply_ginv(const double* Ginv, long long ldgi, const DevSketch& sk,
                               const int* flag, const double* r, double* gbuf, double* delta,
-                              double* sdelta, Ctrl* ctrl, cudaStream_t st) {
+                              double* sdelta, Ctrl* ctrl, cudaStream_t st, bool first) {
   if (sk.tau > AG_MAXTAU) return cudaErrorInvalidValue;
-  k_sketch_g<<<(unsigned)((sk.tau + AG_WARPS - 1) / AG_WARPS), AG_WARPS * 32, 0, st>>>(sk, flag, r,
-                                                                                      gbuf, ctrl);
-  {
+  // few entries per bucket (subsample, SubCount): g = S^T r is formed inside the first GEMV kernel
+  const bool fuse = sk.len <= 8 * sk.tau && sk.len <= AP_MAXFUSE;
+  const double* gv = nullptr;
+  if (!fuse) {
+    k_sketch_g<<<(unsigned)((sk.tau + AG_WARPS - 1) / AG_WARPS), AG_WARPS * 32, 0, st>>>(
+        sk, flag, r, gbuf, ctrl);
     const cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
+    gv = gbuf;
+    first = false;   // k_sketch_g is the ordinary launch of the chain
   }
-  const dim3 grid((unsigned)((sk.tau + AP_ROWS - 1) / AP_ROWS)), blk(AG_WARPS * 32);
+  // the first kernel of a group follows the factorisation that wrote the slot: ordinary launch
+  auto launch = [&](auto kern, const double* xin, double* out) {
+    const dim3 grid((unsigned)((sk.tau + AP_ROWS - 1) / AP_ROWS)), blk(AG_WARPS * 32);
+    const size_t smem = (size_t)sk.tau * 8 + (xin ? 0 : (size_t)(sk.tau + 1 + sk.len) * 4);
+    if (first) {
+      kern<<<grid, blk, smem, st>>>(Ginv, ldgi, sk, flag, xin, r, out, sdelta, ctrl);
+      return cudaGetLastError();
+    }
+    return launch_pdl(kern, grid, blk, smem, st, Ginv, ldgi, sk, flag, xin, r, out, sdelta, ctrl);
+  };
   if (sk.tau > BF_MAXTAU) {   // slot holds W = L^{-1} (lower) and W^T (upper): delta = W^T (W g)
     double* tv = gbuf + sk.tau;
-    const cudaError_t e = launch_pdl(k_apply_rows<AP_LOWER>, grid, blk, 0, st, Ginv, ldgi, sk, flag,
-                                     (const double*)gbuf, tv, sdelta, ctrl);
+    const cudaError_t e = launch(k_apply_rows<AP_LOWER>, gv, tv);
     if (e != cudaSuccess) return e;
-    return launch_pdl(k_apply_rows<AP_UPPER>, grid, blk, 0, st, Ginv, ldgi, sk, flag,
-                      (const double*)tv, delta, sdelta, ctrl);
+    first = false;
+    return launch(k_apply_rows<AP_UPPER>, (const double*)tv, delta);
   }
-  return launch_pdl(k_apply_rows<AP_FULL>, grid, blk, 0, st, Ginv, ldgi, sk, flag,
-                    (const double*)gbuf, delta, sdelta, ctrl);
+  return launch(k_apply_rows<AP_FULL>, gv, delta);
 }
 
 bool pdl_enabled() {

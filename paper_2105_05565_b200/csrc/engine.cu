@@ -475,6 +475,12 @@ rs_status Problem::ensure_workspace(int kind, int tau, int ksum, int depth, bool
     RS_TRY(dalloc(&skb.bucket, L * depth));
     RS_TRY(dalloc(&skb.bptr, (size_t)(tau + 1) * depth));
     if (kind == SK_COUNT) RS_TRY(dalloc(&skb.cmap, (size_t)m * depth));
+    // slots the device skips (beyond max_iter) are never written, but the PDL-chained kernels read
+    // a slot's sketch before they learn that the solve has stopped: keep every slot well-formed
+    RS_CUDA(cudaMemsetAsync(skb.coord, 0, L * depth * sizeof(int), st));
+    RS_CUDA(cudaMemsetAsync(skb.sign, 0, L * depth, st));
+    RS_CUDA(cudaMemsetAsync(skb.bucket, 0, L * depth * sizeof(int), st));
+    RS_CUDA(cudaMemsetAsync(skb.bptr, 0, (size_t)(tau + 1) * depth * sizeof(int), st));
     if (mode == RS_AS_EXPLICIT) {   // count: A S^T rows per slot; subsample / SubCount read A directly
       if (kind == SK_COUNT) RS_TRY(dalloc(&ASt_slots, (size_t)as_stride * depth));
     } else {
@@ -643,8 +649,9 @@ rs_status Problem::enqueue_pipelined_iteration(const rs_solve_opts* o, int slot,
   };
   const DevSketch sq = skb.at(slot);
   mark(RS_K_SOLVE, 0);
+  // slot 0 follows the group's factorisation (ordinary launch); later slots chain by PDL
   RS_CUDA(launch_apply_ginv(Ginv_slots + (long long)slot * gi_stride, ld_gi, sq, slot_flags + slot,
-                            r, sw.Gx, sw.delta, sdelta, ctrl, st));               // a4 + a5
+                            r, sw.Gx, sw.delta, sdelta, ctrl, st, slot == 0));    // a4 + a5
   mark(RS_K_SOLVE, 1);
   if (mode == RS_AS_EXPLICIT) {
     mark(RS_K_UPDATE, 0);

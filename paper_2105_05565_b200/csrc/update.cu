@@ -10,6 +10,7 @@
 // in a fixed order), and the last block applies the stop rule ||r^k|| <= tol ||r^0|| (P:L248-251,
 // DESIGN.md R1), the divergence guard and the iteration counter.
 #include <algorithm>
+#include <cooperative_groups.h>
 
 #include "rs_internal.cuh"
 
@@ -233,102 +234,127 @@ k_update_vec(const double* __restrict__ u, double lambda, double* __restrict__ s
 // sd_e = sign_e delta[bucket_e] (A symmetric: row coord_e = column coord_e).  Launched as the last
 // kernel of the iteration's PDL chain (bfactor.cu): the first RW_PRE rows of each warp (A and the
 // sketch are static) are loaded into registers BEFORE pdl_wait(), overlapping the solve kernels.
+// The gridDim.y row splits of a column block form one thread-block cluster: their partial sums
+// are added in rank order through distributed shared memory by the rank-0 block, which applies
+// the momentum update to its 64 coordinates and contributes ||r||^2 (the last column block to
+// arrive finishes the iteration).
 constexpr int RW_Y = 8;
-constexpr int RW_PRE = 8;
+constexpr int RW_PRE = 8;     // rows per warp loaded before pdl_wait()
+constexpr int RW_B = 16;      // rows per warp per later batch (loads first)
 constexpr int RW_COLS = 64;
-constexpr int RW_MAXS = 16;
-// u = A S delta over the rows e of slot `sk`, split over gridDim.y row ranges: block (cb, sp) sums
-// rows e in its range for columns 64 cb .. 64 cb + 63 into upart[sp][j]; the last split of a column
-// block (counter cnt[cb]) adds the splits in order (deterministic), applies the momentum update to
-// its 64 coordinates and contributes ||r||^2; the last column block finishes the iteration.
+constexpr int RW_MAXS = 8;    // portable cluster size
+template <bool CLUSTER>
 __global__ void __launch_bounds__(32 * RW_Y)
 k_update_rows(const double* __restrict__ A, long long lda, DevSketch sk,
               const double* __restrict__ delta, double* __restrict__ sdelta,
               double* __restrict__ w, double* __restrict__ dw, double* __restrict__ r,
               double* __restrict__ dr, long long m, double gamma, double beta,
-              double* __restrict__ partials, double* __restrict__ upart, int* __restrict__ cnt,
-              Ctrl* ctrl) {
+              double* __restrict__ partials, Ctrl* ctrl) {
   pdl_trigger();
-  if (ctrl->done) return;   // previous iteration's stop rule (static for this chain)
+  namespace cg = cooperative_groups;
+  extern __shared__ double rw_sd[];   // [per] sd_e, then [per] coord_e
   __shared__ double red[RW_Y][2][33];
-  __shared__ bool s_last;
+  __shared__ double part[2][32];
+  __shared__ int s_flag;
   const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * 32 + tx;
   const int len = sk.len;   // = bptr[tau] for subsample / SubCount / count
   const int ns = gridDim.y, sp = blockIdx.y;
   const int per = (len + ns - 1) / ns;
   const int e0 = min(len, sp * per), e1 = min(len, e0 + per), span = e1 - e0;
+  int* s_co = reinterpret_cast<int*>(rw_sd + per);
+  // static: the block's sketch coordinates, then the first RW_PRE rows of each warp
+  for (int e = tid; e < span; e += 32 * RW_Y) s_co[e] = sk.coord[e0 + e];
+  __syncthreads();
   // lane tx owns columns j0, j0 + 1 (lda is a multiple of 4 doubles, so the pair is 16-B aligned and
   // inside the row's padding when j0 + 1 == m)
   const long long j0 = (long long)blockIdx.x * RW_COLS + 2 * tx;
   const bool jin = j0 < m;
   double2 v[RW_PRE];
-  int sb[RW_PRE];   // bucket, bit-complemented for a negative sign
 #pragma unroll
   for (int u = 0; u < RW_PRE; ++u) {
     const int e = ty + RW_Y * u;
-    v[u] = make_double2(0.0, 0.0);
-    sb[u] = 0;
-    if (e < span) {
-      const int c = sk.coord[e0 + e];
-      sb[u] = sk.sign[e0 + e] > 0 ? sk.bucket[e0 + e] : ~sk.bucket[e0 + e];
-      if (jin) v[u] = __ldg(reinterpret_cast<const double2*>(A + (long long)c * lda + j0));
-    }
+    v[u] = (jin && e < span)
+               ? __ldg(reinterpret_cast<const double2*>(A + (long long)s_co[e] * lda + j0))
+               : make_double2(0.0, 0.0);
   }
   pdl_wait();
+  // block-uniform exits only: every block of a cluster reaches both cluster barriers or none does
+  if (ctrl->done) return;
   if (ctrl->status >= ST_NOTSPD) {   // set by the solve kernels of this iteration
     if (blockIdx.x == 0 && blockIdx.y == 0 && tid == 0) ctrl->done = 1;
     return;
   }
   mom_at(ctrl, gamma, beta);   // schedule (gamma_k, beta_k), rs_momentum
+  for (int e = tid; e < span; e += 32 * RW_Y) {
+    const double dv = delta[sk.bucket[e0 + e]];
+    rw_sd[e] = sk.sign[e0 + e] > 0 ? dv : -dv;
+  }
+  __syncthreads();
   double a0 = 0.0, a1 = 0.0;
 #pragma unroll
   for (int u = 0; u < RW_PRE; ++u) {
-    if (ty + RW_Y * u < span) {
-      const double dv = delta[sb[u] >= 0 ? sb[u] : ~sb[u]];
-      const double sd = sb[u] >= 0 ? dv : -dv;
-      a0 += sd * v[u].x;
-      a1 += sd * v[u].y;
+    const int e = ty + RW_Y * u;
+    if (e < span) {
+      a0 += rw_sd[e] * v[u].x;
+      a1 += rw_sd[e] * v[u].y;
     }
   }
-  for (int e = ty + RW_Y * RW_PRE; e < span; e += RW_Y) {
-    const int c = sk.coord[e0 + e];
-    const double dv = delta[sk.bucket[e0 + e]];
-    const double sd = sk.sign[e0 + e] > 0 ? dv : -dv;
-    if (jin) {
-      const double2 x = __ldg(reinterpret_cast<const double2*>(A + (long long)c * lda + j0));
-      a0 += sd * x.x;
-      a1 += sd * x.y;
+  for (int eb = ty + RW_Y * RW_PRE; eb < span; eb += RW_Y * RW_B) {
+    double2 x[RW_B];
+#pragma unroll
+    for (int u = 0; u < RW_B; ++u) {
+      const int e = eb + RW_Y * u;
+      x[u] = (jin && e < span)
+                 ? __ldg(reinterpret_cast<const double2*>(A + (long long)s_co[e] * lda + j0))
+                 : make_double2(0.0, 0.0);
+    }
+#pragma unroll
+    for (int u = 0; u < RW_B; ++u) {
+      const int e = eb + RW_Y * u;
+      if (e < span) {
+        a0 += rw_sd[e] * x[u].x;
+        a1 += rw_sd[e] * x[u].y;
+      }
     }
   }
   red[ty][0][tx] = a0;
   red[ty][1][tx] = a1;
   __syncthreads();
+  double u0 = 0.0, u1 = 0.0;
   if (ty == 0) {
-    double u0 = 0.0, u1 = 0.0;
 #pragma unroll
     for (int q = 0; q < RW_Y; ++q) {
       u0 += red[q][0][tx];
       u1 += red[q][1][tx];
     }
-    if (j0 < m) upart[(long long)sp * m + j0] = u0;
-    if (j0 + 1 < m) upart[(long long)sp * m + j0 + 1] = u1;
-    __threadfence();
-    __syncwarp();
-    if (tx == 0) s_last = atomicAdd(&cnt[blockIdx.x], 1) == ns - 1;
-    __syncwarp();
   }
-  __syncthreads();
-  if (!s_last) return;
-  // last split of this column block: u_j = sum of the splits in order, then the update
+  bool leader = true;
+  if constexpr (CLUSTER) {   // add the splits of the column block in rank order through DSMEM
+    cg::cluster_group cl = cg::this_cluster();
+    if (ty == 0) {
+      part[0][tx] = u0;
+      part[1][tx] = u1;
+    }
+    cl.sync();
+    leader = cl.block_rank() == 0;
+    if (leader && ty == 0) {
+      u0 = u1 = 0.0;
+      for (int q = 0; q < ns; ++q) {   // rank order = split order (the cluster spans gridDim.y)
+        const double* pq = cl.map_shared_rank(&part[0][0], q);
+        u0 += pq[tx];
+        u1 += pq[32 + tx];
+      }
+    }
+    cl.sync();   // the other splits' shared memory stays alive until rank 0 has read it
+  }
+  if (!leader) return;
   if (ty == 0) {
-    __threadfence();
     double r2 = 0.0;
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       const long long j = j0 + h;
       if (j < m) {
-        double u = 0.0;
-        for (int q = 0; q < ns; ++q) u += __ldcg(&upart[(long long)q * m + j]);
+        const double u = h ? u1 : u0;
         const double drj = beta * dr[j] - gamma * u;
         const double rj = r[j] + drj;
         dr[j] = drj;
@@ -344,15 +370,14 @@ k_update_rows(const double* __restrict__ A, long long lda, DevSketch sk,
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) r2 += __shfl_down_sync(0xffffffffu, r2, o);
     if (tx == 0) {
-      cnt[blockIdx.x] = 0;
       partials[blockIdx.x] = r2;
       __threadfence();
       const unsigned prev = atomicAdd(&ctrl->arrive, 1u);
-      s_last = (prev == gridDim.x - 1);
+      s_flag = (prev == gridDim.x - 1);
     }
   }
   __syncthreads();
-  if (!s_last) return;
+  if (!s_flag) return;
   __threadfence();
   double s2 = 0.0;
   for (unsigned q = tid; q < gridDim.x; q += 32 * RW_Y) s2 += __ldcg(&partials[q]);
@@ -369,7 +394,11 @@ k_update_rows(const double* __restrict__ A, long long lda, DevSketch sk,
 }  // namespace
 
 cudaError_t update_init() {
-  return cudaSuccess;
+  cudaError_t e = cudaFuncSetAttribute(k_update_rows<true>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  if (e != cudaSuccess) return e;
+  return cudaFuncSetAttribute(k_update_rows<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              200 * 1024);
 }
 
 size_t update_rows_scratch(long long m) { return (size_t)RW_MAXS * (size_t)m; }
@@ -380,13 +409,42 @@ cudaError_t launch_update_rows(const double* A, long long lda, const DevSketch& 
                                double* r, double* dr, long long m, double gamma, double beta,
                                double* partials, double* upart, int* cnt, int num_sms, Ctrl* ctrl,
                                cudaStream_t st) {
+  (void)upart;
+  (void)cnt;
   const long long cb = (m + RW_COLS - 1) / RW_COLS;
-  // splits: every warp's rows fit its register preload when possible, and >= 2 blocks per SM
-  long long ns = (sk.len + RW_Y * RW_PRE - 1) / (RW_Y * RW_PRE);
-  ns = std::max(ns, (2LL * num_sms + cb - 1) / cb);
-  ns = std::max(1LL, std::min<long long>({ns, (long long)RW_MAXS, (long long)sk.len / RW_Y}));
-  return launch_pdl(k_update_rows, dim3((unsigned)cb, (unsigned)ns), dim3(32, RW_Y), 0, st, A, lda,
-                    sk, delta, sdelta, w, dw, r, dr, m, gamma, beta, partials, upart, cnt, ctrl);
+  // splits (one cluster per column block): about two blocks per SM in total (128 registers per
+  // thread), at least 4 rows per warp, at most the portable cluster size
+  long long ns = (4LL * num_sms + cb / 2) / cb;   // about four blocks per SM in total
+  ns = std::min<long long>(ns, (sk.len + 4 * RW_Y - 1) / (4 * RW_Y));   // >= 4 rows per warp
+  ns = std::max(1LL, std::min<long long>(ns, RW_MAXS));
+  const int per = (int)((sk.len + ns - 1) / ns);
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3((unsigned)cb, (unsigned)ns);
+  cfg.blockDim = dim3(32, RW_Y);
+  cfg.dynamicSmemBytes = (size_t)per * 12;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[2];
+  int na = 0;
+  if (pdl_enabled()) {
+    attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[na].val.programmaticStreamSerializationAllowed = 1;
+    ++na;
+  }
+  if (ns > 1) {
+    attr[na].id = cudaLaunchAttributeClusterDimension;
+    attr[na].val.clusterDim.x = 1;
+    attr[na].val.clusterDim.y = (unsigned)ns;
+    attr[na].val.clusterDim.z = 1;
+    ++na;
+  }
+  cfg.attrs = attr;
+  cfg.numAttrs = na;
+  if (cfg.dynamicSmemBytes > 200 * 1024) return cudaErrorInvalidValue;
+  if (ns > 1)
+    return cudaLaunchKernelEx(&cfg, k_update_rows<true>, A, lda, sk, delta, sdelta, w, dw, r, dr, m,
+                              gamma, beta, partials, ctrl);
+  return cudaLaunchKernelEx(&cfg, k_update_rows<false>, A, lda, sk, delta, sdelta, w, dw, r, dr, m,
+                            gamma, beta, partials, ctrl);
 }
 
 cudaError_t launch_update_vec(const double* u, double lambda, double* sdelta, double* w, double* dw,

@@ -1,0 +1,8 @@
+# explicit bench lines (c2, c5, k1, c4) + explicit GPU tests
+set -x
+python -c "import __graft_entry__ as g; g.build()" || exit 1
+timeout 900 python -m pytest tests -m gpu -q -x -k "explicit or kernel or config5 or config2 or momentum or dirty" 2>&1 | grep -E "^E  .*Error|passed|failed|FAILED" | head | tee gpurun_out/pytest_gpu.log
+timeout 600 python bench.py --mode explicit --no-cpu-baseline --no-e2e > gpurun_out/bench_c2_explicit.json 2>/dev/null
+timeout 1200 python bench.py --config c5 --mode explicit --steps 148 --max-iter-tol 2000 --no-cpu-baseline --no-e2e > gpurun_out/bench_c5_explicit.json 2>/dev/null
+timeout 1200 python bench.py --config k1 --steps 148 --max-iter-tol 2000 --no-cpu-baseline --no-e2e > gpurun_out/bench_k1.json 2>/dev/null
+timeout 900 python bench.py --config c4 --mode explicit --steps 148 --max-iter-tol 20000 --no-cpu-baseline --no-e2e > gpurun_out/bench_c4_explicit.json 2>/dev/null
