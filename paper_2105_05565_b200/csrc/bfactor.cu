@@ -21,6 +21,7 @@
 // block row (block (I, J), J <= I, at index I(I+1)/2 + J), each block row-major with an XOR swizzle
 // (column c of row r at c ^ 4((r >> 1) & 1)) so DMMA fragment loads -- plain and transposed -- are
 // bank-conflict free; then a panel temp of Tc blocks.
+#include <algorithm>
 #include <cstdlib>
 
 #include "rs_internal.cuh"
@@ -397,7 +398,8 @@ constexpr int BB_THREADS = 512;
 constexpr int BB_WARPS = BB_THREADS / 32;
 constexpr int BB_MAXTAU = 4096;
 
-__host__ __device__ __forceinline__ int bb_tp(int tau) { return (tau + 31) / 32 * 32; }
+// padded size: a whole number of 64-wide tile pairs (identity padding)
+__host__ __device__ __forceinline__ int bb_tp(int tau) { return (tau + 63) / 64 * 64; }
 
 // acc[R][C] (8 x 8 blocks of a 32 x 32 tile) += op(A) op(B) (op(A) scaled by `sign`), with
 // op(A)[r][k] = TA ? A[k][r] : A[r][k] and op(B)[k][c] = TB ? B[c][k] : B[k][c]; A has leading
@@ -618,6 +620,346 @@ k_bfactor_big(FactorSrc src, DevSketch skb, double* __restrict__ Ginv, long long
   if (tid == 0) flags[slot] = 0;
 }
 
+// -------------------------------------------------------------------------------------------------
+// Left-looking variant (default for tau > 224): block columns are processed in PAIRS (64 wide), and
+// the operand every strip of a step shares -- rows p0, p0+1 of L (Cholesky) or block columns J0, J1
+// of L (inverse) -- is staged in shared memory in chunks of LP_KC tile pairs (cp.async, double
+// buffered).  Each warp accumulates a 32 x 64 strip in registers (acc[4][8][2]) from its own row
+// tiles read once per PAIR of block columns, so global traffic is about Tc^3/12 tiles per phase
+// (the right-looking kernel above re-reads and rewrites the trailing matrix every 32 columns).
+//   Cholesky, pair p0 = 2P:  [C_i,p0 C_i,p0+1] = [G_i,p0 G_i,p0+1] - sum_{k<p0} L_ik [L_p0,k L_p0+1,k]^T
+//     diagonal pair (warp 0): L00 = chol(C00), L10 = C10 L00^-T, L11 = chol(C11 - L10 L10^T)
+//     strips i > p0+1: L_i,p0 = C_i,p0 L00^-T, L_i,p0+1 = (C_i,p0+1 - L_i,p0 L10^T) L11^-T
+//   Inverse W = L^-1, pair (J0, J1 = J0+1) from the last: strips I > J1 (highest first, so that a
+//   round never stages a row an earlier round has overwritten):
+//     [T_I,J0 T_I,J1] = sum_{K=J1+1..I} W_IK [L_K,J0 L_K,J1]
+//     W_I,J1 = -T_I,J1 W_J1J1,  W_I,J0 = -(T_I,J0 + W_I,J1 L_J1,J0) W_J0J0
+//     diagonal pair: W_J1,J0 = -W_J1J1 L_J1,J0 W_J0J0
+constexpr int LP_WARPS = 8;                     // 255 registers: acc[4][8][2] per lane
+constexpr int LP_THREADS = LP_WARPS * 32;
+constexpr int LP_KC = 4;                        // k tiles per staged chunk
+constexpr int LP_LD = 36;                       // staged tile row stride (conflict-free fragments)
+constexpr int LP_TILE = 32 * LP_LD;
+constexpr int LP_CHUNK = 2 * LP_KC * LP_TILE;   // doubles per chunk buffer
+constexpr size_t LP_SMEM = 2 * LP_CHUNK * sizeof(double);
+
+__device__ __forceinline__ void lp_cp16(double* smem, const double* gmem) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem));
+}
+
+__global__ void __launch_bounds__(LP_THREADS, 1)
+k_bfactor_lp(FactorSrc src, DevSketch skb, double* __restrict__ Ginv, long long ldgi,
+             long long gi_stride, double* work, long long work_stride, int* __restrict__ flags,
+             const Ctrl* ctrl) {
+  if (slot_unused(ctrl, blockIdx.x)) return;
+  extern __shared__ __align__(16) double lp_sm[];   // 2 chunk buffers (the a4 gather: sketch)
+  __shared__ double sL[32][33];
+  __shared__ int s_bad;
+  const int slot = blockIdx.x;
+  const DevSketch sk = skb.at(slot);
+  const int tau = sk.tau, tp = bb_tp(tau), Tc = tp / 32;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int q = lane >> 2, k4 = lane & 3;
+  double* Wm = work + slot * work_stride;           // tp x tp, row-major
+  double* dinv = Wm + (long long)tp * tp;           // Tc tiles 32 x 32 (L_pp^{-1})
+  double* scr = dinv + (long long)Tc * 1024;        // 2 tiles per warp
+  auto T = [&](int I, int J) { return Wm + (long long)(32 * I) * tp + 32 * J; };
+  if (tid == 0) s_bad = 0;
+
+  // ---- a4: lower triangle of G (R3 empty-bucket rule), identity on the padding.  From explicit A
+  // with the slot's sketch staged in the (not yet used) chunk buffers: coord_e (sign folded in as
+  // bit complement) and bptr, so each element costs one independent gather of A.
+  const double* ASt = src.ASt ? src.ASt + slot * src.as_stride : nullptr;
+  const double* Gram = src.Gram ? src.Gram + slot * src.gram_stride : nullptr;
+  int* s_bp = reinterpret_cast<int*>(lp_sm);
+  int* s_ce = s_bp + tau + 1;
+  const bool staged = !Gram && !ASt && (size_t)(tau + 1 + sk.len) * 4 <= LP_SMEM;
+  if (staged) {
+    for (int b = tid; b <= tau; b += LP_THREADS) s_bp[b] = sk.bptr[b];
+    for (int e = tid; e < sk.len; e += LP_THREADS) s_ce[e] = sk.sign[e] > 0 ? sk.coord[e] : ~sk.coord[e];
+    __syncthreads();
+  }
+  for (int a = warp; a < tp; a += LP_WARPS) {
+    const int a32 = a & ~31;
+    const int e0 = a < tau ? (staged ? s_bp[a] : sk.bptr[a]) : 0;
+    const int e1 = a < tau ? (staged ? s_bp[a + 1] : sk.bptr[a + 1]) : 0;
+    if (staged && a < tau && e1 - e0 == 1) {   // subsample row: one entry
+      const int ca = s_ce[e0];
+      const double* Ae = src.A + (long long)(ca >= 0 ? ca : ~ca) * src.lda;
+      const double sa = ca >= 0 ? 1.0 : -1.0;
+      double* dst = Wm + (long long)a * tp;
+      const bool single = sk.len == tau;   // subsample: exactly one entry per bucket
+      const int n = a + 1;                 // columns c <= a (< tau)
+      if (single) {   // batches of 8 independent gathers per lane
+        for (int c0 = lane; c0 < n; c0 += 8 * 32) {
+          double x[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const int c = c0 + 32 * u;
+            const int cf = c < n ? s_ce[c] : 0;
+            x[u] = c < n ? __ldg(Ae + (cf >= 0 ? cf : ~cf)) : 0.0;
+            if (cf < 0) x[u] = -x[u];
+          }
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const int c = c0 + 32 * u;
+            if (c < n) dst[c] = sa * x[u];
+          }
+        }
+      } else {
+        for (int c = lane; c < n; c += 32) {
+          const int f0 = s_bp[c], f1 = s_bp[c + 1];
+          double v = 0.0;
+          for (int f = f0; f < f1; ++f) {
+            const int cf = s_ce[f];
+            const double x = __ldg(Ae + (cf >= 0 ? cf : ~cf));
+            v += cf >= 0 ? x : -x;
+          }
+          v *= sa;
+          if (f0 == f1) v = 0.0;   // empty bucket c != a (R3)
+          dst[c] = v;
+        }
+      }
+      for (int c = n + lane; c < a32 + 32; c += 32) dst[c] = 0.0;   // above the diagonal
+      continue;
+    }
+    for (int c = lane; c < a32 + 32; c += 32) {   // every lower tile of row a
+      double v = 0.0;
+      if (a >= tau || c >= tau || c > a) {
+        v = (a == c) ? 1.0 : 0.0;
+      } else if (Gram) {
+        v = Gram[(long long)a * src.ld_gram + c];
+        if (a == c) v += src.lambda * (double)(e1 - e0);
+      } else if (!ASt) {
+        const int f0 = staged ? s_bp[c] : sk.bptr[c], f1 = staged ? s_bp[c + 1] : sk.bptr[c + 1];
+        for (int e = e0; e < e1; ++e) {
+          const double* Ae = src.A + (long long)sk.coord[e] * src.lda;
+          double t = 0.0;
+          for (int f = f0; f < f1; ++f) {
+            const double x = Ae[sk.coord[f]];
+            t += sk.sign[f] > 0 ? x : -x;
+          }
+          v += sk.sign[e] > 0 ? t : -t;
+        }
+        if (e0 == e1 || f0 == f1) v = (a == c) ? 1.0 : 0.0;
+      } else {
+        const double* col = ASt + (long long)c * src.ld_as;
+        for (int e = e0; e < e1; ++e) {
+          const double x = col[sk.coord[e]];
+          v += sk.sign[e] > 0 ? x : -x;
+        }
+      }
+      if (a < tau && c < tau && c <= a && (Gram || ASt) && (e0 == e1 || sk.bptr[c] == sk.bptr[c + 1]))
+        v = (a == c) ? 1.0 : 0.0;
+      Wm[(long long)a * tp + c] = v;
+    }
+  }
+  __syncthreads();
+
+  // chunk staging: tiles (h, kk), h = 0, 1, kk < LP_KC; Cholesky: T(p0 + h, k), inverse: T(k, p0 + h)
+  auto stage = [&](int buf, bool chol, int p0, int k0, int kend) {
+    double* dst = lp_sm + buf * LP_CHUNK;
+    for (int t = tid; t < 2 * LP_KC * 32 * 16; t += LP_THREADS) {   // 16-byte pieces
+      const int tile = t >> 9, rr = (t >> 4) & 31, c16 = t & 15;
+      const int h = tile / LP_KC, kk = tile % LP_KC, k = k0 + kk;
+      if (k >= kend) continue;
+      const double* srcp = chol ? T(p0 + h, k) : T(k, p0 + h);
+      lp_cp16(dst + tile * LP_TILE + rr * LP_LD + 2 * c16, srcp + (long long)rr * tp + 2 * c16);
+    }
+    asm volatile("cp.async.commit_group;\n");
+  };
+  // strip accumulation over staged chunks [kb, ke); strip row i uses k <= klim only
+  double acc[4][8][2];
+  auto accumulate = [&](bool chol, int p0, int kb, int ke, int i, int klim) {
+#pragma unroll
+    for (int R = 0; R < 4; ++R)
+#pragma unroll
+      for (int C = 0; C < 8; ++C) acc[R][C][0] = acc[R][C][1] = 0.0;
+    const int nch = (ke - kb + LP_KC - 1) / LP_KC;
+    if (nch > 0) stage(0, chol, p0, kb, ke);
+    for (int c = 0; c < nch; ++c) {
+      if (c + 1 < nch) stage((c + 1) & 1, chol, p0, kb + (c + 1) * LP_KC, ke);
+      else asm volatile("cp.async.commit_group;\n");
+      asm volatile("cp.async.wait_group 1;\n");
+      __syncthreads();
+      const double* ys = lp_sm + (c & 1) * LP_CHUNK;
+      if (i >= 0) {
+        for (int kk = 0; kk < LP_KC; ++kk) {
+          const int k = kb + c * LP_KC + kk;
+          if (k >= ke || k > klim) break;
+          const double* X = T(i, k);
+          if (k + 1 < ke && k + 1 <= klim) {   // next tile of the strip row into L1 (2 lines per row)
+            const double* nx = X + 32 + (long long)lane * tp;
+            asm volatile("prefetch.global.L1 [%0];\n" ::"l"(nx));
+            asm volatile("prefetch.global.L1 [%0];\n" ::"l"(nx + 16));
+          }
+          const double* y0 = ys + kk * LP_TILE;
+          const double* y1 = ys + (LP_KC + kk) * LP_TILE;
+#pragma unroll 2
+          for (int K = 0; K < 8; ++K) {
+            double a[4];
+#pragma unroll
+            for (int R = 0; R < 4; ++R) a[R] = X[(long long)(8 * R + q) * tp + 4 * K + k4];
+#pragma unroll
+            for (int C = 0; C < 8; ++C) {
+              const double* y = C < 4 ? y0 : y1;
+              const int n = 8 * (C & 3) + q, kq = 4 * K + k4;
+              const double b = chol ? y[n * LP_LD + kq] : y[kq * LP_LD + n];
+#pragma unroll
+              for (int R = 0; R < 4; ++R) dmma(acc[R][C], a[R], b);
+            }
+          }
+        }
+      }
+      __syncthreads();
+    }
+  };
+  // store half h of the strip accumulator (8 x 8 blocks C = 4h .. 4h+3) to a 32 x 32 tile,
+  // optionally as base - acc
+  auto store_half = [&](int h, double* Ct, int ld, const double* base, int ldb) {
+#pragma unroll
+    for (int R = 0; R < 4; ++R)
+#pragma unroll
+      for (int C = 0; C < 4; ++C) {
+        const int r = 8 * R + q, c = 8 * C + 2 * k4;
+        double v0 = acc[R][4 * h + C][0], v1 = acc[R][4 * h + C][1];
+        if (base) {
+          v0 = base[(long long)r * ldb + c] - v0;
+          v1 = base[(long long)r * ldb + c + 1] - v1;
+        }
+        Ct[(long long)r * ld + c] = v0;
+        Ct[(long long)r * ld + c + 1] = v1;
+      }
+  };
+  double t32[4][4][2];   // 32 x 32 tile products (mma_tile)
+
+  // ---- a5: Cholesky G = L L^T, block-column pairs
+  for (int p0 = 0; p0 < Tc; p0 += 2) {
+    const int nstrip = Tc - p0, rounds = (nstrip + LP_WARPS - 1) / LP_WARPS;
+    for (int rd = 0; rd < rounds; ++rd) {
+      const int i = p0 + rd * LP_WARPS + warp;
+      accumulate(true, p0, 0, p0, i < Tc ? i : -1, Tc);
+      if (i < Tc) {
+        store_half(0, T(i, p0), tp, T(i, p0), tp);
+        if (i > p0) store_half(1, T(i, p0 + 1), tp, T(i, p0 + 1), tp);
+      }
+    }
+    __syncthreads();
+    if (warp == 0) {   // diagonal pair
+      bool bad = diag_factor(T(p0, p0), tp, dinv + (long long)p0 * 1024, sL, lane);
+      __syncwarp();
+      acc_zero(t32);
+      mma_tile<false, true>(t32, T(p0 + 1, p0), tp, dinv + (long long)p0 * 1024, 32, lane, 1.0);
+      __syncwarp();
+      acc_store(t32, T(p0 + 1, p0), tp, lane);   // L10
+      __syncwarp();
+      acc_load(t32, T(p0 + 1, p0 + 1), tp, lane);
+      mma_tile<false, true>(t32, T(p0 + 1, p0), tp, T(p0 + 1, p0), tp, lane, -1.0);
+      __syncwarp();
+      acc_store(t32, T(p0 + 1, p0 + 1), tp, lane);
+      __syncwarp();
+      bad |= diag_factor(T(p0 + 1, p0 + 1), tp, dinv + (long long)(p0 + 1) * 1024, sL, lane);
+      if (bad && lane == 0) s_bad = 1;
+    }
+    __syncthreads();
+    for (int i = p0 + 2 + warp; i < Tc; i += LP_WARPS) {   // panel strips
+      acc_zero(t32);
+      mma_tile<false, true>(t32, T(i, p0), tp, dinv + (long long)p0 * 1024, 32, lane, 1.0);
+      __syncwarp();
+      acc_store(t32, T(i, p0), tp, lane);                  // L_i,p0
+      __syncwarp();
+      acc_load(t32, T(i, p0 + 1), tp, lane);
+      mma_tile<false, true>(t32, T(i, p0), tp, T(p0 + 1, p0), tp, lane, -1.0);
+      __syncwarp();
+      acc_store(t32, T(i, p0 + 1), tp, lane);
+      __syncwarp();
+      acc_zero(t32);
+      mma_tile<false, true>(t32, T(i, p0 + 1), tp, dinv + (long long)(p0 + 1) * 1024, 32, lane, 1.0);
+      __syncwarp();
+      acc_store(t32, T(i, p0 + 1), tp, lane);              // L_i,p0+1
+    }
+    __syncthreads();
+  }
+  if (s_bad) {
+    if (tid == 0) flags[slot] = 1;
+    return;
+  }
+  // ---- W = L^{-1}, block-column pairs from the last
+  double* S0 = scr + (long long)warp * 2048;
+  double* S1 = S0 + 1024;
+  for (int J0 = Tc - 2; J0 >= 0; J0 -= 2) {
+    const int J1 = J0 + 1, nstrip = Tc - 1 - J1;
+    const int rounds = (nstrip + LP_WARPS - 1) / LP_WARPS;
+    for (int rd = 0; rd < rounds; ++rd) {   // highest strips first
+      const int I = Tc - 1 - (rd * LP_WARPS + warp);
+      const bool act = I > J1;
+      const int kend = Tc - rd * LP_WARPS;   // rows of this round are <= kend - 1
+      accumulate(false, J0, J1 + 1, kend, act ? I : -1, act ? I : -1);
+      if (act) {
+        store_half(0, S0, 32, nullptr, 0);
+        store_half(1, S1, 32, nullptr, 0);
+        __syncwarp();
+        acc_zero(t32);
+        mma_tile<false, false>(t32, S1, 32, dinv + (long long)J1 * 1024, 32, lane, -1.0);
+        __syncwarp();
+        acc_store(t32, T(I, J1), tp, lane);               // W_I,J1
+        __syncwarp();
+        acc_load(t32, S0, 32, lane);
+        mma_tile<false, false>(t32, T(I, J1), tp, T(J1, J0), tp, lane, 1.0);
+        __syncwarp();
+        acc_store(t32, S0, 32, lane);
+        __syncwarp();
+        acc_zero(t32);
+        mma_tile<false, false>(t32, S0, 32, dinv + (long long)J0 * 1024, 32, lane, -1.0);
+        __syncwarp();
+        acc_store(t32, T(I, J0), tp, lane);               // W_I,J0
+      }
+    }
+    __syncthreads();
+    if (warp == 0) {   // diagonal pair
+      acc_zero(t32);
+      mma_tile<false, false>(t32, dinv + (long long)J1 * 1024, 32, T(J1, J0), tp, lane, 1.0);
+      __syncwarp();
+      acc_store(t32, S0, 32, lane);
+      __syncwarp();
+      acc_zero(t32);
+      mma_tile<false, false>(t32, S0, 32, dinv + (long long)J0 * 1024, 32, lane, -1.0);
+      __syncwarp();
+      acc_store(t32, T(J1, J0), tp, lane);                // W_J1,J0
+      for (int qd = lane; qd < 1024; qd += 32) {
+        T(J0, J0)[(long long)(qd >> 5) * tp + (qd & 31)] = dinv[(long long)J0 * 1024 + qd];
+        T(J1, J1)[(long long)(qd >> 5) * tp + (qd & 31)] = dinv[(long long)J1 * 1024 + qd];
+      }
+    }
+    __syncthreads();
+  }
+  // ---- the slot receives W (lower triangle) and W^T (upper triangle), both row-contiguous:
+  // tile (I, J), J <= I, goes to Gi[I][J] and, transposed through a per-warp shared tile, to
+  // Gi[J][I] (coalesced both ways)
+  double* Gi = Ginv + slot * gi_stride;
+  double* tt = lp_sm + warp * (32 * 33);
+  const int ntile = Tc * (Tc + 1) / 2;
+  for (int t = warp; t < ntile; t += LP_WARPS) {
+    int I, J;
+    tri_decode(t, I, J);
+    if (32 * J >= tau) continue;
+    for (int rr = 0; rr < 32; ++rr) {
+      const int row = 32 * I + rr, col = 32 * J + lane;
+      const double x = (row < tau && col <= row) ? T(I, J)[(long long)rr * tp + lane] : 0.0;
+      tt[rr * 33 + lane] = x;
+      if (row < tau && col <= row) Gi[(long long)row * ldgi + col] = x;
+    }
+    __syncwarp();
+    for (int rr = 0; rr < 32; ++rr) {   // row 32 J + rr of the upper triangle: W[32 I + lane][32 J + rr]
+      const int row = 32 * J + rr, col = 32 * I + lane;
+      if (row < tau && col < tau && col > row) Gi[(long long)row * ldgi + col] = tt[lane * 33 + rr];
+    }
+    __syncwarp();
+  }
+  if (tid == 0) flags[slot] = 0;
+}
+
 }  // namespace
 
 int bfactor_max_tau() { return BB_MAXTAU; }
@@ -625,7 +967,8 @@ int bfactor_max_tau() { return BB_MAXTAU; }
 size_t bfactor_work_elems(int tau) {
   if (tau <= BF_MAXTAU) return 0;
   const long long tp = bb_tp(tau);
-  return (size_t)(tp * tp + 2 * (tp / 32) * 1024);
+  // work matrix, Tc L_pp^{-1} tiles, then Tc tiles (right-looking T_I) or 2 per warp (left-looking)
+  return (size_t)(tp * tp + (tp / 32) * 1024 + std::max<long long>(tp / 32, 2 * LP_WARPS) * 1024);
 }
 
 cudaError_t bfactor_init() {
@@ -639,6 +982,8 @@ cudaError_t bfactor_init() {
     e = cudaFuncSetAttribute(k_apply_rows<AP_UPPER>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              ap_smem);
   if (e != cudaSuccess) return e;
+  e = cudaFuncSetAttribute(k_bfactor_lp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)LP_SMEM);
+  if (e != cudaSuccess) return e;
   return cudaFuncSetAttribute(k_bfactor_small, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               (int)bf_smem(BF_MAXTAU));
 }
@@ -649,8 +994,14 @@ cudaError_t launch_bfactor(const FactorSrc& src, const DevSketch& skb, int nslot
   if (skb.tau > BB_MAXTAU || nslots < 1) return cudaErrorInvalidValue;
   if (skb.tau > BF_MAXTAU) {
     if (!work) return cudaErrorInvalidValue;
-    k_bfactor_big<<<nslots, BB_THREADS, 0, st>>>(src, skb, Ginv, ldgi, gi_stride, work,
-                                                 (long long)bfactor_work_elems(skb.tau), flags, ctrl);
+    static const bool rl = std::getenv("RS_BF_RIGHT") != nullptr;   // A/B: right-looking kernel
+    if (rl)
+      k_bfactor_big<<<nslots, BB_THREADS, 0, st>>>(src, skb, Ginv, ldgi, gi_stride, work,
+                                                   (long long)bfactor_work_elems(skb.tau), flags, ctrl);
+    else
+      k_bfactor_lp<<<nslots, LP_THREADS, LP_SMEM, st>>>(src, skb, Ginv, ldgi, gi_stride, work,
+                                                        (long long)bfactor_work_elems(skb.tau), flags,
+                                                        ctrl);
     return cudaGetLastError();
   }
   k_bfactor_small<<<nslots, BF_THREADS, bf_smem(skb.tau), st>>>(src, skb, Ginv, ldgi, gi_stride,
