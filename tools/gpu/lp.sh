@@ -6,4 +6,3 @@ timeout 1200 python bench.py --config c5 --mode explicit --steps 148 --max-iter-
 
 timeout 1200 python bench.py --config k1 --steps 148 --max-iter-tol 2000 --no-cpu-baseline --no-e2e > gpurun_out/bench_k1.json 2>/dev/null
 timeout 900 python bench.py --config c4 --mode explicit --steps 148 --max-iter-tol 20000 --no-cpu-baseline --no-e2e > gpurun_out/bench_c4_explicit.json 2>/dev/null
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_bfactor_lp" -c 1 -o gpurun_out/prof_lp python tools/prof_step.py c5 explicit 150 > gpurun_out/ncu_lp.log 2>&1
