@@ -34,6 +34,10 @@ Problem::~Problem() {
   if (st) cudaStreamSynchronize(st);
   free_workspace();
   dfree(XT);
+  dfree(kbase_dev);
+  if (st2) cudaStreamDestroy(st2);
+  if (ev_fork) cudaEventDestroy(ev_fork);
+  if (ev_join) cudaEventDestroy(ev_join);
   if (own_X) dfree(X);
   dfree(y);
   dfree(b);
@@ -724,6 +728,59 @@ rs_status Problem::enqueue_group_xg(const rs_solve_opts* o, int g, cudaEvent_t* 
   return RS_OK;
 }
 
+// Concurrent group (dense GRAM with X^T, one rank): the Grams of the other slot set (the next
+// group's iterations, drawn here first) run on st2 -- lean k_gram_xt, 8 warps / ~96 KB -- while the
+// P iterations run on st with the lean X pass (2 consumer warps / ~96 KB), so an SM holds one CTA
+// of each: the DMMA-bound Gram overlaps the HBM-bound X stream.  The Grams read the group's base
+// iteration from a snapshot (ctrl->k advances under them).  Then the other set is factored.
+rs_status Problem::enqueue_group_xc(const rs_solve_opts* o, int g, cudaEvent_t* ev) {
+  auto mark = [&](int q, int cls, int edge) {
+    if (ev) cudaEventRecordWithFlags(ev[(size_t)q * 2 * RS_K_NCLASSES + 2 * cls + edge], st,
+                                     cudaEventRecordExternal);
+  };
+  const int cur = g, nxt = 1 - g;
+  const DevSketch sc = skb.at(cur * P), sn = skb.at(nxt * P);
+  mark(0, RS_K_PRE, 0);
+  RS_CUDA(launch_sketch_batch(sn, P, o->seed, ctrl, -1, st, P));                  // a1 x P (ahead)
+  RS_CUDA(launch_snap_k(ctrl, kbase_dev, st));
+  mark(0, RS_K_PRE, 1);
+  RS_CUDA(cudaEventRecord(ev_fork, st));
+  RS_CUDA(cudaStreamWaitEvent(st2, ev_fork, 0));
+  for (int q = 0; q < P; ++q) {                                                   // st2: Grams ahead
+    const long long ns = (long long)nxt * P + q;
+    RS_CUDA(launch_gram_xt(XT, ldxt, rows_loc, sn.at(q), gf_part, Gram_slots + ns * gram_stride,
+                           ld_gram, num_sms, ctrl, st2, P + q, kbase_dev, true));
+  }
+  RS_CUDA(cudaEventRecord(ev_join, st2));
+  for (int q = 0; q < P; ++q) {                                                   // st: iterations
+    const long long cs = (long long)cur * P + q;
+    const DevSketch sq = sc.at(q);
+    mark(q, RS_K_SOLVE, 0);
+    RS_CUDA(launch_apply_ginv(Ginv_slots + cs * gi_stride, ld_gi, sq, slot_flags + cs, r, sw.Gx,
+                              sw.delta, sdelta, ctrl, st));                       // a4 + a5
+    mark(q, RS_K_SOLVE, 1);
+    mark(q, RS_K_AS, 0);
+    RS_CUDA(launch_xpass(X, ldx, rows_loc, m, sdelta, xp_part, uvec, num_sms, ctrl, st, &sq,
+                         sw.delta, true));                                        // X^T X S delta
+    mark(q, RS_K_AS, 1);
+    mark(q, RS_K_UPDATE, 0);
+    RS_CUDA(launch_update_vec(uvec, lambda, sdelta, w, dw, r, dr, m, o->gamma, o->beta, partials,
+                              ctrl, st));                                          // a6 + a7
+    mark(q, RS_K_UPDATE, 1);
+  }
+  RS_CUDA(cudaStreamWaitEvent(st, ev_join, 0));
+  FactorSrc src{};
+  src.Gram = Gram_slots + (long long)nxt * P * gram_stride;
+  src.ld_gram = ld_gram;
+  src.gram_stride = gram_stride;
+  src.lambda = lambda;
+  mark(0, RS_K_FACTOR, 0);
+  RS_CUDA(launch_bfactor(src, sn, P, Ginv_slots + (long long)nxt * P * gi_stride, ld_gi, gi_stride,
+                         slot_flags + (long long)nxt * P, bf_work, ctrl, st));   // a4 + a5 ahead
+  mark(0, RS_K_FACTOR, 1);
+  return RS_OK;
+}
+
 static int status_of(int st) {
   switch (st) {
     case ST_DIVERGED: return RS_EDIVERGED;
@@ -773,8 +830,16 @@ rs_status Problem::solve(const rs_solve_opts* o, double* w_out, rs_mem w_mem, do
                                        : (want_pipe ? (o->tau > 224 ? num_sms : 64) : 16));
   // fused X pass + Gram ahead (k_xpass_gram1, opt-in RS_XG=1: on c2 it measures 0.69 ms per
   // iteration vs 0.65 ms for the separate k_xpass_tma + k_gram_fused, profiles/README.md)
-  const bool want_xg = want_pipe && fmt == 0 && mode == RS_AS_GRAM && rows_loc > 0 &&
-                       xpass_gram_ok((int)o->kind, (int)o->tau, d, ldx) && std::getenv("RS_XG");
+  const bool want_xg0 = want_pipe && fmt == 0 && mode == RS_AS_GRAM && rows_loc > 0 &&
+                        xpass_gram_ok((int)o->kind, (int)o->tau, d, ldx) && std::getenv("RS_XG");
+  // concurrent Gram / X-pass groups (opt-in RS_XC=1): dense GRAM, subsample tau <= 200 (X^T
+  // Gram), d <= 2048 (lean row-owner X pass), one rank.  On c2 it measures 0.85 ms per iteration
+  // against 0.44 ms sequential: with one CTA of each kernel per SM the register file leaves the X
+  // pass 2 consumer warps, which cannot keep up with the HBM stream
+  const bool want_xc = want_pipe && !want_xg0 && fmt == 0 && mode == RS_AS_GRAM && rows_loc > 0 &&
+                       world == 1 && gram_fused_ok((int)o->kind, (int)o->tau) && d <= 2048 &&
+                       ldx * 8 <= 32768 && !std::getenv("RS_NO_XT") && std::getenv("RS_XC");
+  const bool want_xg = want_xg0 || want_xc;
   if (want_xg) chunk = std::max(2, chunk & ~1);   // two groups of P = chunk / 2
   int depth = 0;
   if (want_pipe) {   // one batched factorisation wave: <= num_sms slots, <= ~6 GB of slots
@@ -790,6 +855,13 @@ rs_status Problem::solve(const rs_solve_opts* o, double* w_out, rs_mem w_mem, do
     }
   }
   RS_TRY(ensure_workspace((int)o->kind, (int)o->tau, ksum, depth, want_xg));
+  pipe_xc = want_xc && pipe_xg && XT != nullptr;
+  if (pipe_xc && !st2) {
+    RS_CUDA(cudaStreamCreateWithFlags(&st2, cudaStreamNonBlocking));
+    RS_CUDA(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
+    RS_CUDA(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming));
+    RS_TRY(dalloc(&kbase_dev, 1));
+  }
   // state: w^{-1} = w^0 = 0, r^{-1} = r^0 = -b
   RS_CUDA(launch_fill(w, m, 0.0, st));
   RS_CUDA(launch_fill(dw, m, 0.0, st));
@@ -852,7 +924,7 @@ rs_status Problem::solve(const rs_solve_opts* o, double* w_out, rs_mem w_mem, do
     auto evs = [&](int i) { return o->profile ? &prof_events[(size_t)i * 2 * RS_K_NCLASSES] : nullptr; };
     for (int i = 0; i < chunk && s == RS_OK;) {
       if (pipe_xg) {   // two groups, alternating slot sets
-        s = enqueue_group_xg(o, (i / P) & 1, evs(i));
+        s = pipe_xc ? enqueue_group_xc(o, (i / P) & 1, evs(i)) : enqueue_group_xg(o, (i / P) & 1, evs(i));
         i += P;
       } else if (pipe) {   // group: precompute ns slots, then ns iterations on them
         const int ns = std::min(P, chunk - i);

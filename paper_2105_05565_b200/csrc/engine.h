@@ -98,6 +98,12 @@ struct Problem {
   // set g % 2, its X passes also form the Grams of the other set (k_xpass_gram)
   bool pipe_xg = false;
   int ws_xg = -1;
+  // concurrent variant (dense GRAM with X^T, one rank): the Grams of the other set run on a second
+  // stream (lean k_gram_xt) while the iterations' lean X passes stream X (enqueue_group_xc)
+  bool pipe_xc = false;
+  cudaStream_t st2 = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  long long* kbase_dev = nullptr;   // the group's base iteration, for the concurrent Grams
   double* gf_part = nullptr;
   SolveWork sw{};
   double* partials = nullptr;
@@ -113,6 +119,7 @@ struct Problem {
   rs_status allreduce(double* buf, size_t count);
   rs_status ensure_workspace(int kind, int tau, int ksum, int depth, bool xg = false);
   rs_status enqueue_group_xg(const rs_solve_opts* o, int g, cudaEvent_t* ev);
+  rs_status enqueue_group_xc(const rs_solve_opts* o, int g, cudaEvent_t* ev);
   rs_status enqueue_iteration(const rs_solve_opts* o, cudaEvent_t* ev);
   rs_status enqueue_precompute(const rs_solve_opts* o, int nslots, cudaEvent_t* ev);
   rs_status enqueue_pipelined_iteration(const rs_solve_opts* o, int slot, cudaEvent_t* ev);

@@ -192,12 +192,11 @@ k_xpass_tma(const double* __restrict__ X, long long ldx, long long rows, long lo
 // Every warp waits on every block's "full" barrier in order (also blocks without a row of its own),
 // so no warp can run two phases ahead of a stage; "empty" counts the R row releases of a stage.  At
 // the end the 8 warp accumulators are summed in warp order through shared memory (deterministic).
-constexpr int XR_CONS = 8;
-constexpr int XR_THREADS = (XR_CONS + 1) * 32;
 constexpr int XR_NQ = 64;                     // d <= 2048
 constexpr int XR_MAXLEN = 4096;               // sketch entries
 
-__global__ void __launch_bounds__(XR_THREADS, 1)
+template <int XR_CONS>
+__global__ void __launch_bounds__((XR_CONS + 1) * 32)
 k_xpass_rows(const double* __restrict__ X, long long ldx, long long rows, long long d, DevSketch sk,
              const double* __restrict__ delta, double* __restrict__ partials,
              long long rows_per_cta, int R, int stages, const Ctrl* ctrl) {
@@ -220,7 +219,7 @@ k_xpass_rows(const double* __restrict__ X, long long ldx, long long rows, long l
     }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
-  for (int e = tid; e < len; e += XR_THREADS) {
+  for (int e = tid; e < len; e += (XR_CONS + 1) * 32) {
     const double dv = delta[sk.bucket[e]];
     s_sd[e] = sk.sign[e] > 0 ? dv : -dv;
     s_co[e] = sk.coord[e];
@@ -441,88 +440,100 @@ __device__ __forceinline__ void cp_async16z(void* smem, const void* gmem, int sr
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(src_bytes));
 }
 
-template <int GX_BK>
-__global__ void __launch_bounds__(GF_THREADS, 1)
+// NW warps per CTA; the (tau / 40)-region list is covered in ceil(regions / NW) passes over the
+// K slice (NW = 16: one pass; NW = 8: the lean variant that shares an SM with the X pass).
+// kbase (optional): the group's base iteration, for a Gram running concurrently with the
+// iterations that advance ctrl->k (slot q is needed iff kbase + q < max_iter).
+template <int GX_BK, int NW>
+__global__ void __launch_bounds__(NW * 32)
 k_gram_xt(const double* __restrict__ XT, long long ldxt, long long rows, DevSketch sk,
-          long long rows_per_cta, double* __restrict__ partials, int slot, const Ctrl* ctrl) {
-  constexpr int GX_LDK = GxCfg<GX_BK>::LDK, GX_STAGES = GxCfg<GX_BK>::STAGES;
-  if (slot_unused(ctrl, slot)) return;
+          long long rows_per_cta, double* __restrict__ partials, int slot, const Ctrl* ctrl,
+          const long long* kbase) {
+  constexpr int GX_LDK = GxCfg<GX_BK>::LDK, NT = NW * 32;
+  constexpr int GX_STAGES = NW == 8 ? GxCfg<GX_BK>::STAGES / 2 : GxCfg<GX_BK>::STAGES;   // lean: half
+  if (ctrl->done || (kbase ? *kbase : ctrl->k) + slot >= ctrl->max_iter) return;
   extern __shared__ __align__(16) double gsm[];   // [GX_STAGES][ng * 40][GX_LDK]
   __shared__ int s_col[GF_MAXTAU];
   const int tau = sk.tau, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  for (int b = tid; b < tau; b += GF_THREADS) s_col[b] = sk.coord[sk.bptr[b]];
+  for (int b = tid; b < tau; b += NT) s_col[b] = sk.coord[sk.bptr[b]];
   __syncthreads();
   const long long r0 = (long long)blockIdx.x * rows_per_cta;
   const long long r1 = min(rows, r0 + rows_per_cta);
   const int nkb = r0 < r1 ? (int)((r1 - r0 + GX_BK - 1) / GX_BK) : 0;
   const int ng = (tau + 39) / 40, srows = ng * 40;
+  const int nreg = ng * (ng + 1) / 2, passes = (nreg + NW - 1) / NW;
   const int stage_elems = srows * GX_LDK;
   auto load = [&](int stage, int kb) {
     double* dst = gsm + stage * stage_elems;
     const long long k0 = r0 + (long long)kb * GX_BK;
-    for (int q = tid; q < srows * (GX_BK / 2); q += GF_THREADS) {
+    for (int q = tid; q < srows * (GX_BK / 2); q += NT) {
       const int b = q / (GX_BK / 2), h = q % (GX_BK / 2);
       const long long k = k0 + 2 * h;
       const int nb = (b < tau) ? (int)max(0LL, min(2LL, r1 - k)) * 8 : 0;
       cp_async16z(dst + b * GX_LDK + 2 * h, nb ? XT + (long long)s_col[b] * ldxt + k : XT, nb);
     }
   };
-#pragma unroll
-  for (int s = 0; s < GX_STAGES - 1; ++s) {
-    if (s < nkb) load(s, s);
-    asm volatile("cp.async.commit_group;\n");
-  }
-  int I = -1, J = -1;
-  {
-    int t = 0;
-    for (int a = 0; a < ng; ++a)
-      for (int b = 0; b <= a; ++b, ++t)
-        if (t == warp) { I = a; J = b; }
-  }
-  const bool active = I >= 0, diag = I == J;
-  double acc[5][5][2];
-#pragma unroll
-  for (int x = 0; x < 5; ++x)
-#pragma unroll
-    for (int y = 0; y < 5; ++y) acc[x][y][0] = acc[x][y][1] = 0.0;
   const int kq = lane & 3, mq = lane >> 2;
-  for (int kb = 0; kb < nkb; ++kb) {
-    asm volatile("cp.async.wait_group %0;\n" ::"n"(GX_STAGES - 2));
-    __syncthreads();
-    const int nxt = kb + GX_STAGES - 1;
-    if (nxt < nkb) load(nxt % GX_STAGES, nxt);
-    asm volatile("cp.async.commit_group;\n");
-    if (active) {
-      const double* st = gsm + (kb % GX_STAGES) * stage_elems + mq * GX_LDK + kq;
-      const double* sa = st + (I * 40) * GX_LDK;
-      const double* sb = st + (J * 40) * GX_LDK;
+  double* out = partials + (long long)blockIdx.x * GF_MAXTAU * GF_MAXTAU;
+  for (int pass = 0; pass < passes; ++pass) {
 #pragma unroll
-      for (int kk = 0; kk < GX_BK; kk += 4) {
-        double bf[5];
+    for (int s = 0; s < GX_STAGES - 1; ++s) {
+      if (s < nkb) load(s, s);
+      asm volatile("cp.async.commit_group;\n");
+    }
+    int I = -1, J = -1;
+    {
+      const int want = warp + pass * NW;
+      int t = 0;
+      for (int a = 0; a < ng; ++a)
+        for (int b = 0; b <= a; ++b, ++t)
+          if (t == want) { I = a; J = b; }
+    }
+    const bool active = I >= 0, diag = I == J;
+    double acc[5][5][2];
 #pragma unroll
-        for (int y = 0; y < 5; ++y) bf[y] = sb[y * 8 * GX_LDK + kk];
+    for (int x = 0; x < 5; ++x)
 #pragma unroll
-        for (int x = 0; x < 5; ++x) {
-          const double af = sa[x * 8 * GX_LDK + kk];
+      for (int y = 0; y < 5; ++y) acc[x][y][0] = acc[x][y][1] = 0.0;
+    for (int kb = 0; kb < nkb; ++kb) {
+      asm volatile("cp.async.wait_group %0;\n" ::"n"(GX_STAGES - 2));
+      __syncthreads();
+      const int nxt = kb + GX_STAGES - 1;
+      if (nxt < nkb) load(nxt % GX_STAGES, nxt);
+      asm volatile("cp.async.commit_group;\n");
+      if (active) {
+        const double* st = gsm + (kb % GX_STAGES) * stage_elems + mq * GX_LDK + kq;
+        const double* sa = st + (I * 40) * GX_LDK;
+        const double* sb = st + (J * 40) * GX_LDK;
 #pragma unroll
-          for (int y = 0; y < 5; ++y)
-            if (!diag || y <= x) dmma_g(acc[x][y], af, bf[y]);   // diagonal region: lower tiles
+        for (int kk = 0; kk < GX_BK; kk += 4) {
+          double bf[5];
+#pragma unroll
+          for (int y = 0; y < 5; ++y) bf[y] = sb[y * 8 * GX_LDK + kk];
+#pragma unroll
+          for (int x = 0; x < 5; ++x) {
+            const double af = sa[x * 8 * GX_LDK + kk];
+#pragma unroll
+            for (int y = 0; y < 5; ++y)
+              if (!diag || y <= x) dmma_g(acc[x][y], af, bf[y]);   // diagonal region: lower tiles
+          }
         }
       }
     }
-  }
-  asm volatile("cp.async.wait_group 0;\n");
-  if (!active) return;
-  double* out = partials + (long long)blockIdx.x * GF_MAXTAU * GF_MAXTAU;
+    asm volatile("cp.async.wait_group 0;\n");
+    __syncthreads();   // the ring is reused by the next pass
+    if (active) {
 #pragma unroll
-  for (int x = 0; x < 5; ++x) {
-    const int a = I * 40 + x * 8 + (lane >> 2);
+      for (int x = 0; x < 5; ++x) {
+        const int a = I * 40 + x * 8 + (lane >> 2);
 #pragma unroll
-    for (int y = 0; y < 5; ++y) {
-      const int b = J * 40 + y * 8 + 2 * (lane & 3);
-      if (a < tau) {
-        if (b < tau) out[a * GF_MAXTAU + b] = acc[x][y][0];
-        if (b + 1 < tau) out[a * GF_MAXTAU + b + 1] = acc[x][y][1];
+        for (int y = 0; y < 5; ++y) {
+          const int b = J * 40 + y * 8 + 2 * (lane & 3);
+          if (a < tau) {
+            if (b < tau) out[a * GF_MAXTAU + b] = acc[x][y][0];
+            if (b + 1 < tau) out[a * GF_MAXTAU + b + 1] = acc[x][y][1];
+          }
+        }
       }
     }
   }
@@ -561,8 +572,8 @@ __global__ void k_transpose(const double* __restrict__ X, long long ldx, long lo
 // square GF_MAXTAU x GF_MAXTAU partial layout x 8 slices; entries above the diagonal are skipped.
 __global__ void __launch_bounds__(256)
 k_gram_reduce(const double* __restrict__ partials, int nparts, int tau, double* __restrict__ G,
-              long long ldg, const Ctrl* ctrl, int slot = 0) {
-  if (slot_unused(ctrl, slot)) return;
+              long long ldg, const Ctrl* ctrl, int slot = 0, const long long* kbase = nullptr) {
+  if (ctrl->done || (kbase ? *kbase : ctrl->k) + slot >= ctrl->max_iter) return;
   __shared__ double red[8][33];
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
   const int q = blockIdx.x * 32 + tx, a = q / GF_MAXTAU, b = q % GF_MAXTAU;
@@ -944,13 +955,18 @@ cudaError_t gram_init() {
   cudaError_t e = cudaFuncSetAttribute(k_xpass_tma, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        210 * 1024);
   if (e != cudaSuccess) return e;
-  e = cudaFuncSetAttribute(k_xpass_rows, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+  e = cudaFuncSetAttribute(k_xpass_rows<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
   if (e != cudaSuccess) return e;
-  e = cudaFuncSetAttribute(k_gram_xt<16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  e = cudaFuncSetAttribute(k_xpass_rows<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+  if (e != cudaSuccess) return e;
+  e = cudaFuncSetAttribute(k_gram_xt<16, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)gram_xt_smem<16>(GF_MAXTAU));
   if (e != cudaSuccess) return e;
-  e = cudaFuncSetAttribute(k_gram_xt<32>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  e = cudaFuncSetAttribute(k_gram_xt<32, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)gram_xt_smem<32>(GF_MAXTAU));
+  if (e != cudaSuccess) return e;
+  e = cudaFuncSetAttribute(k_gram_xt<16, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)gram_xt_smem<16>(GF_MAXTAU) / 2);
   if (e != cudaSuccess) return e;
   return cudaFuncSetAttribute(k_gram_fused, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               GF_STAGES * GF_BK * GF_LD * (int)sizeof(double));
@@ -978,19 +994,33 @@ cudaError_t launch_transpose(const double* X, long long ldx, long long rows, lon
 
 cudaError_t launch_gram_xt(const double* XT, long long ldxt, long long rows, const DevSketch& sk,
                            double* partials, double* G, long long ldg, int num_sms,
-                           const Ctrl* ctrl, cudaStream_t st, int slot) {
+                           const Ctrl* ctrl, cudaStream_t st, int slot, const long long* kbase,
+                           bool lean) {
   const int nc = num_sms;
-  const int bk = gx_bk();
+  const int bk = lean ? 16 : gx_bk();
   const long long rpc = std::max<long long>(bk, ((rows + nc - 1) / nc + bk - 1) / bk * bk);
-  if (bk == 16)
-    k_gram_xt<16><<<nc, GF_THREADS, gram_xt_smem<16>(sk.tau), st>>>(XT, ldxt, rows, sk, rpc, partials,
-                                                                   slot, ctrl);
+  if (lean)   // 8 warps, 3 stages of 16 rows: ~96 KB, leaves room for the lean X pass
+    k_gram_xt<16, 8><<<nc, 8 * 32, gram_xt_smem<16>(sk.tau) / 2, st>>>(XT, ldxt, rows, sk, rpc,
+                                                                       partials, slot, ctrl, kbase);
+  else if (bk == 16)
+    k_gram_xt<16, 16><<<nc, GF_THREADS, gram_xt_smem<16>(sk.tau), st>>>(XT, ldxt, rows, sk, rpc,
+                                                                       partials, slot, ctrl, kbase);
   else
-    k_gram_xt<32><<<nc, GF_THREADS, gram_xt_smem<32>(sk.tau), st>>>(XT, ldxt, rows, sk, rpc, partials,
-                                                                   slot, ctrl);
+    k_gram_xt<32, 16><<<nc, GF_THREADS, gram_xt_smem<32>(sk.tau), st>>>(XT, ldxt, rows, sk, rpc,
+                                                                       partials, slot, ctrl, kbase);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
-  k_gram_reduce<<<gram_reduce_grid(sk.tau), 256, 0, st>>>(partials, nc, sk.tau, G, ldg, ctrl, slot);
+  k_gram_reduce<<<gram_reduce_grid(sk.tau), 256, 0, st>>>(partials, nc, sk.tau, G, ldg, ctrl, slot,
+                                                          kbase);
+  return cudaGetLastError();
+}
+
+namespace {
+__global__ void k_snap_k(const Ctrl* ctrl, long long* out) { *out = ctrl->k; }
+}  // namespace
+
+cudaError_t launch_snap_k(const Ctrl* ctrl, long long* out, cudaStream_t st) {
+  k_snap_k<<<1, 1, 0, st>>>(ctrl, out);
   return cudaGetLastError();
 }
 
@@ -1000,25 +1030,35 @@ size_t xpass_partials(long long d, int num_sms) { return (size_t)num_sms * (size
 cudaError_t launch_xpass(const double* X, long long ldx, long long rows, long long d,
                          const double* v, double* partials, double* u, int num_sms,
                          const Ctrl* ctrl, cudaStream_t st, const DevSketch* sk,
-                         const double* delta) {
+                         const double* delta, bool lean) {
   if (d > (long long)XP_THREADS * XP_Q) return cudaErrorInvalidValue;
   const int nc = xpass_ctas(num_sms);
   const long long rpc = std::max<long long>(1, (rows + nc - 1) / nc);
   static const bool no_tma = std::getenv("RS_NO_TMA_XPASS") != nullptr;
   static const bool no_rows = std::getenv("RS_NO_XPASS_ROWS") != nullptr;
-  // ring: R rows per stage (~64 KB), as many stages as fit in ~200 KB (>= 2)
+  // ring: R rows per stage (~64 KB), as many stages as fit in ~200 KB (>= 2); lean (shares the SM
+  // with a concurrent Gram kernel): 2 consumer warps, ~96 KB
   const long long row_bytes = ldx * 8;
-  int R = (int)std::max<long long>(1, std::min<long long>(XT_MAXR, 65536 / row_bytes));
+  const long long stage_target = lean ? 32768 : 65536, ring_target = lean ? 98304 : 200 * 1024;
+  int R = (int)std::max<long long>(1, std::min<long long>(XT_MAXR, stage_target / row_bytes));
   static const char* er = std::getenv("RS_XP_R");   // tuning overrides (bench sweeps only)
-  if (er) R = std::max(1, std::min(XT_MAXR, atoi(er)));
-  int stages = (int)std::min<long long>(8, (200 * 1024) / (R * row_bytes));
+  if (er && !lean) R = std::max(1, std::min(XT_MAXR, atoi(er)));
+  int stages = (int)std::min<long long>(8, ring_target / (R * row_bytes));
   static const char* es = std::getenv("RS_XP_STAGES");
-  if (es) stages = std::max(2, std::min(stages, atoi(es)));
+  if (es && !lean) stages = std::max(2, std::min(stages, atoi(es)));
   const size_t ring = (size_t)stages * R * row_bytes;
+  const int cons = lean ? 2 : 8;
   if (!no_tma && !no_rows && sk && delta && d <= 32LL * XR_NQ && sk->len <= XR_MAXLEN &&
-      stages >= 2 && ring >= (size_t)XR_CONS * d * 8 && ring + (size_t)sk->len * 12 <= 220 * 1024) {
-    k_xpass_rows<<<nc, XR_THREADS, ring + (size_t)sk->len * 12, st>>>(X, ldx, rows, d, *sk, delta,
-                                                                      partials, rpc, R, stages, ctrl);
+      stages >= 2 && ring >= (size_t)cons * d * 8 && ring + (size_t)sk->len * 12 <= 220 * 1024) {
+    const size_t smem = ring + (size_t)sk->len * 12;
+    if (lean)
+      k_xpass_rows<2><<<nc, 3 * 32, smem, st>>>(X, ldx, rows, d, *sk, delta, partials, rpc, R, stages,
+                                                ctrl);
+    else
+      k_xpass_rows<8><<<nc, 9 * 32, smem, st>>>(X, ldx, rows, d, *sk, delta, partials, rpc, R, stages,
+                                                ctrl);
+  } else if (lean) {
+    return cudaErrorInvalidValue;
   } else if (!no_tma && stages >= 2 && d <= (long long)XT_CONS * 32 * XT_Q) {
     k_xpass_tma<<<nc, XT_THREADS, ring, st>>>(X, ldx, rows, d, v, partials, rpc, R, stages, ctrl);
   } else {

@@ -232,13 +232,16 @@ cudaError_t launch_transpose(const double* X, long long ldx, long long rows, lon
                              long long ldxt, cudaStream_t st);
 cudaError_t launch_gram_xt(const double* XT, long long ldxt, long long rows, const DevSketch& sk,
                            double* partials, double* G, long long ldg, int num_sms,
-                           const Ctrl* ctrl, cudaStream_t st, int slot = 0);
+                           const Ctrl* ctrl, cudaStream_t st, int slot = 0,
+                           const long long* kbase = nullptr, bool lean = false);
+// *out = ctrl->k (a group's base iteration for kernels running beside the iterations)
+cudaError_t launch_snap_k(const Ctrl* ctrl, long long* out, cudaStream_t st);
 // v = S delta (dense, m); when the sketch and delta are given and d <= 2048, the row-owner kernel
 // forms <X_i, v> from the sketch entries only.
 cudaError_t launch_xpass(const double* X, long long ldx, long long rows, long long d,
                          const double* v, double* partials, double* u, int num_sms,
                          const Ctrl* ctrl, cudaStream_t st, const DevSketch* sk = nullptr,
-                         const double* delta = nullptr);
+                         const double* delta = nullptr, bool lean = false);
 // Fused gather + Gram (subsample, tau <= 200): G lower = sum_i X[i,C]^T X[i,C], no XS written.
 bool gram_fused_ok(int kind, int tau);
 // Fused X pass: u = X^T (X v) for this iteration AND the Gram (X S')^T (X S') of a future

@@ -338,11 +338,13 @@ def test_dense_large_tau_sketch_ahead(rs, kind, tau, k, mode):
     assert rel(r, ref["r"]) <= 1e-10
 
 
+@pytest.mark.parametrize("env", ["RS_XG", "RS_XC"])
 @pytest.mark.parametrize("n,d,tau,check_every", [(1000, 50, 10, 7), (3001, 470, 200, 64), (2999, 1990, 123, 2)])
-def test_dense_fused_xpass_gram(rs, monkeypatch, n, d, tau, check_every):
-    """Opt-in fused pipeline (RS_XG=1, k_xpass_gram1): each X pass also forms the Gram of the
-    sketch P iterations ahead; two alternating slot sets."""
-    monkeypatch.setenv("RS_XG", "1")
+def test_dense_fused_xpass_gram(rs, monkeypatch, env, n, d, tau, check_every):
+    """Opt-in two-set pipelines: RS_XG=1 (k_xpass_gram1: each X pass also forms the Gram of the
+    sketch P iterations ahead) and RS_XC=1 (the next set's Grams from X^T on a second stream,
+    concurrent with the lean X passes); two alternating slot sets."""
+    monkeypatch.setenv(env, "1")
     X, y = rsinputs.dense_problem(n, d, seed=4)
     X, y = X.numpy(), y.numpy()
     h = rs.rs_create_dense(X, y, 0.3, mode="gram")
