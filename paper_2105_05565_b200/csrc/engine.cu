@@ -285,59 +285,62 @@ static rs_status create_dense(rs_problem* out, int64_t n, int64_t d, const doubl
     if (ce != cudaSuccess) return guard(fail(RS_ECUDA, cudaGetErrorString(ce)));
     if (h) return guard(fail(RS_EINVAL, "X or y has non-finite entries"));
   }
-  cudaEventRecord(e0, p->st);
-  // b = X^T y  (primal, P:L143), summed over ranks
+  // every buffer of the setup is allocated before e0 (and freed after e1), so setup_seconds is the
+  // device work of b = X^T y and the explicit A build, not host allocator time
   s = dalloc(&p->b, d);
   if (s != RS_OK) return guard(s);
-  {
-    double* work = nullptr;
-    s = dalloc(&work, dense_xty_work(rows, d));
-    if (s != RS_OK) return guard(s);
-    cudaError_t ce = launch_dense_xty(p->X, p->ldx, rows, d, p->y, p->b, work, p->st);
-    cudaStreamSynchronize(p->st);
-    dfree(work);
-    if (ce != cudaSuccess) return guard(fail(RS_ECUDA, cudaGetErrorString(ce)));
-    s = p->allreduce(p->b, d);
-    if (s != RS_OK) return guard(s);
-  }
-  if (mode == RS_AS_EXPLICIT) {  // A = X^T X + lambda I, built once (DSYRK-shaped DMMA contraction)
+  double* xty_work = nullptr;
+  s = dalloc(&xty_work, dense_xty_work(rows, d));
+  if (s != RS_OK) return guard(s);
+  double* a_work = nullptr;
+  TmaGemm tg{};
+  GemmPlan gp{};
+  const bool a_cpasync = rows > 0 && std::getenv("RS_A_BUILD_CPASYNC");   // comparison path
+  cudaError_t ce = cudaSuccess;
+  if (mode == RS_AS_EXPLICIT) {
     p->lda = round_up(d, 4);
     s = dalloc(&p->A, (size_t)d * p->lda);
     if (s != RS_OK) return guard(s);
-    // lower-triangle tiles only on the TMA/DMMA contraction (d^2 n flop instead of 2 d^2 n), then
-    // the upper triangle mirrored: A is symmetric (P:L143)
-    double* work = nullptr;
-    cudaError_t ce = cudaSuccess;
-    if (rows > 0 && std::getenv("RS_A_BUILD_CPASYNC")) {   // comparison path (k_tn_gemm, full)
-      GemmPlan gp = plan_tn_gemm(d, d, rows, p->num_sms);
-      if (gp.work_elems) {
-        s = dalloc(&work, gp.work_elems);
-        if (s != RS_OK) return guard(s);
-      }
-      ce = launch_tn_gemm(p->X, p->ldx, p->X, p->ldx, d, d, rows, p->A, p->lda, gp, work, nullptr, p->st);
+    if (a_cpasync) {
+      gp = plan_tn_gemm(d, d, rows, p->num_sms);
+      if (gp.work_elems) s = dalloc(&a_work, gp.work_elems);
     } else if (rows > 0) {
-      TmaGemm tg{};
       ce = tma_gemm_plan(&tg, p->X, p->ldx, p->X, p->ldx, d, d, rows, p->num_sms);
       if (std::getenv("RS_VERBOSE"))
         fprintf(stderr, "[rs] A build: TMA variant %d (%dx%d), splits %d\n", tg.variant, tg.bm, tg.bn, tg.splits);
       tg.lower = 1;
-      if (ce == cudaSuccess && tg.work_elems) {
-        s = dalloc(&work, tg.work_elems);
-        if (s != RS_OK) return guard(s);
-      }
-      if (ce == cudaSuccess) ce = tma_gemm_launch(tg, p->A, p->lda, work, nullptr, p->st);
+      if (ce == cudaSuccess && tg.work_elems) s = dalloc(&a_work, tg.work_elems);
+    }
+    if (s != RS_OK) return guard(s);
+    if (ce != cudaSuccess) return guard(fail(RS_ECUDA, std::string("A build: ") + cudaGetErrorString(ce)));
+  }
+  cudaEventRecord(e0, p->st);
+  // b = X^T y  (primal, P:L143), summed over ranks
+  ce = launch_dense_xty(p->X, p->ldx, rows, d, p->y, p->b, xty_work, p->st);
+  if (ce != cudaSuccess) return guard(fail(RS_ECUDA, cudaGetErrorString(ce)));
+  s = p->allreduce(p->b, d);
+  if (s != RS_OK) return guard(s);
+  if (mode == RS_AS_EXPLICIT) {  // A = X^T X + lambda I, built once (DSYRK-shaped DMMA contraction)
+    // lower-triangle tiles only on the TMA/DMMA contraction (d^2 n flop instead of 2 d^2 n), then
+    // the upper triangle mirrored: A is symmetric (P:L143)
+    if (a_cpasync) {
+      ce = launch_tn_gemm(p->X, p->ldx, p->X, p->ldx, d, d, rows, p->A, p->lda, gp, a_work, nullptr, p->st);
+    } else if (rows > 0) {
+      ce = tma_gemm_launch(tg, p->A, p->lda, a_work, nullptr, p->st);
       if (ce == cudaSuccess) ce = launch_mirror_lower(p->A, p->lda, d, p->st);
     } else {
       ce = launch_fill(p->A, (long long)d * p->lda, 0.0, p->st);
     }
-    cudaStreamSynchronize(p->st);
-    dfree(work);
     if (ce != cudaSuccess) return guard(fail(RS_ECUDA, std::string("A build: ") + cudaGetErrorString(ce)));
     s = p->allreduce(p->A, (size_t)d * p->lda);
     if (s != RS_OK) return guard(s);
     launch_add_diag(p->A, p->lda, d, lambda, p->st);
   }
   cudaEventRecord(e1, p->st);
+  ce = cudaStreamSynchronize(p->st);
+  dfree(xty_work);
+  dfree(a_work);
+  if (ce != cudaSuccess) return guard(fail(RS_ECUDA, cudaGetErrorString(ce)));
   s = finish_setup(p);
   if (s != RS_OK) return guard(s);
   float ms = 0;
@@ -345,7 +348,7 @@ static rs_status create_dense(rs_problem* out, int64_t n, int64_t d, const doubl
   p->setup_seconds = ms * 1e-3;
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
-  cudaError_t ce = cudaGetLastError();
+  ce = cudaGetLastError();
   if (ce != cudaSuccess) return guard(fail(RS_ECUDA, cudaGetErrorString(ce)));
   *out = reinterpret_cast<rs_problem>(p);
   return RS_OK;
