@@ -88,10 +88,6 @@ void Problem::free_workspace() {
   sw = SolveWork{};
   dfree(partials);
   partials = nullptr;
-  dfree(rows_part);
-  rows_part = nullptr;
-  dfree(rows_cnt);
-  rows_cnt = nullptr;
   dfree(skb.coord);
   dfree(skb.sign);
   dfree(skb.bucket);
@@ -504,11 +500,6 @@ rs_status Problem::ensure_workspace(int kind, int tau, int ksum, int depth, bool
   RS_TRY(dalloc(&sw.Gx, solve_gx_elems(tau)));
   RS_TRY(dalloc(&sw.delta, tau));
   RS_TRY(dalloc(&partials, update_partials(m)));
-  if (mode == RS_AS_EXPLICIT) {   // split-row update scratch (k_update_rows)
-    RS_TRY(dalloc(&rows_part, update_rows_scratch(m)));
-    RS_TRY(dalloc(&rows_cnt, update_rows_counters(m)));
-    RS_CUDA(cudaMemsetAsync(rows_cnt, 0, update_rows_counters(m) * sizeof(int), st));
-  }
   ws_kind = kind;
   ws_tau = tau;
   ws_ksum = ksum;
@@ -667,7 +658,7 @@ rs_status Problem::enqueue_pipelined_iteration(const rs_solve_opts* o, int slot,
                             sdelta, w, dw, r, dr, m, o->gamma, o->beta, partials, ctrl, st));  // a6+a7
     else   // A S delta from the sketched rows of A
       RS_CUDA(launch_update_rows(A, lda, sq, sw.delta, sdelta, w, dw, r, dr, m, o->gamma, o->beta,
-                                 partials, rows_part, rows_cnt, num_sms, ctrl, st));          // a6+a7
+                                 partials, num_sms, ctrl, st));          // a6+a7
     mark(RS_K_UPDATE, 1);
     return RS_OK;
   }

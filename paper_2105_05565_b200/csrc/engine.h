@@ -107,8 +107,6 @@ struct Problem {
   double* gf_part = nullptr;
   SolveWork sw{};
   double* partials = nullptr;
-  double* rows_part = nullptr;   // EXPLICIT: split partials of k_update_rows
-  int* rows_cnt = nullptr;
   cudaGraphExec_t graph_exec = nullptr;
   GraphKey graph_key{};
   std::vector<cudaEvent_t> prof_events;

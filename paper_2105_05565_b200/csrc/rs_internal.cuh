@@ -259,13 +259,10 @@ cudaError_t launch_gram_fused(const double* X, long long ldx, long long rows, co
                               int slot = 0);
 // explicit A, sketch with few entries (subsample / SubCount):
 //   u_j = sum_e sign_e delta[bucket_e] A[coord_e][j]  (= (A S delta)_j, A symmetric), then the update
-size_t update_rows_scratch(long long m);    // doubles of `upart`
-size_t update_rows_counters(long long m);   // ints of `cnt` (zeroed once; self-resetting)
 cudaError_t launch_update_rows(const double* A, long long lda, const DevSketch& sk,
                                const double* delta, double* sdelta, double* w, double* dw,
                                double* r, double* dr, long long m, double gamma, double beta,
-                               double* partials, double* upart, int* cnt, int num_sms, Ctrl* ctrl,
-                               cudaStream_t st);
+                               double* partials, int num_sms, Ctrl* ctrl, cudaStream_t st);
 // update with a dense u = X^T X S delta:  u_j + lambda sdelta_j  is A S delta
 cudaError_t launch_update_vec(const double* u, double lambda, double* sdelta, double* w, double* dw,
                               double* r, double* dr, long long m, double gamma, double beta,

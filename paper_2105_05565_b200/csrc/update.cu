@@ -401,16 +401,11 @@ cudaError_t update_init() {
                               200 * 1024);
 }
 
-size_t update_rows_scratch(long long m) { return (size_t)RW_MAXS * (size_t)m; }
-size_t update_rows_counters(long long m) { return (size_t)((m + 31) / 32); }
 
 cudaError_t launch_update_rows(const double* A, long long lda, const DevSketch& sk,
                                const double* delta, double* sdelta, double* w, double* dw,
                                double* r, double* dr, long long m, double gamma, double beta,
-                               double* partials, double* upart, int* cnt, int num_sms, Ctrl* ctrl,
-                               cudaStream_t st) {
-  (void)upart;
-  (void)cnt;
+                               double* partials, int num_sms, Ctrl* ctrl, cudaStream_t st) {
   const long long cb = (m + RW_COLS - 1) / RW_COLS;
   // splits (one cluster per column block): about two blocks per SM in total (128 registers per
   // thread), at least 4 rows per warp, at most the portable cluster size

@@ -621,3 +621,45 @@ def test_csr_explicit_config4_full_size(rs):
                    subcount_k=cfg.subcount_k)
     assert rel(it, ref["w"]) <= 1e-10
     assert rel(r, ref["r"]) <= 1e-10
+
+
+# ------------------------------------------------- process-level switches (read once per process)
+_SWITCH_CHILD = r"""
+import sys, numpy as np
+sys.path.insert(0, sys.argv[1])
+import rsinputs
+from paper_2105_05565_b200 import ridgesketch as rs
+X, y = rsinputs.dense_problem(3001, 600, seed=4)
+X, y = X.numpy(), y.numpy()
+out = {}
+for mode, kind, tau, k in [("explicit", "subsample", 300, 0), ("explicit", "subcount", 250, 2),
+                           ("gram", "subsample", 150, 0)]:
+    h = rs.rs_create_dense(X, y, 0.5, mode=mode)
+    w, rep = rs.rs_solve(h, kind, tau, 1.0, 0.5, 0.0, 12, 3, k, check_every=5)
+    _, r = rs.rs_get_state(h)
+    rs.rs_destroy(h)
+    out[f"{mode}_{kind}_w"], out[f"{mode}_{kind}_r"] = w, r
+np.savez(sys.argv[2], **out)
+"""
+
+
+@pytest.mark.parametrize("env", [{"RS_PDL": "0"}, {"RS_BF_RIGHT": "1"}, {}])
+def test_process_switches_parity(tmp_path, env):
+    """The PDL chain off (RS_PDL=0) and the right-looking large-tau factorisation (RS_BF_RIGHT=1)
+    are read once per process: run them in a child and compare with the oracle (tau 300 / 250 > 224
+    use the W = L^{-1} slots; 12 iterations span three check_every chunks)."""
+    import os, subprocess, sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outp = tmp_path / "out.npz"
+    e = dict(os.environ, **env)
+    res = subprocess.run([sys.executable, "-c", _SWITCH_CHILD, root, str(outp)], env=e,
+                         capture_output=True, text=True, timeout=600)
+    assert res.returncode == 0, res.stderr[-2000:]
+    got = np.load(outp)
+    X, y = rsinputs.dense_problem(3001, 600, seed=4)
+    X, y = X.numpy(), y.numpy()
+    for mode, kind, tau, k in [("explicit", "subsample", 300, 0), ("explicit", "subcount", 250, 2),
+                               ("gram", "subsample", 150, 0)]:
+        ref = OV.solve(X, y, 0.5, kind, tau, 1.0, 0.5, 0.0, 12, seed=3, subcount_k=k)
+        assert rel(got[f"{mode}_{kind}_w"], ref["w"]) <= 1e-10, (env, mode, kind)
+        assert rel(got[f"{mode}_{kind}_r"], ref["r"]) <= 1e-10, (env, mode, kind)
