@@ -437,6 +437,7 @@ rs_status Problem::ensure_workspace(int kind, int tau, int ksum, int depth, bool
     }
     if (rows_loc > 0 && !gram_fused) {
       RS_CUDA(tma_gemm_plan(&tg_gram, XS, ld_xs, XS, ld_xs, tau, tau, rows_loc, num_sms));
+      tg_gram.lower = 1;   // G is symmetric and only its lower triangle is read (R12)
       if (tg_gram.work_elems) RS_TRY(dalloc(&gemm_work, tg_gram.work_elems));
       if (std::getenv("RS_VERBOSE"))
         fprintf(stderr, "[rs] gram gemm M=N=%d K=%lld: variant %d (%dx%d), splits %d\n", tau,
