@@ -498,7 +498,8 @@ rs_status Problem::csr_gram_workspace(int kind, int tau) {
   return RS_OK;
 }
 
-rs_status Problem::csr_gram_into(const DevSketch& s, double* G, cudaEvent_t* ev, int slot) {
+rs_status Problem::csr_gram_into(const DevSketch& s, double* G, cudaEvent_t* ev, int slot,
+                                  bool reduce) {
   auto mark = [&](int cls, int edge) {
     if (ev) cudaEventRecordWithFlags(ev[2 * cls + edge], st, cudaEventRecordExternal);
   };
@@ -536,7 +537,7 @@ rs_status Problem::csr_gram_into(const DevSketch& s, double* G, cudaEvent_t* ev,
     mark(RS_K_GRAM, 0);
     RS_CUDA(launch_fill(G, (long long)tau * ld_gram, 0.0, st));
   }
-  RS_TRY(allreduce(G, (size_t)tau * ld_gram));
+  if (reduce) RS_TRY(allreduce(G, (size_t)tau * ld_gram));   // else the caller sums a batch
   mark(RS_K_GRAM, 1);
   return RS_OK;
 }

@@ -612,7 +612,7 @@ rs_status Problem::enqueue_precompute(const rs_solve_opts* o, int ns, cudaEvent_
       const DevSketch sq = skb.at(q);
       double* Gq = Gram_slots + (long long)q * gram_stride;
       if (fmt == 1) {
-        RS_TRY(csr_gram_into(sq, Gq, ev ? ev + (size_t)q * 2 * RS_K_NCLASSES : nullptr, q));
+        RS_TRY(csr_gram_into(sq, Gq, ev ? ev + (size_t)q * 2 * RS_K_NCLASSES : nullptr, q, false));
         continue;
       }
       mark(q, RS_K_GRAM, 0);
@@ -626,9 +626,10 @@ rs_status Problem::enqueue_precompute(const rs_solve_opts* o, int ns, cudaEvent_
       } else {
         RS_CUDA(launch_fill(Gq, gram_stride, 0.0, st));
       }
-      RS_TRY(allreduce(Gq, (size_t)gram_stride));
       mark(q, RS_K_GRAM, 1);
     }
+    // the ns partial Grams of the rank's rows, summed over ranks in ONE collective per group
+    RS_TRY(allreduce(Gram_slots, (size_t)ns * gram_stride));
     src.Gram = Gram_slots;
     src.ld_gram = ld_gram;
     src.gram_stride = gram_stride;

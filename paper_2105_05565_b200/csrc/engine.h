@@ -135,7 +135,8 @@ struct Problem {
   rs_status csr_build_explicit();                              // csr_explicit.cu
   rs_status csr_gram_workspace(int kind, int tau);
   rs_status csr_enqueue_gram(const rs_solve_opts* o, cudaEvent_t* ev);
-  rs_status csr_gram_into(const DevSketch& s, double* G, cudaEvent_t* ev, int slot = 0);   // (R S)^T (R S)
+  rs_status csr_gram_into(const DevSketch& s, double* G, cudaEvent_t* ev, int slot = 0,
+                          bool reduce = true);   // (R S)^T (R S)
   rs_status csr_gram_apply(const double* v, double* u);        // u = R^T (R v), local part
 };
 
