@@ -426,12 +426,13 @@ rs_status Problem::ensure_workspace(int kind, int tau, int ksum, int depth, bool
     if (gram_fused && rows_loc > 0 && !XT && !std::getenv("RS_NO_XT")) {
       // the Gram reads the tau sketched columns as contiguous rows of X^T: built once per
       // problem when it fits next to X (2 GiB margin)
-      const long long ldt = round_up(rows_loc, 4);
+      const long long ldt = round_up(rows_loc, 64);   // zero padding >= one 32-row K chunk
       size_t fr = 0, tot = 0;
       cudaMemGetInfo(&fr, &tot);
       if ((double)m * ldt * 8.0 + 2.0 * (1 << 30) < (double)fr) {
         RS_TRY(dalloc(&XT, (size_t)m * ldt));
         ldxt = ldt;
+        RS_CUDA(cudaMemsetAsync(XT, 0, (size_t)m * ldt * sizeof(double), st));
         RS_CUDA(launch_transpose(X, ldx, rows_loc, m, XT, ldxt, st));
       }
     }

@@ -539,6 +539,112 @@ k_gram_xt(const double* __restrict__ XT, long long ldxt, long long rows, DevSket
   }
 }
 
+// Warp-specialised Gram from X^T (default for the one-pass case): warp 15 is a producer that
+// streams each stage's tau row segments (32 k-values = 256 B each, one cp.async.bulk per row,
+// completion on the stage's "full" mbarrier by transaction count) into a 3-deep ring; the 15
+// consumer warps wait on "full", run their region's DMMA k-steps and release the stage with one
+// arrive each on "empty" -- no CTA-wide barrier in the main loop.  X^T's rows are zero-padded to a
+// multiple of 64, and interior K slices are whole 32-row chunks, so every copy is a full segment.
+constexpr int GW_BK = 32, GW_LDK = 36, GW_STAGES = 3, GW_CONS = 15;
+constexpr int GW_THREADS = (GW_CONS + 1) * 32;
+size_t gram_xtw_smem(int tau) { return (size_t)GW_STAGES * ((tau + 39) / 40 * 40) * GW_LDK * 8; }
+
+__global__ void __launch_bounds__(GW_THREADS, 1)
+k_gram_xtw(const double* __restrict__ XT, long long ldxt, long long rows, DevSketch sk,
+           long long rows_per_cta, double* __restrict__ partials, int slot, const Ctrl* ctrl) {
+  if (slot_unused(ctrl, slot)) return;
+  extern __shared__ __align__(128) double gsm[];   // [GW_STAGES][ng * 40][GW_LDK]
+  __shared__ __align__(8) uint64_t full[GW_STAGES], empty[GW_STAGES];
+  __shared__ int s_col[GF_MAXTAU];
+  const int tau = sk.tau, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int b = tid; b < tau; b += GW_THREADS) s_col[b] = sk.coord[sk.bptr[b]];
+  if (tid == 0) {
+    for (int s = 0; s < GW_STAGES; ++s) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(su32(&full[s])));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(su32(&empty[s])), "r"(GW_CONS));
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+  const long long r0 = (long long)blockIdx.x * rows_per_cta;
+  const long long r1 = min(rows, r0 + rows_per_cta);
+  const int nkb = r0 < r1 ? (int)((r1 - r0 + GW_BK - 1) / GW_BK) : 0;
+  const int ng = (tau + 39) / 40, srows = ng * 40;
+  const int stage_elems = srows * GW_LDK;
+  if (warp == GW_CONS) {   // producer warp
+    for (int kb = 0; kb < nkb; ++kb) {
+      const int s = kb % GW_STAGES;
+      if (kb >= GW_STAGES) xt_wait(&empty[s], ((kb / GW_STAGES) - 1) & 1);
+      if (lane == 0)
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(su32(&full[s])),
+                     "r"((unsigned)(tau * GW_BK * 8)) : "memory");
+      __syncwarp();
+      const long long k0 = r0 + (long long)kb * GW_BK;
+      double* dst = gsm + s * stage_elems;
+      for (int b = lane; b < tau; b += 32)
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n"
+            ::"r"(su32(dst + b * GW_LDK)), "l"(XT + (long long)s_col[b] * ldxt + k0),
+            "r"(GW_BK * 8), "r"(su32(&full[s]))
+            : "memory");
+    }
+    return;
+  }
+  // consumers: region of this warp (I, J), I >= J
+  int I = -1, J = -1;
+  {
+    int t = 0;
+    for (int a = 0; a < ng; ++a)
+      for (int b = 0; b <= a; ++b, ++t)
+        if (t == warp) { I = a; J = b; }
+  }
+  const bool active = I >= 0, diag = I == J;
+  double acc[5][5][2];
+#pragma unroll
+  for (int x = 0; x < 5; ++x)
+#pragma unroll
+    for (int y = 0; y < 5; ++y) acc[x][y][0] = acc[x][y][1] = 0.0;
+  const int kq = lane & 3, mq = lane >> 2;
+  for (int kb = 0; kb < nkb; ++kb) {
+    const int s = kb % GW_STAGES;
+    xt_wait(&full[s], (kb / GW_STAGES) & 1);
+    if (active) {
+      const double* st = gsm + s * stage_elems + mq * GW_LDK + kq;
+      const double* sa = st + (I * 40) * GW_LDK;
+      const double* sb = st + (J * 40) * GW_LDK;
+#pragma unroll
+      for (int kk = 0; kk < GW_BK; kk += 4) {
+        double bf[5];
+#pragma unroll
+        for (int y = 0; y < 5; ++y) bf[y] = sb[y * 8 * GW_LDK + kk];
+#pragma unroll
+        for (int x = 0; x < 5; ++x) {
+          const double af = sa[x * 8 * GW_LDK + kk];
+#pragma unroll
+          for (int y = 0; y < 5; ++y)
+            if (!diag || y <= x) dmma_g(acc[x][y], af, bf[y]);
+        }
+      }
+    }
+    __syncwarp();
+    if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(su32(&empty[s])) : "memory");
+  }
+  if (!active) return;
+  double* out = partials + (long long)blockIdx.x * GF_MAXTAU * GF_MAXTAU;
+#pragma unroll
+  for (int x = 0; x < 5; ++x) {
+    const int a = I * 40 + x * 8 + (lane >> 2);
+#pragma unroll
+    for (int y = 0; y < 5; ++y) {
+      const int b = J * 40 + y * 8 + 2 * (lane & 3);
+      if (a < tau) {
+        if (b < tau) out[a * GF_MAXTAU + b] = acc[x][y][0];
+        if (b + 1 < tau) out[a * GF_MAXTAU + b + 1] = acc[x][y][1];
+      }
+    }
+  }
+}
+
 template <int BK>
 size_t gram_xt_smem(int tau) {
   return (size_t)GxCfg<BK>::STAGES * ((tau + 39) / 40 * 40) * GxCfg<BK>::LDK * 8;
@@ -965,6 +1071,9 @@ cudaError_t gram_init() {
   e = cudaFuncSetAttribute(k_gram_xt<32, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)gram_xt_smem<32>(GF_MAXTAU));
   if (e != cudaSuccess) return e;
+  e = cudaFuncSetAttribute(k_gram_xtw, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)gram_xtw_smem(GF_MAXTAU));
+  if (e != cudaSuccess) return e;
   e = cudaFuncSetAttribute(k_gram_xt<16, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)gram_xt_smem<16>(GF_MAXTAU) / 2);
   if (e != cudaSuccess) return e;
@@ -999,7 +1108,12 @@ cudaError_t launch_gram_xt(const double* XT, long long ldxt, long long rows, con
   const int nc = num_sms;
   const int bk = lean ? 16 : gx_bk();
   const long long rpc = std::max<long long>(bk, ((rows + nc - 1) / nc + bk - 1) / bk * bk);
-  if (lean)   // 8 warps, 3 stages of 16 rows: ~96 KB, leaves room for the lean X pass
+  static const bool no_ws = std::getenv("RS_GX_SYNC") != nullptr;   // A/B: the barrier-synced kernel
+  if (!lean && !no_ws && ldxt % 64 == 0) {
+    const long long rpw = std::max<long long>(GW_BK, ((rows + nc - 1) / nc + GW_BK - 1) / GW_BK * GW_BK);
+    k_gram_xtw<<<nc, GW_THREADS, gram_xtw_smem(sk.tau), st>>>(XT, ldxt, rows, sk, rpw, partials, slot,
+                                                             ctrl);
+  } else if (lean)   // 8 warps, 3 stages of 16 rows: ~96 KB, leaves room for the lean X pass
     k_gram_xt<16, 8><<<nc, 8 * 32, gram_xt_smem<16>(sk.tau) / 2, st>>>(XT, ldxt, rows, sk, rpc,
                                                                        partials, slot, ctrl, kbase);
   else if (bk == 16)
