@@ -14,15 +14,19 @@ $B --config c4 --mode explicit --steps 148 --max-iter-tol 20000 --no-cpu-baselin
 for c in c2 c3 c4; do $B --config $c --steps 148 --max-iter-tol 20000 --no-cpu-baseline --no-e2e --momentum theory > gpurun_out/bench_${c}_theory.json 2>/dev/null; done
 $B --config c5 --mode explicit --steps 148 --max-iter-tol 2000 > gpurun_out/bench_c5_explicit.json 2>/dev/null
 $B --config k1 --steps 148 --max-iter-tol 2000 --no-cpu-baseline > gpurun_out/bench_k1.json 2>/dev/null
+$B --config c5 --mode gram --steps 20 --max-iter-tol 400 --no-cpu-baseline --no-e2e > gpurun_out/bench_c5_gram.json 2>/dev/null
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 600 --csv --log-file gpurun_out/launches_c2_gram.csv python bench.py --steps 10 --warmup 3 --no-e2e --no-cpu-baseline --max-iter-tol 10 > /dev/null 2>&1
 M="--metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum --clock-control none --csv"
 P="python tools/prof_step.py"
-timeout 900 ncu $M -k regex:"k_xpass_rows|k_gram_xt" -c 8 --log-file gpurun_out/tr_c2_gram.csv $P c2 gram 64 > /dev/null 2>&1
+timeout 900 ncu $M -k regex:"k_gram_xt" -c 4 --log-file gpurun_out/tr_c2_gram.csv $P c2 gram 8 > /dev/null 2>&1
+RS_NO_XC=1 timeout 900 ncu $M -k regex:"k_xpass_rows" -c 4 --log-file gpurun_out/tr_c2_gram_xpass.csv $P c2 gram 8 > /dev/null 2>&1
+timeout 900 ncu $M -k regex:"k_spmv" -c 4 --log-file gpurun_out/tr_c4_spmv.csv $P c4 gram 4 > /dev/null 2>&1
 timeout 900 ncu $M -k regex:"k_tn_gemm" -c 4 --log-file gpurun_out/tr_c2_implicit.csv $P c2 implicit 4 > /dev/null 2>&1
 timeout 900 ncu $M -k regex:"k_update_rows|k_bfactor|k_apply_rows" -c 12 --log-file gpurun_out/tr_c2_explicit.csv $P c2 explicit 64 > /dev/null 2>&1
 for c in c3 c4; do timeout 900 ncu $M -k regex:"k_gram_bands|k_hash_rows|k_spmv" -c 12 --log-file gpurun_out/tr_$c.csv $P $c gram 4 > /dev/null 2>&1; done
 timeout 900 ncu $M -k regex:"k_update_rows|k_apply_rows" -c 8 --log-file gpurun_out/tr_c4_explicit.csv $P c4 explicit 16 > /dev/null 2>&1
 timeout 900 ncu $M -k regex:"k_bfactor|k_update_rows|k_apply_rows" -c 9 --log-file gpurun_out/tr_c5_explicit.csv $P c5 explicit 150 > /dev/null 2>&1
 timeout 900 ncu $M -k regex:"k_bfactor|k_update_rows|k_apply_rows" -c 9 --log-file gpurun_out/tr_k1.csv $P k1 explicit 150 > /dev/null 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_xpass_rows|k_gram_xt" -c 2 -o gpurun_out/prof_c2_gram_full $P c2 gram 64 > /dev/null 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_gram_xtw" -c 1 -o gpurun_out/prof_c2_gram_full $P c2 gram 8 > /dev/null 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_xpass_rows" -c 1 -o gpurun_out/prof_c2_xpass_full $P c2 gram 8 > /dev/null 2>&1
 ls gpurun_out/
