@@ -40,22 +40,52 @@ def _peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks and throttle reasons sampled every 200 ms during the timed region."""
+    """SM clocks and clock-event (throttle) reasons sampled every 50 ms during the timed region, in
+    process through NVML (pynvml) from a background thread: no nvidia-smi process whose start-up or
+    driver queries could stall the timed region's host-side launches.  Falls back to nvidia-smi."""
 
     FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    NAMES = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
 
     def __init__(self, device):
         self.device = device
         self.proc = None
+        self.samples = []   # (sm_mhz, max_mhz, set of reasons)
+        self.lines = []
+
+    def _nvml_loop(self, nv, h):
+        bits = {"hw_slowdown": nv.nvmlClocksEventReasonHwSlowdown,
+                "hw_thermal_slowdown": nv.nvmlClocksEventReasonHwThermalSlowdown,
+                "sw_thermal_slowdown": nv.nvmlClocksEventReasonSwThermalSlowdown,
+                "sw_power_cap": nv.nvmlClocksEventReasonSwPowerCap}
+        mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+        while True:
+            try:
+                sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+                rs = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+                self.samples.append((float(sm), float(mx), {k for k, v in bits.items() if rs & v}))
+            except Exception:
+                pass
+            self._first.set()
+            if self._stop.wait(0.05):
+                break
 
     def __enter__(self):
-        # the sampler's own start-up (NVML init) must not overlap the timed region: wait for its
-        # first sample before returning; lines are collected by a reader thread
         import threading
-        self.lines = []
+        self._first, self._stop = threading.Event(), threading.Event()
         try:
+            import pynvml as nv
+            nv.nvmlInit()
+            h = nv.nvmlDeviceGetHandleByIndex(self.device)
+            self.thread = threading.Thread(target=self._nvml_loop, args=(nv, h), daemon=True)
+            self.thread.start()
+            self._first.wait(timeout=5.0)
+            return self
+        except Exception:
+            self.thread = None
+        try:   # fallback: nvidia-smi, started (and first sample taken) before the region
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
                  "--format=csv,noheader,nounits", "-lms", "200"],
@@ -63,22 +93,25 @@ class ClockSampler:
         except Exception:
             self.proc = None
             return self
-        first = threading.Event()
 
         def reader():
             for ln in self.proc.stdout:
                 if ln.strip():
                     self.lines.append(ln)
-                    first.set()
-            first.set()
+                    self._first.set()
+            self._first.set()
 
         self.thread = threading.Thread(target=reader, daemon=True)
         self.thread.start()
-        first.wait(timeout=5.0)
-        self.n_before = len(self.lines)
+        self._first.wait(timeout=5.0)
         return self
 
     def __exit__(self, *a):
+        if self.proc is None and self.thread is not None:
+            time.sleep(0.06)
+            self._stop.set()
+            self.thread.join(timeout=5)
+            return
         if self.proc is not None:
             time.sleep(0.25)
             self.proc.terminate()
@@ -90,8 +123,11 @@ class ClockSampler:
 
     def summary(self):
         sm, mx, reasons = [], None, set()
-        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
-        for ln in getattr(self, "lines", []):
+        for s_mhz, m_mhz, rs in self.samples:
+            sm.append(s_mhz)
+            mx = m_mhz
+            reasons |= rs
+        for ln in self.lines:
             p = [t.strip() for t in ln.split(",")]
             if len(p) < 8:
                 continue
@@ -100,11 +136,12 @@ class ClockSampler:
                 mx = float(p[1])
             except ValueError:
                 continue
-            for nm, v in zip(names, p[4:8]):
+            for nm, v in zip(self.NAMES, p[4:8]):
                 if v.lower().startswith("active"):
                     reasons.add(nm)
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
-                "reasons": sorted(reasons), "samples": len(sm)}
+                "reasons": sorted(reasons), "samples": len(sm),
+                "source": "nvml" if self.samples else "nvidia-smi"}
 
 
 def _dist_env():

@@ -315,8 +315,15 @@ template <int MODE>
 __global__ void __launch_bounds__(AG_WARPS * 32)
 k_apply_rows(const double* __restrict__ Mx, long long ldm, DevSketch sk, const int* __restrict__ flag,
              const double* __restrict__ x, const double* __restrict__ r, double* __restrict__ out,
-             double* __restrict__ sdelta, Ctrl* ctrl) {
+             double* __restrict__ sdelta, Ctrl* ctrl, const double* __restrict__ pfA, long long pf_lda,
+             unsigned pf_bytes) {
   pdl_trigger();
+  if (pfA && threadIdx.x < 32) {   // EXPLICIT: pull this iteration's sketched rows of A into L2 for
+    // the update kernel at the end of the chain (static data; one bulk prefetch per row)
+    for (int e = blockIdx.x * 32 + threadIdx.x; e < sk.len; e += gridDim.x * 32)
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(pfA + (long long)sk.coord[e] * pf_lda),
+                   "r"(pf_bytes) : "memory");
+  }
   extern __shared__ double xs[];     // [tau] x, then (fused g) s_bp[tau + 1], s_ce[len]
   __shared__ double red[AG_WARPS];
   const int bad = *flag;    // factor slot not SPD (static)
@@ -1011,7 +1018,12 @@ cudaError_t launch_bfactor(const FactorSrc& src, const DevSketch& skb, int nslot
 
 cudaError_t launch_apply_ginv(const double* Ginv, long long ldgi, const DevSketch& sk,
                               const int* flag, const double* r, double* gbuf, double* delta,
-                              double* sdelta, Ctrl* ctrl, cudaStream_t st, bool first) {
+                              double* sdelta, Ctrl* ctrl, cudaStream_t st, bool first,
+                              const double* pfA, long long pf_lda, long long pf_m) {
+  // L2 prefetch of the sketched rows of A only while they fit comfortably in the 126 MB L2
+  static const bool no_pf = std::getenv("RS_NO_L2PF") != nullptr;
+  if (no_pf || !pfA || (double)sk.len * pf_m * 8.0 > 48e6) pfA = nullptr;
+  const unsigned pf_bytes = (unsigned)(((pf_m * 8) + 15) / 16 * 16);
   if (sk.tau > AG_MAXTAU) return cudaErrorInvalidValue;
   // few entries per bucket (subsample, SubCount): g = S^T r is formed inside the first GEMV kernel
   const bool fuse = sk.len <= 8 * sk.tau && sk.len <= AP_MAXFUSE;
@@ -1025,23 +1037,24 @@ cudaError_t launch_apply_ginv(const double* Ginv, long long ldgi, const DevSketc
     first = false;   // k_sketch_g is the ordinary launch of the chain
   }
   // the first kernel of a group follows the factorisation that wrote the slot: ordinary launch
-  auto launch = [&](auto kern, const double* xin, double* out) {
+  auto launch = [&](auto kern, const double* xin, double* out, const double* pf) {
     const dim3 grid((unsigned)((sk.tau + AP_ROWS - 1) / AP_ROWS)), blk(AG_WARPS * 32);
     const size_t smem = (size_t)sk.tau * 8 + (xin ? 0 : (size_t)(sk.tau + 1 + sk.len) * 4);
     if (first) {
-      kern<<<grid, blk, smem, st>>>(Ginv, ldgi, sk, flag, xin, r, out, sdelta, ctrl);
+      kern<<<grid, blk, smem, st>>>(Ginv, ldgi, sk, flag, xin, r, out, sdelta, ctrl, pf, pf_lda, pf_bytes);
       return cudaGetLastError();
     }
-    return launch_pdl(kern, grid, blk, smem, st, Ginv, ldgi, sk, flag, xin, r, out, sdelta, ctrl);
+    return launch_pdl(kern, grid, blk, smem, st, Ginv, ldgi, sk, flag, xin, r, out, sdelta, ctrl, pf,
+                      pf_lda, pf_bytes);
   };
   if (sk.tau > BF_MAXTAU) {   // slot holds W = L^{-1} (lower) and W^T (upper): delta = W^T (W g)
     double* tv = gbuf + sk.tau;
-    const cudaError_t e = launch(k_apply_rows<AP_LOWER>, gv, tv);
+    const cudaError_t e = launch(k_apply_rows<AP_LOWER>, gv, tv, pfA);
     if (e != cudaSuccess) return e;
     first = false;
-    return launch(k_apply_rows<AP_UPPER>, (const double*)tv, delta);
+    return launch(k_apply_rows<AP_UPPER>, (const double*)tv, delta, (const double*)nullptr);
   }
-  return launch(k_apply_rows<AP_FULL>, gv, delta);
+  return launch(k_apply_rows<AP_FULL>, gv, delta, pfA);
 }
 
 bool pdl_enabled() {

@@ -651,8 +651,10 @@ rs_status Problem::enqueue_pipelined_iteration(const rs_solve_opts* o, int slot,
   const DevSketch sq = skb.at(slot);
   mark(RS_K_SOLVE, 0);
   // slot 0 follows the group's factorisation (ordinary launch); later slots chain by PDL
+  const bool rows_of_A = mode == RS_AS_EXPLICIT && !ASt_slots;   // k_update_rows reads A rows
   RS_CUDA(launch_apply_ginv(Ginv_slots + (long long)slot * gi_stride, ld_gi, sq, slot_flags + slot,
-                            r, sw.Gx, sw.delta, sdelta, ctrl, st, slot == 0));    // a4 + a5
+                            r, sw.Gx, sw.delta, sdelta, ctrl, st, slot == 0,
+                            rows_of_A ? A : nullptr, lda, m));                     // a4 + a5
   mark(RS_K_SOLVE, 1);
   if (mode == RS_AS_EXPLICIT) {
     mark(RS_K_UPDATE, 0);

@@ -296,7 +296,8 @@ cudaError_t launch_bfactor(const FactorSrc& src, const DevSketch& skb, int nslot
 // delta = W^T (W g).  gbuf: 2 tau doubles of scratch (g, W g).
 cudaError_t launch_apply_ginv(const double* Ginv, long long ldgi, const DevSketch& sk,
                               const int* flag, const double* r, double* gbuf, double* delta,
-                              double* sdelta, Ctrl* ctrl, cudaStream_t st, bool first = true);
+                              double* sdelta, Ctrl* ctrl, cudaStream_t st, bool first = true,
+                              const double* pfA = nullptr, long long pf_lda = 0, long long pf_m = 0);
 
 // misc
 // *out += number of non-finite entries of the rows x cols block.
