@@ -127,14 +127,17 @@ k_hash_rows(const long long* __restrict__ ptr, const int* __restrict__ idx,
     for (int j = 0; j < nr; ++j) {
       const long long a = __shfl_sync(FULL, pa, j), e = __shfl_sync(FULL, pe, j);
       if (e - a > heavy) continue;   // k_hash_rows_heavy
-      for (long long base = a; base < e; base += 64) {
+      bool touched = false;   // rows with no sketched entry (most of a dual R under SubCount) skip
+      for (long long base = a; base < e; base += 64) {   // the merge and its flush
         const long long t0 = base + lane, t1 = base + 32 + lane;
         const int cm0 = cm_of(cmap, idx, t0, e), cm1 = cm_of(cmap, idx, t1, e);
+        if (!__ballot_sync(FULL, cm0 >= 0 || cm1 >= 0)) continue;
+        touched = true;
         const double v0 = cm0 >= 0 ? val[t0] : 0.0, v1 = cm1 >= 0 ? val[t1] : 0.0;
         M.add(cm0, (cm0 & 1) ? -v0 : v0, lane);
         M.add(cm1, (cm1 & 1) ? -v1 : v1, lane);
       }
-      const int total = M.flush(a, hb, hv, lane);
+      const int total = touched ? M.flush(a, hb, hv, lane) : 0;
       if (lane == 0) hcnt[i0 + j] = total;
     }
   }
