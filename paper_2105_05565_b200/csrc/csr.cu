@@ -76,6 +76,13 @@ __global__ void k_csc_fill(const int* perm, const int* row_of, const double* val
   }
 }
 
+// inv[perm[q]] = q
+__global__ void k_inv_perm(const int* perm, int* inv, long long n) {
+  for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < n;
+       q += (long long)gridDim.x * blockDim.x)
+    inv[perm[q]] = (int)q;
+}
+
 // colptr[c] = first q with sorted_col[q] >= c  (binary search), c in [0, cols]
 __global__ void k_colptr(const int* sorted_col, long long nnz, long long cols, long long* colptr) {
   for (long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x; c <= cols;
@@ -270,6 +277,7 @@ void Problem::csr_free() {
   dfree(csr->rowidx);
   dfree(csr->cvals);
   dfree(csr->cmap_all);
+  dfree(csr->cscpos);
   delete csr;
   csr = nullptr;
 }
@@ -481,6 +489,11 @@ rs_status create_csr(rs_problem* out, int64_t n, int64_t d, int64_t nnz_local, c
     cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, c->colidx, keys_out, perm_in, perm_out,
                                     (int)nnz_local, 0, end_bit, st);
     k_csc_fill<<<4096, 256, 0, st>>>(perm_out, row_of, c->vals, c->rowidx, c->cvals, nnz_local);
+    if (rt == 2 && mode == RS_AS_GRAM && nnz_local > 0) {   // R entry of every X entry (csr_gram.cu)
+      s = dalloc(&c->cscpos, nnz_local);
+      if (s != RS_OK) return guard(s);
+      k_inv_perm<<<4096, 256, 0, st>>>(perm_out, c->cscpos, nnz_local);
+    }
     k_colptr<<<(unsigned)std::min<long long>((cols + 256) / 256, 65535), 256, 0, st>>>(keys_out, nnz_local, cols, c->colptr);
     cudaMemcpyAsync(&c->max_row_nnz, mx, 8, cudaMemcpyDeviceToHost, st);
     cudaError_t ce = cudaStreamSynchronize(st);

@@ -37,6 +37,14 @@ struct CsrData {
   int* heavy_rowsRt = nullptr;
   int nheavyR = 0, nheavyRt = 0;
   int* chunk_h0 = nullptr;       // [nchunks + 1] first heavy row (sorted list) of every chunk
+  // dual GRAM with a subsample / SubCount sketch: R = X^T rows are formed from the s selected
+  // samples only.  cscpos[p] = R (CSC) position of X's CSR entry p; cmR[q] = (bucket << 1 | neg)
+  // of R entry q for this sketch, else -1; tflag / tlist / tcount: the touched R rows
+  int* cscpos = nullptr;
+  int* cmR = nullptr;
+  int* tflag = nullptr;
+  int* tlist = nullptr;
+  int* tcount = nullptr;
   size_t hr_smem = 0, gb_smem = 0;
 };
 

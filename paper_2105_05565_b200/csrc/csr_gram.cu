@@ -188,6 +188,105 @@ k_hash_rows_heavy(const long long* __restrict__ ptr, const int* __restrict__ idx
   }
 }
 
+// ---------------------------------------------------------------- stage 1, selected samples (dual)
+// Dual route with a subsample / SubCount sketch: only the s selected samples (rows of X) carry
+// sketched entries.  k_sel_emit walks their X rows (s x ~nnz/row entries instead of all of R) and
+// marks each entry's position in R = X^T with its (bucket << 1 | neg) code, collecting the touched
+// R rows; k_sel_merge then merges every touched light row exactly like k_hash_rows (same R order,
+// same lane order: bit-identical rows of R S) reading the codes contiguously, and resets them.
+__global__ void __launch_bounds__(256)
+k_sel_emit(DevSketch sk, const long long* __restrict__ rowptr, const int* __restrict__ colidx,
+           const int* __restrict__ cscpos, int* __restrict__ cmR, int* __restrict__ tflag,
+           int* __restrict__ tlist, int* __restrict__ tcount, int slot, const Ctrl* ctrl) {
+  if (slot_unused(ctrl, slot)) return;
+  const int lane = threadIdx.x & 31;
+  const int e = blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (e >= sk.len) return;
+  const int i = sk.coord[e];
+  const int code = (sk.bucket[e] << 1) | (sk.sign[e] > 0 ? 0 : 1);
+  for (long long p = rowptr[i] + lane; p < rowptr[i + 1]; p += 32) {
+    cmR[cscpos[p]] = code;
+    const int f = colidx[p];
+    if (atomicExch(&tflag[f], 1) == 0) tlist[atomicAdd(tcount, 1)] = f;
+  }
+}
+
+__global__ void __launch_bounds__(HR_WARPS * 32)
+k_sel_merge(const long long* __restrict__ ptr, const double* __restrict__ val, long long heavy,
+            int* __restrict__ cmR, int* __restrict__ tflag, const int* __restrict__ tlist,
+            const int* __restrict__ tcount, int tau, int* __restrict__ hb, double* __restrict__ hv,
+            int* __restrict__ hcnt, int slot, const Ctrl* ctrl) {
+  if (slot_unused(ctrl, slot)) return;
+  extern __shared__ double hsm[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  WarpMerge M(hsm, tau, warp);
+  for (int q = lane; q < M.nw; q += 32) M.bits[q] = 0u;
+  __syncwarp();
+  const int nt = *tcount;
+  for (int k = blockIdx.x * HR_WARPS + warp; k < nt; k += gridDim.x * HR_WARPS) {
+    const int f = tlist[k];
+    if (lane == 0) tflag[f] = 0;
+    const long long a = ptr[f], e = ptr[f + 1];
+    if (e - a > heavy) continue;   // heavy rows: k_sel_heavy
+    for (long long base = a; base < e; base += 64) {
+      const long long t0 = base + lane, t1 = base + 32 + lane;
+      const int cm0 = t0 < e ? cmR[t0] : -1, cm1 = t1 < e ? cmR[t1] : -1;
+      if (!__ballot_sync(FULL, cm0 >= 0 || cm1 >= 0)) continue;
+      const double v0 = cm0 >= 0 ? val[t0] : 0.0, v1 = cm1 >= 0 ? val[t1] : 0.0;
+      M.add(cm0, (cm0 & 1) ? -v0 : v0, lane);
+      M.add(cm1, (cm1 & 1) ? -v1 : v1, lane);
+      if (cm0 >= 0) cmR[t0] = -1;
+      if (cm1 >= 0) cmR[t1] = -1;
+    }
+    const int total = M.flush(a, hb, hv, lane);
+    if (lane == 0) hcnt[f] = total;
+  }
+}
+
+// heavy rows (all of them: Zipf-popular features are touched by nearly every sketch): one CTA per
+// row, codes read from cmR (and reset), warps merged in warp order as in k_hash_rows_heavy
+__global__ void __launch_bounds__(HR_WARPS * 32)
+k_sel_heavy(const long long* __restrict__ ptr, const double* __restrict__ val,
+            const int* __restrict__ heavy_rows, int* __restrict__ cmR, int tau, int* __restrict__ hb,
+            double* __restrict__ hv, int* __restrict__ hcnt, int slot, const Ctrl* ctrl) {
+  if (slot_unused(ctrl, slot)) return;
+  extern __shared__ double hsm[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  WarpMerge M(hsm, tau, warp);
+  for (int q = lane; q < M.nw; q += 32) M.bits[q] = 0u;
+  __syncwarp();
+  const long long i = heavy_rows[blockIdx.x];
+  const long long a = ptr[i], e = ptr[i + 1];
+  for (long long base = a + 32LL * warp; base < e; base += 32LL * HR_WARPS) {
+    const long long t = base + lane;
+    const int cm = t < e ? cmR[t] : -1;
+    if (!__ballot_sync(FULL, cm >= 0)) continue;
+    const double v = cm >= 0 ? val[t] : 0.0;
+    M.add(cm, (cm & 1) ? -v : v, lane);
+    if (cm >= 0) cmR[t] = -1;
+  }
+  __syncthreads();
+  WarpMerge M0(hsm, tau, 0);
+  for (int b = threadIdx.x; b < tau; b += HR_WARPS * 32) {
+    double s = 0.0;
+    bool any = false;
+    for (int w = 0; w < HR_WARPS; ++w) {
+      WarpMerge Mw(hsm, tau, w);
+      if (Mw.bits[b >> 5] & (1u << (b & 31))) {
+        s += Mw.acc[b];
+        any = true;
+      }
+    }
+    M0.acc[b] = s;
+    if (any) atomicOr(&M0.bits[b >> 5], 1u << (b & 31));
+  }
+  __syncthreads();
+  if (warp == 0) {
+    const int total = M.flush(a, hb, hv, lane);
+    if (lane == 0) hcnt[i] = total;
+  }
+}
+
 // ------------------------------------------------------------------------------------ stage 2
 __global__ void __launch_bounds__(GB_THREADS, 1)
 k_gram_bands(const long long* __restrict__ ptr, const int* __restrict__ hcnt,
@@ -391,6 +490,11 @@ void Problem::csr_gram_free() {
   dfree(csr->heavy_rowsRt);
   dfree(csr->chunk_h0);
   csr->chunk_h0 = nullptr;
+  dfree(csr->cmR);
+  dfree(csr->tflag);
+  dfree(csr->tlist);
+  dfree(csr->tcount);
+  csr->cmR = csr->tflag = csr->tlist = csr->tcount = nullptr;
   csr->heavy_rowsR = csr->heavy_rowsRt = nullptr;
   csr->nheavyR = csr->nheavyRt = 0;
   csr->hb = nullptr;
@@ -409,6 +513,15 @@ rs_status Problem::csr_gram_workspace(int kind, int tau) {
   const RView R = route == 1 ? RView{c->rowptr, c->colidx, c->vals, c->rows}
                              : RView{c->colptr, c->rowidx, c->cvals, c->cols};
   if (kind != SK_COUNT) RS_TRY(dalloc(&c->cmap_all, m));
+  if (route == 2 && kind != SK_COUNT && c->cscpos && !std::getenv("RS_NO_SELROWS")) {
+    RS_TRY(dalloc(&c->cmR, std::max<long long>(1, c->nnz)));
+    RS_TRY(dalloc(&c->tflag, std::max<long long>(1, R.rows)));
+    RS_TRY(dalloc(&c->tlist, std::max<long long>(1, R.rows)));
+    RS_TRY(dalloc(&c->tcount, 1));
+    RS_CUDA(cudaMemsetAsync(c->cmR, 0xFF, std::max<long long>(1, c->nnz) * sizeof(int), st));
+    RS_CUDA(cudaMemsetAsync(c->tflag, 0, std::max<long long>(1, R.rows) * sizeof(int), st));
+    RS_CUDA(cudaMemsetAsync(c->tcount, 0, sizeof(int), st));
+  }
   RS_TRY(dalloc(&c->hb, c->nnz));
   RS_TRY(dalloc(&c->hv, c->nnz));
   RS_TRY(dalloc(&c->hcnt, R.rows));
@@ -512,11 +625,25 @@ rs_status Problem::csr_gram_into(const DevSketch& s, double* G, cudaEvent_t* ev,
   const int tau = s.tau;
   const int* cmap = s.cmap;
   mark(RS_K_XS, 0);
-  if (s.kind != SK_COUNT) {
+  const bool sel = s.kind != SK_COUNT && c->cmR != nullptr;   // dual: from the selected samples
+  if (s.kind != SK_COUNT && !sel) {
     RS_CUDA(launch_cmap_build(s, c->cmap_all, m, ctrl, st, slot));
     cmap = c->cmap_all;
   }
-  if (R.rows > 0) {   // a2: rows of R S, merged and bucket-sorted
+  if (R.rows > 0 && sel) {   // a2: rows of R S from the s selected rows of X
+    RS_CUDA(cudaMemsetAsync(c->hcnt, 0, R.rows * sizeof(int), st));
+    k_sel_emit<<<(unsigned)std::max(1, (s.len + 7) / 8), 256, 0, st>>>(
+        s, c->rowptr, c->colidx, c->cscpos, c->cmR, c->tflag, c->tlist, c->tcount, slot, ctrl);
+    const unsigned grid = (unsigned)((long long)num_sms * 8);
+    k_sel_merge<<<grid, HR_WARPS * 32, c->hr_smem, st>>>(R.ptr, R.val, c->heavyR, c->cmR, c->tflag,
+                                                         c->tlist, c->tcount, tau, c->hb, c->hv,
+                                                         c->hcnt, slot, ctrl);
+    if (c->nheavyR > 0)
+      k_sel_heavy<<<c->nheavyR, HR_WARPS * 32, c->hr_smem, st>>>(
+          R.ptr, R.val, c->heavy_rowsR, c->cmR, tau, c->hb, c->hv, c->hcnt, slot, ctrl);
+    RS_CUDA(cudaMemsetAsync(c->tcount, 0, sizeof(int), st));
+    RS_CUDA(cudaGetLastError());
+  } else if (R.rows > 0) {   // a2: rows of R S, merged and bucket-sorted
     const unsigned grid = (unsigned)std::max<long long>(
         1, std::min<long long>((R.rows + HR_WARPS - 1) / HR_WARPS, (long long)num_sms * 8));
     k_hash_rows<<<grid, HR_WARPS * 32, c->hr_smem, st>>>(R.ptr, R.idx, R.val, R.rows, c->heavyR,
@@ -525,6 +652,8 @@ rs_status Problem::csr_gram_into(const DevSketch& s, double* G, cudaEvent_t* ev,
       k_hash_rows_heavy<<<c->nheavyR, HR_WARPS * 32, c->hr_smem, st>>>(
           R.ptr, R.idx, R.val, c->heavy_rowsR, cmap, tau, c->hb, c->hv, c->hcnt, slot, ctrl);
     RS_CUDA(cudaGetLastError());
+  }
+  if (R.rows > 0) {
     mark(RS_K_XS, 1);
     mark(RS_K_GRAM, 0);
     // a3/a4: (R S)^T (R S), lower triangle
