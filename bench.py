@@ -270,7 +270,14 @@ def _csr_pairs(rs, cfg, host):
     keep = b >= 0
     key = np.unique(r[keep] * cfg.tau + b[keep])
     L = np.bincount(key // cfg.tau)
-    return int(key.size), int((L * (L + 1) // 2).sum())
+    sel = None
+    if dual and cfg.sketch != "count":
+        # selected-row path (k_sel_emit / k_sel_merge): the X entries of the s selected samples,
+        # and the entries of every R row (feature) they touch (the code scan)
+        feat_nnz = np.bincount(ci, minlength=cfg.d)
+        touched = np.unique(ci[keep])
+        sel = (int(keep.sum()), int(feat_nnz[touched].sum()))
+    return int(key.size), int((L * (L + 1) // 2).sum()), sel
 
 
 def _roofline(args, cfg, world, kms, kl, dom, prof_ms, host, rs):
@@ -336,7 +343,7 @@ def _roofline(args, cfg, world, kms, kl, dom, prof_ms, host, rs):
         nnz = int(host[0][-1])
         m = cfg.d if cfg.d <= cfg.n else cfg.n
         if args.mode == "gram" and dom in ("gram", "xs"):
-            ent, pairs = _csr_pairs(rs, cfg, host)
+            ent, pairs, sel = _csr_pairs(rs, cfg, host)
             if dom == "gram":
                 w = pairs * 16.0 / world
                 roof = dict(kernel="k_gram_bands: G_lower += v_i v_i^T over the merged rows of R S "
@@ -346,6 +353,18 @@ def _roofline(args, cfg, world, kms, kl, dom, prof_ms, host, rs):
                                         "(B200_PROFILING.md unit counts and clocks)",
                             algorithmic_per_launch=f"{w:.3e} bytes (16 B x {pairs:.3e} pair "
                                                    f"updates, sketch of iteration 0)")
+            elif sel is not None:   # dual, subsample / SubCount: the selected-row path
+                se, tn = sel
+                rows_r = cfg.d
+                w = (se * 12.0 + tn * 4.0 + ent * 20.0 + rows_r * 4.0) / world
+                roof = dict(kernel="k_sel_emit + k_sel_merge + k_sel_heavy: rows of R S from the s "
+                                   "selected samples", bound="hbm",
+                            achieved=w / (ms * 1e-3) / 1e9, peak=hbm, unit="GB/s",
+                            peak_source=hbm_src,
+                            algorithmic_per_launch=f"{w:.3e} bytes ({se:.3e} selected X entries x "
+                                                   f"12 B, {tn:.3e} codes of the touched R rows x "
+                                                   f"4 B, {ent:.3e} merged entries x 20 B, hcnt "
+                                                   f"reset)")
             else:
                 w = (nnz * 16.0 + ent * 12.0) / world
                 roof = dict(kernel="k_hash_rows: rows of R S, merged and bucket-sorted", bound="hbm",

@@ -23,7 +23,7 @@ RS_NO_XC=1 timeout 900 ncu $M -k regex:"k_xpass_rows" -c 4 --log-file gpurun_out
 timeout 900 ncu $M -k regex:"k_spmv" -c 4 --log-file gpurun_out/tr_c4_spmv.csv $P c4 gram 4 > /dev/null 2>&1
 timeout 900 ncu $M -k regex:"k_tn_gemm" -c 4 --log-file gpurun_out/tr_c2_implicit.csv $P c2 implicit 4 > /dev/null 2>&1
 timeout 900 ncu $M -k regex:"k_update_rows|k_bfactor|k_apply_rows" -c 12 --log-file gpurun_out/tr_c2_explicit.csv $P c2 explicit 64 > /dev/null 2>&1
-for c in c3 c4; do timeout 900 ncu $M -k regex:"k_gram_bands|k_hash_rows|k_spmv" -c 12 --log-file gpurun_out/tr_$c.csv $P $c gram 4 > /dev/null 2>&1; done
+for c in c3 c4; do timeout 900 ncu $M -k regex:"k_gram_bands|k_hash_rows|k_sel_|k_spmv" -c 12 --log-file gpurun_out/tr_$c.csv $P $c gram 4 > /dev/null 2>&1; done
 timeout 900 ncu $M -k regex:"k_update_rows|k_apply_rows" -c 8 --log-file gpurun_out/tr_c4_explicit.csv $P c4 explicit 16 > /dev/null 2>&1
 timeout 900 ncu $M -k regex:"k_bfactor|k_update_rows|k_apply_rows" -c 9 --log-file gpurun_out/tr_c5_explicit.csv $P c5 explicit 150 > /dev/null 2>&1
 timeout 900 ncu $M -k regex:"k_bfactor|k_update_rows|k_apply_rows" -c 9 --log-file gpurun_out/tr_k1.csv $P k1 explicit 150 > /dev/null 2>&1
