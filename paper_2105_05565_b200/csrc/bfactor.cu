@@ -698,18 +698,18 @@ k_bfactor_lp(FactorSrc src, DevSketch skb, double* __restrict__ Ginv, long long 
       double* dst = Wm + (long long)a * tp;
       const bool single = sk.len == tau;   // subsample: exactly one entry per bucket
       const int n = a + 1;                 // columns c <= a (< tau)
-      if (single) {   // batches of 8 independent gathers per lane
-        for (int c0 = lane; c0 < n; c0 += 8 * 32) {
-          double x[8];
+      if (single) {   // batches of 32 independent gathers per lane (one batch for n <= 1024)
+        for (int c0 = lane; c0 < n; c0 += 32 * 32) {
+          double x[32];
 #pragma unroll
-          for (int u = 0; u < 8; ++u) {
+          for (int u = 0; u < 32; ++u) {
             const int c = c0 + 32 * u;
             const int cf = c < n ? s_ce[c] : 0;
             x[u] = c < n ? __ldg(Ae + (cf >= 0 ? cf : ~cf)) : 0.0;
             if (cf < 0) x[u] = -x[u];
           }
 #pragma unroll
-          for (int u = 0; u < 8; ++u) {
+          for (int u = 0; u < 32; ++u) {
             const int c = c0 + 32 * u;
             if (c < n) dst[c] = sa * x[u];
           }
@@ -951,9 +951,13 @@ k_bfactor_lp(FactorSrc src, DevSketch skb, double* __restrict__ Ginv, long long 
     int I, J;
     tri_decode(t, I, J);
     if (32 * J >= tau) continue;
+    double xr[32];   // the whole tile in flight first: 32 independent loads per lane
+#pragma unroll
+    for (int rr = 0; rr < 32; ++rr) xr[rr] = T(I, J)[(long long)rr * tp + lane];
+#pragma unroll
     for (int rr = 0; rr < 32; ++rr) {
       const int row = 32 * I + rr, col = 32 * J + lane;
-      const double x = (row < tau && col <= row) ? T(I, J)[(long long)rr * tp + lane] : 0.0;
+      const double x = (row < tau && col <= row) ? xr[rr] : 0.0;
       tt[rr * 33 + lane] = x;
       if (row < tau && col <= row) Gi[(long long)row * ldgi + col] = x;
     }
