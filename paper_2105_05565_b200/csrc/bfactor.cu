@@ -415,7 +415,7 @@ template <bool TA, bool TB>
 __device__ __forceinline__ void mma_tile(double (&acc)[4][4][2], const double* A, int lda,
                                          const double* B, int ldb, int lane, double sign) {
   const int q = lane >> 2, k4 = lane & 3;
-#pragma unroll 2
+#pragma unroll 4
   for (int K = 0; K < 8; ++K) {
     double a[4], b[4];
 #pragma unroll
@@ -440,9 +440,9 @@ __device__ __forceinline__ void acc_load(double (&acc)[4][4][2], const double* C
   for (int R = 0; R < 4; ++R)
 #pragma unroll
     for (int C = 0; C < 4; ++C) {
-      const double* p = Ct + (long long)(8 * R + q) * ld + 8 * C + 2 * k4;
-      acc[R][C][0] = p[0];
-      acc[R][C][1] = p[1];
+      const double2 v = *reinterpret_cast<const double2*>(Ct + (long long)(8 * R + q) * ld + 8 * C + 2 * k4);
+      acc[R][C][0] = v.x;
+      acc[R][C][1] = v.y;
     }
 }
 __device__ __forceinline__ void acc_zero(double (&acc)[4][4][2]) {
@@ -457,9 +457,8 @@ __device__ __forceinline__ void acc_store(const double (&acc)[4][4][2], double* 
   for (int R = 0; R < 4; ++R)
 #pragma unroll
     for (int C = 0; C < 4; ++C) {
-      double* p = Ct + (long long)(8 * R + q) * ld + 8 * C + 2 * k4;
-      p[0] = acc[R][C][0];
-      p[1] = acc[R][C][1];
+      *reinterpret_cast<double2*>(Ct + (long long)(8 * R + q) * ld + 8 * C + 2 * k4) =
+          make_double2(acc[R][C][0], acc[R][C][1]);
     }
 }
 
@@ -825,6 +824,16 @@ k_bfactor_lp(FactorSrc src, DevSketch skb, double* __restrict__ Ginv, long long 
   // store half h of the strip accumulator (8 x 8 blocks C = 4h .. 4h+3) to a 32 x 32 tile,
   // optionally as base - acc
   auto store_half = [&](int h, double* Ct, int ld, const double* base, int ldb) {
+    // base (may alias Ct) is read in full before the first store: one batch of 16 double2 loads
+    // instead of 16 load -> store round trips
+    double2 bv[4][4];
+#pragma unroll
+    for (int R = 0; R < 4; ++R)
+#pragma unroll
+      for (int C = 0; C < 4; ++C)
+        bv[R][C] = base ? *reinterpret_cast<const double2*>(base + (long long)(8 * R + q) * ldb +
+                                                            8 * C + 2 * k4)
+                        : make_double2(0.0, 0.0);
 #pragma unroll
     for (int R = 0; R < 4; ++R)
 #pragma unroll
@@ -832,11 +841,10 @@ k_bfactor_lp(FactorSrc src, DevSketch skb, double* __restrict__ Ginv, long long 
         const int r = 8 * R + q, c = 8 * C + 2 * k4;
         double v0 = acc[R][4 * h + C][0], v1 = acc[R][4 * h + C][1];
         if (base) {
-          v0 = base[(long long)r * ldb + c] - v0;
-          v1 = base[(long long)r * ldb + c + 1] - v1;
+          v0 = bv[R][C].x - v0;
+          v1 = bv[R][C].y - v1;
         }
-        Ct[(long long)r * ld + c] = v0;
-        Ct[(long long)r * ld + c + 1] = v1;
+        *reinterpret_cast<double2*>(Ct + (long long)r * ld + c) = make_double2(v0, v1);
       }
   };
   double t32[4][4][2];   // 32 x 32 tile products (mma_tile)
