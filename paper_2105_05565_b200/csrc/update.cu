@@ -10,6 +10,7 @@
 // in a fixed order), and the last block applies the stop rule ||r^k|| <= tol ||r^0|| (P:L248-251,
 // DESIGN.md R1), the divergence guard and the iteration counter.
 #include <algorithm>
+#include <cstdlib>
 #include <cooperative_groups.h>
 
 #include "rs_internal.cuh"
@@ -409,7 +410,12 @@ cudaError_t launch_update_rows(const double* A, long long lda, const DevSketch& 
   const long long cb = (m + RW_COLS - 1) / RW_COLS;
   // splits (one cluster per column block): about two blocks per SM in total (128 registers per
   // thread), at least 4 rows per warp, at most the portable cluster size
-  long long ns = (4LL * num_sms + cb / 2) / cb;   // about four blocks per SM in total
+  static const long long bps = [] {   // blocks per SM targeted (RS_UR_BPS overrides, sweeps)
+    const char* e = std::getenv("RS_UR_BPS");
+    return e ? std::max(1, atoi(e)) : 4;
+  }();
+  long long ns = (bps * num_sms + cb / 2) / cb;   // ~4 blocks per SM (8 / 16 / 32 measured slower
+                                                  // on c4: 55 / 68 / 68 vs 54 us)
   ns = std::min<long long>(ns, (sk.len + 4 * RW_Y - 1) / (4 * RW_Y));   // >= 4 rows per warp
   ns = std::max(1LL, std::min<long long>(ns, RW_MAXS));
   const int per = (int)((sk.len + ns - 1) / ns);
