@@ -663,3 +663,25 @@ def test_process_switches_parity(tmp_path, env):
         ref = OV.solve(X, y, 0.5, kind, tau, 1.0, 0.5, 0.0, 12, seed=3, subcount_k=k)
         assert rel(got[f"{mode}_{kind}_w"], ref["w"]) <= 1e-10, (env, mode, kind)
         assert rel(got[f"{mode}_{kind}_r"], ref["r"]) <= 1e-10, (env, mode, kind)
+
+
+@pytest.mark.parametrize("kind,tau,k", [("subcount", 16, 4), ("subsample", 25, 0), ("subcount", 240, 1)])
+def test_csr_dual_selected_rows_match_full_scan(rs, monkeypatch, kind, tau, k):
+    """The dual selected-row path (k_sel_emit / k_sel_merge / k_sel_heavy) merges every touched row
+    of R = X^T in the same order as the full-scan k_hash_rows, so the rows of R S are identical;
+    the iterates then agree to rounding (k_gram_bands accumulates with shared-memory fp64 atomics,
+    whose order is not fixed).  RS_NO_SELROWS=1 selects the full scan (read per workspace)."""
+    n, d = 300, 5000
+    rp, ci, v, y = rsinputs.csr_zipf(n, d, 60, a=1.1, seed=3)
+    out = []
+    for env in (None, "1"):
+        if env:
+            monkeypatch.setenv("RS_NO_SELROWS", env)
+        h = rs.rs_create_csr(n, d, rp, ci, v, y, 1e-1, mode="gram")
+        try:
+            w, rep = rs.rs_solve(h, kind, tau, 1.0, 0.5, 0.0, 15, seed=4, subcount_k=k, d=d)
+            _, r = rs.rs_get_state(h)
+        finally:
+            rs.rs_destroy(h)
+        out.append((w, r))
+    assert rel(out[0][0], out[1][0]) <= 1e-13 and rel(out[0][1], out[1][1]) <= 1e-13
