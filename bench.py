@@ -596,7 +596,7 @@ def run_ours(args):
         line = {
             "metric": METRIC, "value": value, "unit": "iters/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": el_ms / args.steps,
-            "higher_is_better": True, "scaling": "strong" if world > 1 else "weak",
+            "higher_is_better": True, "scaling": "strong",   # one solve, X sharded over ranks
             "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded; DESIGN.md §5 recipe for BASELINE.json " + cfg.name + ")",
             "config": _config_dict(cfg, args, world),
