@@ -287,6 +287,22 @@ k_sel_heavy(const long long* __restrict__ ptr, const double* __restrict__ val,
   }
 }
 
+// t = R v = X^T v for the dual with v = S delta nonzero on the s selected samples only: each
+// selected sample's X row is scattered into t (fp64 atomics at L2: t's summation order is not
+// fixed; t feeds u = X t, which every rank allreduces)
+__global__ void __launch_bounds__(256)
+k_sel_scatter(DevSketch sk, const double* __restrict__ v, const long long* __restrict__ rowptr,
+              const int* __restrict__ colidx, const double* __restrict__ vals,
+              double* __restrict__ t, const Ctrl* ctrl) {
+  if (ctrl->done) return;
+  const int lane = threadIdx.x & 31;
+  const int e = blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (e >= sk.len) return;
+  const int i = sk.coord[e];
+  const double sd = v[i];
+  for (long long p = rowptr[i] + lane; p < rowptr[i + 1]; p += 32) atomicAdd(&t[colidx[p]], sd * vals[p]);
+}
+
 // ------------------------------------------------------------------------------------ stage 2
 __global__ void __launch_bounds__(GB_THREADS, 1)
 k_gram_bands(const long long* __restrict__ ptr, const int* __restrict__ hcnt,
@@ -674,14 +690,21 @@ rs_status Problem::csr_gram_into(const DevSketch& s, double* G, cudaEvent_t* ev,
   return RS_OK;
 }
 
-rs_status Problem::csr_gram_apply(const double* v, double* u) {
+rs_status Problem::csr_gram_apply(const double* v, double* u, const DevSketch* s) {
   CsrData* c = csr;
   const RView R = route == 1 ? RView{c->rowptr, c->colidx, c->vals, c->rows}
                              : RView{c->colptr, c->rowidx, c->cvals, c->cols};
   const RView Rt = route == 1 ? RView{c->colptr, c->rowidx, c->cvals, c->cols}
                               : RView{c->rowptr, c->colidx, c->vals, c->rows};
-  RS_CUDA(launch_spmv(R.ptr, R.idx, R.val, R.rows, c->nnz, c->heavyR, c->heavy_rowsR, c->nheavyR,
-                      v, c->tvec, num_sms, ctrl, st));
+  if (s && c->cmR && s->kind != SK_COUNT) {   // dual, selected samples: t = R v from their X rows
+    RS_CUDA(cudaMemsetAsync(c->tvec, 0, std::max<long long>(1, R.rows) * sizeof(double), st));
+    k_sel_scatter<<<(unsigned)std::max(1, (s->len + 7) / 8), 256, 0, st>>>(
+        *s, v, c->rowptr, c->colidx, c->vals, c->tvec, ctrl);
+    RS_CUDA(cudaGetLastError());
+  } else {
+    RS_CUDA(launch_spmv(R.ptr, R.idx, R.val, R.rows, c->nnz, c->heavyR, c->heavy_rowsR, c->nheavyR,
+                        v, c->tvec, num_sms, ctrl, st));
+  }
   RS_CUDA(launch_spmv(Rt.ptr, Rt.idx, Rt.val, Rt.rows, c->nnz, c->heavyRt, c->heavy_rowsRt,
                       c->nheavyRt, c->tvec, u, num_sms, ctrl, st));
   return RS_OK;
@@ -698,7 +721,7 @@ rs_status Problem::csr_enqueue_gram(const rs_solve_opts* o, cudaEvent_t* ev) {
                                 st));                                              // a4 + a5
   mark(RS_K_SOLVE, 1);
   mark(RS_K_AS, 0);   // u = R^T (R (S delta)), summed over ranks
-  RS_TRY(csr_gram_apply(sdelta, uvec));
+  RS_TRY(csr_gram_apply(sdelta, uvec, &sk));
   RS_TRY(allreduce(uvec, (size_t)m));
   mark(RS_K_AS, 1);
   mark(RS_K_UPDATE, 0);

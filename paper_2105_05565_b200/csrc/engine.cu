@@ -669,7 +669,7 @@ rs_status Problem::enqueue_pipelined_iteration(const rs_solve_opts* o, int slot,
   }
   mark(RS_K_AS, 0);
   if (fmt == 1)
-    RS_TRY(csr_gram_apply(sdelta, uvec));                                        // R^T R S delta
+    RS_TRY(csr_gram_apply(sdelta, uvec, &sq));                                   // R^T R S delta
   else if (rows_loc > 0)
     RS_CUDA(launch_xpass(X, ldx, rows_loc, m, sdelta, xp_part, uvec, num_sms, ctrl, st, &sq,
                          sw.delta));

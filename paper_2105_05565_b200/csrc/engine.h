@@ -137,7 +137,8 @@ struct Problem {
   rs_status csr_enqueue_gram(const rs_solve_opts* o, cudaEvent_t* ev);
   rs_status csr_gram_into(const DevSketch& s, double* G, cudaEvent_t* ev, int slot = 0,
                           bool reduce = true);   // (R S)^T (R S)
-  rs_status csr_gram_apply(const double* v, double* u);        // u = R^T (R v), local part
+  rs_status csr_gram_apply(const double* v, double* u,          // u = R^T (R v), local part
+                           const DevSketch* s = nullptr);
 };
 
 rs_status finish_setup(Problem* p);

@@ -1,0 +1,6 @@
+set -x
+python -c "import __graft_entry__ as g; g.build()" || exit 1
+timeout 900 python -m pytest tests -m gpu -q -x -k "csr" 2>&1 | grep -E "^E  .*Error|passed|failed|FAILED" | head | tee gpurun_out/pytest_gpu.log
+B="timeout 1200 python bench.py --no-cpu-baseline --no-e2e"
+$B --config c4 --steps 296 --max-iter-tol 20000 > gpurun_out/bench_c4.json 2>/dev/null
+RS_NO_SELROWS=1 $B --config c4 --steps 296 --max-iter-tol 3000 > gpurun_out/bench_c4_old.json 2>/dev/null
