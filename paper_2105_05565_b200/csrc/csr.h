@@ -45,6 +45,11 @@ struct CsrData {
   int* tflag = nullptr;
   int* tlist = nullptr;
   int* tcount = nullptr;
+  // heavy R rows on the selected-row path: hidx[f] = position of feature f in heavy_rowsR or -1;
+  // hacc / hbits: per heavy row a dense tau-vector of merged values and its touched-bucket bits
+  int* hidx = nullptr;
+  double* hacc = nullptr;
+  unsigned* hbits = nullptr;
   size_t hr_smem = 0, gb_smem = 0;
 };
 

@@ -193,22 +193,75 @@ k_hash_rows_heavy(const long long* __restrict__ ptr, const int* __restrict__ idx
 // sketched entries.  k_sel_emit walks their X rows (s x ~nnz/row entries instead of all of R) and
 // marks each entry's position in R = X^T with its (bucket << 1 | neg) code, collecting the touched
 // R rows; k_sel_merge then merges every touched light row exactly like k_hash_rows (same R order,
-// same lane order: bit-identical rows of R S) reading the codes contiguously, and resets them.
+// same lane order) reading the codes contiguously, and resets them; entries of heavy (Zipf-popular)
+// rows go straight into a dense tau-vector per heavy row (fp64 atomics), flushed in bucket order by
+// k_sel_heavy_flush -- no scan of those long rows.
 __global__ void __launch_bounds__(256)
 k_sel_emit(DevSketch sk, const long long* __restrict__ rowptr, const int* __restrict__ colidx,
-           const int* __restrict__ cscpos, int* __restrict__ cmR, int* __restrict__ tflag,
-           int* __restrict__ tlist, int* __restrict__ tcount, int slot, const Ctrl* ctrl) {
+           const double* __restrict__ vals, const int* __restrict__ cscpos, int* __restrict__ cmR,
+           int* __restrict__ tflag, int* __restrict__ tlist, int* __restrict__ tcount,
+           const int* __restrict__ hidx, double* __restrict__ hacc, unsigned* __restrict__ hbits,
+           int slot, const Ctrl* ctrl) {
   if (slot_unused(ctrl, slot)) return;
   const int lane = threadIdx.x & 31;
   const int e = blockIdx.x * 8 + (threadIdx.x >> 5);
   if (e >= sk.len) return;
   const int i = sk.coord[e];
-  const int code = (sk.bucket[e] << 1) | (sk.sign[e] > 0 ? 0 : 1);
+  const int b = sk.bucket[e], tau = sk.tau, nw = (tau + 31) >> 5;
+  const bool neg = sk.sign[e] <= 0;
+  const int code = (b << 1) | (neg ? 1 : 0);
   for (long long p = rowptr[i] + lane; p < rowptr[i + 1]; p += 32) {
-    cmR[cscpos[p]] = code;
     const int f = colidx[p];
-    if (atomicExch(&tflag[f], 1) == 0) tlist[atomicAdd(tcount, 1)] = f;
+    const int h = hidx[f];
+    if (h >= 0) {   // heavy (Zipf-popular) feature: straight into its dense tau-vector
+      const double x = vals[p];
+      atomicAdd(&hacc[(long long)h * tau + b], neg ? -x : x);
+      atomicOr(&hbits[(long long)h * nw + (b >> 5)], 1u << (b & 31));
+      continue;
+    }
+    cmR[cscpos[p]] = code;
+    if (tflag[f] == 0 && atomicExch(&tflag[f], 1) == 0) tlist[atomicAdd(tcount, 1)] = f;
   }
+}
+
+// heavy rows: warp per row, the touched buckets of its tau-vector in ascending order (then reset)
+__global__ void __launch_bounds__(256)
+k_sel_heavy_flush(const long long* __restrict__ ptr, const int* __restrict__ heavy_rows, int nheavy,
+                  int tau, double* __restrict__ hacc, unsigned* __restrict__ hbits,
+                  int* __restrict__ hb, double* __restrict__ hv, int* __restrict__ hcnt, int slot,
+                  const Ctrl* ctrl) {
+  if (slot_unused(ctrl, slot)) return;
+  const int lane = threadIdx.x & 31;
+  const int h = blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (h >= nheavy) return;
+  const int nw = (tau + 31) >> 5;
+  const long long f = heavy_rows[h];
+  const long long a = ptr[f];
+  unsigned* bits = hbits + (long long)h * nw;
+  double* acc = hacc + (long long)h * tau;
+  int total = 0;
+  for (int w0 = 0; w0 < nw; w0 += 32) {
+    const int wi = w0 + lane;
+    unsigned word = wi < nw ? bits[wi] : 0u;
+    const int c = __popc(word);
+    int incl = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(FULL, incl, o);
+      if (lane >= o) incl += y;
+    }
+    long long pos = a + total + incl - c;
+    for (; word; word &= word - 1) {
+      const int bucket = wi * 32 + __ffs(word) - 1;
+      hb[pos] = bucket;
+      hv[pos] = acc[bucket];
+      acc[bucket] = 0.0;
+      ++pos;
+    }
+    if (wi < nw) bits[wi] = 0u;
+    total += __shfl_sync(FULL, incl, 31);
+  }
+  if (lane == 0) hcnt[f] = total;
 }
 
 __global__ void __launch_bounds__(HR_WARPS * 32)
@@ -227,7 +280,7 @@ k_sel_merge(const long long* __restrict__ ptr, const double* __restrict__ val, l
     const int f = tlist[k];
     if (lane == 0) tflag[f] = 0;
     const long long a = ptr[f], e = ptr[f + 1];
-    if (e - a > heavy) continue;   // heavy rows: k_sel_heavy
+    if (e - a > heavy) continue;   // heavy rows: k_sel_heavy_flush
     for (long long base = a; base < e; base += 64) {
       const long long t0 = base + lane, t1 = base + 32 + lane;
       const int cm0 = t0 < e ? cmR[t0] : -1, cm1 = t1 < e ? cmR[t1] : -1;
@@ -240,50 +293,6 @@ k_sel_merge(const long long* __restrict__ ptr, const double* __restrict__ val, l
     }
     const int total = M.flush(a, hb, hv, lane);
     if (lane == 0) hcnt[f] = total;
-  }
-}
-
-// heavy rows (all of them: Zipf-popular features are touched by nearly every sketch): one CTA per
-// row, codes read from cmR (and reset), warps merged in warp order as in k_hash_rows_heavy
-__global__ void __launch_bounds__(HR_WARPS * 32)
-k_sel_heavy(const long long* __restrict__ ptr, const double* __restrict__ val,
-            const int* __restrict__ heavy_rows, int* __restrict__ cmR, int tau, int* __restrict__ hb,
-            double* __restrict__ hv, int* __restrict__ hcnt, int slot, const Ctrl* ctrl) {
-  if (slot_unused(ctrl, slot)) return;
-  extern __shared__ double hsm[];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  WarpMerge M(hsm, tau, warp);
-  for (int q = lane; q < M.nw; q += 32) M.bits[q] = 0u;
-  __syncwarp();
-  const long long i = heavy_rows[blockIdx.x];
-  const long long a = ptr[i], e = ptr[i + 1];
-  for (long long base = a + 32LL * warp; base < e; base += 32LL * HR_WARPS) {
-    const long long t = base + lane;
-    const int cm = t < e ? cmR[t] : -1;
-    if (!__ballot_sync(FULL, cm >= 0)) continue;
-    const double v = cm >= 0 ? val[t] : 0.0;
-    M.add(cm, (cm & 1) ? -v : v, lane);
-    if (cm >= 0) cmR[t] = -1;
-  }
-  __syncthreads();
-  WarpMerge M0(hsm, tau, 0);
-  for (int b = threadIdx.x; b < tau; b += HR_WARPS * 32) {
-    double s = 0.0;
-    bool any = false;
-    for (int w = 0; w < HR_WARPS; ++w) {
-      WarpMerge Mw(hsm, tau, w);
-      if (Mw.bits[b >> 5] & (1u << (b & 31))) {
-        s += Mw.acc[b];
-        any = true;
-      }
-    }
-    M0.acc[b] = s;
-    if (any) atomicOr(&M0.bits[b >> 5], 1u << (b & 31));
-  }
-  __syncthreads();
-  if (warp == 0) {
-    const int total = M.flush(a, hb, hv, lane);
-    if (lane == 0) hcnt[i] = total;
   }
 }
 
@@ -507,6 +516,12 @@ void Problem::csr_gram_free() {
   dfree(csr->chunk_h0);
   csr->chunk_h0 = nullptr;
   dfree(csr->cmR);
+  dfree(csr->hidx);
+  dfree(csr->hacc);
+  dfree(csr->hbits);
+  csr->hidx = nullptr;
+  csr->hacc = nullptr;
+  csr->hbits = nullptr;
   dfree(csr->tflag);
   dfree(csr->tlist);
   dfree(csr->tcount);
@@ -613,6 +628,17 @@ rs_status Problem::csr_gram_workspace(int kind, int tau) {
       RS_CUDA(cudaMemcpy(c->heavy_rowsR, hl.data(), hl.size() * sizeof(int), cudaMemcpyHostToDevice));
     RS_TRY(dalloc(&c->chunk_h0, h0.size()));
     RS_CUDA(cudaMemcpy(c->chunk_h0, h0.data(), h0.size() * sizeof(int), cudaMemcpyHostToDevice));
+    if (c->cmR) {   // selected-row path: heavy rows accumulate into dense tau-vectors
+      std::vector<int> hx(std::max<long long>(1, R.rows), -1);
+      for (int k = 0; k < c->nheavyR; ++k) hx[hl[k]] = k;
+      RS_TRY(dalloc(&c->hidx, hx.size()));
+      RS_CUDA(cudaMemcpy(c->hidx, hx.data(), hx.size() * sizeof(int), cudaMemcpyHostToDevice));
+      const long long nh = std::max(1, c->nheavyR), nw = (tau + 31) / 32;
+      RS_TRY(dalloc(&c->hacc, (size_t)nh * tau));
+      RS_TRY(dalloc(&c->hbits, (size_t)nh * nw));
+      RS_CUDA(cudaMemsetAsync(c->hacc, 0, (size_t)nh * tau * sizeof(double), st));
+      RS_CUDA(cudaMemsetAsync(c->hbits, 0, (size_t)nh * nw * sizeof(unsigned), st));
+    }
   }
   c->gb_smem = (size_t)maxband * sizeof(double);
   c->hr_smem = (size_t)HR_WARPS * (tau + 32) * sizeof(double) + (size_t)HR_WARPS * ((tau + 31) / 32) * 4;
@@ -649,14 +675,16 @@ rs_status Problem::csr_gram_into(const DevSketch& s, double* G, cudaEvent_t* ev,
   if (R.rows > 0 && sel) {   // a2: rows of R S from the s selected rows of X
     RS_CUDA(cudaMemsetAsync(c->hcnt, 0, R.rows * sizeof(int), st));
     k_sel_emit<<<(unsigned)std::max(1, (s.len + 7) / 8), 256, 0, st>>>(
-        s, c->rowptr, c->colidx, c->cscpos, c->cmR, c->tflag, c->tlist, c->tcount, slot, ctrl);
+        s, c->rowptr, c->colidx, c->vals, c->cscpos, c->cmR, c->tflag, c->tlist, c->tcount, c->hidx,
+        c->hacc, c->hbits, slot, ctrl);
     const unsigned grid = (unsigned)((long long)num_sms * 8);
     k_sel_merge<<<grid, HR_WARPS * 32, c->hr_smem, st>>>(R.ptr, R.val, c->heavyR, c->cmR, c->tflag,
                                                          c->tlist, c->tcount, tau, c->hb, c->hv,
                                                          c->hcnt, slot, ctrl);
     if (c->nheavyR > 0)
-      k_sel_heavy<<<c->nheavyR, HR_WARPS * 32, c->hr_smem, st>>>(
-          R.ptr, R.val, c->heavy_rowsR, c->cmR, tau, c->hb, c->hv, c->hcnt, slot, ctrl);
+      k_sel_heavy_flush<<<(unsigned)((c->nheavyR + 7) / 8), 256, 0, st>>>(
+          R.ptr, c->heavy_rowsR, c->nheavyR, tau, c->hacc, c->hbits, c->hb, c->hv, c->hcnt, slot,
+          ctrl);
     RS_CUDA(cudaMemsetAsync(c->tcount, 0, sizeof(int), st));
     RS_CUDA(cudaGetLastError());
   } else if (R.rows > 0) {   // a2: rows of R S, merged and bucket-sorted
