@@ -46,10 +46,15 @@ struct CsrData {
   int* tlist = nullptr;
   int* tcount = nullptr;
   // heavy R rows on the selected-row path: hidx[f] = position of feature f in heavy_rowsR or -1;
-  // hacc / hbits: per heavy row a dense tau-vector of merged values and its touched-bucket bits
+  // hacc: per heavy row its row of R S as a dense tau-vector (ld ldh); their Gram contribution
+  // H^T H is one lower-tile DMMA GEMM (tg_heavy) into gh, added by the band reduction
   int* hidx = nullptr;
   double* hacc = nullptr;
-  unsigned* hbits = nullptr;
+  long long ldh = 0;
+  TmaGemm tg_heavy{};
+  double* gh = nullptr;
+  double* gh_work = nullptr;
+  int* chunk_h0_none = nullptr;   // [nchunks + 1] zeros: k_gram_bands without its heavy phase
   size_t hr_smem = 0, gb_smem = 0;
 };
 

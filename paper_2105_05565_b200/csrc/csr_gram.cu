@@ -194,20 +194,20 @@ k_hash_rows_heavy(const long long* __restrict__ ptr, const int* __restrict__ idx
 // marks each entry's position in R = X^T with its (bucket << 1 | neg) code, collecting the touched
 // R rows; k_sel_merge then merges every touched light row exactly like k_hash_rows (same R order,
 // same lane order) reading the codes contiguously, and resets them; entries of heavy (Zipf-popular)
-// rows go straight into a dense tau-vector per heavy row (fp64 atomics), flushed in bucket order by
-// k_sel_heavy_flush -- no scan of those long rows.
+// rows go straight into a dense tau-vector per heavy row (fp64 atomics) whose Gram contribution is
+// one lower-tile DMMA GEMM H^T H -- no scan of those long rows, no pair loop over them.
 __global__ void __launch_bounds__(256)
 k_sel_emit(DevSketch sk, const long long* __restrict__ rowptr, const int* __restrict__ colidx,
            const double* __restrict__ vals, const int* __restrict__ cscpos, int* __restrict__ cmR,
            int* __restrict__ tflag, int* __restrict__ tlist, int* __restrict__ tcount,
-           const int* __restrict__ hidx, double* __restrict__ hacc, unsigned* __restrict__ hbits,
-           int slot, const Ctrl* ctrl) {
+           const int* __restrict__ hidx, double* __restrict__ hacc, long long ldh, int slot,
+           const Ctrl* ctrl) {
   if (slot_unused(ctrl, slot)) return;
   const int lane = threadIdx.x & 31;
   const int e = blockIdx.x * 8 + (threadIdx.x >> 5);
   if (e >= sk.len) return;
   const int i = sk.coord[e];
-  const int b = sk.bucket[e], tau = sk.tau, nw = (tau + 31) >> 5;
+  const int b = sk.bucket[e];
   const bool neg = sk.sign[e] <= 0;
   const int code = (b << 1) | (neg ? 1 : 0);
   for (long long p = rowptr[i] + lane; p < rowptr[i + 1]; p += 32) {
@@ -215,53 +215,12 @@ k_sel_emit(DevSketch sk, const long long* __restrict__ rowptr, const int* __rest
     const int h = hidx[f];
     if (h >= 0) {   // heavy (Zipf-popular) feature: straight into its dense tau-vector
       const double x = vals[p];
-      atomicAdd(&hacc[(long long)h * tau + b], neg ? -x : x);
-      atomicOr(&hbits[(long long)h * nw + (b >> 5)], 1u << (b & 31));
+      atomicAdd(&hacc[(long long)h * ldh + b], neg ? -x : x);
       continue;
     }
     cmR[cscpos[p]] = code;
     if (tflag[f] == 0 && atomicExch(&tflag[f], 1) == 0) tlist[atomicAdd(tcount, 1)] = f;
   }
-}
-
-// heavy rows: warp per row, the touched buckets of its tau-vector in ascending order (then reset)
-__global__ void __launch_bounds__(256)
-k_sel_heavy_flush(const long long* __restrict__ ptr, const int* __restrict__ heavy_rows, int nheavy,
-                  int tau, double* __restrict__ hacc, unsigned* __restrict__ hbits,
-                  int* __restrict__ hb, double* __restrict__ hv, int* __restrict__ hcnt, int slot,
-                  const Ctrl* ctrl) {
-  if (slot_unused(ctrl, slot)) return;
-  const int lane = threadIdx.x & 31;
-  const int h = blockIdx.x * 8 + (threadIdx.x >> 5);
-  if (h >= nheavy) return;
-  const int nw = (tau + 31) >> 5;
-  const long long f = heavy_rows[h];
-  const long long a = ptr[f];
-  unsigned* bits = hbits + (long long)h * nw;
-  double* acc = hacc + (long long)h * tau;
-  int total = 0;
-  for (int w0 = 0; w0 < nw; w0 += 32) {
-    const int wi = w0 + lane;
-    unsigned word = wi < nw ? bits[wi] : 0u;
-    const int c = __popc(word);
-    int incl = c;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int y = __shfl_up_sync(FULL, incl, o);
-      if (lane >= o) incl += y;
-    }
-    long long pos = a + total + incl - c;
-    for (; word; word &= word - 1) {
-      const int bucket = wi * 32 + __ffs(word) - 1;
-      hb[pos] = bucket;
-      hv[pos] = acc[bucket];
-      acc[bucket] = 0.0;
-      ++pos;
-    }
-    if (wi < nw) bits[wi] = 0u;
-    total += __shfl_sync(FULL, incl, 31);
-  }
-  if (lane == 0) hcnt[f] = total;
 }
 
 __global__ void __launch_bounds__(HR_WARPS * 32)
@@ -280,7 +239,7 @@ k_sel_merge(const long long* __restrict__ ptr, const double* __restrict__ val, l
     const int f = tlist[k];
     if (lane == 0) tflag[f] = 0;
     const long long a = ptr[f], e = ptr[f + 1];
-    if (e - a > heavy) continue;   // heavy rows: k_sel_heavy_flush
+    if (e - a > heavy) continue;   // heavy rows: dense H^T H (csr_gram_into)
     for (long long base = a; base < e; base += 64) {
       const long long t0 = base + lane, t1 = base + 32 + lane;
       const int cm0 = t0 < e ? cmR[t0] : -1, cm1 = t1 < e ? cmR[t1] : -1;
@@ -388,12 +347,12 @@ k_gram_bands(const long long* __restrict__ ptr, const int* __restrict__ hcnt,
 
 __global__ void k_gram_band_reduce(const double* __restrict__ part, int nchunks,
                                    long long part_stride, double* __restrict__ G, long long ldg,
-                                   int slot, const Ctrl* ctrl) {
+                                   int slot, const Ctrl* ctrl, const double* __restrict__ gh = nullptr) {
   if (slot_unused(ctrl, slot)) return;
   const int a = blockIdx.x;
   const long long base = tri(a);
   for (int c = threadIdx.x; c <= a; c += blockDim.x) {
-    double s = 0.0;
+    double s = gh ? gh[(long long)a * ldg + c] : 0.0;   // heavy rows' H^T H (same ld as G)
     for (int k = 0; k < nchunks; ++k) s += part[k * part_stride + base + c];
     G[(long long)a * ldg + c] = s;
   }
@@ -518,10 +477,13 @@ void Problem::csr_gram_free() {
   dfree(csr->cmR);
   dfree(csr->hidx);
   dfree(csr->hacc);
-  dfree(csr->hbits);
+  dfree(csr->gh);
+  dfree(csr->gh_work);
+  dfree(csr->chunk_h0_none);
   csr->hidx = nullptr;
   csr->hacc = nullptr;
-  csr->hbits = nullptr;
+  csr->gh = csr->gh_work = nullptr;
+  csr->chunk_h0_none = nullptr;
   dfree(csr->tflag);
   dfree(csr->tlist);
   dfree(csr->tcount);
@@ -633,11 +595,19 @@ rs_status Problem::csr_gram_workspace(int kind, int tau) {
       for (int k = 0; k < c->nheavyR; ++k) hx[hl[k]] = k;
       RS_TRY(dalloc(&c->hidx, hx.size()));
       RS_CUDA(cudaMemcpy(c->hidx, hx.data(), hx.size() * sizeof(int), cudaMemcpyHostToDevice));
-      const long long nh = std::max(1, c->nheavyR), nw = (tau + 31) / 32;
-      RS_TRY(dalloc(&c->hacc, (size_t)nh * tau));
-      RS_TRY(dalloc(&c->hbits, (size_t)nh * nw));
-      RS_CUDA(cudaMemsetAsync(c->hacc, 0, (size_t)nh * tau * sizeof(double), st));
-      RS_CUDA(cudaMemsetAsync(c->hbits, 0, (size_t)nh * nw * sizeof(unsigned), st));
+      const long long nh = std::max(1, c->nheavyR);
+      c->ldh = round_up(tau, 4);
+      RS_TRY(dalloc(&c->hacc, (size_t)nh * c->ldh));
+      RS_CUDA(cudaMemsetAsync(c->hacc, 0, (size_t)nh * c->ldh * sizeof(double), st));
+      RS_TRY(dalloc(&c->chunk_h0_none, h0.size()));
+      RS_CUDA(cudaMemsetAsync(c->chunk_h0_none, 0, h0.size() * sizeof(int), st));
+      if (c->nheavyR > 0) {
+        RS_CUDA(tma_gemm_plan(&c->tg_heavy, c->hacc, c->ldh, c->hacc, c->ldh, tau, tau, c->nheavyR,
+                              num_sms));
+        c->tg_heavy.lower = 1;
+        if (c->tg_heavy.work_elems) RS_TRY(dalloc(&c->gh_work, c->tg_heavy.work_elems));
+        RS_TRY(dalloc(&c->gh, (size_t)tau * round_up(tau, 4)));
+      }
     }
   }
   c->gb_smem = (size_t)maxband * sizeof(double);
@@ -676,15 +646,15 @@ rs_status Problem::csr_gram_into(const DevSketch& s, double* G, cudaEvent_t* ev,
     RS_CUDA(cudaMemsetAsync(c->hcnt, 0, R.rows * sizeof(int), st));
     k_sel_emit<<<(unsigned)std::max(1, (s.len + 7) / 8), 256, 0, st>>>(
         s, c->rowptr, c->colidx, c->vals, c->cscpos, c->cmR, c->tflag, c->tlist, c->tcount, c->hidx,
-        c->hacc, c->hbits, slot, ctrl);
+        c->hacc, c->ldh, slot, ctrl);
     const unsigned grid = (unsigned)((long long)num_sms * 8);
     k_sel_merge<<<grid, HR_WARPS * 32, c->hr_smem, st>>>(R.ptr, R.val, c->heavyR, c->cmR, c->tflag,
                                                          c->tlist, c->tcount, tau, c->hb, c->hv,
                                                          c->hcnt, slot, ctrl);
-    if (c->nheavyR > 0)
-      k_sel_heavy_flush<<<(unsigned)((c->nheavyR + 7) / 8), 256, 0, st>>>(
-          R.ptr, c->heavy_rowsR, c->nheavyR, tau, c->hacc, c->hbits, c->hb, c->hv, c->hcnt, slot,
-          ctrl);
+    if (c->nheavyR > 0) {   // heavy rows: H^T H on the lower DMMA tiles, then H cleared
+      RS_CUDA(tma_gemm_launch(c->tg_heavy, c->gh, ld_gram, c->gh_work, ctrl, st));
+      RS_CUDA(cudaMemsetAsync(c->hacc, 0, (size_t)c->nheavyR * c->ldh * sizeof(double), st));
+    }
     RS_CUDA(cudaMemsetAsync(c->tcount, 0, sizeof(int), st));
     RS_CUDA(cudaGetLastError());
   } else if (R.rows > 0) {   // a2: rows of R S, merged and bucket-sorted
@@ -701,12 +671,13 @@ rs_status Problem::csr_gram_into(const DevSketch& s, double* G, cudaEvent_t* ev,
     mark(RS_K_XS, 1);
     mark(RS_K_GRAM, 0);
     // a3/a4: (R S)^T (R S), lower triangle
+    const bool hgemm = sel && c->nheavyR > 0;   // heavy rows already in gh
     k_gram_bands<<<dim3((unsigned)c->nbands, (unsigned)c->nchunks), GB_THREADS, c->gb_smem, st>>>(
         R.ptr, c->hcnt, c->hb, c->hv, c->band_a0, c->chunk_r0, c->heavyR, c->heavy_rowsR,
-        c->chunk_h0, c->gpart, c->gpart_stride, slot, ctrl);
+        hgemm ? c->chunk_h0_none : c->chunk_h0, c->gpart, c->gpart_stride, slot, ctrl);
     RS_CUDA(cudaGetLastError());
     k_gram_band_reduce<<<tau, 256, 0, st>>>(c->gpart, c->nchunks, c->gpart_stride, G, ld_gram, slot,
-                                            ctrl);
+                                            ctrl, hgemm ? c->gh : nullptr);
     RS_CUDA(cudaGetLastError());
   } else {
     mark(RS_K_XS, 1);
