@@ -277,7 +277,10 @@ k_gram_bands(const long long* __restrict__ ptr, const int* __restrict__ hcnt,
              const int* __restrict__ hb, const double* __restrict__ hv,
              const int* __restrict__ band_a0, const long long* __restrict__ chunk_r0,
              long long heavy, const int* __restrict__ heavy_rows, const int* __restrict__ chunk_h0,
-             double* __restrict__ part, long long part_stride, int slot, const Ctrl* ctrl) {
+             double* __restrict__ part, long long part_stride, int slot, const Ctrl* ctrl,
+             const int* __restrict__ rlist = nullptr, const int* __restrict__ rcount = nullptr) {
+  // rlist (optional): visit only the listed rows (the touched rows of the selected-row path),
+  // chunk y taking list entries [y n / nchunks, (y + 1) n / nchunks)
   if (slot_unused(ctrl, slot)) return;
   extern __shared__ double band[];
   const int a0 = band_a0[blockIdx.x], a1 = band_a0[blockIdx.x + 1];
@@ -286,10 +289,16 @@ k_gram_bands(const long long* __restrict__ ptr, const int* __restrict__ hcnt,
   for (int q = threadIdx.x; q < sz; q += GB_THREADS) band[q] = 0.0;
   __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const long long r0 = chunk_r0[blockIdx.y], r1 = chunk_r0[blockIdx.y + 1];
+  long long r0 = chunk_r0[blockIdx.y], r1 = chunk_r0[blockIdx.y + 1];
+  if (rlist) {
+    const long long n = *rcount;
+    r0 = n * blockIdx.y / gridDim.y;
+    r1 = n * (blockIdx.y + 1) / gridDim.y;
+  }
   for (long long rb = r0 + 32LL * warp; rb < r1; rb += 32LL * (GB_THREADS / 32)) {
-    const long long rl = rb + lane;
-    int Ll = rl < r1 ? hcnt[rl] : 0;
+    const long long rk = rb + lane;
+    const long long rl = rk < r1 ? (rlist ? (long long)rlist[rk] : rk) : 0;
+    int Ll = rk < r1 ? hcnt[rl] : 0;
     const long long offl = Ll ? ptr[rl] : 0;
     if (Ll && ptr[rl + 1] - offl > heavy) Ll = 0;   // heavy phase below
     for (unsigned nz = __ballot_sync(FULL, Ll > 0); nz; nz &= nz - 1) {
@@ -655,7 +664,6 @@ rs_status Problem::csr_gram_into(const DevSketch& s, double* G, cudaEvent_t* ev,
       RS_CUDA(tma_gemm_launch(c->tg_heavy, c->gh, ld_gram, c->gh_work, ctrl, st));
       RS_CUDA(cudaMemsetAsync(c->hacc, 0, (size_t)c->nheavyR * c->ldh * sizeof(double), st));
     }
-    RS_CUDA(cudaMemsetAsync(c->tcount, 0, sizeof(int), st));
     RS_CUDA(cudaGetLastError());
   } else if (R.rows > 0) {   // a2: rows of R S, merged and bucket-sorted
     const unsigned grid = (unsigned)std::max<long long>(
@@ -674,8 +682,10 @@ rs_status Problem::csr_gram_into(const DevSketch& s, double* G, cudaEvent_t* ev,
     const bool hgemm = sel && c->nheavyR > 0;   // heavy rows already in gh
     k_gram_bands<<<dim3((unsigned)c->nbands, (unsigned)c->nchunks), GB_THREADS, c->gb_smem, st>>>(
         R.ptr, c->hcnt, c->hb, c->hv, c->band_a0, c->chunk_r0, c->heavyR, c->heavy_rowsR,
-        hgemm ? c->chunk_h0_none : c->chunk_h0, c->gpart, c->gpart_stride, slot, ctrl);
+        hgemm ? c->chunk_h0_none : c->chunk_h0, c->gpart, c->gpart_stride, slot, ctrl,
+        sel ? c->tlist : nullptr, sel ? c->tcount : nullptr);
     RS_CUDA(cudaGetLastError());
+    if (sel) RS_CUDA(cudaMemsetAsync(c->tcount, 0, sizeof(int), st));   // touched list consumed
     k_gram_band_reduce<<<tau, 256, 0, st>>>(c->gpart, c->nchunks, c->gpart_stride, G, ld_gram, slot,
                                             ctrl, hgemm ? c->gh : nullptr);
     RS_CUDA(cudaGetLastError());
