@@ -40,7 +40,7 @@ def _peaks():
 
 
 class ClockSampler:
-    """SM clocks and clock-event (throttle) reasons sampled every 50 ms during the timed region, in
+    """SM clocks and clock-event (throttle) reasons sampled every 100 ms during the timed region, in
     process through NVML (pynvml) from a background thread: no nvidia-smi process whose start-up or
     driver queries could stall the timed region's host-side launches.  Falls back to nvidia-smi."""
 
@@ -69,7 +69,7 @@ class ClockSampler:
             except Exception:
                 pass
             self._first.set()
-            if self._stop.wait(0.05):
+            if self._stop.wait(0.1):
                 break
 
     def __enter__(self):
@@ -618,7 +618,7 @@ def run_ours(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--steps", type=int, default=1000)   # a timed region of ~0.4 s on c2
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c2")
