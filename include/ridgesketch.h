@@ -48,7 +48,8 @@ typedef enum {
   RS_EINVAL = 1,        /* invalid argument: dimensions, lambda <= 0, non-finite data, CSR
                            invariants, tau not in [1, m], subcount k*tau > m, gamma not in (0,1],
                            beta not in [0,1], tol < 0, max_iter < 0, NULL pointers            */
-  RS_EUNSUPPORTED = 2,  /* valid but not implemented (e.g. explicit A with CSR X)             */
+  RS_EUNSUPPORTED = 2,  /* valid but not implemented (e.g. CSR GRAM with tau > 1536, kernel
+                           ridge with world > 1)                                              */
   RS_ENOMEM = 3,        /* device allocation failed                                           */
   RS_ECUDA = 4,         /* CUDA runtime / launch failure, or no usable device                 */
   RS_ENCCL = 5,         /* NCCL failure; the communicator is aborted, only rs_destroy is legal */
@@ -60,12 +61,14 @@ typedef enum { RS_ROUTE_AUTO = 0, RS_ROUTE_PRIMAL = 1, RS_ROUTE_DUAL = 2 } rs_ro
 
 /* How A S is formed (R10).
  *   IMPLICIT: A S = X^T (X S) + lambda S (primal) or X (X^T S) + lambda S (dual); A never formed.
- *   EXPLICIT: A = B + lambda I is built once in rs_create (dense SYRK-style product), and every
- *             iteration gathers / sums the sketched rows of A (A symmetric, so rows = columns).
- *             Dense X only (RS_EUNSUPPORTED for CSR).                                            */
-/*   GRAM    : (dense primal only) A S is never formed: G = (XS)^T(XS) + lambda S^T S
- *             and A S delta = X^T (X S delta) + lambda S delta (one streaming pass over X per
- *             iteration).  Same iterates as IMPLICIT in exact arithmetic.          */
+ *   EXPLICIT: A = B + lambda I is built once in rs_create (dense X: lower-tile DMMA product;
+ *             CSR X: dense A from the sparse rows, RS_ENOMEM if m x m doubles do
+ *             not fit), and every iteration gathers / sums the sketched rows of A (A symmetric,
+ *             so rows = columns).
+ *   GRAM    : (dense primal, CSR primal and dual) A S is never formed:
+ *             G = (RS)^T(RS) + lambda S^T S with R = X (primal) or X^T (dual), and
+ *             A S delta = R^T (R S delta) + lambda S delta (one streaming pass over X per iteration).
+ *             Same iterates as IMPLICIT in exact arithmetic.                       */
 typedef enum { RS_AS_IMPLICIT = 0, RS_AS_EXPLICIT = 1, RS_AS_GRAM = 2 } rs_as_mode;
 
 typedef enum {
@@ -87,8 +90,9 @@ typedef enum { RS_MEM_HOST = 0, RS_MEM_DEVICE_COPY = 1, RS_MEM_DEVICE_BORROW = 2
 /* Process layout (one process per GPU).  NULL means world = 1 on the current device with the
  * whole X.  Primal: X_local holds rows [shard_begin, shard_begin + shard_len) of X.  Dual: X_local
  * holds columns [shard_begin, shard_begin + shard_len) (features).  Sketches are regenerated on
- * every rank from (seed, k); the only per-iteration exchange is an NCCL sum-allreduce of the
- * partial A S. */
+ * every rank from (seed, k); the per-iteration exchange is an NCCL sum-allreduce of the partial
+ * A S (IMPLICIT) or of u = R^T R S delta (GRAM, plus one allreduce of a sketch-ahead group's
+ * Grams); EXPLICIT iterations need none. */
 typedef struct {
   int device;                  /* CUDA device ordinal used by this rank                         */
   int rank, world;
@@ -99,8 +103,10 @@ typedef struct {
 } rs_dist;
 
 /* Create a problem from dense X (n x d, row-major, leading dimension ldx >= d) and y (n).
- * For world > 1, X_local / y are the rank's shard (rows for primal: y is the matching rows;
- * columns for dual: y is the full n-vector).  n, d are the GLOBAL dimensions. */
+ * For world > 1, X_local / y are the rank's shard of rows (primal; y is the matching rows).
+ * n, d are the GLOBAL dimensions.  The dual route (n < d) is served in EXPLICIT mode
+ * on one GPU (A = X X^T + lambda I, n x n; rs_solve then returns w = X^T alpha);
+ * IMPLICIT / GRAM or world > 1 with a dense dual route return RS_EUNSUPPORTED. */
 rs_status rs_create_dense(rs_problem* out, int64_t n, int64_t d, const double* X_local,
                           int64_t ldx, const double* y, double lambda, rs_route route,
                           rs_as_mode mode, rs_mem mem, const rs_dist* dist);

@@ -220,10 +220,13 @@ static rs_status create_dense(rs_problem* out, int64_t n, int64_t d, const doubl
   if (mode != RS_AS_IMPLICIT && mode != RS_AS_EXPLICIT && mode != RS_AS_GRAM)
     return fail(RS_EINVAL, "bad as_mode");
   const int rt = route == RS_ROUTE_AUTO ? (d <= n ? 1 : 2) : (route == RS_ROUTE_PRIMAL ? 1 : 2);
-  if (rt == 2) return fail(RS_EUNSUPPORTED, "dense dual route not implemented yet (use CSR or primal)");
+  if (rt == 2 && mode != RS_AS_EXPLICIT)   // dense dual: A = X X^T + lambda I formed once
+    return fail(RS_EUNSUPPORTED, "dense dual route (n < d): EXPLICIT mode only (or CSR X)");
+  if (rt == 2 && dist && dist->world > 1)
+    return fail(RS_EUNSUPPORTED, "dense dual route: one GPU in this version");
   if (mode == RS_AS_GRAM && d > 4096) return fail(RS_EUNSUPPORTED, "GRAM mode needs d <= 4096");
   RS_TRY(validate_dist(dist, rt == 1 ? n : d));
-  const long long rows = dist ? dist->shard_len : n;
+  const long long rows = rt == 1 && dist ? dist->shard_len : n;
 
   Problem* p = new Problem();
   auto guard = [&](rs_status s) {
@@ -237,7 +240,7 @@ static rs_status create_dense(rs_problem* out, int64_t n, int64_t d, const doubl
   p->mode = mode;
   p->n = n;
   p->d = d;
-  p->m = d;
+  p->m = rt == 1 ? d : n;   // primal: w in R^d; dual: alpha in R^n
   p->rows_loc = rows;
   p->lambda = lambda;
 
@@ -283,17 +286,32 @@ static rs_status create_dense(rs_problem* out, int64_t n, int64_t d, const doubl
   }
   // every buffer of the setup is allocated before e0 (and freed after e1), so setup_seconds is the
   // device work of b = X^T y and the explicit A build, not host allocator time
-  s = dalloc(&p->b, d);
+  const long long m = p->m;
+  s = dalloc(&p->b, m);
   if (s != RS_OK) return guard(s);
   double* xty_work = nullptr;
   s = dalloc(&xty_work, dense_xty_work(rows, d));
   if (s != RS_OK) return guard(s);
+  double* xt = nullptr;   // dual: X^T (d x ldt), the operand of A = X X^T = (X^T)^T X^T
+  long long ldt = 0;
   double* a_work = nullptr;
   TmaGemm tg{};
   GemmPlan gp{};
   const bool a_cpasync = rows > 0 && std::getenv("RS_A_BUILD_CPASYNC");   // comparison path
   cudaError_t ce = cudaSuccess;
-  if (mode == RS_AS_EXPLICIT) {
+  if (mode == RS_AS_EXPLICIT && rt == 2) {
+    p->lda = round_up(n, 4);
+    s = dalloc(&p->A, (size_t)n * p->lda);
+    if (s != RS_OK) return guard(s);
+    ldt = round_up(n, 4);
+    s = dalloc(&xt, (size_t)d * ldt);
+    if (s != RS_OK) return guard(s);
+    ce = tma_gemm_plan(&tg, xt, ldt, xt, ldt, n, n, d, p->num_sms);
+    tg.lower = 1;
+    if (ce == cudaSuccess && tg.work_elems) s = dalloc(&a_work, tg.work_elems);
+    if (s != RS_OK) return guard(s);
+    if (ce != cudaSuccess) return guard(fail(RS_ECUDA, std::string("A build: ") + cudaGetErrorString(ce)));
+  } else if (mode == RS_AS_EXPLICIT) {
     p->lda = round_up(d, 4);
     s = dalloc(&p->A, (size_t)d * p->lda);
     if (s != RS_OK) return guard(s);
@@ -311,12 +329,21 @@ static rs_status create_dense(rs_problem* out, int64_t n, int64_t d, const doubl
     if (ce != cudaSuccess) return guard(fail(RS_ECUDA, std::string("A build: ") + cudaGetErrorString(ce)));
   }
   cudaEventRecord(e0, p->st);
+  if (rt == 2) {   // dual: b = y, A = X X^T + lambda I on the lower DMMA tiles of X^T
+    ce = cudaMemcpyAsync(p->b, p->y, n * 8, cudaMemcpyDeviceToDevice, p->st);
+    if (ce == cudaSuccess) ce = launch_transpose(p->X, p->ldx, n, d, xt, ldt, p->st);
+    if (ce == cudaSuccess) ce = tma_gemm_launch(tg, p->A, p->lda, a_work, nullptr, p->st);
+    if (ce == cudaSuccess) ce = launch_mirror_lower(p->A, p->lda, n, p->st);
+    if (ce != cudaSuccess) return guard(fail(RS_ECUDA, std::string("dual A build: ") + cudaGetErrorString(ce)));
+    launch_add_diag(p->A, p->lda, n, lambda, p->st);
+  } else {
   // b = X^T y  (primal), summed over ranks
   ce = launch_dense_xty(p->X, p->ldx, rows, d, p->y, p->b, xty_work, p->st);
   if (ce != cudaSuccess) return guard(fail(RS_ECUDA, cudaGetErrorString(ce)));
   s = p->allreduce(p->b, d);
   if (s != RS_OK) return guard(s);
-  if (mode == RS_AS_EXPLICIT) {  // A = X^T X + lambda I, built once (DSYRK-shaped DMMA contraction)
+  }
+  if (mode == RS_AS_EXPLICIT && rt == 1) {  // A = X^T X + lambda I, built once (DSYRK-shaped DMMA contraction)
     // lower-triangle tiles only on the TMA/DMMA contraction (d^2 n flop instead of 2 d^2 n), then
     // the upper triangle mirrored: A is symmetric
     if (a_cpasync) {
@@ -336,6 +363,7 @@ static rs_status create_dense(rs_problem* out, int64_t n, int64_t d, const doubl
   ce = cudaStreamSynchronize(p->st);
   dfree(xty_work);
   dfree(a_work);
+  dfree(xt);
   if (ce != cudaSuccess) return guard(fail(RS_ECUDA, cudaGetErrorString(ce)));
   s = finish_setup(p);
   if (s != RS_OK) return guard(s);
@@ -1038,6 +1066,18 @@ rs_status Problem::write_weights(double* w_out, rs_mem w_mem, double* alpha_out)
   const cudaMemcpyKind kd = w_mem == RS_MEM_HOST ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice;
   if (route == 1) {
     RS_CUDA(cudaMemcpyAsync(w_out, w, m * 8, kd, st));
+  } else if (fmt == 0) {   // dense dual: w = X^T alpha
+    double *wd = nullptr, *work = nullptr;
+    RS_TRY(dalloc(&wd, d));
+    rs_status s = dalloc(&work, dense_xty_work(n, d));
+    if (s == RS_OK && launch_dense_xty(X, ldx, n, d, w, wd, work, st) != cudaSuccess)
+      s = fail(RS_ECUDA, "dual weights");
+    if (s == RS_OK && cudaMemcpyAsync(w_out, wd, d * 8, kd, st) != cudaSuccess) s = fail(RS_ECUDA, "copy w");
+    cudaStreamSynchronize(st);
+    dfree(wd);
+    dfree(work);
+    RS_TRY(s);
+    if (alpha_out) RS_CUDA(cudaMemcpyAsync(alpha_out, w, m * 8, cudaMemcpyDeviceToHost, st));
   } else {
     RS_TRY(csr_dual_weights(w_out, kd));
     if (alpha_out) RS_CUDA(cudaMemcpyAsync(alpha_out, w, m * 8, cudaMemcpyDeviceToHost, st));

@@ -685,3 +685,30 @@ def test_csr_dual_selected_rows_match_full_scan(rs, monkeypatch, kind, tau, k):
             rs.rs_destroy(h)
         out.append((w, r))
     assert rel(out[0][0], out[1][0]) <= 1e-13 and rel(out[0][1], out[1][1]) <= 1e-13
+
+
+@pytest.mark.parametrize("kind,tau,k", [("subsample", 40, 0), ("subcount", 30, 2), ("count", 25, 0),
+                                        ("subsample", 240, 0)])
+def test_dense_dual_explicit_parity(rs, kind, tau, k):
+    """Dense X with n < d: the dual route in EXPLICIT mode, A = X X^T + lambda I built
+    on the lower DMMA tiles of X^T; alpha and r after 15 steps and w = X^T alpha equal the
+    oracle's (tau 240 > 224: the W = L^{-1} slots)."""
+    X, y = rsinputs.dense_problem(300, 900, seed=4)
+    X, y = X.numpy(), y.numpy()
+    h = rs.rs_create_dense(X, y, 0.5, mode="explicit")
+    try:
+        w, rep = rs.rs_solve(h, kind, tau, 1.0, 0.5, 0.0, 15, 3, k, check_every=7, d=900, alpha=True)
+        alpha, r = rs.rs_get_state(h)
+    finally:
+        rs.rs_destroy(h)
+    ref = OV.solve(X, y, 0.5, kind, tau, 1.0, 0.5, 0.0, 15, seed=3, subcount_k=k)
+    assert ref["route"] == "dual"
+    assert rel(alpha, ref["w"]) <= 1e-10 and rel(r, ref["r"]) <= 1e-10
+    assert rel(rep["alpha"], ref["w"]) <= 1e-10
+    assert rel(w, ref["weights"]) <= 1e-10
+
+
+def test_dense_dual_implicit_unsupported(rs):
+    X, y = rsinputs.dense_problem(50, 80, seed=4)
+    with pytest.raises(rs.RSError, match="UNSUPPORTED"):
+        rs.rs_create_dense(X.numpy(), y.numpy(), 0.5, mode="implicit")
