@@ -446,7 +446,8 @@ cudaError_t launch_spmv(const long long* ptr, const int* idx, const double* val,
   const double avg = (double)nnz / (double)rows;
   const unsigned grid = (unsigned)std::max<long long>(1, std::min<long long>((rows * 32 + 255) / 256,
                                                                              (long long)num_sms * 16));
-  if (avg >= 24) k_spmv<32><<<grid, 256, 0, st>>>(ptr, idx, val, rows, heavy, v, out, ctrl);
+  // lanes per row: about four entries per lane or more (latency: the index -> gather chain)
+  if (avg >= 64) k_spmv<32><<<grid, 256, 0, st>>>(ptr, idx, val, rows, heavy, v, out, ctrl);
   else if (avg >= 12) k_spmv<16><<<grid, 256, 0, st>>>(ptr, idx, val, rows, heavy, v, out, ctrl);
   else if (avg >= 6) k_spmv<8><<<grid, 256, 0, st>>>(ptr, idx, val, rows, heavy, v, out, ctrl);
   else k_spmv<4><<<grid, 256, 0, st>>>(ptr, idx, val, rows, heavy, v, out, ctrl);
