@@ -478,7 +478,10 @@ def run_ours(args):
             pg.barrier()
         torch.cuda.synchronize()
 
-    chunk = min(args.steps, 256)   # graph size: very large graphs (10k+ nodes) delay submission
+    # iterations per graph launch: EXPLICIT iterations are a few kernel nodes each (1024 per graph);
+    # GRAM / IMPLICIT groups add several nodes per sketch-ahead slot, and a graph of 10k+ nodes
+    # delays its own submission (256 per graph)
+    chunk = min(args.steps, 1024 if (args.mode == "explicit" or cfg.kind == "kernel") else 256)
     # warm-up (W iterations, untimed) with the timed run's launch parameters, so the captured
     # iteration graph is built (and cached by the library) before the timed region
     rs.rs_solve(h, tol=0.0, max_iter=args.warmup, check_every=chunk, **common)
