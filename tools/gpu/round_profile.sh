@@ -9,11 +9,11 @@ B="timeout 1200 python bench.py"
 $B > gpurun_out/bench_c2_gram.json 2> gpurun_out/bench_c2_gram.err
 $B --impl reference --steps 3 --warmup 1 > gpurun_out/bench_c2_reference.json 2>/dev/null
 for m in explicit implicit; do $B --mode $m --no-cpu-baseline > gpurun_out/bench_c2_$m.json 2>/dev/null; done
-for c in c3 c4; do $B --config $c --steps 148 --max-iter-tol 20000 --cpu-seconds 20 > gpurun_out/bench_$c.json 2>/dev/null; done
-$B --config c4 --mode explicit --steps 148 --max-iter-tol 20000 --no-cpu-baseline > gpurun_out/bench_c4_explicit.json 2>/dev/null
-for c in c2 c3 c4; do $B --config $c --steps 148 --max-iter-tol 20000 --no-cpu-baseline --no-e2e --momentum theory > gpurun_out/bench_${c}_theory.json 2>/dev/null; done
-$B --config c5 --mode explicit --steps 148 --max-iter-tol 2000 > gpurun_out/bench_c5_explicit.json 2>/dev/null
-$B --config k1 --steps 148 --max-iter-tol 2000 --no-cpu-baseline > gpurun_out/bench_k1.json 2>/dev/null
+for c in c3 c4; do $B --config $c --max-iter-tol 20000 --cpu-seconds 20 > gpurun_out/bench_$c.json 2>/dev/null; done
+$B --config c4 --mode explicit --max-iter-tol 20000 --no-cpu-baseline > gpurun_out/bench_c4_explicit.json 2>/dev/null
+for c in c2 c3 c4; do $B --config $c --max-iter-tol 20000 --no-cpu-baseline --no-e2e --momentum theory > gpurun_out/bench_${c}_theory.json 2>/dev/null; done
+$B --config c5 --mode explicit --max-iter-tol 2000 > gpurun_out/bench_c5_explicit.json 2>/dev/null
+$B --config k1 --max-iter-tol 2000 --no-cpu-baseline > gpurun_out/bench_k1.json 2>/dev/null
 $B --config c5 --mode gram --steps 20 --max-iter-tol 400 --no-cpu-baseline --no-e2e > gpurun_out/bench_c5_gram.json 2>/dev/null
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 600 --csv --log-file gpurun_out/launches_c2_gram.csv python bench.py --steps 10 --warmup 3 --no-e2e --no-cpu-baseline --max-iter-tol 10 > /dev/null 2>&1
 M="--metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum --clock-control none --csv"
