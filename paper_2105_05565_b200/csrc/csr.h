@@ -56,6 +56,8 @@ struct CsrData {
   double* gh_work = nullptr;
   int* chunk_h0_none = nullptr;   // [nchunks + 1] zeros: k_gram_bands without its heavy phase
   size_t hr_smem = 0, gb_smem = 0;
+  int gb_cap = 0;          // band capacity (doubles) before the per-warp row staging
+  bool gb_stage = false;   // k_gram_bands<true>: light rows staged in shared memory
 };
 
 // per-iteration map coordinate -> (bucket << 1 | neg), -1 outside the sketch (subsample / SubCount)

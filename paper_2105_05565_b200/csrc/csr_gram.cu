@@ -39,7 +39,8 @@ constexpr unsigned FULL = 0xffffffffu;
 constexpr int HR_WARPS = 8;
 constexpr int HR_MAXTAU = 1536;
 constexpr int GB_THREADS = 1024;
-constexpr int GB_BUDGET = 26624;   // doubles of one band (208 KB of shared memory, 1 CTA / SM)
+constexpr int GB_BUDGET = 25856;   // doubles of one band (202 KB of shared memory + 24 KB of
+                                   // per-warp row staging, 1 CTA / SM)
 
 __host__ __device__ __forceinline__ long long tri(long long a) { return a * (a + 1) / 2; }
 
@@ -272,17 +273,20 @@ k_sel_scatter(DevSketch sk, const double* __restrict__ v, const long long* __res
 }
 
 // ------------------------------------------------------------------------------------ stage 2
+constexpr int GB_STAGE = 64;   // entries of a light row staged per warp (shared memory)
+constexpr size_t GB_STAGE_BYTES = (size_t)(GB_THREADS / 32) * GB_STAGE * 12;
+template <bool STAGE>
 __global__ void __launch_bounds__(GB_THREADS, 1)
 k_gram_bands(const long long* __restrict__ ptr, const int* __restrict__ hcnt,
              const int* __restrict__ hb, const double* __restrict__ hv,
              const int* __restrict__ band_a0, const long long* __restrict__ chunk_r0,
              long long heavy, const int* __restrict__ heavy_rows, const int* __restrict__ chunk_h0,
              double* __restrict__ part, long long part_stride, int slot, const Ctrl* ctrl,
-             const int* __restrict__ rlist = nullptr, const int* __restrict__ rcount = nullptr) {
+             const int* __restrict__ rlist, const int* __restrict__ rcount, int sz_cap) {
   // rlist (optional): visit only the listed rows (the touched rows of the selected-row path),
   // chunk y taking list entries [y n / nchunks, (y + 1) n / nchunks)
   if (slot_unused(ctrl, slot)) return;
-  extern __shared__ double band[];
+  extern __shared__ double band[];   // [sz_cap] band, then (STAGE) per-warp V[64], B[64]
   const int a0 = band_a0[blockIdx.x], a1 = band_a0[blockIdx.x + 1];
   const long long base = tri(a0);
   const int sz = (int)(tri(a1) - base);
@@ -318,6 +322,28 @@ k_gram_bands(const long long* __restrict__ ptr, const int* __restrict__ hcnt,
       // pairs (s, t), s0 <= s < s1, t <= s, enumerated q = tri(s) + t: every lane busy, its
       // cursor advancing by 32 pairs per step
       const int np = (int)(tri(s1) - tri(s0));
+      if (STAGE && s1 <= GB_STAGE && np >= 96) {   // (short rows: the copy does not pay)
+        // the row's first s1 entries staged in the warp's shared buffer: the pair loop reads
+        // shared memory only and forms the packed offset in 32-bit arithmetic
+        double* wV = reinterpret_cast<double*>(band + sz_cap) + warp * GB_STAGE;
+        int* wB = reinterpret_cast<int*>(band + sz_cap + (GB_THREADS / 32) * GB_STAGE) + warp * GB_STAGE;
+        __syncwarp();
+        for (int q = lane; q < s1; q += 32) {
+          wB[q] = B[q];
+          wV[q] = V[q];
+        }
+        __syncwarp();
+        const int ib = (int)base;
+        int ss = s0, tt = lane;
+        while (tt > ss) { tt -= ss + 1; ++ss; }
+        for (int p = lane; p < np; p += 32) {
+          const int bs = wB[ss];
+          atomicAdd(&band[bs * (bs + 1) / 2 - ib + wB[tt]], wV[ss] * wV[tt]);
+          tt += 32;
+          while (tt > ss) { tt -= ss + 1; ++ss; }
+        }
+        continue;
+      }
       int s = s0, t = lane;
       while (t > s) { t -= s + 1; ++s; }
       for (int p = lane; p < np; p += 32) {
@@ -622,7 +648,15 @@ rs_status Problem::csr_gram_workspace(int kind, int tau) {
   }
   c->gb_smem = (size_t)maxband * sizeof(double);
   c->hr_smem = (size_t)HR_WARPS * (tau + 32) * sizeof(double) + (size_t)HR_WARPS * ((tau + 31) / 32) * 4;
-  RS_CUDA(cudaFuncSetAttribute(k_gram_bands, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  c->gb_cap = (int)round_up(maxband, 2);
+  // staged light rows pay on long rows (c3: 50 entries, Gram 2.06 -> 1.85 ms); on short Zipf rows
+  // (c4: 10) the unstaged loop is 2 % faster
+  c->gb_stage = std::getenv("RS_GB_NOSTAGE") == nullptr && c->nnz >= 32 * std::max(1LL, R.rows) &&
+                (size_t)c->gb_cap * 8 + GB_STAGE_BYTES <= 227 * 1024;
+  if (c->gb_stage) c->gb_smem = (size_t)c->gb_cap * 8 + GB_STAGE_BYTES;
+  RS_CUDA(cudaFuncSetAttribute(k_gram_bands<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)std::max<size_t>(c->gb_smem, 48 * 1024)));
+  RS_CUDA(cudaFuncSetAttribute(k_gram_bands<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                (int)std::max<size_t>(c->gb_smem, 48 * 1024)));
   RS_CUDA(cudaFuncSetAttribute(k_hash_rows, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                (int)std::max<size_t>(c->hr_smem, 48 * 1024)));
@@ -681,10 +715,11 @@ rs_status Problem::csr_gram_into(const DevSketch& s, double* G, cudaEvent_t* ev,
     mark(RS_K_GRAM, 0);
     // a3/a4: (R S)^T (R S), lower triangle
     const bool hgemm = sel && c->nheavyR > 0;   // heavy rows already in gh
-    k_gram_bands<<<dim3((unsigned)c->nbands, (unsigned)c->nchunks), GB_THREADS, c->gb_smem, st>>>(
+    (c->gb_stage ? k_gram_bands<true> : k_gram_bands<false>)
+        <<<dim3((unsigned)c->nbands, (unsigned)c->nchunks), GB_THREADS, c->gb_smem, st>>>(
         R.ptr, c->hcnt, c->hb, c->hv, c->band_a0, c->chunk_r0, c->heavyR, c->heavy_rowsR,
         hgemm ? c->chunk_h0_none : c->chunk_h0, c->gpart, c->gpart_stride, slot, ctrl,
-        sel ? c->tlist : nullptr, sel ? c->tcount : nullptr);
+        sel ? c->tlist : nullptr, sel ? c->tcount : nullptr, c->gb_cap);
     RS_CUDA(cudaGetLastError());
     if (sel) RS_CUDA(cudaMemsetAsync(c->tcount, 0, sizeof(int), st));   // touched list consumed
     k_gram_band_reduce<<<tau, 256, 0, st>>>(c->gpart, c->nchunks, c->gpart_stride, G, ld_gram, slot,

@@ -1,0 +1,50 @@
+// Microbenchmark: scatter-add throughput into a 26k-double band (the CSR Gram's k_gram_bands
+// pattern): shared fp64 atomicAdd (CAS loop on sm_100a), racy shared RMW (ceiling), shared fp32
+// atomicAdd (native), global fp64 RED into a 1 MB L2-resident array.
+// nvcc -gencode arch=compute_100a,code=sm_100a -O3 tools/ubench_atom.cu -o tools/ubench_atom
+#include <cstdio>
+#include <cuda_runtime.h>
+constexpr int BAND = 26624, NOPS = 4096;
+__device__ __forceinline__ unsigned hsh(unsigned x) {
+  x ^= x >> 16; x *= 0x7feb352dU; x ^= x >> 15; x *= 0x846ca68bU; x ^= x >> 16; return x;
+}
+template <int V>
+__global__ void __launch_bounds__(1024, 1) k(double* g, float* gf) {
+  extern __shared__ double sb[];
+  for (int q = threadIdx.x; q < BAND; q += blockDim.x) sb[q] = 0;
+  __syncthreads();
+  unsigned st = hsh(blockIdx.x * 1024 + threadIdx.x);
+  const double v = 1.0 + threadIdx.x;
+  for (int i = 0; i < NOPS; ++i) {
+    st = hsh(st + i);
+    const int a = st % BAND;
+    if (V == 0) atomicAdd(&sb[a], v);
+    else if (V == 1) sb[a] += v;
+    else if (V == 2) atomicAdd(reinterpret_cast<float*>(sb) + a, (float)v);
+    else if (V == 3) atomicAdd(&g[(blockIdx.x & 3) * 0 + (st % 131072)], v);
+  }
+  __syncthreads();
+  for (int q = threadIdx.x; q < 64; q += blockDim.x) g[blockIdx.x * 64 + q + 200000] = sb[q];
+}
+int main() {
+  double* g; float* gf;
+  cudaMalloc(&g, 64 << 20); cudaMalloc(&gf, 4 << 20);
+  cudaMemset(g, 0, 64 << 20);
+  cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
+  const char* nm[4] = {"shared fp64 atomicAdd (CAS)", "shared racy RMW", "shared fp32 atomicAdd",
+                       "global fp64 RED (1 MB)"};
+  auto run = [&](int v, auto kern) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, BAND * 8);
+    float best = 1e9;
+    for (int it = 0; it < 5; ++it) {
+      cudaEventRecord(e0);
+      kern<<<148, 1024, BAND * 8>>>(g, gf);
+      cudaEventRecord(e1); cudaEventSynchronize(e1);
+      float ms; cudaEventElapsedTime(&ms, e0, e1); if (ms < best) best = ms;
+    }
+    const double ops = 148.0 * 1024 * NOPS;
+    printf("%-30s %8.3f ms  %6.2f ops/clk/SM (1.965 GHz)  %s\n", nm[v], best, ops / (best * 1e-3) / 148 / 1.965e9,
+           cudaGetErrorString(cudaGetLastError()));
+  };
+  run(0, k<0>); run(1, k<1>); run(2, k<2>); run(3, k<3>);
+}
