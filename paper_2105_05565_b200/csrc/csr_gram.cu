@@ -197,7 +197,11 @@ k_hash_rows_heavy(const long long* __restrict__ ptr, const int* __restrict__ idx
 // same lane order) reading the codes contiguously, and resets them; entries of heavy (Zipf-popular)
 // rows go straight into a dense tau-vector per heavy row (fp64 atomics) whose Gram contribution is
 // one lower-tile DMMA GEMM H^T H -- no scan of those long rows, no pair loop over them.
-__global__ void __launch_bounds__(256)
+// One warp per selected sample, 4 warps per block (the s = 1024 samples of c4 spread over every
+// SM); each lane walks 4 entries per step with independent load chains (colidx -> hidx / cscpos /
+// tflag), and first touches are appended with one warp-aggregated atomic on the list counter.
+constexpr int SE_WARPS = 4, SE_U = 4;
+__global__ void __launch_bounds__(SE_WARPS * 32)
 k_sel_emit(DevSketch sk, const long long* __restrict__ rowptr, const int* __restrict__ colidx,
            const double* __restrict__ vals, const int* __restrict__ cscpos, int* __restrict__ cmR,
            int* __restrict__ tflag, int* __restrict__ tlist, int* __restrict__ tcount,
@@ -205,22 +209,46 @@ k_sel_emit(DevSketch sk, const long long* __restrict__ rowptr, const int* __rest
            const Ctrl* ctrl) {
   if (slot_unused(ctrl, slot)) return;
   const int lane = threadIdx.x & 31;
-  const int e = blockIdx.x * 8 + (threadIdx.x >> 5);
+  const int e = blockIdx.x * SE_WARPS + (threadIdx.x >> 5);
   if (e >= sk.len) return;
   const int i = sk.coord[e];
   const int b = sk.bucket[e];
   const bool neg = sk.sign[e] <= 0;
   const int code = (b << 1) | (neg ? 1 : 0);
-  for (long long p = rowptr[i] + lane; p < rowptr[i + 1]; p += 32) {
-    const int f = colidx[p];
-    const int h = hidx[f];
-    if (h >= 0) {   // heavy (Zipf-popular) feature: straight into its dense tau-vector
-      const double x = vals[p];
-      atomicAdd(&hacc[(long long)h * ldh + b], neg ? -x : x);
-      continue;
+  const long long p1 = rowptr[i + 1];
+  for (long long pb = rowptr[i]; pb < p1; pb += 32 * SE_U) {   // warp-uniform trip count
+    int f[SE_U], h[SE_U];
+#pragma unroll
+    for (int u = 0; u < SE_U; ++u) {
+      const long long p = pb + 32 * u + lane;
+      f[u] = p < p1 ? colidx[p] : -1;
     }
-    cmR[cscpos[p]] = code;
-    if (tflag[f] == 0 && atomicExch(&tflag[f], 1) == 0) tlist[atomicAdd(tcount, 1)] = f;
+#pragma unroll
+    for (int u = 0; u < SE_U; ++u) h[u] = f[u] >= 0 ? hidx[f[u]] : -1;
+    bool need[SE_U];
+#pragma unroll
+    for (int u = 0; u < SE_U; ++u) {
+      const long long p = pb + 32 * u + lane;
+      need[u] = false;
+      if (f[u] < 0) continue;
+      if (h[u] >= 0) {   // heavy (Zipf-popular) feature: straight into its dense tau-vector
+        const double x = vals[p];
+        atomicAdd(&hacc[(long long)h[u] * ldh + b], neg ? -x : x);
+        continue;
+      }
+      cmR[cscpos[p]] = code;
+      need[u] = tflag[f[u]] == 0 && atomicExch(&tflag[f[u]], 1) == 0;
+    }
+#pragma unroll
+    for (int u = 0; u < SE_U; ++u) {
+      const unsigned m = __ballot_sync(FULL, need[u]);
+      if (!m) continue;
+      const int leader = __ffs(m) - 1;
+      int base = 0;
+      if (lane == leader) base = atomicAdd(tcount, __popc(m));
+      base = __shfl_sync(FULL, base, leader);
+      if (need[u]) tlist[base + __popc(m & ((1u << lane) - 1u))] = f[u];
+    }
   }
 }
 
@@ -259,13 +287,13 @@ k_sel_merge(const long long* __restrict__ ptr, const double* __restrict__ val, l
 // t = R v = X^T v for the dual with v = S delta nonzero on the s selected samples only: each
 // selected sample's X row is scattered into t (fp64 atomics at L2: t's summation order is not
 // fixed; t feeds u = X t, which every rank allreduces)
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(SE_WARPS * 32)
 k_sel_scatter(DevSketch sk, const double* __restrict__ v, const long long* __restrict__ rowptr,
               const int* __restrict__ colidx, const double* __restrict__ vals,
               double* __restrict__ t, const Ctrl* ctrl) {
   if (ctrl->done) return;
   const int lane = threadIdx.x & 31;
-  const int e = blockIdx.x * 8 + (threadIdx.x >> 5);
+  const int e = blockIdx.x * SE_WARPS + (threadIdx.x >> 5);
   if (e >= sk.len) return;
   const int i = sk.coord[e];
   const double sd = v[i];
@@ -688,7 +716,7 @@ rs_status Problem::csr_gram_into(const DevSketch& s, double* G, cudaEvent_t* ev,
   }
   if (R.rows > 0 && sel) {   // a2: rows of R S from the s selected rows of X
     RS_CUDA(cudaMemsetAsync(c->hcnt, 0, R.rows * sizeof(int), st));
-    k_sel_emit<<<(unsigned)std::max(1, (s.len + 7) / 8), 256, 0, st>>>(
+    k_sel_emit<<<(unsigned)std::max(1, (s.len + SE_WARPS - 1) / SE_WARPS), SE_WARPS * 32, 0, st>>>(
         s, c->rowptr, c->colidx, c->vals, c->cscpos, c->cmR, c->tflag, c->tlist, c->tcount, c->hidx,
         c->hacc, c->ldh, slot, ctrl);
     const unsigned grid = (unsigned)((long long)num_sms * 8);
@@ -743,7 +771,7 @@ rs_status Problem::csr_gram_apply(const double* v, double* u, const DevSketch* s
                               : RView{c->rowptr, c->colidx, c->vals, c->rows};
   if (s && c->cmR && s->kind != SK_COUNT) {   // dual, selected samples: t = R v from their X rows
     RS_CUDA(cudaMemsetAsync(c->tvec, 0, std::max<long long>(1, R.rows) * sizeof(double), st));
-    k_sel_scatter<<<(unsigned)std::max(1, (s->len + 7) / 8), 256, 0, st>>>(
+    k_sel_scatter<<<(unsigned)std::max(1, (s->len + SE_WARPS - 1) / SE_WARPS), SE_WARPS * 32, 0, st>>>(
         *s, v, c->rowptr, c->colidx, c->vals, c->tvec, ctrl);
     RS_CUDA(cudaGetLastError());
   } else {
