@@ -850,6 +850,12 @@ rs_status Problem::solve(const rs_solve_opts* o, double* w_out, rs_mem w_mem, do
   int ksum = 1;
   RS_TRY(validate_opts(this, o, &ksum));
   if (!w_out) return fail(RS_EINVAL, "w_out is NULL");
+  // RS_TIMING: host time of the solve's phases on stderr (diagnostics of the timed regions)
+  static const bool timing = std::getenv("RS_TIMING") != nullptr;
+  const auto h0 = std::chrono::steady_clock::now();
+  auto hms = [&](std::chrono::steady_clock::time_point a) {
+    return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - a).count();
+  };
   RS_CUDA(cudaSetDevice(device));
   const bool want_pipe = pipeline_applies(this, (int)o->tau);
   // iterations per CUDA-graph launch (between host reads of the stop flag)
@@ -991,6 +997,8 @@ rs_status Problem::solve(const rs_solve_opts* o, double* w_out, rs_mem w_mem, do
   cudaEvent_t t0, t1;
   RS_CUDA(cudaEventCreate(&t0));
   RS_CUDA(cudaEventCreate(&t1));
+  if (timing) fprintf(stderr, "[rs] solve preamble %.3f ms (graph %s)\n", hms(h0), rebuild ? "built" : "reused");
+  const auto h1 = std::chrono::steady_clock::now();
   RS_CUDA(cudaEventRecord(t0, st));
   // fused pipeline: slot set 0 (iterations 0 .. P-1) is formed and factored up front
   if (pipe_xg && !ctrl_host->done) RS_TRY(enqueue_precompute(o, P, nullptr));
@@ -1027,6 +1035,7 @@ rs_status Problem::solve(const rs_solve_opts* o, double* w_out, rs_mem w_mem, do
   }
   RS_CUDA(cudaEventRecord(t1, st));
   RS_CUDA(cudaEventSynchronize(t1));
+  const auto h2 = std::chrono::steady_clock::now();
   float solve_ms = 0;
   cudaEventElapsedTime(&solve_ms, t0, t1);
   cudaEventDestroy(t0);
@@ -1056,6 +1065,9 @@ rs_status Problem::solve(const rs_solve_opts* o, double* w_out, rs_mem w_mem, do
     return fail(RS_ENOTSPD, "Cholesky pivot <= 0 in S^T A S at iteration " + std::to_string(h.k));
   // outputs (also on divergence: the last iterate)
   RS_TRY(write_weights(w_out, w_mem, alpha_out));
+  if (timing)
+    fprintf(stderr, "[rs] solve loop %.3f ms host (%.3f device), %lld graph launches; outputs %.3f ms\n",
+            std::chrono::duration<double, std::milli>(h2 - h1).count(), solve_ms, graph_launches, hms(h2));
   if (rc == RS_EDIVERGED)
     return fail(RS_EDIVERGED, "residual diverged (non-finite or > 1e8 relative) at iteration " +
                                   std::to_string(h.k));
