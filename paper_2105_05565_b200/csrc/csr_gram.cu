@@ -108,7 +108,10 @@ __device__ __forceinline__ int cm_of(const int* __restrict__ cmap, const int* __
 }
 
 // light rows (<= heavy threshold): one warp per row, 32-row blocks of row pointers per warp,
-// 64 entries loaded per step
+// 64 entries loaded per step.  ALL (count sketch: every coordinate mapped): the first 64 entries
+// of the NEXT row (codes and values, loaded unconditionally) are in flight while the current row
+// merges, so the idx -> cmap -> val chain of one row overlaps the merge of the previous one.
+template <bool ALL>
 __global__ void __launch_bounds__(HR_WARPS * 32)
 k_hash_rows(const long long* __restrict__ ptr, const int* __restrict__ idx,
             const double* __restrict__ val, long long rows, long long heavy, const int* __restrict__ cmap,
@@ -125,6 +128,46 @@ k_hash_rows(const long long* __restrict__ ptr, const int* __restrict__ idx,
     const long long il = i0 + lane;
     const long long pa = il < rows ? ptr[il] : 0, pe = il < rows ? ptr[il + 1] : 0;
     const int nr = (int)min(32LL, rows - i0);
+    if (ALL) {
+      // prefetched head (first 64 entries) of row j
+      auto head = [&](int j, int& c0, int& c1, double& v0, double& v1) {
+        const long long a = __shfl_sync(FULL, pa, j), e = __shfl_sync(FULL, pe, j);
+        const long long t0 = a + lane, t1 = a + 32 + lane;
+        const bool in = e - a <= heavy;
+        c0 = in ? cm_of(cmap, idx, t0, e) : -1;
+        c1 = in ? cm_of(cmap, idx, t1, e) : -1;
+        v0 = in && t0 < e ? val[t0] : 0.0;
+        v1 = in && t1 < e ? val[t1] : 0.0;
+      };
+      int nc0, nc1;
+      double nv0, nv1;
+      head(0, nc0, nc1, nv0, nv1);
+      for (int j = 0; j < nr; ++j) {
+        const int cm0 = nc0, cm1 = nc1;
+        const double v0 = nv0, v1 = nv1;
+        if (j + 1 < nr) head(j + 1, nc0, nc1, nv0, nv1);
+        const long long a = __shfl_sync(FULL, pa, j), e = __shfl_sync(FULL, pe, j);
+        if (e - a > heavy) continue;   // k_hash_rows_heavy
+        bool touched = false;
+        if (__ballot_sync(FULL, cm0 >= 0 || cm1 >= 0)) {
+          touched = true;
+          M.add(cm0, (cm0 & 1) ? -v0 : v0, lane);
+          M.add(cm1, (cm1 & 1) ? -v1 : v1, lane);
+        }
+        for (long long base = a + 64; base < e; base += 64) {   // rows longer than 64
+          const long long t0 = base + lane, t1 = base + 32 + lane;
+          const int c0 = cm_of(cmap, idx, t0, e), c1 = cm_of(cmap, idx, t1, e);
+          if (!__ballot_sync(FULL, c0 >= 0 || c1 >= 0)) continue;
+          touched = true;
+          const double w0 = c0 >= 0 ? val[t0] : 0.0, w1 = c1 >= 0 ? val[t1] : 0.0;
+          M.add(c0, (c0 & 1) ? -w0 : w0, lane);
+          M.add(c1, (c1 & 1) ? -w1 : w1, lane);
+        }
+        const int total = touched ? M.flush(a, hb, hv, lane) : 0;
+        if (lane == 0) hcnt[i0 + j] = total;
+      }
+      continue;
+    }
     for (int j = 0; j < nr; ++j) {
       const long long a = __shfl_sync(FULL, pa, j), e = __shfl_sync(FULL, pe, j);
       if (e - a > heavy) continue;   // k_hash_rows_heavy
@@ -686,7 +729,9 @@ rs_status Problem::csr_gram_workspace(int kind, int tau) {
                                (int)std::max<size_t>(c->gb_smem, 48 * 1024)));
   RS_CUDA(cudaFuncSetAttribute(k_gram_bands<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                (int)std::max<size_t>(c->gb_smem, 48 * 1024)));
-  RS_CUDA(cudaFuncSetAttribute(k_hash_rows, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  RS_CUDA(cudaFuncSetAttribute(k_hash_rows<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)std::max<size_t>(c->hr_smem, 48 * 1024)));
+  RS_CUDA(cudaFuncSetAttribute(k_hash_rows<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                (int)std::max<size_t>(c->hr_smem, 48 * 1024)));
   RS_CUDA(cudaFuncSetAttribute(k_hash_rows_heavy, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                (int)std::max<size_t>(c->hr_smem, 48 * 1024)));
@@ -731,8 +776,10 @@ rs_status Problem::csr_gram_into(const DevSketch& s, double* G, cudaEvent_t* ev,
   } else if (R.rows > 0) {   // a2: rows of R S, merged and bucket-sorted
     const unsigned grid = (unsigned)std::max<long long>(
         1, std::min<long long>((R.rows + HR_WARPS - 1) / HR_WARPS, (long long)num_sms * 8));
-    k_hash_rows<<<grid, HR_WARPS * 32, c->hr_smem, st>>>(R.ptr, R.idx, R.val, R.rows, c->heavyR,
-                                                          cmap, tau, c->hb, c->hv, c->hcnt, slot, ctrl);
+    static const bool no_hpf = std::getenv("RS_HR_NOPF") != nullptr;
+    (s.kind == SK_COUNT && !no_hpf ? k_hash_rows<true> : k_hash_rows<false>)
+        <<<grid, HR_WARPS * 32, c->hr_smem, st>>>(R.ptr, R.idx, R.val, R.rows, c->heavyR, cmap, tau,
+                                                  c->hb, c->hv, c->hcnt, slot, ctrl);
     if (c->nheavyR > 0)
       k_hash_rows_heavy<<<c->nheavyR, HR_WARPS * 32, c->hr_smem, st>>>(
           R.ptr, R.idx, R.val, c->heavy_rowsR, cmap, tau, c->hb, c->hv, c->hcnt, slot, ctrl);
