@@ -30,6 +30,7 @@ struct CsrData {
   int nbands = 0, nchunks = 0;
   double* gpart = nullptr;       // [nchunks][tau (tau + 1) / 2] packed lower-triangle partials
   long long gpart_stride = 0;
+  double* gtrace = nullptr;      // trace(G) of the current slot's merged rows (fixed-point scale)
   double* tvec = nullptr;        // [R rows]  t = R (S delta)
   // rows longer than `heavy` are handled one CTA per row (Zipf-popular features of c4)
   long long heavyR = 0, heavyRt = 0;

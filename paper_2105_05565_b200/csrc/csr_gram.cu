@@ -51,6 +51,7 @@ struct WarpMerge {
   double* stage;
   unsigned* bits;
   int nw;
+  double sq = 0.0;   // lane-local sum of squares of the flushed values (trace of the row Grams)
   __device__ WarpMerge(double* hsm, int tau, int w) {
     nw = (tau + 31) >> 5;
     acc = hsm + (size_t)w * tau;
@@ -90,8 +91,10 @@ struct WarpMerge {
       long long pos = a + total + incl - c;
       for (; word; word &= word - 1) {
         const int bucket = wi * 32 + __ffs(word) - 1;
+        const double x = acc[bucket];
         hb[pos] = bucket;
-        hv[pos] = acc[bucket];
+        hv[pos] = x;
+        sq += x * x;
         ++pos;
       }
       if (wi < nw) bits[wi] = 0u;
@@ -100,7 +103,30 @@ struct WarpMerge {
     __syncwarp();
     return total;
   }
+  // the warp's share of trace(G) = sum over flushed entries of v^2 (one fp64 atomic per warp)
+  __device__ __forceinline__ void trace_out(double* gtr, int lane) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) sq += __shfl_xor_sync(FULL, sq, o);
+    if (lane == 0 && sq != 0.0) atomicAdd(gtr, sq);
+  }
 };
+
+// Fixed-point accumulation of the CSR Gram bands (sm_100a has no native shared fp64 add; 32-bit
+// shared atomics are native): an entry is an int64 in units of 2^-E, added as two 32-bit words
+// with the carry of the low word taken from the value the low-word atomic returns.  Two's
+// complement addition is exact modulo 2^64, so the result is exact whenever the final value fits:
+// |G_ab| <= max_a G_aa <= trace(G) < 2^(ilogb(trace) + 1) and E = 61 - ilogb(trace) leave two bits
+// of headroom.  Each product is rounded once to 2^-E = trace * 2^-61 (about 2^-53 of a diagonal
+// entry for tau = 500); the sum itself is exact and order independent.
+__device__ __forceinline__ void fx_add(unsigned* w, long long x) {
+  const unsigned lo = (unsigned)x;
+  const unsigned old = atomicAdd(w, lo);
+  const int h = (int)(x >> 32) + (old + lo < old ? 1 : 0);
+  if (h) atomicAdd(reinterpret_cast<int*>(w) + 1, h);
+}
+__device__ __forceinline__ int fx_exponent(double trace) {
+  return trace > 0.0 && trace < 1e300 ? 61 - ilogb(trace) : 0;
+}
 
 __device__ __forceinline__ int cm_of(const int* __restrict__ cmap, const int* __restrict__ idx,
                                      long long t, long long e) {
@@ -116,7 +142,7 @@ __global__ void __launch_bounds__(HR_WARPS * 32)
 k_hash_rows(const long long* __restrict__ ptr, const int* __restrict__ idx,
             const double* __restrict__ val, long long rows, long long heavy, const int* __restrict__ cmap,
             int tau, int* __restrict__ hb, double* __restrict__ hv, int* __restrict__ hcnt,
-            int slot, const Ctrl* ctrl) {
+            int slot, const Ctrl* ctrl, double* __restrict__ gtr) {
   if (slot_unused(ctrl, slot)) return;
   extern __shared__ double hsm[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -185,6 +211,7 @@ k_hash_rows(const long long* __restrict__ ptr, const int* __restrict__ idx,
       if (lane == 0) hcnt[i0 + j] = total;
     }
   }
+  M.trace_out(gtr, lane);
 }
 
 // heavy rows: one CTA per row; warp w merges chunks w, w + 8, ... into its own accumulator, then the
@@ -193,7 +220,8 @@ __global__ void __launch_bounds__(HR_WARPS * 32)
 k_hash_rows_heavy(const long long* __restrict__ ptr, const int* __restrict__ idx,
                   const double* __restrict__ val, const int* __restrict__ heavy_rows,
                   const int* __restrict__ cmap, int tau, int* __restrict__ hb,
-                  double* __restrict__ hv, int* __restrict__ hcnt, int slot, const Ctrl* ctrl) {
+                  double* __restrict__ hv, int* __restrict__ hcnt, int slot, const Ctrl* ctrl,
+                  double* __restrict__ gtr) {
   if (slot_unused(ctrl, slot)) return;
   extern __shared__ double hsm[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -229,6 +257,7 @@ k_hash_rows_heavy(const long long* __restrict__ ptr, const int* __restrict__ idx
   if (warp == 0) {
     const int total = M.flush(a, hb, hv, lane);
     if (lane == 0) hcnt[i] = total;
+    M.trace_out(gtr, lane);
   }
 }
 
@@ -299,7 +328,7 @@ __global__ void __launch_bounds__(HR_WARPS * 32)
 k_sel_merge(const long long* __restrict__ ptr, const double* __restrict__ val, long long heavy,
             int* __restrict__ cmR, int* __restrict__ tflag, const int* __restrict__ tlist,
             const int* __restrict__ tcount, int tau, int* __restrict__ hb, double* __restrict__ hv,
-            int* __restrict__ hcnt, int slot, const Ctrl* ctrl) {
+            int* __restrict__ hcnt, int slot, const Ctrl* ctrl, double* __restrict__ gtr) {
   if (slot_unused(ctrl, slot)) return;
   extern __shared__ double hsm[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -325,6 +354,7 @@ k_sel_merge(const long long* __restrict__ ptr, const double* __restrict__ val, l
     const int total = M.flush(a, hb, hv, lane);
     if (lane == 0) hcnt[f] = total;
   }
+  M.trace_out(gtr, lane);
 }
 
 // t = R v = X^T v for the dual with v = S delta nonzero on the s selected samples only: each
@@ -353,7 +383,8 @@ k_gram_bands(const long long* __restrict__ ptr, const int* __restrict__ hcnt,
              const int* __restrict__ band_a0, const long long* __restrict__ chunk_r0,
              long long heavy, const int* __restrict__ heavy_rows, const int* __restrict__ chunk_h0,
              double* __restrict__ part, long long part_stride, int slot, const Ctrl* ctrl,
-             const int* __restrict__ rlist, const int* __restrict__ rcount, int sz_cap) {
+             const int* __restrict__ rlist, const int* __restrict__ rcount, int sz_cap,
+             const double* __restrict__ gtr) {
   // rlist (optional): visit only the listed rows (the touched rows of the selected-row path),
   // chunk y taking list entries [y n / nchunks, (y + 1) n / nchunks)
   if (slot_unused(ctrl, slot)) return;
@@ -361,7 +392,12 @@ k_gram_bands(const long long* __restrict__ ptr, const int* __restrict__ hcnt,
   const int a0 = band_a0[blockIdx.x], a1 = band_a0[blockIdx.x + 1];
   const long long base = tri(a0);
   const int sz = (int)(tri(a1) - base);
-  for (int q = threadIdx.x; q < sz; q += GB_THREADS) band[q] = 0.0;
+  // the band holds int64 fixed-point entries (fx_add); trace(G) of this slot's merged rows
+  const int E = fx_exponent(*gtr);
+  const double sc = ldexp(1.0, E);
+  unsigned* bw = reinterpret_cast<unsigned*>(band);
+  long long* bl = reinterpret_cast<long long*>(band);
+  for (int q = threadIdx.x; q < sz; q += GB_THREADS) bl[q] = 0;
   __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   long long r0 = chunk_r0[blockIdx.y], r1 = chunk_r0[blockIdx.y + 1];
@@ -376,18 +412,42 @@ k_gram_bands(const long long* __restrict__ ptr, const int* __restrict__ hcnt,
     int Ll = rk < r1 ? hcnt[rl] : 0;
     const long long offl = Ll ? ptr[rl] : 0;
     if (Ll && ptr[rl + 1] - offl > heavy) Ll = 0;   // heavy phase below
-    for (unsigned nz = __ballot_sync(FULL, Ll > 0); nz; nz &= nz - 1) {
+    // STAGE: the first 64 entries of the NEXT row of the ballot order are loaded into registers
+    // while the current row's pairs run (its band bounds and staging then need no global loads)
+    const unsigned nz0 = __ballot_sync(FULL, Ll > 0);
+    int pb0 = INT_MAX, pb1 = INT_MAX;
+    double pv0 = 0.0, pv1 = 0.0;
+    auto fetch = [&](unsigned m) {   // warp-uniform m
+      if (!m) return;
+      const int jj = __ffs(m) - 1;
+      const int LL = __shfl_sync(FULL, Ll, jj);
+      const long long oo = __shfl_sync(FULL, offl, jj);
+      pb0 = lane < LL ? hb[oo + lane] : INT_MAX;
+      pb1 = lane + 32 < LL ? hb[oo + 32 + lane] : INT_MAX;
+      pv0 = lane < LL ? hv[oo + lane] : 0.0;
+      pv1 = lane + 32 < LL ? hv[oo + 32 + lane] : 0.0;
+    };
+    if (STAGE) fetch(nz0);
+    for (unsigned nz = nz0; nz; nz &= nz - 1) {
+      const int cb0 = pb0, cb1 = pb1;
+      const double cv0 = pv0, cv1 = pv1;
+      if (STAGE) fetch(nz & (nz - 1));
       const int j = __ffs(nz) - 1;
       const int L = __shfl_sync(FULL, Ll, j);
       const long long off = __shfl_sync(FULL, offl, j);
       const int* B = hb + off;
       const double* V = hv + off;
       int s0 = 0, s1 = 0;   // entries with bucket < a0, < a1 (B ascending)
-      for (int q = 0; q < L; q += 32) {
-        const int bq = q + lane < L ? B[q + lane] : INT_MAX;
-        s0 += __popc(__ballot_sync(FULL, bq < a0));
-        s1 += __popc(__ballot_sync(FULL, bq < a1));
-        if (__shfl_sync(FULL, bq, 31) >= a1) break;
+      if (STAGE && L <= GB_STAGE) {
+        s0 = __popc(__ballot_sync(FULL, cb0 < a0)) + __popc(__ballot_sync(FULL, cb1 < a0));
+        s1 = __popc(__ballot_sync(FULL, cb0 < a1)) + __popc(__ballot_sync(FULL, cb1 < a1));
+      } else {
+        for (int q = 0; q < L; q += 32) {
+          const int bq = q + lane < L ? B[q + lane] : INT_MAX;
+          s0 += __popc(__ballot_sync(FULL, bq < a0));
+          s1 += __popc(__ballot_sync(FULL, bq < a1));
+          if (__shfl_sync(FULL, bq, 31) >= a1) break;
+        }
       }
       if (s1 == s0) continue;
       // pairs (s, t), s0 <= s < s1, t <= s, enumerated q = tri(s) + t: every lane busy, its
@@ -399,26 +459,49 @@ k_gram_bands(const long long* __restrict__ ptr, const int* __restrict__ hcnt,
         double* wV = reinterpret_cast<double*>(band + sz_cap) + warp * GB_STAGE;
         int* wB = reinterpret_cast<int*>(band + sz_cap + (GB_THREADS / 32) * GB_STAGE) + warp * GB_STAGE;
         __syncwarp();
-        for (int q = lane; q < s1; q += 32) {
-          wB[q] = B[q];
-          wV[q] = V[q];
+        if (L <= GB_STAGE) {
+          if (lane < s1) { wB[lane] = cb0; wV[lane] = cv0; }
+          if (lane + 32 < s1) { wB[lane + 32] = cb1; wV[lane + 32] = cv1; }
+        } else {
+          for (int q = lane; q < s1; q += 32) {
+            wB[q] = B[q];
+            wV[q] = V[q];
+          }
         }
         __syncwarp();
         const int ib = (int)base;
         int ss = s0, tt = lane;
         while (tt > ss) { tt -= ss + 1; ++ss; }
-        for (int p = lane; p < np; p += 32) {
-          const int bs = wB[ss];
-          atomicAdd(&band[bs * (bs + 1) / 2 - ib + wB[tt]], wV[ss] * wV[tt]);
-          tt += 32;
+        // two pairs per lane per step: both low-word atomics are in flight before either carry
+        int p = lane;
+        for (; p + 32 < np; p += 64) {
+          int s2 = ss, t2 = tt + 32;
+          while (t2 > s2) { t2 -= s2 + 1; ++s2; }
+          const int b1 = wB[ss], b2 = wB[s2];
+          unsigned* w1 = bw + 2 * (b1 * (b1 + 1) / 2 - ib + wB[tt]);
+          unsigned* w2 = bw + 2 * (b2 * (b2 + 1) / 2 - ib + wB[t2]);
+          const long long x1 = __double2ll_rn(wV[ss] * wV[tt] * sc);
+          const long long x2 = __double2ll_rn(wV[s2] * wV[t2] * sc);
+          const unsigned o1 = atomicAdd(w1, (unsigned)x1);
+          const unsigned o2 = atomicAdd(w2, (unsigned)x2);
+          const int h1 = (int)(x1 >> 32) + (o1 + (unsigned)x1 < o1 ? 1 : 0);
+          const int h2 = (int)(x2 >> 32) + (o2 + (unsigned)x2 < o2 ? 1 : 0);
+          if (h1) atomicAdd(reinterpret_cast<int*>(w1) + 1, h1);
+          if (h2) atomicAdd(reinterpret_cast<int*>(w2) + 1, h2);
+          ss = s2;
+          tt = t2 + 32;
           while (tt > ss) { tt -= ss + 1; ++ss; }
+        }
+        if (p < np) {
+          const int bs = wB[ss];
+          fx_add(bw + 2 * (bs * (bs + 1) / 2 - ib + wB[tt]), __double2ll_rn(wV[ss] * wV[tt] * sc));
         }
         continue;
       }
       int s = s0, t = lane;
       while (t > s) { t -= s + 1; ++s; }
       for (int p = lane; p < np; p += 32) {
-        atomicAdd(&band[tri(B[s]) - base + B[t]], V[s] * V[t]);
+        fx_add(bw + 2 * (tri(B[s]) - base + B[t]), __double2ll_rn(V[s] * V[t] * sc));
         t += 32;
         while (t > s) { t -= s + 1; ++s; }
       }
@@ -441,20 +524,23 @@ k_gram_bands(const long long* __restrict__ ptr, const int* __restrict__ hcnt,
         const int s = q + __ffs(mine) - 1;
         const int bs = B[s];
         const double vs = V[s];
-        double* rowp = band + (tri(bs) - base);
-        for (int t = lane; t <= s; t += 32) rowp[B[t]] += vs * V[t];
+        long long* rowp = bl + (tri(bs) - base);
+        for (int t = lane; t <= s; t += 32) rowp[B[t]] += __double2ll_rn(vs * V[t] * sc);
       }
     }
   }
   __syncthreads();
   double* out = part + blockIdx.y * part_stride + base;
-  for (int q = threadIdx.x; q < sz; q += GB_THREADS) out[q] = band[q];
+  const double isc = ldexp(1.0, -E);
+  for (int q = threadIdx.x; q < sz; q += GB_THREADS) out[q] = (double)bl[q] * isc;
 }
 
 __global__ void k_gram_band_reduce(const double* __restrict__ part, int nchunks,
                                    long long part_stride, double* __restrict__ G, long long ldg,
-                                   int slot, const Ctrl* ctrl, const double* __restrict__ gh = nullptr) {
+                                   int slot, const Ctrl* ctrl, const double* __restrict__ gh,
+                                   double* __restrict__ gtr) {
   if (slot_unused(ctrl, slot)) return;
+  if (blockIdx.x == 0 && threadIdx.x == 0) *gtr = 0.0;   // consumed by k_gram_bands (stream order)
   const int a = blockIdx.x;
   const long long base = tri(a);
   for (int c = threadIdx.x; c <= a; c += blockDim.x) {
@@ -576,6 +662,7 @@ void Problem::csr_gram_free() {
   dfree(csr->band_a0);
   dfree(csr->chunk_r0);
   dfree(csr->gpart);
+  dfree(csr->gtrace);
   dfree(csr->tvec);
   dfree(csr->heavy_rowsR);
   dfree(csr->heavy_rowsRt);
@@ -660,6 +747,8 @@ rs_status Problem::csr_gram_workspace(int kind, int tau) {
   RS_CUDA(cudaGetLastError());
   c->gpart_stride = round_up(total, 4);
   RS_TRY(dalloc(&c->gpart, (size_t)c->gpart_stride * c->nchunks));
+  RS_TRY(dalloc(&c->gtrace, 1));
+  RS_CUDA(cudaMemsetAsync(c->gtrace, 0, sizeof(double), st));
   // heavy-row lists of R and R^T
   {
     const RView Rt = route == 1 ? RView{c->colptr, c->rowidx, c->cvals, c->cols}
@@ -767,7 +856,7 @@ rs_status Problem::csr_gram_into(const DevSketch& s, double* G, cudaEvent_t* ev,
     const unsigned grid = (unsigned)((long long)num_sms * 8);
     k_sel_merge<<<grid, HR_WARPS * 32, c->hr_smem, st>>>(R.ptr, R.val, c->heavyR, c->cmR, c->tflag,
                                                          c->tlist, c->tcount, tau, c->hb, c->hv,
-                                                         c->hcnt, slot, ctrl);
+                                                         c->hcnt, slot, ctrl, c->gtrace);
     if (c->nheavyR > 0) {   // heavy rows: H^T H on the lower DMMA tiles, then H cleared
       RS_CUDA(tma_gemm_launch(c->tg_heavy, c->gh, ld_gram, c->gh_work, ctrl, st));
       RS_CUDA(cudaMemsetAsync(c->hacc, 0, (size_t)c->nheavyR * c->ldh * sizeof(double), st));
@@ -779,10 +868,10 @@ rs_status Problem::csr_gram_into(const DevSketch& s, double* G, cudaEvent_t* ev,
     static const bool no_hpf = std::getenv("RS_HR_NOPF") != nullptr;
     (s.kind == SK_COUNT && !no_hpf ? k_hash_rows<true> : k_hash_rows<false>)
         <<<grid, HR_WARPS * 32, c->hr_smem, st>>>(R.ptr, R.idx, R.val, R.rows, c->heavyR, cmap, tau,
-                                                  c->hb, c->hv, c->hcnt, slot, ctrl);
+                                                  c->hb, c->hv, c->hcnt, slot, ctrl, c->gtrace);
     if (c->nheavyR > 0)
       k_hash_rows_heavy<<<c->nheavyR, HR_WARPS * 32, c->hr_smem, st>>>(
-          R.ptr, R.idx, R.val, c->heavy_rowsR, cmap, tau, c->hb, c->hv, c->hcnt, slot, ctrl);
+          R.ptr, R.idx, R.val, c->heavy_rowsR, cmap, tau, c->hb, c->hv, c->hcnt, slot, ctrl, c->gtrace);
     RS_CUDA(cudaGetLastError());
   }
   if (R.rows > 0) {
@@ -794,11 +883,11 @@ rs_status Problem::csr_gram_into(const DevSketch& s, double* G, cudaEvent_t* ev,
         <<<dim3((unsigned)c->nbands, (unsigned)c->nchunks), GB_THREADS, c->gb_smem, st>>>(
         R.ptr, c->hcnt, c->hb, c->hv, c->band_a0, c->chunk_r0, c->heavyR, c->heavy_rowsR,
         hgemm ? c->chunk_h0_none : c->chunk_h0, c->gpart, c->gpart_stride, slot, ctrl,
-        sel ? c->tlist : nullptr, sel ? c->tcount : nullptr, c->gb_cap);
+        sel ? c->tlist : nullptr, sel ? c->tcount : nullptr, c->gb_cap, c->gtrace);
     RS_CUDA(cudaGetLastError());
     if (sel) RS_CUDA(cudaMemsetAsync(c->tcount, 0, sizeof(int), st));   // touched list consumed
     k_gram_band_reduce<<<tau, 256, 0, st>>>(c->gpart, c->nchunks, c->gpart_stride, G, ld_gram, slot,
-                                            ctrl, hgemm ? c->gh : nullptr);
+                                            ctrl, hgemm ? c->gh : nullptr, c->gtrace);
     RS_CUDA(cudaGetLastError());
   } else {
     mark(RS_K_XS, 1);
