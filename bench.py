@@ -238,7 +238,10 @@ def _csr_column_block(np, rowptr, colidx, vals, c0, clen):
     return rp, (colidx[keep] - c0).astype(np.int32), vals[keep]
 
 
-SMEM_PEAK_GBS = 148 * 128 * 1.965   # shared-memory pipe, 128 B/clk/SM x 148 SMs x 1965 MHz (GB/s)
+# CSR Gram pair updates: int64 fixed-point adds (two u32 shared atomics) on random addresses,
+# measured 3.26 per clock per SM (tools/ubench_atom.cu, profiles/r01_ubench_atom.txt), x 148 SMs x
+# 1965 MHz, in 1e9 updates/s
+SMEM_FXADD_PEAK = 3.26 * 148 * 1.965
 
 
 def _traffic(cfg, args, cls):
@@ -345,14 +348,14 @@ def _roofline(args, cfg, world, kms, kl, dom, prof_ms, host, rs):
         if args.mode == "gram" and dom in ("gram", "xs"):
             ent, pairs, sel = _csr_pairs(rs, cfg, host)
             if dom == "gram":
-                w = pairs * 16.0 / world
+                w = pairs / world
                 roof = dict(kernel="k_gram_bands: G_lower += v_i v_i^T over the merged rows of R S "
-                                   "(shared-memory fp64 read-modify-write per pair)", bound="alu",
-                            achieved=w / (ms * 1e-3) / 1e9, peak=SMEM_PEAK_GBS, unit="GB/s",
-                            peak_source="shared-memory pipe 128 B/clk/SM x 148 SMs x 1965 MHz "
-                                        "(B200_PROFILING.md unit counts and clocks)",
-                            algorithmic_per_launch=f"{w:.3e} bytes (16 B x {pairs:.3e} pair "
-                                                   f"updates, sketch of iteration 0)")
+                                   "(one int64 fixed-point shared-memory add per pair)", bound="alu",
+                            achieved=w / (ms * 1e-3) / 1e9, peak=SMEM_FXADD_PEAK, unit="Gupdates/s",
+                            peak_source="shared-memory fixed-point add on random addresses "
+                                        "(2 x u32 atomics, tools/ubench_atom.cu on this pool's "
+                                        "B200: 3.26 per clk per SM) x 148 SMs x 1965 MHz",
+                            algorithmic_per_launch=f"{w:.3e} pair updates (sketch of iteration 0)")
             elif sel is not None:   # dual, subsample / SubCount: the selected-row path
                 se, tn = sel
                 rows_r = cfg.d

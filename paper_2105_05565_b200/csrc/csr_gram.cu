@@ -14,8 +14,8 @@
 //   k_gram_bands  stage 2: G_lower = sum_i v_i v_i^T, v_i = row i of R S.  The packed lower triangle
 //                 is cut into bands of G rows that fit one CTA's shared memory; CTA (band, chunk)
 //                 accumulates, for the rows of its nnz-balanced chunk, every pair (s, t), t <= s, of
-//                 merged entries whose row bucket b_s lies in the band (shared fp64 atomics), then
-//                 writes its band to a per-chunk partial; k_gram_band_reduce sums the partials in
+//                 merged entries whose row bucket b_s lies in the band (int64 fixed-point shared
+//                 atomics, fx_add: exact sums), then writes its band to a per-chunk partial; k_gram_band_reduce sums the partials in
 //                 chunk order into the row-major Gram.
 //   k_spmv        t = R (S d), u = R^T t through the CSR and CSC copies (sub-warp per row).
 //
@@ -108,6 +108,20 @@ struct WarpMerge {
 #pragma unroll
     for (int o = 16; o; o >>= 1) sq += __shfl_xor_sync(FULL, sq, o);
     if (lane == 0 && sq != 0.0) atomicAdd(gtr, sq);
+  }
+  // the block's share: warps reduced in shared memory, one fp64 atomic per block (every thread of
+  // the block calls it; ~1e4 same-address atomics per launch serialise at L2)
+  __device__ __forceinline__ void trace_out_block(double* gtr, int lane, int warp) {
+    __shared__ double red[HR_WARPS];
+#pragma unroll
+    for (int o = 16; o; o >>= 1) sq += __shfl_xor_sync(FULL, sq, o);
+    if (lane == 0) red[warp] = sq;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double t = 0.0;
+      for (int w = 0; w < HR_WARPS; ++w) t += red[w];
+      if (t != 0.0) atomicAdd(gtr, t);
+    }
   }
 };
 
@@ -211,7 +225,7 @@ k_hash_rows(const long long* __restrict__ ptr, const int* __restrict__ idx,
       if (lane == 0) hcnt[i0 + j] = total;
     }
   }
-  M.trace_out(gtr, lane);
+  M.trace_out_block(gtr, lane, warp);
 }
 
 // heavy rows: one CTA per row; warp w merges chunks w, w + 8, ... into its own accumulator, then the
@@ -354,7 +368,7 @@ k_sel_merge(const long long* __restrict__ ptr, const double* __restrict__ val, l
     const int total = M.flush(a, hb, hv, lane);
     if (lane == 0) hcnt[f] = total;
   }
-  M.trace_out(gtr, lane);
+  M.trace_out_block(gtr, lane, warp);
 }
 
 // t = R v = X^T v for the dual with v = S delta nonzero on the s selected samples only: each

@@ -324,6 +324,24 @@ def test_csr_primal_long_rows(rs, kind, tau, k, mode):
     assert rel(r, ref["r"]) <= 1e-10
 
 
+def test_csr_primal_gram_bitwise_reproducible(rs):
+    """CSR primal GRAM with a count sketch: row hashing merges in a fixed lane order, the Gram bands
+    are exact int64 fixed-point sums (DESIGN R26), the band partials are reduced in chunk order and
+    the SpMVs have fixed per-row order, so two solves give bit-identical iterates (the fp64 CAS
+    adds this replaced did not).  Rows of 70 entries exercise the staged pair loop."""
+    n, d = 3000, 400
+    rp, ci, v, y, Xs = _csr_primal(n, d, per_row=70, seed=11)
+    h = rs.rs_create_csr(n, d, rp, ci, v, y, 1e-2, mode="gram")
+    try:
+        w1, _ = rs.rs_solve(h, "count", 64, 1.0, 0.5, 0.0, 30, seed=4)
+        w2, _ = rs.rs_solve(h, "count", 64, 1.0, 0.5, 0.0, 30, seed=4)
+    finally:
+        rs.rs_destroy(h)
+    assert np.array_equal(w1, w2)
+    ref = OV.solve(Xs, y, 1e-2, "count", 64, 1.0, 0.5, 0.0, 30, seed=4)
+    assert rel(w1, ref["w"]) <= 1e-10
+
+
 @pytest.mark.parametrize("kind,tau,k", [("subsample", 260, 0), ("count", 300, 0), ("subcount", 230, 2)])
 @pytest.mark.parametrize("mode", ["explicit", "gram"])
 def test_dense_large_tau_sketch_ahead(rs, kind, tau, k, mode):
@@ -669,8 +687,9 @@ def test_process_switches_parity(tmp_path, env):
 def test_csr_dual_selected_rows_match_full_scan(rs, monkeypatch, kind, tau, k):
     """The dual selected-row path (k_sel_emit / k_sel_merge / k_sel_heavy) merges every touched row
     of R = X^T in the same order as the full-scan k_hash_rows, so the rows of R S are identical;
-    the iterates then agree to rounding (k_gram_bands accumulates with shared-memory fp64 atomics,
-    whose order is not fixed).  RS_NO_SELROWS=1 selects the full scan (read per workspace)."""
+    the iterates then agree to rounding (heavy rows enter the Gram through a DMMA GEMM on the
+    selected-row path and through the band kernel on the full scan, and the u = X t scatter uses
+    L2 fp64 atomics).  RS_NO_SELROWS=1 selects the full scan (read per workspace)."""
     n, d = 300, 5000
     rp, ci, v, y = rsinputs.csr_zipf(n, d, 60, a=1.1, seed=3)
     out = []

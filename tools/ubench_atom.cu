@@ -57,6 +57,4 @@ int main() {
            cudaGetErrorString(cudaGetLastError()));
   };
   run(0, k<0>); run(1, k<1>); run(2, k<2>); run(3, k<3>); run(4, k<4>); run(5, k<5>);
-  // hash-only baseline (the address generation every variant pays)
-  run(1, k<6>);
 }
