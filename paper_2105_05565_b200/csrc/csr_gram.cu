@@ -76,6 +76,7 @@ struct WarpMerge {
     __syncwarp();
   }
   // write the touched buckets in ascending order to hb/hv at `a`, clear; returns the count
+  template <bool SQ = true>
   __device__ __forceinline__ int flush(long long a, int* hb, double* hv, int lane) {
     int total = 0;
     for (int w0 = 0; w0 < nw; w0 += 32) {
@@ -94,7 +95,7 @@ struct WarpMerge {
         const double x = acc[bucket];
         hb[pos] = bucket;
         hv[pos] = x;
-        sq += x * x;
+        if (SQ) sq += x * x;
         ++pos;
       }
       if (wi < nw) bits[wi] = 0u;
@@ -292,7 +293,7 @@ k_sel_emit(DevSketch sk, const long long* __restrict__ rowptr, const int* __rest
            const double* __restrict__ vals, const int* __restrict__ cscpos, int* __restrict__ cmR,
            int* __restrict__ tflag, int* __restrict__ tlist, int* __restrict__ tcount,
            const int* __restrict__ hidx, double* __restrict__ hacc, long long ldh, int slot,
-           const Ctrl* ctrl) {
+           const Ctrl* ctrl, double* __restrict__ gtr) {
   if (slot_unused(ctrl, slot)) return;
   const int lane = threadIdx.x & 31;
   const int e = blockIdx.x * SE_WARPS + (threadIdx.x >> 5);
@@ -302,6 +303,7 @@ k_sel_emit(DevSketch sk, const long long* __restrict__ rowptr, const int* __rest
   const bool neg = sk.sign[e] <= 0;
   const int code = (b << 1) | (neg ? 1 : 0);
   const long long p1 = rowptr[i + 1];
+  double sq = 0.0;   // squares of the light entries: trace bound for the fixed-point Gram
   for (long long pb = rowptr[i]; pb < p1; pb += 32 * SE_U) {   // warp-uniform trip count
     int f[SE_U], h[SE_U];
 #pragma unroll
@@ -323,6 +325,8 @@ k_sel_emit(DevSketch sk, const long long* __restrict__ rowptr, const int* __rest
         continue;
       }
       cmR[cscpos[p]] = code;
+      const double x = vals[p];
+      sq += x * x;
       need[u] = tflag[f[u]] == 0 && atomicExch(&tflag[f[u]], 1) == 0;
     }
 #pragma unroll
@@ -336,13 +340,19 @@ k_sel_emit(DevSketch sk, const long long* __restrict__ rowptr, const int* __rest
       if (need[u]) tlist[base + __popc(m & ((1u << lane) - 1u))] = f[u];
     }
   }
+  // trace(G_light) = sum_f sum_b (sum_{e in (f, b)} sign_e x_e)^2 <= kmax sum_e x_e^2 (Cauchy-
+  // Schwarz; kmax = entries of one bucket: k for SubCount, 1 for subsample): an upper bound, so the
+  // fixed-point range holds; over-estimating by <= kmax costs log2(kmax) bits of resolution
+#pragma unroll
+  for (int o = 16; o; o >>= 1) sq += __shfl_xor_sync(FULL, sq, o);
+  if (lane == 0 && sq != 0.0) atomicAdd(gtr, sq * (double)max(1, sk.ksum));
 }
 
 __global__ void __launch_bounds__(HR_WARPS * 32)
 k_sel_merge(const long long* __restrict__ ptr, const double* __restrict__ val, long long heavy,
             int* __restrict__ cmR, int* __restrict__ tflag, const int* __restrict__ tlist,
             const int* __restrict__ tcount, int tau, int* __restrict__ hb, double* __restrict__ hv,
-            int* __restrict__ hcnt, int slot, const Ctrl* ctrl, double* __restrict__ gtr) {
+            int* __restrict__ hcnt, int slot, const Ctrl* ctrl) {
   if (slot_unused(ctrl, slot)) return;
   extern __shared__ double hsm[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -365,10 +375,9 @@ k_sel_merge(const long long* __restrict__ ptr, const double* __restrict__ val, l
       if (cm0 >= 0) cmR[t0] = -1;
       if (cm1 >= 0) cmR[t1] = -1;
     }
-    const int total = M.flush(a, hb, hv, lane);
+    const int total = M.template flush<false>(a, hb, hv, lane);
     if (lane == 0) hcnt[f] = total;
   }
-  M.trace_out_block(gtr, lane, warp);
 }
 
 // t = R v = X^T v for the dual with v = S delta nonzero on the s selected samples only: each
@@ -866,11 +875,11 @@ rs_status Problem::csr_gram_into(const DevSketch& s, double* G, cudaEvent_t* ev,
     RS_CUDA(cudaMemsetAsync(c->hcnt, 0, R.rows * sizeof(int), st));
     k_sel_emit<<<(unsigned)std::max(1, (s.len + SE_WARPS - 1) / SE_WARPS), SE_WARPS * 32, 0, st>>>(
         s, c->rowptr, c->colidx, c->vals, c->cscpos, c->cmR, c->tflag, c->tlist, c->tcount, c->hidx,
-        c->hacc, c->ldh, slot, ctrl);
+        c->hacc, c->ldh, slot, ctrl, c->gtrace);
     const unsigned grid = (unsigned)((long long)num_sms * 8);
     k_sel_merge<<<grid, HR_WARPS * 32, c->hr_smem, st>>>(R.ptr, R.val, c->heavyR, c->cmR, c->tflag,
                                                          c->tlist, c->tcount, tau, c->hb, c->hv,
-                                                         c->hcnt, slot, ctrl, c->gtrace);
+                                                         c->hcnt, slot, ctrl);
     if (c->nheavyR > 0) {   // heavy rows: H^T H on the lower DMMA tiles, then H cleared
       RS_CUDA(tma_gemm_launch(c->tg_heavy, c->gh, ld_gram, c->gh_work, ctrl, st));
       RS_CUDA(cudaMemsetAsync(c->hacc, 0, (size_t)c->nheavyR * c->ldh * sizeof(double), st));
