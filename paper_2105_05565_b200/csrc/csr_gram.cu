@@ -140,7 +140,9 @@ __device__ __forceinline__ void fx_add(unsigned* w, long long x) {
   if (h) atomicAdd(reinterpret_cast<int*>(w) + 1, h);
 }
 __device__ __forceinline__ int fx_exponent(double trace) {
-  return trace > 0.0 && trace < 1e300 ? 61 - ilogb(trace) : 0;
+  // clamped so that 2^E and 2^-E are finite normal numbers (|log2 trace| < ~960 for any data
+  // whose Gram is representable)
+  return trace > 0.0 && isfinite(trace) ? max(-1021, min(1022, 61 - ilogb(trace))) : 0;
 }
 
 __device__ __forceinline__ int cm_of(const int* __restrict__ cmap, const int* __restrict__ idx,

@@ -324,6 +324,37 @@ def test_csr_primal_long_rows(rs, kind, tau, k, mode):
     assert rel(r, ref["r"]) <= 1e-10
 
 
+@pytest.mark.parametrize("scale", [1e-50, 1e50])
+def test_csr_gram_fixed_point_scale_invariance(rs, scale):
+    """The CSR Gram's fixed-point scale follows trace(G) (DESIGN R26): data scaled by 1e+-50
+    (lambda by scale^2) gives the oracle's iterates, primal (count: full scan) and dual
+    (SubCount: the selected-row path's trace bound).  (The residual norms are plain fp64 sums of
+    squares: a primal b = X^T y scales as scale^2 and ||b||^2 as scale^4, so 1e+-100 would leave
+    the fp64 range there, in any mode.)"""
+    n, d = 3000, 400
+    rp, ci, v, y, Xs = _csr_primal(n, d, per_row=70, seed=12)
+    lam = 1e-2 * scale * scale
+    h = rs.rs_create_csr(n, d, rp, ci, v * scale, y * scale, lam, mode="gram")
+    try:
+        w, _ = rs.rs_solve(h, "count", 64, 1.0, 0.5, 0.0, 12, seed=5)
+    finally:
+        rs.rs_destroy(h)
+    ref = OV.solve(Xs * scale, y * scale, lam, "count", 64, 1.0, 0.5, 0.0, 12, seed=5)
+    assert rel(w, ref["w"]) <= 1e-10
+    n, d = 300, 5000
+    rp, ci, v, y = rsinputs.csr_zipf(n, d, 60, a=1.1, seed=3)
+    Xs = rsinputs.csr_to_scipy(rp, ci, v, n, d)
+    h = rs.rs_create_csr(n, d, rp, ci, v * scale, y * scale, lam, mode="gram")
+    try:
+        w, _ = rs.rs_solve(h, "subcount", 16, 1.0, 0.5, 0.0, 12, seed=6, subcount_k=4, d=d)
+    finally:
+        rs.rs_destroy(h)
+    ref = OV.solve(Xs * scale, y * scale, lam, "subcount", 16, 1.0, 0.5, 0.0, 12, seed=6,
+                   subcount_k=4)
+    assert ref["route"] == "dual"
+    assert rel(w, ref["weights"]) <= 1e-10
+
+
 def test_csr_primal_gram_bitwise_reproducible(rs):
     """CSR primal GRAM with a count sketch: row hashing merges in a fixed lane order, the Gram bands
     are exact int64 fixed-point sums (DESIGN R26), the band partials are reduced in chunk order and
