@@ -54,7 +54,9 @@ typedef enum {
   RS_ECUDA = 4,         /* CUDA runtime / launch failure, or no usable device                 */
   RS_ENCCL = 5,         /* NCCL failure; the communicator is aborted, only rs_destroy is legal */
   RS_ENOTSPD = 6,       /* a Cholesky pivot of S^T A S was <= 0 or not finite                 */
-  RS_EDIVERGED = 7      /* maintained residual non-finite or ||r||/||b|| > 1e8      */
+  RS_EDIVERGED = 7      /* maintained residual non-finite or ||r||/||b|| > 1e8; the
+                           norms are fp64 sums of squares, so this is also the outcome when
+                           ||b||^2 leaves the fp64 range (||b|| > ~1e154)                      */
 } rs_status;
 
 typedef enum { RS_ROUTE_AUTO = 0, RS_ROUTE_PRIMAL = 1, RS_ROUTE_DUAL = 2 } rs_route;
