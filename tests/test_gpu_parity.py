@@ -11,6 +11,7 @@ import rsinputs
 from oracle import problem as OP
 from oracle import sketch as OS
 from oracle import solver as OV
+from parity_util import assert_close, rel
 
 pytestmark = pytest.mark.gpu
 
@@ -24,9 +25,6 @@ def rs():
     return ridgesketch
 
 
-def rel(a, b):
-    nb = np.linalg.norm(b)
-    return np.linalg.norm(a - b) / (nb if nb > 0 else 1.0)
 
 
 # ---------------------------------------------------------------------------------- a1 sketches
@@ -83,8 +81,8 @@ def test_config1_50_steps(rs, beta, mode):
     w, r, rep = _run_gpu_dense(rs, X, y, cfg.lam, mode, "subsample", cfg.tau, beta, 50)
     ref = OV.solve(X, y, cfg.lam, "subsample", cfg.tau, 1.0, beta, 0.0, 50, seed=0)
     assert rep["iterations"] == 50
-    assert rel(w, ref["w"]) <= 1e-10
-    assert rel(r, ref["r"]) <= 1e-10
+    assert_close(w, ref["w"], 1e-10)
+    assert_close(r, ref["r"], 1e-10)
 
 
 @pytest.mark.parametrize("mode", ["implicit", "explicit", "gram"])
@@ -95,9 +93,9 @@ def test_config1_final_vs_direct(rs, mode):
     pr = OP.build(X, y, cfg.lam)
     w_star = OP.direct_solve(pr["A"], pr["b"])
     assert rep["iterations"] == 300
-    assert rel(w, w_star) <= 1e-6
+    assert_close(w, w_star, 1e-6)
     w5, _, _ = _run_gpu_dense(rs, X, y, cfg.lam, mode, "subsample", cfg.tau, 0.5, 1000)
-    assert rel(w5, w_star) <= 1e-6
+    assert_close(w5, w_star, 1e-6)
 
 
 @pytest.mark.parametrize("kind,tau,k", [("subsample", 37, 0), ("count", 37, 0), ("subcount", 29, 3),
@@ -111,8 +109,8 @@ def test_dense_ragged_parity(rs, kind, tau, k, mode):
                                device_input=True)
     ref = OV.solve(X, y, lam, kind, tau, 1.0, 0.5, 0.0, 12, seed=5, subcount_k=k)
     assert rep["iterations"] == 12
-    assert rel(w, ref["w"]) <= 1e-10
-    assert rel(r, ref["r"]) <= 1e-10
+    assert_close(w, ref["w"], 1e-10)
+    assert_close(r, ref["r"], 1e-10)
 
 
 @pytest.mark.parametrize("mode", ["implicit", "explicit", "gram"])
@@ -124,8 +122,8 @@ def test_dense_count_empty_buckets(rs, mode):
     w, r, rep = _run_gpu_dense(rs, X, y, cfg.lam, mode, "count", cfg.tau, 0.5, 60, seed=2)
     ref = OV.solve(X, y, cfg.lam, "count", cfg.tau, 1.0, 0.5, 0.0, 60, seed=2)
     assert rep["iterations"] == 60
-    assert rel(w, ref["w"]) <= 1e-10
-    assert rel(r, ref["r"]) <= 1e-10
+    assert_close(w, ref["w"], 1e-10)
+    assert_close(r, ref["r"], 1e-10)
 
 
 @pytest.mark.parametrize("mode", ["explicit", "gram"])
@@ -142,8 +140,8 @@ def test_sketch_ahead_group_sizes(rs, mode, check_every):
         rs.rs_destroy(h)
     ref = OV.solve(X, y, 0.7, "subsample", 48, 1.0, 0.5, 0.0, 150, seed=11)
     assert rep["iterations"] == 150
-    assert rel(w, ref["w"]) <= 1e-10
-    assert rel(r, ref["r"]) <= 1e-10
+    assert_close(w, ref["w"], 1e-10)
+    assert_close(r, ref["r"], 1e-10)
 
 
 def test_dense_identity_sketch_one_step_explicit(rs):
@@ -151,7 +149,7 @@ def test_dense_identity_sketch_one_step_explicit(rs):
     X, y = _dense(400, 64, seed=4)
     w, r, rep = _run_gpu_dense(rs, X, y, 0.5, "explicit", "subsample", 64, 0.0, 1)
     pr = OP.build(X, y, 0.5)
-    assert rel(w, OP.direct_solve(pr["A"], pr["b"])) <= 1e-11
+    assert_close(w, OP.direct_solve(pr["A"], pr["b"]), 1e-11)
     assert np.linalg.norm(r) <= 1e-11 * np.linalg.norm(pr["b"])
 
 
@@ -160,14 +158,15 @@ def test_dense_identity_sketch_one_step(rs):
     w, r, rep = _run_gpu_dense(rs, X, y, 0.5, "implicit", "subsample", 64, 0.0, 1)
     pr = OP.build(X, y, 0.5)
     w_star = np.linalg.solve(pr["A"], pr["b"])
-    assert rel(w, w_star) <= 1e-10 and np.linalg.norm(r) <= 1e-9 * np.linalg.norm(pr["b"])
+    assert_close(w, w_star, 1e-10)
+    assert np.linalg.norm(r) <= 1e-9 * np.linalg.norm(pr["b"])
 
 
 def test_dense_tau1_coordinate_descent(rs):
     X, y = _dense(200, 20, seed=5)
     w, r, rep = _run_gpu_dense(rs, X, y, 0.2, "implicit", "subsample", 1, 0.3, 40, seed=17)
     ref = OV.solve(X, y, 0.2, "subsample", 1, 1.0, 0.3, 0.0, 40, seed=17)
-    assert rel(w, ref["w"]) <= 1e-10
+    assert_close(w, ref["w"], 1e-10)
 
 
 def test_tolerance_stop_iteration_count(rs):
@@ -182,7 +181,7 @@ def test_tolerance_stop_iteration_count(rs):
     assert abs(rep["iterations"] - ref["iterations"]) <= 1
     n = min(len(rep["trace"]), len(ref["trace"]))
     assert np.allclose(rep["trace"][:n], ref["trace"][:n], rtol=1e-8, atol=0)
-    assert rel(w, ref["w"]) <= 1e-8
+    assert_close(w, ref["w"], 1e-8)
 
 
 def test_zero_rhs_and_zero_iterations(rs):
@@ -241,8 +240,8 @@ def test_csr_primal_parity(rs, kind, tau, k, mode):
     finally:
         rs.rs_destroy(h)
     ref = OV.solve(Xs, y, lam, kind, tau, 1.0, 0.5, 0.0, 15, seed=2, subcount_k=k)
-    assert rel(w, ref["w"]) <= 1e-10
-    assert rel(r, ref["r"]) <= 1e-10
+    assert_close(w, ref["w"], 1e-10)
+    assert_close(r, ref["r"], 1e-10)
 
 
 @pytest.mark.parametrize("kind,tau,k", [("subcount", 16, 4), ("subsample", 25, 0), ("count", 12, 0),
@@ -261,10 +260,10 @@ def test_csr_dual_parity(rs, kind, tau, k, mode):
         rs.rs_destroy(h)
     ref = OV.solve(Xs, y, lam, kind, tau, 1.0, 0.5, 0.0, 15, seed=4, subcount_k=k)
     assert ref["route"] == "dual"
-    assert rel(alpha, ref["w"]) <= 1e-10
-    assert rel(rep["alpha"], ref["w"]) <= 1e-10
-    assert rel(r, ref["r"]) <= 1e-10
-    assert rel(w, ref["weights"]) <= 1e-10
+    assert_close(alpha, ref["w"], 1e-10)
+    assert_close(rep["alpha"], ref["w"], 1e-10)
+    assert_close(r, ref["r"], 1e-10)
+    assert_close(w, ref["weights"], 1e-10)
 
 
 @pytest.mark.parametrize("mode", ["implicit", "gram"])
@@ -282,7 +281,7 @@ def test_csr_dual_converges_to_direct(rs, mode):
     pr = OP.build(X, y, lam, "primal")
     w_star = np.linalg.solve(pr["A"], pr["b"])
     assert rep["converged"]
-    assert rel(w, w_star) <= 1e-6
+    assert_close(w, w_star, 1e-6)
 
 
 # ---------------------------------------------------------------------------------- full size
@@ -302,8 +301,8 @@ def test_config2_full_size_sampled(rs, mode):
     X, y = Xd.cpu().numpy(), yd.cpu().numpy()
     del Xd, yd
     ref = OV.solve(X, y, cfg.lam, "subsample", cfg.tau, 1.0, cfg.beta, 0.0, 3, seed=0)
-    assert rel(w, ref["w"]) <= 1e-10
-    assert rel(r, ref["r"]) <= 1e-10
+    assert_close(w, ref["w"], 1e-10)
+    assert_close(r, ref["r"], 1e-10)
 
 
 @pytest.mark.parametrize("kind,tau,k", [("count", 64, 0), ("subsample", 150, 0), ("subcount", 50, 4)])
@@ -320,8 +319,8 @@ def test_csr_primal_long_rows(rs, kind, tau, k, mode):
     finally:
         rs.rs_destroy(h)
     ref = OV.solve(Xs, y, lam, kind, tau, 1.0, 0.5, 0.0, 12, seed=3, subcount_k=k)
-    assert rel(w, ref["w"]) <= 1e-10
-    assert rel(r, ref["r"]) <= 1e-10
+    assert_close(w, ref["w"], 1e-10)
+    assert_close(r, ref["r"], 1e-10)
 
 
 @pytest.mark.parametrize("scale", [1e-50, 1e50])
@@ -340,7 +339,7 @@ def test_csr_gram_fixed_point_scale_invariance(rs, scale):
     finally:
         rs.rs_destroy(h)
     ref = OV.solve(Xs * scale, y * scale, lam, "count", 64, 1.0, 0.5, 0.0, 12, seed=5)
-    assert rel(w, ref["w"]) <= 1e-10
+    assert_close(w, ref["w"], 1e-10)
     n, d = 300, 5000
     rp, ci, v, y = rsinputs.csr_zipf(n, d, 60, a=1.1, seed=3)
     Xs = rsinputs.csr_to_scipy(rp, ci, v, n, d)
@@ -352,7 +351,7 @@ def test_csr_gram_fixed_point_scale_invariance(rs, scale):
     ref = OV.solve(Xs * scale, y * scale, lam, "subcount", 16, 1.0, 0.5, 0.0, 12, seed=6,
                    subcount_k=4)
     assert ref["route"] == "dual"
-    assert rel(w, ref["weights"]) <= 1e-10
+    assert_close(w, ref["weights"], 1e-10)
 
 
 def test_csr_primal_gram_bitwise_reproducible(rs):
@@ -370,7 +369,7 @@ def test_csr_primal_gram_bitwise_reproducible(rs):
         rs.rs_destroy(h)
     assert np.array_equal(w1, w2)
     ref = OV.solve(Xs, y, 1e-2, "count", 64, 1.0, 0.5, 0.0, 30, seed=4)
-    assert rel(w1, ref["w"]) <= 1e-10
+    assert_close(w1, ref["w"], 1e-10)
 
 
 @pytest.mark.parametrize("kind,tau,k", [("subsample", 260, 0), ("count", 300, 0), ("subcount", 230, 2)])
@@ -383,8 +382,8 @@ def test_dense_large_tau_sketch_ahead(rs, kind, tau, k, mode):
     X, y = X.numpy(), y.numpy()
     w, r, rep = _run_gpu_dense(rs, X, y, 0.5, mode, kind, tau, 0.5, 10, seed=6, k=k)
     ref = OV.solve(X, y, 0.5, kind, tau, 1.0, 0.5, 0.0, 10, seed=6, subcount_k=k)
-    assert rel(w, ref["w"]) <= 1e-10
-    assert rel(r, ref["r"]) <= 1e-10
+    assert_close(w, ref["w"], 1e-10)
+    assert_close(r, ref["r"], 1e-10)
 
 
 @pytest.mark.parametrize("env", ["RS_XG", "RS_XC"])
@@ -404,8 +403,8 @@ def test_dense_fused_xpass_gram(rs, monkeypatch, env, n, d, tau, check_every):
         rs.rs_destroy(h)
     ref = OV.solve(X, y, 0.3, "subsample", tau, 1.0, 0.5, 0.0, 11, seed=8)
     assert rep["iterations"] == 11
-    assert rel(w, ref["w"]) <= 1e-10
-    assert rel(r, ref["r"]) <= 1e-10
+    assert_close(w, ref["w"], 1e-10)
+    assert_close(r, ref["r"], 1e-10)
 
 
 # ------------------------------------------------------------- full size, bench launch config
@@ -435,8 +434,8 @@ def test_csr_configs_full_size(rs, name, iters):
     ref = OV.solve(Xs, y, cfg.lam, cfg.sketch, cfg.tau, cfg.gamma, cfg.beta, 0.0, iters, seed=0,
                    subcount_k=cfg.subcount_k)
     assert rep["iterations"] == iters
-    assert rel(it, ref["w"]) <= 1e-10
-    assert rel(r, ref["r"]) <= 1e-10
+    assert_close(it, ref["w"], 1e-10)
+    assert_close(r, ref["r"], 1e-10)
 
 
 def test_config5_full_size_invariants(rs):
@@ -511,8 +510,8 @@ def test_momentum_schedules_dense(rs, momentum, eta, mode):
     ref = OV.solve(X, y, 0.2, "subsample", 6, tol=0.0, max_iter=260, seed=3, momentum=momentum,
                    eta=eta)
     assert rep["iterations"] == 260
-    assert rel(w, ref["w"]) <= 1e-9
-    assert rel(r, ref["r"]) <= 1e-9
+    assert_close(w, ref["w"], 1e-9)
+    assert_close(r, ref["r"], 1e-9)
 
 
 @pytest.mark.parametrize("momentum", ["heuristic", "theory"])
@@ -526,8 +525,8 @@ def test_momentum_schedules_csr(rs, momentum):
     finally:
         rs.rs_destroy(h)
     ref = OV.solve(Xs, y, 1e-2, "count", 30, tol=0.0, max_iter=220, seed=5, momentum=momentum)
-    assert rel(w, ref["w"]) <= 1e-9
-    assert rel(r, ref["r"]) <= 1e-9
+    assert_close(w, ref["w"], 1e-9)
+    assert_close(r, ref["r"], 1e-9)
 
 
 def test_momentum_invalid(rs):
@@ -586,8 +585,8 @@ def test_kernel_ridge_converges_and_predicts(rs):
     s = OP.build_kernel(X, y, lam, sigma)
     a_star = OP.direct_solve(s["A"], s["b"])
     assert rep["converged"]
-    assert rel(a, a_star) <= 1e-6
-    assert rel(s["K"] @ a, s["K"] @ a_star) <= 1e-7   # predictions on the inputs
+    assert_close(a, a_star, 1e-6)
+    assert_close(s["K"] @ a, s["K"] @ a_star, 1e-7)   # predictions on the inputs
 
 
 def test_kernel_invalid(rs):
@@ -614,8 +613,8 @@ def test_dirty_device_memory(rs, mode, kind, tau):
     X, y = X.numpy(), y.numpy()
     w, r, rep = _run_gpu_dense(rs, X, y, 0.7, mode, kind, tau, 0.5, 9, seed=2)
     ref = OV.solve(X, y, 0.7, kind, tau, 1.0, 0.5, 0.0, 9, seed=2)
-    assert rel(w, ref["w"]) <= 1e-10
-    assert rel(r, ref["r"]) <= 1e-10
+    assert_close(w, ref["w"], 1e-10)
+    assert_close(r, ref["r"], 1e-10)
 
 
 # -------------------------------------------------------------- sparse explicit A (NEXT-3)
@@ -631,8 +630,8 @@ def test_csr_explicit_primal(rs, kind, tau, k):
     finally:
         rs.rs_destroy(h)
     ref = OV.solve(Xs, y, 1e-2, kind, tau, 1.0, 0.5, 0.0, 15, seed=2, subcount_k=k, explicit=True)
-    assert rel(w, ref["w"]) <= 1e-10
-    assert rel(r, ref["r"]) <= 1e-10
+    assert_close(w, ref["w"], 1e-10)
+    assert_close(r, ref["r"], 1e-10)
 
 
 @pytest.mark.parametrize("kind,tau,k", [("subcount", 16, 4), ("subsample", 25, 0), ("count", 12, 0),
@@ -648,9 +647,9 @@ def test_csr_explicit_dual(rs, kind, tau, k):
     finally:
         rs.rs_destroy(h)
     ref = OV.solve(Xs, y, 1e-1, kind, tau, 1.0, 0.5, 0.0, 15, seed=4, subcount_k=k, explicit=True)
-    assert rel(alpha, ref["w"]) <= 1e-10
-    assert rel(r, ref["r"]) <= 1e-10
-    assert rel(w, ref["weights"]) <= 1e-10
+    assert_close(alpha, ref["w"], 1e-10)
+    assert_close(r, ref["r"], 1e-10)
+    assert_close(w, ref["weights"], 1e-10)
 
 
 def test_csr_explicit_config4_full_size(rs):
@@ -668,8 +667,8 @@ def test_csr_explicit_config4_full_size(rs):
     Xs = rsinputs.csr_to_scipy(rp, ci, va, cfg.n, cfg.d)
     ref = OV.solve(Xs, y, cfg.lam, cfg.sketch, cfg.tau, cfg.gamma, cfg.beta, 0.0, 3, seed=0,
                    subcount_k=cfg.subcount_k)
-    assert rel(it, ref["w"]) <= 1e-10
-    assert rel(r, ref["r"]) <= 1e-10
+    assert_close(it, ref["w"], 1e-10)
+    assert_close(r, ref["r"], 1e-10)
 
 
 # ------------------------------------------------- process-level switches (read once per process)
@@ -710,8 +709,8 @@ def test_process_switches_parity(tmp_path, env):
     for mode, kind, tau, k in [("explicit", "subsample", 300, 0), ("explicit", "subcount", 250, 2),
                                ("gram", "subsample", 150, 0)]:
         ref = OV.solve(X, y, 0.5, kind, tau, 1.0, 0.5, 0.0, 12, seed=3, subcount_k=k)
-        assert rel(got[f"{mode}_{kind}_w"], ref["w"]) <= 1e-10, (env, mode, kind)
-        assert rel(got[f"{mode}_{kind}_r"], ref["r"]) <= 1e-10, (env, mode, kind)
+        assert_close(got[f"{mode}_{kind}_w"], ref["w"], 1e-10, f"{env} {mode} {kind} w")
+        assert_close(got[f"{mode}_{kind}_r"], ref["r"], 1e-10, f"{env} {mode} {kind} r")
 
 
 @pytest.mark.parametrize("kind,tau,k", [("subcount", 16, 4), ("subsample", 25, 0), ("subcount", 240, 1)])
@@ -734,7 +733,8 @@ def test_csr_dual_selected_rows_match_full_scan(rs, monkeypatch, kind, tau, k):
         finally:
             rs.rs_destroy(h)
         out.append((w, r))
-    assert rel(out[0][0], out[1][0]) <= 1e-13 and rel(out[0][1], out[1][1]) <= 1e-13
+    assert_close(out[0][0], out[1][0], 1e-13)
+    assert_close(out[0][1], out[1][1], 1e-13)
 
 
 @pytest.mark.parametrize("kind,tau,k", [("subsample", 40, 0), ("subcount", 30, 2), ("count", 25, 0),
@@ -753,9 +753,10 @@ def test_dense_dual_explicit_parity(rs, kind, tau, k):
         rs.rs_destroy(h)
     ref = OV.solve(X, y, 0.5, kind, tau, 1.0, 0.5, 0.0, 15, seed=3, subcount_k=k)
     assert ref["route"] == "dual"
-    assert rel(alpha, ref["w"]) <= 1e-10 and rel(r, ref["r"]) <= 1e-10
-    assert rel(rep["alpha"], ref["w"]) <= 1e-10
-    assert rel(w, ref["weights"]) <= 1e-10
+    assert_close(alpha, ref["w"], 1e-10)
+    assert_close(r, ref["r"], 1e-10)
+    assert_close(rep["alpha"], ref["w"], 1e-10)
+    assert_close(w, ref["weights"], 1e-10)
 
 
 def test_dense_dual_implicit_unsupported(rs):
