@@ -4,16 +4,21 @@
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config c2]
                     [--mode implicit|explicit]
 
-One "step" = one iteration of Alg. 2: sketch draw, X S, A S, S^T A S + Cholesky,
-fused momentum update -- every row of SURVEY §8(a).  Workload at N=1: BASELINE.json configs[1]
-(c2: dense primal 1e5 x 2000, subsample tau=200, gamma=1, beta=0.5, lambda=1e-4 n, tol 1e-4),
-synthetic data generated on the device from a fixed seed.
+One "step" = one iteration of Alg. 2: sketch draw, rows of A S, S^T A S + Cholesky,
+fused momentum update -- every row of SURVEY §8(a).  Workload at N=1: the largest single-GPU
+BASELINE.json config, configs[4] (c5: dense primal 2e6 x 4096 fp64 = 65.5 GB, subsample
+tau=1024, gamma=1, beta=0.5, lambda=1e-4 n, tol 1e-4) on the EXPLICIT route (A = X^T X + lambda I
+built once by the lower-tile DMMA contraction, then per iteration the sketched rows of A), the
+route with the shortest measured time to tolerance; the GRAM and IMPLICIT routes of the same data
+are measured over a few iterations and reported as `alt_routes`.  Synthetic data generated on the
+device from a fixed seed.
 
 Prints ONE JSON line (rank 0).  `value` = iterations per second of the solve (device time, CUDA
 events on the solver stream, max over ranks), `e2e` = the same metric through the public API from
 pinned host buffers (H2D of X and y, setup, solve to tol, D2H of w inside the timed region),
-`time_to_tol_s` = device seconds to ||r||/||b|| <= 1e-4, `roofline` = the dominant kernel (A S
-contraction, FP64 DMMA) against the measured FP64 peak, `cpu_baseline` = the oracle on the host.
+`time_to_tol_s` = device seconds to ||r||/||b|| <= 1e-4 (median over sketch seeds 0..4, quartiles
+in `time_to_tol_seeds`), `roofline` = the dominant kernel class against its measured peak,
+`cpu_baseline` = the oracle on the host cores.
 """
 
 import argparse
@@ -27,6 +32,10 @@ import time
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
+# AS route of each config's line: the one with the shortest measured time to tolerance (DESIGN.md
+# §9); c5's GRAM / IMPLICIT routes are measured beside it (`alt_routes`)
+DEFAULT_MODE = {"c1": "gram", "c2": "gram", "c3": "gram", "c4": "gram", "c5": "explicit",
+                "k1": "explicit"}
 METRIC = "sketch-and-project iters/s & s to ‖r‖/‖b‖≤1e-4; AS-pass HBM GB/s vs peak"
 FP64_DMMA_PEAK = 37.1   # TFLOP/s, measured on this pool's B200 (profiles/r01_fp64_peak.txt)
 
@@ -152,39 +161,69 @@ def _dist_env():
 
 
 # ------------------------------------------------------------------------------ reference arm
+# c5's A = X^T X (3.4e13 flop) is far beyond a bounded host sample: the oracle's EXPLICIT iteration
+# on the m = 4096 system costs the same for any A of that size, so the host legs build A from the
+# first ORACLE_ROWS rows of the same X ("CPU oracle")
+ORACLE_ROWS = 100_000
+
+
+def _oracle_operator(cfg, mode, X, y):
+    """The oracle's operator for `cfg` (X, y host arrays; kernel ridge: X, y are its inputs)."""
+    from oracle import solver as OV
+    if cfg.kind == "kernel":
+        from oracle import problem as OP
+        sysk = OP.build_kernel(X, y, cfg.lam, cfg.extra["sigma"])
+        return OV.Operator.from_system(sysk["A"], sysk["b"])
+    return OV.Operator(X, y, cfg.lam, explicit=(mode == "explicit"))
+
+
+def _host_inputs(cfg, dev):
+    """(X, y, sample description) on the host for the oracle legs."""
+    import numpy as np
+    import rsinputs
+    if cfg.kind == "kernel":
+        X, y = rsinputs.kernel_problem(cfg.n, cfg.d, seed=0, noise=cfg.noise)
+        return X, y, "full kernel system"
+    if cfg.kind == "dense":
+        big = cfg.n * cfg.d * 8 > 32e9
+        if big and dev == "cpu":   # no device to draw the full X on: a same-shaped row sample
+            X, y = rsinputs.dense_problem(ORACLE_ROWS, cfg.d, seed=0, col_decay=cfg.col_decay,
+                                          noise=cfg.noise)
+            return X.numpy(), y.numpy(), (f"A = X_s^T X_s + lambda I from {ORACLE_ROWS} rows drawn "
+                                          f"like X (an EXPLICIT iteration costs the same for any "
+                                          f"{cfg.d} x {cfg.d} A)")
+        X, y = rsinputs.dense_problem(cfg.n, cfg.d, seed=0, col_decay=cfg.col_decay,
+                                      noise=cfg.noise, device=dev)
+        if big:
+            X, y = X[:ORACLE_ROWS].cpu().numpy(), y[:ORACLE_ROWS].cpu().numpy()
+            return X, y, (f"A = X_s^T X_s + lambda I from the first {ORACLE_ROWS} of the {cfg.n} rows "
+                          f"(an EXPLICIT iteration costs the same for any {cfg.d} x {cfg.d} A)")
+        return X.cpu().numpy(), y.cpu().numpy(), "full X"
+    if cfg.zipf_a > 0:
+        rp, ci, va, y = rsinputs.csr_zipf(cfg.n, cfg.d, cfg.nnz_per_row, a=cfg.zipf_a, seed=0)
+    else:
+        rp, ci, va, y = rsinputs.csr_uniform(cfg.n, cfg.d, cfg.nnz_per_row, seed=0)
+    return rsinputs.csr_to_scipy(rp, ci, va, cfg.n, cfg.d), y, "full X"
+
+
 def run_reference(args):
     """The oracle (oracle/, plain NumPy/SciPy fp64) on the same workload, on the host cores."""
     world, rank, _ = _dist_env()
     if rank != 0:
         return 0
-    import numpy as np
     import torch
     import rsinputs
     from oracle import solver as OV
     cfg = rsinputs.CONFIGS[args.config]
-    dev = "cuda" if torch.cuda.is_available() else "cpu"
-    if cfg.kind == "kernel":
-        from oracle import problem as OP
-        Xk, yk = rsinputs.kernel_problem(cfg.n, cfg.d, seed=0, noise=cfg.noise)
-        sysk = OP.build_kernel(Xk, yk, cfg.lam, cfg.extra["sigma"])
-        X, y = None, None
-        args.mode = "explicit"
-    elif cfg.kind == "dense":
-        X, y = rsinputs.dense_problem(cfg.n, cfg.d, seed=0, col_decay=cfg.col_decay,
-                                      noise=cfg.noise, device=dev)
-        X, y = X.cpu().numpy(), y.cpu().numpy()
-    elif cfg.zipf_a > 0:
-        rp, ci, va, y = rsinputs.csr_zipf(cfg.n, cfg.d, cfg.nnz_per_row, a=cfg.zipf_a, seed=0)
-        X = rsinputs.csr_to_scipy(rp, ci, va, cfg.n, cfg.d)
-    else:
-        rp, ci, va, y = rsinputs.csr_uniform(cfg.n, cfg.d, cfg.nnz_per_row, seed=0)
-        X = rsinputs.csr_to_scipy(rp, ci, va, cfg.n, cfg.d)
     if args.mode is None:
-        args.mode = "gram"
+        args.mode = DEFAULT_MODE.get(cfg.name, "gram")
     if cfg.kind == "kernel":
-        op = OV.Operator.from_system(sysk["A"], sysk["b"])
-    else:
-        op = OV.Operator(X, y, cfg.lam, explicit=(args.mode == "explicit"))
+        args.mode = "explicit"
+    dev = "cuda" if torch.cuda.is_available() else "cpu"
+    X, y, sample = _host_inputs(cfg, dev)
+    if dev == "cuda":
+        torch.cuda.empty_cache()
+    op = _oracle_operator(cfg, args.mode, X, y)
     kw = dict(seed=0, subcount_k=cfg.subcount_k)
     OV.solve_momentum(op, cfg.sketch, cfg.tau, cfg.gamma, cfg.beta, 0.0, args.warmup, **kw)
     t0 = time.perf_counter()
@@ -200,7 +239,8 @@ def run_reference(args):
         "config": _config_dict(cfg, args, world),
         "cpu_baseline": {"value": v, "unit": "iters/s", "cores": cores, "kind": "oracle",
                          "sample": f"{args.steps} oracle Alg. 2 iterations of {args.config} "
-                                   f"(full X) after {args.warmup} warm-up iterations"},
+                                   f"({args.mode} AS; {sample}) after {args.warmup} warm-up "
+                                   f"iterations"},
         "e2e": {"value": v, "unit": "iters/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -333,6 +373,13 @@ def _roofline(args, cfg, world, kms, kl, dom, prof_ms, host, rs):
                         achieved=w / (ms * 1e-3) / 1e12, peak=FP64_DMMA_PEAK, unit="TFLOP/s",
                         peak_source=dmma_src,
                         algorithmic_per_launch=f"{w:.3e} flop ({what} per G_k, x {slots:.0f} slots)")
+        elif dom == "solve" and (args.mode == "explicit" or "rows" in cfg.extra):
+            w = float(cfg.tau) * cfg.tau * 8.0
+            roof = dict(kernel="class solve: delta = G_k^{-1} S^T r from the factor slot (tau <= 224: "
+                               "G^{-1} row GEMV; else W = L^{-1} and W^T, two triangular GEMVs, "
+                               "k_apply_rows)", bound="hbm",
+                        achieved=w / (ms * 1e-3) / 1e9, peak=hbm, unit="GB/s", peak_source=hbm_src,
+                        algorithmic_per_launch=f"{w:.3e} bytes (tau^2 x 8: the slot's factor read once)")
         else:   # explicit: rows of A + GEMV + update
             rows_s = cfg.extra.get("rows", cfg.tau)
             w = (rows_s * cfg.d + 10 * cfg.d) * 8.0
@@ -397,6 +444,14 @@ def _roofline(args, cfg, world, kms, kl, dom, prof_ms, host, rs):
 
 
 # ------------------------------------------------------------------------------ our arm
+def _quartiles(xs):
+    xs = sorted(xs)
+    if len(xs) == 1:
+        return xs[0], xs[0], xs[0]
+    q = statistics.quantiles(xs, n=4, method="inclusive")
+    return q[0], statistics.median(xs), q[2]
+
+
 def run_ours(args):
     import numpy as np
     import torch
@@ -411,6 +466,8 @@ def run_ours(args):
     pg = None
     if world > 1:
         import torch.distributed as tdist
+        # NCCL's own log (stderr) shows the transport (NVLS / P2P) and each communicator's nranks
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
         tdist.init_process_group("nccl", device_id=torch.device("cuda", local))
         pg = tdist
         obj = [rs.rs_nccl_unique_id() if rank == 0 else None]
@@ -419,7 +476,8 @@ def run_ours(args):
     cfg = rsinputs.CONFIGS[args.config]
     stream = torch.cuda.current_stream()
     if args.mode is None:
-        args.mode = "gram"
+        args.mode = DEFAULT_MODE.get(cfg.name, "gram")
+    big = cfg.kind == "dense" and cfg.n * cfg.d * 8 > 32e9   # c5: 65.5 GB of X
     if cfg.kind == "kernel":
         if world > 1:
             raise SystemExit("kernel ridge route: one GPU (rs_create_kernel v1)")
@@ -461,156 +519,210 @@ def run_ours(args):
         dist = dict(device=local, rank=0, world=1, cuda_stream=stream.cuda_stream,
                     shard_begin=0, shard_len=ln)
 
-    def create(X, y, borrow):
+    def create(X, y, borrow, mode=None):
         if cfg.kind == "kernel":
             return rs.rs_create_kernel(X, y, cfg.lam, cfg.extra["sigma"])
         if cfg.kind == "dense":
-            return rs.rs_create_dense(X, y, cfg.lam, mode=args.mode, n=cfg.n, d=cfg.d,
+            return rs.rs_create_dense(X, y, cfg.lam, mode=mode or args.mode, n=cfg.n, d=cfg.d,
                                       borrow=borrow, dist=dist)
-        return rs.rs_create_csr(cfg.n, cfg.d, X[0], X[1], X[2], y, cfg.lam, mode=args.mode,
+        return rs.rs_create_csr(cfg.n, cfg.d, X[0], X[1], X[2], y, cfg.lam, mode=mode or args.mode,
                                 dist=dist)
-
-    torch.cuda.synchronize()
-    h = create(Xd, yd, True)
-    common = dict(kind=cfg.sketch, tau=cfg.tau, gamma=cfg.gamma, beta=cfg.beta, seed=0,
-                  subcount_k=cfg.subcount_k, d=cfg.n if cfg.kind == "kernel" else cfg.d,
-                  momentum=args.momentum, eta=args.eta)
 
     def barrier():
         if pg is not None:
             pg.barrier()
         torch.cuda.synchronize()
 
-    # iterations per graph launch: EXPLICIT iterations are a few kernel nodes each (1024 per graph);
-    # GRAM / IMPLICIT groups add several nodes per sketch-ahead slot, and a graph of 10k+ nodes
-    # delays its own submission (256 per graph)
-    chunk = min(args.steps, 1024 if (args.mode == "explicit" or cfg.kind == "kernel") else 256)
-    # warm-up (W iterations, untimed) with the timed run's launch parameters, so the captured
-    # iteration graph is built (and cached by the library) before the timed region
-    rs.rs_solve(h, tol=0.0, max_iter=args.warmup, check_every=chunk, **common)
-    # timed: exactly K iterations of the whole hot path (graph launches of `chunk` iterations)
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    barrier()
-    with ClockSampler(local) as clk:
-        e0.record(stream)
-        _, rep = rs.rs_solve(h, tol=0.0, max_iter=args.steps, check_every=chunk, **common)
-        e1.record(stream)
-        barrier()
-    el_ms = e0.elapsed_time(e1)
-    # per-kernel-class breakdown: a separate run with CUDA events inside the graph (the events
-    # perturb the step time, so this run is not the timed one)
-    rs.rs_solve(h, tol=0.0, max_iter=args.warmup, check_every=chunk, profile=True, **common)
-    _, rep_prof = rs.rs_solve(h, tol=0.0, max_iter=args.steps, check_every=chunk, profile=True,
-                              **common)
-    prof_ms = rep_prof["solve_seconds"] * 1e3
-    if pg is not None:
-        t = torch.tensor([el_ms], device="cuda", dtype=torch.float64)
+    def max_over_ranks(ms):
+        if pg is None:
+            return ms
+        t = torch.tensor([ms], device="cuda", dtype=torch.float64)
         pg.all_reduce(t, op=pg.ReduceOp.MAX)
-        el_ms = float(t.item())
-    assert rep["iterations"] == args.steps
-    value = args.steps / (el_ms / 1e3)
+        return float(t.item())
 
-    # time to tolerance (second half of the metric), device time; first solve builds the graph
-    rs.rs_solve(h, tol=cfg.tol, max_iter=args.max_iter_tol, check_every=0, **common)
-    barrier()
-    e2, e3 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e2.record(stream)
-    _, rep_tol = rs.rs_solve(h, tol=cfg.tol, max_iter=args.max_iter_tol, check_every=0, **common)
-    e3.record(stream)
-    barrier()
-    tol_ms = e2.elapsed_time(e3)
-    if pg is not None:
-        t = torch.tensor([tol_ms], device="cuda", dtype=torch.float64)
-        pg.all_reduce(t, op=pg.ReduceOp.MAX)
-        tol_ms = float(t.item())
-    rs.rs_destroy(h)
-
-    # the other dense route on the same data (informational, not the line's value): EXPLICIT mode
-    # pays the A = X^T X + lambda I build once and then never streams X, so for solves longer
-    # than ~100 iterations it reaches the tolerance sooner; device time of rs_create + rs_solve
-    alt = None
-    if (cfg.kind == "dense" and args.mode != "explicit" and world == 1
-            and cfg.n * cfg.d * 8 <= 32e9 and cfg.d <= 8192):
-        ea, eb, ec = (torch.cuda.Event(enable_timing=True) for _ in range(3))
-        hx = rs.rs_create_dense(Xd, yd, cfg.lam, mode="explicit", n=cfg.n, d=cfg.d, borrow=True,
-                                dist=dist)
-        rs.rs_solve(hx, tol=cfg.tol, max_iter=args.max_iter_tol, check_every=0, **common)
-        rs.rs_destroy(hx)
+    def timed(h, **kw):
+        """(device ms, report) of one rs_solve, CUDA events on the solver stream, max over ranks."""
         barrier()
+        ea, eb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         ea.record(stream)
-        hx = rs.rs_create_dense(Xd, yd, cfg.lam, mode="explicit", n=cfg.n, d=cfg.d, borrow=True,
-                                dist=dist)
+        out = rs.rs_solve(h, **kw)
         eb.record(stream)
-        _, rep_x = rs.rs_solve(hx, tol=cfg.tol, max_iter=args.max_iter_tol, check_every=0,
-                               **common)
-        ec.record(stream)
         barrier()
-        rs.rs_destroy(hx)
-        build_s, solve_s = ea.elapsed_time(eb) / 1e3, eb.elapsed_time(ec) / 1e3
-        alt = {"mode": "explicit", "time_to_tol_s": build_s + solve_s,
-               "a_build_s": build_s, "solve_s": solve_s,
-               "iterations_to_tol": rep_x["iterations"], "converged": rep_x["converged"],
-               "note": "same data and sketch stream; device time incl. rs_create (A build)"}
+        return max_over_ranks(ea.elapsed_time(eb)), out[1]
 
-    # roofline of the dominant kernel class (live CUDA events inside the graph, per launch)
-    kms, kl = rep_prof["kernel_ms"], rep_prof["kernel_launches"]
-    dom = max(kms, key=lambda k: kms[k])
-    roof = _roofline(args, cfg, world, kms, kl, dom, prof_ms, host, rs)
-    roof["step_share_by_class"] = {k: kms[k] / max(prof_ms, 1e-9) for k in kms}
-    roof["dominant_class"] = dom
+    common = dict(kind=cfg.sketch, tau=cfg.tau, gamma=cfg.gamma, beta=cfg.beta, seed=0,
+                  subcount_k=cfg.subcount_k, d=cfg.n if cfg.kind == "kernel" else cfg.d,
+                  momentum=args.momentum, eta=args.eta)
 
-    # end to end through the public API from pinned host buffers (rank-local shard)
-    e2e = None
-    big = cfg.kind == "dense" and cfg.n * cfg.d * 8 > 32e9   # c5: 65 GB of X
-    if big and not args.no_e2e:
-        e2e = {"skipped": "X is %.1f GB: pinned-host copy not attempted" % (cfg.n * cfg.d * 8e-9)}
-    if not args.no_e2e and not big:
-        if cfg.kind in ("dense", "kernel"):
-            Xh = Xd.cpu().pin_memory()
+    def chunk_of(mode, steps):
+        # iterations per graph launch: EXPLICIT iterations are a few kernel nodes each (1024 per
+        # graph); GRAM / IMPLICIT groups add several nodes per sketch-ahead slot, and a graph of
+        # 10k+ nodes delays its own submission (256 per graph)
+        return min(steps, 1024 if (mode == "explicit" or cfg.kind == "kernel") else 256)
+
+    def measure(h, mode, steps, warmup, clk=None):
+        """iters/s over exactly `steps` iterations (tol = 0) after `warmup` untimed ones with the
+        same launch parameters (so the captured iteration graph exists before the timed region),
+        then the per-class breakdown from a separate profiled run (events perturb the step)."""
+        chunk = chunk_of(mode, steps)
+        rs.rs_solve(h, tol=0.0, max_iter=warmup, check_every=chunk, **common)
+        if clk is not None:
+            with clk:
+                el_ms, rep = timed(h, tol=0.0, max_iter=steps, check_every=chunk, **common)
         else:
-            Xh = tuple(t.cpu().pin_memory() for t in Xd)
-        yh = yd.cpu().pin_memory()
-        h2d = sum(t.numel() * t.element_size() for t in (Xh if isinstance(Xh, tuple) else (Xh,)))
-        h2d += yh.numel() * 8
-        barrier()
-        e4, e5 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e4.record(stream)
-        h2 = create(Xh, yh, False)
-        w, rep_e2e = rs.rs_solve(h2, tol=cfg.tol, max_iter=args.max_iter_tol, check_every=0,
-                                 **common)
-        e5.record(stream)
-        barrier()
-        rs.rs_destroy(h2)
-        e2e_ms = e4.elapsed_time(e5)
-        if pg is not None:
-            t = torch.tensor([e2e_ms], device="cuda", dtype=torch.float64)
-            pg.all_reduce(t, op=pg.ReduceOp.MAX)
-            e2e_ms = float(t.item())
-        e2e = {"value": rep_e2e["iterations"] / (e2e_ms / 1e3), "unit": "iters/s",
-               "h2d_bytes_per_step": int(h2d),
-               "d2h_bytes_per_step": int(w.size * 8),
-               "step": "one public-API solve: rs_create_(dense|csr)(pinned host X, y) + rs_solve "
-                       "to tol + w to host",
-               "seconds": e2e_ms / 1e3, "iterations": rep_e2e["iterations"]}
-        del Xh, yh
+            el_ms, rep = timed(h, tol=0.0, max_iter=steps, check_every=chunk, **common)
+        assert rep["iterations"] == steps, rep
+        rs.rs_solve(h, tol=0.0, max_iter=warmup, check_every=chunk, profile=True, **common)
+        _, rep_prof = rs.rs_solve(h, tol=0.0, max_iter=steps, check_every=chunk, profile=True,
+                                  **common)
+        kms, kl = rep_prof["kernel_ms"], rep_prof["kernel_launches"]
+        prof_ms = rep_prof["solve_seconds"] * 1e3
+        dom = max(kms, key=lambda k: kms[k])
+        saved = args.mode
+        args.mode = mode
+        roof = _roofline(args, cfg, world, kms, kl, dom, prof_ms, host, rs)
+        others = {}
+        for cls in sorted(kms, key=lambda k: -kms[k]):
+            if cls != dom and kms[cls] > 0.1 * prof_ms:
+                try:
+                    o = _roofline(args, cfg, world, kms, kl, cls, prof_ms, host, rs)
+                    others[cls] = {k: o[k] for k in ("kernel", "bound", "achieved", "peak", "unit",
+                                                     "frac", "traffic", "avg_launch_ms",
+                                                     "share_of_step") if k in o}
+                except Exception:
+                    pass
+        args.mode = saved
+        roof["step_share_by_class"] = {k: kms[k] / max(prof_ms, 1e-9) for k in kms}
+        roof["dominant_class"] = dom
+        if others:
+            roof["other_classes"] = others
+        return steps / (el_ms / 1e3), el_ms, rep, roof, {k: kms[k] / steps for k in kms}
+
+    torch.cuda.synchronize()
+    h = create(Xd, yd, True)
+    clk = ClockSampler(local)
+    value, el_ms, rep, roof, kms_step = measure(h, args.mode, args.steps, args.warmup, clk)
+
+    # time to tolerance (second half of the metric): device time of rs_solve to ||r||/||b|| <= tol
+    # for sketch seeds 0 .. seeds-1 (the paper reports medians and quartiles over runs, P:L909);
+    # each seed's first solve builds its graph (untimed)
+    tol_runs = []
+    for sd in range(args.seeds):
+        kw = dict(common, seed=sd)
+        rs.rs_solve(h, tol=cfg.tol, max_iter=args.max_iter_tol, check_every=0, **kw)
+        ms, rp_ = timed(h, tol=cfg.tol, max_iter=args.max_iter_tol, check_every=0, **kw)
+        tol_runs.append((sd, ms / 1e3, rp_["iterations"], rp_["converged"], rp_["rel_residual"]))
+    setup_s = rep["setup_seconds"]
+    rs.rs_destroy(h)
+    t_q = _quartiles([t for _, t, _, _, _ in tol_runs])
+    i_q = _quartiles([i for _, _, i, _, _ in tol_runs])
+    seeds_rec = {"seeds": [s_ for s_, _, _, _, _ in tol_runs],
+                 "seconds": [t for _, t, _, _, _ in tol_runs],
+                 "iterations": [i for _, _, i, _, _ in tol_runs],
+                 "converged": [c for _, _, _, c, _ in tol_runs],
+                 "seconds_q1_median_q3": list(t_q), "iterations_q1_median_q3": list(i_q)}
+    conv_all = all(c for _, _, _, c, _ in tol_runs)
+
+    # the other routes on the same resident data (informational; device time).  EXPLICIT pays the
+    # A = X^T X + lambda I build once (rs_create's setup_seconds: device work only, no allocator
+    # time) and then never streams X; GRAM streams X once per iteration; IMPLICIT forms A S on the
+    # FP64 tensor cores every iteration (SURVEY §8(a) a3).
+    alt = {}
+    if cfg.kind == "dense" and world == 1 and not args.no_alt:
+        routes = ["gram", "implicit"] if args.mode == "explicit" else ["explicit"]
+        for mode in routes:
+            if mode == args.mode:
+                continue
+            try:
+                ha = create(Xd, yd, True, mode)
+                steps_a = {"explicit": args.steps, "gram": 8 if big else args.steps,
+                           "implicit": 2 if big else 20}[mode]
+                warm_a = 3 if mode != "implicit" or not big else 1
+                v_a, _, rep_a, roof_a, _ = measure(ha, mode, steps_a, warm_a)
+                rec = {"iters_per_s": v_a, "steps": steps_a, "warmup": warm_a,
+                       "setup_s": rep_a["setup_seconds"],
+                       "roofline": {k: roof_a[k] for k in ("kernel", "bound", "achieved", "peak",
+                                                           "unit", "frac", "dominant_class",
+                                                           "share_of_step") if k in roof_a}}
+                if mode == "explicit" or steps_a * 8 >= i_q[1]:
+                    rs.rs_solve(ha, tol=cfg.tol, max_iter=args.max_iter_tol, check_every=0,
+                                **common)
+                    ms, rp_ = timed(ha, tol=cfg.tol, max_iter=args.max_iter_tol, check_every=0,
+                                    **common)
+                    rec.update(time_to_tol_s=ms / 1e3, iterations_to_tol=rp_["iterations"],
+                               converged=rp_["converged"])
+                else:   # same sketch stream, same iterates: the headline route's iteration count
+                    rec.update(time_to_tol_s_extrapolated=tol_runs[0][2] / v_a,
+                               note=f"extrapolated: {tol_runs[0][2]} iterations (seed 0, same "
+                                    f"sketch stream) / measured iters/s")
+                rec["time_to_tol_incl_setup_s"] = rec.get(
+                    "time_to_tol_s", rec.get("time_to_tol_s_extrapolated", 0.0)) + rec["setup_s"]
+                rs.rs_destroy(ha)
+                alt[mode] = rec
+            except Exception as ex:   # an informational leg must not sink the line
+                alt[mode] = {"error": str(ex)[:300]}
+
+    # end to end through the public API from pinned host buffers (rank-local shard): H2D of X and
+    # y, rs_create (setup: A build / b), rs_solve to tol, w to the host -- all inside the region
+    e2e = None
+    Xh = None
+    if not args.no_e2e:
+        try:
+            if cfg.kind in ("dense", "kernel"):
+                Xh = torch.empty(tuple(Xd.shape), dtype=torch.float64, pin_memory=True)
+                Xh.copy_(Xd)
+            else:
+                Xh = tuple(t.cpu().pin_memory() for t in Xd)
+            yh = yd.cpu().pin_memory()
+            if big:   # the device copy is the library's from here on: free the resident one
+                del Xd
+                torch.cuda.synchronize()
+                torch.cuda.empty_cache()
+                Xd = None
+            h2d = sum(t.numel() * t.element_size() for t in (Xh if isinstance(Xh, tuple) else (Xh,)))
+            h2d += yh.numel() * 8
+            barrier()
+            e4, e5 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e4.record(stream)
+            h2 = create(Xh, yh, False)
+            w, rep_e2e = rs.rs_solve(h2, tol=cfg.tol, max_iter=args.max_iter_tol, check_every=0,
+                                     **common)
+            e5.record(stream)
+            barrier()
+            rs.rs_destroy(h2)
+            e2e_ms = max_over_ranks(e4.elapsed_time(e5))
+            e2e = {"value": rep_e2e["iterations"] / (e2e_ms / 1e3), "unit": "iters/s",
+                   "h2d_bytes_per_step": int(h2d),
+                   "d2h_bytes_per_step": int(w.size * 8),
+                   "step": "one public-API solve: rs_create_(dense|csr)(pinned host X, y) + rs_solve "
+                           "to tol + w to host",
+                   "seconds": e2e_ms / 1e3, "iterations": rep_e2e["iterations"],
+                   "setup_s": rep_e2e["setup_seconds"], "solve_s": rep_e2e["solve_seconds"]}
+        except Exception as ex:
+            e2e = {"skipped": f"{type(ex).__name__}: {str(ex)[:300]}"}
 
     # CPU baseline: the oracle on a bounded sample, rank 0, N = 1 only
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline and not big:
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
         from oracle import solver as OV
-        if host is None:
-            X = Xd.cpu().numpy()
-            y = yd.cpu().numpy()
-        else:
+        if host is not None:
             X = rsinputs.csr_to_scipy(host[0], host[1], host[2], cfg.n, cfg.d)
             y = host[3]
-        if cfg.kind == "kernel":
-            from oracle import problem as OP
-            sysk = OP.build_kernel(X, y, cfg.lam, cfg.extra["sigma"])
-            op = OV.Operator.from_system(sysk["A"], sysk["b"])
-            del sysk
+            sample = "full X"
+        elif cfg.kind == "kernel":
+            X, y = Xk, yk
+            sample = "full kernel system"
+        elif big:
+            src = Xh if isinstance(Xh, torch.Tensor) else Xd
+            X = src[:ORACLE_ROWS].cpu().numpy()
+            y = yd[:ORACLE_ROWS].cpu().numpy()
+            sample = (f"A = X_s^T X_s + lambda I from the first {ORACLE_ROWS} of the {cfg.n} rows "
+                      f"(an EXPLICIT iteration costs the same for any {cfg.d} x {cfg.d} A)")
         else:
-            op = OV.Operator(X, y, cfg.lam, explicit=(args.mode == "explicit"))
+            X = Xd.cpu().numpy() if Xd is not None else Xh.numpy()
+            y = yd.cpu().numpy()
+            sample = "full X"
+        op = _oracle_operator(cfg, args.mode, X, y)
         kw = dict(seed=0, subcount_k=cfg.subcount_k)
         OV.solve_momentum(op, cfg.sketch, cfg.tau, cfg.gamma, cfg.beta, 0.0, 1, **kw)
         t0 = time.perf_counter()
@@ -620,10 +732,10 @@ def run_ours(args):
             OV.solve_momentum(op, cfg.sketch, cfg.tau, cfg.gamma, cfg.beta, 0.0, 1, **kw)
         el = time.perf_counter() - t0
         cpu = {"value": n_it / el, "unit": "iters/s", "cores": os.cpu_count(), "kind": "oracle",
-               "sample": f"{n_it} oracle Alg. 2 iterations of {cfg.name} (full X, NumPy/SciPy "
-                         f"fp64, BLAS on all host cores, 1 warm-up iteration excluded), "
-                         f"{el:.1f} s"}
-        del X, y
+               "sample": f"{n_it} oracle Alg. 2 iterations of {cfg.name} ({args.mode} AS; "
+                         f"{sample}; NumPy/SciPy fp64, BLAS on all host cores, 1 warm-up iteration "
+                         f"excluded), {el:.1f} s"}
+        del X, y, op
 
     if rank == 0:
         line = {
@@ -633,14 +745,16 @@ def run_ours(args):
             "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded; DESIGN.md §5 recipe for BASELINE.json " + cfg.name + ")",
             "config": _config_dict(cfg, args, world),
-            "time_to_tol_s": tol_ms / 1e3, "iterations_to_tol": rep_tol["iterations"],
-            "setup_s": rep_tol["setup_seconds"],
+            "time_to_tol_s": t_q[1], "iterations_to_tol": i_q[1],
+            "time_to_tol_seeds": seeds_rec,
+            "time_to_tol_incl_setup_s": t_q[1] + setup_s,
+            "setup_s": setup_s,
             "setup": "device work of rs_create: b = X^T y (+ explicit A = X^T X + lambda I, CSC copy)",
-            "converged": rep_tol["converged"], "rel_residual": rep_tol["rel_residual"],
-            "alt_route": alt,
+            "converged": conv_all, "rel_residual": tol_runs[0][4],
+            "alt_routes": alt or None,
             "e2e": e2e, "gpu_launches": rep["gpu_launches"], "roofline": roof,
             "cpu_baseline": cpu, "clocks": clk.summary(),
-            "kernel_ms_per_step": {k: kms[k] / args.steps for k in kms},
+            "kernel_ms_per_step": kms_step,
         }
         print(json.dumps(line), flush=True)
     if pg is not None:
@@ -655,9 +769,11 @@ def main():
     ap.add_argument("--steps", type=int, default=1000)   # a timed region of ~0.4 s on c2
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="c2")
+    ap.add_argument("--config", default="c5")
     ap.add_argument("--mode", default=None, choices=["implicit", "explicit", "gram"],
-                    help="how A S is formed (default: gram)")
+                    help="how A S is formed (default: DEFAULT_MODE of the config)")
+    ap.add_argument("--seeds", type=int, default=5, help="sketch seeds of the time-to-tol runs")
+    ap.add_argument("--no-alt", action="store_true", help="skip the other routes' measurements")
     ap.add_argument("--max-iter-tol", type=int, default=20000)
     ap.add_argument("--momentum", default="constant", choices=["constant", "heuristic", "theory", "cor1"],
                     help="momentum schedule (BASELINE.json configs: constant gamma, beta)")
