@@ -38,7 +38,7 @@ def _flags():
     return ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3",
                    "-I" + os.path.join(ROOT, "include"), "-I" + inc,
                    f'-DRS_NCCL_WHEEL_PATH="{lib}"' if lib else "-DRS_NCCL_WHEEL_PATH=nullptr",
-                   "-Xptxas", "-warn-spills"]
+                   "-Xptxas", "-warn-spills"] + os.environ.get("RS_NVCC_EXTRA", "").split()
 
 
 def _sources():

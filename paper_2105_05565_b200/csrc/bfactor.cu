@@ -413,15 +413,18 @@ __host__ __device__ __forceinline__ int bb_tp(int tau) { return (tau + 63) / 64 
 // dimension lda, B ldb (row-major).
 template <bool TA, bool TB>
 __device__ __forceinline__ void mma_tile(double (&acc)[4][4][2], const double* A, int lda,
-                                         const double* B, int ldb, int lane, double sign) {
+                                         const double* B, int ldb, int lane, double sign,
+                                         int R0 = 0, int nR = 4) {
+  // only the 8-row blocks R0 .. R0+nR-1 of the tile (warp-uniform range)
   const int q = lane >> 2, k4 = lane & 3;
-#pragma unroll 4
+#pragma unroll 1
   for (int K = 0; K < 8; ++K) {
     double a[4], b[4];
 #pragma unroll
     for (int R = 0; R < 4; ++R) {
       const int r = 8 * R + q, k = 4 * K + k4;
-      a[R] = sign * (TA ? A[(long long)k * lda + r] : A[(long long)r * lda + k]);
+      a[R] = (R >= R0 && R < R0 + nR)
+                 ? sign * (TA ? A[(long long)k * lda + r] : A[(long long)r * lda + k]) : 0.0;
     }
 #pragma unroll
     for (int C = 0; C < 4; ++C) {
@@ -430,8 +433,9 @@ __device__ __forceinline__ void mma_tile(double (&acc)[4][4][2], const double* A
     }
 #pragma unroll
     for (int R = 0; R < 4; ++R)
+      if (R >= R0 && R < R0 + nR)
 #pragma unroll
-      for (int C = 0; C < 4; ++C) dmma(acc[R][C], a[R], b[C]);
+        for (int C = 0; C < 4; ++C) dmma(acc[R][C], a[R], b[C]);
   }
 }
 __device__ __forceinline__ void acc_load(double (&acc)[4][4][2], const double* Ct, int ld, int lane) {
@@ -451,10 +455,12 @@ __device__ __forceinline__ void acc_zero(double (&acc)[4][4][2]) {
 #pragma unroll
     for (int C = 0; C < 4; ++C) acc[R][C][0] = acc[R][C][1] = 0.0;
 }
-__device__ __forceinline__ void acc_store(const double (&acc)[4][4][2], double* Ct, int ld, int lane) {
+__device__ __forceinline__ void acc_store(const double (&acc)[4][4][2], double* Ct, int ld, int lane,
+                                          int R0 = 0, int nR = 4) {
   const int q = lane >> 2, k4 = lane & 3;
 #pragma unroll
   for (int R = 0; R < 4; ++R)
+    if (R >= R0 && R < R0 + nR)
 #pragma unroll
     for (int C = 0; C < 4; ++C) {
       *reinterpret_cast<double2*>(Ct + (long long)(8 * R + q) * ld + 8 * C + 2 * k4) =
@@ -462,177 +468,63 @@ __device__ __forceinline__ void acc_store(const double (&acc)[4][4][2], double* 
     }
 }
 
-// Diagonal tile p (warp 0): L_pp in registers (lane i = row i, right-looking), written back over
-// the tile; L_pp^{-1} (lane j = column j, forward substitution) written to Di (32 x 32 row-major,
-// zeros above the diagonal).  Returns false if a pivot was <= 0 or non-finite.
-__device__ __noinline__ bool diag_factor(double* D, int ld, double* Di, double (*sL)[33], int lane) {
+// Diagonal tile (one warp), on chip and in compact loops (it runs twice per block-column pair, from
+// a cold instruction cache: fully unrolled register code measured 5x slower): D (32 x 32 shared,
+// leading dim ldd, lower triangle read) is factored in place, right-looking, lane r owning row r;
+// L goes to Lg (global, zeros above the diagonal) and L^{-1} (lane j = column j, forward
+// substitution against the rows of L) to Dig (global, 32 x 32) and Dis (shared, leading dim ldis).
+// Returns true if a pivot was <= 0 or not finite.
+__device__ __noinline__ bool diag_factor_s(double* D, int ldd, double* Lg, int ldl, double* Dig,
+                                           double* Dis, int ldis, int lane) {
   bool bad = false;
-  double v[32];
-#pragma unroll
-  for (int k = 0; k < 32; ++k) v[k] = k <= lane ? D[(long long)lane * ld + k] : 0.0;
-#pragma unroll
+#pragma unroll 1
   for (int j = 0; j < 32; ++j) {
-    double d = __shfl_sync(0xffffffffu, v[j], j);
+    double d = D[j * ldd + j];
     if (!(d > 0.0) || !isfinite(d)) {
       bad = true;
       d = 1.0;
     }
     const double ljj = sqrt(d), inv = 1.0 / ljj;
-    if (lane == j) v[j] = ljj;
-    else if (lane > j) v[j] *= inv;
-    const double lij = lane > j ? v[j] : 0.0;
-#pragma unroll
-    for (int k = j + 1; k < 32; ++k) v[k] -= lij * __shfl_sync(0xffffffffu, lij, k);
-  }
-#pragma unroll
-  for (int k = 0; k < 32; ++k) {
-    const double x = k <= lane ? v[k] : 0.0;
-    D[(long long)lane * ld + k] = x;
-    sL[lane][k] = x;
-  }
-  __syncwarp();
-#pragma unroll 1
-  for (int i = 0; i < 32; ++i) {   // column `lane` of L^{-1}: x_i, reusing v as x
-    double s = (i == lane) ? 1.0 : 0.0;
-#pragma unroll
-    for (int k = 0; k < 32; ++k)
-      if (k < i) s -= sL[i][k] * Di[k * 32 + lane];
-    Di[i * 32 + lane] = i < lane ? 0.0 : s / sL[i][i];
+    __syncwarp();
+    double lrj = 0.0;
+    if (lane > j) {
+      lrj = D[lane * ldd + j] * inv;
+      D[lane * ldd + j] = lrj;
+    }
+    if (lane == j) D[j * ldd + j] = ljj;
+    __syncwarp();
+#pragma unroll 4
+    for (int k = j + 1; k <= lane; ++k) D[lane * ldd + k] -= lrj * D[k * ldd + j];
     __syncwarp();
   }
+#pragma unroll 4
+  for (int r = 0; r < 32; ++r) Lg[(long long)r * ldl + lane] = lane <= r ? D[r * ldd + lane] : 0.0;
+  // x = column `lane` of L^{-1}: x_i = (delta_{i,lane} - sum_{k<i} L_ik x_k) / L_ii (zero for i < lane)
+#pragma unroll 1
+  for (int i = 0; i < 32; ++i) {
+    double t = (i == lane) ? 1.0 : 0.0;
+#pragma unroll 4
+    for (int k = lane; k < i; ++k) t -= D[i * ldd + k] * Dis[k * ldis + lane];
+    const double x = i < lane ? 0.0 : t / D[i * ldd + i];
+    __syncwarp();   // row i of L (read above) may share storage with row i of L^{-1} (Dis == D)
+    Dis[i * ldis + lane] = x;
+    Dig[i * 32 + lane] = x;
+    __syncwarp();
+  }
+  __syncwarp();
   return bad;
 }
 
-__global__ void __launch_bounds__(BB_THREADS, 1)
-k_bfactor_big(FactorSrc src, DevSketch skb, double* __restrict__ Ginv, long long ldgi,
-              long long gi_stride, double* work, long long work_stride, int* __restrict__ flags,
-              const Ctrl* ctrl) {
-  if (slot_unused(ctrl, blockIdx.x)) return;
-  __shared__ double sL[32][33];
-  __shared__ int s_bad;
-  const int slot = blockIdx.x;
-  const DevSketch sk = skb.at(slot);
-  const int tau = sk.tau, tp = bb_tp(tau), Tc = tp / 32;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  double* Wm = work + slot * work_stride;           // tp x tp, row-major
-  double* dinv = Wm + (long long)tp * tp;           // Tc tiles 32 x 32 (L_pp^{-1})
-  double* tmp = dinv + (long long)Tc * 1024;        // Tc tiles (T_I)
-  auto T = [&](int I, int J) { return Wm + (long long)(32 * I) * tp + 32 * J; };
-  if (tid == 0) s_bad = 0;
-
-  // ---- a4: lower triangle of G (R3 empty-bucket rule), identity on the padding
-  const double* ASt = src.ASt ? src.ASt + slot * src.as_stride : nullptr;
-  const double* Gram = src.Gram ? src.Gram + slot * src.gram_stride : nullptr;
-  for (int a = warp; a < tp; a += BB_WARPS) {
-    const int a32 = a & ~31;
-    const int e0 = a < tau ? sk.bptr[a] : 0, e1 = a < tau ? sk.bptr[a + 1] : 0;
-    for (int c = lane; c < a32 + 32; c += 32) {   // every lower tile of row a
-      double v = 0.0;
-      if (a >= tau || c >= tau || c > a) {
-        v = (a == c) ? 1.0 : 0.0;
-      } else if (Gram) {
-        v = Gram[(long long)a * src.ld_gram + c];
-        if (a == c) v += src.lambda * (double)(e1 - e0);
-      } else if (!ASt) {
-        const int f0 = sk.bptr[c], f1 = sk.bptr[c + 1];
-        for (int e = e0; e < e1; ++e) {
-          const double* Ae = src.A + (long long)sk.coord[e] * src.lda;
-          double t = 0.0;
-          for (int f = f0; f < f1; ++f) {
-            const double x = Ae[sk.coord[f]];
-            t += sk.sign[f] > 0 ? x : -x;
-          }
-          v += sk.sign[e] > 0 ? t : -t;
-        }
-      } else {
-        const double* col = ASt + (long long)c * src.ld_as;
-        for (int e = e0; e < e1; ++e) {
-          const double x = col[sk.coord[e]];
-          v += sk.sign[e] > 0 ? x : -x;
-        }
-      }
-      if (a < tau && c < tau && c <= a && (e0 == e1 || sk.bptr[c] == sk.bptr[c + 1]))
-        v = (a == c) ? 1.0 : 0.0;
-      Wm[(long long)a * tp + c] = v;
-    }
-  }
-  __syncthreads();
-
-  double acc[4][4][2];
-  // ---- a5: Cholesky G = L L^T
-  for (int p = 0; p < Tc; ++p) {
-    if (warp == 0) {
-      const bool bad = diag_factor(T(p, p), tp, dinv + (long long)p * 1024, sL, lane);
-      if (bad && lane == 0) s_bad = 1;
-    }
-    __syncthreads();
-    // panel: L_ip = G_ip (L_pp^{-1})^T, in place (the warp reads its whole tile before storing)
-    for (int i = p + 1 + warp; i < Tc; i += BB_WARPS) {
-      acc_zero(acc);
-      mma_tile<false, true>(acc, T(i, p), tp, dinv + (long long)p * 1024, 32, lane, 1.0);
-      acc_store(acc, T(i, p), tp, lane);
-    }
-    __syncthreads();
-    // trailing: G_ij -= L_ip L_jp^T, p < j <= i
-    {
-      const int nt = Tc - 1 - p, ntiles = nt * (nt + 1) / 2;
-      for (int t = warp; t < ntiles; t += BB_WARPS) {
-        int Ii, Jj;
-        tri_decode(t, Ii, Jj);
-        const int i = p + 1 + Ii, j = p + 1 + Jj;
-        acc_load(acc, T(i, j), tp, lane);
-        mma_tile<false, true>(acc, T(i, p), tp, T(j, p), tp, lane, -1.0);
-        acc_store(acc, T(i, j), tp, lane);
-      }
-    }
-    __syncthreads();
-  }
-  if (s_bad) {
-    if (tid == 0) flags[slot] = 1;
-    return;
-  }
-  // ---- W = L^{-1}, block columns J = Tc-1 .. 0 (W_IK final for K > J; L_KJ still L)
-  for (int J = Tc - 1; J >= 0; --J) {
-    for (int I = J + 1 + warp; I < Tc; I += BB_WARPS) {
-      acc_zero(acc);
-      for (int K = J + 1; K <= I; ++K) mma_tile<false, false>(acc, T(I, K), tp, T(K, J), tp, lane, 1.0);
-      acc_store(acc, tmp + (long long)I * 1024, 32, lane);
-    }
-    __syncthreads();
-    // W_IJ = -T_I W_JJ over L_IJ;  W_JJ = L_JJ^{-1} over L_JJ
-    for (int I = J + 1 + warp; I < Tc; I += BB_WARPS) {
-      acc_zero(acc);
-      mma_tile<false, false>(acc, tmp + (long long)I * 1024, 32, dinv + (long long)J * 1024, 32, lane,
-                             -1.0);
-      acc_store(acc, T(I, J), tp, lane);
-    }
-    if (warp == BB_WARPS - 1) {
-      const double* Wjj = dinv + (long long)J * 1024;
-      double* D = T(J, J);
-      for (int q = lane; q < 1024; q += 32) D[(long long)(q >> 5) * tp + (q & 31)] = Wjj[q];
-    }
-    __syncthreads();
-  }
-  // ---- the slot receives W = L^{-1} in its lower triangle and W^T in its upper triangle (both
-  // row-contiguous): G^{-1} = W^T W is applied as two triangular GEMVs per iteration (k_apply_w,
-  // k_apply_wt), which saves the W^T W product (a third of the factorisation's flops)
-  double* Gi = Ginv + slot * gi_stride;
-  for (int row = warp; row < tau; row += BB_WARPS)
-    for (int col = lane; col <= row; col += 32) {
-      const double x = Wm[(long long)row * tp + col];
-      Gi[(long long)row * ldgi + col] = x;
-      if (col < row) Gi[(long long)col * ldgi + row] = x;
-    }
-  if (tid == 0) flags[slot] = 0;
-}
-
 // -------------------------------------------------------------------------------------------------
-// Left-looking variant (default for tau > 224): block columns are processed in PAIRS (64 wide), and
-// the operand every strip of a step shares -- rows p0, p0+1 of L (Cholesky) or block columns J0, J1
-// of L (inverse) -- is staged in shared memory in chunks of LP_KC tile pairs (cp.async, double
-// buffered).  Each warp accumulates a 32 x 64 strip in registers (acc[4][8][2]) from its own row
-// tiles read once per PAIR of block columns, so global traffic is about Tc^3/12 tiles per phase
-// (the right-looking kernel above re-reads and rewrites the trailing matrix every 32 columns).
+// Left-looking variant (default for tau > 224): block columns are processed in PAIRS (64 wide).
+// Each warp accumulates a 32 x 64 strip in registers (acc[4][8][2]) from its own row tiles (the A
+// operand) and the rows every strip of a step shares -- rows p0, p0+1 of L (Cholesky) or block
+// columns J0, J1 of L (inverse), the B operand.  BOTH operands stream through an LP_STAGES-deep
+// cp.async ring in 16-wide k slices (per stage: B 64 x 16 or 16 x 64, and one 32 x 16 A slice per
+// warp), so the DMMA loop reads shared memory only and the slot's work matrix -- which 148 slots
+// in flight keep in HBM, not L2 -- is fetched LP_STAGES - 1 slices ahead.  Global traffic is about
+// Tc^3/12 tiles per phase (the right-looking kernel above re-reads and rewrites the trailing matrix
+// every 32 columns).
 //   Cholesky, pair p0 = 2P:  [C_i,p0 C_i,p0+1] = [G_i,p0 G_i,p0+1] - sum_{k<p0} L_ik [L_p0,k L_p0+1,k]^T
 //     diagonal pair (warp 0): L00 = chol(C00), L10 = C10 L00^-T, L11 = chol(C11 - L10 L10^T)
 //     strips i > p0+1: L_i,p0 = C_i,p0 L00^-T, L_i,p0+1 = (C_i,p0+1 - L_i,p0 L10^T) L11^-T
@@ -643,50 +535,85 @@ k_bfactor_big(FactorSrc src, DevSketch skb, double* __restrict__ Ginv, long long
 //     diagonal pair: W_J1,J0 = -W_J1J1 L_J1,J0 W_J0J0
 constexpr int LP_WARPS = 8;                     // 255 registers: acc[4][8][2] per lane
 constexpr int LP_THREADS = LP_WARPS * 32;
-constexpr int LP_KC = 4;                        // k tiles per staged chunk
-constexpr int LP_LD = 36;                       // staged tile row stride (conflict-free fragments)
-constexpr int LP_TILE = 32 * LP_LD;
-constexpr int LP_CHUNK = 2 * LP_KC * LP_TILE;   // doubles per chunk buffer
-constexpr size_t LP_SMEM = 2 * LP_CHUNK * sizeof(double);
+constexpr int LP_STAGES = 2;                    // double-buffered k tiles (32 deep)
+constexpr int LP_BLD = 36;                      // B [n][k] row stride (Cholesky) and A [r][k]:
+constexpr int LP_ALD = 36;                      //   36 = 4 mod 16 -> conflict-free fragments
+constexpr int LP_BTLD = 68;                     // B [k][n] row stride (inverse), 68 = 4 mod 16
+constexpr int LP_BSZ = 64 * LP_BLD;             // >= 32 * LP_BTLD
+constexpr int LP_ASZ = 32 * LP_ALD;
+constexpr int LP_STAGE = LP_BSZ + LP_WARPS * LP_ASZ;   // doubles per stage
+#ifdef RS_BF_PHASES
+// development probe (build with RS_NVCC_EXTRA=-DRS_BF_PHASES): SM cycles per factor phase, summed
+// over CTAs: 0 gather, 1 chol accumulate, 2 chol diag, 3 chol total, 4 inv accumulate, 5 inv total,
+// 6 inv diag, 7 write-out
+__device__ unsigned long long g_bf_phase[8];
+#define BF_T(v) long long v = clock64()
+#define BF_ADD(ph, a, b) if (threadIdx.x == 0) atomicAdd(&g_bf_phase[ph], (unsigned long long)((b) - (a)))
+#else
+#define BF_T(v)
+#define BF_ADD(ph, a, b)
+#endif
+constexpr size_t LP_SMEM = ((size_t)LP_STAGES * LP_STAGE + 3 * 32 * 36) * sizeof(double);   // ring + pair tiles
+static_assert(LP_WARPS * 32 * 36 <= LP_STAGES * LP_STAGE, "finishing scratch must fit the ring");
+static_assert(32 * LP_BTLD <= LP_BSZ, "inverse B tile must fit the B region");
+
+// One 32-deep k tile of a strip: acc[R][C] += A[8R+q][k] B(k, 8C+q) -- A [r][k] (LP_ALD), B [n][k]
+// (LP_BLD, Cholesky) or [k][n] (LP_BTLD, inverse).
+template <bool CHOL>
+__device__ __forceinline__ void lp_slice(double (&acc)[4][8][2], const double* xs, const double* ys,
+                                         int q, int k4);
 
 __device__ __forceinline__ void lp_cp16(double* smem, const double* gmem) {
   const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem));
 }
 
-__global__ void __launch_bounds__(LP_THREADS, 1)
-k_bfactor_lp(FactorSrc src, DevSketch skb, double* __restrict__ Ginv, long long ldgi,
-             long long gi_stride, double* work, long long work_stride, int* __restrict__ flags,
-             const Ctrl* ctrl) {
-  if (slot_unused(ctrl, blockIdx.x)) return;
-  extern __shared__ __align__(16) double lp_sm[];   // 2 chunk buffers (the a4 gather: sketch)
-  __shared__ double sL[32][33];
-  __shared__ int s_bad;
-  const int slot = blockIdx.x;
-  const DevSketch sk = skb.at(slot);
-  const int tau = sk.tau, tp = bb_tp(tau), Tc = tp / 32;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int q = lane >> 2, k4 = lane & 3;
-  double* Wm = work + slot * work_stride;           // tp x tp, row-major
-  double* dinv = Wm + (long long)tp * tp;           // Tc tiles 32 x 32 (L_pp^{-1})
-  double* scr = dinv + (long long)Tc * 1024;        // 2 tiles per warp
-  auto T = [&](int I, int J) { return Wm + (long long)(32 * I) * tp + 32 * J; };
-  if (tid == 0) s_bad = 0;
+template <bool CHOL>
+__device__ __forceinline__ void lp_slice(double (&acc)[4][8][2], const double* xs, const double* ys,
+                                         int q, int k4) {
+#pragma unroll
+  for (int K = 0; K < 8; ++K) {
+    double a[4];
+#pragma unroll
+    for (int R = 0; R < 4; ++R) a[R] = xs[(8 * R + q) * LP_ALD + 4 * K + k4];
+#pragma unroll
+    for (int C = 0; C < 8; ++C) {
+      const int n = 8 * C + q, kq = 4 * K + k4;
+      const double b = CHOL ? ys[n * LP_BLD + kq] : ys[kq * LP_BTLD + n];
+#pragma unroll
+      for (int R = 0; R < 4; ++R) dmma(acc[R][C], a[R], b);
+    }
+  }
+}
 
-  // ---- a4: lower triangle of G (R3 empty-bucket rule), identity on the padding.  From explicit A
-  // with the slot's sketch staged in the (not yet used) chunk buffers: coord_e (sign folded in as
-  // bit complement) and bptr, so each element costs one independent gather of A.
+// a4 for the large-tau factorisation: the lower triangle of G = S^T A S (R3 empty-bucket rule,
+// identity on the padding) into each slot's work matrix, one warp per row, blockIdx.y = slot.  A
+// kernel of its own (many warps per SM, no shared-memory ring) so that the random gathers from A
+// have full memory-level parallelism.  The slot's sketch is staged per block: coord_e (sign folded
+// in as bit complement) and bptr, so each element costs one independent gather of A.
+constexpr int GA_WARPS = 8;
+constexpr size_t GA_SMEM = (size_t)(4096 + 1 + 8192) * 4;
+__global__ void __launch_bounds__(GA_WARPS * 32)
+k_bf_gather(FactorSrc src, DevSketch skb, double* work, long long work_stride, const Ctrl* ctrl) {
+  const int slot = blockIdx.y;
+  if (slot_unused(ctrl, slot)) return;
+  extern __shared__ __align__(16) double ga_sm[];
+  const DevSketch sk = skb.at(slot);
+  const int tau = sk.tau, tp = bb_tp(tau);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  double* Wm = work + slot * work_stride;
+
   const double* ASt = src.ASt ? src.ASt + slot * src.as_stride : nullptr;
   const double* Gram = src.Gram ? src.Gram + slot * src.gram_stride : nullptr;
-  int* s_bp = reinterpret_cast<int*>(lp_sm);
+  int* s_bp = reinterpret_cast<int*>(ga_sm);
   int* s_ce = s_bp + tau + 1;
-  const bool staged = !Gram && !ASt && (size_t)(tau + 1 + sk.len) * 4 <= LP_SMEM;
+  const bool staged = !Gram && !ASt && (size_t)(tau + 1 + sk.len) * 4 <= GA_SMEM;
   if (staged) {
-    for (int b = tid; b <= tau; b += LP_THREADS) s_bp[b] = sk.bptr[b];
-    for (int e = tid; e < sk.len; e += LP_THREADS) s_ce[e] = sk.sign[e] > 0 ? sk.coord[e] : ~sk.coord[e];
+    for (int b = tid; b <= tau; b += GA_WARPS * 32) s_bp[b] = sk.bptr[b];
+    for (int e = tid; e < sk.len; e += GA_WARPS * 32) s_ce[e] = sk.sign[e] > 0 ? sk.coord[e] : ~sk.coord[e];
     __syncthreads();
   }
-  for (int a = warp; a < tp; a += LP_WARPS) {
+  for (int a = blockIdx.x * GA_WARPS + warp; a < tp; a += gridDim.x * GA_WARPS) {
     const int a32 = a & ~31;
     const int e0 = a < tau ? (staged ? s_bp[a] : sk.bptr[a]) : 0;
     const int e1 = a < tau ? (staged ? s_bp[a + 1] : sk.bptr[a + 1]) : 0;
@@ -761,78 +688,135 @@ k_bfactor_lp(FactorSrc src, DevSketch skb, double* __restrict__ Ginv, long long 
       Wm[(long long)a * tp + c] = v;
     }
   }
-  __syncthreads();
+}
 
-  // chunk staging: tiles (h, kk), h = 0, 1, kk < LP_KC; Cholesky: T(p0 + h, k), inverse: T(k, p0 + h)
-  auto stage = [&](int buf, bool chol, int p0, int k0, int kend) {
-    double* dst = lp_sm + buf * LP_CHUNK;
-    for (int t = tid; t < 2 * LP_KC * 32 * 16; t += LP_THREADS) {   // 16-byte pieces
-      const int tile = t >> 9, rr = (t >> 4) & 31, c16 = t & 15;
-      const int h = tile / LP_KC, kk = tile % LP_KC, k = k0 + kk;
-      if (k >= kend) continue;
-      const double* srcp = chol ? T(p0 + h, k) : T(k, p0 + h);
-      lp_cp16(dst + tile * LP_TILE + rr * LP_LD + 2 * c16, srcp + (long long)rr * tp + 2 * c16);
+__global__ void __launch_bounds__(LP_THREADS, 1)
+k_bfactor_lp(FactorSrc src, DevSketch skb, double* __restrict__ Ginv, long long ldgi,
+             long long gi_stride, double* work, long long work_stride, int* __restrict__ flags,
+             const Ctrl* ctrl) {
+  if (slot_unused(ctrl, blockIdx.x)) return;
+  BF_T(t_start);
+  extern __shared__ __align__(16) double lp_sm[];   // LP_STAGES slice buffers (a4 gather: sketch)
+  __shared__ int s_bad;
+  const int slot = blockIdx.x;
+  const DevSketch sk = skb.at(slot);
+  const int tau = sk.tau, tp = bb_tp(tau), Tc = tp / 32;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int q = lane >> 2, k4 = lane & 3;
+  double* Wm = work + slot * work_stride;           // tp x tp, row-major
+  double* dinv = Wm + (long long)tp * tp;           // Tc tiles 32 x 32 (L_pp^{-1})
+  double* scr = dinv + (long long)Tc * 1024;        // 2 tiles per warp
+  auto T = [&](int I, int J) { return Wm + (long long)(32 * I) * tp + 32 * J; };
+  if (tid == 0) s_bad = 0;
+
+  // ---- a4: lower triangle of G in the work matrix (k_bf_gather, the preceding launch)
+
+
+  // Work split of a round of m strips (m <= LP_WARPS): spw warps per strip, part `part` of them
+  // accumulating the k tiles kt with (kt - kb) % spw == part; the partial accumulators are summed
+  // into part 0 in part order (deterministic) -- short rounds (the last pairs of each phase) keep
+  // every warp on the DMMA pipe.  Returns the strip slot j (-1: idle warp).
+  auto split = [&](int m, int& spw, int& part) {
+    spw = m <= 2 ? 4 : (m <= 4 ? 2 : 1);
+    part = warp % spw;
+    const int j = warp / spw;
+    return j < m ? j : -1;
+  };
+  // k slice s of [kb, ke) = tile kb + s (32 deep).  Stage buffer: B then one A tile per warp.  Every
+  // thread commits one group per slice (possibly empty), so wait_group counts stay uniform.
+  double acc[4][8][2];
+  auto issue = [&](int s, bool chol, int p0, int kb, bool act_a, int i) {
+    double* buf = lp_sm + (s % LP_STAGES) * LP_STAGE;
+    const int kt = kb + s;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {   // B: 1024 pieces of 16 bytes, four per thread
+      const int t = tid + LP_THREADS * u;
+      if (chol) {   // rows n of L_{p0 + n/32, kt} -> [n][LP_BLD]
+        const int n = t >> 4, c16 = t & 15;
+        lp_cp16(buf + n * LP_BLD + 2 * c16, T(p0 + (n >> 5), kt) + (long long)(n & 31) * tp + 2 * c16);
+      } else {      // rows kr of tiles (kt, p0 + h), all 64 columns -> [kr][LP_BTLD]
+        const int kr = t >> 5, n32 = t & 31;
+        lp_cp16(buf + kr * LP_BTLD + 2 * n32, T(kt, p0 + (n32 >> 4)) + (long long)kr * tp + 2 * (n32 & 15));
+      }
+    }
+    if (act_a) {   // A: the warp's tile T(i, kt), 16 pieces per lane
+      double* a = buf + LP_BSZ + warp * LP_ASZ;
+      const double* srcA = T(i, kt);
+#pragma unroll
+      for (int u = 0; u < 16; ++u) {
+        const int t = lane + 32 * u, r = t >> 4, c16 = t & 15;
+        lp_cp16(a + r * LP_ALD + 2 * c16, srcA + (long long)r * tp + 2 * c16);
+      }
     }
     asm volatile("cp.async.commit_group;\n");
   };
-  // strip accumulation over staged chunks [kb, ke); strip row i uses k <= klim only
-  double acc[4][8][2];
-  auto accumulate = [&](bool chol, int p0, int kb, int ke, int i, int klim) {
+  // strip accumulation over k tiles [kb, ke); strip row i (-1: idle warp) uses k <= klim only
+  auto accumulate = [&](bool chol, int p0, int kb, int ke, int i, int klim, int spw, int part) {
 #pragma unroll
     for (int R = 0; R < 4; ++R)
 #pragma unroll
       for (int C = 0; C < 8; ++C) acc[R][C][0] = acc[R][C][1] = 0.0;
-    const int nch = (ke - kb + LP_KC - 1) / LP_KC;
-    if (nch > 0) stage(0, chol, p0, kb, ke);
-    for (int c = 0; c < nch; ++c) {
-      if (c + 1 < nch) stage((c + 1) & 1, chol, p0, kb + (c + 1) * LP_KC, ke);
+    const int ns = ke - kb;
+    if (ns <= 0) return;
+    __syncthreads();   // the ring doubles as the strips' finishing scratch
+    BF_T(t_acc0);
+    auto mine = [&](int s) { return i >= 0 && kb + s <= klim && (s % spw) == part; };
+#pragma unroll 1
+    for (int s = 0; s < LP_STAGES - 1; ++s) {
+      if (s < ns) issue(s, chol, p0, kb, mine(s), i);
       else asm volatile("cp.async.commit_group;\n");
-      asm volatile("cp.async.wait_group 1;\n");
-      __syncthreads();
-      const double* ys = lp_sm + (c & 1) * LP_CHUNK;
-      if (i >= 0) {
-        for (int kk = 0; kk < LP_KC; ++kk) {
-          const int k = kb + c * LP_KC + kk;
-          if (k >= ke || k > klim) break;
-          const double* X = T(i, k);
-          if (k + 1 < ke && k + 1 <= klim) {   // next tile of the strip row into L1 (2 lines per row)
-            const double* nx = X + 32 + (long long)lane * tp;
-            asm volatile("prefetch.global.L1 [%0];\n" ::"l"(nx));
-            asm volatile("prefetch.global.L1 [%0];\n" ::"l"(nx + 16));
-          }
-          const double* y0 = ys + kk * LP_TILE;
-          const double* y1 = ys + (LP_KC + kk) * LP_TILE;
-#pragma unroll 2
-          for (int K = 0; K < 8; ++K) {
-            double a[4];
+    }
+#pragma unroll 1
+    for (int s = 0; s < ns; ++s) {
+      asm volatile("cp.async.wait_group %0;\n" ::"n"(LP_STAGES - 2));
+      __syncthreads();   // slice s landed for every warp; slice s-1's buffer is free
+      if (s + LP_STAGES - 1 < ns) issue(s + LP_STAGES - 1, chol, p0, kb, mine(s + LP_STAGES - 1), i);
+      else asm volatile("cp.async.commit_group;\n");
+      if (mine(s)) {
+        const double* buf = lp_sm + (s % LP_STAGES) * LP_STAGE;
+        const double* xs = buf + LP_BSZ + warp * LP_ASZ;
+        if (chol) lp_slice<true>(acc, xs, buf, q, k4);
+        else lp_slice<false>(acc, xs, buf, q, k4);
+      }
+    }
+    asm volatile("cp.async.wait_group 0;\n");
+    __syncthreads();   // the ring is free for the caller (and for the next accumulate)
+    if (spw > 1) {     // sum the parts into part 0, in part order, through the ring
+      double* red = lp_sm + warp * 2048;
+      if (part > 0 && i >= 0)
 #pragma unroll
-            for (int R = 0; R < 4; ++R) a[R] = X[(long long)(8 * R + q) * tp + 4 * K + k4];
+        for (int R = 0; R < 4; ++R)
+#pragma unroll
+          for (int C = 0; C < 8; ++C) {
+            red[((R * 8 + C) * 2 + 0) * 32 + lane] = acc[R][C][0];
+            red[((R * 8 + C) * 2 + 1) * 32 + lane] = acc[R][C][1];
+          }
+      __syncthreads();
+      if (part == 0 && i >= 0)
+        for (int pp = 1; pp < spw; ++pp) {
+          const double* rp = lp_sm + (warp + pp) * 2048;
+#pragma unroll
+          for (int R = 0; R < 4; ++R)
 #pragma unroll
             for (int C = 0; C < 8; ++C) {
-              const double* y = C < 4 ? y0 : y1;
-              const int n = 8 * (C & 3) + q, kq = 4 * K + k4;
-              const double b = chol ? y[n * LP_LD + kq] : y[kq * LP_LD + n];
-#pragma unroll
-              for (int R = 0; R < 4; ++R) dmma(acc[R][C], a[R], b);
+              acc[R][C][0] += rp[((R * 8 + C) * 2 + 0) * 32 + lane];
+              acc[R][C][1] += rp[((R * 8 + C) * 2 + 1) * 32 + lane];
             }
-          }
         }
-      }
       __syncthreads();
     }
+    BF_T(t_acc1);
+    BF_ADD(chol ? 1 : 4, t_acc0, t_acc1);
   };
   // store half h of the strip accumulator (8 x 8 blocks C = 4h .. 4h+3) to a 32 x 32 tile,
-  // optionally as base - acc
+  // optionally as base - acc (base may alias Ct: read in full before the stores)
   auto store_half = [&](int h, double* Ct, int ld, const double* base, int ldb) {
-    // base (may alias Ct) is read in full before the first store: one batch of 16 double2 loads
-    // instead of 16 load -> store round trips
     double2 bv[4][4];
 #pragma unroll
     for (int R = 0; R < 4; ++R)
 #pragma unroll
       for (int C = 0; C < 4; ++C)
-        bv[R][C] = base ? *reinterpret_cast<const double2*>(base + (long long)(8 * R + q) * ldb +
-                                                            8 * C + 2 * k4)
+        bv[R][C] = base ? *reinterpret_cast<const double2*>(base + (long long)(8 * R + q) * ldb + 8 * C + 2 * k4)
                         : make_double2(0.0, 0.0);
 #pragma unroll
     for (int R = 0; R < 4; ++R)
@@ -848,107 +832,243 @@ k_bfactor_lp(FactorSrc src, DevSketch skb, double* __restrict__ Ginv, long long 
       }
   };
   double t32[4][4][2];   // 32 x 32 tile products (mma_tile)
+  // the three tiles every strip of a pair step needs (row-major, LD 36):
+  //   Cholesky: L_p0p0^{-1}, L_p0+1,p0, L_p0+1p0+1^{-1} (written by the diagonal-pair warp);
+  //   inverse:  W_J0J0, L_J1,J0, W_J1J1 (staged once per pair)
+  double* P3 = lp_sm + LP_STAGES * LP_STAGE;
+  constexpr int PLD = 36, PT = 32 * PLD;
+  auto stage3 = [&](const double* t0, int ld0, const double* t1, int ld1, const double* t2, int ld2) {
+    double v[12];   // 3 x 1024 elements, 12 per thread, all loads in flight before the stores
+#pragma unroll
+    for (int u = 0; u < 12; ++u) {
+      const int x = tid + LP_THREADS * u, w = x >> 10, rr = (x >> 5) & 31, cc = x & 31;
+      const double* src = w == 0 ? t0 + (long long)rr * ld0 : w == 1 ? t1 + (long long)rr * ld1
+                                                                     : t2 + (long long)rr * ld2;
+      v[u] = src[cc];
+    }
+#pragma unroll
+    for (int u = 0; u < 12; ++u) {
+      const int x = tid + LP_THREADS * u, w = x >> 10, rr = (x >> 5) & 31, cc = x & 31;
+      P3[w * PT + rr * PLD + cc] = v[u];
+    }
+  };
+  // per-warp 32 x 32 scratch (LD 36) in the slice ring, free between accumulations
+  double* S = lp_sm + warp * PT;
+  // finish Cholesky strip i of pair p0 from its accumulator
+  // acc = sum_{k<p0} L_ik [L_p0,k L_p0+1,k]^T:
+  //   L_i,p0 = (G_i,p0 - acc_0) L00^{-T},  L_i,p0+1 = (G_i,p0+1 - acc_1 - L_i,p0 L10^T) L11^{-T}
+  auto finish_chol = [&](int i, int p0) {
+    store_half(0, S, PLD, T(i, p0), tp);                       // C0
+    __syncwarp();
+    acc_zero(t32);
+    mma_tile<false, true>(t32, S, PLD, P3, PLD, lane, 1.0);    // L_i,p0
+    __syncwarp();
+    acc_store(t32, S, PLD, lane);
+    acc_store(t32, T(i, p0), tp, lane);
+    const double* base = T(i, p0 + 1);
+#pragma unroll
+    for (int R = 0; R < 4; ++R)
+#pragma unroll
+      for (int C = 0; C < 4; ++C) {
+        double2 bv = make_double2(0.0, 0.0);
+        bv = *reinterpret_cast<const double2*>(base + (long long)(8 * R + q) * tp + 8 * C + 2 * k4);
+        t32[R][C][0] = bv.x - acc[R][4 + C][0];
+        t32[R][C][1] = bv.y - acc[R][4 + C][1];
+      }
+    __syncwarp();
+    mma_tile<false, true>(t32, S, PLD, P3 + PT, PLD, lane, -1.0);   // - L_i,p0 L10^T
+    __syncwarp();
+    acc_store(t32, S, PLD, lane);
+    __syncwarp();
+    acc_zero(t32);
+    mma_tile<false, true>(t32, S, PLD, P3 + 2 * PT, PLD, lane, 1.0);   // L_i,p0+1
+    acc_store(t32, T(i, p0 + 1), tp, lane);
+    __syncwarp();
+  };
+  // finish inverse strip I of pair (J0, J1) from acc = [T_I,J0 T_I,J1]:
+  //   W_I,J1 = -T_I,J1 W_J1J1,  W_I,J0 = -(T_I,J0 + W_I,J1 L_J1,J0) W_J0J0
+  auto finish_inv = [&](int I, int J0) {
+    store_half(1, S, PLD, nullptr, 0);                          // T_I,J1
+    __syncwarp();
+    acc_zero(t32);
+    mma_tile<false, false>(t32, S, PLD, P3 + 2 * PT, PLD, lane, -1.0);   // W_I,J1
+    __syncwarp();
+    acc_store(t32, S, PLD, lane);
+    acc_store(t32, T(I, J0 + 1), tp, lane);
+#pragma unroll
+    for (int R = 0; R < 4; ++R)
+#pragma unroll
+      for (int C = 0; C < 4; ++C) {
+        t32[R][C][0] = acc[R][C][0];
+        t32[R][C][1] = acc[R][C][1];
+      }
+    __syncwarp();
+    mma_tile<false, false>(t32, S, PLD, P3 + PT, PLD, lane, 1.0);   // T_I,J0 + W_I,J1 L_J1,J0
+    __syncwarp();
+    acc_store(t32, S, PLD, lane);
+    __syncwarp();
+    acc_zero(t32);
+    mma_tile<false, false>(t32, S, PLD, P3, PLD, lane, -1.0);       // W_I,J0
+    acc_store(t32, T(I, J0), tp, lane);
+    __syncwarp();
+  };
 
-  // ---- a5: Cholesky G = L L^T, block-column pairs
+  // ---- a5: Cholesky G = L L^T, block-column pairs.  Round 0 holds the diagonal pair's rows: their
+  // strips are stored as C, warp 0 factors the pair on chip (C00, L10 and C11 in the pair-tile
+  // buffer, which ends up holding L00^{-1}, L10, L11^{-1} for the panel), and every other strip is
+  // finished from its register accumulator (no C round trip, no panel pass).
+  BF_T(t_c0);
   for (int p0 = 0; p0 < Tc; p0 += 2) {
     const int nstrip = Tc - p0, rounds = (nstrip + LP_WARPS - 1) / LP_WARPS;
     for (int rd = 0; rd < rounds; ++rd) {
-      const int i = p0 + rd * LP_WARPS + warp;
-      accumulate(true, p0, 0, p0, i < Tc ? i : -1, Tc);
-      if (i < Tc) {
-        store_half(0, T(i, p0), tp, T(i, p0), tp);
-        if (i > p0) store_half(1, T(i, p0 + 1), tp, T(i, p0 + 1), tp);
+      int spw, part;
+      const int j = split(min(LP_WARPS, nstrip - rd * LP_WARPS), spw, part);
+      const int i = j < 0 ? -1 : p0 + rd * LP_WARPS + j;
+      const bool own = i >= 0 && part == 0;   // holds the strip's summed accumulator
+      accumulate(true, p0, 0, p0, i, Tc, spw, part);
+      if (rd == 0) {
+        if (own && i == p0) store_half(0, T(i, p0), tp, T(i, p0), tp);
+        if (own && i == p0 + 1) {
+          store_half(0, T(i, p0), tp, T(i, p0), tp);
+          store_half(1, T(i, p0 + 1), tp, T(i, p0 + 1), tp);
+        }
+        __syncthreads();
+        BF_T(t_d0);
+        {   // diagonal pair (64 x 64), all warps, on chip: right-looking with the unscaled rank-1
+            // update M_rc -= M_rj M_cj / M_jj, one barrier per column; column j of L to Lm
+          double* M = lp_sm;                 // 64 x 65 (the ring is free here)
+          double* Lm = lp_sm + 64 * 65;      // 64 x 65
+          {
+            double v[16];
+#pragma unroll
+            for (int u = 0; u < 16; ++u) {
+              const int x = tid + LP_THREADS * u, r = x >> 6, c = x & 63;
+              v[u] = (c <= r) ? T(p0 + (r >> 5), p0 + (c >> 5))[(long long)(r & 31) * tp + (c & 31)] : 0.0;
+            }
+#pragma unroll
+            for (int u = 0; u < 16; ++u) {
+              const int x = tid + LP_THREADS * u, r = x >> 6, c = x & 63;
+              M[r * 65 + c] = v[u];
+              Lm[r * 65 + c] = 0.0;
+            }
+          }
+          __syncthreads();
+          const int ur = tid >> 2, uc = tid & 3;   // update: row j + 1 + ur, columns j + 1 + uc + 4 t
+#pragma unroll 1
+          for (int j = 0; j < 64; ++j) {
+            double d = M[j * 65 + j];
+            if (!(d > 0.0) || !isfinite(d)) {
+              if (tid == 0) s_bad = 1;
+              d = 1.0;
+            }
+            if (tid < 64 && tid >= j) {
+              const double rs = 1.0 / sqrt(d);
+              Lm[tid * 65 + j] = tid == j ? d * rs : M[tid * 65 + j] * rs;
+            }
+            const int r = j + 1 + ur;
+            if (r < 64) {
+              const double f = M[r * 65 + j] / d;
+#pragma unroll 4
+              for (int c = j + 1 + uc; c <= r; c += 4) M[r * 65 + c] -= f * M[c * 65 + j];
+            }
+            __syncthreads();
+          }
+          // L00^{-1} -> P3[0], L11^{-1} -> P3[2]: column jc of block b by 4 threads (partial sums
+          // over k = jc + part (mod 4), shuffle-reduced), rows in order
+          {
+            const int col = tid >> 2, part = tid & 3, b = col >> 5, jc = col & 31;
+            double* Di = P3 + (b ? 2 * PT : 0);
+            const double* Lb = Lm + (32 * b) * 65 + 32 * b;
+#pragma unroll 1
+            for (int i = 0; i < 32; ++i) {
+              double t = 0.0;
+              for (int k = jc + part; k < i; k += 4) t += Lb[i * 65 + k] * Di[k * PLD + jc];
+              t += __shfl_xor_sync(0xffffffffu, t, 1);
+              t += __shfl_xor_sync(0xffffffffu, t, 2);
+              const double x = i < jc ? 0.0 : ((i == jc ? 1.0 : 0.0) - t) / Lb[i * 65 + i];
+              __syncwarp();
+              if (part == 0) Di[i * PLD + jc] = x;
+              __syncwarp();
+            }
+          }
+          __syncthreads();
+          // L tiles to the work matrix, L10 to P3[1], the inverses to dinv
+#pragma unroll 4
+          for (int x = tid; x < 64 * 64; x += LP_THREADS) {
+            const int r = x >> 6, c = x & 63;
+            if (c < 32 || r >= 32) {   // tiles (p0,p0), (p0+1,p0), (p0+1,p0+1)
+              const double lv = c <= r ? Lm[r * 65 + c] : 0.0;
+              T(p0 + (r >> 5), p0 + (c >> 5))[(long long)(r & 31) * tp + (c & 31)] = lv;
+              if (r >= 32 && c < 32) P3[PT + (r - 32) * PLD + c] = lv;
+            }
+          }
+          for (int x = tid; x < 2 * 1024; x += LP_THREADS) {
+            const int b = x >> 10, rr = (x >> 5) & 31, cc = x & 31;
+            dinv[(long long)(p0 + b) * 1024 + rr * 32 + cc] = P3[(b ? 2 * PT : 0) + rr * PLD + cc];
+          }
+        }
+        __syncthreads();
+        BF_T(t_d1);
+        BF_ADD(2, t_d0, t_d1);
       }
+      if (own && i >= p0 + 2) finish_chol(i, p0);
     }
-    __syncthreads();
-    if (warp == 0) {   // diagonal pair
-      bool bad = diag_factor(T(p0, p0), tp, dinv + (long long)p0 * 1024, sL, lane);
-      __syncwarp();
-      acc_zero(t32);
-      mma_tile<false, true>(t32, T(p0 + 1, p0), tp, dinv + (long long)p0 * 1024, 32, lane, 1.0);
-      __syncwarp();
-      acc_store(t32, T(p0 + 1, p0), tp, lane);   // L10
-      __syncwarp();
-      acc_load(t32, T(p0 + 1, p0 + 1), tp, lane);
-      mma_tile<false, true>(t32, T(p0 + 1, p0), tp, T(p0 + 1, p0), tp, lane, -1.0);
-      __syncwarp();
-      acc_store(t32, T(p0 + 1, p0 + 1), tp, lane);
-      __syncwarp();
-      bad |= diag_factor(T(p0 + 1, p0 + 1), tp, dinv + (long long)(p0 + 1) * 1024, sL, lane);
-      if (bad && lane == 0) s_bad = 1;
-    }
-    __syncthreads();
-    for (int i = p0 + 2 + warp; i < Tc; i += LP_WARPS) {   // panel strips
-      acc_zero(t32);
-      mma_tile<false, true>(t32, T(i, p0), tp, dinv + (long long)p0 * 1024, 32, lane, 1.0);
-      __syncwarp();
-      acc_store(t32, T(i, p0), tp, lane);                  // L_i,p0
-      __syncwarp();
-      acc_load(t32, T(i, p0 + 1), tp, lane);
-      mma_tile<false, true>(t32, T(i, p0), tp, T(p0 + 1, p0), tp, lane, -1.0);
-      __syncwarp();
-      acc_store(t32, T(i, p0 + 1), tp, lane);
-      __syncwarp();
-      acc_zero(t32);
-      mma_tile<false, true>(t32, T(i, p0 + 1), tp, dinv + (long long)(p0 + 1) * 1024, 32, lane, 1.0);
-      __syncwarp();
-      acc_store(t32, T(i, p0 + 1), tp, lane);              // L_i,p0+1
-    }
-    __syncthreads();
   }
+  __syncthreads();
+  BF_T(t_c1);
+  BF_ADD(3, t_c0, t_c1);
   if (s_bad) {
     if (tid == 0) flags[slot] = 1;
     return;
   }
   // ---- W = L^{-1}, block-column pairs from the last
-  double* S0 = scr + (long long)warp * 2048;
-  double* S1 = S0 + 1024;
   for (int J0 = Tc - 2; J0 >= 0; J0 -= 2) {
     const int J1 = J0 + 1, nstrip = Tc - 1 - J1;
     const int rounds = (nstrip + LP_WARPS - 1) / LP_WARPS;
+    if (rounds > 0) {
+      __syncthreads();
+      stage3(dinv + (long long)J0 * 1024, 32, T(J1, J0), tp, dinv + (long long)J1 * 1024, 32);
+      __syncthreads();
+    }
     for (int rd = 0; rd < rounds; ++rd) {   // highest strips first
-      const int I = Tc - 1 - (rd * LP_WARPS + warp);
-      const bool act = I > J1;
+      int spw, part;
+      const int j = split(min(LP_WARPS, nstrip - rd * LP_WARPS), spw, part);
+      const int I = j < 0 ? -1 : Tc - 1 - (rd * LP_WARPS + j);
       const int kend = Tc - rd * LP_WARPS;   // rows of this round are <= kend - 1
-      accumulate(false, J0, J1 + 1, kend, act ? I : -1, act ? I : -1);
-      if (act) {
-        store_half(0, S0, 32, nullptr, 0);
-        store_half(1, S1, 32, nullptr, 0);
-        __syncwarp();
+      accumulate(false, J0, J1 + 1, kend, I, I, spw, part);
+      if (I > J1 && part == 0) finish_inv(I, J0);
+    }
+    __syncthreads();
+    BF_T(t_i0);
+    if (rounds == 0) {   // the pair tiles (staged above for pairs with strips)
+      __syncthreads();
+      stage3(dinv + (long long)J0 * 1024, 32, T(J1, J0), tp, dinv + (long long)J1 * 1024, 32);
+      __syncthreads();
+    }
+    {   // diagonal pair: W_J1,J0 = -W_J1J1 L_J1,J0 W_J0J0, warp w < 4 owning rows 8w .. 8w+7
+      double* X = lp_sm;   // 32 x 36 (the ring is free here)
+      if (warp < 4) {
         acc_zero(t32);
-        mma_tile<false, false>(t32, S1, 32, dinv + (long long)J1 * 1024, 32, lane, -1.0);
-        __syncwarp();
-        acc_store(t32, T(I, J1), tp, lane);               // W_I,J1
-        __syncwarp();
-        acc_load(t32, S0, 32, lane);
-        mma_tile<false, false>(t32, T(I, J1), tp, T(J1, J0), tp, lane, 1.0);
-        __syncwarp();
-        acc_store(t32, S0, 32, lane);
-        __syncwarp();
+        mma_tile<false, false>(t32, P3 + 2 * PT, PLD, P3 + PT, PLD, lane, 1.0, warp, 1);
+        acc_store(t32, X, PLD, lane, warp, 1);
+      }
+      __syncthreads();
+      if (warp < 4) {
         acc_zero(t32);
-        mma_tile<false, false>(t32, S0, 32, dinv + (long long)J0 * 1024, 32, lane, -1.0);
-        __syncwarp();
-        acc_store(t32, T(I, J0), tp, lane);               // W_I,J0
+        mma_tile<false, false>(t32, X, PLD, P3, PLD, lane, -1.0, warp, 1);
+        acc_store(t32, T(J1, J0), tp, lane, warp, 1);   // W_J1,J0
+      }
+      for (int qd = tid; qd < 1024; qd += LP_THREADS) {
+        T(J0, J0)[(long long)(qd >> 5) * tp + (qd & 31)] = P3[(qd >> 5) * PLD + (qd & 31)];
+        T(J1, J1)[(long long)(qd >> 5) * tp + (qd & 31)] = P3[2 * PT + (qd >> 5) * PLD + (qd & 31)];
       }
     }
     __syncthreads();
-    if (warp == 0) {   // diagonal pair
-      acc_zero(t32);
-      mma_tile<false, false>(t32, dinv + (long long)J1 * 1024, 32, T(J1, J0), tp, lane, 1.0);
-      __syncwarp();
-      acc_store(t32, S0, 32, lane);
-      __syncwarp();
-      acc_zero(t32);
-      mma_tile<false, false>(t32, S0, 32, dinv + (long long)J0 * 1024, 32, lane, -1.0);
-      __syncwarp();
-      acc_store(t32, T(J1, J0), tp, lane);                // W_J1,J0
-      for (int qd = lane; qd < 1024; qd += 32) {
-        T(J0, J0)[(long long)(qd >> 5) * tp + (qd & 31)] = dinv[(long long)J0 * 1024 + qd];
-        T(J1, J1)[(long long)(qd >> 5) * tp + (qd & 31)] = dinv[(long long)J1 * 1024 + qd];
-      }
-    }
-    __syncthreads();
+    BF_T(t_i1);
+    BF_ADD(6, t_i0, t_i1);
   }
+  BF_T(t_w0);
+  BF_ADD(5, t_c1, t_w0);
   // ---- the slot receives W (lower triangle) and W^T (upper triangle), both row-contiguous:
   // tile (I, J), J <= I, goes to Gi[I][J] and, transposed through a per-warp shared tile, to
   // Gi[J][I] (coalesced both ways)
@@ -976,12 +1096,26 @@ k_bfactor_lp(FactorSrc src, DevSketch skb, double* __restrict__ Ginv, long long 
     }
     __syncwarp();
   }
+  BF_T(t_w1);
+  BF_ADD(7, t_w0, t_w1);
   if (tid == 0) flags[slot] = 0;
 }
 
 }  // namespace
 
 int bfactor_max_tau() { return BB_MAXTAU; }
+
+#ifdef RS_BF_PHASES
+extern "C" int rs_debug_bf_phases(unsigned long long* out, int reset) {
+  cudaDeviceSynchronize();
+  if (cudaMemcpyFromSymbol(out, g_bf_phase, sizeof(g_bf_phase)) != cudaSuccess) return -1;
+  if (reset) {
+    unsigned long long z[8] = {0};
+    cudaMemcpyToSymbol(g_bf_phase, z, sizeof(z));
+  }
+  return 0;
+}
+#endif
 
 size_t bfactor_work_elems(int tau) {
   if (tau <= BF_MAXTAU) return 0;
@@ -1001,6 +1135,8 @@ cudaError_t bfactor_init() {
     e = cudaFuncSetAttribute(k_apply_rows<AP_UPPER>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              ap_smem);
   if (e != cudaSuccess) return e;
+  e = cudaFuncSetAttribute(k_bf_gather, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)GA_SMEM);
+  if (e != cudaSuccess) return e;
   e = cudaFuncSetAttribute(k_bfactor_lp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)LP_SMEM);
   if (e != cudaSuccess) return e;
   return cudaFuncSetAttribute(k_bfactor_small, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1013,12 +1149,11 @@ cudaError_t launch_bfactor(const FactorSrc& src, const DevSketch& skb, int nslot
   if (skb.tau > BB_MAXTAU || nslots < 1) return cudaErrorInvalidValue;
   if (skb.tau > BF_MAXTAU) {
     if (!work) return cudaErrorInvalidValue;
-    static const bool rl = std::getenv("RS_BF_RIGHT") != nullptr;   // A/B: right-looking kernel
-    if (rl)
-      k_bfactor_big<<<nslots, BB_THREADS, 0, st>>>(src, skb, Ginv, ldgi, gi_stride, work,
-                                                   (long long)bfactor_work_elems(skb.tau), flags, ctrl);
-    else
-      k_bfactor_lp<<<nslots, LP_THREADS, LP_SMEM, st>>>(src, skb, Ginv, ldgi, gi_stride, work,
+    const int tp = bb_tp(skb.tau);
+    const long long ws = (long long)bfactor_work_elems(skb.tau);
+    k_bf_gather<<<dim3((unsigned)((tp + GA_WARPS - 1) / GA_WARPS), (unsigned)nslots), GA_WARPS * 32,
+                  std::min(GA_SMEM, (size_t)(skb.tau + 1 + skb.len) * 4), st>>>(src, skb, work, ws, ctrl);
+    k_bfactor_lp<<<nslots, LP_THREADS, LP_SMEM, st>>>(src, skb, Ginv, ldgi, gi_stride, work,
                                                         (long long)bfactor_work_elems(skb.tau), flags,
                                                         ctrl);
     return cudaGetLastError();

@@ -375,8 +375,9 @@ def test_csr_primal_gram_bitwise_reproducible(rs):
 @pytest.mark.parametrize("kind,tau,k", [("subsample", 260, 0), ("count", 300, 0), ("subcount", 230, 2)])
 @pytest.mark.parametrize("mode", ["explicit", "gram"])
 def test_dense_large_tau_sketch_ahead(rs, kind, tau, k, mode):
-    """tau > 224: the sketch-ahead pipeline factors G_k in global memory (k_bfactor_big, 32 x 32
-    DMMA tiles, ragged tau padded with an identity tail)."""
+    """tau > 224: the sketch-ahead pipeline gathers G_k into a per-slot work matrix (k_bf_gather) and
+    factors it there (k_bfactor_lp: 32 x 32 DMMA tiles, block-column pairs, ragged tau padded with an
+    identity tail)."""
     n, d = 3000, 700
     X, y = rsinputs.dense_problem(n, d, seed=11)
     X, y = X.numpy(), y.numpy()
@@ -691,10 +692,10 @@ np.savez(sys.argv[2], **out)
 """
 
 
-@pytest.mark.parametrize("env", [{"RS_PDL": "0"}, {"RS_BF_RIGHT": "1"}, {}])
+@pytest.mark.parametrize("env", [{"RS_PDL": "0"}, {}])
 def test_process_switches_parity(tmp_path, env):
-    """The PDL chain off (RS_PDL=0) and the right-looking large-tau factorisation (RS_BF_RIGHT=1)
-    are read once per process: run them in a child and compare with the oracle (tau 300 / 250 > 224
+    """The PDL chain off (RS_PDL=0) is read once per process: run it in a child and compare with the
+    oracle (tau 300 / 250 > 224
     use the W = L^{-1} slots; 12 iterations span three check_every chunks)."""
     import os, subprocess, sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
