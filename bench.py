@@ -362,7 +362,7 @@ def _roofline(args, cfg, world, kms, kl, dom, prof_ms, host, rs):
                         peak_source=dmma_src,
                         algorithmic_per_launch=f"{w:.3e} flop (n tau (tau + 1): lower triangle)")
         elif dom == "factor":
-            slots = kl["update"] / max(kl["factor"], 1)   # iterations (G_k) per group
+            slots = args.steps / max(kl["factor"], 1)   # iterations (G_k) per group
             big = cfg.tau > 224   # k_bfactor_big stores W = L^{-1}; W^T W is applied as two GEMVs
             w = float(cfg.tau) ** 3 * (2.0 / 3.0 if big else 1.0) * slots
             what = ("tau^3/3 Cholesky + tau^3/3 inverse" if big else
@@ -380,14 +380,19 @@ def _roofline(args, cfg, world, kms, kl, dom, prof_ms, host, rs):
                                "k_apply_rows)", bound="hbm",
                         achieved=w / (ms * 1e-3) / 1e9, peak=hbm, unit="GB/s", peak_source=hbm_src,
                         algorithmic_per_launch=f"{w:.3e} bytes (tau^2 x 8: the slot's factor read once)")
-        else:   # explicit: rows of A + GEMV + update
+        else:   # explicit: rows of A + GEMV + update (the group kernel runs a whole group per launch)
             rows_s = cfg.extra.get("rows", cfg.tau)
-            w = (rows_s * cfg.d + 10 * cfg.d) * 8.0
+            its = max(1.0, round(args.steps / max(kl[dom], 1))) if kl.get("solve", 0) == 0 else 1.0
+            w = (rows_s * cfg.d + 10 * cfg.d + (float(cfg.tau) * cfg.tau if its > 1 else 0.0)) * 8.0 * its
             a_mb = cfg.d * cfg.d * 8 / 1e6
-            roof = dict(kernel=f"class {dom}: u = A S delta from the tau sketched rows of A, fused "
-                               "momentum update (k_update_rows)", bound="hbm",
+            roof = dict(kernel=(f"class {dom}: the group's iterations in one persistent kernel "
+                                "(k_iterate: g = S^T r, delta = G^-1 g from the factor slot, u = A S "
+                                "delta from the sketched rows of A, fused momentum update)") if its > 1 else
+                               (f"class {dom}: u = A S delta from the tau sketched rows of A, fused "
+                                "momentum update (k_update_rows)"), bound="hbm",
                         achieved=w / (ms * 1e-3) / 1e9, peak=hbm, unit="GB/s", peak_source=hbm_src,
-                        algorithmic_per_launch=f"{w:.3e} bytes ({rows_s} sketched rows of A x m x 8 + 10 m-vectors)",
+                        algorithmic_per_launch=f"{w:.3e} bytes ({rows_s} sketched rows of A x m x 8 + 10 m-vectors"
+                                               + (f" + the tau^2 slot, x {its:.0f} iterations)" if its > 1 else ")"),
                         note=f"A = {a_mb:.0f} MB ({'fits' if a_mb < 126 else 'exceeds'} the 126 MB L2)")
     else:
         nnz = int(host[0][-1])

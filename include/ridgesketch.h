@@ -39,7 +39,7 @@
 extern "C" {
 #endif
 
-#define RS_ABI_VERSION 2
+#define RS_ABI_VERSION 3
 
 typedef struct rs_problem_t* rs_problem;
 
@@ -89,19 +89,33 @@ typedef enum {
  * producer (or pass its stream in rs_dist) first. */
 typedef enum { RS_MEM_HOST = 0, RS_MEM_DEVICE_COPY = 1, RS_MEM_DEVICE_BORROW = 2 } rs_mem;
 
-/* Process layout (one process per GPU).  NULL means world = 1 on the current device with the
- * whole X.  Primal: X_local holds rows [shard_begin, shard_begin + shard_len) of X.  Dual: X_local
- * holds columns [shard_begin, shard_begin + shard_len) (features).  Sketches are regenerated on
- * every rank from (seed, k); the per-iteration exchange is an NCCL sum-allreduce of the partial
- * A S (IMPLICIT) or of u = R^T R S delta (GRAM, plus one allreduce of a sketch-ahead group's
- * Grams); EXPLICIT iterations need none. */
+/* Collective backend of a multi-rank problem (rs_dist.collective).
+ *   NCCL : ncclAllReduce (sum, fp64) on the solver stream, one process per GPU -- production.
+ *   HOST : host-staged sum over a POSIX shared-memory segment of the world's processes on one
+ *          machine, the ranks' buffers summed in rank order (the same result on every rank); each
+ *          allreduce is a D2H copy, a host function node and an H2D copy on the solver stream (so
+ *          it is captured in the iteration graph like the NCCL call).  No kernel waits on another
+ *          rank, so several ranks may share one GPU: this is how the multi-rank path is executed
+ *          and tested on a single-GPU machine.  A rank waiting more than 300 s for the others
+ *          fails the solve with RS_ENCCL. */
+typedef enum { RS_COLL_NCCL = 0, RS_COLL_HOST = 1 } rs_collective;
+
+/* Process layout (one process per GPU, or, with RS_COLL_HOST, any number of rank processes on one
+ * machine).  NULL means world = 1 on the current device with the whole X.  Primal: X_local holds
+ * rows [shard_begin, shard_begin + shard_len) of X.  Dual: X_local holds columns
+ * [shard_begin, shard_begin + shard_len) (features).  Sketches are regenerated on every rank from
+ * (seed, k); the per-iteration exchange is a sum-allreduce of the partial A S (IMPLICIT) or of
+ * u = R^T R S delta (GRAM, plus one allreduce of a sketch-ahead group's Grams); EXPLICIT iterations
+ * need none. */
 typedef struct {
   int device;                  /* CUDA device ordinal used by this rank                         */
   int rank, world;
-  const void* nccl_unique_id;  /* 128 bytes from rs_nccl_unique_id() on rank 0 (broadcast by the
-                                  caller); ignored when world == 1                               */
+  const void* nccl_unique_id;  /* 128 bytes, the same on every rank, ignored when world == 1:
+                                  NCCL: from rs_nccl_unique_id() on rank 0;
+                                  HOST: from rs_host_coll_id() on rank 0 (a segment name)       */
   void* cuda_stream;           /* cudaStream_t to run on, or NULL for a library-owned stream     */
   int64_t shard_begin, shard_len;
+  int collective;              /* rs_collective (0 = NCCL)                                      */
 } rs_dist;
 
 /* Create a problem from dense X (n x d, row-major, leading dimension ldx >= d) and y (n).
@@ -222,6 +236,8 @@ rs_status rs_shard_rows_nnz(int64_t n_rows, const int64_t* rowptr, int rank, int
                             int64_t* begin, int64_t* len);
 /* Write 128 bytes of NCCL unique id (rank 0 only), loading NCCL on demand. */
 rs_status rs_nccl_unique_id(void* out128);
+/* Write 128 bytes naming a fresh RS_COLL_HOST group (rank 0 only; host only, no GPU needed). */
+rs_status rs_host_coll_id(void* out128);
 
 void rs_destroy(rs_problem p);
 const char* rs_status_string(rs_status s);

@@ -177,3 +177,56 @@ def solve_kernel(X, y, lam, sigma, kind, tau, gamma=1.0, beta=0.0, tol=0.0, max_
     res["weights"] = res["w"]
     res["K"] = sysk["K"]
     return res
+
+
+# ------------------------------------------------------------------ extended precision (x87, 64-bit)
+def cholesky_solve_ld(G, g):
+    """G^{-1} g for SPD G in np.longdouble: the textbook Cholesky G = L L^T (column by column,
+    L_jj = sqrt(G_jj - sum_k L_jk^2), L_ij = (G_ij - sum_k L_ik L_jk) / L_jj, lower triangle read),
+    then L y = g and L^T x = y by substitution (P:L217 least-norm solution = G^{-1} g, DESIGN R3)."""
+    G = np.array(G, dtype=np.longdouble)
+    n = G.shape[0]
+    L = np.zeros((n, n), dtype=np.longdouble)
+    for j in range(n):
+        d = G[j, j] - np.dot(L[j, :j], L[j, :j])
+        if not d > 0:
+            raise np.linalg.LinAlgError("not SPD")
+        L[j, j] = np.sqrt(d)
+        L[j + 1:, j] = (G[j + 1:, j] - L[j + 1:, :j] @ L[j, :j]) / L[j, j]
+    y = np.zeros(n, dtype=np.longdouble)
+    for i in range(n):
+        y[i] = (g[i] - np.dot(L[i, :i], y[:i])) / L[i, i]
+    x = np.zeros(n, dtype=np.longdouble)
+    for i in range(n - 1, -1, -1):
+        x[i] = (y[i] - np.dot(L[i + 1:, i], x[i + 1:])) / L[i, i]
+    return x
+
+
+def solve_system_ld(A, b, kind, tau, gamma=1.0, beta=0.0, iters=10, seed=0, subcount_k=0):
+    """Alg. 2 on an explicit system A w = b carried out in np.longdouble (64-bit
+    significand, eps = 2^-63): the reference that an ill-conditioned fp64 run is compared against.
+    Same sketch stream, same recurrences as solve_momentum; A and b are converted exactly."""
+    A = np.asarray(A, dtype=np.longdouble)
+    b = np.asarray(b, dtype=np.longdouble)
+    m = A.shape[0]
+    w_prev = np.zeros(m, dtype=np.longdouble)
+    w = np.zeros(m, dtype=np.longdouble)
+    r_prev, r = -b.copy(), -b.copy()
+    g_, b_ = np.longdouble(gamma), np.longdouble(beta)
+    for k in range(iters):
+        sk = SK.draw(kind, m, tau, k, seed, subcount_k)
+        S = np.zeros((m, tau), dtype=np.longdouble)
+        S[sk["coord"], sk["bucket"]] = sk["sign"]
+        AS = A @ S
+        G = S.T @ AS
+        g = S.T @ r
+        for bkt in SK.empty_buckets(sk):
+            G[bkt, :] = 0
+            G[:, bkt] = 0
+            G[bkt, bkt] = 1
+            g[bkt] = 0
+        delta = cholesky_solve_ld(G, g)
+        w_next = (1 + b_) * w - b_ * w_prev - g_ * (S @ delta)
+        r_next = (1 + b_) * r - b_ * r_prev - g_ * (AS @ delta)
+        w_prev, w, r_prev, r = w, w_next, r, r_next
+    return dict(w=w, r=r, iterations=iters)

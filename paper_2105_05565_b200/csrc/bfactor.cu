@@ -697,12 +697,19 @@ k_bfactor_lp(FactorSrc src, DevSketch skb, double* __restrict__ Ginv, long long 
   if (slot_unused(ctrl, blockIdx.x)) return;
   BF_T(t_start);
   extern __shared__ __align__(16) double lp_sm[];   // LP_STAGES slice buffers (a4 gather: sketch)
-  __shared__ int s_bad;
+  __shared__ int s_bad, s_stop;
   const int slot = blockIdx.x;
   const DevSketch sk = skb.at(slot);
   const int tau = sk.tau, tp = bb_tp(tau), Tc = tp / 32;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int q = lane >> 2, k4 = lane & 3;
+  // the solve may finish while this group is factored ahead (overlapped pipeline): poll its flag
+  // once per block-column pair, block-uniformly
+  auto stopped = [&]() {
+    if (tid == 0) s_stop = ctrl ? *reinterpret_cast<const volatile int*>(&ctrl->done) : 0;
+    __syncthreads();
+    return s_stop != 0;
+  };
   double* Wm = work + slot * work_stride;           // tp x tp, row-major
   double* dinv = Wm + (long long)tp * tp;           // Tc tiles 32 x 32 (L_pp^{-1})
   double* scr = dinv + (long long)Tc * 1024;        // 2 tiles per warp
@@ -919,6 +926,7 @@ k_bfactor_lp(FactorSrc src, DevSketch skb, double* __restrict__ Ginv, long long 
   // finished from its register accumulator (no C round trip, no panel pass).
   BF_T(t_c0);
   for (int p0 = 0; p0 < Tc; p0 += 2) {
+    if (stopped()) return;
     const int nstrip = Tc - p0, rounds = (nstrip + LP_WARPS - 1) / LP_WARPS;
     for (int rd = 0; rd < rounds; ++rd) {
       int spw, part;
@@ -1023,6 +1031,7 @@ k_bfactor_lp(FactorSrc src, DevSketch skb, double* __restrict__ Ginv, long long 
   }
   // ---- W = L^{-1}, block-column pairs from the last
   for (int J0 = Tc - 2; J0 >= 0; J0 -= 2) {
+    if (stopped()) return;
     const int J1 = J0 + 1, nstrip = Tc - 1 - J1;
     const int rounds = (nstrip + LP_WARPS - 1) / LP_WARPS;
     if (rounds > 0) {
@@ -1168,8 +1177,7 @@ cudaError_t launch_apply_ginv(const double* Ginv, long long ldgi, const DevSketc
                               double* sdelta, Ctrl* ctrl, cudaStream_t st, bool first,
                               const double* pfA, long long pf_lda, long long pf_m) {
   // L2 prefetch of the sketched rows of A only while they fit comfortably in the 126 MB L2
-  static const bool no_pf = std::getenv("RS_NO_L2PF") != nullptr;
-  if (no_pf || !pfA || (double)sk.len * pf_m * 8.0 > 48e6) pfA = nullptr;
+  if (!pfA || (double)sk.len * pf_m * 8.0 > 48e6) pfA = nullptr;
   const unsigned pf_bytes = (unsigned)(((pf_m * 8) + 15) / 16 * 16);
   if (sk.tau > AG_MAXTAU) return cudaErrorInvalidValue;
   // few entries per bucket (subsample, SubCount): g = S^T r is formed inside the first GEMV kernel

@@ -836,7 +836,7 @@ rs_status Problem::csr_gram_workspace(int kind, int tau) {
   c->gb_cap = (int)round_up(maxband, 2);
   // staged light rows pay on long rows (c3: 50 entries, Gram 2.06 -> 1.85 ms); on short Zipf rows
   // (c4: 10) the unstaged loop is 2 % faster
-  c->gb_stage = std::getenv("RS_GB_NOSTAGE") == nullptr && c->nnz >= 32 * std::max(1LL, R.rows) &&
+  c->gb_stage = c->nnz >= 32 * std::max(1LL, R.rows) &&
                 (size_t)c->gb_cap * 8 + GB_STAGE_BYTES <= 227 * 1024;
   if (c->gb_stage) c->gb_smem = (size_t)c->gb_cap * 8 + GB_STAGE_BYTES;
   RS_CUDA(cudaFuncSetAttribute(k_gram_bands<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -890,8 +890,7 @@ rs_status Problem::csr_gram_into(const DevSketch& s, double* G, cudaEvent_t* ev,
   } else if (R.rows > 0) {   // a2: rows of R S, merged and bucket-sorted
     const unsigned grid = (unsigned)std::max<long long>(
         1, std::min<long long>((R.rows + HR_WARPS - 1) / HR_WARPS, (long long)num_sms * 8));
-    static const bool no_hpf = std::getenv("RS_HR_NOPF") != nullptr;
-    (s.kind == SK_COUNT && !no_hpf ? k_hash_rows<true> : k_hash_rows<false>)
+    (s.kind == SK_COUNT ? k_hash_rows<true> : k_hash_rows<false>)
         <<<grid, HR_WARPS * 32, c->hr_smem, st>>>(R.ptr, R.idx, R.val, R.rows, c->heavyR, cmap, tau,
                                                   c->hb, c->hv, c->hcnt, slot, ctrl, c->gtrace);
     if (c->nheavyR > 0)

@@ -9,6 +9,8 @@
 //      FP64 tensor path and measures 37.1 TFLOP/s on this B200 (profiles/r01_fp64_peak.txt).
 //  explicit A = X^T X + lambda I is the same TN contraction with Bop = X, built once.
 //  explicit a2: AS^T[b,:] = sum_{e in b} sign_e A[coord_e, :] (A symmetric, rows are columns).
+#include <algorithm>
+
 #include "rs_internal.cuh"
 
 namespace rs {
@@ -325,6 +327,22 @@ cudaError_t launch_explicit_rows_batch(const double* A, long long lda, long long
 cudaError_t launch_add_lambda_s(double lambda, const DevSketch& sk, double* ASt, long long ld_as,
                                 bool as_rowmajor, const Ctrl* ctrl, cudaStream_t st) {
   k_add_lambda_s<<<(sk.len + 255) / 256, 256, 0, st>>>(lambda, sk, ASt, ld_as, as_rowmajor, ctrl);
+  return cudaGetLastError();
+}
+
+namespace {
+__global__ void k_add_lower(double* __restrict__ A, const double* __restrict__ T, long long lda,
+                            long long m) {
+  const long long r = blockIdx.y;
+  for (long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x; c <= r && c < m;
+       c += (long long)gridDim.x * blockDim.x)
+    A[r * lda + c] += T[r * lda + c];
+}
+}  // namespace
+
+cudaError_t launch_add_lower(double* A, const double* T, long long lda, long long m, cudaStream_t st) {
+  if (m <= 0) return cudaSuccess;
+  k_add_lower<<<dim3((unsigned)std::min<long long>((m + 255) / 256, 16), (unsigned)m), 256, 0, st>>>(A, T, lda, m);
   return cudaGetLastError();
 }
 

@@ -34,7 +34,6 @@ Problem::~Problem() {
   if (st) cudaStreamSynchronize(st);
   free_workspace();
   dfree(XT);
-  dfree(kbase_dev);
   if (st2) cudaStreamDestroy(st2);
   if (ev_fork) cudaEventDestroy(ev_fork);
   if (ev_join) cudaEventDestroy(ev_join);
@@ -57,6 +56,7 @@ Problem::~Problem() {
     std::string err;
     if (const NcclApi* api = nccl_api(&err)) api->ncclCommDestroy(comm);
   }
+  hostcoll_destroy(hcoll);
   if (own_stream && st) cudaStreamDestroy(st);
 }
 
@@ -104,8 +104,9 @@ void Problem::free_workspace() {
   slot_flags = nullptr;
   dfree(bf_work);
   bf_work = nullptr;
-  dfree(gf_part);
-  gf_part = nullptr;
+  dfree(it_scratch);
+  it_scratch = nullptr;
+  use_iterate = false;
   pipe_xg = false;
   ws_xg = -1;
   pipe = false;
@@ -119,6 +120,11 @@ void Problem::free_workspace() {
 
 rs_status Problem::allreduce(double* buf, size_t count) {
   if (world <= 1) return RS_OK;
+  if (coll == RS_COLL_HOST) {
+    if (!hcoll) return fail(RS_ENCCL, "host collective not attached");
+    RS_CUDA(hostcoll_allreduce(hcoll, buf, count, st));
+    return RS_OK;
+  }
   std::string err;
   const NcclApi* api = nccl_api(&err);
   if (!api) return fail(RS_ENCCL, err);
@@ -149,6 +155,7 @@ rs_status setup_common(Problem* p, const rs_dist* dist) {
   RS_CUDA(gram_init());
   RS_CUDA(bfactor_init());
   RS_CUDA(update_init());
+  RS_CUDA(iterate_init());
   if (dist && dist->cuda_stream) {
     p->st = static_cast<cudaStream_t>(dist->cuda_stream);
     p->own_stream = false;
@@ -158,7 +165,15 @@ rs_status setup_common(Problem* p, const rs_dist* dist) {
   }
   p->rank = dist ? dist->rank : 0;
   p->world = dist ? dist->world : 1;
-  if (p->world > 1) {
+  p->coll = dist ? dist->collective : RS_COLL_NCCL;
+  if (p->world > 1 && p->coll == RS_COLL_HOST) {
+    char name[129];
+    std::memcpy(name, dist->nccl_unique_id, 128);
+    name[128] = 0;
+    std::string err;
+    p->hcoll = hostcoll_create(name, p->rank, p->world, &err);
+    if (!p->hcoll) return fail(RS_ENCCL, "host collective: " + err);
+  } else if (p->world > 1) {
     std::string err;
     const NcclApi* api = nccl_api(&err);
     if (!api) return fail(RS_ENCCL, err);
@@ -180,7 +195,9 @@ rs_status validate_dist(const rs_dist* dist, long long total) {
   if (dist->world < 1 || dist->rank < 0 || dist->rank >= dist->world)
     return fail(RS_EINVAL, "rs_dist: need 0 <= rank < world");
   if (dist->world > 1 && !dist->nccl_unique_id)
-    return fail(RS_EINVAL, "rs_dist: world > 1 needs nccl_unique_id");
+    return fail(RS_EINVAL, "rs_dist: world > 1 needs nccl_unique_id (the group id)");
+  if (dist->collective != RS_COLL_NCCL && dist->collective != RS_COLL_HOST)
+    return fail(RS_EINVAL, "rs_dist: bad collective");
   if (dist->shard_begin < 0 || dist->shard_len < 0 || dist->shard_begin + dist->shard_len > total)
     return fail(RS_EINVAL, "rs_dist: shard out of range");
   if (dist->world == 1 && (dist->shard_begin != 0 || dist->shard_len != total))
@@ -247,6 +264,11 @@ static rs_status create_dense(rs_problem* out, int64_t n, int64_t d, const doubl
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
+  // Host X for an EXPLICIT primal build of >= 2 GB: streamed in row chunks on a copy stream while
+  // A = sum_c X_c^T X_c accumulates chunk by chunk on the solver stream (the H2D copy, not the
+  // DMMA contraction, bounds rs_create then; c5: 65.5 GB).  setup_seconds covers both.
+  const bool streamed = mem == RS_MEM_HOST && mode == RS_AS_EXPLICIT && rt == 1 && rows > 0 &&
+                        (double)rows * (double)d * 8.0 >= 2e9;
   // X: library copy with ld a multiple of 4 doubles (16-byte cp.async rows), unless borrowable
   if (mem == RS_MEM_DEVICE_BORROW && ldx % 4 == 0) {
     p->X = const_cast<double*>(X_local);
@@ -257,7 +279,7 @@ static rs_status create_dense(rs_problem* out, int64_t n, int64_t d, const doubl
     s = dalloc(&p->X, (size_t)std::max<long long>(rows, 1) * p->ldx);
     if (s != RS_OK) return guard(s);
     p->own_X = true;
-    if (rows > 0) {
+    if (rows > 0 && !streamed) {
       cudaError_t ce = cudaMemcpy2DAsync(p->X, p->ldx * 8, X_local, ldx * 8, d * 8, rows,
                                          kind_of(mem), p->st);
       if (ce != cudaSuccess) return guard(fail(RS_ECUDA, std::string("copy X: ") + cudaGetErrorString(ce)));
@@ -269,13 +291,62 @@ static rs_status create_dense(rs_problem* out, int64_t n, int64_t d, const doubl
     cudaError_t ce = cudaMemcpyAsync(p->y, y, rows * 8, kind_of(mem), p->st);
     if (ce != cudaSuccess) return guard(fail(RS_ECUDA, std::string("copy y: ") + cudaGetErrorString(ce)));
   }
+  // streamed EXPLICIT build: chunk c's H2D (copy stream) overlaps chunk c-1's lower-tile DMMA
+  // contraction (solver stream); the finiteness count runs on each chunk as it lands
+  unsigned long long* cnt = nullptr;
+  s = dalloc(&cnt, 1);
+  if (s != RS_OK) return guard(s);
+  cudaMemsetAsync(cnt, 0, 8, p->st);
+  if (streamed) {
+    p->lda = round_up(d, 4);
+    s = dalloc(&p->A, (size_t)d * p->lda);
+    double* tacc = nullptr;
+    if (s == RS_OK) s = dalloc(&tacc, (size_t)d * p->lda);
+    if (s != RS_OK) return guard(s);
+    const int nch = (int)std::max<double>(2.0, std::ceil((double)rows * d * 8.0 / 4e9));
+    const long long rc = (rows + nch - 1) / nch;
+    std::vector<TmaGemm> plans;
+    size_t wmax = 0;
+    for (long long r0 = 0; r0 < rows; r0 += rc) {
+      TmaGemm tgc{};
+      const double* Xc = p->X + r0 * p->ldx;
+      cudaError_t ce = tma_gemm_plan(&tgc, Xc, p->ldx, Xc, p->ldx, d, d, std::min(rc, rows - r0), p->num_sms);
+      if (ce != cudaSuccess) return guard(fail(RS_ECUDA, std::string("A build plan: ") + cudaGetErrorString(ce)));
+      tgc.lower = 1;
+      wmax = std::max(wmax, tgc.work_elems);
+      plans.push_back(tgc);
+    }
+    double* swork = nullptr;
+    if (wmax) s = dalloc(&swork, wmax);
+    if (s != RS_OK) return guard(s);
+    cudaStream_t cs = nullptr;
+    RS_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+    std::vector<cudaEvent_t> landed(plans.size());
+    for (auto& ev : landed) cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+    cudaEventRecord(e0, p->st);
+    RS_CUDA(cudaStreamWaitEvent(cs, e0, 0));   // y copied, counters cleared
+    cudaError_t ce = cudaSuccess;
+    for (size_t c = 0; c < plans.size() && ce == cudaSuccess; ++c) {
+      const long long r0 = (long long)c * rc, nr = std::min(rc, rows - r0);
+      ce = cudaMemcpy2DAsync(p->X + r0 * p->ldx, p->ldx * 8, X_local + r0 * ldx, ldx * 8, d * 8, nr,
+                             cudaMemcpyHostToDevice, cs);
+      if (ce == cudaSuccess) ce = cudaEventRecord(landed[c], cs);
+      if (ce == cudaSuccess) ce = cudaStreamWaitEvent(p->st, landed[c], 0);
+      if (ce == cudaSuccess) ce = launch_count_nonfinite(p->X + r0 * p->ldx, p->ldx, nr, d, cnt, p->st);
+      if (ce == cudaSuccess) ce = tma_gemm_launch(plans[c], c == 0 ? p->A : tacc, p->lda, swork, nullptr, p->st);
+      if (ce == cudaSuccess && c > 0) ce = launch_add_lower(p->A, tacc, p->lda, d, p->st);
+    }
+    cudaError_t ce2 = cudaStreamSynchronize(p->st);
+    for (auto& ev : landed) cudaEventDestroy(ev);
+    cudaStreamDestroy(cs);
+    dfree(swork);
+    dfree(tacc);
+    if (ce == cudaSuccess) ce = ce2;
+    if (ce != cudaSuccess) return guard(fail(RS_ECUDA, std::string("streamed A build: ") + cudaGetErrorString(ce)));
+  }
   // finiteness check of the local data
   {
-    unsigned long long* cnt = nullptr;
-    s = dalloc(&cnt, 1);
-    if (s != RS_OK) return guard(s);
-    cudaMemsetAsync(cnt, 0, 8, p->st);
-    launch_count_nonfinite(p->X, p->ldx, rows, d, cnt, p->st);
+    if (!streamed) launch_count_nonfinite(p->X, p->ldx, rows, d, cnt, p->st);
     launch_count_nonfinite(p->y, 1, rows, 1, cnt, p->st);
     unsigned long long h = 0;
     cudaMemcpyAsync(&h, cnt, 8, cudaMemcpyDeviceToHost, p->st);
@@ -297,7 +368,6 @@ static rs_status create_dense(rs_problem* out, int64_t n, int64_t d, const doubl
   double* a_work = nullptr;
   TmaGemm tg{};
   GemmPlan gp{};
-  const bool a_cpasync = rows > 0 && std::getenv("RS_A_BUILD_CPASYNC");   // comparison path
   cudaError_t ce = cudaSuccess;
   if (mode == RS_AS_EXPLICIT && rt == 2) {
     p->lda = round_up(n, 4);
@@ -311,14 +381,11 @@ static rs_status create_dense(rs_problem* out, int64_t n, int64_t d, const doubl
     if (ce == cudaSuccess && tg.work_elems) s = dalloc(&a_work, tg.work_elems);
     if (s != RS_OK) return guard(s);
     if (ce != cudaSuccess) return guard(fail(RS_ECUDA, std::string("A build: ") + cudaGetErrorString(ce)));
-  } else if (mode == RS_AS_EXPLICIT) {
+  } else if (mode == RS_AS_EXPLICIT && !streamed) {
     p->lda = round_up(d, 4);
     s = dalloc(&p->A, (size_t)d * p->lda);
     if (s != RS_OK) return guard(s);
-    if (a_cpasync) {
-      gp = plan_tn_gemm(d, d, rows, p->num_sms);
-      if (gp.work_elems) s = dalloc(&a_work, gp.work_elems);
-    } else if (rows > 0) {
+    if (rows > 0) {
       ce = tma_gemm_plan(&tg, p->X, p->ldx, p->X, p->ldx, d, d, rows, p->num_sms);
       if (std::getenv("RS_VERBOSE"))
         fprintf(stderr, "[rs] A build: TMA variant %d (%dx%d), splits %d\n", tg.variant, tg.bm, tg.bn, tg.splits);
@@ -328,7 +395,7 @@ static rs_status create_dense(rs_problem* out, int64_t n, int64_t d, const doubl
     if (s != RS_OK) return guard(s);
     if (ce != cudaSuccess) return guard(fail(RS_ECUDA, std::string("A build: ") + cudaGetErrorString(ce)));
   }
-  cudaEventRecord(e0, p->st);
+  if (!streamed) cudaEventRecord(e0, p->st);   // (streamed: recorded before the first chunk)
   if (rt == 2) {   // dual: b = y, A = X X^T + lambda I on the lower DMMA tiles of X^T
     ce = cudaMemcpyAsync(p->b, p->y, n * 8, cudaMemcpyDeviceToDevice, p->st);
     if (ce == cudaSuccess) ce = launch_transpose(p->X, p->ldx, n, d, xt, ldt, p->st);
@@ -346,8 +413,8 @@ static rs_status create_dense(rs_problem* out, int64_t n, int64_t d, const doubl
   if (mode == RS_AS_EXPLICIT && rt == 1) {  // A = X^T X + lambda I, built once (DSYRK-shaped DMMA contraction)
     // lower-triangle tiles only on the TMA/DMMA contraction (d^2 n flop instead of 2 d^2 n), then
     // the upper triangle mirrored: A is symmetric
-    if (a_cpasync) {
-      ce = launch_tn_gemm(p->X, p->ldx, p->X, p->ldx, d, d, rows, p->A, p->lda, gp, a_work, nullptr, p->st);
+    if (streamed) {   // the chunks' lower tiles are summed already
+      ce = launch_mirror_lower(p->A, p->lda, d, p->st);
     } else if (rows > 0) {
       ce = tma_gemm_launch(tg, p->A, p->lda, a_work, nullptr, p->st);
       if (ce == cudaSuccess) ce = launch_mirror_lower(p->A, p->lda, d, p->st);
@@ -416,7 +483,7 @@ static bool pipeline_applies(const Problem* p, int tau) {
                       (p->mode == RS_AS_EXPLICIT || p->mode == RS_AS_GRAM)) ||
                      p->mode == RS_AS_EXPLICIT;   // CSR explicit: dense A built in rs_create_csr
   const bool csr = p->fmt == 1 && p->mode == RS_AS_GRAM;
-  return (dense || csr) && tau <= bfactor_max_tau() && !std::getenv("RS_NO_PIPE");
+  return (dense || csr) && tau <= bfactor_max_tau();
 }
 
 rs_status Problem::ensure_workspace(int kind, int tau, int ksum, int depth, bool xg) {
@@ -450,8 +517,8 @@ rs_status Problem::ensure_workspace(int kind, int tau, int ksum, int depth, bool
     RS_TRY(dalloc(&Gram, (size_t)tau * ld_gram));
     RS_TRY(dalloc(&xp_part, std::max(xpass_partials(m, num_sms), gram_fused_partials(num_sms))));
     RS_TRY(dalloc(&uvec, m));
-    gram_fused = gram_fused_ok(kind, tau) && !std::getenv("RS_NO_GRAM_FUSED");
-    if (gram_fused && rows_loc > 0 && !XT && !std::getenv("RS_NO_XT")) {
+    gram_fused = gram_fused_ok(kind, tau);
+    if (gram_fused && rows_loc > 0 && !XT) {
       // the Gram reads the tau sketched columns as contiguous rows of X^T: built once per
       // problem when it fits next to X (2 GiB margin)
       const long long ldt = round_up(rows_loc, 64);   // zero padding >= one 32-row K chunk
@@ -479,7 +546,7 @@ rs_status Problem::ensure_workspace(int kind, int tau, int ksum, int depth, bool
   if (fmt == 0 && mode == RS_AS_IMPLICIT) {
     ld_xs = round_up(tau, 4);
     RS_TRY(dalloc(&XS, (size_t)std::max<long long>(rows_loc, 1) * ld_xs));
-    use_tma = !std::getenv("RS_NO_TMA") && rows_loc > 0;
+    use_tma = rows_loc > 0;   // an empty shard contributes zeros through the cp.async GEMM
     if (use_tma) {
       RS_CUDA(tma_gemm_plan(&tg, XS, ld_xs, X, ldx, tau, m, rows_loc, num_sms));
       if (tg.work_elems) RS_TRY(dalloc(&gemm_work, tg.work_elems));
@@ -497,10 +564,7 @@ rs_status Problem::ensure_workspace(int kind, int tau, int ksum, int depth, bool
     pipe = true;
     pipe_xg = xg;
     P = depth;
-    if (xg) {
-      depth *= 2;
-      RS_TRY(dalloc(&gf_part, gram_fused_partials(num_sms)));
-    }
+    if (xg) depth *= 2;
     skb = sk;   // same geometry, `depth` slots
     skb.coord = nullptr; skb.sign = nullptr; skb.bucket = nullptr; skb.bptr = nullptr; skb.cmap = nullptr;
     RS_TRY(dalloc(&skb.coord, L * depth));
@@ -525,6 +589,9 @@ rs_status Problem::ensure_workspace(int kind, int tau, int ksum, int depth, bool
     RS_TRY(dalloc(&Ginv_slots, (size_t)gi_stride * depth));
     RS_TRY(dalloc(&slot_flags, depth));
     if (bfactor_work_elems(tau)) RS_TRY(dalloc(&bf_work, bfactor_work_elems(tau) * depth));
+    // EXPLICIT: the group's iterations as one persistent kernel (iterate.cu)
+    use_iterate = mode == RS_AS_EXPLICIT && iterate_ok(sk, m, xg ? OV_SMS : num_sms);
+    if (use_iterate) RS_TRY(dalloc(&it_scratch, 2 * (size_t)tau + num_sms));
   }
   sw = plan_solve(tau, num_sms);
   RS_TRY(dalloc(&sw.Gx, solve_gx_elems(tau)));
@@ -712,99 +779,74 @@ rs_status Problem::enqueue_pipelined_iteration(const rs_solve_opts* o, int slot,
   return RS_OK;
 }
 
-// One group of P iterations of the fused pipeline on slot set g (g = 0, 1): draw the sketches of
-// the other set (iterations k0 + P .. k0 + 2P - 1), run the P iterations -- each X pass also forms
-// the Gram of the other set's slot q -- then factor the other set.
-rs_status Problem::enqueue_group_xg(const rs_solve_opts* o, int g, cudaEvent_t* ev) {
-  auto mark = [&](int q, int cls, int edge) {
-    if (ev) cudaEventRecordWithFlags(ev[(size_t)q * 2 * RS_K_NCLASSES + 2 * cls + edge], st,
-                                     cudaEventRecordExternal);
-  };
-  const int cur = g, nxt = 1 - g;
-  const DevSketch sc = skb.at(cur * P), sn = skb.at(nxt * P);
-  mark(0, RS_K_PRE, 0);
-  RS_CUDA(launch_sketch_batch(sn, P, o->seed, ctrl, -1, st, P));                  // a1 x P (ahead)
-  mark(0, RS_K_PRE, 1);
-  for (int q = 0; q < P; ++q) {
-    const long long cs = (long long)cur * P + q, ns = (long long)nxt * P + q;
-    mark(q, RS_K_SOLVE, 0);
-    RS_CUDA(launch_apply_ginv(Ginv_slots + cs * gi_stride, ld_gi, sc.at(q), slot_flags + cs, r, sw.Gx,
-                              sw.delta, sdelta, ctrl, st));                       // a4 + a5
-    mark(q, RS_K_SOLVE, 1);
-    mark(q, RS_K_AS, 0);
-    double* Gq = Gram_slots + ns * gram_stride;
-    RS_CUDA(launch_xpass_gram(X, ldx, rows_loc, m, sdelta, xp_part, uvec, sn.at(q), gf_part, Gq,
-                              ld_gram, num_sms, ctrl, st, P));    // X^T X S delta + Gram ahead
-    RS_TRY(allreduce(uvec, (size_t)m));
-    RS_TRY(allreduce(Gq, (size_t)gram_stride));
-    mark(q, RS_K_AS, 1);
-    mark(q, RS_K_UPDATE, 0);
-    RS_CUDA(launch_update_vec(uvec, lambda, sdelta, w, dw, r, dr, m, o->gamma, o->beta, partials,
-                              ctrl, st));                                          // a6 + a7
-    mark(q, RS_K_UPDATE, 1);
-  }
-  FactorSrc src{};
-  src.Gram = Gram_slots + (long long)nxt * P * gram_stride;
-  src.ld_gram = ld_gram;
-  src.gram_stride = gram_stride;
-  src.lambda = lambda;
-  mark(0, RS_K_FACTOR, 0);
-  RS_CUDA(launch_bfactor(src, sn, P, Ginv_slots + (long long)nxt * P * gi_stride, ld_gi, gi_stride,
-                         slot_flags + (long long)nxt * P, bf_work, ctrl, st));   // a4 + a5 ahead
-  mark(0, RS_K_FACTOR, 1);
+// The ns iterations of a precomputed EXPLICIT group as one persistent cooperative kernel.
+rs_status Problem::enqueue_iterate_group(const rs_solve_opts* o, int ns, cudaEvent_t* ev, int slot0,
+                                         int grid) {
+  if (ev) cudaEventRecordWithFlags(ev[2 * RS_K_UPDATE], st, cudaEventRecordExternal);
+  IterArgs ia{};
+  ia.Ginv = Ginv_slots + (long long)slot0 * gi_stride;
+  ia.ld_gi = ld_gi;
+  ia.gi_stride = gi_stride;
+  ia.skb = skb.at(slot0);
+  ia.flags = slot_flags + slot0;
+  ia.A = A;
+  ia.lda = lda;
+  ia.ASt = ASt_slots ? ASt_slots + (long long)slot0 * as_stride : nullptr;
+  ia.ld_as = ld_as;
+  ia.as_stride = as_stride;
+  ia.m = m;
+  ia.w = w;
+  ia.dw = dw;
+  ia.r = r;
+  ia.dr = dr;
+  ia.sdelta = sdelta;
+  ia.tvec = it_scratch;
+  ia.dvec = it_scratch + skb.tau;
+  ia.partials = it_scratch + 2 * (long long)skb.tau;
+  ia.gamma = o->gamma;
+  ia.beta = o->beta;
+  ia.nslots = ns;
+  ia.big = skb.tau > 224;
+  RS_CUDA(launch_iterate(ia, grid > 0 ? grid : num_sms, ctrl, st));
+  if (ev) cudaEventRecordWithFlags(ev[2 * RS_K_UPDATE + 1], st, cudaEventRecordExternal);
   return RS_OK;
 }
 
-// Concurrent group (dense GRAM with X^T, one rank): the Grams of the other slot set (the next
-// group's iterations, drawn here first) run on st2 -- lean k_gram_xt, 8 warps / ~96 KB -- while the
-// P iterations run on st with the lean X pass (2 consumer warps / ~96 KB), so an SM holds one CTA
-// of each: the DMMA-bound Gram overlaps the HBM-bound X stream.  The Grams read the group's base
-// iteration from a snapshot (ctrl->k advances under them).  Then the other set is factored.
-rs_status Problem::enqueue_group_xc(const rs_solve_opts* o, int g, cudaEvent_t* ev) {
-  auto mark = [&](int q, int cls, int edge) {
-    if (ev) cudaEventRecordWithFlags(ev[(size_t)q * 2 * RS_K_NCLASSES + 2 * cls + edge], st,
+// One group of an overlapped EXPLICIT pipeline (tau > 224) on slot set g: the sketches of the next
+// group (set 1 - g, iterations k0 + P ..) are drawn first; then, concurrently, st2 gathers and
+// factors them (k_bf_gather + k_bfactor_lp on P = num_sms - OV_SMS CTAs) while st runs this group's
+// P iterations (k_iterate on the OV_SMS SMs left free).  The factorisation kernels read ctrl->k only
+// to skip slots beyond max_iter; the concurrent iterations can only make that test skip fewer slots.
+rs_status Problem::enqueue_group_ov(const rs_solve_opts* o, int g, cudaEvent_t* ev) {
+  auto mark = [&](cudaStream_t s, int q, int cls, int edge) {
+    if (ev) cudaEventRecordWithFlags(ev[(size_t)q * 2 * RS_K_NCLASSES + 2 * cls + edge], s,
                                      cudaEventRecordExternal);
   };
   const int cur = g, nxt = 1 - g;
-  const DevSketch sc = skb.at(cur * P), sn = skb.at(nxt * P);
-  mark(0, RS_K_PRE, 0);
-  RS_CUDA(launch_sketch_batch(sn, P, o->seed, ctrl, -1, st, P));                  // a1 x P (ahead)
-  RS_CUDA(launch_snap_k(ctrl, kbase_dev, st));
-  mark(0, RS_K_PRE, 1);
+  const DevSketch sn = skb.at(nxt * P);
+  mark(st, 0, RS_K_PRE, 0);
+  RS_CUDA(launch_sketch_batch(sn, P, o->seed, ctrl, -1, st, P));   // a1 x P (next group)
+  mark(st, 0, RS_K_PRE, 1);
   RS_CUDA(cudaEventRecord(ev_fork, st));
   RS_CUDA(cudaStreamWaitEvent(st2, ev_fork, 0));
-  for (int q = 0; q < P; ++q) {                                                   // st2: Grams ahead
-    const long long ns = (long long)nxt * P + q;
-    RS_CUDA(launch_gram_xt(XT, ldxt, rows_loc, sn.at(q), gf_part, Gram_slots + ns * gram_stride,
-                           ld_gram, num_sms, ctrl, st2, P + q, kbase_dev, true));
-  }
-  RS_CUDA(cudaEventRecord(ev_join, st2));
-  for (int q = 0; q < P; ++q) {                                                   // st: iterations
-    const long long cs = (long long)cur * P + q;
-    const DevSketch sq = sc.at(q);
-    mark(q, RS_K_SOLVE, 0);
-    RS_CUDA(launch_apply_ginv(Ginv_slots + cs * gi_stride, ld_gi, sq, slot_flags + cs, r, sw.Gx,
-                              sw.delta, sdelta, ctrl, st));                       // a4 + a5
-    mark(q, RS_K_SOLVE, 1);
-    mark(q, RS_K_AS, 0);
-    RS_CUDA(launch_xpass(X, ldx, rows_loc, m, sdelta, xp_part, uvec, num_sms, ctrl, st, &sq,
-                         sw.delta, true));                                        // X^T X S delta
-    mark(q, RS_K_AS, 1);
-    mark(q, RS_K_UPDATE, 0);
-    RS_CUDA(launch_update_vec(uvec, lambda, sdelta, w, dw, r, dr, m, o->gamma, o->beta, partials,
-                              ctrl, st));                                          // a6 + a7
-    mark(q, RS_K_UPDATE, 1);
-  }
-  RS_CUDA(cudaStreamWaitEvent(st, ev_join, 0));
   FactorSrc src{};
-  src.Gram = Gram_slots + (long long)nxt * P * gram_stride;
-  src.ld_gram = ld_gram;
-  src.gram_stride = gram_stride;
-  src.lambda = lambda;
-  mark(0, RS_K_FACTOR, 0);
+  mark(st2, 0, RS_K_FACTOR, 0);
+  if (ASt_slots) {   // count: the slots' rows of A S^T
+    double* as_n = ASt_slots + (long long)nxt * P * as_stride;
+    RS_CUDA(launch_explicit_rows_batch(A, lda, m, sn, P, as_n, ld_as, as_stride, ctrl, st2));
+    src.ASt = as_n;
+    src.ld_as = ld_as;
+    src.as_stride = as_stride;
+  } else {
+    src.A = A;
+    src.lda = lda;
+  }
   RS_CUDA(launch_bfactor(src, sn, P, Ginv_slots + (long long)nxt * P * gi_stride, ld_gi, gi_stride,
-                         slot_flags + (long long)nxt * P, bf_work, ctrl, st));   // a4 + a5 ahead
-  mark(0, RS_K_FACTOR, 1);
+                         slot_flags + (long long)nxt * P, bf_work, ctrl, st2));   // a4 + a5 ahead
+  mark(st2, 0, RS_K_FACTOR, 1);
+  RS_CUDA(cudaEventRecord(ev_join, st2));
+  RS_TRY(enqueue_iterate_group(o, P, ev, cur * P, OV_SMS));                       // a4-a7 x P
+  RS_CUDA(cudaStreamWaitEvent(st, ev_join, 0));
   return RS_OK;
 }
 
@@ -813,6 +855,7 @@ static int status_of(int st) {
     case ST_DIVERGED: return RS_EDIVERGED;
     case ST_NOTSPD: return RS_ENOTSPD;
     case ST_OVERFLOW: return RS_EUNSUPPORTED;
+    case ST_SKETCHFAIL: return RS_EUNSUPPORTED;
     default: return RS_OK;
   }
 }
@@ -861,18 +904,19 @@ rs_status Problem::solve(const rs_solve_opts* o, double* w_out, rs_mem w_mem, do
   // iterations per CUDA-graph launch (between host reads of the stop flag)
   int chunk = (int)(o->check_every > 0 ? std::min<long long>(o->check_every, 1024)
                                        : (want_pipe ? (o->tau > 224 ? num_sms : 64) : 16));
-  // fused X pass + Gram ahead (k_xpass_gram1, opt-in RS_XG=1: on c2 it measures 0.69 ms per
-  // iteration vs 0.65 ms for the separate k_xpass_tma + k_gram_fused, profiles/README.md)
-  const bool want_xg0 = want_pipe && fmt == 0 && mode == RS_AS_GRAM && rows_loc > 0 &&
-                        xpass_gram_ok((int)o->kind, (int)o->tau, d, ldx) && std::getenv("RS_XG");
-  // concurrent Gram / X-pass groups (opt-in RS_XC=1): dense GRAM, subsample tau <= 200 (X^T
-  // Gram), d <= 2048 (lean row-owner X pass), one rank.  On c2 it measures 0.85 ms per iteration
-  // against 0.44 ms sequential: with one CTA of each kernel per SM the register file leaves the X
-  // pass 2 consumer warps, which cannot keep up with the HBM stream
-  const bool want_xc = want_pipe && !want_xg0 && fmt == 0 && mode == RS_AS_GRAM && rows_loc > 0 &&
-                       world == 1 && gram_fused_ok((int)o->kind, (int)o->tau) && d <= 2048 &&
-                       ldx * 8 <= 32768 && !std::getenv("RS_NO_XT") && std::getenv("RS_XC");
-  const bool want_xg = want_xg0 || want_xc;
+  // EXPLICIT with tau > 224: overlap the next group's factorisation with the current group's
+  // iterations when the factorisation is the longer of the two.  Estimates per iteration: the
+  // factor's 2 tau^3 / 3 flop at ~15 TFLOP/s (measured, ~0.4 of the DMMA peak) against the group
+  // kernel's sketched rows of A (len m 8 bytes) on OV_SMS SMs at ~45 GB/s each plus ~15 us of
+  // barriers (profiles/README.md, k_iterate phases)
+  const double tau_d = (double)o->tau;
+  const double len_d = (double)sketch_max_len((int)o->kind, (int)m, (int)o->tau, ksum);
+  const double est_factor_us = 2.0 * tau_d * tau_d * tau_d / 3.0 / 15e6;
+  const double est_iter_us = len_d * (double)m * 8.0 / (OV_SMS * 45e3) + 15.0;
+  const bool want_ov = want_pipe && mode == RS_AS_EXPLICIT && o->tau > 224 && num_sms > 2 * OV_SMS &&
+                       len_d <= 8192 && est_factor_us > est_iter_us;
+  if (want_ov) chunk = 2 * (num_sms - OV_SMS);
+  const bool want_xg = want_ov;   // two slot sets
   if (want_xg) chunk = std::max(2, chunk & ~1);   // two groups of P = chunk / 2
   int depth = 0;
   if (want_pipe) {   // one batched factorisation wave: <= num_sms slots, <= ~6 GB of slots
@@ -883,17 +927,16 @@ rs_status Problem::solve(const rs_solve_opts* o, double* w_out, rs_mem w_mem, do
     depth = (int)std::max<long long>(1, std::min<long long>({(long long)chunk, (long long)num_sms,
                                                              6000000000LL / slot_bytes}));
     if (want_xg) {
-      depth = std::min(depth, chunk / 2);
+      depth = std::min<long long>({(long long)depth, (long long)chunk / 2, 3000000000LL / slot_bytes});
       chunk = 2 * depth;
     }
   }
   RS_TRY(ensure_workspace((int)o->kind, (int)o->tau, ksum, depth, want_xg));
-  pipe_xc = want_xc && pipe_xg && XT != nullptr;
-  if (pipe_xc && !st2) {
+  pipe_ov = want_ov && pipe_xg;
+  if (pipe_ov && !st2) {
     RS_CUDA(cudaStreamCreateWithFlags(&st2, cudaStreamNonBlocking));
     RS_CUDA(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
     RS_CUDA(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming));
-    RS_TRY(dalloc(&kbase_dev, 1));
   }
   // state: w^{-1} = w^0 = 0, r^{-1} = r^0 = -b
   RS_CUDA(launch_fill(w, m, 0.0, st));
@@ -957,12 +1000,15 @@ rs_status Problem::solve(const rs_solve_opts* o, double* w_out, rs_mem w_mem, do
     auto evs = [&](int i) { return o->profile ? &prof_events[(size_t)i * 2 * RS_K_NCLASSES] : nullptr; };
     for (int i = 0; i < chunk && s == RS_OK;) {
       if (pipe_xg) {   // two groups, alternating slot sets
-        s = pipe_xc ? enqueue_group_xc(o, (i / P) & 1, evs(i)) : enqueue_group_xg(o, (i / P) & 1, evs(i));
+        s = enqueue_group_ov(o, (i / P) & 1, evs(i));
         i += P;
       } else if (pipe) {   // group: precompute ns slots, then ns iterations on them
         const int ns = std::min(P, chunk - i);
         s = enqueue_precompute(o, ns, evs(i));
-        for (int q = 0; q < ns && s == RS_OK; ++q) s = enqueue_pipelined_iteration(o, q, evs(i + q));
+        if (use_iterate && s == RS_OK)
+          s = enqueue_iterate_group(o, ns, evs(i));
+        else
+          for (int q = 0; q < ns && s == RS_OK; ++q) s = enqueue_pipelined_iteration(o, q, evs(i + q));
         i += ns;
       } else {
         s = enqueue_iteration(o, evs(i));
@@ -1000,7 +1046,7 @@ rs_status Problem::solve(const rs_solve_opts* o, double* w_out, rs_mem w_mem, do
   if (timing) fprintf(stderr, "[rs] solve preamble %.3f ms (graph %s)\n", hms(h0), rebuild ? "built" : "reused");
   const auto h1 = std::chrono::steady_clock::now();
   RS_CUDA(cudaEventRecord(t0, st));
-  // fused pipeline: slot set 0 (iterations 0 .. P-1) is formed and factored up front
+  // overlapped pipeline: slot set 0 (iterations 0 .. P-1) is formed and factored up front
   if (pipe_xg && !ctrl_host->done) RS_TRY(enqueue_precompute(o, P, nullptr));
   long long k_prev = 0, graph_launches = 0;
   while (!ctrl_host->done) {
@@ -1021,6 +1067,8 @@ rs_status Problem::solve(const rs_solve_opts* o, double* w_out, rs_mem w_mem, do
         }
       cudaGetLastError();
     }
+    if (world > 1 && hostcoll_failed(hcoll))
+      return fail(RS_ENCCL, "host collective: a rank timed out in an allreduce");
     if (world > 1 && comm) {
       std::string err;
       const NcclApi* api = nccl_api(&err);
@@ -1059,6 +1107,8 @@ rs_status Problem::solve(const rs_solve_opts* o, double* w_out, rs_mem w_mem, do
   if (o->trace && R.trace_len > 0)
     RS_CUDA(cudaMemcpy(o->trace, trace_dev, R.trace_len * 8, cudaMemcpyDeviceToHost));
   const int rc = status_of(h.status);
+  if (h.status == ST_SKETCHFAIL)
+    return fail(RS_EUNSUPPORTED, "sketch selection: more than 1024 coordinates share one 64-bit key");
   if (rc == RS_EUNSUPPORTED)
     return fail(RS_EUNSUPPORTED, "CSR dual: sketched-row hash table overflow (bucket too dense)");
   if (rc == RS_ENOTSPD)
@@ -1183,12 +1233,15 @@ rs_status rs_sketch_draw(rs_sketch_kind kind, int64_t m, int64_t tau, int64_t su
   if (e == cudaSuccess) e = cudaMemcpy(coord, sk.coord, L * 4, cudaMemcpyDeviceToHost);
   if (e == cudaSuccess) e = cudaMemcpy(bucket, sk.bucket, L * 4, cudaMemcpyDeviceToHost);
   if (e == cudaSuccess) e = cudaMemcpy(sign, sk.sign, L, cudaMemcpyDeviceToHost);
+  int serr = 0;
+  if (e == cudaSuccess) e = rs::sketch_err_take(&serr);
   cudaFree(sk.coord);
   cudaFree(sk.bucket);
   cudaFree(sk.sign);
   cudaFree(sk.bptr);
   if (sk.cmap) cudaFree(sk.cmap);
   if (e != cudaSuccess) return fail(RS_ECUDA, std::string("sketch draw: ") + cudaGetErrorString(e));
+  if (serr) return fail(RS_EUNSUPPORTED, "sketch selection: more than 1024 coordinates share one 64-bit key");
   *len_out = (int64_t)L;
   return RS_OK;
 }
@@ -1235,6 +1288,12 @@ rs_status rs_nccl_unique_id(void* out128) {
   ncclResult_t e = api->ncclGetUniqueId(&id);
   if (e != ncclSuccess) return fail(RS_ENCCL, api->ncclGetErrorString(e));
   std::memcpy(out128, &id, sizeof(id));
+  return RS_OK;
+}
+
+rs_status rs_host_coll_id(void* out128) {
+  if (!out128) return fail(RS_EINVAL, "NULL output");
+  rs::hostcoll_new_name(static_cast<char*>(out128));
   return RS_OK;
 }
 

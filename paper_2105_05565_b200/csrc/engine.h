@@ -8,6 +8,7 @@
 
 #include "../../include/ridgesketch.h"
 #include "rs_internal.cuh"
+#include "hostcoll.h"
 
 namespace rs {
 
@@ -37,6 +38,8 @@ struct Problem {
   bool own_stream = false;
   int rank = 0, world = 1;
   ncclComm_t comm = nullptr;
+  int coll = 0;                    // rs_collective
+  struct HostColl* hcoll = nullptr;   // RS_COLL_HOST
   // problem
   int fmt = 0;      // 0 dense, 1 CSR
   int route = 1;    // 1 primal (m = d), 2 dual (m = n)
@@ -94,17 +97,15 @@ struct Problem {
   long long ld_gi = 0, gi_stride = 0;
   int* slot_flags = nullptr;
   double* bf_work = nullptr;     // tau > 224: per-slot work matrices of the batched factorisation
-  // fused pipeline (dense GRAM, subsample tau <= 200): two slot sets of P; while group g runs on
-  // set g % 2, its X passes also form the Grams of the other set (k_xpass_gram)
-  bool pipe_xg = false;
+  double* it_scratch = nullptr;  // EXPLICIT group kernel (iterate.cu): t, delta (tau each), partials
+  bool use_iterate = false;
+  // EXPLICIT, tau > 224: two slot sets of P; the next group's factorisation (st2) overlaps the
+  // current group's iterations (st, k_iterate on the SMs the factor grid leaves free)
+  bool pipe_xg = false;   // two slot sets
+  bool pipe_ov = false;
   int ws_xg = -1;
-  // concurrent variant (dense GRAM with X^T, one rank): the Grams of the other set run on a second
-  // stream (lean k_gram_xt) while the iterations' lean X passes stream X (enqueue_group_xc)
-  bool pipe_xc = false;
   cudaStream_t st2 = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
-  long long* kbase_dev = nullptr;   // the group's base iteration, for the concurrent Grams
-  double* gf_part = nullptr;
   SolveWork sw{};
   double* partials = nullptr;
   cudaGraphExec_t graph_exec = nullptr;
@@ -116,11 +117,12 @@ struct Problem {
   void free_workspace();
   rs_status allreduce(double* buf, size_t count);
   rs_status ensure_workspace(int kind, int tau, int ksum, int depth, bool xg = false);
-  rs_status enqueue_group_xg(const rs_solve_opts* o, int g, cudaEvent_t* ev);
-  rs_status enqueue_group_xc(const rs_solve_opts* o, int g, cudaEvent_t* ev);
   rs_status enqueue_iteration(const rs_solve_opts* o, cudaEvent_t* ev);
   rs_status enqueue_precompute(const rs_solve_opts* o, int nslots, cudaEvent_t* ev);
   rs_status enqueue_pipelined_iteration(const rs_solve_opts* o, int slot, cudaEvent_t* ev);
+  rs_status enqueue_iterate_group(const rs_solve_opts* o, int ns, cudaEvent_t* ev, int slot0 = 0,
+                                  int grid = 0);
+  rs_status enqueue_group_ov(const rs_solve_opts* o, int g, cudaEvent_t* ev);
   rs_status solve(const rs_solve_opts* o, double* w_out, rs_mem w_mem, double* alpha_out,
                   rs_report* rep);
   rs_status write_weights(double* w_out, rs_mem w_mem, double* alpha_out);

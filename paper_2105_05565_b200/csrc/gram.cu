@@ -425,121 +425,10 @@ k_gram_fused(const double* __restrict__ X, long long ldx, long long rows, DevSke
 
 // Gram from the transposed copy XT (d x n, row-major, built once per problem): the tau sketched
 // columns of X are tau contiguous rows of XT, so a K-slice of the Gram reads tau coalesced
-// 128-byte segments per 16 rows of X (the algorithmic tau n 8 bytes) instead of gathering 8-byte
-// elements that touch ~0.8 of X's lines.  Stage layout [region rows][GX_LDK] (k contiguous,
-// stride 20 doubles: conflict-free DMMA fragments); the same 15-warp 40 x 40 region split and
-// per-CTA partials as k_gram_fused, reduced in order by k_gram_reduce.
-// BK k-values per stage (row stride BK + 4 doubles: conflict-free fragments), STAGES deep
-template <int BK> struct GxCfg {
-  static constexpr int LDK = BK + 4;
-  static constexpr int STAGES = BK == 16 ? 6 : 3;
-};
-
-__device__ __forceinline__ void cp_async16z(void* smem, const void* gmem, int src_bytes) {
-  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(src_bytes));
-}
-
-// NW warps per CTA; the (tau / 40)-region list is covered in ceil(regions / NW) passes over the
-// K slice (NW = 16: one pass; NW = 8: the lean variant that shares an SM with the X pass).
-// kbase (optional): the group's base iteration, for a Gram running concurrently with the
-// iterations that advance ctrl->k (slot q is needed iff kbase + q < max_iter).
-template <int GX_BK, int NW>
-__global__ void __launch_bounds__(NW * 32)
-k_gram_xt(const double* __restrict__ XT, long long ldxt, long long rows, DevSketch sk,
-          long long rows_per_cta, double* __restrict__ partials, int slot, const Ctrl* ctrl,
-          const long long* kbase) {
-  constexpr int GX_LDK = GxCfg<GX_BK>::LDK, NT = NW * 32;
-  constexpr int GX_STAGES = NW == 8 ? GxCfg<GX_BK>::STAGES / 2 : GxCfg<GX_BK>::STAGES;   // lean: half
-  if (ctrl->done || (kbase ? *kbase : ctrl->k) + slot >= ctrl->max_iter) return;
-  extern __shared__ __align__(16) double gsm[];   // [GX_STAGES][ng * 40][GX_LDK]
-  __shared__ int s_col[GF_MAXTAU];
-  const int tau = sk.tau, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  for (int b = tid; b < tau; b += NT) s_col[b] = sk.coord[sk.bptr[b]];
-  __syncthreads();
-  const long long r0 = (long long)blockIdx.x * rows_per_cta;
-  const long long r1 = min(rows, r0 + rows_per_cta);
-  const int nkb = r0 < r1 ? (int)((r1 - r0 + GX_BK - 1) / GX_BK) : 0;
-  const int ng = (tau + 39) / 40, srows = ng * 40;
-  const int nreg = ng * (ng + 1) / 2, passes = (nreg + NW - 1) / NW;
-  const int stage_elems = srows * GX_LDK;
-  auto load = [&](int stage, int kb) {
-    double* dst = gsm + stage * stage_elems;
-    const long long k0 = r0 + (long long)kb * GX_BK;
-    for (int q = tid; q < srows * (GX_BK / 2); q += NT) {
-      const int b = q / (GX_BK / 2), h = q % (GX_BK / 2);
-      const long long k = k0 + 2 * h;
-      const int nb = (b < tau) ? (int)max(0LL, min(2LL, r1 - k)) * 8 : 0;
-      cp_async16z(dst + b * GX_LDK + 2 * h, nb ? XT + (long long)s_col[b] * ldxt + k : XT, nb);
-    }
-  };
-  const int kq = lane & 3, mq = lane >> 2;
-  double* out = partials + (long long)blockIdx.x * GF_MAXTAU * GF_MAXTAU;
-  for (int pass = 0; pass < passes; ++pass) {
-#pragma unroll
-    for (int s = 0; s < GX_STAGES - 1; ++s) {
-      if (s < nkb) load(s, s);
-      asm volatile("cp.async.commit_group;\n");
-    }
-    int I = -1, J = -1;
-    {
-      const int want = warp + pass * NW;
-      int t = 0;
-      for (int a = 0; a < ng; ++a)
-        for (int b = 0; b <= a; ++b, ++t)
-          if (t == want) { I = a; J = b; }
-    }
-    const bool active = I >= 0, diag = I == J;
-    double acc[5][5][2];
-#pragma unroll
-    for (int x = 0; x < 5; ++x)
-#pragma unroll
-      for (int y = 0; y < 5; ++y) acc[x][y][0] = acc[x][y][1] = 0.0;
-    for (int kb = 0; kb < nkb; ++kb) {
-      asm volatile("cp.async.wait_group %0;\n" ::"n"(GX_STAGES - 2));
-      __syncthreads();
-      const int nxt = kb + GX_STAGES - 1;
-      if (nxt < nkb) load(nxt % GX_STAGES, nxt);
-      asm volatile("cp.async.commit_group;\n");
-      if (active) {
-        const double* st = gsm + (kb % GX_STAGES) * stage_elems + mq * GX_LDK + kq;
-        const double* sa = st + (I * 40) * GX_LDK;
-        const double* sb = st + (J * 40) * GX_LDK;
-#pragma unroll
-        for (int kk = 0; kk < GX_BK; kk += 4) {
-          double bf[5];
-#pragma unroll
-          for (int y = 0; y < 5; ++y) bf[y] = sb[y * 8 * GX_LDK + kk];
-#pragma unroll
-          for (int x = 0; x < 5; ++x) {
-            const double af = sa[x * 8 * GX_LDK + kk];
-#pragma unroll
-            for (int y = 0; y < 5; ++y)
-              if (!diag || y <= x) dmma_g(acc[x][y], af, bf[y]);   // diagonal region: lower tiles
-          }
-        }
-      }
-    }
-    asm volatile("cp.async.wait_group 0;\n");
-    __syncthreads();   // the ring is reused by the next pass
-    if (active) {
-#pragma unroll
-      for (int x = 0; x < 5; ++x) {
-        const int a = I * 40 + x * 8 + (lane >> 2);
-#pragma unroll
-        for (int y = 0; y < 5; ++y) {
-          const int b = J * 40 + y * 8 + 2 * (lane & 3);
-          if (a < tau) {
-            if (b < tau) out[a * GF_MAXTAU + b] = acc[x][y][0];
-            if (b + 1 < tau) out[a * GF_MAXTAU + b + 1] = acc[x][y][1];
-          }
-        }
-      }
-    }
-  }
-}
-
-// Warp-specialised Gram from X^T (default for the one-pass case): warp 15 is a producer that
+// 256-byte segments (the algorithmic tau n 8 bytes) instead of gathering 8-byte elements that
+// touch ~0.8 of X's lines.  Stage layout [region rows][GW_LDK] (k contiguous, conflict-free DMMA
+// fragments); the same 15-warp 40 x 40 region split and per-CTA partials as k_gram_fused, reduced
+// in order by k_gram_reduce.  Warp-specialised: warp 15 is a producer that
 // streams each stage's tau row segments (32 k-values = 256 B each, one cp.async.bulk per row,
 // completion on the stage's "full" mbarrier by transaction count) into a 3-deep ring; the 15
 // consumer warps wait on "full", run their region's DMMA k-steps and release the stage with one
@@ -553,7 +442,7 @@ __global__ void __launch_bounds__(GW_THREADS, 1)
 k_gram_xtw(const double* __restrict__ XT, long long ldxt, long long rows, DevSketch sk,
            long long rows_per_cta, double* __restrict__ partials, int slot, const Ctrl* ctrl) {
   if (slot_unused(ctrl, slot)) return;
-  extern __shared__ __align__(128) double gsm[];   // [GW_STAGES][ng * 40][GW_LDK]
+  extern __shared__ __align__(16) double gsm[];   // [GW_STAGES][ng * 40][GW_LDK]
   __shared__ __align__(8) uint64_t full[GW_STAGES], empty[GW_STAGES];
   __shared__ int s_col[GF_MAXTAU];
   const int tau = sk.tau, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -645,18 +534,6 @@ k_gram_xtw(const double* __restrict__ XT, long long ldxt, long long rows, DevSke
   }
 }
 
-template <int BK>
-size_t gram_xt_smem(int tau) {
-  return (size_t)GxCfg<BK>::STAGES * ((tau + 39) / 40 * 40) * GxCfg<BK>::LDK * 8;
-}
-int gx_bk() {
-  static const int bk = [] {
-    const char* e = std::getenv("RS_GX_BK");
-    return e && atoi(e) == 16 ? 16 : 32;
-  }();
-  return bk;
-}
-
 // XT[j][i] = X[i][j] (32 x 32 tiles through shared memory)
 __global__ void k_transpose(const double* __restrict__ X, long long ldx, long long rows, long long d,
                             double* __restrict__ XT, long long ldxt) {
@@ -701,357 +578,6 @@ k_gram_reduce(const double* __restrict__ partials, int nparts, int tau, double* 
 inline unsigned gram_reduce_grid(int tau) { return (unsigned)((tau * GF_MAXTAU + 31) / 32); }
 
 
-// ---------------------------------------------------------------------------------------------
-// Fused X pass (dense GRAM, subsample tau <= 200, d <= 3360): one TMA-staged stream of X serves
-//   (1) this iteration's u = X^T (X v), v = S_k delta_k                 (k_xpass_tma's work)
-//   (2) the Gram (X S')^T (X S') of a FUTURE sketch S' = S_{k+P}       (k_gram_fused's work)
-// G_{k+P} does not depend on the iterate (S_k is drawn independently of w^k), so the
-// sketch-ahead pipeline computes it while X streams through shared memory for iteration k: X is
-// read from HBM once per iteration instead of twice (the column gather of k_gram_fused alone
-// touches ~0.8 of X's sectors).  4 rows of X per ring stage = one DMMA k-step of the Gram.
-constexpr int XG_CONS = 15;                 // 16 warps = 4 per SMSP -> 128 registers per thread
-constexpr int XG_THREADS = (XG_CONS + 1) * 32;
-constexpr int XG_R = 4;
-
-
-// Single-CTA variant: 15 consumer warps + 1 producer (4 warps per SMSP -> 128 registers).
-// Per ring stage (4 rows of X): every consumer thread forms its Q partial row dots and gathers <= 2
-// of the stage's 4 x tau sketched values into a compact slab (GF_LD stride, conflict-free DMMA
-// fragments, double-buffered); one named barrier; then the row-dot reduction + axpy, and the warp's
-// <= 22 Gram tiles (row-major order of the lower 8 x 8 tiles, tile list in shared memory, 44
-// accumulator doubles per thread) as one DMMA k-step.  v is read from shared memory; the row
-// loops run over whole 480-column strides (columns >= d are selected to zero, never stored).
-constexpr int XG1_TPW = 22;   // tiles per warp
-
-template <int Q>
-__global__ void __launch_bounds__(XG_THREADS, 1)
-k_xpass_gram1(const double* __restrict__ X, long long ldx, long long rows, long long d,
-              const double* __restrict__ v, double* __restrict__ upart, long long rows_per_cta,
-              int stages, DevSketch skg, double* __restrict__ gpart, int gofs, const Ctrl* ctrl) {
-  if (ctrl->done) return;
-  constexpr int NC = XG_CONS * 32;                      // consumer threads
-  extern __shared__ __align__(128) double xs_ring[];   // [stages][XG_R * ldx] + pad, v[NC * Q]
-  __shared__ __align__(8) uint64_t full[8], empty[8];
-  __shared__ double red[2][XG_R][XG_CONS];
-  __shared__ __align__(16) double slab[2][XG_R][GF_LD];
-  __shared__ short2 s_tile[XG_CONS][XG1_TPW];
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int tau = slot_unused(ctrl, gofs) ? 0 : skg.tau;   // future slot needed?
-  const int ldxi = (int)ldx;
-  const int stage_elems = XG_R * ldxi;
-  double* sv = xs_ring + (size_t)stages * stage_elems + NC * Q;   // after the ring + a pad
-  for (int j = tid; j < NC * Q; j += XG_THREADS) sv[j] = j < d ? v[j] : 0.0;
-  const int T8 = (tau + 7) / 8, ntiles = T8 * (T8 + 1) / 2;
-  for (int t = tid; t < XG_CONS * XG1_TPW; t += XG_THREADS) {
-    int i = (int)((sqrtf(8.0f * (float)t + 1.0f) - 1.0f) * 0.5f);
-    while ((i + 1) * (i + 2) / 2 <= t) ++i;
-    while (i * (i + 1) / 2 > t) --i;
-    s_tile[t / XG1_TPW][t % XG1_TPW] = make_short2((short)(i * 8), (short)((t - i * (i + 1) / 2) * 8));
-  }
-  // this thread's gather slots e = tid, tid + NC of the 4 x (8 T8) slab: row e / (8 T8), col e % ..
-  const int tw = 8 * T8;
-  int gcol[2], grow[2], gdst[2];
-#pragma unroll
-  for (int h = 0; h < 2; ++h) {
-    const int e = tid + h * NC;
-    const int rr = tw ? e / tw : XG_R, b = tw ? e % tw : 0;
-    const int c = (rr < XG_R && b < tau) ? skg.coord[skg.bptr[b]] : -1;
-    grow[h] = rr < XG_R ? rr : -1;
-    gcol[h] = c;
-    gdst[h] = rr < XG_R ? rr * GF_LD + b : -1;
-  }
-  const long long r0 = (long long)blockIdx.x * rows_per_cta;
-  const long long r1 = min(rows, r0 + rows_per_cta);
-  const int nblk = r0 < r1 ? (int)((r1 - r0 + XG_R - 1) / XG_R) : 0;
-  if (tid == 0) {
-    for (int s = 0; s < stages; ++s) {
-      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(su32(&full[s])));
-      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(su32(&empty[s])), "r"(XG_CONS));
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-  }
-  __syncthreads();
-  if (warp == XG_CONS) {   // producer
-    if (lane == 0) {
-      for (int b = 0; b < nblk; ++b) {
-        const int s = b % stages;
-        if (b >= stages) xt_wait(&empty[s], ((b / stages) - 1) & 1);
-        const long long i0 = r0 + (long long)b * XG_R;
-        const int nr = (int)min((long long)XG_R, r1 - i0);
-        const unsigned bytes = (unsigned)(nr * ldx * 8);
-        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(su32(&full[s])),
-                     "r"(bytes) : "memory");
-        asm volatile(
-            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n"
-            ::"r"(su32(xs_ring + s * stage_elems)), "l"(X + i0 * ldx), "r"(bytes), "r"(su32(&full[s]))
-            : "memory");
-      }
-    }
-    return;
-  }
-  double acc[Q];
-#pragma unroll
-  for (int q = 0; q < Q; ++q) acc[q] = 0.0;
-  const int t0 = warp * XG1_TPW;
-  const int nt = max(0, min(XG1_TPW, ntiles - t0));
-  double gacc[XG1_TPW][2];
-#pragma unroll
-  for (int q = 0; q < XG1_TPW; ++q) gacc[q][0] = gacc[q][1] = 0.0;
-  const int arow = lane & 3, acol = lane >> 2;
-  int buf = 0;
-  for (int b = 0; b < nblk; ++b) {
-    const int s = b % stages;
-    xt_wait(&full[s], (b / stages) & 1);
-    const double* xs = xs_ring + s * stage_elems;
-    const int nr = (int)min((long long)XG_R, r1 - (r0 + (long long)b * XG_R));
-    // row dots (rows >= nr: stale ring data, their results are never used; columns >= d are
-    // selected away -- the padding of X and the bytes after a row are not guaranteed finite)
-#pragma unroll
-    for (int r = 0; r < XG_R; ++r) {
-      const double* row = xs + r * ldxi + tid;
-      double sdot = 0.0;
-#pragma unroll
-      for (int q = 0; q < Q; ++q) {
-        const double x = row[q * NC];
-        sdot += (tid + q * NC < d ? x : 0.0) * sv[tid + q * NC];
-      }
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) sdot += __shfl_xor_sync(0xffffffffu, sdot, o);
-      if (lane == 0) red[buf][r][warp] = sdot;
-    }
-    // gather the sketched columns of the stage into the slab (rows >= nr as zeros)
-#pragma unroll
-    for (int h = 0; h < 2; ++h)
-      if (gdst[h] >= 0)
-        slab[buf][0][gdst[h]] = (gcol[h] >= 0 && grow[h] < nr) ? xs[grow[h] * ldxi + gcol[h]] : 0.0;
-    asm volatile("bar.sync 1, %0;\n" ::"n"(NC) : "memory");
-#pragma unroll
-    for (int r = 0; r < XG_R; ++r) {
-      if (r < nr) {
-        double t = 0.0;
-#pragma unroll
-        for (int w = 0; w < XG_CONS; ++w) t += red[buf][r][w];
-        const double* row = xs + r * ldxi + tid;
-#pragma unroll
-        for (int q = 0; q < Q; ++q) acc[q] += t * row[q * NC];
-      }
-    }
-    const double* sl = &slab[buf][arow][acol];
-#pragma unroll
-    for (int q = 0; q < XG1_TPW; ++q) {
-      if (q < nt) {
-        const short2 ij = s_tile[warp][q];
-        dmma_g(gacc[q], sl[ij.x], sl[ij.y]);
-      }
-    }
-    buf ^= 1;
-    __syncwarp();
-    if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(su32(&empty[s])) : "memory");
-  }
-#pragma unroll
-  for (int q = 0; q < Q; ++q) {
-    const long long j = tid + (long long)NC * q;
-    if (j < d) upart[(long long)blockIdx.x * d + j] = acc[q];
-  }
-  double* out = gpart + (long long)blockIdx.x * GF_MAXTAU * GF_MAXTAU;
-#pragma unroll
-  for (int q = 0; q < XG1_TPW; ++q) {
-    if (q < nt) {
-      const short2 ij = s_tile[warp][q];
-      const int a = ij.x + (lane >> 2), c = ij.y + 2 * (lane & 3);
-      if (a < tau) {
-        if (c <= a && c < tau) out[a * GF_MAXTAU + c] = gacc[q][0];
-        if (c + 1 <= a && c + 1 < tau) out[a * GF_MAXTAU + c + 1] = gacc[q][1];
-      }
-    }
-  }
-}
-
-// Cluster-pair variant: the Gram accumulators of a whole tau <= 200 lower triangle (20100 doubles)
-// do not fit one SM's register file next to the X-pass state, so two CTAs of a cluster on two SMs
-// share ONE stream of X: CTA rank 0 multicasts every ring stage (cp.async.bulk ...
-// .multicast::cluster) into both CTAs' shared memory; each CTA owns half of the Gram's 40 x 40
-// regions (every warp 5 x 3 or 5 x 2 DMMA tiles) and the X-pass rows of every other stage.
-// Stage reuse: each CTA's `empty` barrier counts the consumer warps of BOTH CTAs (local arrive +
-// remote arrive through mapa), each CTA's producer re-arms its own `full` barrier with the stage's
-// byte count, so both copies of a stage are free before rank 0 overwrites them.
-__device__ __forceinline__ unsigned cluster_rank() {
-  unsigned r;
-  asm volatile("mov.u32 %0, %%cluster_ctarank;\n" : "=r"(r));
-  return r;
-}
-__device__ __forceinline__ void cluster_sync_all() {
-  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
-}
-__device__ __forceinline__ void mbar_arrive_remote(uint64_t* bar, unsigned rank) {
-  asm volatile(
-      "{\n.reg .b32 ra;\nmapa.shared::cluster.u32 ra, %0, %1;\n"
-      "mbarrier.arrive.release.cluster.shared::cluster.b64 _, [ra];\n}\n" ::"r"(su32(bar)), "r"(rank)
-      : "memory");
-}
-
-template <int Q>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(XG_THREADS, 1)
-k_xpass_gram2(const double* __restrict__ X, long long ldx, long long rows, long long d,
-              const double* __restrict__ v, double* __restrict__ upart, long long rows_per_pair,
-              int stages, DevSketch skg, double* __restrict__ gpart, int gofs, const Ctrl* ctrl) {
-  if (ctrl->done) return;   // uniform over the grid (ctrl is not written during this kernel)
-  extern __shared__ __align__(128) double xs_ring[];   // [stages][XG_R * ldx]
-  __shared__ __align__(8) uint64_t full[8], empty[8];
-  __shared__ double red[2][XG_R][XG_CONS];
-  __shared__ int s_col[GF_MAXTAU + 8];
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const unsigned rank = cluster_rank(), peer = rank ^ 1u;
-  const int tau = slot_unused(ctrl, gofs) ? 0 : skg.tau;   // future slot needed?
-  for (int b = tid; b < GF_MAXTAU + 8; b += XG_THREADS)
-    s_col[b] = b < tau ? skg.coord[skg.bptr[b]] : -1;
-  const long long pair = blockIdx.x >> 1;
-  const long long r0 = pair * rows_per_pair;
-  const long long r1 = min(rows, r0 + rows_per_pair);
-  const int nblk = r0 < r1 ? (int)((r1 - r0 + XG_R - 1) / XG_R) : 0;
-  const long long stage_elems = (long long)XG_R * ldx;
-  if (tid == 0) {
-    for (int s = 0; s < stages; ++s) {
-      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(su32(&full[s])));
-      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(su32(&empty[s])), "r"(2 * XG_CONS));
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-  }
-  __syncthreads();
-  cluster_sync_all();   // both CTAs' barriers initialised before any remote arrive / multicast
-  if (warp == XG_CONS) {   // producer: re-arm the local full barrier; rank 0 issues the multicast
-    if (lane == 0) {
-      for (int b = 0; b < nblk; ++b) {
-        const int s = b % stages;
-        if (b >= stages) xt_wait(&empty[s], ((b / stages) - 1) & 1);
-        const long long i0 = r0 + (long long)b * XG_R;
-        const int nr = (int)min((long long)XG_R, r1 - i0);
-        const unsigned bytes = (unsigned)(nr * ldx * 8);
-        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(su32(&full[s])),
-                     "r"(bytes) : "memory");
-        if (rank == 0) {
-          const unsigned short mask = 3;
-          asm volatile(
-              "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
-              " [%0], [%1], %2, [%3], %4;\n"
-              ::"r"(su32(xs_ring + s * stage_elems)), "l"(X + i0 * ldx), "r"(bytes),
-                "r"(su32(&full[s])), "h"(mask) : "memory");
-        }
-      }
-    }
-  } else {
-    // consumers: X pass on the stages b with b % 2 == rank
-    double vr[Q], acc[Q];
-#pragma unroll
-    for (int q = 0; q < Q; ++q) {
-      const long long j = tid + (long long)(XG_CONS * 32) * q;
-      vr[q] = j < d ? v[j] : 0.0;
-      acc[q] = 0.0;
-    }
-    // Gram: half-region h = 15 rank + warp of the 15 (I >= J) 40 x 40 regions x 2 halves:
-    // region h / 2, tile columns y in [0, 3) (h even) or [3, 5) (h odd)
-    const int ng = (tau + 39) / 40;
-    const int h = XG_CONS * (int)rank + warp;
-    const int t = h >> 1;
-    int I = -1, J = -1;
-    {
-      int u = 0;
-      for (int a = 0; a < ng; ++a)
-        for (int b = 0; b <= a; ++b, ++u)
-          if (u == t) { I = a; J = b; }
-    }
-    const bool gactive = I >= 0;
-    const int y0 = (h & 1) ? 3 : 0, ny = (h & 1) ? 2 : 3;
-    double gacc[5][3][2];
-#pragma unroll
-    for (int x = 0; x < 5; ++x)
-#pragma unroll
-      for (int y = 0; y < 3; ++y) gacc[x][y][0] = gacc[x][y][1] = 0.0;
-    const int arow = lane & 3, acol = lane >> 2;
-    int buf = 0;
-    for (int b = 0; b < nblk; ++b) {
-      const int s = b % stages;
-      xt_wait(&full[s], (b / stages) & 1);
-      const double* xs = xs_ring + s * stage_elems;
-      const long long i0 = r0 + (long long)b * XG_R;
-      const int nr = (int)min((long long)XG_R, r1 - i0);
-      const bool mine = (b & 1) == (int)rank;
-      if (mine) {
-        for (int r = 0; r < nr; ++r) {
-          const double* row = xs + r * ldx;
-          double sdot = 0.0;
-#pragma unroll
-          for (int q = 0; q < Q; ++q) {
-            const long long j = tid + (long long)(XG_CONS * 32) * q;
-            if (j < d) sdot += row[j] * vr[q];
-          }
-#pragma unroll
-          for (int o = 16; o > 0; o >>= 1) sdot += __shfl_xor_sync(0xffffffffu, sdot, o);
-          if (lane == 0) red[buf][r][warp] = sdot;
-        }
-      }
-      if (gactive) {   // k-step over the stage's 4 rows (rows >= nr read as zero)
-        const bool rok = arow < nr;
-        const double* rp = xs + arow * ldx;
-        double bf[3];
-#pragma unroll
-        for (int y = 0; y < 3; ++y) {
-          const int c = y < ny ? s_col[J * 40 + (y0 + y) * 8 + acol] : -1;
-          bf[y] = (rok && c >= 0) ? rp[c] : 0.0;
-        }
-#pragma unroll
-        for (int x = 0; x < 5; ++x) {
-          const int c = s_col[I * 40 + x * 8 + acol];
-          const double af = (rok && c >= 0) ? rp[c] : 0.0;
-#pragma unroll
-          for (int y = 0; y < 3; ++y)
-            if (y < ny) dmma_g(gacc[x][y], af, bf[y]);
-        }
-      }
-      if (mine) {
-        asm volatile("bar.sync 1, %0;\n" ::"n"(XG_CONS * 32) : "memory");
-        for (int r = 0; r < nr; ++r) {
-          double tt = 0.0;
-#pragma unroll
-          for (int w = 0; w < XG_CONS; ++w) tt += red[buf][r][w];
-          const double* row = xs + r * ldx;
-#pragma unroll
-          for (int q = 0; q < Q; ++q) {
-            const long long j = tid + (long long)(XG_CONS * 32) * q;
-            if (j < d) acc[q] += tt * row[j];
-          }
-        }
-        buf ^= 1;
-      }
-      __syncwarp();
-      if (lane == 0) {
-        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(su32(&empty[s])) : "memory");
-        mbar_arrive_remote(&empty[s], peer);
-      }
-    }
-#pragma unroll
-    for (int q = 0; q < Q; ++q) {
-      const long long j = tid + (long long)(XG_CONS * 32) * q;
-      if (j < d) upart[(long long)blockIdx.x * d + j] = acc[q];
-    }
-    if (gactive) {
-      double* out = gpart + pair * GF_MAXTAU * GF_MAXTAU;
-#pragma unroll
-      for (int x = 0; x < 5; ++x) {
-        const int a = I * 40 + x * 8 + (lane >> 2);
-#pragma unroll
-        for (int y = 0; y < 3; ++y) {
-          const int c = J * 40 + (y0 + y) * 8 + 2 * (lane & 3);
-          if (y < ny && a < tau) {
-            if (c < tau) out[a * GF_MAXTAU + c] = gacc[x][y][0];
-            if (c + 1 < tau) out[a * GF_MAXTAU + c + 1] = gacc[x][y][1];
-          }
-        }
-      }
-    }
-  }
-  cluster_sync_all();   // the peer may still arrive on our barriers / receive our multicast
-}
 }  // namespace
 
 bool gram_fused_ok(int kind, int tau) { return kind == SK_SUBSAMPLE && tau <= GF_MAXTAU; }
@@ -1063,19 +589,9 @@ cudaError_t gram_init() {
   if (e != cudaSuccess) return e;
   e = cudaFuncSetAttribute(k_xpass_rows<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
   if (e != cudaSuccess) return e;
-  e = cudaFuncSetAttribute(k_xpass_rows<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
-  if (e != cudaSuccess) return e;
-  e = cudaFuncSetAttribute(k_gram_xt<16, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)gram_xt_smem<16>(GF_MAXTAU));
-  if (e != cudaSuccess) return e;
-  e = cudaFuncSetAttribute(k_gram_xt<32, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)gram_xt_smem<32>(GF_MAXTAU));
-  if (e != cudaSuccess) return e;
+
   e = cudaFuncSetAttribute(k_gram_xtw, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)gram_xtw_smem(GF_MAXTAU));
-  if (e != cudaSuccess) return e;
-  e = cudaFuncSetAttribute(k_gram_xt<16, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)gram_xt_smem<16>(GF_MAXTAU) / 2);
   if (e != cudaSuccess) return e;
   return cudaFuncSetAttribute(k_gram_fused, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               GF_STAGES * GF_BK * GF_LD * (int)sizeof(double));
@@ -1103,38 +619,16 @@ cudaError_t launch_transpose(const double* X, long long ldx, long long rows, lon
 
 cudaError_t launch_gram_xt(const double* XT, long long ldxt, long long rows, const DevSketch& sk,
                            double* partials, double* G, long long ldg, int num_sms,
-                           const Ctrl* ctrl, cudaStream_t st, int slot, const long long* kbase,
-                           bool lean) {
+                           const Ctrl* ctrl, cudaStream_t st, int slot) {
   const int nc = num_sms;
-  const int bk = lean ? 16 : gx_bk();
-  const long long rpc = std::max<long long>(bk, ((rows + nc - 1) / nc + bk - 1) / bk * bk);
-  static const bool no_ws = std::getenv("RS_GX_SYNC") != nullptr;   // A/B: the barrier-synced kernel
-  if (!lean && !no_ws && ldxt % 64 == 0) {
-    const long long rpw = std::max<long long>(GW_BK, ((rows + nc - 1) / nc + GW_BK - 1) / GW_BK * GW_BK);
-    k_gram_xtw<<<nc, GW_THREADS, gram_xtw_smem(sk.tau), st>>>(XT, ldxt, rows, sk, rpw, partials, slot,
-                                                             ctrl);
-  } else if (lean)   // 8 warps, 3 stages of 16 rows: ~96 KB, leaves room for the lean X pass
-    k_gram_xt<16, 8><<<nc, 8 * 32, gram_xt_smem<16>(sk.tau) / 2, st>>>(XT, ldxt, rows, sk, rpc,
-                                                                       partials, slot, ctrl, kbase);
-  else if (bk == 16)
-    k_gram_xt<16, 16><<<nc, GF_THREADS, gram_xt_smem<16>(sk.tau), st>>>(XT, ldxt, rows, sk, rpc,
-                                                                       partials, slot, ctrl, kbase);
-  else
-    k_gram_xt<32, 16><<<nc, GF_THREADS, gram_xt_smem<32>(sk.tau), st>>>(XT, ldxt, rows, sk, rpc,
-                                                                       partials, slot, ctrl, kbase);
+  if (ldxt % 64 != 0) return cudaErrorInvalidValue;   // rows of X^T are zero-padded to 64
+  const long long rpw = std::max<long long>(GW_BK, ((rows + nc - 1) / nc + GW_BK - 1) / GW_BK * GW_BK);
+  k_gram_xtw<<<nc, GW_THREADS, gram_xtw_smem(sk.tau), st>>>(XT, ldxt, rows, sk, rpw, partials, slot,
+                                                           ctrl);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   k_gram_reduce<<<gram_reduce_grid(sk.tau), 256, 0, st>>>(partials, nc, sk.tau, G, ldg, ctrl, slot,
-                                                          kbase);
-  return cudaGetLastError();
-}
-
-namespace {
-__global__ void k_snap_k(const Ctrl* ctrl, long long* out) { *out = ctrl->k; }
-}  // namespace
-
-cudaError_t launch_snap_k(const Ctrl* ctrl, long long* out, cudaStream_t st) {
-  k_snap_k<<<1, 1, 0, st>>>(ctrl, out);
+                                                          nullptr);
   return cudaGetLastError();
 }
 
@@ -1144,36 +638,21 @@ size_t xpass_partials(long long d, int num_sms) { return (size_t)num_sms * (size
 cudaError_t launch_xpass(const double* X, long long ldx, long long rows, long long d,
                          const double* v, double* partials, double* u, int num_sms,
                          const Ctrl* ctrl, cudaStream_t st, const DevSketch* sk,
-                         const double* delta, bool lean) {
+                         const double* delta) {
   if (d > (long long)XP_THREADS * XP_Q) return cudaErrorInvalidValue;
   const int nc = xpass_ctas(num_sms);
   const long long rpc = std::max<long long>(1, (rows + nc - 1) / nc);
-  static const bool no_tma = std::getenv("RS_NO_TMA_XPASS") != nullptr;
-  static const bool no_rows = std::getenv("RS_NO_XPASS_ROWS") != nullptr;
-  // ring: R rows per stage (~64 KB), as many stages as fit in ~200 KB (>= 2); lean (shares the SM
-  // with a concurrent Gram kernel): 2 consumer warps, ~96 KB
+  // ring: R rows per stage (~64 KB), as many stages as fit in ~200 KB (>= 2)
   const long long row_bytes = ldx * 8;
-  const long long stage_target = lean ? 32768 : 65536, ring_target = lean ? 98304 : 200 * 1024;
-  int R = (int)std::max<long long>(1, std::min<long long>(XT_MAXR, stage_target / row_bytes));
-  static const char* er = std::getenv("RS_XP_R");   // tuning overrides (bench sweeps only)
-  if (er && !lean) R = std::max(1, std::min(XT_MAXR, atoi(er)));
-  int stages = (int)std::min<long long>(8, ring_target / (R * row_bytes));
-  static const char* es = std::getenv("RS_XP_STAGES");
-  if (es && !lean) stages = std::max(2, std::min(stages, atoi(es)));
+  const int R = (int)std::max<long long>(1, std::min<long long>(XT_MAXR, 65536 / row_bytes));
+  const int stages = (int)std::min<long long>(8, (200 * 1024) / (R * row_bytes));
   const size_t ring = (size_t)stages * R * row_bytes;
-  const int cons = lean ? 2 : 8;
-  if (!no_tma && !no_rows && sk && delta && d <= 32LL * XR_NQ && sk->len <= XR_MAXLEN &&
-      stages >= 2 && ring >= (size_t)cons * d * 8 && ring + (size_t)sk->len * 12 <= 220 * 1024) {
-    const size_t smem = ring + (size_t)sk->len * 12;
-    if (lean)
-      k_xpass_rows<2><<<nc, 3 * 32, smem, st>>>(X, ldx, rows, d, *sk, delta, partials, rpc, R, stages,
-                                                ctrl);
-    else
-      k_xpass_rows<8><<<nc, 9 * 32, smem, st>>>(X, ldx, rows, d, *sk, delta, partials, rpc, R, stages,
-                                                ctrl);
-  } else if (lean) {
-    return cudaErrorInvalidValue;
-  } else if (!no_tma && stages >= 2 && d <= (long long)XT_CONS * 32 * XT_Q) {
+  if (sk && delta && d <= 32LL * XR_NQ && sk->len <= XR_MAXLEN && stages >= 2 &&
+      ring >= (size_t)8 * d * 8 && ring + (size_t)sk->len * 12 <= 220 * 1024) {
+    // warp-owned rows, <X_i, S delta> from the sketch entries only
+    k_xpass_rows<8><<<nc, 9 * 32, ring + (size_t)sk->len * 12, st>>>(X, ldx, rows, d, *sk, delta, partials,
+                                                                   rpc, R, stages, ctrl);
+  } else if (stages >= 2 && d <= (long long)XT_CONS * 32 * XT_Q) {
     k_xpass_tma<<<nc, XT_THREADS, ring, st>>>(X, ldx, rows, d, v, partials, rpc, R, stages, ctrl);
   } else {
     k_xpass<<<nc, XP_THREADS, 0, st>>>(X, ldx, rows, d, v, partials, rpc, ctrl);
@@ -1181,56 +660,6 @@ cudaError_t launch_xpass(const double* X, long long ldx, long long rows, long lo
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   k_xpass_reduce<<<(unsigned)((d + 31) / 32), dim3(32, XR_Y), 0, st>>>(partials, nc, d, u, ctrl);
-  return cudaGetLastError();
-}
-
-bool xpass_gram_ok(int kind, int tau, long long d, long long ldx) {
-  return kind == SK_SUBSAMPLE && tau <= GF_MAXTAU && d <= 7 * XG_CONS * 32 &&
-         2 * XG_R * ldx * 8 <= 200 * 1024;
-}
-
-cudaError_t launch_xpass_gram(const double* X, long long ldx, long long rows, long long d,
-                              const double* v, double* upart, double* u, const DevSketch& skg,
-                              double* gpart, double* G, long long ldg, int num_sms,
-                              const Ctrl* ctrl, cudaStream_t st, int gofs) {
-  const int nc = xpass_ctas(num_sms) & ~1;   // cluster pairs
-  const int npairs = nc / 2;
-  const long long rpp = std::max<long long>(1, (rows + npairs - 1) / npairs);
-  const long long stage_bytes = (long long)XG_R * ldx * 8;
-  const int stages = (int)std::min<long long>(8, (200 * 1024) / stage_bytes);
-  if (stages < 2 || skg.tau > GF_MAXTAU) return cudaErrorInvalidValue;
-  const size_t smem = (size_t)stages * stage_bytes;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_xpass_gram2<5>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    cudaFuncSetAttribute(k_xpass_gram2<7>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    cudaFuncSetAttribute(k_xpass_gram1<5>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    cudaFuncSetAttribute(k_xpass_gram1<7>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    attr = true;
-  }
-  static const bool pair = std::getenv("RS_XG_PAIR") != nullptr;
-  if (pair) {
-    if (d <= 5 * XG_CONS * 32)
-      k_xpass_gram2<5><<<nc, XG_THREADS, smem, st>>>(X, ldx, rows, d, v, upart, rpp, stages, skg, gpart, gofs, ctrl);
-    else
-      k_xpass_gram2<7><<<nc, XG_THREADS, smem, st>>>(X, ldx, rows, d, v, upart, rpp, stages, skg, gpart, gofs, ctrl);
-  } else {   // single CTA per SM: stages from 200 KB minus v
-    const int Q = d <= 5 * XG_CONS * 32 ? 5 : 7;
-    const long long extra = 2LL * Q * XG_CONS * 32 * 8;   // read pad after the ring + v
-    const int st1 = (int)std::min<long long>(8, (200 * 1024 - extra) / stage_bytes);
-    if (st1 < 2) return cudaErrorInvalidValue;
-    const size_t smem1 = (size_t)st1 * stage_bytes + (size_t)extra;
-    const long long rpc = std::max<long long>(1, (rows + nc - 1) / nc);
-    if (d <= 5 * XG_CONS * 32)
-      k_xpass_gram1<5><<<nc, XG_THREADS, smem1, st>>>(X, ldx, rows, d, v, upart, rpc, st1, skg, gpart, gofs, ctrl);
-    else
-      k_xpass_gram1<7><<<nc, XG_THREADS, smem1, st>>>(X, ldx, rows, d, v, upart, rpc, st1, skg, gpart, gofs, ctrl);
-  }
-  cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess) return e;
-  k_xpass_reduce<<<(unsigned)((d + 31) / 32), dim3(32, XR_Y), 0, st>>>(upart, nc, d, u, ctrl);
-  if (skg.tau > 0)
-    k_gram_reduce<<<gram_reduce_grid(skg.tau), 256, 0, st>>>(gpart, pair ? npairs : nc, skg.tau, G, ldg, ctrl, gofs);
   return cudaGetLastError();
 }
 }  // namespace rs

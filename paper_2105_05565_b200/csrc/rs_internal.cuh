@@ -13,7 +13,8 @@ enum : int {
   ST_RUNNING = 0, ST_CONVERGED = 1, ST_MAXITER = 2,
   // errors (>= ST_DIVERGED): set by the kernel that detects them; the update kernel turns them
   // into `done` (a cooperative kernel must never set `done` itself, see chol.cu)
-  ST_DIVERGED = 3, ST_NOTSPD = 4, ST_OVERFLOW = 5
+  ST_DIVERGED = 3, ST_NOTSPD = 4, ST_OVERFLOW = 5,
+  ST_SKETCHFAIL = 6   // sketch selection met > 1024 equal 64-bit keys (never seen; fails loudly)
 };
 
 struct Ctrl {
@@ -146,6 +147,8 @@ cudaError_t launch_sketch(const DevSketch& sk, uint64_t seed, const Ctrl* ctrl, 
 cudaError_t launch_sketch_batch(const DevSketch& skb, int nslots, uint64_t seed, const Ctrl* ctrl,
                                 long long fixed_k, cudaStream_t st, long long kofs = 0);
 size_t sketch_max_len(int kind, int m, int tau, int ksum);
+// rs_sketch_draw (no control block): the select's failure flag, read and cleared
+cudaError_t sketch_err_take(int* out);
 
 // a2 dense: XS[i, b] = sum_{e in b} sign_e X[i, coord_e],  i < rows, row-major ld_xs (>= tau, pad
 // columns zeroed).
@@ -193,11 +196,38 @@ cudaError_t tma_gemm_plan(TmaGemm* g, const double* Aop, long long lda, const do
 cudaError_t tma_gemm_launch(const TmaGemm& g, double* C, long long ldc, double* work,
                             const Ctrl* ctrl, cudaStream_t st);
 
+// The EXPLICIT iterations of a sketch-ahead group as one persistent cooperative kernel (iterate.cu).
+struct IterArgs {
+  const double* Ginv;            // factor slots: G^{-1} (tau <= 224) or W lower / W^T upper
+  long long ld_gi, gi_stride;
+  DevSketch skb;                 // slot q's sketch: skb.at(q)
+  const int* flags;              // slot not SPD
+  const double* A;               // explicit A (rows of A S for subsample / SubCount), or
+  long long lda;
+  const double* ASt;             // the slots' A S^T rows (count sketch), null otherwise
+  long long ld_as, as_stride;
+  long long m;
+  double *w, *dw, *r, *dr, *sdelta;
+  double *tvec, *dvec;           // tau each
+  double* partials;              // one per CTA (grid = num_sms)
+  double gamma, beta;
+  int nslots;                    // iterations of the group
+  int big;                       // tau > 224
+};
+// SMs left to the iterations while the next group's factorisation runs (EXPLICIT, tau > 224)
+constexpr int OV_SMS = 24;
+size_t iterate_smem();
+bool iterate_ok(const DevSketch& sk, long long m, int grid);   // the group kernel applies
+cudaError_t iterate_init();
+cudaError_t launch_iterate(const IterArgs& args, int grid, Ctrl* ctrl, cudaStream_t st);
+
 // lambda S:  AS^T[b_e, coord_e] += lambda * sign_e  (as_rowmajor: AS[coord_e, b_e]).
 cudaError_t launch_add_lambda_s(double lambda, const DevSketch& sk, double* ASt, long long ld_as,
                                 bool as_rowmajor, const Ctrl* ctrl, cudaStream_t st);
 // A += lambda I on a dense m x m.
 cudaError_t launch_add_diag(double* A, long long lda, long long m, double lambda, cudaStream_t st);
+// A[r][c] += T[r][c] for c <= r < m (lower triangles, ld lda)
+cudaError_t launch_add_lower(double* A, const double* T, long long lda, long long m, cudaStream_t st);
 
 // a4 + a5: G = S^T (A S) (lower), g = S^T r, empty-bucket rule, Cholesky, solves; writes
 // sdelta[coord_e] = sign_e * delta[b_e].  Gx / delta are workspace.
@@ -232,25 +262,15 @@ cudaError_t launch_transpose(const double* X, long long ldx, long long rows, lon
                              long long ldxt, cudaStream_t st);
 cudaError_t launch_gram_xt(const double* XT, long long ldxt, long long rows, const DevSketch& sk,
                            double* partials, double* G, long long ldg, int num_sms,
-                           const Ctrl* ctrl, cudaStream_t st, int slot = 0,
-                           const long long* kbase = nullptr, bool lean = false);
-// *out = ctrl->k (a group's base iteration for kernels running beside the iterations)
-cudaError_t launch_snap_k(const Ctrl* ctrl, long long* out, cudaStream_t st);
+                           const Ctrl* ctrl, cudaStream_t st, int slot = 0);
 // v = S delta (dense, m); when the sketch and delta are given and d <= 2048, the row-owner kernel
 // forms <X_i, v> from the sketch entries only.
 cudaError_t launch_xpass(const double* X, long long ldx, long long rows, long long d,
                          const double* v, double* partials, double* u, int num_sms,
                          const Ctrl* ctrl, cudaStream_t st, const DevSketch* sk = nullptr,
-                         const double* delta = nullptr, bool lean = false);
+                         const double* delta = nullptr);
 // Fused gather + Gram (subsample, tau <= 200): G lower = sum_i X[i,C]^T X[i,C], no XS written.
 bool gram_fused_ok(int kind, int tau);
-// Fused X pass: u = X^T (X v) for this iteration AND the Gram (X S')^T (X S') of a future
-// subsample sketch S' (skg.tau == 0: none) from the same TMA-staged rows of X; d <= 3200.
-bool xpass_gram_ok(int kind, int tau, long long d, long long ldx);
-cudaError_t launch_xpass_gram(const double* X, long long ldx, long long rows, long long d,
-                              const double* v, double* upart, double* u, const DevSketch& skg,
-                              double* gpart, double* G, long long ldg, int num_sms,
-                              const Ctrl* ctrl, cudaStream_t st, int gofs);
 size_t gram_fused_partials(int num_sms);
 cudaError_t gram_init();
 cudaError_t launch_gram_fused(const double* X, long long ldx, long long rows, const DevSketch& sk,

@@ -100,8 +100,16 @@ k_sketch_select(DevSketch skb, uint2 key, const Ctrl* ctrl, long long fixed_k, l
   const unsigned n_eq = s_neq;
   if (tid == 0) { s_lesscount = 0; s_eqcount = 0; }
   __syncthreads();
-  if (n_eq > 1024) {   // astronomically unlikely with 64-bit Philox keys
-    if (tid == 0) atomicExch(err, 1);
+  if (n_eq > 1024) {   // astronomically unlikely with 64-bit Philox keys: fail the solve loudly
+    if (tid == 0) {
+      if (ctrl) {
+        Ctrl* c = const_cast<Ctrl*>(ctrl);
+        c->status = ST_SKETCHFAIL;
+        c->done = 1;
+      } else {
+        atomicExch(err, 1);   // rs_sketch_draw reads and clears it
+      }
+    }
     return;
   }
   for (int i = tid; i < m; i += kThreads) {
@@ -254,6 +262,14 @@ cudaError_t sketch_init() {
     if (e != cudaSuccess) return e;
     e = cudaMemset(g_err_flag, 0, sizeof(int));
   }
+  return e;
+}
+
+cudaError_t sketch_err_take(int* out) {
+  *out = 0;
+  if (!g_err_flag) return cudaSuccess;
+  cudaError_t e = cudaMemcpy(out, g_err_flag, sizeof(int), cudaMemcpyDeviceToHost);
+  if (e == cudaSuccess && *out) e = cudaMemset(g_err_flag, 0, sizeof(int));
   return e;
 }
 

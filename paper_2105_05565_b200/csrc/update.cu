@@ -410,10 +410,7 @@ cudaError_t launch_update_rows(const double* A, long long lda, const DevSketch& 
   const long long cb = (m + RW_COLS - 1) / RW_COLS;
   // splits (one cluster per column block): about two blocks per SM in total (128 registers per
   // thread), at least 4 rows per warp, at most the portable cluster size
-  static const long long bps = [] {   // blocks per SM targeted (RS_UR_BPS overrides, sweeps)
-    const char* e = std::getenv("RS_UR_BPS");
-    return e ? std::max(1, atoi(e)) : 4;
-  }();
+  const long long bps = 4;   // blocks per SM targeted
   long long ns = (bps * num_sms + cb / 2) / cb;   // ~4 blocks per SM (8 / 16 / 32 measured slower
                                                   // on c4: 55 / 68 / 68 vs 54 us)
   ns = std::min<long long>(ns, (sk.len + 4 * RW_Y - 1) / (4 * RW_Y));   // >= 4 rows per warp

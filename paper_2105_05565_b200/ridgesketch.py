@@ -38,7 +38,8 @@ KERNEL_CLASSES = ("sketch", "xs", "as", "solve", "update", "gram", "pre", "facto
 class rs_dist(C.Structure):
     _fields_ = [("device", C.c_int), ("rank", C.c_int), ("world", C.c_int),
                 ("nccl_unique_id", C.c_void_p), ("cuda_stream", C.c_void_p),
-                ("shard_begin", C.c_int64), ("shard_len", C.c_int64)]
+                ("shard_begin", C.c_int64), ("shard_len", C.c_int64), ("collective", C.c_int)]
+COLLECTIVES = {"nccl": 0, "host": 1}
 
 
 class rs_solve_opts(C.Structure):
@@ -76,6 +77,7 @@ _lib.rs_shard_range.argtypes = [C.c_int64, C.c_int, C.c_int, C.POINTER(C.c_int64
 _lib.rs_shard_rows_nnz.argtypes = [C.c_int64, _P, C.c_int, C.c_int, C.POINTER(C.c_int64),
                                    C.POINTER(C.c_int64)]
 _lib.rs_nccl_unique_id.argtypes = [_P]
+_lib.rs_host_coll_id.argtypes = [_P]
 _lib.rs_destroy.argtypes = [_P]
 _lib.rs_destroy.restype = None
 _lib.rs_status_string.argtypes = [C.c_int]
@@ -83,7 +85,8 @@ _lib.rs_status_string.restype = C.c_char_p
 _lib.rs_last_error.restype = C.c_char_p
 _lib.rs_abi_version.restype = C.c_int
 for _f in ("rs_create_dense", "rs_create_csr", "rs_solve", "rs_get_state", "rs_get_info",
-           "rs_sketch_draw", "rs_shard_range", "rs_shard_rows_nnz", "rs_nccl_unique_id"):
+           "rs_sketch_draw", "rs_shard_range", "rs_shard_rows_nnz", "rs_nccl_unique_id",
+           "rs_host_coll_id"):
     getattr(_lib, _f).restype = C.c_int
 
 
@@ -150,6 +153,7 @@ def _dist(dist):
     d.cuda_stream = dist.get("cuda_stream") or None
     d.shard_begin = dist.get("shard_begin", 0)
     d.shard_len = dist["shard_len"]
+    d.collective = COLLECTIVES[dist.get("collective", "nccl")]
     return d
 
 
@@ -302,6 +306,13 @@ def rs_shard_rows_nnz(rowptr, rank, world):
 def rs_nccl_unique_id():
     buf = C.create_string_buffer(128)
     _check(_lib.rs_nccl_unique_id(buf), "rs_nccl_unique_id")
+    return buf.raw
+
+
+def rs_host_coll_id():
+    """128-byte name of a fresh host-staged collective group (rs_dist collective "host")."""
+    buf = C.create_string_buffer(128)
+    _check(_lib.rs_host_coll_id(buf), "rs_host_coll_id")
     return buf.raw
 
 

@@ -40,7 +40,7 @@ def test_library_exports_every_declared_symbol(rs):
 
 
 def test_abi_version_and_status_strings(rs):
-    assert rs.rs_abi_version() == 2
+    assert rs.rs_abi_version() == 3
     assert rs.rs_status_string(0) == "RS_OK"
     for s in range(1, 8):
         assert rs.rs_status_string(s).startswith("RS_E")
@@ -102,3 +102,12 @@ def test_no_cpu_fallback_without_gpu(rs):
     with pytest.raises(rs.RSError) as e:
         rs.rs_sketch_draw("subsample", 10, 3, 0, 0)
     assert e.value.status == rs.RS_ECUDA
+
+
+def test_host_coll_id(rs):
+    """Group names of the host-staged collective (RS_COLL_HOST): distinct, NUL-terminated, a POSIX
+    shared-memory name (leading '/', no other '/')."""
+    a, b = rs.rs_host_coll_id(), rs.rs_host_coll_id()
+    assert a != b and len(a) == 128
+    name = a.split(b"\0")[0].decode()
+    assert name.startswith("/") and "/" not in name[1:] and 1 < len(name) < 100

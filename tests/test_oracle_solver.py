@@ -234,3 +234,26 @@ def test_tolerance_stop_rule():
     assert res["converged"]
     tr = res["trace"]
     assert tr[-1] <= 1e-6 and all(t > 1e-6 for t in tr[:-1])
+
+
+def test_extended_precision_oracle_matches_fp64_on_well_conditioned():
+    """solve_system_ld (np.longdouble Alg. 2, hand-written Cholesky) agrees with the fp64 oracle to
+    ~1e-14 on a well-conditioned explicit system, and its Cholesky solve reproduces
+    numpy.linalg.solve on a random SPD matrix: pins the extended-precision reference that the
+    ill-conditioned kernel-ridge GPU case is compared against."""
+    import numpy as np
+    from oracle import problem as P
+    from oracle import solver as OV
+    rng = np.random.default_rng(3)
+    M = rng.standard_normal((30, 30))
+    G = M @ M.T + 30 * np.eye(30)
+    g = rng.standard_normal(30)
+    x = OV.cholesky_solve_ld(G, g)
+    assert np.allclose(np.asarray(x, dtype=np.float64), np.linalg.solve(G, g), rtol=1e-13, atol=0)
+    X = rng.standard_normal((200, 12))
+    y = rng.standard_normal(200)
+    pr = P.build(X, y, 0.7)
+    ref = OV.solve_momentum(OV.Operator.from_system(pr["A"], pr["b"]), "count", 5, 1.0, 0.5, 0.0, 25, seed=2)
+    ld = OV.solve_system_ld(pr["A"], pr["b"], "count", 5, 1.0, 0.5, 25, seed=2)
+    w = np.asarray(ld["w"], dtype=np.float64)
+    assert np.linalg.norm(w - ref["w"]) <= 1e-13 * np.linalg.norm(ref["w"])
