@@ -33,8 +33,10 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 # AS route of each config's line: the one with the shortest measured time to tolerance (DESIGN.md
-# §9); c5's GRAM / IMPLICIT routes are measured beside it (`alt_routes`)
-DEFAULT_MODE = {"c1": "gram", "c2": "gram", "c3": "gram", "c4": "gram", "c5": "explicit",
+# §9); the dense configs' other routes are measured beside it (`alt_routes`).  c4 (CSR dual):
+# EXPLICIT through the sparse A build (NEXT-3) -- 4.4x faster per iteration than the selected-row
+# GRAM path in round 1 (14.2k vs 3.2k iters/s), and 0.67 + 0.3 s vs 3.05 s to 1e-4.
+DEFAULT_MODE = {"c1": "gram", "c2": "gram", "c3": "gram", "c4": "explicit", "c5": "explicit",
                 "k1": "explicit"}
 METRIC = "sketch-and-project iters/s & s to ‖r‖/‖b‖≤1e-4; AS-pass HBM GB/s vs peak"
 FP64_DMMA_PEAK = 37.1   # TFLOP/s, measured on this pool's B200 (profiles/r01_fp64_peak.txt)

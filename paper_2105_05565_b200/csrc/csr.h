@@ -30,7 +30,8 @@ struct CsrData {
   int nbands = 0, nchunks = 0;
   double* gpart = nullptr;       // [nchunks][tau (tau + 1) / 2] packed lower-triangle partials
   long long gpart_stride = 0;
-  double* gtrace = nullptr;      // trace(G) of the current slot's merged rows (fixed-point scale)
+  double* fsc = nullptr;         // per-bucket fixed-point scales 2^e_b of the current slot's Gram
+  double* cnorm = nullptr;       // column norms of R (static; bounds of the bucket columns of R S)
   double* tvec = nullptr;        // [R rows]  t = R (S delta)
   // rows longer than `heavy` are handled one CTA per row (Zipf-popular features of c4)
   long long heavyR = 0, heavyRt = 0;

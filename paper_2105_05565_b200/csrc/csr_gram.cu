@@ -51,8 +51,8 @@ struct WarpMerge {
   double* stage;
   unsigned* bits;
   int nw;
-  double sq = 0.0;   // lane-local sum of squares of the flushed values (trace of the row Grams)
-  __device__ WarpMerge(double* hsm, int tau, int w) {
+  const double* fsc;   // per-bucket fixed-point scale 2^e_b of the slot (k_bucket_scale)
+  __device__ WarpMerge(double* hsm, int tau, int w, const double* f) : fsc(f) {
     nw = (tau + 31) >> 5;
     acc = hsm + (size_t)w * tau;
     stage = hsm + (size_t)HR_WARPS * tau + w * 32;
@@ -75,8 +75,8 @@ struct WarpMerge {
     }
     __syncwarp();
   }
-  // write the touched buckets in ascending order to hb/hv at `a`, clear; returns the count
-  template <bool SQ = true>
+  // write the touched buckets in ascending order to hb/hv at `a` (values pre-scaled by the bucket's
+  // 2^e_b: exact), clear; returns the count
   __device__ __forceinline__ int flush(long long a, int* hb, double* hv, int lane) {
     int total = 0;
     for (int w0 = 0; w0 < nw; w0 += 32) {
@@ -92,10 +92,8 @@ struct WarpMerge {
       long long pos = a + total + incl - c;
       for (; word; word &= word - 1) {
         const int bucket = wi * 32 + __ffs(word) - 1;
-        const double x = acc[bucket];
         hb[pos] = bucket;
-        hv[pos] = x;
-        if (SQ) sq += x * x;
+        hv[pos] = acc[bucket] * fsc[bucket];
         ++pos;
       }
       if (wi < nw) bits[wi] = 0u;
@@ -104,45 +102,19 @@ struct WarpMerge {
     __syncwarp();
     return total;
   }
-  // the warp's share of trace(G) = sum over flushed entries of v^2 (one fp64 atomic per warp)
-  __device__ __forceinline__ void trace_out(double* gtr, int lane) {
-#pragma unroll
-    for (int o = 16; o; o >>= 1) sq += __shfl_xor_sync(FULL, sq, o);
-    if (lane == 0 && sq != 0.0) atomicAdd(gtr, sq);
-  }
-  // the block's share: warps reduced in shared memory, one fp64 atomic per block (every thread of
-  // the block calls it; ~1e4 same-address atomics per launch serialise at L2)
-  __device__ __forceinline__ void trace_out_block(double* gtr, int lane, int warp) {
-    __shared__ double red[HR_WARPS];
-#pragma unroll
-    for (int o = 16; o; o >>= 1) sq += __shfl_xor_sync(FULL, sq, o);
-    if (lane == 0) red[warp] = sq;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      double t = 0.0;
-      for (int w = 0; w < HR_WARPS; ++w) t += red[w];
-      if (t != 0.0) atomicAdd(gtr, t);
-    }
-  }
 };
 
 // Fixed-point accumulation of the CSR Gram bands (sm_100a has no native shared fp64 add; 32-bit
 // shared atomics are native): an entry is an int64 in units of 2^-E, added as two 32-bit words
 // with the carry of the low word taken from the value the low-word atomic returns.  Two's
-// complement addition is exact modulo 2^64, so the result is exact whenever the final value fits:
-// |G_ab| <= max_a G_aa <= trace(G) < 2^(ilogb(trace) + 1) and E = 61 - ilogb(trace) leave two bits
-// of headroom.  Each product is rounded once to 2^-E = trace * 2^-61 (about 2^-53 of a diagonal
-// entry for tau = 500); the sum itself is exact and order independent.
+// complement addition is exact modulo 2^64, so the result is exact whenever the final value fits,
+// which the per-bucket scales of k_bucket_scale guarantee (|G_ab| 2^(e_a + e_b) < 2^61).  Each
+// product is rounded once; the sum itself is exact and order independent.
 __device__ __forceinline__ void fx_add(unsigned* w, long long x) {
   const unsigned lo = (unsigned)x;
   const unsigned old = atomicAdd(w, lo);
   const int h = (int)(x >> 32) + (old + lo < old ? 1 : 0);
   if (h) atomicAdd(reinterpret_cast<int*>(w) + 1, h);
-}
-__device__ __forceinline__ int fx_exponent(double trace) {
-  // clamped so that 2^E and 2^-E are finite normal numbers (|log2 trace| < ~960 for any data
-  // whose Gram is representable)
-  return trace > 0.0 && isfinite(trace) ? max(-1021, min(1022, 61 - ilogb(trace))) : 0;
 }
 
 __device__ __forceinline__ int cm_of(const int* __restrict__ cmap, const int* __restrict__ idx,
@@ -159,11 +131,11 @@ __global__ void __launch_bounds__(HR_WARPS * 32)
 k_hash_rows(const long long* __restrict__ ptr, const int* __restrict__ idx,
             const double* __restrict__ val, long long rows, long long heavy, const int* __restrict__ cmap,
             int tau, int* __restrict__ hb, double* __restrict__ hv, int* __restrict__ hcnt,
-            int slot, const Ctrl* ctrl, double* __restrict__ gtr) {
+            int slot, const Ctrl* ctrl, const double* __restrict__ fsc) {
   if (slot_unused(ctrl, slot)) return;
   extern __shared__ double hsm[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  WarpMerge M(hsm, tau, warp);
+  WarpMerge M(hsm, tau, warp, fsc);
   for (int q = lane; q < M.nw; q += 32) M.bits[q] = 0u;
   __syncwarp();
   const long long nwarps = (long long)gridDim.x * HR_WARPS;
@@ -228,7 +200,6 @@ k_hash_rows(const long long* __restrict__ ptr, const int* __restrict__ idx,
       if (lane == 0) hcnt[i0 + j] = total;
     }
   }
-  M.trace_out_block(gtr, lane, warp);
 }
 
 // heavy rows: one CTA per row; warp w merges chunks w, w + 8, ... into its own accumulator, then the
@@ -238,11 +209,11 @@ k_hash_rows_heavy(const long long* __restrict__ ptr, const int* __restrict__ idx
                   const double* __restrict__ val, const int* __restrict__ heavy_rows,
                   const int* __restrict__ cmap, int tau, int* __restrict__ hb,
                   double* __restrict__ hv, int* __restrict__ hcnt, int slot, const Ctrl* ctrl,
-                  double* __restrict__ gtr) {
+                  const double* __restrict__ fsc) {
   if (slot_unused(ctrl, slot)) return;
   extern __shared__ double hsm[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  WarpMerge M(hsm, tau, warp);
+  WarpMerge M(hsm, tau, warp, fsc);
   for (int q = lane; q < M.nw; q += 32) M.bits[q] = 0u;
   __syncwarp();
   const long long i = heavy_rows[blockIdx.x];
@@ -256,12 +227,12 @@ k_hash_rows_heavy(const long long* __restrict__ ptr, const int* __restrict__ idx
   __syncthreads();
   // sum the warps' accumulators into warp 0's (thread owns bucket b; other threads only set
   // other bits of warp 0's words, so the read of bit b is race free)
-  WarpMerge M0(hsm, tau, 0);
+  WarpMerge M0(hsm, tau, 0, fsc);
   for (int b = threadIdx.x; b < tau; b += HR_WARPS * 32) {
     double s = 0.0;
     bool any = false;
     for (int w = 0; w < HR_WARPS; ++w) {
-      WarpMerge Mw(hsm, tau, w);
+      WarpMerge Mw(hsm, tau, w, fsc);
       if (Mw.bits[b >> 5] & (1u << (b & 31))) {
         s += Mw.acc[b];
         any = true;
@@ -274,7 +245,6 @@ k_hash_rows_heavy(const long long* __restrict__ ptr, const int* __restrict__ idx
   if (warp == 0) {
     const int total = M.flush(a, hb, hv, lane);
     if (lane == 0) hcnt[i] = total;
-    M.trace_out(gtr, lane);
   }
 }
 
@@ -295,7 +265,7 @@ k_sel_emit(DevSketch sk, const long long* __restrict__ rowptr, const int* __rest
            const double* __restrict__ vals, const int* __restrict__ cscpos, int* __restrict__ cmR,
            int* __restrict__ tflag, int* __restrict__ tlist, int* __restrict__ tcount,
            const int* __restrict__ hidx, double* __restrict__ hacc, long long ldh, int slot,
-           const Ctrl* ctrl, double* __restrict__ gtr) {
+           const Ctrl* ctrl) {
   if (slot_unused(ctrl, slot)) return;
   const int lane = threadIdx.x & 31;
   const int e = blockIdx.x * SE_WARPS + (threadIdx.x >> 5);
@@ -305,7 +275,6 @@ k_sel_emit(DevSketch sk, const long long* __restrict__ rowptr, const int* __rest
   const bool neg = sk.sign[e] <= 0;
   const int code = (b << 1) | (neg ? 1 : 0);
   const long long p1 = rowptr[i + 1];
-  double sq = 0.0;   // squares of the light entries: trace bound for the fixed-point Gram
   for (long long pb = rowptr[i]; pb < p1; pb += 32 * SE_U) {   // warp-uniform trip count
     int f[SE_U], h[SE_U];
 #pragma unroll
@@ -327,8 +296,6 @@ k_sel_emit(DevSketch sk, const long long* __restrict__ rowptr, const int* __rest
         continue;
       }
       cmR[cscpos[p]] = code;
-      const double x = vals[p];
-      sq += x * x;
       need[u] = tflag[f[u]] == 0 && atomicExch(&tflag[f[u]], 1) == 0;
     }
 #pragma unroll
@@ -342,23 +309,17 @@ k_sel_emit(DevSketch sk, const long long* __restrict__ rowptr, const int* __rest
       if (need[u]) tlist[base + __popc(m & ((1u << lane) - 1u))] = f[u];
     }
   }
-  // trace(G_light) = sum_f sum_b (sum_{e in (f, b)} sign_e x_e)^2 <= kmax sum_e x_e^2 (Cauchy-
-  // Schwarz; kmax = entries of one bucket: k for SubCount, 1 for subsample): an upper bound, so the
-  // fixed-point range holds; over-estimating by <= kmax costs log2(kmax) bits of resolution
-#pragma unroll
-  for (int o = 16; o; o >>= 1) sq += __shfl_xor_sync(FULL, sq, o);
-  if (lane == 0 && sq != 0.0) atomicAdd(gtr, sq * (double)max(1, sk.ksum));
 }
 
 __global__ void __launch_bounds__(HR_WARPS * 32)
 k_sel_merge(const long long* __restrict__ ptr, const double* __restrict__ val, long long heavy,
             int* __restrict__ cmR, int* __restrict__ tflag, const int* __restrict__ tlist,
             const int* __restrict__ tcount, int tau, int* __restrict__ hb, double* __restrict__ hv,
-            int* __restrict__ hcnt, int slot, const Ctrl* ctrl) {
+            int* __restrict__ hcnt, int slot, const Ctrl* ctrl, const double* __restrict__ fsc) {
   if (slot_unused(ctrl, slot)) return;
   extern __shared__ double hsm[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  WarpMerge M(hsm, tau, warp);
+  WarpMerge M(hsm, tau, warp, fsc);
   for (int q = lane; q < M.nw; q += 32) M.bits[q] = 0u;
   __syncwarp();
   const int nt = *tcount;
@@ -377,7 +338,7 @@ k_sel_merge(const long long* __restrict__ ptr, const double* __restrict__ val, l
       if (cm0 >= 0) cmR[t0] = -1;
       if (cm1 >= 0) cmR[t1] = -1;
     }
-    const int total = M.template flush<false>(a, hb, hv, lane);
+    const int total = M.flush(a, hb, hv, lane);
     if (lane == 0) hcnt[f] = total;
   }
 }
@@ -408,8 +369,7 @@ k_gram_bands(const long long* __restrict__ ptr, const int* __restrict__ hcnt,
              const int* __restrict__ band_a0, const long long* __restrict__ chunk_r0,
              long long heavy, const int* __restrict__ heavy_rows, const int* __restrict__ chunk_h0,
              double* __restrict__ part, long long part_stride, int slot, const Ctrl* ctrl,
-             const int* __restrict__ rlist, const int* __restrict__ rcount, int sz_cap,
-             const double* __restrict__ gtr) {
+             const int* __restrict__ rlist, const int* __restrict__ rcount, int sz_cap) {
   // rlist (optional): visit only the listed rows (the touched rows of the selected-row path),
   // chunk y taking list entries [y n / nchunks, (y + 1) n / nchunks)
   if (slot_unused(ctrl, slot)) return;
@@ -417,9 +377,9 @@ k_gram_bands(const long long* __restrict__ ptr, const int* __restrict__ hcnt,
   const int a0 = band_a0[blockIdx.x], a1 = band_a0[blockIdx.x + 1];
   const long long base = tri(a0);
   const int sz = (int)(tri(a1) - base);
-  // the band holds int64 fixed-point entries (fx_add); trace(G) of this slot's merged rows
-  const int E = fx_exponent(*gtr);
-  const double sc = ldexp(1.0, E);
+  // the band holds int64 fixed-point entries (fx_add); the merged values carry their bucket's scale
+  // 2^e_b (k_bucket_scale), so a product is already in units of 2^-(e_a + e_b)
+  const double sc = 1.0;
   unsigned* bw = reinterpret_cast<unsigned*>(band);
   long long* bl = reinterpret_cast<long long*>(band);
   for (int q = threadIdx.x; q < sz; q += GB_THREADS) bl[q] = 0;
@@ -555,24 +515,75 @@ k_gram_bands(const long long* __restrict__ ptr, const int* __restrict__ hcnt,
     }
   }
   __syncthreads();
-  double* out = part + blockIdx.y * part_stride + base;
-  const double isc = ldexp(1.0, -E);
-  for (int q = threadIdx.x; q < sz; q += GB_THREADS) out[q] = (double)bl[q] * isc;
+  double* out = part + blockIdx.y * part_stride + base;   // scaled units (k_gram_band_reduce)
+  for (int q = threadIdx.x; q < sz; q += GB_THREADS) out[q] = (double)bl[q];
 }
 
 __global__ void k_gram_band_reduce(const double* __restrict__ part, int nchunks,
                                    long long part_stride, double* __restrict__ G, long long ldg,
                                    int slot, const Ctrl* ctrl, const double* __restrict__ gh,
-                                   double* __restrict__ gtr) {
+                                   const double* __restrict__ fsc) {
   if (slot_unused(ctrl, slot)) return;
-  if (blockIdx.x == 0 && threadIdx.x == 0) *gtr = 0.0;   // consumed by k_gram_bands (stream order)
   const int a = blockIdx.x;
   const long long base = tri(a);
+  const double ia = 1.0 / fsc[a];   // powers of two: exact
   for (int c = threadIdx.x; c <= a; c += blockDim.x) {
-    double s = gh ? gh[(long long)a * ldg + c] : 0.0;   // heavy rows' H^T H (same ld as G)
+    double s = 0.0;
     for (int k = 0; k < nchunks; ++k) s += part[k * part_stride + base + c];
+    s *= ia * (1.0 / fsc[c]);
+    if (gh) s += gh[(long long)a * ldg + c];   // heavy rows' H^T H (true units, same ld as G)
     G[(long long)a * ldg + c] = s;
   }
+}
+
+// Column norms of R (rows of R^T), one warp per row in lane order: the static input of the
+// per-bucket fixed-point scales.  With rptr (the CSR row pointer of R) the entries of heavy rows of
+// R (longer than `heavy`) are left out: on the dual selected-row path those rows go to dense
+// tau-vectors in fp64 (H^T H on DMMA), not into the fixed-point bands.
+__global__ void k_row_norms(const long long* __restrict__ ptr, const int* __restrict__ idx,
+                            const double* __restrict__ val, long long rows,
+                            const long long* __restrict__ rptr, long long heavy,
+                            double* __restrict__ out) {
+  const long long r = (long long)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (r >= rows) return;
+  double s = 0.0;
+  for (long long q = ptr[r] + lane; q < ptr[r + 1]; q += 32) {
+    if (rptr) {
+      const long long i = idx[q];
+      if (rptr[i + 1] - rptr[i] > heavy) continue;
+    }
+    s += val[q] * val[q];
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(FULL, s, o);
+  if (lane == 0) out[r] = sqrt(s);
+}
+
+// Per-bucket fixed-point scale of the slot's Gram: column b of R S is sum_{e in b} sign_e R[:, c_e],
+// so G_bb <= B_b = (sum_{e in b} ||R[:, c_e]||)^2 (triangle inequality), and with
+// e_b = floor((60 - ilogb(B_b)) / 2), |G_ab| 2^(e_a + e_b) <= sqrt(B_a B_b) 2^(e_a + e_b) < 2^61
+// (Cauchy-Schwarz): every band entry fits the int64 with two bits to spare, and a product is
+// rounded to 2^-(e_a + e_b), about 2^-59 of sqrt(B_a B_b) -- relative to its own buckets, not to
+// trace(G) (one column scaled by 1e6 no longer costs the other buckets their precision).  The
+// bound depends on the sketch and on static norms only: deterministic, no pass over the data.
+__global__ void k_bucket_scale(DevSketch sk, const double* __restrict__ cn, double* __restrict__ fsc,
+                               int slot, const Ctrl* ctrl) {
+  if (slot_unused(ctrl, slot)) return;
+  const int b = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (b >= sk.tau) return;
+  double s = 0.0;
+  for (int e = sk.bptr[b] + lane; e < sk.bptr[b + 1]; e += 32) s += cn[sk.coord[e]];
+#pragma unroll
+  for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(FULL, s, o);
+  const double B = s * s;
+  int e = 0;
+  if (B > 0.0 && isfinite(B)) {
+    const int t = 60 - ilogb(B);
+    e = max(-480, min(480, t >= 0 ? t / 2 : -((1 - t) / 2)));   // floor(t / 2)
+  }
+  if (lane == 0) fsc[b] = ldexp(1.0, e);
 }
 
 // chunk boundaries: first row r with ptr[r] >= c * nnz / nchunks (nnz-balanced)
@@ -687,7 +698,10 @@ void Problem::csr_gram_free() {
   dfree(csr->band_a0);
   dfree(csr->chunk_r0);
   dfree(csr->gpart);
-  dfree(csr->gtrace);
+  dfree(csr->fsc);
+  dfree(csr->cnorm);
+  csr->fsc = nullptr;
+  csr->cnorm = nullptr;
   dfree(csr->tvec);
   dfree(csr->heavy_rowsR);
   dfree(csr->heavy_rowsRt);
@@ -772,8 +786,6 @@ rs_status Problem::csr_gram_workspace(int kind, int tau) {
   RS_CUDA(cudaGetLastError());
   c->gpart_stride = round_up(total, 4);
   RS_TRY(dalloc(&c->gpart, (size_t)c->gpart_stride * c->nchunks));
-  RS_TRY(dalloc(&c->gtrace, 1));
-  RS_CUDA(cudaMemsetAsync(c->gtrace, 0, sizeof(double), st));
   // heavy-row lists of R and R^T
   {
     const RView Rt = route == 1 ? RView{c->colptr, c->rowidx, c->cvals, c->cols}
@@ -831,6 +843,18 @@ rs_status Problem::csr_gram_workspace(int kind, int tau) {
       }
     }
   }
+  // per-bucket fixed-point scales (k_bucket_scale) from the column norms of R = rows of R^T
+  RS_TRY(dalloc(&c->fsc, tau));
+  RS_TRY(dalloc(&c->cnorm, std::max<long long>(1, m)));
+  {
+    const RView Rt = route == 1 ? RView{c->colptr, c->rowidx, c->cvals, c->cols}
+                                : RView{c->rowptr, c->colidx, c->vals, c->rows};
+    const bool light_only = route == 2 && c->cmR != nullptr;   // selected-row path (heavy: fp64)
+    if (Rt.rows > 0)
+      k_row_norms<<<(unsigned)((Rt.rows + 7) / 8), 256, 0, st>>>(
+          Rt.ptr, Rt.idx, Rt.val, Rt.rows, light_only ? R.ptr : nullptr, c->heavyR, c->cnorm);
+    RS_CUDA(cudaGetLastError());
+  }
   c->gb_smem = (size_t)maxband * sizeof(double);
   c->hr_smem = (size_t)HR_WARPS * (tau + 32) * sizeof(double) + (size_t)HR_WARPS * ((tau + 31) / 32) * 4;
   c->gb_cap = (int)round_up(maxband, 2);
@@ -857,6 +881,12 @@ rs_status Problem::csr_gram_workspace(int kind, int tau) {
   return RS_OK;
 }
 
+static cudaError_t launch_bucket_scale(const DevSketch& s, const double* cn, double* fsc, int slot,
+                                       const Ctrl* ctrl, cudaStream_t st) {
+  k_bucket_scale<<<(unsigned)((s.tau + 7) / 8), 256, 0, st>>>(s, cn, fsc, slot, ctrl);
+  return cudaGetLastError();
+}
+
 rs_status Problem::csr_gram_into(const DevSketch& s, double* G, cudaEvent_t* ev, int slot,
                                   bool reduce) {
   auto mark = [&](int cls, int edge) {
@@ -868,6 +898,7 @@ rs_status Problem::csr_gram_into(const DevSketch& s, double* G, cudaEvent_t* ev,
   const int tau = s.tau;
   const int* cmap = s.cmap;
   mark(RS_K_XS, 0);
+  RS_CUDA(launch_bucket_scale(s, c->cnorm, c->fsc, slot, ctrl, st));
   const bool sel = s.kind != SK_COUNT && c->cmR != nullptr;   // dual: from the selected samples
   if (s.kind != SK_COUNT && !sel) {
     RS_CUDA(launch_cmap_build(s, c->cmap_all, m, ctrl, st, slot));
@@ -877,11 +908,11 @@ rs_status Problem::csr_gram_into(const DevSketch& s, double* G, cudaEvent_t* ev,
     RS_CUDA(cudaMemsetAsync(c->hcnt, 0, R.rows * sizeof(int), st));
     k_sel_emit<<<(unsigned)std::max(1, (s.len + SE_WARPS - 1) / SE_WARPS), SE_WARPS * 32, 0, st>>>(
         s, c->rowptr, c->colidx, c->vals, c->cscpos, c->cmR, c->tflag, c->tlist, c->tcount, c->hidx,
-        c->hacc, c->ldh, slot, ctrl, c->gtrace);
+        c->hacc, c->ldh, slot, ctrl);
     const unsigned grid = (unsigned)((long long)num_sms * 8);
     k_sel_merge<<<grid, HR_WARPS * 32, c->hr_smem, st>>>(R.ptr, R.val, c->heavyR, c->cmR, c->tflag,
                                                          c->tlist, c->tcount, tau, c->hb, c->hv,
-                                                         c->hcnt, slot, ctrl);
+                                                         c->hcnt, slot, ctrl, c->fsc);
     if (c->nheavyR > 0) {   // heavy rows: H^T H on the lower DMMA tiles, then H cleared
       RS_CUDA(tma_gemm_launch(c->tg_heavy, c->gh, ld_gram, c->gh_work, ctrl, st));
       RS_CUDA(cudaMemsetAsync(c->hacc, 0, (size_t)c->nheavyR * c->ldh * sizeof(double), st));
@@ -892,10 +923,10 @@ rs_status Problem::csr_gram_into(const DevSketch& s, double* G, cudaEvent_t* ev,
         1, std::min<long long>((R.rows + HR_WARPS - 1) / HR_WARPS, (long long)num_sms * 8));
     (s.kind == SK_COUNT ? k_hash_rows<true> : k_hash_rows<false>)
         <<<grid, HR_WARPS * 32, c->hr_smem, st>>>(R.ptr, R.idx, R.val, R.rows, c->heavyR, cmap, tau,
-                                                  c->hb, c->hv, c->hcnt, slot, ctrl, c->gtrace);
+                                                  c->hb, c->hv, c->hcnt, slot, ctrl, c->fsc);
     if (c->nheavyR > 0)
       k_hash_rows_heavy<<<c->nheavyR, HR_WARPS * 32, c->hr_smem, st>>>(
-          R.ptr, R.idx, R.val, c->heavy_rowsR, cmap, tau, c->hb, c->hv, c->hcnt, slot, ctrl, c->gtrace);
+          R.ptr, R.idx, R.val, c->heavy_rowsR, cmap, tau, c->hb, c->hv, c->hcnt, slot, ctrl, c->fsc);
     RS_CUDA(cudaGetLastError());
   }
   if (R.rows > 0) {
@@ -907,11 +938,11 @@ rs_status Problem::csr_gram_into(const DevSketch& s, double* G, cudaEvent_t* ev,
         <<<dim3((unsigned)c->nbands, (unsigned)c->nchunks), GB_THREADS, c->gb_smem, st>>>(
         R.ptr, c->hcnt, c->hb, c->hv, c->band_a0, c->chunk_r0, c->heavyR, c->heavy_rowsR,
         hgemm ? c->chunk_h0_none : c->chunk_h0, c->gpart, c->gpart_stride, slot, ctrl,
-        sel ? c->tlist : nullptr, sel ? c->tcount : nullptr, c->gb_cap, c->gtrace);
+        sel ? c->tlist : nullptr, sel ? c->tcount : nullptr, c->gb_cap);
     RS_CUDA(cudaGetLastError());
     if (sel) RS_CUDA(cudaMemsetAsync(c->tcount, 0, sizeof(int), st));   // touched list consumed
     k_gram_band_reduce<<<tau, 256, 0, st>>>(c->gpart, c->nchunks, c->gpart_stride, G, ld_gram, slot,
-                                            ctrl, hgemm ? c->gh : nullptr, c->gtrace);
+                                            ctrl, hgemm ? c->gh : nullptr, c->fsc);
     RS_CUDA(cudaGetLastError());
   } else {
     mark(RS_K_XS, 1);

@@ -831,3 +831,37 @@ def test_explicit_streamed_host_build(rs):
     assert rep["iterations"] == 6
     assert_close(w, ref["w"], 1e-10)
     assert_close(r, ref["r"], 1e-10)
+
+
+@pytest.mark.parametrize("case", ["primal_count_col", "dual_subcount_row"])
+def test_csr_gram_uneven_scales(rs, case):
+    """CSR GRAM accumulates the Gram bands in int64 fixed point; the scale of each band entry comes
+    from its two buckets (k_bucket_scale), so one column of R scaled by 1e6 -- one bucket's
+    diagonal 1e12 times the others -- leaves the other buckets their full precision and the
+    iterates equal the oracle's within 1e-10 (advisor finding on the former trace(G) scale).
+    Primal: R = X, a column of X; dual: R = X^T, a sample (row of X).  (Scaling a feature of the
+    dual instead adds a rank-one 1e12 term across buckets: G itself becomes ill-conditioned, which
+    no accumulation precision can repair.)"""
+    if case.startswith("primal"):
+        n, d = 4000, 600
+        rp, ci, v, y = rsinputs.csr_uniform(n, d, 12, seed=1)
+        v = v.copy()
+        v[ci == 7] *= 1e6
+        kind, tau, k, lam = "count", 40, 0, 1e-2
+    else:
+        n, d = 300, 5000
+        rp, ci, v, y = rsinputs.csr_zipf(n, d, 40, a=1.1, seed=6)
+        v = v.copy()
+        v[rp[3]:rp[4]] *= 1e6                            # one sample
+        kind, tau, k, lam = "subcount", 16, 4, 1e-3
+    Xs = rsinputs.csr_to_scipy(rp, ci, v, n, d)
+    h = rs.rs_create_csr(n, d, rp, ci, v, y, lam, mode="gram")
+    try:
+        w, rep = rs.rs_solve(h, kind, tau, 1.0, 0.5, 0.0, 12, seed=2, subcount_k=k, d=d)
+        ws, r = rs.rs_get_state(h)
+    finally:
+        rs.rs_destroy(h)
+    ref = OV.solve(Xs, y, lam, kind, tau, 1.0, 0.5, 0.0, 12, seed=2, subcount_k=k)
+    assert rep["iterations"] == 12
+    assert_close(ws, ref["w"], 1e-10)
+    assert_close(r, ref["r"], 1e-10)
