@@ -119,10 +119,12 @@ typedef struct {
 } rs_dist;
 
 /* Create a problem from dense X (n x d, row-major, leading dimension ldx >= d) and y (n).
- * For world > 1, X_local / y are the rank's shard of rows (primal; y is the matching rows).
- * n, d are the GLOBAL dimensions.  The dual route (n < d) is served in EXPLICIT mode
- * on one GPU (A = X X^T + lambda I, n x n; rs_solve then returns w = X^T alpha);
- * IMPLICIT / GRAM or world > 1 with a dense dual route return RS_EUNSUPPORTED. */
+ * n, d are the GLOBAL dimensions.  Primal route: for world > 1, X_local / y are the rank's shard of
+ * rows (y the matching rows).  Dual route (n < d): X_local is the rank's block of columns
+ * [shard_begin, shard_begin + shard_len) (n x shard_len, ld ldx) and y is whole; EXPLICIT builds
+ * A = X X^T + lambda I (one GPU), IMPLICIT / GRAM run the primal machinery on R = X^T (A = R^T R +
+ * lambda I, feature shards = row shards of R); rs_solve returns w = X^T alpha.  GRAM needs
+ * m <= 4096 (m = d primal, n dual). */
 rs_status rs_create_dense(rs_problem* out, int64_t n, int64_t d, const double* X_local,
                           int64_t ldx, const double* y, double lambda, rs_route route,
                           rs_as_mode mode, rs_mem mem, const rs_dist* dist);

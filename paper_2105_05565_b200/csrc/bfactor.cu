@@ -892,6 +892,21 @@ k_bfactor_lp(FactorSrc src, DevSketch skb, double* __restrict__ Ginv, long long 
     acc_store(t32, T(i, p0 + 1), tp, lane);
     __syncwarp();
   };
+  // a finished W tile (I, J) (src: 32 x 32 row-major, ld lds, shared or global) into the slot: W in
+  // its lower triangle, W^T in its upper triangle, both row-contiguous (coalesced both ways)
+  double* Gi = Ginv + slot * gi_stride;
+  auto emit_w = [&](int I, int J, const double* src, int lds) {
+#pragma unroll 4
+    for (int rr = 0; rr < 32; ++rr) {
+      const int row = 32 * I + rr, col = 32 * J + lane;
+      if (row < tau && col <= row) Gi[(long long)row * ldgi + col] = src[rr * lds + lane];
+    }
+#pragma unroll 4
+    for (int rr = 0; rr < 32; ++rr) {   // row 32 J + rr of the upper triangle: W[32 I + lane][32 J + rr]
+      const int row = 32 * J + rr, col = 32 * I + lane;
+      if (row < tau && col < tau && col > row) Gi[(long long)row * ldgi + col] = src[lane * lds + rr];
+    }
+  };
   // finish inverse strip I of pair (J0, J1) from acc = [T_I,J0 T_I,J1]:
   //   W_I,J1 = -T_I,J1 W_J1J1,  W_I,J0 = -(T_I,J0 + W_I,J1 L_J1,J0) W_J0J0
   auto finish_inv = [&](int I, int J0) {
@@ -902,6 +917,8 @@ k_bfactor_lp(FactorSrc src, DevSketch skb, double* __restrict__ Ginv, long long 
     __syncwarp();
     acc_store(t32, S, PLD, lane);
     acc_store(t32, T(I, J0 + 1), tp, lane);
+    __syncwarp();
+    emit_w(I, J0 + 1, S, PLD);
 #pragma unroll
     for (int R = 0; R < 4; ++R)
 #pragma unroll
@@ -917,6 +934,10 @@ k_bfactor_lp(FactorSrc src, DevSketch skb, double* __restrict__ Ginv, long long 
     acc_zero(t32);
     mma_tile<false, false>(t32, S, PLD, P3, PLD, lane, -1.0);       // W_I,J0
     acc_store(t32, T(I, J0), tp, lane);
+    __syncwarp();
+    acc_store(t32, S, PLD, lane);
+    __syncwarp();
+    emit_w(I, J0, S, PLD);
     __syncwarp();
   };
 
@@ -1073,38 +1094,14 @@ k_bfactor_lp(FactorSrc src, DevSketch skb, double* __restrict__ Ginv, long long 
       }
     }
     __syncthreads();
+    if (warp == 0) emit_w(J1, J0, T(J1, J0), tp);                 // W_J1,J0
+    else if (warp == 1) emit_w(J0, J0, P3, PLD);                  // W_J0J0
+    else if (warp == 2) emit_w(J1, J1, P3 + 2 * PT, PLD);         // W_J1J1
     BF_T(t_i1);
     BF_ADD(6, t_i0, t_i1);
   }
   BF_T(t_w0);
   BF_ADD(5, t_c1, t_w0);
-  // ---- the slot receives W (lower triangle) and W^T (upper triangle), both row-contiguous:
-  // tile (I, J), J <= I, goes to Gi[I][J] and, transposed through a per-warp shared tile, to
-  // Gi[J][I] (coalesced both ways)
-  double* Gi = Ginv + slot * gi_stride;
-  double* tt = lp_sm + warp * (32 * 33);
-  const int ntile = Tc * (Tc + 1) / 2;
-  for (int t = warp; t < ntile; t += LP_WARPS) {
-    int I, J;
-    tri_decode(t, I, J);
-    if (32 * J >= tau) continue;
-    double xr[32];   // the whole tile in flight first: 32 independent loads per lane
-#pragma unroll
-    for (int rr = 0; rr < 32; ++rr) xr[rr] = T(I, J)[(long long)rr * tp + lane];
-#pragma unroll
-    for (int rr = 0; rr < 32; ++rr) {
-      const int row = 32 * I + rr, col = 32 * J + lane;
-      const double x = (row < tau && col <= row) ? xr[rr] : 0.0;
-      tt[rr * 33 + lane] = x;
-      if (row < tau && col <= row) Gi[(long long)row * ldgi + col] = x;
-    }
-    __syncwarp();
-    for (int rr = 0; rr < 32; ++rr) {   // row 32 J + rr of the upper triangle: W[32 I + lane][32 J + rr]
-      const int row = 32 * J + rr, col = 32 * I + lane;
-      if (row < tau && col < tau && col > row) Gi[(long long)row * ldgi + col] = tt[lane * 33 + rr];
-    }
-    __syncwarp();
-  }
   BF_T(t_w1);
   BF_ADD(7, t_w0, t_w1);
   if (tid == 0) flags[slot] = 0;

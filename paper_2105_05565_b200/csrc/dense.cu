@@ -41,6 +41,68 @@ __global__ void k_dense_xs(const double* __restrict__ X, long long ldx, long lon
   }
 }
 
+// a2 with the sketch staged in shared memory (coord with the sign folded in as bit complement, and
+// the bucket pointers): one warp per row (XW_ROWS rows per warp in flight), lane b takes buckets
+// b, b + 32, ...; a subsample bucket is one independent gather, so a row of tau = 1024 is 32
+// gathers per lane in flight instead of a bptr -> coord -> X chain per element.  Rows are written
+// whole (lanes on consecutive buckets: coalesced), the padding columns tau .. ld_xs zeroed.
+constexpr int XW_WARPS = 8, XW_ROWS = 2;
+constexpr size_t XW_SMEM = 48 * 1024;
+__global__ void __launch_bounds__(XW_WARPS * 32)
+k_dense_xs_warp(const double* __restrict__ X, long long ldx, long long rows, DevSketch sk,
+                double* __restrict__ XS, long long ld_xs, const Ctrl* ctrl, int slot) {
+  if (slot_unused(ctrl, slot)) return;
+  extern __shared__ int xw_sm[];
+  int* s_bp = xw_sm;
+  int* s_ce = xw_sm + sk.tau + 1;
+  const int tau = sk.tau, len = sk.len;
+  for (int b = threadIdx.x; b <= tau; b += blockDim.x) s_bp[b] = sk.bptr[b];
+  for (int e = threadIdx.x; e < len; e += blockDim.x) s_ce[e] = sk.sign[e] > 0 ? sk.coord[e] : ~sk.coord[e];
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const bool single = len == tau;   // subsample: one entry per bucket
+  for (long long i0 = ((long long)blockIdx.x * XW_WARPS + warp) * XW_ROWS; i0 < rows;
+       i0 += (long long)gridDim.x * XW_WARPS * XW_ROWS) {
+    for (int b0 = 0; b0 < ld_xs; b0 += 32 * 16) {   // 16 buckets per lane per pass
+      double v[XW_ROWS][16];
+#pragma unroll
+      for (int r = 0; r < XW_ROWS; ++r) {
+        const long long i = i0 + r;
+        const double* xr = X + (i < rows ? i : 0) * ldx;
+#pragma unroll
+        for (int u = 0; u < 16; ++u) {
+          const int b = b0 + lane + 32 * u;
+          double x = 0.0;
+          if (i < rows && b < tau) {
+            if (single) {
+              const int ce = s_ce[b];
+              x = __ldg(xr + (ce >= 0 ? ce : ~ce));
+              if (ce < 0) x = -x;
+            } else {
+              for (int e = s_bp[b]; e < s_bp[b + 1]; ++e) {
+                const int ce = s_ce[e];
+                const double y = __ldg(xr + (ce >= 0 ? ce : ~ce));
+                x += ce >= 0 ? y : -y;
+              }
+            }
+          }
+          v[r][u] = x;
+        }
+      }
+#pragma unroll
+      for (int r = 0; r < XW_ROWS; ++r) {
+        const long long i = i0 + r;
+        if (i >= rows) break;
+#pragma unroll
+        for (int u = 0; u < 16; ++u) {
+          const int b = b0 + lane + 32 * u;
+          if (b < ld_xs) XS[i * ld_xs + b] = v[r][u];
+        }
+      }
+    }
+  }
+}
+
 __global__ void k_explicit_rows(const double* __restrict__ A, long long lda, long long m,
                                 DevSketch sk, double* __restrict__ ASt, long long ld_as,
                                 long long as_stride, const Ctrl* ctrl) {
@@ -304,6 +366,17 @@ cudaError_t launch_dense_xs(const double* X, long long ldx, long long rows, cons
                             double* XS, long long ld_xs, const Ctrl* ctrl, cudaStream_t st,
                             int slot) {
   if (rows <= 0) return cudaSuccess;
+  const size_t smem = (size_t)(sk.len + sk.tau + 1) * 4;
+  if (smem <= XW_SMEM) {   // sketch staged per block, warp-owned rows, independent gathers
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const long long blocks = std::min<long long>((rows + XW_WARPS * XW_ROWS - 1) / (XW_WARPS * XW_ROWS),
+                                                 (long long)sms * 8);
+    k_dense_xs_warp<<<(unsigned)std::max(1LL, blocks), XW_WARPS * 32, smem, st>>>(X, ldx, rows, sk, XS,
+                                                                                  ld_xs, ctrl, slot);
+    return cudaGetLastError();
+  }
   const int rpb = (int)std::max<long long>(1, 2048 / ld_xs);
   const long long grid = (rows + rpb - 1) / rpb;
   k_dense_xs<<<(unsigned)grid, 256, 0, st>>>(X, ldx, rows, sk, XS, ld_xs, rpb, ctrl, slot);

@@ -38,6 +38,7 @@ Problem::~Problem() {
   if (ev_fork) cudaEventDestroy(ev_fork);
   if (ev_join) cudaEventDestroy(ev_join);
   if (own_X) dfree(X);
+  if (own_Xo) dfree(Xo);
   dfree(y);
   dfree(b);
   dfree(A);
@@ -229,7 +230,6 @@ static rs_status create_dense(rs_problem* out, int64_t n, int64_t d, const doubl
   if (n < 1 || d < 1) return fail(RS_EINVAL, "need n >= 1 and d >= 1");
   if (!(lambda > 0.0) || !std::isfinite(lambda)) return fail(RS_EINVAL, "need finite lambda > 0 (P:L36)");
   if (!X_local || !y) return fail(RS_EINVAL, "X and y must be non-NULL");
-  if (ldx < d) return fail(RS_EINVAL, "ldx < d");
   if (mem != RS_MEM_HOST && mem != RS_MEM_DEVICE_COPY && mem != RS_MEM_DEVICE_BORROW)
     return fail(RS_EINVAL, "bad rs_mem");
   if (route != RS_ROUTE_AUTO && route != RS_ROUTE_PRIMAL && route != RS_ROUTE_DUAL)
@@ -237,13 +237,17 @@ static rs_status create_dense(rs_problem* out, int64_t n, int64_t d, const doubl
   if (mode != RS_AS_IMPLICIT && mode != RS_AS_EXPLICIT && mode != RS_AS_GRAM)
     return fail(RS_EINVAL, "bad as_mode");
   const int rt = route == RS_ROUTE_AUTO ? (d <= n ? 1 : 2) : (route == RS_ROUTE_PRIMAL ? 1 : 2);
-  if (rt == 2 && mode != RS_AS_EXPLICIT)   // dense dual: A = X X^T + lambda I formed once
-    return fail(RS_EUNSUPPORTED, "dense dual route (n < d): EXPLICIT mode only (or CSR X)");
-  if (rt == 2 && dist && dist->world > 1)
-    return fail(RS_EUNSUPPORTED, "dense dual route: one GPU in this version");
-  if (mode == RS_AS_GRAM && d > 4096) return fail(RS_EUNSUPPORTED, "GRAM mode needs d <= 4096");
+  // dense dual in IMPLICIT / GRAM mode: the primal machinery on R = X^T (d x n), whose A = R^T R +
+  // lambda I = X X^T + lambda I; feature shards of X are row shards of R
+  const bool dual_r = rt == 2 && mode != RS_AS_EXPLICIT;
+  if (rt == 2 && mode == RS_AS_EXPLICIT && dist && dist->world > 1)
+    return fail(RS_EUNSUPPORTED, "dense dual EXPLICIT route: one GPU in this version");
+  if (mode == RS_AS_GRAM && (dual_r ? n : d) > 4096)
+    return fail(RS_EUNSUPPORTED, "GRAM mode needs m <= 4096 (the X pass)");
   RS_TRY(validate_dist(dist, rt == 1 ? n : d));
   const long long rows = rt == 1 && dist ? dist->shard_len : n;
+  const long long cols = rt == 2 && dist ? dist->shard_len : d;   // columns of the local X block
+  if (ldx < cols) return fail(RS_EINVAL, "ldx < columns of the local X block");
 
   Problem* p = new Problem();
   auto guard = [&](rs_status s) {
@@ -275,12 +279,12 @@ static rs_status create_dense(rs_problem* out, int64_t n, int64_t d, const doubl
     p->ldx = ldx;
     p->own_X = false;
   } else {
-    p->ldx = round_up(d, 4);
+    p->ldx = round_up(cols, 4);
     s = dalloc(&p->X, (size_t)std::max<long long>(rows, 1) * p->ldx);
     if (s != RS_OK) return guard(s);
     p->own_X = true;
-    if (rows > 0 && !streamed) {
-      cudaError_t ce = cudaMemcpy2DAsync(p->X, p->ldx * 8, X_local, ldx * 8, d * 8, rows,
+    if (rows > 0 && cols > 0 && !streamed) {
+      cudaError_t ce = cudaMemcpy2DAsync(p->X, p->ldx * 8, X_local, ldx * 8, cols * 8, rows,
                                          kind_of(mem), p->st);
       if (ce != cudaSuccess) return guard(fail(RS_ECUDA, std::string("copy X: ") + cudaGetErrorString(ce)));
     }
@@ -346,7 +350,7 @@ static rs_status create_dense(rs_problem* out, int64_t n, int64_t d, const doubl
   }
   // finiteness check of the local data
   {
-    if (!streamed) launch_count_nonfinite(p->X, p->ldx, rows, d, cnt, p->st);
+    if (!streamed) launch_count_nonfinite(p->X, p->ldx, rows, cols, cnt, p->st);
     launch_count_nonfinite(p->y, 1, rows, 1, cnt, p->st);
     unsigned long long h = 0;
     cudaMemcpyAsync(&h, cnt, 8, cudaMemcpyDeviceToHost, p->st);
@@ -354,6 +358,44 @@ static rs_status create_dense(rs_problem* out, int64_t n, int64_t d, const doubl
     dfree(cnt);
     if (ce != cudaSuccess) return guard(fail(RS_ECUDA, cudaGetErrorString(ce)));
     if (h) return guard(fail(RS_EINVAL, "X or y has non-finite entries"));
+  }
+  if (dual_r) {   // R = X_local^T (cols x n, ld a multiple of 4), b = y; X kept for w = X^T alpha
+    const long long ldr = round_up(n, 4);
+    double* R = nullptr;
+    s = dalloc(&R, (size_t)std::max<long long>(cols, 1) * ldr);
+    if (s == RS_OK) s = dalloc(&p->b, n);
+    if (s != RS_OK) {
+      dfree(R);
+      return guard(s);
+    }
+    cudaEventRecord(e0, p->st);
+    cudaError_t ce = cols > 0 ? launch_transpose(p->X, p->ldx, n, cols, R, ldr, p->st) : cudaSuccess;
+    if (ce == cudaSuccess) ce = cudaMemcpyAsync(p->b, p->y, n * 8, cudaMemcpyDeviceToDevice, p->st);
+    cudaEventRecord(e1, p->st);
+    if (ce == cudaSuccess) ce = cudaStreamSynchronize(p->st);
+    if (ce != cudaSuccess) {
+      dfree(R);
+      return guard(fail(RS_ECUDA, std::string("dual R = X^T: ") + cudaGetErrorString(ce)));
+    }
+    p->Xo = p->X;
+    p->ldxo = p->ldx;
+    p->own_Xo = p->own_X;
+    p->X = R;
+    p->ldx = ldr;
+    p->own_X = true;
+    p->rows_loc = cols;
+    p->dual_r = true;
+    p->col0 = dist ? dist->shard_begin : 0;
+    p->cols_loc = cols;
+    s = finish_setup(p);
+    if (s != RS_OK) return guard(s);
+    float ms = 0;
+    cudaEventElapsedTime(&ms, e0, e1);
+    p->setup_seconds = ms * 1e-3;
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    *out = reinterpret_cast<rs_problem>(p);
+    return RS_OK;
   }
   // every buffer of the setup is allocated before e0 (and freed after e1), so setup_seconds is the
   // device work of b = X^T y and the explicit A build, not host allocator time
@@ -479,7 +521,7 @@ static rs_status validate_opts(const Problem* p, const rs_solve_opts* o, int* ks
 // Sketch-ahead pipeline (bfactor.cu) applies to dense primal EXPLICIT and GRAM modes with
 // tau <= bfactor_max_tau(): there G_k needs no per-iteration contraction of the iterate's data.
 static bool pipeline_applies(const Problem* p, int tau) {
-  const bool dense = (p->fmt == 0 && p->route == 1 &&
+  const bool dense = (p->fmt == 0 && (p->route == 1 || p->dual_r) &&
                       (p->mode == RS_AS_EXPLICIT || p->mode == RS_AS_GRAM)) ||
                      p->mode == RS_AS_EXPLICIT;   // CSR explicit: dense A built in rs_create_csr
   const bool csr = p->fmt == 1 && p->mode == RS_AS_GRAM;
@@ -905,16 +947,17 @@ rs_status Problem::solve(const rs_solve_opts* o, double* w_out, rs_mem w_mem, do
   int chunk = (int)(o->check_every > 0 ? std::min<long long>(o->check_every, 1024)
                                        : (want_pipe ? (o->tau > 224 ? num_sms : 64) : 16));
   // EXPLICIT with tau > 224: overlap the next group's factorisation with the current group's
-  // iterations when the factorisation is the longer of the two.  Estimates per iteration: the
-  // factor's 2 tau^3 / 3 flop at ~15 TFLOP/s (measured, ~0.4 of the DMMA peak) against the group
-  // kernel's sketched rows of A (len m 8 bytes) on OV_SMS SMs at ~45 GB/s each plus ~15 us of
-  // barriers (profiles/README.md, k_iterate phases)
+  // iterations when that shortens an iteration.  Per-iteration estimates: the factor's 2 tau^3 / 3
+  // flop at ~15 TFLOP/s on all SMs (measured, ~0.4 of the DMMA peak; num_sms / (num_sms - OV_SMS)
+  // slower on the SMs the overlap leaves it), the group kernel's sketched rows of A (len m 8 bytes)
+  // at ~45 GB/s per SM plus ~15 us of barriers (profiles/README.md, k_iterate phases)
   const double tau_d = (double)o->tau;
   const double len_d = (double)sketch_max_len((int)o->kind, (int)m, (int)o->tau, ksum);
-  const double est_factor_us = 2.0 * tau_d * tau_d * tau_d / 3.0 / 15e6;
-  const double est_iter_us = len_d * (double)m * 8.0 / (OV_SMS * 45e3) + 15.0;
+  const double f_us = 2.0 * tau_d * tau_d * tau_d / 3.0 / 15e6;
+  auto it_us = [&](int sms) { return len_d * (double)m * 8.0 / (sms * 45e3) + 15.0; };
+  const double ov_us = std::max(f_us * num_sms / std::max(1, num_sms - OV_SMS), it_us(OV_SMS));
   const bool want_ov = want_pipe && mode == RS_AS_EXPLICIT && o->tau > 224 && num_sms > 2 * OV_SMS &&
-                       len_d <= 8192 && est_factor_us > est_iter_us;
+                       len_d <= 8192 && ov_us < f_us + it_us(num_sms);
   if (want_ov) chunk = 2 * (num_sms - OV_SMS);
   const bool want_xg = want_ov;   // two slot sets
   if (want_xg) chunk = std::max(2, chunk & ~1);   // two groups of P = chunk / 2
@@ -1128,12 +1171,16 @@ rs_status Problem::write_weights(double* w_out, rs_mem w_mem, double* alpha_out)
   const cudaMemcpyKind kd = w_mem == RS_MEM_HOST ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice;
   if (route == 1) {
     RS_CUDA(cudaMemcpyAsync(w_out, w, m * 8, kd, st));
-  } else if (fmt == 0) {   // dense dual: w = X^T alpha
+  } else if (fmt == 0) {   // dense dual: w = X^T alpha; feature shards assembled
+    const double* Xd = dual_r ? Xo : X;
+    const long long ldd = dual_r ? ldxo : ldx, dl = dual_r ? cols_loc : d;
     double *wd = nullptr, *work = nullptr;
     RS_TRY(dalloc(&wd, d));
-    rs_status s = dalloc(&work, dense_xty_work(n, d));
-    if (s == RS_OK && launch_dense_xty(X, ldx, n, d, w, wd, work, st) != cudaSuccess)
+    rs_status s = dalloc(&work, dense_xty_work(n, std::max<long long>(dl, 1)));
+    if (s == RS_OK && world > 1 && launch_fill(wd, d, 0.0, st) != cudaSuccess) s = fail(RS_ECUDA, "dual weights");
+    if (s == RS_OK && dl > 0 && launch_dense_xty(Xd, ldd, n, dl, w, wd + (world > 1 ? col0 : 0), work, st) != cudaSuccess)
       s = fail(RS_ECUDA, "dual weights");
+    if (s == RS_OK && world > 1) s = allreduce(wd, (size_t)d);   // zero-padded feature blocks
     if (s == RS_OK && cudaMemcpyAsync(w_out, wd, d * 8, kd, st) != cudaSuccess) s = fail(RS_ECUDA, "copy w");
     cudaStreamSynchronize(st);
     dfree(wd);

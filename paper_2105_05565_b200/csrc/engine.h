@@ -50,6 +50,12 @@ struct Problem {
   double* X = nullptr;
   long long ldx = 0;
   bool own_X = false;
+  // dense dual in IMPLICIT / GRAM mode: X above is R = X_local^T (cols_loc x n); Xo is X_local
+  // (n x cols_loc) for w = X^T alpha; col0 = the rank's first feature
+  bool dual_r = false;
+  double* Xo = nullptr;
+  long long ldxo = 0, col0 = 0, cols_loc = 0;
+  bool own_Xo = false;
   double* y = nullptr;
   double* b = nullptr;
   double bnorm2 = 0.0;

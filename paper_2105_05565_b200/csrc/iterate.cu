@@ -35,7 +35,7 @@ constexpr int IT_MAXLEN = 8192;
 #ifdef RS_IT_PHASES
 // development probe (build with RS_NVCC_EXTRA=-DRS_IT_PHASES): SM cycles of CTA 0 per phase:
 // 0 A, 1 sync1, 2 B, 3 sync2, 4 C, 5 next-slot staging, 6 sync3, 7 stop rule
-__device__ unsigned long long g_it_phase[8];
+__device__ unsigned long long g_it_phase[12];   // 8: A g gather, 9: A prefetch issue, 10: A rows
 #define IT_T(v) long long v = clock64()
 #define IT_ADD(ph, t0_, t1_) if (blockIdx.x == 0 && threadIdx.x == 0) g_it_phase[ph] += (unsigned long long)((t1_) - (t0_))
 #else
@@ -146,6 +146,8 @@ k_iterate(IterArgs a, Ctrl* ctrl) {
       xs[b] = g;
     }
     __syncthreads();
+    IT_T(ta_g);
+    IT_ADD(8, ta0, ta_g);
     {   // this CTA's column block of the rows phase C reads, pulled into L2 meanwhile
       const unsigned bytes = (unsigned)(((j1 - j0) * 8 + 15) & ~15LL);
       if (bytes > 0)
@@ -154,20 +156,27 @@ k_iterate(IterArgs a, Ctrl* ctrl) {
           pf_l2(X + (long long)row * ldx + j0, bytes);
         }
     }
+    IT_T(ta_p);
+    IT_ADD(9, ta_g, ta_p);
+    auto scatter = [&](int row, double d) {
+      for (int e = s_bp[row] + lane; e < s_bp[row + 1]; e += 32) {
+        const int ce = s_ce[e];
+        a.sdelta[ce >= 0 ? ce : ~ce] = ce >= 0 ? d : -d;
+      }
+    };
     for (int row = gw; row < tau; row += GW) {
       const double* rw = Gi + (long long)row * a.ld_gi;
-      if (a.big) {
+      if (a.big) {   // t = W g, lower rows
         const double t = row_dot(rw, xs, 0, row + 1, lane);
         if (lane == 0) a.tvec[row] = t;
-      } else {
+      } else {       // delta = G^{-1} g, full rows
         const double d = row_dot(rw, xs, 0, tau, lane);
         if (lane == 0) a.dvec[row] = d;
-        for (int e = s_bp[row] + lane; e < s_bp[row + 1]; e += 32) {
-          const int ce = s_ce[e];
-          a.sdelta[ce >= 0 ? ce : ~ce] = ce >= 0 ? d : -d;
-        }
+        scatter(row, d);
       }
     }
+    IT_T(ta_r);
+    IT_ADD(10, ta_p, ta_r);
     if (a.big) {   // this CTA's rows of W^T, pulled into L2 for phase B
       for (int row = gw; row < tau; row += GW)
         if (lane == 0)
@@ -182,13 +191,10 @@ k_iterate(IterArgs a, Ctrl* ctrl) {
     if (a.big) {
       for (int b = tid; b < tau; b += IT_THREADS) xs[b] = __ldcg(a.tvec + b);
       __syncthreads();
-      for (int row = gw; row < tau; row += GW) {
+      for (int row = gw; row < tau; row += GW) {   // delta = W^T t, upper rows
         const double d = row_dot(Gi + (long long)row * a.ld_gi, xs, row, tau, lane);
         if (lane == 0) a.dvec[row] = d;
-        for (int e = s_bp[row] + lane; e < s_bp[row + 1]; e += 32) {
-          const int ce = s_ce[e];
-          a.sdelta[ce >= 0 ? ce : ~ce] = ce >= 0 ? d : -d;
-        }
+        scatter(row, d);
       }
       IT_T(tb1);
       IT_ADD(2, tb0, tb1);
@@ -335,7 +341,7 @@ extern "C" int rs_debug_it_phases(unsigned long long* out, int reset) {
   cudaDeviceSynchronize();
   if (cudaMemcpyFromSymbol(out, g_it_phase, sizeof(g_it_phase)) != cudaSuccess) return -1;
   if (reset) {
-    unsigned long long z[8] = {0};
+    unsigned long long z[12] = {0};
     cudaMemcpyToSymbol(g_it_phase, z, sizeof(z));
   }
   return 0;

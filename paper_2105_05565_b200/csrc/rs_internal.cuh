@@ -215,7 +215,7 @@ struct IterArgs {
   int big;                       // tau > 224
 };
 // SMs left to the iterations while the next group's factorisation runs (EXPLICIT, tau > 224)
-constexpr int OV_SMS = 28;
+constexpr int OV_SMS = 22;
 size_t iterate_smem();
 bool iterate_ok(const DevSketch& sk, long long m, int grid);   // the group kernel applies
 cudaError_t iterate_init();

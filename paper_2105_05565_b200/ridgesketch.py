@@ -356,10 +356,7 @@ class RidgeSketch:
                               self.alpha, self.route, self.as_mode)
         else:
             n, d = X.shape
-            dual = self.route == "dual" or (self.route == "auto" and n < d)
-            # dense dual (n < d) is served by the EXPLICIT route (A = X X^T + alpha I)
-            mode = "explicit" if dual else self.as_mode
-            h = rs_create_dense(X, y, self.alpha, self.route, mode)
+            h = rs_create_dense(X, y, self.alpha, self.route, self.as_mode)
         try:
             w, rep = rs_solve(h, self.solver, self.sketch_size, self.gamma, self.beta, self.tol,
                               self.max_iter, self.seed, self.subcount_k, d=d,

@@ -31,6 +31,11 @@ CASES = {
                            tau=30, k=3, iters=12, seed=3, sseed=7),
     "dense_explicit_big": dict(data="dense", n=4001, d=601, lam=0.4, mode="explicit", kind="subsample",
                                tau=260, iters=10, seed=3, sseed=8),
+    # dense dual (n < d) through R = X^T: feature shards of X are row shards of R
+    "dense_dual_gram": dict(data="dense", n=300, d=1201, lam=0.5, mode="gram", kind="subsample", tau=40,
+                            iters=12, seed=5, sseed=3, dual=True),
+    "dense_dual_implicit": dict(data="dense", n=300, d=1201, lam=0.5, mode="implicit", kind="count",
+                                tau=30, iters=12, seed=5, sseed=4, dual=True),
     # CSR primal, nnz-balanced row shards
     "csr_primal_gram": dict(data="csr", make=_csr_primal, n=3001, d=400, lam=1e-2, mode="gram",
                             kind="count", tau=40, iters=12, sseed=2),

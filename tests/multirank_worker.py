@@ -38,10 +38,16 @@ def main():
         if c["data"] == "dense":
             X, y = rsinputs.dense_problem(c["n"], c["d"], seed=c["seed"], col_decay=True, noise=0.01)
             X, y = X.numpy(), y.numpy()
-            b0, ln = rs.rs_shard_range(c["n"], rank, world)
-            dist.update(shard_begin=b0, shard_len=ln)
-            h = rs.rs_create_dense(np.ascontiguousarray(X[b0:b0 + ln]), np.ascontiguousarray(y[b0:b0 + ln]),
-                                   c["lam"], mode=c["mode"], n=c["n"], d=c["d"], dist=dist)
+            if c.get("dual"):   # feature (column) shards; y whole
+                b0, ln = rs.rs_shard_range(c["d"], rank, world)
+                dist.update(shard_begin=b0, shard_len=ln)
+                h = rs.rs_create_dense(np.ascontiguousarray(X[:, b0:b0 + ln]), y, c["lam"], route="dual",
+                                       mode=c["mode"], n=c["n"], d=c["d"], dist=dist)
+            else:
+                b0, ln = rs.rs_shard_range(c["n"], rank, world)
+                dist.update(shard_begin=b0, shard_len=ln)
+                h = rs.rs_create_dense(np.ascontiguousarray(X[b0:b0 + ln]), np.ascontiguousarray(y[b0:b0 + ln]),
+                                       c["lam"], mode=c["mode"], n=c["n"], d=c["d"], dist=dist)
         else:
             rp, ci, v, y = c["make"]()
             n, d = c["n"], c["d"]

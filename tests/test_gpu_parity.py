@@ -774,10 +774,26 @@ def test_dense_dual_explicit_parity(rs, kind, tau, k):
     assert_close(w, ref["weights"], 1e-10)
 
 
-def test_dense_dual_implicit_unsupported(rs):
-    X, y = rsinputs.dense_problem(50, 80, seed=4)
-    with pytest.raises(rs.RSError, match="UNSUPPORTED"):
-        rs.rs_create_dense(X.numpy(), y.numpy(), 0.5, mode="implicit")
+@pytest.mark.parametrize("kind,tau,k", [("subsample", 40, 0), ("subcount", 30, 2), ("count", 25, 0),
+                                        ("subsample", 240, 0)])
+@pytest.mark.parametrize("mode", ["implicit", "gram"])
+def test_dense_dual_r_parity(rs, kind, tau, k, mode):
+    """Dense X with n < d in IMPLICIT / GRAM mode: the primal machinery on R = X^T (d x n), whose
+    A = R^T R + lambda I = X X^T + lambda I: A S = R^T (R S) + lambda S, or the Gram of
+    R S and u = R^T (R S delta); alpha, r and w = X^T alpha equal the oracle's."""
+    X, y = rsinputs.dense_problem(300, 900, seed=4)
+    X, y = X.numpy(), y.numpy()
+    h = rs.rs_create_dense(X, y, 0.5, mode=mode)
+    try:
+        w, rep = rs.rs_solve(h, kind, tau, 1.0, 0.5, 0.0, 15, 3, k, check_every=7, d=900, alpha=True)
+        alpha, r = rs.rs_get_state(h)
+    finally:
+        rs.rs_destroy(h)
+    ref = OV.solve(X, y, 0.5, kind, tau, 1.0, 0.5, 0.0, 15, seed=3, subcount_k=k)
+    assert ref["route"] == "dual"
+    assert_close(alpha, ref["w"], 1e-10)
+    assert_close(r, ref["r"], 1e-10)
+    assert_close(w, ref["weights"], 1e-10)
 
 
 # ------------------------------------------------------------------ failure paths (SURVEY §8(b))

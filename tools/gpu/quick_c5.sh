@@ -1,5 +1,5 @@
-# Quick c5 check: parity of the large-tau paths, then the default bench line without the slow legs.
+# Quick check: explicit / dual / multi-rank / tau = 1024 parity subset, then the OV_SMS sweep of
+# the c5 line (bench without the slow legs)
 python -c "import __graft_entry__ as g; g.build()" || exit 1
-timeout 900 python -m pytest tests -m gpu -q -x -k "tau1024 or large_tau or kernel_ridge or process_switches or config5" 2>&1 | tail -3 > gpurun_out/quick_pytest.log
-timeout 600 python bench.py --no-alt --no-e2e --no-cpu-baseline ${BENCH_ARGS} > gpurun_out/quick_bench.json 2> gpurun_out/quick_bench.err
-cat gpurun_out/quick_pytest.log
+timeout 1200 python -m pytest tests -m gpu -q -p no:cacheprovider --timeout 300 -k "${PYK:-explicit or dual or multirank or tau1024 or kernel or config1 or ragged or xs}" 2>&1 | tail -4 | tee gpurun_out/quick_pytest.log
+SWEEP="${SWEEP:-22 26 30}" bash tools/gpu/ov_sweep.sh
