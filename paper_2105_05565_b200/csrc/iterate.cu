@@ -148,14 +148,8 @@ k_iterate(IterArgs a, Ctrl* ctrl) {
     __syncthreads();
     IT_T(ta_g);
     IT_ADD(8, ta0, ta_g);
-    {   // this CTA's column block of the rows phase C reads, pulled into L2 meanwhile
-      const unsigned bytes = (unsigned)(((j1 - j0) * 8 + 15) & ~15LL);
-      if (bytes > 0)
-        for (int e = tid; e < nr; e += IT_THREADS) {
-          const int row = a.ASt ? e : (s_ce[e] >= 0 ? s_ce[e] : ~s_ce[e]);
-          pf_l2(X + (long long)row * ldx + j0, bytes);
-        }
-    }
+    // (no L2 prefetch of phase C's row segments: ~1000 cp.async.bulk.prefetch per CTA cost 7 us of
+    // issue per iteration on c5, more than the loads they would cover)
     IT_T(ta_p);
     IT_ADD(9, ta_g, ta_p);
     auto scatter = [&](int row, double d) {
