@@ -533,15 +533,31 @@ __device__ __noinline__ bool diag_factor_s(double* D, int ldd, double* Lg, int l
 //     [T_I,J0 T_I,J1] = sum_{K=J1+1..I} W_IK [L_K,J0 L_K,J1]
 //     W_I,J1 = -T_I,J1 W_J1J1,  W_I,J0 = -(T_I,J0 + W_I,J1 L_J1,J0) W_J0J0
 //     diagonal pair: W_J1,J0 = -W_J1J1 L_J1,J0 W_J0J0
-constexpr int LP_WARPS = 8;                     // 255 registers: acc[4][8][2] per lane
-constexpr int LP_THREADS = LP_WARPS * 32;
-constexpr int LP_STAGES = 2;                    // double-buffered k tiles (32 deep)
-constexpr int LP_BLD = 36;                      // B [n][k] row stride (Cholesky) and A [r][k]:
-constexpr int LP_ALD = 36;                      //   36 = 4 mod 16 -> conflict-free fragments
-constexpr int LP_BTLD = 68;                     // B [k][n] row stride (inverse), 68 = 4 mod 16
-constexpr int LP_BSZ = 64 * LP_BLD;             // >= 32 * LP_BTLD
-constexpr int LP_ASZ = 32 * LP_ALD;
-constexpr int LP_STAGE = LP_BSZ + LP_WARPS * LP_ASZ;   // doubles per stage
+// Two shapes of the same kernel (LpCfg<NW>): 8 warps with 32-deep slices, one CTA per SM (the
+// pipeline-fill group, all SMs free), and 4 warps with 16-deep slices, two CTAs per SM, so that one
+// slot's barriers, diagonal pairs and finishing steps run while the other slot's warps keep the DMMA
+// pipe busy (one warp per SM sub-partition nearly saturates it: profiles/r01_fp64_peak.txt).
+template <int NW>
+struct LpCfg {
+  static constexpr int WARPS = NW;
+  static constexpr int THREADS = NW * 32;           // 255 registers: acc[4][8][2] per lane
+  static constexpr int CTAS = NW == 8 ? 1 : 2;      // resident CTAs per SM
+  static constexpr int KS = NW == 8 ? 32 : 16;      // k slice depth
+  static constexpr int STAGES = 2;                  // double-buffered k slices
+  static constexpr int BLD = KS + 4;                // B [n][k] row stride (Cholesky) and A [r][k]:
+  static constexpr int ALD = KS + 4;                //   36 / 20 = 4 mod 16 -> conflict-free fragments
+  static constexpr int BTLD = 68;                   // B [k][n] row stride (inverse), 68 = 4 mod 16
+  static constexpr int BSZ = 64 * BLD;              // >= KS * BTLD
+  static constexpr int ASZ = 32 * ALD;
+  static constexpr int STAGE = BSZ + NW * ASZ;      // doubles per stage
+  static constexpr int cmax(int a, int b) { return a > b ? a : b; }
+  // the ring doubles as the diagonal pair's 64 x 65 M and Lm, the split-reduce buffers (2048 per
+  // warp) and the per-warp 32 x 36 finishing tiles
+  static constexpr int RING = cmax(cmax(STAGES * STAGE, 2 * 64 * 65), NW * 2048);
+  static constexpr size_t SMEM = ((size_t)RING + 3 * 32 * 36) * sizeof(double);   // ring + pair tiles
+  static_assert(KS * BTLD <= BSZ, "inverse B tile must fit the B region");
+  static_assert(NW * 32 * 36 <= RING, "finishing scratch must fit the ring");
+};
 #ifdef RS_BF_PHASES
 // development probe (build with RS_NVCC_EXTRA=-DRS_BF_PHASES): SM cycles per factor phase, summed
 // over CTAs: 0 gather, 1 chol accumulate, 2 chol diag, 3 chol total, 4 inv accumulate, 5 inv total,
@@ -553,33 +569,26 @@ __device__ unsigned long long g_bf_phase[8];
 #define BF_T(v)
 #define BF_ADD(ph, a, b)
 #endif
-constexpr size_t LP_SMEM = ((size_t)LP_STAGES * LP_STAGE + 3 * 32 * 36) * sizeof(double);   // ring + pair tiles
-static_assert(LP_WARPS * 32 * 36 <= LP_STAGES * LP_STAGE, "finishing scratch must fit the ring");
-static_assert(32 * LP_BTLD <= LP_BSZ, "inverse B tile must fit the B region");
-
-// One 32-deep k tile of a strip: acc[R][C] += A[8R+q][k] B(k, 8C+q) -- A [r][k] (LP_ALD), B [n][k]
-// (LP_BLD, Cholesky) or [k][n] (LP_BTLD, inverse).
-template <bool CHOL>
-__device__ __forceinline__ void lp_slice(double (&acc)[4][8][2], const double* xs, const double* ys,
-                                         int q, int k4);
 
 __device__ __forceinline__ void lp_cp16(double* smem, const double* gmem) {
   const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem));
 }
 
-template <bool CHOL>
+// One k slice of a strip: acc[R][C] += A[8R+q][k] B(k, 8C+q) -- A [r][k] (ALD), B [n][k] (BLD,
+// Cholesky) or [k][n] (BTLD, inverse).
+template <bool CHOL, class CF>
 __device__ __forceinline__ void lp_slice(double (&acc)[4][8][2], const double* xs, const double* ys,
                                          int q, int k4) {
 #pragma unroll
-  for (int K = 0; K < 8; ++K) {
+  for (int K = 0; K < CF::KS / 4; ++K) {
     double a[4];
 #pragma unroll
-    for (int R = 0; R < 4; ++R) a[R] = xs[(8 * R + q) * LP_ALD + 4 * K + k4];
+    for (int R = 0; R < 4; ++R) a[R] = xs[(8 * R + q) * CF::ALD + 4 * K + k4];
 #pragma unroll
     for (int C = 0; C < 8; ++C) {
       const int n = 8 * C + q, kq = 4 * K + k4;
-      const double b = CHOL ? ys[n * LP_BLD + kq] : ys[kq * LP_BTLD + n];
+      const double b = CHOL ? ys[n * CF::BLD + kq] : ys[kq * CF::BTLD + n];
 #pragma unroll
       for (int R = 0; R < 4; ++R) dmma(acc[R][C], a[R], b);
     }
@@ -690,15 +699,21 @@ k_bf_gather(FactorSrc src, DevSketch skb, double* work, long long work_stride, c
   }
 }
 
-__global__ void __launch_bounds__(LP_THREADS, 1)
-k_bfactor_lp(FactorSrc src, DevSketch skb, double* __restrict__ Ginv, long long ldgi,
-             long long gi_stride, double* work, long long work_stride, int* __restrict__ flags,
-             const Ctrl* ctrl) {
-  if (slot_unused(ctrl, blockIdx.x)) return;
+// One slot's factorisation by the whole CTA; false: the solve has stopped (abandon the launch).
+template <int NW>
+__device__ __forceinline__ bool lp_factor_slot(const FactorSrc& src, const DevSketch& skb,
+                                               double* __restrict__ Ginv, long long ldgi,
+                                               long long gi_stride, double* work,
+                                               long long work_stride, int* __restrict__ flags,
+                                               const Ctrl* ctrl, const int slot, int& s_bad,
+                                               int& s_stop) {
+  using CF = LpCfg<NW>;
+  constexpr int LP_WARPS = CF::WARPS, LP_THREADS = CF::THREADS, LP_STAGES = CF::STAGES;
+  constexpr int LP_STAGE = CF::STAGE, LP_BSZ = CF::BSZ, LP_ASZ = CF::ASZ, KS = CF::KS;
+  constexpr int SPT = 32 / KS;   // k slices per 32-wide tile
+  if (slot_unused(ctrl, slot)) return true;
   BF_T(t_start);
-  extern __shared__ __align__(16) double lp_sm[];   // LP_STAGES slice buffers (a4 gather: sketch)
-  __shared__ int s_bad, s_stop;
-  const int slot = blockIdx.x;
+  extern __shared__ __align__(16) double lp_sm[];   // slice ring, then the pair tiles
   const DevSketch sk = skb.at(slot);
   const int tau = sk.tau, tp = bb_tp(tau), Tc = tp / 32;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -724,35 +739,37 @@ k_bfactor_lp(FactorSrc src, DevSketch skb, double* __restrict__ Ginv, long long 
   // into part 0 in part order (deterministic) -- short rounds (the last pairs of each phase) keep
   // every warp on the DMMA pipe.  Returns the strip slot j (-1: idle warp).
   auto split = [&](int m, int& spw, int& part) {
-    spw = m <= 2 ? 4 : (m <= 4 ? 2 : 1);
+    spw = m <= LP_WARPS / 4 ? 4 : (m <= LP_WARPS / 2 ? 2 : 1);
     part = warp % spw;
     const int j = warp / spw;
     return j < m ? j : -1;
   };
-  // k slice s of [kb, ke) = tile kb + s (32 deep).  Stage buffer: B then one A tile per warp.  Every
-  // thread commits one group per slice (possibly empty), so wait_group counts stay uniform.
+  // k slice s of [kb, ke): columns co .. co + KS - 1 of tile kt = kb + s / SPT (co = KS (s % SPT)).
+  // Stage buffer: B then one A slice per warp.  Every thread commits one group per slice (possibly
+  // empty), so wait_group counts stay uniform.
   double acc[4][8][2];
   auto issue = [&](int s, bool chol, int p0, int kb, bool act_a, int i) {
     double* buf = lp_sm + (s % LP_STAGES) * LP_STAGE;
-    const int kt = kb + s;
+    const int kt = kb + s / SPT, co = KS * (s % SPT);
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {   // B: 1024 pieces of 16 bytes, four per thread
+    for (int u = 0; u < 32 * KS / LP_THREADS; ++u) {   // B: 32 KS pieces of 16 bytes
       const int t = tid + LP_THREADS * u;
-      if (chol) {   // rows n of L_{p0 + n/32, kt} -> [n][LP_BLD]
-        const int n = t >> 4, c16 = t & 15;
-        lp_cp16(buf + n * LP_BLD + 2 * c16, T(p0 + (n >> 5), kt) + (long long)(n & 31) * tp + 2 * c16);
-      } else {      // rows kr of tiles (kt, p0 + h), all 64 columns -> [kr][LP_BTLD]
+      if (chol) {   // rows n of L_{p0 + n/32, kt} -> [n][BLD]
+        const int n = t / (KS / 2), c16 = t % (KS / 2);
+        lp_cp16(buf + n * CF::BLD + 2 * c16, T(p0 + (n >> 5), kt) + (long long)(n & 31) * tp + co + 2 * c16);
+      } else {      // rows co + kr of tiles (kt, p0 + h), all 64 columns -> [kr][BTLD]
         const int kr = t >> 5, n32 = t & 31;
-        lp_cp16(buf + kr * LP_BTLD + 2 * n32, T(kt, p0 + (n32 >> 4)) + (long long)kr * tp + 2 * (n32 & 15));
+        lp_cp16(buf + kr * CF::BTLD + 2 * n32,
+                T(kt, p0 + (n32 >> 4)) + (long long)(co + kr) * tp + 2 * (n32 & 15));
       }
     }
-    if (act_a) {   // A: the warp's tile T(i, kt), 16 pieces per lane
+    if (act_a) {   // A: columns co .. of the warp's tile T(i, kt), KS / 2 pieces per lane
       double* a = buf + LP_BSZ + warp * LP_ASZ;
-      const double* srcA = T(i, kt);
+      const double* srcA = T(i, kt) + co;
 #pragma unroll
-      for (int u = 0; u < 16; ++u) {
-        const int t = lane + 32 * u, r = t >> 4, c16 = t & 15;
-        lp_cp16(a + r * LP_ALD + 2 * c16, srcA + (long long)r * tp + 2 * c16);
+      for (int u = 0; u < KS / 2; ++u) {
+        const int t = lane + 32 * u, r = t / (KS / 2), c16 = t % (KS / 2);
+        lp_cp16(a + r * CF::ALD + 2 * c16, srcA + (long long)r * tp + 2 * c16);
       }
     }
     asm volatile("cp.async.commit_group;\n");
@@ -763,11 +780,11 @@ k_bfactor_lp(FactorSrc src, DevSketch skb, double* __restrict__ Ginv, long long 
     for (int R = 0; R < 4; ++R)
 #pragma unroll
       for (int C = 0; C < 8; ++C) acc[R][C][0] = acc[R][C][1] = 0.0;
-    const int ns = ke - kb;
+    const int ns = (ke - kb) * SPT;
     if (ns <= 0) return;
     __syncthreads();   // the ring doubles as the strips' finishing scratch
     BF_T(t_acc0);
-    auto mine = [&](int s) { return i >= 0 && kb + s <= klim && (s % spw) == part; };
+    auto mine = [&](int s) { return i >= 0 && kb + s / SPT <= klim && (s % spw) == part; };
 #pragma unroll 1
     for (int s = 0; s < LP_STAGES - 1; ++s) {
       if (s < ns) issue(s, chol, p0, kb, mine(s), i);
@@ -782,8 +799,8 @@ k_bfactor_lp(FactorSrc src, DevSketch skb, double* __restrict__ Ginv, long long 
       if (mine(s)) {
         const double* buf = lp_sm + (s % LP_STAGES) * LP_STAGE;
         const double* xs = buf + LP_BSZ + warp * LP_ASZ;
-        if (chol) lp_slice<true>(acc, xs, buf, q, k4);
-        else lp_slice<false>(acc, xs, buf, q, k4);
+        if (chol) lp_slice<true, CF>(acc, xs, buf, q, k4);
+        else lp_slice<false, CF>(acc, xs, buf, q, k4);
       }
     }
     asm volatile("cp.async.wait_group 0;\n");
@@ -842,21 +859,25 @@ k_bfactor_lp(FactorSrc src, DevSketch skb, double* __restrict__ Ginv, long long 
   // the three tiles every strip of a pair step needs (row-major, LD 36):
   //   Cholesky: L_p0p0^{-1}, L_p0+1,p0, L_p0+1p0+1^{-1} (written by the diagonal-pair warp);
   //   inverse:  W_J0J0, L_J1,J0, W_J1J1 (staged once per pair)
-  double* P3 = lp_sm + LP_STAGES * LP_STAGE;
+  double* P3 = lp_sm + CF::RING;
   constexpr int PLD = 36, PT = 32 * PLD;
   auto stage3 = [&](const double* t0, int ld0, const double* t1, int ld1, const double* t2, int ld2) {
-    double v[12];   // 3 x 1024 elements, 12 per thread, all loads in flight before the stores
+    // 3 x 1024 elements, 12 per thread per pass, all loads of a pass in flight before its stores
+#pragma unroll 1
+    for (int x0 = 0; x0 < 3072; x0 += 12 * LP_THREADS) {
+      double v[12];
 #pragma unroll
-    for (int u = 0; u < 12; ++u) {
-      const int x = tid + LP_THREADS * u, w = x >> 10, rr = (x >> 5) & 31, cc = x & 31;
-      const double* src = w == 0 ? t0 + (long long)rr * ld0 : w == 1 ? t1 + (long long)rr * ld1
-                                                                     : t2 + (long long)rr * ld2;
-      v[u] = src[cc];
-    }
+      for (int u = 0; u < 12; ++u) {
+        const int x = x0 + tid + LP_THREADS * u, w = x >> 10, rr = (x >> 5) & 31, cc = x & 31;
+        const double* src = w == 0 ? t0 + (long long)rr * ld0 : w == 1 ? t1 + (long long)rr * ld1
+                                                                       : t2 + (long long)rr * ld2;
+        v[u] = src[cc];
+      }
 #pragma unroll
-    for (int u = 0; u < 12; ++u) {
-      const int x = tid + LP_THREADS * u, w = x >> 10, rr = (x >> 5) & 31, cc = x & 31;
-      P3[w * PT + rr * PLD + cc] = v[u];
+      for (int u = 0; u < 12; ++u) {
+        const int x = x0 + tid + LP_THREADS * u, w = x >> 10, rr = (x >> 5) & 31, cc = x & 31;
+        P3[w * PT + rr * PLD + cc] = v[u];
+      }
     }
   };
   // per-warp 32 x 32 scratch (LD 36) in the slice ring, free between accumulations
@@ -947,7 +968,7 @@ k_bfactor_lp(FactorSrc src, DevSketch skb, double* __restrict__ Ginv, long long 
   // finished from its register accumulator (no C round trip, no panel pass).
   BF_T(t_c0);
   for (int p0 = 0; p0 < Tc; p0 += 2) {
-    if (stopped()) return;
+    if (stopped()) return false;
     const int nstrip = Tc - p0, rounds = (nstrip + LP_WARPS - 1) / LP_WARPS;
     for (int rd = 0; rd < rounds; ++rd) {
       int spw, part;
@@ -967,22 +988,25 @@ k_bfactor_lp(FactorSrc src, DevSketch skb, double* __restrict__ Ginv, long long 
             // update M_rc -= M_rj M_cj / M_jj, one barrier per column; column j of L to Lm
           double* M = lp_sm;                 // 64 x 65 (the ring is free here)
           double* Lm = lp_sm + 64 * 65;      // 64 x 65
-          {
+#pragma unroll 1
+          for (int x0 = 0; x0 < 4096; x0 += 16 * LP_THREADS) {
             double v[16];
 #pragma unroll
             for (int u = 0; u < 16; ++u) {
-              const int x = tid + LP_THREADS * u, r = x >> 6, c = x & 63;
+              const int x = x0 + tid + LP_THREADS * u, r = x >> 6, c = x & 63;
               v[u] = (c <= r) ? T(p0 + (r >> 5), p0 + (c >> 5))[(long long)(r & 31) * tp + (c & 31)] : 0.0;
             }
 #pragma unroll
             for (int u = 0; u < 16; ++u) {
-              const int x = tid + LP_THREADS * u, r = x >> 6, c = x & 63;
+              const int x = x0 + tid + LP_THREADS * u, r = x >> 6, c = x & 63;
               M[r * 65 + c] = v[u];
               Lm[r * 65 + c] = 0.0;
             }
           }
           __syncthreads();
-          const int ur = tid >> 2, uc = tid & 3;   // update: row j + 1 + ur, columns j + 1 + uc + 4 t
+          // update: row j + 1 + ur, columns j + 1 + uc + UC t
+          constexpr int UC = LP_THREADS / 64;
+          const int ur = tid / UC, uc = tid % UC;
 #pragma unroll 1
           for (int j = 0; j < 64; ++j) {
             double d = M[j * 65 + j];
@@ -998,14 +1022,15 @@ k_bfactor_lp(FactorSrc src, DevSketch skb, double* __restrict__ Ginv, long long 
             if (r < 64) {
               const double f = M[r * 65 + j] / d;
 #pragma unroll 4
-              for (int c = j + 1 + uc; c <= r; c += 4) M[r * 65 + c] -= f * M[c * 65 + j];
+              for (int c = j + 1 + uc; c <= r; c += UC) M[r * 65 + c] -= f * M[c * 65 + j];
             }
             __syncthreads();
           }
           // L00^{-1} -> P3[0], L11^{-1} -> P3[2]: column jc of block b by 4 threads (partial sums
           // over k = jc + part (mod 4), shuffle-reduced), rows in order
-          {
-            const int col = tid >> 2, part = tid & 3, b = col >> 5, jc = col & 31;
+#pragma unroll 1
+          for (int c0 = 0; c0 < 64; c0 += LP_THREADS / 4) {
+            const int col = c0 + (tid >> 2), part = tid & 3, b = col >> 5, jc = col & 31;
             double* Di = P3 + (b ? 2 * PT : 0);
             const double* Lb = Lm + (32 * b) * 65 + 32 * b;
 #pragma unroll 1
@@ -1047,12 +1072,16 @@ k_bfactor_lp(FactorSrc src, DevSketch skb, double* __restrict__ Ginv, long long 
   BF_T(t_c1);
   BF_ADD(3, t_c0, t_c1);
   if (s_bad) {
-    if (tid == 0) flags[slot] = 1;
-    return;
+    __syncthreads();   // (every thread has read s_bad before the next slot resets it)
+    if (tid == 0) {
+      __threadfence();
+      flags[slot] = 1;
+    }
+    return true;
   }
   // ---- W = L^{-1}, block-column pairs from the last
   for (int J0 = Tc - 2; J0 >= 0; J0 -= 2) {
-    if (stopped()) return;
+    if (stopped()) return false;
     const int J1 = J0 + 1, nstrip = Tc - 1 - J1;
     const int rounds = (nstrip + LP_WARPS - 1) / LP_WARPS;
     if (rounds > 0) {
@@ -1104,7 +1133,60 @@ k_bfactor_lp(FactorSrc src, DevSketch skb, double* __restrict__ Ginv, long long 
   BF_ADD(5, t_c1, t_w0);
   BF_T(t_w1);
   BF_ADD(7, t_w0, t_w1);
-  if (tid == 0) flags[slot] = 0;
+  __syncthreads();   // every W tile of the slot written (emit_w) before the flag
+  if (tid == 0) {
+    __threadfence();
+    flags[slot] = 0;
+  }
+  return true;
+}
+
+// The batched factorisation: one slot per CTA (claim == null: slot = blockIdx.x), or slots claimed
+// from claim[0] by CTAs that run on at most max_sms distinct SMs, so that the overlapped
+// pipeline's factorisation leaves num_sms - max_sms SMs to the concurrent iteration kernel even
+// when the GPU dispatches the factorisation first (claim[1]: CTAs started, claim[2]: CTAs allowed,
+// claim[3]: SMs taken, claim[4 + smid]: 0 unseen, 1 allowed, 2 refused, 3 deciding; a refused CTA
+// that starts last while none was allowed works anyway, so every launch completes its slots).
+template <int NW>
+__global__ void __launch_bounds__(LpCfg<NW>::THREADS, LpCfg<NW>::CTAS)
+k_bfactor_lp(FactorSrc src, DevSketch skb, double* __restrict__ Ginv, long long ldgi,
+             long long gi_stride, double* work, long long work_stride, int* __restrict__ flags,
+             const Ctrl* ctrl, int nslots, int* claim, int max_sms) {
+  __shared__ int s_bad, s_stop, s_slot;
+  const int tid = threadIdx.x;
+  if (!claim) {
+    lp_factor_slot<NW>(src, skb, Ginv, ldgi, gi_stride, work, work_stride, flags, ctrl, blockIdx.x,
+                       s_bad, s_stop);
+    return;
+  }
+  if (tid == 0) {
+    unsigned sm;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+    int* st = claim + 4 + (sm & 255);
+    int v = atomicCAS(st, 0, 3);
+    if (v == 0) {   // first CTA on this SM: take it if the budget allows
+      v = atomicAdd(claim + 3, 1) < max_sms ? 1 : 2;
+      atomicExch(st, v);
+    }
+    while (v == 3) v = *reinterpret_cast<volatile int*>(st);
+    if (v == 1) atomicAdd(claim + 2, 1);
+    __threadfence();
+    const int started = atomicAdd(claim + 1, 1);
+    if (v != 1 && started == (int)gridDim.x - 1 && atomicAdd(claim + 2, 0) == 0) v = 1;
+    s_slot = v == 1 ? 0 : -1;
+  }
+  __syncthreads();
+  if (s_slot < 0) return;
+  for (;;) {
+    __syncthreads();   // (s_slot read by every thread of the previous round)
+    if (tid == 0) s_slot = atomicAdd(claim, 1);
+    __syncthreads();
+    const int slot = s_slot;
+    if (slot >= nslots) return;
+    if (!lp_factor_slot<NW>(src, skb, Ginv, ldgi, gi_stride, work, work_stride, flags, ctrl, slot,
+                            s_bad, s_stop))
+      return;
+  }
 }
 
 }  // namespace
@@ -1127,7 +1209,7 @@ size_t bfactor_work_elems(int tau) {
   if (tau <= BF_MAXTAU) return 0;
   const long long tp = bb_tp(tau);
   // work matrix, Tc L_pp^{-1} tiles, then Tc tiles (right-looking T_I) or 2 per warp (left-looking)
-  return (size_t)(tp * tp + (tp / 32) * 1024 + std::max<long long>(tp / 32, 2 * LP_WARPS) * 1024);
+  return (size_t)(tp * tp + (tp / 32) * 1024 + std::max<long long>(tp / 32, 16) * 1024);
 }
 
 cudaError_t bfactor_init() {
@@ -1143,7 +1225,11 @@ cudaError_t bfactor_init() {
   if (e != cudaSuccess) return e;
   e = cudaFuncSetAttribute(k_bf_gather, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)GA_SMEM);
   if (e != cudaSuccess) return e;
-  e = cudaFuncSetAttribute(k_bfactor_lp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)LP_SMEM);
+  e = cudaFuncSetAttribute(k_bfactor_lp<8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)LpCfg<8>::SMEM);
+  if (e != cudaSuccess) return e;
+  e = cudaFuncSetAttribute(k_bfactor_lp<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)LpCfg<4>::SMEM);
   if (e != cudaSuccess) return e;
   return cudaFuncSetAttribute(k_bfactor_small, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               (int)bf_smem(BF_MAXTAU));
@@ -1151,7 +1237,7 @@ cudaError_t bfactor_init() {
 
 cudaError_t launch_bfactor(const FactorSrc& src, const DevSketch& skb, int nslots, double* Ginv,
                            long long ldgi, long long gi_stride, int* flags, double* work,
-                           const Ctrl* ctrl, cudaStream_t st) {
+                           const Ctrl* ctrl, cudaStream_t st, bool dual, const BfClaim* claim) {
   if (skb.tau > BB_MAXTAU || nslots < 1) return cudaErrorInvalidValue;
   if (skb.tau > BF_MAXTAU) {
     if (!work) return cudaErrorInvalidValue;
@@ -1159,9 +1245,21 @@ cudaError_t launch_bfactor(const FactorSrc& src, const DevSketch& skb, int nslot
     const long long ws = (long long)bfactor_work_elems(skb.tau);
     k_bf_gather<<<dim3((unsigned)((tp + GA_WARPS - 1) / GA_WARPS), (unsigned)nslots), GA_WARPS * 32,
                   std::min(GA_SMEM, (size_t)(skb.tau + 1 + skb.len) * 4), st>>>(src, skb, work, ws, ctrl);
-    k_bfactor_lp<<<nslots, LP_THREADS, LP_SMEM, st>>>(src, skb, Ginv, ldgi, gi_stride, work,
-                                                        (long long)bfactor_work_elems(skb.tau), flags,
-                                                        ctrl);
+    int* cw = claim ? claim->words : nullptr;
+    const int max_sms = claim ? claim->max_sms : 0;
+    const int cps = dual ? LpCfg<4>::CTAS : LpCfg<8>::CTAS;
+    // (claimed slots: CTAs on every SM, so that those refused by the SM budget leave enough workers)
+    const unsigned grid = (unsigned)(claim ? cps * claim->num_sms : nslots);
+    if (cw) {
+      const cudaError_t e = cudaMemsetAsync(cw, 0, BF_CLAIM_WORDS * sizeof(int), st);
+      if (e != cudaSuccess) return e;
+    }
+    if (dual)
+      k_bfactor_lp<4><<<grid, LpCfg<4>::THREADS, LpCfg<4>::SMEM, st>>>(
+          src, skb, Ginv, ldgi, gi_stride, work, ws, flags, ctrl, nslots, cw, max_sms);
+    else
+      k_bfactor_lp<8><<<grid, LpCfg<8>::THREADS, LpCfg<8>::SMEM, st>>>(
+          src, skb, Ginv, ldgi, gi_stride, work, ws, flags, ctrl, nslots, cw, max_sms);
     return cudaGetLastError();
   }
   k_bfactor_small<<<nslots, BF_THREADS, bf_smem(skb.tau), st>>>(src, skb, Ginv, ldgi, gi_stride,

@@ -37,6 +37,8 @@ Problem::~Problem() {
   if (st2) cudaStreamDestroy(st2);
   if (ev_fork) cudaEventDestroy(ev_fork);
   if (ev_join) cudaEventDestroy(ev_join);
+  if (ev_pro) cudaEventDestroy(ev_pro);
+  if (ev_pro_tail) cudaEventDestroy(ev_pro_tail);
   if (own_X) dfree(X);
   if (own_Xo) dfree(Xo);
   dfree(y);
@@ -105,6 +107,8 @@ void Problem::free_workspace() {
   slot_flags = nullptr;
   dfree(bf_work);
   bf_work = nullptr;
+  dfree(bf_claim);
+  bf_claim = nullptr;
   dfree(it_scratch);
   it_scratch = nullptr;
   use_iterate = false;
@@ -630,7 +634,10 @@ rs_status Problem::ensure_workspace(int kind, int tau, int ksum, int depth, bool
     gi_stride = (long long)tau * ld_gi;
     RS_TRY(dalloc(&Ginv_slots, (size_t)gi_stride * depth));
     RS_TRY(dalloc(&slot_flags, depth));
+    // (two slot sets: the second region also serves the first set's tail, factored beside the
+    // first group)
     if (bfactor_work_elems(tau)) RS_TRY(dalloc(&bf_work, bfactor_work_elems(tau) * depth));
+    if (xg) RS_TRY(dalloc(&bf_claim, 2 * BF_CLAIM_WORDS));   // two concurrent launches' claims
     // EXPLICIT: the group's iterations as one persistent kernel (iterate.cu)
     use_iterate = mode == RS_AS_EXPLICIT && iterate_ok(sk, m, xg ? OV_SMS : num_sms);
     if (use_iterate) RS_TRY(dalloc(&it_scratch, 2 * (size_t)tau + num_sms));
@@ -725,7 +732,7 @@ rs_status Problem::enqueue_iteration(const rs_solve_opts* o, cudaEvent_t* ev) {
 
 // Group precompute of the sketch-ahead pipeline: sketches S_{k0..k0+ns-1} (k0 = ctrl->k), their
 // A S^T rows (explicit) or Grams (XS)^T XS (gram), and the batched factorisation Ginv = G^{-1}.
-rs_status Problem::enqueue_precompute(const rs_solve_opts* o, int ns, cudaEvent_t* ev) {
+rs_status Problem::enqueue_precompute(const rs_solve_opts* o, int ns, cudaEvent_t* ev, int split) {
   // ev (optional): the event sets of iterations k0 .. k0+ns-1, 2 * RS_K_NCLASSES each; the group's
   // sketches and factorisation are recorded on iteration k0's, slot q's Gram on iteration k0+q's
   auto mark = [&](int q, int cls, int edge) {
@@ -774,8 +781,25 @@ rs_status Problem::enqueue_precompute(const rs_solve_opts* o, int ns, cudaEvent_
     src.lambda = lambda;
   }
   mark(0, RS_K_FACTOR, 0);
-  RS_CUDA(launch_bfactor(src, skb, ns, Ginv_slots, ld_gi, gi_stride, slot_flags, bf_work, ctrl,
-                         st));                                                              // a4+a5
+  if (split > 0 && split < ns) {   // the overlapped pipeline's first set (see solve): slots [0, split)
+    // here, one per SM; slots [split, ns) on st2 with their own scratch, flagged -1 until factored
+    RS_CUDA(launch_bfactor(src, skb, split, Ginv_slots, ld_gi, gi_stride, slot_flags, bf_work, ctrl,
+                           st, false));                                                     // a4+a5
+    RS_CUDA(cudaMemsetAsync(slot_flags + split, 0xff, sizeof(int) * (size_t)(ns - split), st));
+    RS_CUDA(cudaEventRecord(ev_pro, st));
+    RS_CUDA(cudaStreamWaitEvent(st2, ev_pro, 0));
+    FactorSrc s2 = src;
+    if (s2.ASt) s2.ASt += (long long)split * as_stride;
+    const BfClaim cl{bf_claim + BF_CLAIM_WORDS, num_sms - OV_SMS, num_sms};
+    RS_CUDA(launch_bfactor(s2, skb.at(split), ns - split, Ginv_slots + (long long)split * gi_stride,
+                           ld_gi, gi_stride, slot_flags + split,
+                           bf_work + (long long)bfactor_work_elems((int)o->tau) * P, ctrl, st2, false,
+                           &cl));
+    RS_CUDA(cudaEventRecord(ev_pro_tail, st2));
+  } else {
+    RS_CUDA(launch_bfactor(src, skb, ns, Ginv_slots, ld_gi, gi_stride, slot_flags, bf_work, ctrl,
+                           st, bf_dual));                                                   // a4+a5
+  }
   mark(0, RS_K_FACTOR, 1);
   return RS_OK;
 }
@@ -849,6 +873,7 @@ rs_status Problem::enqueue_iterate_group(const rs_solve_opts* o, int ns, cudaEve
   ia.beta = o->beta;
   ia.nslots = ns;
   ia.big = skb.tau > 224;
+  ia.wait = pipe_ov ? 1 : 0;   // the first set's tail may still be factored on st2 (solve)
   RS_CUDA(launch_iterate(ia, grid > 0 ? grid : num_sms, ctrl, st));
   if (ev) cudaEventRecordWithFlags(ev[2 * RS_K_UPDATE + 1], st, cudaEventRecordExternal);
   return RS_OK;
@@ -883,8 +908,10 @@ rs_status Problem::enqueue_group_ov(const rs_solve_opts* o, int g, cudaEvent_t* 
     src.A = A;
     src.lda = lda;
   }
+  // at most num_sms - OV_SMS SMs, the same ones in every group (BfClaim)
+  const BfClaim cl{bf_claim, num_sms - OV_SMS, num_sms};
   RS_CUDA(launch_bfactor(src, sn, P, Ginv_slots + (long long)nxt * P * gi_stride, ld_gi, gi_stride,
-                         slot_flags + (long long)nxt * P, bf_work, ctrl, st2));   // a4 + a5 ahead
+                         slot_flags + (long long)nxt * P, bf_work, ctrl, st2, bf_dual, &cl));   // a4 + a5 ahead
   mark(st2, 0, RS_K_FACTOR, 1);
   RS_CUDA(cudaEventRecord(ev_join, st2));
   RS_TRY(enqueue_iterate_group(o, P, ev, cur * P, OV_SMS));                       // a4-a7 x P
@@ -946,19 +973,28 @@ rs_status Problem::solve(const rs_solve_opts* o, double* w_out, rs_mem w_mem, do
   // iterations per CUDA-graph launch (between host reads of the stop flag)
   int chunk = (int)(o->check_every > 0 ? std::min<long long>(o->check_every, 1024)
                                        : (want_pipe ? (o->tau > 224 ? num_sms : 64) : 16));
+  // overlapped pipeline: the batched factorisation runs two slots per SM (k_bfactor_lp<4>), so a
+  // wave holds 2 x (free SMs) slots (RS_BF_DUAL=0: the 8-warp shape, one per SM)
+  static const bool dual_env = [] {
+    const char* e = std::getenv("RS_BF_DUAL");
+    return !(e && e[0] == '0');
+  }();
   // EXPLICIT with tau > 224: overlap the next group's factorisation with the current group's
   // iterations when that shortens an iteration.  Per-iteration estimates: the factor's 2 tau^3 / 3
-  // flop at ~15 TFLOP/s on all SMs (measured, ~0.4 of the DMMA peak; num_sms / (num_sms - OV_SMS)
-  // slower on the SMs the overlap leaves it), the group kernel's sketched rows of A (len m 8 bytes)
-  // at ~45 GB/s per SM plus ~15 us of barriers (profiles/README.md, k_iterate phases)
+  // flop at ~20 TFLOP/s on all SMs (two slots per SM; ~15 one per SM; measured on c5, num_sms /
+  // (num_sms - OV_SMS) slower on the SMs the overlap leaves it), the group kernel's sketched rows
+  // of A (len m 8 bytes) at ~45 GB/s per SM plus ~15 us of barriers (profiles/README.md, k_iterate
+  // phases)
   const double tau_d = (double)o->tau;
   const double len_d = (double)sketch_max_len((int)o->kind, (int)m, (int)o->tau, ksum);
-  const double f_us = 2.0 * tau_d * tau_d * tau_d / 3.0 / 15e6;
+  const double f_us = 2.0 * tau_d * tau_d * tau_d / 3.0 / (dual_env ? 20e6 : 15e6);
   auto it_us = [&](int sms) { return len_d * (double)m * 8.0 / (sms * 45e3) + 15.0; };
   const double ov_us = std::max(f_us * num_sms / std::max(1, num_sms - OV_SMS), it_us(OV_SMS));
   const bool want_ov = want_pipe && mode == RS_AS_EXPLICIT && o->tau > 224 && num_sms > 2 * OV_SMS &&
                        len_d <= 8192 && ov_us < f_us + it_us(num_sms);
-  if (want_ov) chunk = 2 * (num_sms - OV_SMS);
+  bf_dual = want_ov && dual_env;
+  const int cps = bf_dual ? 2 : 1;
+  if (want_ov) chunk = 2 * cps * (num_sms - OV_SMS);
   const bool want_xg = want_ov;   // two slot sets
   if (want_xg) chunk = std::max(2, chunk & ~1);   // two groups of P = chunk / 2
   int depth = 0;
@@ -967,10 +1003,10 @@ rs_status Problem::solve(const rs_solve_opts* o, double* w_out, rs_mem w_mem, do
         8LL * o->tau * (mode == RS_AS_EXPLICIT ? (o->kind == RS_SKETCH_COUNT ? round_up(m, 4) : 0)
                                                : round_up(o->tau, 4)) +
         8LL * o->tau * round_up(o->tau, 4) + 16LL * m + 8LL * (long long)bfactor_work_elems((int)o->tau);
-    depth = (int)std::max<long long>(1, std::min<long long>({(long long)chunk, (long long)num_sms,
+    depth = (int)std::max<long long>(1, std::min<long long>({(long long)chunk, (long long)cps * num_sms,
                                                              6000000000LL / slot_bytes}));
     if (want_xg) {
-      depth = std::min<long long>({(long long)depth, (long long)chunk / 2, 3000000000LL / slot_bytes});
+      depth = std::min<long long>({(long long)depth, (long long)chunk / 2, 5000000000LL / slot_bytes});
       chunk = 2 * depth;
     }
   }
@@ -980,6 +1016,8 @@ rs_status Problem::solve(const rs_solve_opts* o, double* w_out, rs_mem w_mem, do
     RS_CUDA(cudaStreamCreateWithFlags(&st2, cudaStreamNonBlocking));
     RS_CUDA(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
     RS_CUDA(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming));
+    RS_CUDA(cudaEventCreateWithFlags(&ev_pro, cudaEventDisableTiming));
+    RS_CUDA(cudaEventCreateWithFlags(&ev_pro_tail, cudaEventDisableTiming));
   }
   // state: w^{-1} = w^0 = 0, r^{-1} = r^0 = -b
   RS_CUDA(launch_fill(w, m, 0.0, st));
@@ -1089,8 +1127,19 @@ rs_status Problem::solve(const rs_solve_opts* o, double* w_out, rs_mem w_mem, do
   if (timing) fprintf(stderr, "[rs] solve preamble %.3f ms (graph %s)\n", hms(h0), rebuild ? "built" : "reused");
   const auto h1 = std::chrono::steady_clock::now();
   RS_CUDA(cudaEventRecord(t0, st));
-  // overlapped pipeline: slot set 0 (iterations 0 .. P-1) is formed and factored up front
-  if (pipe_xg && !ctrl_host->done) RS_TRY(enqueue_precompute(o, P, nullptr));
+  // overlapped pipeline: slot set 0 (iterations 0 .. P-1) is formed and factored up front -- with two
+  // slots per SM in the steady state (P > num_sms), its first num_sms slots as one wave of the 8-warp
+  // shape on every SM, the rest on st2 beside the first group, whose iterations wait per slot
+  bool pro_tail = false;
+  if (pipe_xg && !ctrl_host->done) {
+    static const bool split_env = [] {   // RS_OV_SPLIT=0: the whole first set up front
+      const char* e = std::getenv("RS_OV_SPLIT");
+      return !(e && e[0] == '0');
+    }();
+    const int split = pipe_ov && split_env && P > num_sms ? num_sms : P;
+    RS_TRY(enqueue_precompute(o, P, nullptr, split));
+    pro_tail = split < P;
+  }
   long long k_prev = 0, graph_launches = 0;
   while (!ctrl_host->done) {
     RS_CUDA(cudaGraphLaunch(graph_exec, st));
@@ -1124,6 +1173,7 @@ rs_status Problem::solve(const rs_solve_opts* o, double* w_out, rs_mem w_mem, do
     }
     k_prev = ctrl_host->k;
   }
+  if (pro_tail) RS_CUDA(cudaStreamWaitEvent(st, ev_pro_tail, 0));   // (stops early once done)
   RS_CUDA(cudaEventRecord(t1, st));
   RS_CUDA(cudaEventSynchronize(t1));
   const auto h2 = std::chrono::steady_clock::now();

@@ -102,6 +102,7 @@ struct Problem {
   double* Ginv_slots = nullptr;
   long long ld_gi = 0, gi_stride = 0;
   int* slot_flags = nullptr;
+  int* bf_claim = nullptr;   // overlapped pipeline: factor SM registry + tickets (BfClaim)
   double* bf_work = nullptr;     // tau > 224: per-slot work matrices of the batched factorisation
   double* it_scratch = nullptr;  // EXPLICIT group kernel (iterate.cu): t, delta (tau each), partials
   bool use_iterate = false;
@@ -109,9 +110,11 @@ struct Problem {
   // current group's iterations (st, k_iterate on the SMs the factor grid leaves free)
   bool pipe_xg = false;   // two slot sets
   bool pipe_ov = false;
+  bool bf_dual = false;   // tau > 224: the 4-warp factorisation, two slots per SM
   int ws_xg = -1;
   cudaStream_t st2 = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  cudaEvent_t ev_pro = nullptr, ev_pro_tail = nullptr;   // first set's tail on st2 (solve)
   SolveWork sw{};
   double* partials = nullptr;
   cudaGraphExec_t graph_exec = nullptr;
@@ -124,7 +127,8 @@ struct Problem {
   rs_status allreduce(double* buf, size_t count);
   rs_status ensure_workspace(int kind, int tau, int ksum, int depth, bool xg = false);
   rs_status enqueue_iteration(const rs_solve_opts* o, cudaEvent_t* ev);
-  rs_status enqueue_precompute(const rs_solve_opts* o, int nslots, cudaEvent_t* ev);
+  // split < nslots: the overlapped pipeline's first set, slots [split, nslots) factored on st2
+  rs_status enqueue_precompute(const rs_solve_opts* o, int nslots, cudaEvent_t* ev, int split = 0);
   rs_status enqueue_pipelined_iteration(const rs_solve_opts* o, int slot, cudaEvent_t* ev);
   rs_status enqueue_iterate_group(const rs_solve_opts* o, int ns, cudaEvent_t* ev, int slot0 = 0,
                                   int grid = 0);

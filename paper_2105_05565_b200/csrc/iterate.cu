@@ -28,6 +28,7 @@ namespace {
 namespace cg = cooperative_groups;
 
 constexpr int IT_WARPS = 16;
+constexpr int IT_NG = 4;   // 64-column chunks per pass of phase C
 constexpr int IT_THREADS = IT_WARPS * 32;
 constexpr int IT_MAXTAU = 4096;
 constexpr int IT_MAXLEN = 8192;
@@ -71,7 +72,7 @@ __device__ __forceinline__ double row_dot(const double* __restrict__ row, const 
 #pragma unroll
     for (int u = 0; u < 32; ++u) {
       const int c = cb + lane + 32 * u;
-      v[u] = c < c1 ? __ldg(row + c) : 0.0;
+      v[u] = c < c1 ? __ldcg(row + c) : 0.0;   // (L2: the slot may be written during this launch)
     }
 #pragma unroll
     for (int u = 0; u < 32; ++u) {
@@ -99,7 +100,7 @@ __global__ void __launch_bounds__(IT_THREADS, 1)
 k_iterate(IterArgs a, Ctrl* ctrl) {
   cg::grid_group grid = cg::this_grid();
   extern __shared__ __align__(16) double it_sm[];
-  __shared__ double red[IT_WARPS][66];
+  __shared__ double s_wp[IT_WARPS];   // per-warp partials of the block reductions
   __shared__ double s_r2;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int G = gridDim.x, gw = blockIdx.x * IT_WARPS + warp, GW = G * IT_WARPS;
@@ -116,6 +117,9 @@ k_iterate(IterArgs a, Ctrl* ctrl) {
   int* s_ce = reinterpret_cast<int*>(coef + len_c);     // [len] coord (sign as complement)
   int* s_bk = s_ce + len_c;                             // [len] bucket
   int* s_bp = s_bk + len_c;                             // [tau + 1]
+  int* s_ro = s_bp + tau_c + 1;                         // [len] row offsets of u's rows (16 B units)
+  double* red = reinterpret_cast<double*>(                               // [IT_WARPS][IT_NG][64]
+      (reinterpret_cast<uintptr_t>(s_ro + len_c) + 15) & ~(uintptr_t)15);
   const double rsb = 1.0 / sqrt(c0.bnorm2);
   if (a.nslots > 0) stage_sketch(a.skb.at(0), s_ce, s_bk, s_bp, tid);
   __syncthreads();
@@ -123,7 +127,17 @@ k_iterate(IterArgs a, Ctrl* ctrl) {
     const int tau = a.skb.tau;
     const int len = s_bp[tau];
     const double* Gi = a.Ginv + (long long)q * a.gi_stride;
-    if (a.flags[q]) {   // the group's factorisation found S^T A S not SPD (uniform)
+    if (a.wait) {   // the slot may still be in a concurrent factorisation kernel (flag -1)
+      if (tid == 0) {
+        const volatile int* f = a.flags + q;
+        while (*f < 0 && !*reinterpret_cast<const volatile int*>(&ctrl->done)) __nanosleep(500);
+        __threadfence();
+      }
+      __syncthreads();
+    }
+    const int fq = __ldcg(a.flags + q);
+    if (fq < 0) return;   // (only if the solve stopped meanwhile)
+    if (fq) {   // the group's factorisation found S^T A S not SPD (uniform)
       if (blockIdx.x == 0 && tid == 0) {
         ctrl->status = ST_NOTSPD;
         ctrl->done = 1;
@@ -197,51 +211,73 @@ k_iterate(IterArgs a, Ctrl* ctrl) {
       IT_ADD(3, tb1, tb2);
     }
     IT_T(tc0);
-    // ---- phase C: u_j = sum_rows coef_row X[row][j] over this CTA's columns; heavy-ball update
+    // ---- phase C: u_j = sum_rows coef_row X[row][j] over this CTA's columns; heavy-ball update.
+    // Coefficients and row offsets once per iteration; then per batch of 16 rows per lane the
+    // offsets are read once and reused by up to IT_NG 64-column chunks (lane = a column pair,
+    // 16-byte loads: lda and ld_as are multiples of 4, so the pair's second element is inside the
+    // row even at an odd m), the chunks' warp partials reduced in one barrier round
     for (int e = tid; e < nr; e += IT_THREADS) {
+      int row;
       if (a.ASt) {
         coef[e] = __ldcg(a.dvec + e);
+        row = e;
       } else {
         const double d = __ldcg(a.dvec + s_bk[e]);
-        coef[e] = s_ce[e] >= 0 ? d : -d;
+        const int ce = s_ce[e];
+        coef[e] = ce >= 0 ? d : -d;
+        row = ce >= 0 ? ce : ~ce;
       }
+      s_ro[e] = (int)(((long long)row * ldx) >> 1);
     }
     __syncthreads();
-    // 64-column chunks, lane = a column pair (16-byte loads: lda and ld_as are multiples of 4, so
-    // the pair's second element is inside the row even at an odd m), 16 rows per lane in flight
+    const double2* X2 = reinterpret_cast<const double2*>(X);
     double r2 = 0.0;
-    for (long long jb = j0; jb < j1; jb += 64) {
-      const long long j = jb + 2 * lane;
-      const bool jin = j < j1;
-      double s0 = 0.0, s1 = 0.0;
+    const int nch = (int)((j1 - j0 + 63) / 64);
+    for (int c0 = 0; c0 < nch; c0 += IT_NG) {
+      double s[IT_NG][2];
+#pragma unroll
+      for (int c = 0; c < IT_NG; ++c) s[c][0] = s[c][1] = 0.0;
       for (int eb = warp; eb < nr; eb += 16 * IT_WARPS) {
-        double2 x[16];
+        int off[16];
 #pragma unroll
         for (int u = 0; u < 16; ++u) {
           const int e = eb + IT_WARPS * u;
-          int row = 0;
-          if (e < nr) row = a.ASt ? e : (s_ce[e] >= 0 ? s_ce[e] : ~s_ce[e]);
-          x[u] = (jin && e < nr) ? __ldg(reinterpret_cast<const double2*>(X + (long long)row * ldx + j))
-                                 : make_double2(0.0, 0.0);
+          off[u] = e < nr ? s_ro[e] : -1;
         }
 #pragma unroll
-        for (int u = 0; u < 16; ++u) {
-          const int e = eb + IT_WARPS * u;
-          if (e < nr) {
-            s0 += coef[e] * x[u].x;
-            s1 += coef[e] * x[u].y;
+        for (int c = 0; c < IT_NG; ++c) {
+          if (c0 + c >= nch) break;   // (warp-uniform)
+          const long long j = j0 + 64LL * (c0 + c) + 2 * lane;
+          const bool jin = j < j1;
+          const long long jh = j >> 1;
+          double2 x[16];
+#pragma unroll
+          for (int u = 0; u < 16; ++u)
+            x[u] = (jin && off[u] >= 0) ? __ldg(X2 + off[u] + jh) : make_double2(0.0, 0.0);
+#pragma unroll
+          for (int u = 0; u < 16; ++u) {
+            if (off[u] >= 0) {
+              const double cf = coef[eb + IT_WARPS * u];
+              s[c][0] += cf * x[u].x;
+              s[c][1] += cf * x[u].y;
+            }
           }
         }
       }
-      red[warp][2 * lane] = s0;
-      red[warp][2 * lane + 1] = s1;
+#pragma unroll
+      for (int c = 0; c < IT_NG; ++c) {
+        red[(warp * IT_NG + c) * 64 + 2 * lane] = s[c][0];
+        red[(warp * IT_NG + c) * 64 + 2 * lane + 1] = s[c][1];
+      }
       __syncthreads();
-      if (warp == 0 && jin) {
+      const int c = warp;   // warp c < IT_NG updates chunk c0 + c (fixed warp order in the sum)
+      if (c < IT_NG && c0 + c < nch) {
+        const long long j = j0 + 64LL * (c0 + c) + 2 * lane;
         double u0 = 0.0, u1 = 0.0;
 #pragma unroll
         for (int w = 0; w < IT_WARPS; ++w) {
-          u0 += red[w][2 * lane];
-          u1 += red[w][2 * lane + 1];
+          u0 += red[(w * IT_NG + c) * 64 + 2 * lane];
+          u1 += red[(w * IT_NG + c) * 64 + 2 * lane + 1];
         }
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
@@ -260,16 +296,15 @@ k_iterate(IterArgs a, Ctrl* ctrl) {
           r2 += rj * rj;
         }
       }
-      __syncwarp();
       __syncthreads();
     }
     // r2: block reduction into warp 0 (fixed order)
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) r2 += __shfl_xor_sync(0xffffffffu, r2, o);
-    if (lane == 0) red[warp][0] = r2;
+    if (lane == 0) s_wp[warp] = r2;
     __syncthreads();
     if (warp == 0) {
-      r2 = lane < IT_WARPS ? red[lane][0] : 0.0;
+      r2 = lane < IT_WARPS ? s_wp[lane] : 0.0;
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) r2 += __shfl_xor_sync(0xffffffffu, r2, o);
       if (lane == 0) a.partials[blockIdx.x] = r2;
@@ -322,12 +357,20 @@ k_iterate(IterArgs a, Ctrl* ctrl) {
 
 }  // namespace
 
-size_t iterate_smem() { return 218 * 1024; }   // + ~8.4 KB static <= the 227 KB opt-in
+size_t iterate_smem() { return 218 * 1024; }   // + the small static arrays <= the 227 KB opt-in
+
+// dynamic shared memory: g / t and the coefficients (doubles), sketch entries, buckets, bucket
+// pointers and row offsets (ints), phase C's reduction buffer
+static size_t it_smem_bytes(int tau, int len) {
+  return (size_t)(tau + len) * 8 + (size_t)(2 * len + tau + 1) * 4 + (size_t)len * 4 + 16 +
+         (size_t)IT_WARPS * IT_NG * 64 * 8;
+}
 
 bool iterate_ok(const DevSketch& sk, long long m, int grid) {
-  (void)m;
   (void)grid;
-  return sk.tau <= IT_MAXTAU && sk.len <= IT_MAXLEN;
+  // phase C's row offsets are 32-bit in 16-byte units: m x round_up(m, 4) / 2 < 2^31
+  return sk.tau <= IT_MAXTAU && sk.len <= IT_MAXLEN && it_smem_bytes(sk.tau, sk.len) <= iterate_smem() &&
+         m * ((m + 3) / 4 * 4) / 2 < (1LL << 31);
 }
 
 #ifdef RS_IT_PHASES
@@ -349,7 +392,7 @@ cudaError_t iterate_init() {
 cudaError_t launch_iterate(const IterArgs& args, int grid, Ctrl* ctrl, cudaStream_t st) {
   IterArgs a = args;
   // shared memory: the sketch staging of one slot (g / t, coefficients, entries, bucket pointers)
-  const size_t smem = (size_t)(a.skb.tau + a.skb.len) * 8 + (size_t)(2 * a.skb.len + a.skb.tau + 1) * 4;
+  const size_t smem = it_smem_bytes(a.skb.tau, a.skb.len);
   if (smem > iterate_smem()) return cudaErrorInvalidValue;
   int per_sm = 0;
   cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_iterate, IT_THREADS, smem);
@@ -362,11 +405,17 @@ cudaError_t launch_iterate(const IterArgs& args, int grid, Ctrl* ctrl, cudaStrea
   cfg.blockDim = dim3(IT_THREADS);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
-  cudaLaunchAttribute attr[1];
+  // top priority: in the overlapped pipeline the group's CTAs must take their SMs before the
+  // concurrent factorisation's CTAs (two per SM) fill every SM
+  int least = 0, greatest = 0;
+  cudaDeviceGetStreamPriorityRange(&least, &greatest);
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeCooperative;
   attr[0].val.cooperative = 1;
+  attr[1].id = cudaLaunchAttributePriority;
+  attr[1].val.priority = greatest;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = 2;
   return cudaLaunchKernelExC(&cfg, (const void*)k_iterate, kargs);
 }
 

@@ -213,9 +213,11 @@ struct IterArgs {
   double gamma, beta;
   int nslots;                    // iterations of the group
   int big;                       // tau > 224
+  int wait;                      // flags[q] < 0: slot q is still being factored (by a concurrent
+                                 // kernel), spin until it is 0 or 1
 };
 // SMs left to the iterations while the next group's factorisation runs (EXPLICIT, tau > 224)
-constexpr int OV_SMS = 22;
+constexpr int OV_SMS = 32;
 size_t iterate_smem();
 bool iterate_ok(const DevSketch& sk, long long m, int grid);   // the group kernel applies
 cudaError_t iterate_init();
@@ -308,9 +310,20 @@ cudaError_t bfactor_init();
 // flags[s] = 1 if G of slot s was not SPD (a pivot <= 0 or non-finite after the empty-bucket rule)
 // tau > 224: `work` = nslots x bfactor_work_elems(tau) doubles of scratch (null otherwise).
 size_t bfactor_work_elems(int tau);
+// tau > 224: `dual` selects the 4-warp k_bfactor_lp, two CTAs (slots) per SM -- for a wave of about
+// 2 x (free SMs) slots; else the 8-warp shape, one CTA per SM.  claim (optional): slots are claimed
+// dynamically by CTAs on every SM, of which those beyond max_sms distinct SMs step aside, leaving
+// num_sms - max_sms SMs to a concurrent kernel; `words` (BF_CLAIM_WORDS ints, reset by the launch)
+// is the launch's ticket and SM registry -- one per concurrently running launch.
+constexpr int BF_CLAIM_WORDS = 4 + 256;
+struct BfClaim {
+  int* words;
+  int max_sms, num_sms;
+};
 cudaError_t launch_bfactor(const FactorSrc& src, const DevSketch& skb, int nslots, double* Ginv,
                            long long ldgi, long long gi_stride, int* flags, double* work,
-                           const Ctrl* ctrl, cudaStream_t st);
+                           const Ctrl* ctrl, cudaStream_t st, bool dual = false,
+                           const BfClaim* claim = nullptr);
 // delta = Ginv (S^T r), sdelta[coord_e] = sign_e delta[bucket_e]; flag != 0 -> status NOTSPD.
 // tau <= 224: the slot holds G^{-1} (full); tau > 224: it holds W = L^{-1} (lower) and
 // delta = W^T (W g).  gbuf: 2 tau doubles of scratch (g, W g).

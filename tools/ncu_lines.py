@@ -17,8 +17,13 @@ per = [[int(r[j] or 0) for j in ri] for r in rows[2:]]
 sass = [r[1].strip() for r in rows[2:]]
 d = tempfile.mkdtemp()
 subprocess.run(["cuobjdump", "-xelf", "all", os.path.abspath(obj)], cwd=d, capture_output=True)
-cub = [os.path.join(d, f) for f in os.listdir(d) if f.endswith(".cubin")][0]
-dis = subprocess.run(["nvdisasm", "-g", "-c", cub], capture_output=True, text=True).stdout
+dis = ""
+for f in sorted(os.listdir(d)):   # the cubin that holds the kernel (a .so carries one per source)
+    if f.endswith(".cubin"):
+        t = subprocess.run(["nvdisasm", "-g", "-c", os.path.join(d, f)], capture_output=True, text=True).stdout
+        if re.search(r'\.text\.\S*' + re.escape(kname), t):
+            dis = t
+            break
 lines, cur, fn = [], None, None
 for ln in dis.splitlines():
     m = re.match(r'\s*\.text\.(\S+):', ln)
