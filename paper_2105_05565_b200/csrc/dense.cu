@@ -9,6 +9,7 @@
 //      FP64 tensor path and measures 37.1 TFLOP/s on this B200 (profiles/r01_fp64_peak.txt).
 //  explicit A = X^T X + lambda I is the same TN contraction with Bop = X, built once.
 //  explicit a2: AS^T[b,:] = sum_{e in b} sign_e A[coord_e, :] (A symmetric, rows are columns).
+#include <cmath>
 #include <algorithm>
 
 #include "rs_internal.cuh"
@@ -100,6 +101,72 @@ k_dense_xs_warp(const double* __restrict__ X, long long ldx, long long rows, Dev
         }
       }
     }
+  }
+}
+
+// a2 when the sketch touches most 128-byte lines of a row (1 - (1 - len/d)^16 >= 0.7, e.g. c5's
+// tau = 1024 of d = 4096): each row is streamed whole into shared memory by one cp.async.bulk (two
+// rows in flight per CTA, mbarrier transaction counts) and gathered there, so X is read exactly
+// once; the per-lane gathers of k_dense_xs_warp re-fetch lines between passes (ncu: 115 GB of DRAM
+// reads per c5 XS for the 65.5 GB X).  Needs 16-byte aligned rows (X, ldx even, d even).
+constexpr int XR_THREADS = 256;
+__device__ __forceinline__ unsigned xr_su32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__global__ void __launch_bounds__(XR_THREADS)
+k_dense_xs_rows(const double* __restrict__ X, long long ldx, long long rows, DevSketch sk,
+                double* __restrict__ XS, long long ld_xs, const Ctrl* ctrl, int slot) {
+  if (slot_unused(ctrl, slot)) return;
+  extern __shared__ __align__(16) double xr_sm[];
+  const int d = sk.m, tau = sk.tau, len = sk.len, tid = threadIdx.x;
+  double* buf0 = xr_sm;                                            // [2][d]
+  uint64_t* bar = reinterpret_cast<uint64_t*>(xr_sm + 2 * (long long)d);
+  int* s_bp = reinterpret_cast<int*>(bar + 2);
+  int* s_ce = s_bp + tau + 1;
+  for (int b = tid; b <= tau; b += XR_THREADS) s_bp[b] = sk.bptr[b];
+  for (int e = tid; e < len; e += XR_THREADS) s_ce[e] = sk.sign[e] > 0 ? sk.coord[e] : ~sk.coord[e];
+  const unsigned bytes = (unsigned)d * 8u;
+  auto issue = [&](int s, long long i) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(xr_su32(&bar[s])),
+                 "r"(bytes) : "memory");
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n"
+        ::"r"(xr_su32(buf0 + (long long)s * d)), "l"(X + i * ldx), "r"(bytes), "r"(xr_su32(&bar[s]))
+        : "memory");
+  };
+  const long long i0 = blockIdx.x, di = gridDim.x;
+  if (tid == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(xr_su32(&bar[0])));
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(xr_su32(&bar[1])));
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    if (i0 < rows) issue(0, i0);
+    if (i0 + di < rows) issue(1, i0 + di);
+  }
+  __syncthreads();
+  const bool single = len == tau;
+  int k = 0;
+  for (long long i = i0; i < rows; i += di, ++k) {
+    const int s = k & 1;
+    asm volatile(
+        "{\n.reg .pred P;\nW_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n"
+        "@!P bra W_%=;\n}\n" ::"r"(xr_su32(&bar[s])), "r"((unsigned)((k >> 1) & 1)) : "memory");
+    const double* xr = buf0 + (long long)s * d;
+    for (int b = tid; b < ld_xs; b += XR_THREADS) {
+      double x = 0.0;
+      if (b < tau) {
+        if (single) {
+          const int ce = s_ce[b];
+          x = ce >= 0 ? xr[ce] : -xr[~ce];
+        } else {
+          for (int e = s_bp[b]; e < s_bp[b + 1]; ++e) {
+            const int ce = s_ce[e];
+            x += ce >= 0 ? xr[ce] : -xr[~ce];
+          }
+        }
+      }
+      XS[i * ld_xs + b] = x;
+    }
+    __syncthreads();   // every thread is done with buffer s before it is refilled
+    if (tid == 0 && i + 2 * di < rows) issue(s, i + 2 * di);
   }
 }
 
@@ -367,6 +434,22 @@ cudaError_t launch_dense_xs(const double* X, long long ldx, long long rows, cons
                             int slot) {
   if (rows <= 0) return cudaSuccess;
   const size_t smem = (size_t)(sk.len + sk.tau + 1) * 4;
+  // whole rows through shared memory when most of each row's 128-byte lines are touched anyway
+  const double touched = 1.0 - std::pow(1.0 - std::min(1.0, (double)sk.len / std::max(1, sk.m)), 16.0);
+  const size_t rsmem = (size_t)2 * sk.m * 8 + 16 + smem;
+  if (touched >= 0.7 && sk.m % 2 == 0 && ldx % 2 == 0 && ((uintptr_t)X & 15) == 0 && rsmem <= 200 * 1024) {
+    int dev = 0, sms = 148, per_sm = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaError_t e = cudaFuncSetAttribute(k_dense_xs_rows, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)rsmem);
+    if (e == cudaSuccess)
+      e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_dense_xs_rows, XR_THREADS, rsmem);
+    if (e != cudaSuccess) return e;
+    const long long blocks = std::min<long long>(rows, (long long)sms * std::max(1, per_sm));
+    k_dense_xs_rows<<<(unsigned)blocks, XR_THREADS, rsmem, st>>>(X, ldx, rows, sk, XS, ld_xs, ctrl, slot);
+    return cudaGetLastError();
+  }
   if (smem <= XW_SMEM) {   // sketch staged per block, warp-owned rows, independent gathers
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);

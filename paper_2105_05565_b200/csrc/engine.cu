@@ -874,7 +874,14 @@ rs_status Problem::enqueue_iterate_group(const rs_solve_opts* o, int ns, cudaEve
   ia.nslots = ns;
   ia.big = skb.tau > 224;
   ia.wait = pipe_ov ? 1 : 0;   // the first set's tail may still be factored on st2 (solve)
-  RS_CUDA(launch_iterate(ia, grid > 0 ? grid : num_sms, ctrl, st));
+  if (grid <= 0) {   // all SMs, but no fewer than 64 columns per CTA (small m: cheaper grid syncs)
+    static const int g_env = [] {
+      const char* e = std::getenv("RS_IT_GRID");
+      return e ? std::atoi(e) : 0;
+    }();
+    grid = g_env > 0 ? g_env : (int)std::min<long long>(num_sms, std::max<long long>(16, (m + 63) / 64));
+  }
+  RS_CUDA(launch_iterate(ia, grid, ctrl, st));
   if (ev) cudaEventRecordWithFlags(ev[2 * RS_K_UPDATE + 1], st, cudaEventRecordExternal);
   return RS_OK;
 }
