@@ -39,7 +39,7 @@
 extern "C" {
 #endif
 
-#define RS_ABI_VERSION 3
+#define RS_ABI_VERSION 4
 
 typedef struct rs_problem_t* rs_problem;
 
@@ -206,6 +206,9 @@ typedef struct {
   int64_t kernel_launches[RS_K_NCLASSES];
   int64_t gpu_launches;      /* CUDA kernels launched by the iteration loop (graph nodes run,
                                 including no-op launches after the stop flag in the last chunk) */
+  int32_t overlap_sms;       /* EXPLICIT, tau > 224, overlapped pipeline: SMs running the group
+                                kernel while the next group's factorisation runs on the others;
+                                0 when the solve did not overlap                                  */
 } rs_report;
 
 /* Run Alg. 2 from w^0 = 0.  w_out: d doubles (the ridge weights; dual: X^T alpha), host memory

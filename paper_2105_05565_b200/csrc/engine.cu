@@ -1203,6 +1203,7 @@ rs_status Problem::solve(const rs_solve_opts* o, double* w_out, rs_mem w_mem, do
     R.kernel_launches[cls] = klaunch[cls];
   }
   R.gpu_launches = graph_launches * kernels_per_iter;   // kernel nodes per graph launch
+  R.overlap_sms = pipe_ov ? OV_SMS : 0;
   if (rep) *rep = R;
   if (o->trace && R.trace_len > 0)
     RS_CUDA(cudaMemcpy(o->trace, trace_dev, R.trace_len * 8, cudaMemcpyDeviceToHost));

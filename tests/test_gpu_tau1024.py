@@ -68,3 +68,78 @@ def test_c5_shape_tau1024_50_steps(rs, data, kind, mode):
     assert rep["iterations"] == ITERS
     assert_close(w, ref["w"], 1e-10, f"{mode}/{kind} w")
     assert_close(r, ref["r"], 1e-10, f"{mode}/{kind} r")
+
+
+# ---------------------------------------------------------------- overlapped pipeline, many groups
+OV_ITERS = 520   # > 2 groups of P = 2 (num_sms - 32) = 232 slots on a 148-SM B200
+
+_OV_CHILD = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, sys.argv[1])
+import rsinputs
+from paper_2105_05565_b200 import build
+build()
+from paper_2105_05565_b200 import ridgesketch as rs
+X, y = rsinputs.dense_problem(int(sys.argv[3]), int(sys.argv[4]), seed=11, col_decay=True, noise=0.01)
+h = rs.rs_create_dense(X.cuda(), y.cuda(), float(sys.argv[5]), mode="explicit", borrow=True)
+w, rep = rs.rs_solve(h, "subsample", 1024, 1.0, 0.5, 0.0, int(sys.argv[6]), seed=3)
+_, r = rs.rs_get_state(h)
+rs.rs_destroy(h)
+assert rep["overlap_sms"] > 0, rep
+np.savez(sys.argv[2], w=w, r=r)
+"""
+
+
+def _ov_oracle(data, kind):
+    key = ("ov", kind)
+    if key not in _ORACLE:
+        X, y = data
+        tau, k = CASES[kind]
+        _ORACLE[key] = OV.solve(X, y, LAM, kind, tau, 1.0, 0.5, 0.0, OV_ITERS, seed=3, subcount_k=k,
+                                explicit=True)
+    return _ORACLE[key]
+
+
+@pytest.mark.parametrize("kind", ["subsample", "count", "subcount"])
+def test_c5_shape_overlapped_groups(rs, data, kind):
+    """EXPLICIT at c5's tau with a subsample sketch runs the overlapped pipeline: the
+    first set's first num_sms slots are factored up front and the rest beside the first group
+    (per-slot ready flags), then every group's k_iterate on OV_SMS SMs runs beside the next group's
+    two-per-SM factorisation, whose CTAs claim slots and step aside on SMs beyond the budget.  520
+    iterations cross two group boundaries and every slot of both sets (count / SubCount: the
+    sequential group pipeline over the same boundaries); the iterates equal the oracle's (1e-9:
+    520 steps of rounding)."""
+    X, y = data
+    tau, k = CASES[kind]
+    Xd, yd = torch.from_numpy(X).cuda(), torch.from_numpy(y).cuda()
+    h = rs.rs_create_dense(Xd, yd, LAM, mode="explicit", borrow=True)
+    try:
+        w, rep = rs.rs_solve(h, kind, tau, 1.0, 0.5, 0.0, OV_ITERS, seed=3, subcount_k=k)
+        _, r = rs.rs_get_state(h)
+    finally:
+        rs.rs_destroy(h)
+    assert rep["iterations"] == OV_ITERS
+    # subsample (c5's sketch) overlaps; count (tau rows of A S^T over all m coordinates) and
+    # SubCount (2 tau rows) are estimated faster sequentially and run the plain group pipeline
+    assert (rep["overlap_sms"] > 0) == (kind == "subsample"), rep["overlap_sms"]
+    ref = _ov_oracle(data, kind)
+    assert_close(w, ref["w"], 1e-9, f"{kind} w")
+    assert_close(r, ref["r"], 1e-9, f"{kind} r")
+
+
+@pytest.mark.parametrize("env", [{"RS_OV_SPLIT": "0"}, {"RS_BF_DUAL": "0"}])
+def test_c5_shape_overlapped_switches(tmp_path, data, env):
+    """The process-wide A/B switches of the overlapped pipeline (read once per process, so in a
+    child): the whole first set up front (RS_OV_SPLIT=0) and the 8-warp one-slot-per-SM
+    factorisation (RS_BF_DUAL=0) give the oracle's iterates too."""
+    import os, subprocess, sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outp = tmp_path / "ov.npz"
+    res = subprocess.run([sys.executable, "-c", _OV_CHILD, root, str(outp), str(N), str(D), repr(LAM),
+                          str(OV_ITERS)], env=dict(os.environ, **env), capture_output=True, text=True,
+                         timeout=900)
+    assert res.returncode == 0, res.stderr[-2000:]
+    got = np.load(outp)
+    ref = _ov_oracle(data, "subsample")
+    assert_close(got["w"], ref["w"], 1e-9, f"{env} w")
+    assert_close(got["r"], ref["r"], 1e-9, f"{env} r")

@@ -8,4 +8,4 @@ $B --config c2 --mode explicit --seeds 1 > gpurun_out/itc_c2.json 2>/dev/null
 for f in c4 k1 c2; do python -c "
 import json;d=json.loads(open('gpurun_out/itc_$f.json').read().strip().splitlines()[-1])
 print('$f', round(d['value']), d['time_to_tol_s'], {k: round(v*1e3,2) for k, v in d['kernel_ms_per_step'].items() if v})"; done | tee gpurun_out/itc.txt
-SWEEP="${SWEEP:-32 22 26}" bash tools/gpu/ov_sweep.sh
+SWEEP="${SWEEP:-32 22 18}" bash tools/gpu/ov_sweep.sh

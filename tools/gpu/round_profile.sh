@@ -9,6 +9,8 @@ $B > gpurun_out/bench_c5.json 2> gpurun_out/bench_c5.err
 $B --impl reference --steps 20 --warmup 3 > gpurun_out/bench_c5_reference.json 2>/dev/null
 $B --config c2 > gpurun_out/bench_c2_gram.json 2>/dev/null
 $B --config c2 --mode explicit --no-cpu-baseline --no-alt > gpurun_out/bench_c2_explicit.json 2>/dev/null
+$B --config c2 --mode implicit --no-cpu-baseline --no-alt --steps 50 --seeds 1 > gpurun_out/bench_c2_implicit.json 2>/dev/null
+RS_OV_SPLIT=0 $B --no-cpu-baseline --no-alt --no-e2e > gpurun_out/bench_c5_nosplit.json 2>/dev/null
 $B --config c3 --max-iter-tol 20000 --cpu-seconds 20 --seeds 1 > gpurun_out/bench_c3.json 2>/dev/null
 $B --config c4 --max-iter-tol 20000 --cpu-seconds 20 > gpurun_out/bench_c4_explicit.json 2>/dev/null
 $B --config c4 --mode gram --max-iter-tol 20000 --no-cpu-baseline --seeds 1 > gpurun_out/bench_c4_gram.json 2>/dev/null
@@ -22,6 +24,8 @@ timeout 900 ncu $M -k regex:"k_bfactor_lp|k_bf_gather|k_iterate" -c 6 --log-file
 timeout 900 ncu $M -k regex:"k_iterate|k_bfactor_small" -c 6 --log-file gpurun_out/tr_c4_explicit.csv $P c4 explicit 300 > /dev/null 2>&1
 timeout 900 ncu $M -k regex:"k_gram_xtw|k_xpass_rows" -c 6 --log-file gpurun_out/tr_c2_gram.csv $P c2 gram 8 > /dev/null 2>&1
 timeout 900 ncu $M -k regex:"k_gram_bands|k_hash_rows|k_spmv" -c 12 --log-file gpurun_out/tr_c3.csv $P c3 gram 4 > /dev/null 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_bfactor_lp" -c 1 -o gpurun_out/prof_c5_bfactor_full $P c5 explicit 150 > /dev/null 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_iterate" -c 1 -o gpurun_out/prof_c5_iterate_full $P c5 explicit 150 > /dev/null 2>&1
+timeout 900 ncu $M -k regex:"k_dense_xs" -c 4 --log-file gpurun_out/tr_xs_c2.csv $P c2 implicit 4 > /dev/null 2>&1
+timeout 900 ncu $M -k regex:"k_dense_xs" -c 2 --log-file gpurun_out/tr_xs_c5.csv $P c5 gram 2 > /dev/null 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k regex:"bfactor_lp<.int.4" -c 1 -o gpurun_out/prof_c5_bfactor_full $P c5 explicit 300 > /dev/null 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_iterate" -c 1 -o gpurun_out/prof_c5_iterate_full $P c5 explicit 300 > /dev/null 2>&1
 ls gpurun_out/

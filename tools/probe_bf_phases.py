@@ -1,5 +1,5 @@
 """Development probe: per-phase SM cycles of the large-tau factorisation (k_bfactor_lp), from a
-library built with RS_NVCC_EXTRA=-DRS_BF_PHASES.  usage: python tools/probe_bf_phases.py [cfg] [iters]"""
+library built with RS_NVCC_EXTRA=-DRS_BF_PHASES.  usage: python tools/probe_bf_phases.py [cfg] [iters] [slots factored per solve (default min(iters, 148))]"""
 import ctypes as C, os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch
@@ -25,7 +25,7 @@ for rep in range(2):
     lib.rs_debug_bf_phases(buf, 0)
 ph = np.array(list(buf), dtype=np.float64)
 names = ["gather", "chol acc", "chol diag", "chol total", "inv acc", "inv total", "inv diag", "write"]
-slots = min(iters, 148)
+slots = int(sys.argv[3]) if len(sys.argv) > 3 else min(iters, 148)
 print(f"{cfg.name}: solve {r['solve_seconds']*1e3:.3f} ms, factor ms/launch {r['kernel_ms']['factor'] if r['kernel_ms']['factor'] else 0}")
 tot = ph[0] + ph[3] + ph[5] + ph[7]
 for k, nm in enumerate(names):
