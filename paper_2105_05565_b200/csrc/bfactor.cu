@@ -605,7 +605,10 @@ constexpr size_t GA_SMEM = (size_t)(4096 + 1 + 8192) * 4;
 __global__ void __launch_bounds__(GA_WARPS * 32)
 k_bf_gather(FactorSrc src, DevSketch skb, double* work, long long work_stride, const Ctrl* ctrl) {
   const int slot = blockIdx.y;
-  if (slot_unused(ctrl, slot)) return;
+  __shared__ int s_unused;   // one reading per block (ctrl moves under a concurrent group kernel)
+  if (threadIdx.x == 0) s_unused = slot_unused(ctrl, slot) ? 1 : 0;
+  __syncthreads();
+  if (s_unused) return;
   extern __shared__ __align__(16) double ga_sm[];
   const DevSketch sk = skb.at(slot);
   const int tau = sk.tau, tp = bb_tp(tau);
@@ -711,12 +714,18 @@ __device__ __forceinline__ bool lp_factor_slot(const FactorSrc& src, const DevSk
   constexpr int LP_WARPS = CF::WARPS, LP_THREADS = CF::THREADS, LP_STAGES = CF::STAGES;
   constexpr int LP_STAGE = CF::STAGE, LP_BSZ = CF::BSZ, LP_ASZ = CF::ASZ, KS = CF::KS;
   constexpr int SPT = 32 / KS;   // k slices per 32-wide tile
-  if (slot_unused(ctrl, slot)) return true;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  // slot beyond max_iter or solve done: ctrl->k and done move under a concurrent group kernel, so
+  // one reading, shared by the block
+  if (tid == 0) s_stop = slot_unused(ctrl, slot) ? 1 : 0;
+  __syncthreads();
+  const int unused = s_stop;
+  __syncthreads();
+  if (unused) return true;
   BF_T(t_start);
   extern __shared__ __align__(16) double lp_sm[];   // slice ring, then the pair tiles
   const DevSketch sk = skb.at(slot);
   const int tau = sk.tau, tp = bb_tp(tau), Tc = tp / 32;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int q = lane >> 2, k4 = lane & 3;
   // the solve may finish while this group is factored ahead (overlapped pipeline): poll its flag
   // once per block-column pair, block-uniformly

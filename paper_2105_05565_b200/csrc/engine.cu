@@ -639,7 +639,7 @@ rs_status Problem::ensure_workspace(int kind, int tau, int ksum, int depth, bool
     if (bfactor_work_elems(tau)) RS_TRY(dalloc(&bf_work, bfactor_work_elems(tau) * depth));
     if (xg) RS_TRY(dalloc(&bf_claim, 2 * BF_CLAIM_WORDS));   // two concurrent launches' claims
     // EXPLICIT: the group's iterations as one persistent kernel (iterate.cu)
-    use_iterate = mode == RS_AS_EXPLICIT && iterate_ok(sk, m, xg ? OV_SMS : num_sms);
+    use_iterate = mode == RS_AS_EXPLICIT && iterate_ok(sk, m, xg ? ov_sms : num_sms);
     if (use_iterate) RS_TRY(dalloc(&it_scratch, 2 * (size_t)tau + num_sms));
   }
   sw = plan_solve(tau, num_sms);
@@ -790,7 +790,7 @@ rs_status Problem::enqueue_precompute(const rs_solve_opts* o, int ns, cudaEvent_
     RS_CUDA(cudaStreamWaitEvent(st2, ev_pro, 0));
     FactorSrc s2 = src;
     if (s2.ASt) s2.ASt += (long long)split * as_stride;
-    const BfClaim cl{bf_claim + BF_CLAIM_WORDS, num_sms - OV_SMS, num_sms};
+    const BfClaim cl{bf_claim + BF_CLAIM_WORDS, num_sms - ov_sms, num_sms};
     RS_CUDA(launch_bfactor(s2, skb.at(split), ns - split, Ginv_slots + (long long)split * gi_stride,
                            ld_gi, gi_stride, slot_flags + split,
                            bf_work + (long long)bfactor_work_elems((int)o->tau) * P, ctrl, st2, false,
@@ -888,8 +888,8 @@ rs_status Problem::enqueue_iterate_group(const rs_solve_opts* o, int ns, cudaEve
 
 // One group of an overlapped EXPLICIT pipeline (tau > 224) on slot set g: the sketches of the next
 // group (set 1 - g, iterations k0 + P ..) are drawn first; then, concurrently, st2 gathers and
-// factors them (k_bf_gather + k_bfactor_lp on P = num_sms - OV_SMS CTAs) while st runs this group's
-// P iterations (k_iterate on the OV_SMS SMs left free).  The factorisation kernels read ctrl->k only
+// factors them (k_bf_gather + k_bfactor_lp on the num_sms - ov_sms SMs) while st runs this group's
+// P iterations (k_iterate on the ov_sms SMs left free).  The factorisation kernels read ctrl->k only
 // to skip slots beyond max_iter; the concurrent iterations can only make that test skip fewer slots.
 rs_status Problem::enqueue_group_ov(const rs_solve_opts* o, int g, cudaEvent_t* ev) {
   auto mark = [&](cudaStream_t s, int q, int cls, int edge) {
@@ -915,13 +915,13 @@ rs_status Problem::enqueue_group_ov(const rs_solve_opts* o, int g, cudaEvent_t* 
     src.A = A;
     src.lda = lda;
   }
-  // at most num_sms - OV_SMS SMs, the same ones in every group (BfClaim)
-  const BfClaim cl{bf_claim, num_sms - OV_SMS, num_sms};
+  // at most num_sms - ov_sms SMs (BfClaim)
+  const BfClaim cl{bf_claim, num_sms - ov_sms, num_sms};
   RS_CUDA(launch_bfactor(src, sn, P, Ginv_slots + (long long)nxt * P * gi_stride, ld_gi, gi_stride,
                          slot_flags + (long long)nxt * P, bf_work, ctrl, st2, bf_dual, &cl));   // a4 + a5 ahead
   mark(st2, 0, RS_K_FACTOR, 1);
   RS_CUDA(cudaEventRecord(ev_join, st2));
-  RS_TRY(enqueue_iterate_group(o, P, ev, cur * P, OV_SMS));                       // a4-a7 x P
+  RS_TRY(enqueue_iterate_group(o, P, ev, cur * P, ov_sms));                       // a4-a7 x P
   RS_CUDA(cudaStreamWaitEvent(st, ev_join, 0));
   return RS_OK;
 }
@@ -987,21 +987,46 @@ rs_status Problem::solve(const rs_solve_opts* o, double* w_out, rs_mem w_mem, do
     return !(e && e[0] == '0');
   }();
   // EXPLICIT with tau > 224: overlap the next group's factorisation with the current group's
-  // iterations when that shortens an iteration.  Per-iteration estimates: the factor's 2 tau^3 / 3
-  // flop at ~20 TFLOP/s on all SMs (two slots per SM; ~15 one per SM; measured on c5, num_sms /
-  // (num_sms - OV_SMS) slower on the SMs the overlap leaves it), the group kernel's sketched rows
-  // of A (len m 8 bytes) at ~45 GB/s per SM plus ~15 us of barriers (profiles/README.md, k_iterate
-  // phases)
+  // iterations on a split of the SMs when that shortens an iteration, the split chosen by a model
+  // of both (measured on this B200): the group kernel's phase C reads len rows (count:
+  // tau rows of A S^T) x 64-column chunks per CTA at ~45 GB/s per SM, ~4.5 TB/s in all, plus ~12 us
+  // of phases A/B and barriers; one G_k costs ~1924 (tau / 256)^0.70 SM-us of factorisation
+  // (k_bfactor_lp: tau 256 and 1024 measured; the small-tau end is latency-bound).  RS_OV_SMS=n
+  // forces the group kernel's SM count.
   const double tau_d = (double)o->tau;
   const double len_d = (double)sketch_max_len((int)o->kind, (int)m, (int)o->tau, ksum);
-  const double f_us = 2.0 * tau_d * tau_d * tau_d / 3.0 / (dual_env ? 20e6 : 15e6);
-  auto it_us = [&](int sms) { return len_d * (double)m * 8.0 / (sms * 45e3) + 15.0; };
-  const double ov_us = std::max(f_us * num_sms / std::max(1, num_sms - OV_SMS), it_us(OV_SMS));
-  const bool want_ov = want_pipe && mode == RS_AS_EXPLICIT && o->tau > 224 && num_sms > 2 * OV_SMS &&
-                       len_d <= 8192 && ov_us < f_us + it_us(num_sms);
+  const double rows_it = o->kind == RS_SKETCH_COUNT ? tau_d : len_d;
+  auto it_us = [&](int sms) {
+    const long long cw = (m + sms - 1) / sms;
+    const double cols = 64.0 * (double)((cw + 63) / 64);
+    return std::max(rows_it * 8.0 * cols / 45e3, rows_it * (double)m * 8.0 / 4.5e6) + 12.0;
+  };
+  const double fslot = 1924.0 * std::pow(tau_d / 256.0, 0.702);
+  const int it_grid = (int)std::min<long long>(num_sms, std::max<long long>(16, (m + 63) / 64));
+  const double seq_us = fslot / num_sms + it_us(it_grid);
+  static const int ov_env = [] {
+    const char* e = std::getenv("RS_OV_SMS");
+    return e ? std::atoi(e) : 0;
+  }();
+  int ov_best = 0;
+  double ov_us = 1e30;
+  for (int sms = 16; sms <= num_sms - 16; sms += 2) {
+    const double v = std::max(fslot / (num_sms - sms), it_us(sms));
+    if (v < ov_us) {
+      ov_us = v;
+      ov_best = sms;
+    }
+  }
+  if (ov_env > 0 && ov_env < num_sms) {
+    ov_best = ov_env;
+    ov_us = 0.0;
+  }
+  const bool want_ov = want_pipe && mode == RS_AS_EXPLICIT && o->tau > 224 && ov_best > 0 &&
+                       len_d <= 8192 && ov_us < seq_us;
+  if (want_ov) ov_sms = ov_best;
   bf_dual = want_ov && dual_env;
   const int cps = bf_dual ? 2 : 1;
-  if (want_ov) chunk = 2 * cps * (num_sms - OV_SMS);
+  if (want_ov) chunk = 2 * cps * (num_sms - ov_sms);
   const bool want_xg = want_ov;   // two slot sets
   if (want_xg) chunk = std::max(2, chunk & ~1);   // two groups of P = chunk / 2
   int depth = 0;
@@ -1203,7 +1228,7 @@ rs_status Problem::solve(const rs_solve_opts* o, double* w_out, rs_mem w_mem, do
     R.kernel_launches[cls] = klaunch[cls];
   }
   R.gpu_launches = graph_launches * kernels_per_iter;   // kernel nodes per graph launch
-  R.overlap_sms = pipe_ov ? OV_SMS : 0;
+  R.overlap_sms = pipe_ov ? ov_sms : 0;
   if (rep) *rep = R;
   if (o->trace && R.trace_len > 0)
     RS_CUDA(cudaMemcpy(o->trace, trace_dev, R.trace_len * 8, cudaMemcpyDeviceToHost));

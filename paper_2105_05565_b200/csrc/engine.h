@@ -111,6 +111,7 @@ struct Problem {
   bool pipe_xg = false;   // two slot sets
   bool pipe_ov = false;
   bool bf_dual = false;   // tau > 224: the 4-warp factorisation, two slots per SM
+  int ov_sms = 32;        // overlapped pipeline: SMs of the group kernel (solve's model)
   int ws_xg = -1;
   cudaStream_t st2 = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;

@@ -216,8 +216,6 @@ struct IterArgs {
   int wait;                      // flags[q] < 0: slot q is still being factored (by a concurrent
                                  // kernel), spin until it is 0 or 1
 };
-// SMs left to the iterations while the next group's factorisation runs (EXPLICIT, tau > 224)
-constexpr int OV_SMS = 32;
 size_t iterate_smem();
 bool iterate_ok(const DevSketch& sk, long long m, int grid);   // the group kernel applies
 cudaError_t iterate_init();
