@@ -325,7 +325,7 @@ def _csr_pairs(rs, cfg, host):
     return int(key.size), int((L * (L + 1) // 2).sum()), sel
 
 
-def _roofline(args, cfg, world, kms, kl, dom, prof_ms, host, rs):
+def _roofline(args, cfg, world, kms, kl, dom, prof_ms, host, rs, nb=1):
     per = lambda c: max(kms[c] / max(kl[c], 1), 1e-9)   # ms per launch of class c
     share = kms[dom] / max(prof_ms, 1e-9)
     hbm = _peaks().get("hbm_gbs", 6556.5)
@@ -365,9 +365,12 @@ def _roofline(args, cfg, world, kms, kl, dom, prof_ms, host, rs):
                         algorithmic_per_launch=f"{w:.3e} flop (n tau (tau + 1): lower triangle)")
         elif dom == "factor":
             slots = args.steps / max(kl["factor"], 1)   # iterations (G_k) per group
-            big = cfg.tau > 224   # k_bfactor_big stores W = L^{-1}; W^T W is applied as two GEMVs
-            w = float(cfg.tau) ** 3 * (2.0 / 3.0 if big else 1.0) * slots
-            what = ("tau^3/3 Cholesky + tau^3/3 inverse" if big else
+            # tau > 224: the slot holds W = L^{-1} (nb = 1) or the blocked inverse (W_bb = L_bb^{-1}
+            # on nb diagonal super-blocks, L below), applied as triangular GEMVs
+            big = cfg.tau > 224
+            w = float(cfg.tau) ** 3 * ((1.0 + 1.0 / nb ** 2) / 3.0 if big else 1.0) * slots
+            what = ((f"tau^3/3 Cholesky + tau^3/(3 nb^2) inverse of the nb = {nb} diagonal super-blocks"
+                     if nb > 1 else "tau^3/3 Cholesky + tau^3/3 inverse") if big else
                     "tau^3/3 Cholesky + tau^3/3 inverse + tau^3/3 W^T W")
             roof = dict(kernel="batched Cholesky + triangular inverse of the group's G_k "
                                f"({'k_bf_gather + k_bfactor_lp' if big else 'k_bfactor_small'}, DMMA)",
@@ -587,12 +590,14 @@ def run_ours(args):
         dom = max(kms, key=lambda k: kms[k])
         saved = args.mode
         args.mode = mode
-        roof = _roofline(args, cfg, world, kms, kl, dom, prof_ms, host, rs)
+        roof = _roofline(args, cfg, world, kms, kl, dom, prof_ms, host, rs,
+                         nb=int(rep_prof.get("inverse_blocks") or 1))
         others = {}
         for cls in sorted(kms, key=lambda k: -kms[k]):
             if cls != dom and kms[cls] > 0.1 * prof_ms:
                 try:
-                    o = _roofline(args, cfg, world, kms, kl, cls, prof_ms, host, rs)
+                    o = _roofline(args, cfg, world, kms, kl, cls, prof_ms, host, rs,
+                                  nb=int(rep_prof.get("inverse_blocks") or 1))
                     others[cls] = {k: o[k] for k in ("kernel", "bound", "achieved", "peak", "unit",
                                                      "frac", "traffic", "avg_launch_ms",
                                                      "share_of_step") if k in o}

@@ -39,7 +39,7 @@
 extern "C" {
 #endif
 
-#define RS_ABI_VERSION 4
+#define RS_ABI_VERSION 5
 
 typedef struct rs_problem_t* rs_problem;
 
@@ -209,6 +209,10 @@ typedef struct {
   int32_t overlap_sms;       /* EXPLICIT, tau > 224, overlapped pipeline: SMs running the group
                                 kernel while the next group's factorisation runs on the others;
                                 0 when the solve did not overlap                                  */
+  int32_t inverse_blocks;    /* tau > 224 on the group kernel: diagonal super-blocks nb of the
+                                factor slots' blocked inverse (W_bb = L_bb^{-1} on the diagonal,
+                                L below; per G_k tau^3/3 + tau^3/(3 nb^2) flop); 1 = W = L^{-1} in
+                                full; 0 when no large-tau factor slots were used                    */
 } rs_report;
 
 /* Run Alg. 2 from w^0 = 0.  w_out: d doubles (the ridge weights; dual: X^T alpha), host memory

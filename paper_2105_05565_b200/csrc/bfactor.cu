@@ -533,6 +533,10 @@ __device__ __noinline__ bool diag_factor_s(double* D, int ldd, double* Lg, int l
 //     [T_I,J0 T_I,J1] = sum_{K=J1+1..I} W_IK [L_K,J0 L_K,J1]
 //     W_I,J1 = -T_I,J1 W_J1J1,  W_I,J0 = -(T_I,J0 + W_I,J1 L_J1,J0) W_J0J0
 //     diagonal pair: W_J1,J0 = -W_J1J1 L_J1,J0 W_J0J0
+//   Blocked inverse (sbt < Tc, the group kernel's slots): the inverse runs inside each diagonal
+//   super-block of sbt tiles only (strips I < E, the super-block's end), so W_bb = L_bb^{-1} costs
+//   1/nb^2 of the full inverse's flop; the L tiles below the super-blocks go to the slot as their
+//   strips are finished, and the iteration substitutes block by block (iterate.cu).
 // Two shapes of the same kernel (LpCfg<NW>): 8 warps with 32-deep slices, one CTA per SM (the
 // pipeline-fill group, all SMs free), and 4 warps with 16-deep slices, two CTAs per SM, so that one
 // slot's barriers, diagonal pairs and finishing steps run while the other slot's warps keep the DMMA
@@ -708,8 +712,8 @@ __device__ __forceinline__ bool lp_factor_slot(const FactorSrc& src, const DevSk
                                                double* __restrict__ Ginv, long long ldgi,
                                                long long gi_stride, double* work,
                                                long long work_stride, int* __restrict__ flags,
-                                               const Ctrl* ctrl, const int slot, int& s_bad,
-                                               int& s_stop) {
+                                               const Ctrl* ctrl, const int slot, int sbt,
+                                               int& s_bad, int& s_stop) {
   using CF = LpCfg<NW>;
   constexpr int LP_WARPS = CF::WARPS, LP_THREADS = CF::THREADS, LP_STAGES = CF::STAGES;
   constexpr int LP_STAGE = CF::STAGE, LP_BSZ = CF::BSZ, LP_ASZ = CF::ASZ, KS = CF::KS;
@@ -891,6 +895,22 @@ __device__ __forceinline__ bool lp_factor_slot(const FactorSrc& src, const DevSk
   };
   // per-warp 32 x 32 scratch (LD 36) in the slice ring, free between accumulations
   double* S = lp_sm + warp * PT;
+  // a finished tile (I, J) of the slot's blocked inverse (src: 32 x 32 row-major, ld lds, shared or
+  // global) -- W_IJ inside a diagonal super-block, L_IJ below them -- into the slot: the tile in its
+  // lower triangle, its transpose in its upper triangle, both row-contiguous (coalesced both ways)
+  double* Gi = Ginv + slot * gi_stride;
+  auto emit_w = [&](int I, int J, const double* src, int lds) {
+#pragma unroll 4
+    for (int rr = 0; rr < 32; ++rr) {
+      const int row = 32 * I + rr, col = 32 * J + lane;
+      if (row < tau && col <= row) Gi[(long long)row * ldgi + col] = src[rr * lds + lane];
+    }
+#pragma unroll 4
+    for (int rr = 0; rr < 32; ++rr) {   // row 32 J + rr of the upper triangle: W[32 I + lane][32 J + rr]
+      const int row = 32 * J + rr, col = 32 * I + lane;
+      if (row < tau && col < tau && col > row) Gi[(long long)row * ldgi + col] = src[lane * lds + rr];
+    }
+  };
   // finish Cholesky strip i of pair p0 from its accumulator
   // acc = sum_{k<p0} L_ik [L_p0,k L_p0+1,k]^T:
   //   L_i,p0 = (G_i,p0 - acc_0) L00^{-T},  L_i,p0+1 = (G_i,p0+1 - acc_1 - L_i,p0 L10^T) L11^{-T}
@@ -902,6 +922,11 @@ __device__ __forceinline__ bool lp_factor_slot(const FactorSrc& src, const DevSk
     __syncwarp();
     acc_store(t32, S, PLD, lane);
     acc_store(t32, T(i, p0), tp, lane);
+    const bool offd = i / sbt != p0 / sbt;   // tile outside the diagonal super-blocks: the slot keeps L
+    if (offd) {
+      __syncwarp();
+      emit_w(i, p0, S, PLD);
+    }
     const double* base = T(i, p0 + 1);
 #pragma unroll
     for (int R = 0; R < 4; ++R)
@@ -921,20 +946,9 @@ __device__ __forceinline__ bool lp_factor_slot(const FactorSrc& src, const DevSk
     mma_tile<false, true>(t32, S, PLD, P3 + 2 * PT, PLD, lane, 1.0);   // L_i,p0+1
     acc_store(t32, T(i, p0 + 1), tp, lane);
     __syncwarp();
-  };
-  // a finished W tile (I, J) (src: 32 x 32 row-major, ld lds, shared or global) into the slot: W in
-  // its lower triangle, W^T in its upper triangle, both row-contiguous (coalesced both ways)
-  double* Gi = Ginv + slot * gi_stride;
-  auto emit_w = [&](int I, int J, const double* src, int lds) {
-#pragma unroll 4
-    for (int rr = 0; rr < 32; ++rr) {
-      const int row = 32 * I + rr, col = 32 * J + lane;
-      if (row < tau && col <= row) Gi[(long long)row * ldgi + col] = src[rr * lds + lane];
-    }
-#pragma unroll 4
-    for (int rr = 0; rr < 32; ++rr) {   // row 32 J + rr of the upper triangle: W[32 I + lane][32 J + rr]
-      const int row = 32 * J + rr, col = 32 * I + lane;
-      if (row < tau && col < tau && col > row) Gi[(long long)row * ldgi + col] = src[lane * lds + rr];
+    if (offd) {
+      emit_w(i, p0 + 1, T(i, p0 + 1), tp);
+      __syncwarp();
     }
   };
   // finish inverse strip I of pair (J0, J1) from acc = [T_I,J0 T_I,J1]:
@@ -1091,7 +1105,8 @@ __device__ __forceinline__ bool lp_factor_slot(const FactorSrc& src, const DevSk
   // ---- W = L^{-1}, block-column pairs from the last
   for (int J0 = Tc - 2; J0 >= 0; J0 -= 2) {
     if (stopped()) return false;
-    const int J1 = J0 + 1, nstrip = Tc - 1 - J1;
+    const int E = min(Tc, (J0 / sbt + 1) * sbt);   // end of J0's diagonal super-block (tiles)
+    const int J1 = J0 + 1, nstrip = E - 1 - J1;
     const int rounds = (nstrip + LP_WARPS - 1) / LP_WARPS;
     if (rounds > 0) {
       __syncthreads();
@@ -1101,8 +1116,8 @@ __device__ __forceinline__ bool lp_factor_slot(const FactorSrc& src, const DevSk
     for (int rd = 0; rd < rounds; ++rd) {   // highest strips first
       int spw, part;
       const int j = split(min(LP_WARPS, nstrip - rd * LP_WARPS), spw, part);
-      const int I = j < 0 ? -1 : Tc - 1 - (rd * LP_WARPS + j);
-      const int kend = Tc - rd * LP_WARPS;   // rows of this round are <= kend - 1
+      const int I = j < 0 ? -1 : E - 1 - (rd * LP_WARPS + j);
+      const int kend = E - rd * LP_WARPS;   // rows of this round are <= kend - 1
       accumulate(false, J0, J1 + 1, kend, I, I, spw, part);
       if (I > J1 && part == 0) finish_inv(I, J0);
     }
@@ -1160,12 +1175,12 @@ template <int NW>
 __global__ void __launch_bounds__(LpCfg<NW>::THREADS, LpCfg<NW>::CTAS)
 k_bfactor_lp(FactorSrc src, DevSketch skb, double* __restrict__ Ginv, long long ldgi,
              long long gi_stride, double* work, long long work_stride, int* __restrict__ flags,
-             const Ctrl* ctrl, int nslots, int* claim, int max_sms) {
+             const Ctrl* ctrl, int nslots, int* claim, int max_sms, int sbt) {
   __shared__ int s_bad, s_stop, s_slot;
   const int tid = threadIdx.x;
   if (!claim) {
     lp_factor_slot<NW>(src, skb, Ginv, ldgi, gi_stride, work, work_stride, flags, ctrl, blockIdx.x,
-                       s_bad, s_stop);
+                       sbt, s_bad, s_stop);
     return;
   }
   if (tid == 0) {
@@ -1193,7 +1208,7 @@ k_bfactor_lp(FactorSrc src, DevSketch skb, double* __restrict__ Ginv, long long 
     const int slot = s_slot;
     if (slot >= nslots) return;
     if (!lp_factor_slot<NW>(src, skb, Ginv, ldgi, gi_stride, work, work_stride, flags, ctrl, slot,
-                            s_bad, s_stop))
+                            sbt, s_bad, s_stop))
       return;
   }
 }
@@ -1246,7 +1261,8 @@ cudaError_t bfactor_init() {
 
 cudaError_t launch_bfactor(const FactorSrc& src, const DevSketch& skb, int nslots, double* Ginv,
                            long long ldgi, long long gi_stride, int* flags, double* work,
-                           const Ctrl* ctrl, cudaStream_t st, bool dual, const BfClaim* claim) {
+                           const Ctrl* ctrl, cudaStream_t st, bool dual, const BfClaim* claim,
+                           int sb) {
   if (skb.tau > BB_MAXTAU || nslots < 1) return cudaErrorInvalidValue;
   if (skb.tau > BF_MAXTAU) {
     if (!work) return cudaErrorInvalidValue;
@@ -1257,6 +1273,9 @@ cudaError_t launch_bfactor(const FactorSrc& src, const DevSketch& skb, int nslot
     int* cw = claim ? claim->words : nullptr;
     const int max_sms = claim ? claim->max_sms : 0;
     const int cps = dual ? LpCfg<4>::CTAS : LpCfg<8>::CTAS;
+    // super-block width in 32-wide tiles (a whole number of 64-wide pairs); >= tp: full inverse
+    if (sb > 0 && sb % 64) return cudaErrorInvalidValue;
+    const int sbt = sb > 0 && sb < tp ? sb / 32 : tp / 32;
     // (claimed slots: CTAs on every SM, so that those refused by the SM budget leave enough workers)
     const unsigned grid = (unsigned)(claim ? cps * claim->num_sms : nslots);
     if (cw) {
@@ -1265,10 +1284,10 @@ cudaError_t launch_bfactor(const FactorSrc& src, const DevSketch& skb, int nslot
     }
     if (dual)
       k_bfactor_lp<4><<<grid, LpCfg<4>::THREADS, LpCfg<4>::SMEM, st>>>(
-          src, skb, Ginv, ldgi, gi_stride, work, ws, flags, ctrl, nslots, cw, max_sms);
+          src, skb, Ginv, ldgi, gi_stride, work, ws, flags, ctrl, nslots, cw, max_sms, sbt);
     else
       k_bfactor_lp<8><<<grid, LpCfg<8>::THREADS, LpCfg<8>::SMEM, st>>>(
-          src, skb, Ginv, ldgi, gi_stride, work, ws, flags, ctrl, nslots, cw, max_sms);
+          src, skb, Ginv, ldgi, gi_stride, work, ws, flags, ctrl, nslots, cw, max_sms, sbt);
     return cudaGetLastError();
   }
   k_bfactor_small<<<nslots, BF_THREADS, bf_smem(skb.tau), st>>>(src, skb, Ginv, ldgi, gi_stride,

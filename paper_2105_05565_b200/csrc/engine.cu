@@ -532,6 +532,16 @@ static bool pipeline_applies(const Problem* p, int tau) {
   return (dense || csr) && tau <= bfactor_max_tau();
 }
 
+// Diagonal super-blocks of the group kernel's blocked inverse (tau > 224; RS_SB_NB=n forces n)
+static int sb_blocks(int tau) {
+  static const int nb_env = [] {
+    const char* e = std::getenv("RS_SB_NB");
+    return e ? std::atoi(e) : -1;
+  }();
+  if (tau <= 224) return 1;
+  return nb_env >= 1 ? nb_env : (tau >= 512 ? 2 : 1);
+}
+
 rs_status Problem::ensure_workspace(int kind, int tau, int ksum, int depth, bool xg) {
   if (ws_kind == kind && ws_tau == tau && ws_ksum == ksum && ws_depth == depth && ws_xg == (int)xg)
     return RS_OK;
@@ -641,6 +651,14 @@ rs_status Problem::ensure_workspace(int kind, int tau, int ksum, int depth, bool
     // EXPLICIT: the group's iterations as one persistent kernel (iterate.cu)
     use_iterate = mode == RS_AS_EXPLICIT && iterate_ok(sk, m, xg ? ov_sms : num_sms);
     if (use_iterate) RS_TRY(dalloc(&it_scratch, 2 * (size_t)tau + num_sms));
+    // the group kernel solves with a blocked inverse: the factorisation inverts only the nb
+    // diagonal super-blocks of L (2 tau^3 / 3 -> (1 + 1/nb^2) tau^3 / 3 flop) and the iteration
+    // substitutes block by block (2 (nb - 1) more grid barriers per iteration); DESIGN §1
+    bf_sb = 0;
+    if (use_iterate && tau > 224) {
+      const int nb = sb_blocks(tau), pairs = (tau + 63) / 64;
+      if (nb > 1) bf_sb = (pairs + nb - 1) / nb * 64;
+    }
   }
   sw = plan_solve(tau, num_sms);
   RS_TRY(dalloc(&sw.Gx, solve_gx_elems(tau)));
@@ -784,7 +802,7 @@ rs_status Problem::enqueue_precompute(const rs_solve_opts* o, int ns, cudaEvent_
   if (split > 0 && split < ns) {   // the overlapped pipeline's first set (see solve): slots [0, split)
     // here, one per SM; slots [split, ns) on st2 with their own scratch, flagged -1 until factored
     RS_CUDA(launch_bfactor(src, skb, split, Ginv_slots, ld_gi, gi_stride, slot_flags, bf_work, ctrl,
-                           st, false));                                                     // a4+a5
+                           st, false, nullptr, bf_sb));                                     // a4+a5
     RS_CUDA(cudaMemsetAsync(slot_flags + split, 0xff, sizeof(int) * (size_t)(ns - split), st));
     RS_CUDA(cudaEventRecord(ev_pro, st));
     RS_CUDA(cudaStreamWaitEvent(st2, ev_pro, 0));
@@ -794,11 +812,11 @@ rs_status Problem::enqueue_precompute(const rs_solve_opts* o, int ns, cudaEvent_
     RS_CUDA(launch_bfactor(s2, skb.at(split), ns - split, Ginv_slots + (long long)split * gi_stride,
                            ld_gi, gi_stride, slot_flags + split,
                            bf_work + (long long)bfactor_work_elems((int)o->tau) * P, ctrl, st2, false,
-                           &cl));
+                           &cl, bf_sb));
     RS_CUDA(cudaEventRecord(ev_pro_tail, st2));
   } else {
     RS_CUDA(launch_bfactor(src, skb, ns, Ginv_slots, ld_gi, gi_stride, slot_flags, bf_work, ctrl,
-                           st, bf_dual));                                                   // a4+a5
+                           st, bf_dual, nullptr, bf_sb));                                   // a4+a5
   }
   mark(0, RS_K_FACTOR, 1);
   return RS_OK;
@@ -873,6 +891,7 @@ rs_status Problem::enqueue_iterate_group(const rs_solve_opts* o, int ns, cudaEve
   ia.beta = o->beta;
   ia.nslots = ns;
   ia.big = skb.tau > 224;
+  ia.sb = bf_sb;
   ia.wait = pipe_ov ? 1 : 0;   // the first set's tail may still be factored on st2 (solve)
   if (grid <= 0) {   // all SMs, but no fewer than 64 columns per CTA (small m: cheaper grid syncs)
     static const int g_env = [] {
@@ -918,7 +937,7 @@ rs_status Problem::enqueue_group_ov(const rs_solve_opts* o, int g, cudaEvent_t* 
   // at most num_sms - ov_sms SMs (BfClaim)
   const BfClaim cl{bf_claim, num_sms - ov_sms, num_sms};
   RS_CUDA(launch_bfactor(src, sn, P, Ginv_slots + (long long)nxt * P * gi_stride, ld_gi, gi_stride,
-                         slot_flags + (long long)nxt * P, bf_work, ctrl, st2, bf_dual, &cl));   // a4 + a5 ahead
+                         slot_flags + (long long)nxt * P, bf_work, ctrl, st2, bf_dual, &cl, bf_sb));   // a4 + a5 ahead
   mark(st2, 0, RS_K_FACTOR, 1);
   RS_CUDA(cudaEventRecord(ev_join, st2));
   RS_TRY(enqueue_iterate_group(o, P, ev, cur * P, ov_sms));                       // a4-a7 x P
@@ -1001,7 +1020,9 @@ rs_status Problem::solve(const rs_solve_opts* o, double* w_out, rs_mem w_mem, do
     const double cols = 64.0 * (double)((cw + 63) / 64);
     return std::max(rows_it * 8.0 * cols / 45e3, rows_it * (double)m * 8.0 / 4.5e6) + 12.0;
   };
-  const double fslot = 1924.0 * std::pow(tau_d / 256.0, 0.702);
+  // (blocked inverse, nb super-blocks: the inverse step shrinks to 1/nb^2 of its flop)
+  const int nb_sb = len_d <= 8192 ? sb_blocks((int)o->tau) : 1;
+  const double fslot = 1924.0 * std::pow(tau_d / 256.0, 0.702) * (0.5 + 0.5 / (nb_sb * nb_sb));
   const int it_grid = (int)std::min<long long>(num_sms, std::max<long long>(16, (m + 63) / 64));
   const double seq_us = fslot / num_sms + it_us(it_grid);
   static const int ov_env = [] {
@@ -1229,6 +1250,11 @@ rs_status Problem::solve(const rs_solve_opts* o, double* w_out, rs_mem w_mem, do
   }
   R.gpu_launches = graph_launches * kernels_per_iter;   // kernel nodes per graph launch
   R.overlap_sms = pipe_ov ? ov_sms : 0;
+  R.inverse_blocks = 0;
+  if (pipe && o->tau > 224) {
+    const long long sbw = bf_sb > 0 ? bf_sb : o->tau;
+    R.inverse_blocks = use_iterate ? (int)((o->tau + sbw - 1) / sbw) : 1;
+  }
   if (rep) *rep = R;
   if (o->trace && R.trace_len > 0)
     RS_CUDA(cudaMemcpy(o->trace, trace_dev, R.trace_len * 8, cudaMemcpyDeviceToHost));

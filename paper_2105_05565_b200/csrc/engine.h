@@ -106,6 +106,7 @@ struct Problem {
   double* bf_work = nullptr;     // tau > 224: per-slot work matrices of the batched factorisation
   double* it_scratch = nullptr;  // EXPLICIT group kernel (iterate.cu): t, delta (tau each), partials
   bool use_iterate = false;
+  int bf_sb = 0;               // super-block width of the blocked slot inverse (0: W = L^{-1} in full)
   // EXPLICIT, tau > 224: two slot sets of P; the next group's factorisation (st2) overlaps the
   // current group's iterations (st, k_iterate on the SMs the factor grid leaves free)
   bool pipe_xg = false;   // two slot sets

@@ -112,8 +112,9 @@ k_iterate(IterArgs a, Ctrl* ctrl) {
   const long long cw = ((m + G - 1) / G + 1) & ~1LL;
   const long long j0 = min(m, (long long)blockIdx.x * cw), j1 = min(m, j0 + cw);
   const int tau_c = a.skb.tau, len_c = a.skb.len;      // len_c: slot stride of the sketch entries
-  double* xs = it_sm;                                   // [tau]: g (phase A) or t (phase B)
-  double* coef = xs + tau_c;                            // [rows]: coefficient of each row of u
+  double* xs = it_sm;                                   // [tau]: g / h / delta (phases A, B)
+  double* ys = xs + tau_c;                              // [tau]: y = L^{-1} g (tau > 224)
+  double* coef = ys + tau_c;                            // [rows]: coefficient of each row of u
   int* s_ce = reinterpret_cast<int*>(coef + len_c);     // [len] coord (sign as complement)
   int* s_bk = s_ce + len_c;                             // [len] bucket
   int* s_bp = s_bk + len_c;                             // [tau + 1]
@@ -164,51 +165,83 @@ k_iterate(IterArgs a, Ctrl* ctrl) {
     IT_ADD(8, ta0, ta_g);
     // (no L2 prefetch of phase C's row segments: ~1000 cp.async.bulk.prefetch per CTA cost 7 us of
     // issue per iteration on c5, more than the loads they would cover)
-    IT_T(ta_p);
-    IT_ADD(9, ta_g, ta_p);
     auto scatter = [&](int row, double d) {
       for (int e = s_bp[row] + lane; e < s_bp[row + 1]; e += 32) {
         const int ce = s_ce[e];
         a.sdelta[ce >= 0 ? ce : ~ce] = ce >= 0 ? d : -d;
       }
     };
-    for (int row = gw; row < tau; row += GW) {
-      const double* rw = Gi + (long long)row * a.ld_gi;
-      if (a.big) {   // t = W g, lower rows
-        const double t = row_dot(rw, xs, 0, row + 1, lane);
-        if (lane == 0) a.tvec[row] = t;
-      } else {       // delta = G^{-1} g, full rows
-        const double d = row_dot(rw, xs, 0, tau, lane);
+    if (!a.big) {   // delta = G^{-1} g, full rows
+      for (int row = gw; row < tau; row += GW) {
+        const double d = row_dot(Gi + (long long)row * a.ld_gi, xs, 0, tau, lane);
         if (lane == 0) a.dvec[row] = d;
         scatter(row, d);
       }
-    }
-    IT_T(ta_r);
-    IT_ADD(10, ta_p, ta_r);
-    if (a.big) {   // this CTA's rows of W^T, pulled into L2 for phase B
-      for (int row = gw; row < tau; row += GW)
-        if (lane == 0)
-          pf_l2(Gi + (long long)row * a.ld_gi + (row & ~1), (unsigned)(((tau - (row & ~1)) * 8 + 15) & ~15));
-    }
-    IT_T(ta1);
-    IT_ADD(0, ta0, ta1);
-    grid.sync();
-    IT_T(tb0);
-    IT_ADD(1, ta1, tb0);
-    // ---- phase B (tau > 224): delta = W^T t, S delta scattered
-    if (a.big) {
-      for (int b = tid; b < tau; b += IT_THREADS) xs[b] = __ldcg(a.tvec + b);
-      __syncthreads();
-      for (int row = gw; row < tau; row += GW) {   // delta = W^T t, upper rows
-        const double d = row_dot(Gi + (long long)row * a.ld_gi, xs, row, tau, lane);
-        if (lane == 0) a.dvec[row] = d;
-        scatter(row, d);
+      IT_T(ta1);
+      IT_ADD(0, ta0, ta1);
+      grid.sync();
+    } else {
+      // tau > 224: the slot holds, in its lower triangle, W_bb = L_bb^{-1} on the diagonal
+      // super-blocks b (width sbw) and L_bc (b > c) below them, and the transpose in its upper
+      // triangle (bfactor.cu).  delta = G^{-1} g = L^{-T} (L^{-1} g) by block substitution:
+      //   forward   y_b = W_bb (g_b - sum_{c<b} L_bc y_c)             b = 0 .. nb-1
+      //   backward  delta_b = W_bb^T (y_b - sum_{c>b} L_cb^T delta_c)   b = nb-1 .. 0
+      // one grid barrier after every block step; nb = 1 is t = W g, delta = W^T t (W = L^{-1}).
+      // Vectors between CTAs: forward h in dvec, y in tvec; backward h in tvec, delta in dvec (each
+      // buffer is rewritten only after a barrier that follows every CTA's read of it).
+      const int sbw = a.sb > 0 && a.sb < tau ? a.sb : tau;
+      const int nb = (tau + sbw - 1) / sbw;
+      for (int b = 0; b < nb; ++b) {
+        const int r0 = b * sbw, r1 = min(tau, r0 + sbw);
+        if (b > 0) {   // h_b = g_b - L_{b,<b} y_{<b}  (lower rows, columns [0, r0))
+          for (int row = r0 + gw; row < r1; row += GW) {
+            const double h = row_dot(Gi + (long long)row * a.ld_gi, ys, 0, r0, lane);
+            if (lane == 0) a.dvec[row] = xs[row] - h;
+          }
+          grid.sync();
+          for (int x = r0 + tid; x < r1; x += IT_THREADS) xs[x] = __ldcg(a.dvec + x);
+          __syncthreads();
+        }
+        for (int row = r0 + gw; row < r1; row += GW) {   // y_b = W_bb h_b (columns [r0, row])
+          const double t = row_dot(Gi + (long long)row * a.ld_gi, xs, r0, row + 1, lane);
+          if (lane == 0) a.tvec[row] = t;
+        }
+        if (b == 0)   // this CTA's upper rows (the transposed factors), into L2 for the backward steps
+          for (int row = gw; row < tau; row += GW)
+            if (lane == 0)
+              pf_l2(Gi + (long long)row * a.ld_gi + (row & ~1), (unsigned)(((tau - (row & ~1)) * 8 + 15) & ~15));
+        grid.sync();
+        for (int x = r0 + tid; x < r1; x += IT_THREADS) ys[x] = __ldcg(a.tvec + x);
+        __syncthreads();
+      }
+      IT_T(tb0);
+      IT_ADD(0, ta0, tb0);
+      for (int b = nb - 1; b >= 0; --b) {
+        const int r0 = b * sbw, r1 = min(tau, r0 + sbw);
+        const double* hv = ys;
+        if (b < nb - 1) {   // h_b = y_b - L_{>b,b}^T delta_{>b}  (upper rows, columns [r1, tau))
+          for (int row = r0 + gw; row < r1; row += GW) {
+            const double h = row_dot(Gi + (long long)row * a.ld_gi, xs, r1, tau, lane);
+            if (lane == 0) a.tvec[row] = ys[row] - h;
+          }
+          grid.sync();
+          for (int x = r0 + tid; x < r1; x += IT_THREADS) xs[x] = __ldcg(a.tvec + x);
+          __syncthreads();
+          hv = xs;
+        }
+        for (int row = r0 + gw; row < r1; row += GW) {   // delta_b = W_bb^T h_b (columns [row, r1))
+          const double d = row_dot(Gi + (long long)row * a.ld_gi, hv, row, r1, lane);
+          if (lane == 0) a.dvec[row] = d;
+          scatter(row, d);
+        }
+        grid.sync();
+        if (b > 0) {   // delta_b for the next blocks' h (xs[r0, r1): h_b is consumed)
+          for (int x = r0 + tid; x < r1; x += IT_THREADS) xs[x] = __ldcg(a.dvec + x);
+          __syncthreads();
+        }
       }
       IT_T(tb1);
       IT_ADD(2, tb0, tb1);
-      grid.sync();
-      IT_T(tb2);
-      IT_ADD(3, tb1, tb2);
     }
     IT_T(tc0);
     // ---- phase C: u_j = sum_rows coef_row X[row][j] over this CTA's columns; heavy-ball update.
@@ -362,7 +395,7 @@ size_t iterate_smem() { return 218 * 1024; }   // + the small static arrays <= t
 // dynamic shared memory: g / t and the coefficients (doubles), sketch entries, buckets, bucket
 // pointers and row offsets (ints), phase C's reduction buffer
 static size_t it_smem_bytes(int tau, int len) {
-  return (size_t)(tau + len) * 8 + (size_t)(2 * len + tau + 1) * 4 + (size_t)len * 4 + 16 +
+  return (size_t)(2 * tau + len) * 8 + (size_t)(2 * len + tau + 1) * 4 + (size_t)len * 4 + 16 +
          (size_t)IT_WARPS * IT_NG * 64 * 8;
 }
 

@@ -213,6 +213,8 @@ struct IterArgs {
   double gamma, beta;
   int nslots;                    // iterations of the group
   int big;                       // tau > 224
+  int sb;                        // tau > 224: super-block width of the slot's blocked inverse
+                                 // (bfactor.cu; 0 or >= tau: W = L^{-1} in full)
   int wait;                      // flags[q] < 0: slot q is still being factored (by a concurrent
                                  // kernel), spin until it is 0 or 1
 };
@@ -321,7 +323,7 @@ struct BfClaim {
 cudaError_t launch_bfactor(const FactorSrc& src, const DevSketch& skb, int nslots, double* Ginv,
                            long long ldgi, long long gi_stride, int* flags, double* work,
                            const Ctrl* ctrl, cudaStream_t st, bool dual = false,
-                           const BfClaim* claim = nullptr);
+                           const BfClaim* claim = nullptr, int sb = 0);
 // delta = Ginv (S^T r), sdelta[coord_e] = sign_e delta[bucket_e]; flag != 0 -> status NOTSPD.
 // tau <= 224: the slot holds G^{-1} (full); tau > 224: it holds W = L^{-1} (lower) and
 // delta = W^T (W g).  gbuf: 2 tau doubles of scratch (g, W g).

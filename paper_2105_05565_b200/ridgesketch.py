@@ -58,7 +58,7 @@ class rs_report(C.Structure):
                 ("setup_seconds", C.c_double), ("solve_seconds", C.c_double),
                 ("trace_len", C.c_int64), ("kernel_ms", C.c_double * 8),
                 ("kernel_launches", C.c_int64 * 8), ("gpu_launches", C.c_int64),
-                ("overlap_sms", C.c_int32)]
+                ("overlap_sms", C.c_int32), ("inverse_blocks", C.c_int32)]
 
 
 _P = C.c_void_p
@@ -85,7 +85,7 @@ _lib.rs_status_string.argtypes = [C.c_int]
 _lib.rs_status_string.restype = C.c_char_p
 _lib.rs_last_error.restype = C.c_char_p
 _lib.rs_abi_version.restype = C.c_int
-_ABI = 4   # rs_report / rs_solve_opts layouts above
+_ABI = 5   # rs_report / rs_solve_opts layouts above
 if _lib.rs_abi_version() != _ABI:
     raise ImportError(f"libridgesketch.so ABI {_lib.rs_abi_version()} != binding ABI {_ABI}: rebuild "
                       "(python -m paper_2105_05565_b200._build)")
@@ -262,7 +262,8 @@ def rs_solve(h, kind="subsample", tau=1, gamma=1.0, beta=0.0, tol=0.0, max_iter=
                   solve_seconds=rep.solve_seconds,
                   kernel_ms={k: rep.kernel_ms[i] for i, k in enumerate(KERNEL_CLASSES)},
                   kernel_launches={k: rep.kernel_launches[i] for i, k in enumerate(KERNEL_CLASSES)},
-                  gpu_launches=rep.gpu_launches, overlap_sms=rep.overlap_sms)
+                  gpu_launches=rep.gpu_launches, overlap_sms=rep.overlap_sms,
+                  inverse_blocks=rep.inverse_blocks)
     if trace_cap:
         report["trace"] = trace[:rep.trace_len].copy()
     if al is not None:

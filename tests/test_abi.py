@@ -40,7 +40,7 @@ def test_library_exports_every_declared_symbol(rs):
 
 
 def test_abi_version_and_status_strings(rs):
-    assert rs.rs_abi_version() == 4
+    assert rs.rs_abi_version() == 5
     assert rs.rs_status_string(0) == "RS_OK"
     for s in range(1, 8):
         assert rs.rs_status_string(s).startswith("RS_E")

@@ -586,6 +586,32 @@ def test_kernel_ridge_parity(rs, kind, tau, k, beta, lam, sigma):
     assert rel(r, r_ld) <= bound, (rel(r, r_ld), bound)
 
 
+@pytest.mark.parametrize("kind,tau", [("subsample", 600), ("count", 700), ("subsample", 1032)])
+def test_kernel_ridge_blocked_inverse(rs, kind, tau):
+    """Kernel ridge (NEXT-4) at tau >= 512 runs the group kernel on the blocked inverse (two
+    diagonal super-blocks of W_bb = L_bb^{-1}, L below them; bfactor.cu / iterate.cu): tau = 600
+    and 700 leave a ragged second block (320 + 280, 384 + 316), 1032 is k1's tau (576 + 456).
+    Iterates equal the oracle's within 1e-10 (well-conditioned: kappa(G_0) < 1e4 asserted)."""
+    rng = np.random.default_rng(9)
+    n, d, lam, sigma = 1400, 5, 0.5, 0.3
+    X = rng.standard_normal((n, d))
+    y = np.sin(X @ rng.standard_normal(d)) + 0.05 * rng.standard_normal(n)
+    h = rs.rs_create_kernel(X, y, lam, sigma)
+    try:
+        a, rep = rs.rs_solve(h, kind, tau, 1.0, 0.5, 0.0, 30, seed=4)
+        _, r = rs.rs_get_state(h)
+    finally:
+        rs.rs_destroy(h)
+    ref = OV.solve_kernel(X, y, lam, sigma, kind, tau, 1.0, 0.5, 0.0, 30, seed=4)
+    sysk = OP.build_kernel(X, y, lam, sigma)
+    S0 = OS.materialize(OS.draw(kind, n, tau, 0, 4, 0)).toarray()
+    S0 = S0[:, np.abs(S0).sum(axis=0) > 0]   # (count: empty buckets are the identity, R3)
+    assert np.linalg.cond(S0.T @ sysk["A"] @ S0) < 1e4
+    assert rep["iterations"] == 30
+    assert_close(a, ref["w"], 1e-10)
+    assert_close(r, ref["r"], 1e-10)
+
+
 def test_kernel_ridge_converges_and_predicts(rs):
     rng = np.random.default_rng(8)
     n, d = 200, 3

@@ -86,7 +86,7 @@ w, rep = rs.rs_solve(h, "subsample", 1024, 1.0, 0.5, 0.0, int(sys.argv[6]), seed
 _, r = rs.rs_get_state(h)
 rs.rs_destroy(h)
 assert rep["overlap_sms"] > 0, rep
-np.savez(sys.argv[2], w=w, r=r)
+np.savez(sys.argv[2], w=w, r=r, nb=rep["inverse_blocks"])
 """
 
 
@@ -121,16 +121,20 @@ def test_c5_shape_overlapped_groups(rs, data, kind):
     assert rep["iterations"] == OV_ITERS
     # c5's subsample sketch runs the overlapped pipeline (the SM split is the engine's model)
     assert kind != "subsample" or rep["overlap_sms"] > 0, rep["overlap_sms"]
+    assert rep["inverse_blocks"] == 2, rep["inverse_blocks"]   # tau >= 512: two super-blocks
     ref = _ov_oracle(data, kind)
     assert_close(w, ref["w"], 1e-9, f"{kind} w")
     assert_close(r, ref["r"], 1e-9, f"{kind} r")
 
 
-@pytest.mark.parametrize("env", [{"RS_OV_SPLIT": "0"}, {"RS_BF_DUAL": "0"}])
+@pytest.mark.parametrize("env", [{"RS_OV_SPLIT": "0"}, {"RS_BF_DUAL": "0"}, {"RS_SB_NB": "1"},
+                                 {"RS_SB_NB": "3"}, {"RS_SB_NB": "6", "RS_BF_DUAL": "0"}])
 def test_c5_shape_overlapped_switches(tmp_path, data, env):
     """The process-wide A/B switches of the overlapped pipeline (read once per process, so in a
-    child): the whole first set up front (RS_OV_SPLIT=0) and the 8-warp one-slot-per-SM
-    factorisation (RS_BF_DUAL=0) give the oracle's iterates too."""
+    child): the whole first set up front (RS_OV_SPLIT=0), the 8-warp one-slot-per-SM
+    factorisation (RS_BF_DUAL=0) and the blocked inverse's super-block count (RS_SB_NB: 1 = the
+    full W = L^{-1}; 3 = blocks of 384, 384, 256; 6 = five of 192 and one of 64)
+    give the oracle's iterates too (the default is 2 blocks of 512)."""
     import os, subprocess, sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     outp = tmp_path / "ov.npz"
@@ -139,6 +143,7 @@ def test_c5_shape_overlapped_switches(tmp_path, data, env):
                          timeout=900)
     assert res.returncode == 0, res.stderr[-2000:]
     got = np.load(outp)
+    assert int(got["nb"]) == int(env.get("RS_SB_NB", 2)), int(got["nb"])
     ref = _ov_oracle(data, "subsample")
     assert_close(got["w"], ref["w"], 1e-9, f"{env} w")
     assert_close(got["r"], ref["r"], 1e-9, f"{env} r")
