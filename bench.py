@@ -511,8 +511,10 @@ def run_ours(args):
             rp, ci, va, yv = rsinputs.csr_uniform(cfg.n, cfg.d, cfg.nnz_per_row, seed=0)
         host = (rp, ci, va, yv)
         dual = cfg.d > cfg.n
-        if dual:
-            b0, ln = rs.rs_shard_range(cfg.d, rank, world)
+        if dual:   # contiguous feature ranges balanced by nnz (Zipf popularity: plain ranges of
+                   # d / world features would give rank 0 most of the entries)
+            colptr = np.concatenate([[0], np.cumsum(np.bincount(ci, minlength=cfg.d))]).astype(np.int64)
+            b0, ln = rs.rs_shard_rows_nnz(colptr, rank, world)
             rp, ci, va = _csr_column_block(np, rp, ci, va, b0, ln)
         else:
             b0, ln = rs.rs_shard_rows_nnz(rp, rank, world)

@@ -946,8 +946,10 @@ __device__ __forceinline__ bool lp_factor_slot(const FactorSrc& src, const DevSk
     mma_tile<false, true>(t32, S, PLD, P3 + 2 * PT, PLD, lane, 1.0);   // L_i,p0+1
     acc_store(t32, T(i, p0 + 1), tp, lane);
     __syncwarp();
-    if (offd) {
-      emit_w(i, p0 + 1, T(i, p0 + 1), tp);
+    if (offd) {   // (from shared memory: the transposed half reads down columns)
+      acc_store(t32, S, PLD, lane);
+      __syncwarp();
+      emit_w(i, p0 + 1, S, PLD);
       __syncwarp();
     }
   };

@@ -1020,9 +1020,10 @@ rs_status Problem::solve(const rs_solve_opts* o, double* w_out, rs_mem w_mem, do
     const double cols = 64.0 * (double)((cw + 63) / 64);
     return std::max(rows_it * 8.0 * cols / 45e3, rows_it * (double)m * 8.0 / 4.5e6) + 12.0;
   };
-  // (blocked inverse, nb super-blocks: the inverse step shrinks to 1/nb^2 of its flop)
+  // (blocked inverse, nb super-blocks: the inverse step -- ~0.32 of the full-inverse slot time on
+  // c5 -- shrinks to 1/nb^2 of its flop; measured c5 factor per slot 53 -> 40.5 us at nb = 2)
   const int nb_sb = len_d <= 8192 ? sb_blocks((int)o->tau) : 1;
-  const double fslot = 1924.0 * std::pow(tau_d / 256.0, 0.702) * (0.5 + 0.5 / (nb_sb * nb_sb));
+  const double fslot = 1924.0 * std::pow(tau_d / 256.0, 0.702) * (0.68 + 0.32 / (nb_sb * nb_sb));
   const int it_grid = (int)std::min<long long>(num_sms, std::max<long long>(16, (m + 63) / 64));
   const double seq_us = fslot / num_sms + it_us(it_grid);
   static const int ov_env = [] {

@@ -109,3 +109,30 @@ def test_two_rank_partial_sums_match_full():
         for k in ("primal_AS", "primal_b", "primal_A", "csr_AS", "dual_AS", "dual_w"):
             assert o[k] <= 1e-10, (r, k, o[k])
         assert o["sketch_equal"]
+
+
+@pytest.mark.parametrize("world", [2, 4, 8])
+def test_dual_feature_shards_balanced_by_nnz(world):
+    """c4-shaped dual (Zipf(1.1) feature popularity): bench.py shards the features as contiguous
+    ranges balanced by nnz (rs_shard_rows_nnz over the column pointer).  The ranges tile [0, d)
+    exactly once, every rank's nnz is within one feature's nnz of the even share, and the largest
+    shard is no larger than with plain d / world feature ranges."""
+    from paper_2105_05565_b200 import build
+    build()
+    from paper_2105_05565_b200 import ridgesketch as rs
+    n, d = 2000, 100_000
+    rp, ci, va, y = rsinputs.csr_zipf(n, d, 25, a=1.1, seed=0)
+    cnt = np.bincount(ci, minlength=d)
+    colptr = np.concatenate([[0], np.cumsum(cnt)]).astype(np.int64)
+    total = int(colptr[-1])
+    nxt, bal, plain = 0, [], []
+    for r in range(world):
+        b0, ln = rs.rs_shard_rows_nnz(colptr, r, world)
+        assert b0 == nxt and ln >= 0
+        nxt = b0 + ln
+        bal.append(int(colptr[b0 + ln] - colptr[b0]))
+        assert abs(bal[-1] - total / world) <= cnt.max() + 1, (r, bal[-1], total / world)
+        p0, pl = rs.rs_shard_range(d, r, world)
+        plain.append(int(colptr[p0 + pl] - colptr[p0]))
+    assert nxt == d and sum(bal) == total
+    assert max(bal) <= max(plain), (bal, plain)

@@ -67,20 +67,24 @@ k_reg(const double* __restrict__ A, long long lda, const int* __restrict__ rows,
   }
 }
 
-// (b) bulk ring: stage = RPS row segments of cw doubles (cw <= CWMAX)
+// (b) bulk ring: stage = RPS row segments of cw doubles (cw <= CWMAX); warp 16 is the producer
+// (row offsets staged in shared memory, lane 0 issues), warps 0-15 consume
 template <int NST, int RPS, int CWMAX>
-__global__ void __launch_bounds__(512, 1)
+__global__ void __launch_bounds__(544, 1)
 k_ring(const double* __restrict__ A, long long lda, const int* __restrict__ rows, const double* __restrict__ coef,
        int nr, long long m, double* __restrict__ u, int reps) {
   extern __shared__ __align__(128) double sm[];
   uint64_t* full = reinterpret_cast<uint64_t*>(sm + (size_t)NST * RPS * CWMAX);
   uint64_t* empty = full + NST;
   double* red = reinterpret_cast<double*>(empty + NST);   // [16][CWMAX]
+  int* s_row = reinterpret_cast<int*>(red + 16 * CWMAX);
+  double* s_cf = reinterpret_cast<double*>(s_row + nr + (nr & 1));
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const long long cw = ((m + gridDim.x - 1) / gridDim.x + 1) & ~1LL;
   const long long j0 = min(m, (long long)blockIdx.x * cw), j1 = min(m, j0 + cw);
   const int w = (int)(j1 - j0);
   const unsigned seg = (unsigned)w * 8u;
+  for (int e = tid; e < nr; e += 544) { s_row[e] = rows[e]; s_cf[e] = coef[e]; }
   if (tid == 0) {
     for (int s = 0; s < NST; ++s) {
       asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(su32(&full[s])));
@@ -91,24 +95,24 @@ k_ring(const double* __restrict__ A, long long lda, const int* __restrict__ rows
   __syncthreads();
   const int nstage = (nr + RPS - 1) / RPS;
   const int total = nstage * reps;
-  // producer: warp 0 lane 0 issues ahead (it is also a consumer: issue for stage t + NST - 1 first)
   auto wait = [&](uint64_t* b, unsigned ph) {
     asm volatile("{\n.reg .pred P;\nW_%=:\nmbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n@!P bra W_%=;\n}\n"
                  ::"r"(su32(b)), "r"(ph) : "memory");
   };
-  auto issue = [&](int t) {
-    const int s = t % NST, st = t % nstage;
-    const int e0 = st * RPS, n = min(RPS, nr - e0);
-    if (t >= NST) wait(&empty[s], (unsigned)(((t / NST) - 1) & 1));
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(su32(&full[s])), "r"(seg * n) : "memory");
-    for (int q = 0; q < n; ++q)
-      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n"
-                   ::"r"(su32(sm + ((size_t)s * RPS + q) * CWMAX)), "l"(A + (long long)rows[e0 + q] * lda + j0),
-                   "r"(seg), "r"(su32(&full[s])) : "memory");
-  };
-  if (tid == 0)
-    for (int t = 0; t < min(NST, total); ++t) issue(t);
-  // consumers: thread = (row group rg = warp, column pairs lane + 32 k)
+  if (warp == 16) {
+    if (lane == 0)
+      for (int t = 0; t < total; ++t) {
+        const int s = t % NST, st = t % nstage;
+        const int e0 = st * RPS, n = min(RPS, nr - e0);
+        if (t >= NST) wait(&empty[s], (unsigned)(((t / NST) - 1) & 1));
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(su32(&full[s])), "r"(seg * n) : "memory");
+        for (int q = 0; q < n; ++q)
+          asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n"
+                       ::"r"(su32(sm + ((size_t)s * RPS + q) * CWMAX)), "l"(A + (long long)s_row[e0 + q] * lda + j0),
+                       "r"(seg), "r"(su32(&full[s])) : "memory");
+      }
+    return;
+  }
   double acc[CWMAX / 64][2];
   for (int t = 0; t < total; ++t) {
     const int s = t % NST, st = t % nstage;
@@ -118,7 +122,7 @@ k_ring(const double* __restrict__ A, long long lda, const int* __restrict__ rows
     const int e0 = st * RPS, n = min(RPS, nr - e0);
     const double* buf = sm + (size_t)s * RPS * CWMAX;
     for (int q = warp; q < n; q += 16) {
-      const double cf = coef[e0 + q];
+      const double cf = s_cf[e0 + q];
 #pragma unroll
       for (int k = 0; k < CWMAX / 64; ++k) {
         const int c = 2 * (lane + 32 * k);
@@ -131,19 +135,18 @@ k_ring(const double* __restrict__ A, long long lda, const int* __restrict__ rows
     }
     __syncwarp();
     if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(su32(&empty[s])) : "memory");
-    if (tid == 0 && t + NST < total) issue(t + NST);
-    if (st == nstage - 1) {   // end of a rep: reduce the 16 row groups
+    if (st == nstage - 1) {   // end of a rep: reduce the 16 row groups (consumer warps only)
       for (int k = 0; k < CWMAX / 64; ++k) {
         const int c = 2 * (lane + 32 * k);
         if (c < w) { red[warp * CWMAX + c] = acc[k][0]; red[warp * CWMAX + c + 1] = acc[k][1]; }
       }
-      __syncthreads();
+      asm volatile("bar.sync 1, 512;\n" ::: "memory");
       for (int c = tid; c < w; c += 512) {
         double a = 0;
         for (int g = 0; g < 16; ++g) a += red[g * CWMAX + c];
         u[j0 + c] = a;
       }
-      __syncthreads();
+      asm volatile("bar.sync 1, 512;\n" ::: "memory");
     }
   }
 }
@@ -189,25 +192,32 @@ int main(int argc, char** argv) {
   for (int S : {16, 32, 48, 64, 148}) {
     run("reg (k_iterate)", [&](int s) { k_reg<<<s, 512>>>(A, lda, rows, coef, nr, m, u, reps); }, S);
     {
-      constexpr int NST = 12, RPS = 8, CW = 256;
-      const size_t smem = (size_t)NST * RPS * CW * 8 + 2 * NST * 8 + 16 * CW * 8;
+      constexpr int NST = 5, RPS = 16, CW = 256;
+      const size_t smem = (size_t)NST * RPS * CW * 8 + 2 * NST * 8 + 16 * CW * 8 + (size_t)nr * 12 + 8;
       CK(cudaFuncSetAttribute(k_ring<NST, RPS, CW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
       if ((m + S - 1) / S <= CW)
-        run("ring 12x8 (cw<=256)", [&](int s) { k_ring<NST, RPS, CW><<<s, 512, smem>>>(A, lda, rows, coef, nr, m, u, reps); }, S);
+        run("ring 5x16 (cw<=256)", [&](int s) { k_ring<NST, RPS, CW><<<s, 544, smem>>>(A, lda, rows, coef, nr, m, u, reps); }, S);
     }
     {
-      constexpr int NST = 20, RPS = 8, CW = 128;
-      const size_t smem = (size_t)NST * RPS * CW * 8 + 2 * NST * 8 + 16 * CW * 8;
+      constexpr int NST = 10, RPS = 16, CW = 128;
+      const size_t smem = (size_t)NST * RPS * CW * 8 + 2 * NST * 8 + 16 * CW * 8 + (size_t)nr * 12 + 8;
       CK(cudaFuncSetAttribute(k_ring<NST, RPS, CW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
       if ((m + S - 1) / S <= CW)
-        run("ring 20x8 (cw<=128)", [&](int s) { k_ring<NST, RPS, CW><<<s, 512, smem>>>(A, lda, rows, coef, nr, m, u, reps); }, S);
+        run("ring 10x16 (cw<=128)", [&](int s) { k_ring<NST, RPS, CW><<<s, 544, smem>>>(A, lda, rows, coef, nr, m, u, reps); }, S);
     }
     {
-      constexpr int NST = 6, RPS = 4, CW = 1024;
-      const size_t smem = (size_t)NST * RPS * CW * 8 + 2 * NST * 8 + 16 * CW * 8;
+      constexpr int NST = 5, RPS = 32, CW = 128;
+      const size_t smem = (size_t)NST * RPS * CW * 8 + 2 * NST * 8 + 16 * CW * 8 + (size_t)nr * 12 + 8;
       CK(cudaFuncSetAttribute(k_ring<NST, RPS, CW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
       if ((m + S - 1) / S <= CW && smem <= 227 * 1024)
-        run("ring 6x4 (cw<=1024)", [&](int s) { k_ring<NST, RPS, CW><<<s, 512, smem>>>(A, lda, rows, coef, nr, m, u, reps); }, S);
+        run("ring 5x32 (cw<=128)", [&](int s) { k_ring<NST, RPS, CW><<<s, 544, smem>>>(A, lda, rows, coef, nr, m, u, reps); }, S);
+    }
+    {
+      constexpr int NST = 10, RPS = 32, CW = 64;
+      const size_t smem = (size_t)NST * RPS * CW * 8 + 2 * NST * 8 + 16 * CW * 8 + (size_t)nr * 12 + 8;
+      CK(cudaFuncSetAttribute(k_ring<NST, RPS, CW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      if ((m + S - 1) / S <= CW)
+        run("ring 10x32 (cw<=64)", [&](int s) { k_ring<NST, RPS, CW><<<s, 544, smem>>>(A, lda, rows, coef, nr, m, u, reps); }, S);
     }
   }
   return 0;
