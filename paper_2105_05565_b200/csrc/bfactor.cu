@@ -546,10 +546,19 @@ struct LpCfg {
   static constexpr int WARPS = NW;
   static constexpr int THREADS = NW * 32;           // 255 registers: acc[4][8][2] per lane
   static constexpr int CTAS = NW == 8 ? 1 : 2;      // resident CTAs per SM
-  static constexpr int KS = NW == 8 ? 32 : 16;      // k slice depth
-  static constexpr int STAGES = 2;                  // double-buffered k slices
+#ifndef RS_LP4_KS
+#define RS_LP4_KS 16
+#endif
+#ifndef RS_LP4_ST
+#define RS_LP4_ST 2
+#endif
+#ifndef RS_LP8_ST
+#define RS_LP8_ST 2
+#endif
+  static constexpr int KS = NW == 8 ? 32 : RS_LP4_KS;   // k slice depth
+  static constexpr int STAGES = NW == 8 ? RS_LP8_ST : RS_LP4_ST;   // k slices in flight + 1
   static constexpr int BLD = KS + 4;                // B [n][k] row stride (Cholesky) and A [r][k]:
-  static constexpr int ALD = KS + 4;                //   36 / 20 = 4 mod 16 -> conflict-free fragments
+  static constexpr int ALD = KS + 4;                //   36 / 20 / 12 = +-4 mod 16 -> conflict-free
   static constexpr int BTLD = 68;                   // B [k][n] row stride (inverse), 68 = 4 mod 16
   static constexpr int BSZ = 64 * BLD;              // >= KS * BTLD
   static constexpr int ASZ = 32 * ALD;

@@ -99,7 +99,7 @@ rs_status Problem::csr_build_explicit() {
       k_heavy_dense<<<nh, 256, 0, st>>>(R.ptr, R.idx, R.val, list, RH, lda);
       TmaGemm tg{};
       double* work = nullptr;
-      cudaError_t ce = tma_gemm_plan(&tg, RH, lda, RH, lda, m, m, nh, num_sms);
+      cudaError_t ce = tma_gemm_plan(&tg, RH, lda, RH, lda, m, m, nh, num_sms, 1);
       tg.lower = 1;
       if (ce == cudaSuccess && tg.work_elems) s = dalloc(&work, tg.work_elems);
       if (s == RS_OK && ce == cudaSuccess) ce = tma_gemm_launch(tg, A, lda, work, nullptr, st);

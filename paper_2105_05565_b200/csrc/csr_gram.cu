@@ -836,7 +836,7 @@ rs_status Problem::csr_gram_workspace(int kind, int tau) {
       RS_CUDA(cudaMemsetAsync(c->chunk_h0_none, 0, h0.size() * sizeof(int), st));
       if (c->nheavyR > 0) {
         RS_CUDA(tma_gemm_plan(&c->tg_heavy, c->hacc, c->ldh, c->hacc, c->ldh, tau, tau, c->nheavyR,
-                              num_sms));
+                              num_sms, 1));
         c->tg_heavy.lower = 1;
         if (c->tg_heavy.work_elems) RS_TRY(dalloc(&c->gh_work, c->tg_heavy.work_elems));
         RS_TRY(dalloc(&c->gh, (size_t)tau * round_up(tau, 4)));

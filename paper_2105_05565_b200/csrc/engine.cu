@@ -318,7 +318,7 @@ static rs_status create_dense(rs_problem* out, int64_t n, int64_t d, const doubl
     for (long long r0 = 0; r0 < rows; r0 += rc) {
       TmaGemm tgc{};
       const double* Xc = p->X + r0 * p->ldx;
-      cudaError_t ce = tma_gemm_plan(&tgc, Xc, p->ldx, Xc, p->ldx, d, d, std::min(rc, rows - r0), p->num_sms);
+      cudaError_t ce = tma_gemm_plan(&tgc, Xc, p->ldx, Xc, p->ldx, d, d, std::min(rc, rows - r0), p->num_sms, 1);
       if (ce != cudaSuccess) return guard(fail(RS_ECUDA, std::string("A build plan: ") + cudaGetErrorString(ce)));
       tgc.lower = 1;
       wmax = std::max(wmax, tgc.work_elems);
@@ -422,7 +422,7 @@ static rs_status create_dense(rs_problem* out, int64_t n, int64_t d, const doubl
     ldt = round_up(n, 4);
     s = dalloc(&xt, (size_t)d * ldt);
     if (s != RS_OK) return guard(s);
-    ce = tma_gemm_plan(&tg, xt, ldt, xt, ldt, n, n, d, p->num_sms);
+    ce = tma_gemm_plan(&tg, xt, ldt, xt, ldt, n, n, d, p->num_sms, 1);
     tg.lower = 1;
     if (ce == cudaSuccess && tg.work_elems) s = dalloc(&a_work, tg.work_elems);
     if (s != RS_OK) return guard(s);
@@ -432,7 +432,7 @@ static rs_status create_dense(rs_problem* out, int64_t n, int64_t d, const doubl
     s = dalloc(&p->A, (size_t)d * p->lda);
     if (s != RS_OK) return guard(s);
     if (rows > 0) {
-      ce = tma_gemm_plan(&tg, p->X, p->ldx, p->X, p->ldx, d, d, rows, p->num_sms);
+      ce = tma_gemm_plan(&tg, p->X, p->ldx, p->X, p->ldx, d, d, rows, p->num_sms, 1);
       if (std::getenv("RS_VERBOSE"))
         fprintf(stderr, "[rs] A build: TMA variant %d (%dx%d), splits %d\n", tg.variant, tg.bm, tg.bn, tg.splits);
       tg.lower = 1;
@@ -588,7 +588,7 @@ rs_status Problem::ensure_workspace(int kind, int tau, int ksum, int depth, bool
       }
     }
     if (rows_loc > 0 && !gram_fused) {
-      RS_CUDA(tma_gemm_plan(&tg_gram, XS, ld_xs, XS, ld_xs, tau, tau, rows_loc, num_sms));
+      RS_CUDA(tma_gemm_plan(&tg_gram, XS, ld_xs, XS, ld_xs, tau, tau, rows_loc, num_sms, 1));
       tg_gram.lower = 1;   // G is symmetric and only its lower triangle is read (R12)
       if (tg_gram.work_elems) RS_TRY(dalloc(&gemm_work, tg_gram.work_elems));
       if (std::getenv("RS_VERBOSE"))

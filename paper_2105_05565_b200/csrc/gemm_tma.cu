@@ -156,10 +156,17 @@ k_tn_gemm_tma(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ C
 
 __global__ void k_splitk_reduce2(const double* __restrict__ work, int splits, long long split_stride,
                                  long long M, long long N, long long ldw, double* __restrict__ C,
-                                 long long ldc, const Ctrl* ctrl) {
+                                 long long ldc, const Ctrl* ctrl, int lbm, int lbn) {
+  // lbm > 0 (lower use, tiles lbm x lbn): columns in tiles strictly above the diagonal are never
+  // written by the contraction (left to the mirror / never read) and skipped here
   if (ctrl && ctrl->done) return;
   const long long row = blockIdx.y;
-  for (long long j = (long long)blockIdx.x * blockDim.x + threadIdx.x; j < N;
+  long long jmax = N;
+  if (lbm > 0) {
+    const long long mend = (row / lbm) * lbm + lbm;   // a tile works iff n0 < m0 + bm
+    jmax = min(N, (mend + lbn - 1) / lbn * lbn);
+  }
+  for (long long j = (long long)blockIdx.x * blockDim.x + threadIdx.x; j < N && j < jmax;
        j += (long long)gridDim.x * blockDim.x) {
     double s = 0.0;
     for (int z = 0; z < splits; ++z) s += work[z * split_stride + row * ldw + j];
@@ -238,11 +245,22 @@ cudaError_t tma_gemm_init() {
 // Plan (variant, split-K) by the same wave / padded-work cost model as plan_tn_gemm, and encode
 // the two TMA descriptors (the operand pointers are fixed for the life of the workspace).
 cudaError_t tma_gemm_plan(TmaGemm* g, const double* Aop, long long lda, const double* Bop,
-                          long long ldb, long long M, long long N, long long K, int num_sms) {
+                          long long ldb, long long M, long long N, long long K, int num_sms,
+                          int lower) {
   double best_cost = 1e300;
   for (int v = 0; v < kNumT; ++v) {
     const TVariant& V = kT[v];
-    const long long tiles = ((M + V.bm() - 1) / V.bm()) * ((N + V.bn() - 1) / V.bn());
+    // lower: only the tiles on or below the diagonal work (the others return at entry), so the
+    // waves are counted over those (c5's A build: 528 of 1024 128 x 128 tiles)
+    long long tiles = 0;
+    const long long tmn = (M + V.bm() - 1) / V.bm(), tnn = (N + V.bn() - 1) / V.bn();
+    if (lower) {
+      for (long long i = 0; i < tmn; ++i)
+        for (long long j = 0; j < tnn; ++j)
+          if (i * V.bm() + V.bm() > j * V.bn()) ++tiles;
+    } else {
+      tiles = tmn * tnn;
+    }
     const long long slots = (long long)g_tctas[v] * num_sms;
     for (int s = 1; s <= 32; ++s) {
       if (s > 1 && K / s < 256) break;
@@ -259,6 +277,7 @@ cudaError_t tma_gemm_plan(TmaGemm* g, const double* Aop, long long lda, const do
     }
   }
   const TVariant& V = kT[g->variant];
+  g->lower = lower;
   long long kps = (K + g->splits - 1) / g->splits;
   g->k_per_split = (kps + BK - 1) / BK * BK;
   g->M = M;
@@ -296,7 +315,8 @@ cudaError_t tma_gemm_launch(const TmaGemm& g, double* C, long long ldc, double* 
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess || direct) return e;
   dim3 rg((unsigned)std::min<long long>((g.N + 255) / 256, 64), (unsigned)g.M);
-  k_splitk_reduce2<<<rg, 256, 0, st>>>(work, g.splits, so, g.M, g.N, g.ldw, C, ldc, ctrl);
+  k_splitk_reduce2<<<rg, 256, 0, st>>>(work, g.splits, so, g.M, g.N, g.ldw, C, ldc, ctrl,
+                                       g.lower ? V.bm() : 0, V.bn());
   return cudaGetLastError();
 }
 

@@ -154,7 +154,7 @@ rs_status create_kernel(rs_problem* out, int64_t n, int64_t d, const double* X, 
   {
     TmaGemm tg{};
     double* work = nullptr;
-    cudaError_t ce = tma_gemm_plan(&tg, K, p->lda, K, p->lda, n, n, n, p->num_sms);
+    cudaError_t ce = tma_gemm_plan(&tg, K, p->lda, K, p->lda, n, n, n, p->num_sms, 1);
     tg.lower = 1;
     if (ce == cudaSuccess && tg.work_elems) {
       s = dalloc(&work, tg.work_elems);

@@ -192,7 +192,7 @@ struct TmaGemm {
 cudaError_t launch_mirror_lower(double* A, long long lda, long long m, cudaStream_t st);
 cudaError_t tma_gemm_init();
 cudaError_t tma_gemm_plan(TmaGemm* g, const double* Aop, long long lda, const double* Bop,
-                          long long ldb, long long M, long long N, long long K, int num_sms);
+                          long long ldb, long long M, long long N, long long K, int num_sms, int lower = 0);
 cudaError_t tma_gemm_launch(const TmaGemm& g, double* C, long long ldc, double* work,
                             const Ctrl* ctrl, cudaStream_t st);
 
