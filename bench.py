@@ -286,15 +286,20 @@ def _csr_column_block(np, rowptr, colidx, vals, c0, clen):
 SMEM_FXADD_PEAK = 3.26 * 148 * 1.965
 
 
-def _traffic(cfg, args, cls):
+def _traffic(cfg, args, cls, units=None):
     """ncu dram__bytes_read.sum + dram__bytes_write.sum per launch of the dominant kernel, from the
-    committed capture summary profiles/traffic.json (None if not captured)."""
+    committed capture summary profiles/traffic.json (None if not captured).  A group kernel's entry
+    records the units (iterations / slots) of its captured launch; `units` = the units of a launch
+    here, and the bytes are scaled to it (same per-unit basis as `achieved`)."""
     if args.traffic is not None:
         return args.traffic
     try:
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
-            t = json.load(f)
-        return t.get(f"{cfg.name}/{args.mode}/{cls}", {}).get("bytes_per_launch")
+            t = json.load(f).get(f"{cfg.name}/{args.mode}/{cls}", {})
+        b = t.get("bytes_per_launch")
+        if b is not None and units and t.get("units_per_launch"):
+            b = b / t["units_per_launch"] * units
+        return b
     except Exception:
         return None
 
@@ -377,7 +382,8 @@ def _roofline(args, cfg, world, kms, kl, dom, prof_ms, host, rs, nb=1):
                         bound="tensor",
                         achieved=w / (ms * 1e-3) / 1e12, peak=FP64_DMMA_PEAK, unit="TFLOP/s",
                         peak_source=dmma_src,
-                        algorithmic_per_launch=f"{w:.3e} flop ({what} per G_k, x {slots:.0f} slots)")
+                        algorithmic_per_launch=f"{w:.3e} flop ({what} per G_k, x {slots:.0f} slots)",
+                        _units=slots)
         elif dom == "solve" and (args.mode == "explicit" or "rows" in cfg.extra):
             w = float(cfg.tau) * cfg.tau * 8.0
             roof = dict(kernel="class solve: delta = G_k^{-1} S^T r from the factor slot (tau <= 224: "
@@ -398,7 +404,8 @@ def _roofline(args, cfg, world, kms, kl, dom, prof_ms, host, rs, nb=1):
                         achieved=w / (ms * 1e-3) / 1e9, peak=hbm, unit="GB/s", peak_source=hbm_src,
                         algorithmic_per_launch=f"{w:.3e} bytes ({rows_s} sketched rows of A x m x 8 + 10 m-vectors"
                                                + (f" + the tau^2 slot, x {its:.0f} iterations)" if its > 1 else ")"),
-                        note=f"A = {a_mb:.0f} MB ({'fits' if a_mb < 126 else 'exceeds'} the 126 MB L2)")
+                        note=f"A = {a_mb:.0f} MB ({'fits' if a_mb < 126 else 'exceeds'} the 126 MB L2)",
+                        _units=its)
     else:
         nnz = int(host[0][-1])
         m = cfg.d if cfg.d <= cfg.n else cfg.n
@@ -447,7 +454,7 @@ def _roofline(args, cfg, world, kms, kl, dom, prof_ms, host, rs, nb=1):
                         peak_source=hbm_src,
                         algorithmic_per_launch=f"{w:.3e} bytes (X as CSR + CSC read once, A S written)")
     roof["frac"] = roof["achieved"] / roof["peak"]
-    roof["traffic"] = _traffic(cfg, args, dom)
+    roof["traffic"] = _traffic(cfg, args, dom, roof.pop("_units", None))
     roof["avg_launch_ms"] = ms
     roof["share_of_step"] = share
     return roof

@@ -1,4 +1,4 @@
-# Round profile (round 2): full GPU suite + smoke, every bench line, the default command's ncu launch
+# Round profile (round 2, final): full GPU suite + smoke, every bench line, the default command's ncu launch
 # list, ncu DRAM traffic of the dominant kernels, and --set full captures of the c5 step's kernels.
 set -x
 python -c "import __graft_entry__ as g; g.build()" || exit 1
@@ -11,6 +11,7 @@ $B --config c2 > gpurun_out/bench_c2_gram.json 2>/dev/null
 $B --config c2 --mode explicit --no-cpu-baseline --no-alt > gpurun_out/bench_c2_explicit.json 2>/dev/null
 $B --config c2 --mode implicit --no-cpu-baseline --no-alt --steps 50 --seeds 1 > gpurun_out/bench_c2_implicit.json 2>/dev/null
 RS_OV_SPLIT=0 $B --no-cpu-baseline --no-alt --no-e2e > gpurun_out/bench_c5_nosplit.json 2>/dev/null
+RS_SB_NB=1 $B --no-cpu-baseline --no-alt --no-e2e > gpurun_out/bench_c5_nb1.json 2>/dev/null
 $B --config c3 --max-iter-tol 20000 --cpu-seconds 20 --seeds 1 > gpurun_out/bench_c3.json 2>/dev/null
 $B --config c4 --max-iter-tol 20000 --cpu-seconds 20 > gpurun_out/bench_c4_explicit.json 2>/dev/null
 $B --config c4 --mode gram --max-iter-tol 20000 --no-cpu-baseline --seeds 1 > gpurun_out/bench_c4_gram.json 2>/dev/null
