@@ -101,6 +101,9 @@ rs_status Problem::csr_build_explicit() {
       double* work = nullptr;
       cudaError_t ce = tma_gemm_plan(&tg, RH, lda, RH, lda, m, m, nh, num_sms, 1);
       tg.lower = 1;
+      if (std::getenv("RS_VERBOSE"))
+        fprintf(stderr, "[rs] csr explicit heavy GEMM: M %lld K %d, variant %d (%dx%d), splits %d\n", m, nh,
+                tg.variant, tg.bm, tg.bn, tg.splits);
       if (ce == cudaSuccess && tg.work_elems) s = dalloc(&work, tg.work_elems);
       if (s == RS_OK && ce == cudaSuccess) ce = tma_gemm_launch(tg, A, lda, work, nullptr, st);
       cudaStreamSynchronize(st);

@@ -264,6 +264,9 @@ cudaError_t tma_gemm_plan(TmaGemm* g, const double* Aop, long long lda, const do
     const long long slots = (long long)g_tctas[v] * num_sms;
     for (int s = 1; s <= 32; ++s) {
       if (s > 1 && K / s < 256) break;
+      // split-K partials are s full M x N fp64 buffers: at most ~1 GB of them (an m = 2e4 system's
+      // output is 3.2 GB per split -- its allocation and reduce would cost more than the waves)
+      if (s > 1 && (double)s * M * N * 8.0 > 1.0e9) break;
       const long long ctas = tiles * s;
       const long long waves = (ctas + slots - 1) / slots;
       const double wave_work = (double)g_tctas[v] * V.bm() * V.bn() * ((double)K / s);

@@ -124,6 +124,17 @@ k_iterate(IterArgs a, Ctrl* ctrl) {
   const double rsb = 1.0 / sqrt(c0.bnorm2);
   if (a.nslots > 0) stage_sketch(a.skb.at(0), s_ce, s_bk, s_bp, tid);
   __syncthreads();
+  // g = S^T r of the staged sketch into xs, by threads t0, t0 + nt, ..
+  auto gather_g = [&](int t0, int nt) {
+    for (int b = t0; b < tau_c; b += nt) {
+      double g = 0.0;
+      for (int e = s_bp[b]; e < s_bp[b + 1]; ++e) {
+        const int ce = s_ce[e];
+        g += ce >= 0 ? __ldcg(a.r + ce) : -__ldcg(a.r + ~ce);
+      }
+      xs[b] = g;
+    }
+  };
   for (int q = 0; q < a.nslots; ++q) {
     const int tau = a.skb.tau;
     const int len = s_bp[tau];
@@ -150,17 +161,13 @@ k_iterate(IterArgs a, Ctrl* ctrl) {
     const int nr = a.ASt ? tau : len;   // rows of u's sum
     const double* X = a.ASt ? a.ASt + (long long)q * a.as_stride : a.A;
     const long long ldx = a.ASt ? a.ld_as : a.lda;
-    // ---- phase A: g = S^T r in shared memory; delta (tau <= 224) or t = W g
+    // ---- phase A: g = S^T r in shared memory (for q > 0 gathered right after the previous
+    // iteration's last barrier, beside the stop rule's reads); delta (tau <= 224) or t = W g
     IT_T(ta0);
-    for (int b = tid; b < tau; b += IT_THREADS) {
-      double g = 0.0;
-      for (int e = s_bp[b]; e < s_bp[b + 1]; ++e) {
-        const int ce = s_ce[e];
-        g += ce >= 0 ? __ldcg(a.r + ce) : -__ldcg(a.r + ~ce);
-      }
-      xs[b] = g;
+    if (q == 0) {
+      gather_g(tid, IT_THREADS);
+      __syncthreads();
     }
-    __syncthreads();
     IT_T(ta_g);
     IT_ADD(8, ta0, ta_g);
     // (no L2 prefetch of phase C's row segments: ~1000 cp.async.bulk.prefetch per CTA cost 7 us of
@@ -357,13 +364,17 @@ k_iterate(IterArgs a, Ctrl* ctrl) {
     grid.sync();
     IT_T(tc3);
     IT_ADD(6, tc2, tc3);
-    // ---- stop rule: every CTA sums the partials in the same order
+    // ---- stop rule: every CTA sums the partials in the same order (warp 0), while
+    // the other warps gather the next slot's g = S^T r from the final r (discarded if the rule
+    // stops the solve)
     if (warp == 0) {
       double t = 0.0;
       for (int p = lane; p < G; p += 32) t += __ldcg(a.partials + p);
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
       if (lane == 0) s_r2 = t;
+    } else if (q + 1 < a.nslots) {
+      gather_g(tid - 32, IT_THREADS - 32);
     }
     __syncthreads();
     const double tot = s_r2;
