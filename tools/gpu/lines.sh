@@ -1,4 +1,4 @@
-# Final lines after the g-gather overlap and the split-K cap: c5 default (full), c4 / k1 / c2 EXPLICIT, c4 THEORY
+# The EXPLICIT bench lines (c5 default with every leg, c4, c4 THEORY, k1, c2 EXPLICIT) -> gpurun_out/fin_*.json
 python -c "import __graft_entry__ as g; g.build()" || exit 1
 B="timeout 1200 python bench.py"
 $B > gpurun_out/fin_c5.json 2> gpurun_out/fin_c5.err

@@ -1,21 +1,18 @@
-# Blocked inverse: parity subset, RS_OV_SMS sweep on c5 / k1 (nb = 2), phase probes of k_iterate
+# A/B sweep of one environment switch over bench lines (development):
+#   VAR=RS_SB_NB VALUES="1 2 3" CONFIGS="c5 k1" bash tools/gpu/sweep.sh
+# (VAR e.g. RS_OV_SMS, RS_SB_NB, RS_OV_SPLIT, RS_BF_DUAL; an empty value = the default)
 python -c "import __graft_entry__ as g; g.build()" || exit 1
-timeout 1500 python -m pytest tests -m gpu -q -p no:cacheprovider --timeout 600 -k "${PYK:-tau1024 or blocked_inverse or kernel}" 2>&1 | tail -5 | tee gpurun_out/sw_pytest.log
-B="timeout 600 python bench.py --no-alt --no-e2e --no-cpu-baseline --seeds 2"
-for s in ${C5S:-0 24 28 36 40 48}; do
-  RS_OV_SMS=$s $B > gpurun_out/sw_c5_$s.json 2>/dev/null
+B="timeout 900 python bench.py --no-alt --no-e2e --no-cpu-baseline"
+for c in ${CONFIGS:-c5}; do
+  for v in ${VALUES:-""}; do
+    env $VAR=$v $B --config $c --max-iter-tol 20000 --seeds ${SEEDS:-3} > gpurun_out/sweep_${c}_${VAR}_$v.json 2>/dev/null
+  done
 done
-for s in ${K1S:-0 50 74 90}; do
-  RS_OV_SMS=$s $B --config k1 --max-iter-tol 2000 --seeds 1 > gpurun_out/sw_k1_$s.json 2>/dev/null
-done
-python - <<'PY' | tee gpurun_out/sw_summary.txt
+python - <<'PY' | tee gpurun_out/sweep_summary.txt
 import json, glob
-for f in sorted(glob.glob("gpurun_out/sw_*.json")):
+for f in sorted(glob.glob("gpurun_out/sweep_*.json")):
     try: d = json.loads(open(f).read().strip().splitlines()[-1])
-    except Exception as e: print(f, "unreadable"); continue
-    r = d["roofline"]; oc = r.get("other_classes", {})
-    print(f, round(d["value"]), "t_tol_ms", round(d["time_to_tol_s"] * 1e3, 2), "sms", r.get("sms"),
-          {k: round(v * 1e3, 1) for k, v in d["kernel_ms_per_step"].items() if v})
+    except Exception: print(f, "unreadable"); continue
+    print(f, round(d["value"]), "iters/s; to 1e-4", d.get("time_to_tol_seeds", {}).get("seconds_q1_median_q3"),
+          "s; SMs", d["roofline"].get("sms"), {k: round(v * 1e3, 1) for k, v in d["kernel_ms_per_step"].items() if v})
 PY
-RS_NVCC_EXTRA=-DRS_IT_PHASES python -m paper_2105_05565_b200._build --force > /dev/null 2>&1 && \
-  for nb in 1 2; do RS_SB_NB=$nb timeout 300 python tools/probe_it_phases.py c5 232 2>&1 | tail -12 > gpurun_out/sw_itphases_$nb.txt; done
