@@ -99,18 +99,19 @@ k_ring(const double* __restrict__ A, long long lda, const int* __restrict__ rows
     asm volatile("{\n.reg .pred P;\nW_%=:\nmbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n@!P bra W_%=;\n}\n"
                  ::"r"(su32(b)), "r"(ph) : "memory");
   };
-  if (warp == 16) {
-    if (lane == 0)
-      for (int t = 0; t < total; ++t) {
-        const int s = t % NST, st = t % nstage;
-        const int e0 = st * RPS, n = min(RPS, nr - e0);
-        if (t >= NST) wait(&empty[s], (unsigned)(((t / NST) - 1) & 1));
+  if (warp == 16) {   // producer warp: lane q issues row q of each stage (RPS <= 32)
+    for (int t = 0; t < total; ++t) {
+      const int s = t % NST, st = t % nstage;
+      const int e0 = st * RPS, n = min(RPS, nr - e0);
+      if (t >= NST) wait(&empty[s], (unsigned)(((t / NST) - 1) & 1));
+      if (lane == 0)
         asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(su32(&full[s])), "r"(seg * n) : "memory");
-        for (int q = 0; q < n; ++q)
-          asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n"
-                       ::"r"(su32(sm + ((size_t)s * RPS + q) * CWMAX)), "l"(A + (long long)s_row[e0 + q] * lda + j0),
-                       "r"(seg), "r"(su32(&full[s])) : "memory");
-      }
+      __syncwarp();
+      if (lane < n)
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n"
+                     ::"r"(su32(sm + ((size_t)s * RPS + lane) * CWMAX)), "l"(A + (long long)s_row[e0 + lane] * lda + j0),
+                     "r"(seg), "r"(su32(&full[s])) : "memory");
+    }
     return;
   }
   double acc[CWMAX / 64][2];
