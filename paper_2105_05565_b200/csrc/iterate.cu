@@ -387,7 +387,17 @@ k_iterate(IterArgs a, Ctrl* ctrl) {
     if (blockIdx.x == 0 && tid == 0) {
       ctrl->rnorm2 = tot;
       ctrl->k = k;
+#ifdef RS_IT_TIMES
+      // development probe (RS_NVCC_EXTRA=-DRS_IT_TIMES): the trace holds each iteration's
+      // completion time (globaltimer, ns) instead of its relative residual
+      if (c0.trace && k <= c0.trace_cap) {
+        unsigned long long tns;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tns));
+        c0.trace[k - 1] = (double)tns;
+      }
+#else
       if (c0.trace && k <= c0.trace_cap) c0.trace[k - 1] = rel;
+#endif
       if (status != ST_RUNNING) {
         ctrl->status = status;
         ctrl->done = 1;
