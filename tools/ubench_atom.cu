@@ -29,6 +29,9 @@ __global__ void __launch_bounds__(1024, 1) k(double* g, float* gf) {
       const unsigned o = atomicAdd(w, (unsigned)x);
       const int h = (int)(x >> 32) + (o + (unsigned)x < o ? 1 : 0);
       if (h) atomicAdd(reinterpret_cast<int*>(w) + 1, h);
+    } else if (V == 6) {   // the same fixed-point add as one native 64-bit shared atomic (RED)
+      unsigned long long* w = reinterpret_cast<unsigned long long*>(sb) + (a >> 1);
+      atomicAdd(w, (unsigned long long)((long long)st << 12));
     }
   }
   if (V == 4 && acc == 12345u) g[0] = 1.0;
@@ -40,9 +43,9 @@ int main() {
   cudaMalloc(&g, 64 << 20); cudaMalloc(&gf, 4 << 20);
   cudaMemset(g, 0, 64 << 20);
   cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
-  const char* nm[6] = {"shared fp64 atomicAdd (CAS)", "shared racy RMW", "shared fp32 atomicAdd",
+  const char* nm[7] = {"shared fp64 atomicAdd (CAS)", "shared racy RMW", "shared fp32 atomicAdd",
                        "global fp64 RED (1 MB)", "shared u32 atomicAdd, result used",
-                       "shared fixed-point add (2 x u32)"};
+                       "shared fixed-point add (2 x u32)", "shared fixed-point add (u64 atom)"};
   auto run = [&](int v, auto kern) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, BAND * 8);
     float best = 1e9;
@@ -56,5 +59,5 @@ int main() {
     printf("%-30s %8.3f ms  %6.2f ops/clk/SM (1.965 GHz)  %s\n", nm[v], best, ops / (best * 1e-3) / 148 / 1.965e9,
            cudaGetErrorString(cudaGetLastError()));
   };
-  run(0, k<0>); run(1, k<1>); run(2, k<2>); run(3, k<3>); run(4, k<4>); run(5, k<5>);
+  run(0, k<0>); run(1, k<1>); run(2, k<2>); run(3, k<3>); run(4, k<4>); run(5, k<5>); run(6, k<6>);
 }
